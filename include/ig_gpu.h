@@ -1,0 +1,168 @@
+/*
+ * ig_gpu.h — C-ABI of the B200 solve phase (PCG + geometric-multigrid V-cycle
+ * with additive-Schwarz smoothing), the drop-in boundary for the reference's
+ * CPU solve in /root/reference/proj.
+ *
+ * Every array argument is a plain pointer + size; no C++ or torch types cross
+ * this boundary.  Unless a function name ends in `_device`, vector arguments
+ * are HOST pointers and the call is synchronous.  `_device` variants take
+ * device pointers and are asynchronous on the handle's CUDA stream
+ * (ig_hier_stream).
+ *
+ * Interfaces replaced (reference file:line):
+ *   ig_csr            SpMat = Eigen::SparseMatrix<double,RowMajor> compressed
+ *                     (proj/include/immergrid/common.hpp:16): int32 outer/inner
+ *                     indices, ascending inner indices per row.
+ *   ig_blocks         BlockLayout (post-filter) + std::vector<Eigen::LLT<MatX>>
+ *                     (proj/include/immergrid/smoothers.hpp:24-27, :70-75)
+ *   ig_level          MgLevel {A, R, smoother}  (multigrid.hpp:21-26)
+ *   ig_coarse         MgHierarchy::{coarse_chol_, coarse_piv_, rank_}
+ *                     (multigrid.hpp:70-73; built at multigrid.cpp:57-73)
+ *   ig_hier_create    the upload half of MgHierarchy::build (multigrid.cpp:12-75)
+ *   ig_vcycle         MgHierarchy::apply (multigrid.hpp:52)
+ *   ig_vcycle_at      MgHierarchy::vcycle_at (multigrid.hpp:49, multigrid.cpp:90-108)
+ *   ig_coarse_solve   MgHierarchy::coarse_solve (multigrid.cpp:77-88)
+ *   ig_smoother_apply Smoother::apply, additive Schwarz (smoothers.cpp:169-184)
+ *   ig_pcg            pcg(A, b, precond, tol, maxit) with precond = the hierarchy
+ *                     (solvers.hpp:51-53, solvers.cpp:17-71)
+ *   ig_level_spmv     the Eigen RowMajor SpMVs at solvers.cpp:45,
+ *                     multigrid.cpp:99,101,102,104 (debug / parity entry point)
+ *
+ * Status codes mirror the reference's exception types (solvers.hpp:25-47);
+ * exceptions never cross the ABI.  The C++ wrapper in
+ * include/immergrid_gpu/solve.hpp and the Python mirror in
+ * paper_1903_10977_b200/__init__.py re-throw them.
+ */
+#ifndef IG_GPU_H
+#define IG_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum ig_status {
+  IG_OK = 0,                /* converged / success                           */
+  IG_NOT_CONVERGED = 1,     /* NotConverged{report, x}  (solvers.cpp:67-70)  */
+  IG_BREAKDOWN = 2,         /* Breakdown{report}        (solvers.cpp:47-50)  */
+  IG_INVALID_ARGUMENT = 3,  /* std::invalid_argument    (solvers.cpp:20-21)  */
+  IG_CUDA_ERROR = 4,        /* device failure (no reference counterpart)     */
+  IG_UNSUPPORTED = 5        /* smoother kind not implemented on the device   */
+};
+
+/* SmootherKind order of proj/include/immergrid/smoothers.hpp:15. */
+enum ig_smoother_kind {
+  IG_SMOOTHER_JACOBI = 0,
+  IG_SMOOTHER_GAUSS_SEIDEL = 1,
+  IG_SMOOTHER_ADDITIVE_SCHWARZ = 2,
+  IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ = 3
+};
+
+/* CSR == Eigen RowMajor compressed storage. */
+typedef struct {
+  int32_t n_rows, n_cols;
+  int64_t nnz;
+  const int32_t *row_ptr; /* n_rows+1 */
+  const int32_t *col_idx; /* nnz, ascending within a row */
+  const double *val;      /* nnz */
+} ig_csr;
+
+/* Post-filter Schwarz layout.  Block b owns blk_dofs[blk_ptr[b]..blk_ptr[b+1])
+ * (ascending DOFs) and its lower Cholesky factor L_b, s_b x s_b column-major,
+ * at fac[fac_ptr[b] .. fac_ptr[b] + s_b*s_b) (upper triangle ignored).
+ * Blocks are in ascending owner order (smoothers.cpp:56-66). */
+typedef struct {
+  int32_t n_blocks;
+  const int32_t *blk_ptr;  /* n_blocks+1 */
+  const int32_t *blk_dofs; /* blk_ptr[n_blocks] */
+  const int64_t *fac_ptr;  /* n_blocks+1 */
+  const double *fac;
+} ig_blocks;
+
+/* One level.  levels[0] is the coarsest (A only; R empty, no smoother),
+ * levels[n_levels-1] the finest.  R of level l restricts level-l vectors to
+ * level l-1 (n_rows = n_{l-1}, n_cols = n_l), as MgLevel::R. */
+typedef struct {
+  ig_csr A;
+  ig_csr R;
+  int32_t smoother_kind; /* ig_smoother_kind; only ADDITIVE_SCHWARZ on device */
+  double gamma;          /* damping, already resolved (smoothers.cpp:234-239) */
+  ig_blocks blocks;
+} ig_level;
+
+/* Coarsest-level pivoted Cholesky (LAPACK dpstrf('L') output). */
+typedef struct {
+  int32_t n, rank;
+  const double *L;    /* n x n column-major; first `rank` columns are L11 */
+  const int32_t *piv; /* n, 1-based (dpstrf) */
+} ig_coarse;
+
+typedef struct ig_hier ig_hier;
+
+/* Device-side sizes and algorithmic byte counts. */
+typedef struct {
+  int32_t n_levels;
+  int32_t n[16];           /* DOFs per level, [0] coarsest */
+  int64_t nnz_A[16];
+  int64_t nnz_R[16];
+  int32_t n_blocks[16];
+  int32_t n_multi_blocks[16]; /* blocks with s_b > 1 */
+  int64_t sum_s[16];          /* sum of block sizes */
+  int64_t sum_s2[16];         /* sum of s_b^2 (stored factor entries) */
+  int64_t sell_slots_A[16];   /* padded SELL-32 slots of A (>= nnz_A) */
+  int64_t bytes_vcycle;       /* algorithmic bytes of one V-cycle */
+  int64_t bytes_pcg_iter;     /* algorithmic bytes of one PCG iteration */
+  int64_t bytes_spmv_finest;  /* algorithmic bytes of one finest y = A x */
+  int64_t device_bytes;       /* device memory held by the handle */
+  int32_t kernels_vcycle;     /* kernel launches per V-cycle */
+  int32_t kernels_pcg_iter;   /* kernel launches per PCG iteration */
+} ig_info;
+
+/* Upload a hierarchy (copied; the host arrays may be freed afterwards).
+ * Returns IG_INVALID_ARGUMENT on inconsistent sizes. */
+int ig_hier_create(const ig_level *levels, int32_t n_levels,
+                   const ig_coarse *coarse, ig_hier **out);
+void ig_hier_destroy(ig_hier *h);
+int ig_hier_info(const ig_hier *h, ig_info *out);
+/* cudaStream_t of the handle (as void*). */
+void *ig_hier_stream(ig_hier *h);
+
+/* --- reference-shaped entry points (host buffers, synchronous) --------- */
+int ig_vcycle(ig_hier *h, const double *r, double *x);
+int ig_vcycle_at(ig_hier *h, int32_t level, const double *r, double *x);
+int ig_coarse_solve(ig_hier *h, const double *r, double *x);
+int ig_smoother_apply(ig_hier *h, int32_t level, const double *r, double *x);
+/* mode 0: y = A x; 1: y = r - A x (r passed in y); 2: y = R x; 3: y = R^T x */
+int ig_level_spmv(ig_hier *h, int32_t level, const double *x, double *y,
+                  int32_t mode);
+
+/* PCG on A = levels[n_levels-1].A preconditioned by one V-cycle.
+ * residuals must hold maxit+1 doubles; *iterations and the residual prefix
+ * follow ConvergenceReport (solvers.hpp:16-23).  x is written on IG_OK and on
+ * IG_NOT_CONVERGED (the partial iterate).  seconds = device time of the solve
+ * (CUDA events), host copies excluded. */
+int ig_pcg(ig_hier *h, const double *b, double tol, int32_t maxit, double *x,
+           double *residuals, int32_t *iterations, double *seconds);
+
+/* --- device-resident variants (async on ig_hier_stream) ----------------- */
+int ig_vcycle_device(ig_hier *h, const double *d_r, double *d_x);
+/* Launches the whole solve (CUDA graph with a device-side WHILE loop); no
+ * host synchronisation.  Read the outcome with ig_pcg_result. */
+int ig_pcg_device(ig_hier *h, const double *d_b, double tol, int32_t maxit,
+                  double *d_x);
+/* Synchronises the stream and returns the status of the last
+ * ig_pcg_device; residuals (maxit+1, may be NULL), iterations. */
+int ig_pcg_result(ig_hier *h, double *residuals, int32_t *iterations);
+
+/* Thread-local message for the last non-OK status. */
+const char *ig_last_error(void);
+
+/* Build options (set before ig_hier_create; process-wide). 0 = default. */
+#define IG_OPT_USE_GRAPH 1 /* 1 (default): CUDA-graph PCG loop; 0: host loop */
+int ig_set_option(int32_t option, int64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IG_GPU_H */

@@ -1,0 +1,83 @@
+/*
+ * ig_host.h — C-ABI of the host-side setup (CPU, C++/OpenMP): builds the
+ * algebraic multigrid hierarchy that ig_hier_create (ig_gpu.h) uploads.
+ *
+ * Replaces, for the solve-phase drop-in, the reference's setup chain
+ *   build_case            proj/src/runner.cpp:523-532  (trim, build_space, assemble)
+ *   MgHierarchy::build    proj/src/multigrid.cpp:12-75 (coarsen, R, Galerkin,
+ *                         make_smoother per level, dpstrf on the coarsest)
+ *   make_smoother         proj/src/smoothers.cpp:216-241
+ * and writes/reads the same payload as a versioned binary file (.igh).
+ */
+#ifndef IG_HOST_H
+#define IG_HOST_H
+
+#include <stdint.h>
+
+#include "ig_gpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int32_t dim;             /* 2 or 3                                          */
+  const char *geometry;    /* level-set expression (config.hpp:21-31 + 3D)    */
+  double origin[3];
+  double extent[3];
+  int32_t resolution[3];   /* background cells per axis (finest level)        */
+  int32_t family;          /* 0 Lagrange (2D), 1 B-spline                     */
+  int32_t degree;          /* 1..4                                            */
+  int32_t levels;          /* total MG levels, >= 1                           */
+  int32_t quad_depth;      /* cut-cell bisection depth (QuadratureConfig)     */
+  int32_t gauss_order;     /* 0 = p+1 (config.cpp:647-650)                    */
+  int32_t classify_depth;  /* lattice depth for trimming                      */
+  double edge_tol;
+  double body_force;       /* f (constant)                                    */
+  double beta;             /* penalty; 0 = 2/h (assembly.cpp:7-10)            */
+  int32_t dirichlet_box_sides; /* penalty also on embedding-box sides (2D)    */
+  int32_t smoother_kind;   /* ig_smoother_kind                                */
+  double gamma;            /* 0 = automatic (smoothers.cpp:234-239)           */
+  double filter_ratio;     /* block eigen-filter ratio (default 1e-16)        */
+  int32_t threads;         /* host threads for setup; 0 = all                 */
+} igh_config;
+
+typedef struct igh_case igh_case;
+
+typedef struct {
+  int32_t n_levels;
+  int32_t n[16];          /* DOFs per level, [0] coarsest */
+  int64_t nnz[16];
+  int32_t max_nk[16];
+  int64_t filtered_dofs[16];
+  int32_t coarse_rank;
+  int64_t cut_elements;   /* finest level */
+  double eta;             /* min volume fraction, finest level */
+  double seconds_assemble;
+  double seconds_mg_setup;
+} igh_info;
+
+void igh_config_default(igh_config *cfg);
+int igh_build(const igh_config *cfg, igh_case **out);
+/* Pointers stay owned by the case (valid until igh_destroy). */
+int igh_levels(const igh_case *c, const ig_level **levels, int32_t *n_levels,
+               const ig_coarse **coarse);
+const double *igh_rhs(const igh_case *c, int32_t *n);
+int igh_get_info(const igh_case *c, igh_info *out);
+/* Kept anchors of level l as untrimmed tensor indices (ax, ay, az) -> n x 3. */
+int igh_anchors(const igh_case *c, int32_t level, int32_t *out_xyz);
+int igh_write(const igh_case *c, const char *path);
+int igh_read(const char *path, igh_case **out);
+void igh_destroy(igh_case *c);
+const char *igh_last_error(void);
+
+/* Standalone pieces (tests): LAPACK dpstrf('L') restatement on an n x n
+ * column-major matrix (overwritten); returns rank, piv 1-based. */
+int32_t igh_pstrf(int32_t n, double *a, int32_t *piv, double tol);
+/* min volume fraction of a 2D/3D case without building the hierarchy. */
+int igh_eta(const igh_config *cfg, double *eta, int64_t *cut_elements, int32_t *n_dofs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IG_HOST_H */

@@ -1,0 +1,242 @@
+/*
+ * oracle.c — CPU restatement of the reference's solve phase.  TEST
+ * INFRASTRUCTURE ONLY (see oracle.h): the checker for the GPU path and the
+ * timed CPU baseline; never linked into the product.
+ */
+#define _POSIX_C_SOURCE 199309L
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+/* ---------------------------------------------------------- reductions -- */
+
+/* One chunk of 256 values: 8 warps x (32-lane xor butterfly), then
+ * ((w0+w1)+(w2+w3))+((w4+w5)+(w6+w7)).  Mirrors csrc/reduce.cuh. */
+static double tree256(const double *v) {
+  double w[8];
+  for (int g = 0; g < 8; ++g) {
+    double lane[32];
+    memcpy(lane, v + 32 * g, sizeof(lane));
+    for (int off = 16; off >= 1; off >>= 1) {
+      double nxt[32];
+      for (int l = 0; l < 32; ++l) nxt[l] = lane[l] + lane[l ^ off];
+      memcpy(lane, nxt, sizeof(lane));
+    }
+    w[g] = lane[0];
+  }
+  return ((w[0] + w[1]) + (w[2] + w[3])) + ((w[4] + w[5]) + (w[6] + w[7]));
+}
+
+/* Second pass over the chunk partials: lane t sums P[t], P[t+256], ... from
+ * 0.0 in ascending order, then tree256 over the 256 lane sums. */
+static double finish_partials(int64_t nc, const double *P) {
+  double acc[256];
+  for (int t = 0; t < 256; ++t) {
+    double a = 0.0;
+    for (int64_t k = t; k < nc; k += 256) a = a + P[k];
+    acc[t] = a;
+  }
+  return tree256(acc);
+}
+
+double orc_dot(int mode, int64_t n, const double *a, const double *b) {
+  if (mode == ORC_SEQ) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s = s + a[i] * b[i];
+    return s;
+  }
+  const int64_t nc = (n + 255) / 256;
+  double *P = (double *)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1));
+  for (int64_t c = 0; c < nc; ++c) {
+    double v[256];
+    for (int t = 0; t < 256; ++t) {
+      const int64_t i = 256 * c + t;
+      v[t] = i < n ? a[i] * b[i] : 0.0;
+    }
+    P[c] = tree256(v);
+  }
+  const double s = finish_partials(nc, P);
+  free(P);
+  return s;
+}
+
+/* ------------------------------------------------------------- sparse --- */
+
+void orc_spmv(const ig_csr *A, const double *x, double *y, int resid) {
+  for (int32_t i = 0; i < A->n_rows; ++i) {
+    double acc = 0.0;
+    for (int32_t k = A->row_ptr[i]; k < A->row_ptr[i + 1]; ++k) acc = acc + A->val[k] * x[A->col_idx[k]];
+    y[i] = resid ? y[i] - acc : acc;
+  }
+}
+
+void orc_spmv_t(const ig_csr *A, const double *x, double *y) {
+  for (int32_t j = 0; j < A->n_cols; ++j) y[j] = 0.0;
+  for (int32_t c = 0; c < A->n_rows; ++c) {
+    const double xc = x[c];
+    for (int32_t k = A->row_ptr[c]; k < A->row_ptr[c + 1]; ++k) {
+      const int32_t f = A->col_idx[k];
+      y[f] = y[f] + A->val[k] * xc;
+    }
+  }
+}
+
+/* --------------------------------------------------------- block solves -- */
+
+/* Eigen LLT::solve: forward substitution with L (column oriented), then
+ * backward substitution with L^T (row dot products, ascending k). */
+static void llt_solve(int s, const double *L, double *y) {
+  for (int j = 0; j < s; ++j) {
+    const double yj = y[j] / L[(size_t)j * s + j];
+    y[j] = yj;
+    for (int i = j + 1; i < s; ++i) y[i] = y[i] - L[(size_t)j * s + i] * yj;
+  }
+  for (int i = s - 1; i >= 0; --i) {
+    double acc = 0.0;
+    for (int k = i + 1; k < s; ++k) acc = acc + L[(size_t)i * s + k] * y[k]; /* L(k,i) */
+    y[i] = (y[i] - acc) / L[(size_t)i * s + i];
+  }
+}
+
+void orc_as_apply(const ig_level *lv, int32_t n, const double *r, double *x) {
+  const ig_blocks *B = &lv->blocks;
+  for (int32_t i = 0; i < n; ++i) x[i] = 0.0;
+  double y[1024];
+  for (int32_t b = 0; b < B->n_blocks; ++b) {
+    const int32_t o = B->blk_ptr[b];
+    const int s = B->blk_ptr[b + 1] - o;
+    for (int i = 0; i < s; ++i) y[i] = r[B->blk_dofs[o + i]];
+    llt_solve(s, B->fac + B->fac_ptr[b], y);
+    for (int i = 0; i < s; ++i) {
+      const int32_t d = B->blk_dofs[o + i];
+      x[d] = x[d] + y[i];
+    }
+  }
+  for (int32_t i = 0; i < n; ++i) x[i] = lv->gamma * x[i];
+}
+
+void orc_coarse_solve(const ig_coarse *co, const double *r, double *x) {
+  const int n = co->n, rk = co->rank;
+  double *y = (double *)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+  double *perm = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  for (int k = 0; k < n; ++k) perm[k] = r[co->piv[k] - 1];
+  for (int k = 0; k < rk; ++k) y[k] = perm[k];
+  const double *L = co->L;
+  for (int j = 0; j < rk; ++j) {
+    const double yj = y[j] / L[(size_t)j * n + j];
+    y[j] = yj;
+    for (int i = j + 1; i < rk; ++i) y[i] = y[i] - L[(size_t)j * n + i] * yj;
+  }
+  for (int i = rk - 1; i >= 0; --i) {
+    double acc = 0.0;
+    for (int k = i + 1; k < rk; ++k) acc = acc + L[(size_t)i * n + k] * y[k];
+    y[i] = (y[i] - acc) / L[(size_t)i * n + i];
+  }
+  for (int k = 0; k < n; ++k) x[co->piv[k] - 1] = y[k];
+  free(y);
+  free(perm);
+}
+
+/* -------------------------------------------------------------- V-cycle -- */
+
+int orc_vcycle_at(const ig_level *levels, int32_t n_levels, const ig_coarse *co, int32_t l,
+                  const double *r, double *x) {
+  if (l < 0 || l >= n_levels) return IG_INVALID_ARGUMENT;
+  if (l == 0) {
+    orc_coarse_solve(co, r, x);
+    return IG_OK;
+  }
+  const ig_level *lv = &levels[l];
+  const int32_t n = lv->A.n_rows, nc = lv->R.n_rows;
+  double *res = (double *)malloc(sizeof(double) * (size_t)n);
+  double *tmp = (double *)malloc(sizeof(double) * (size_t)n);
+  double *rc = (double *)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1));
+  double *xc = (double *)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1));
+
+  orc_as_apply(lv, n, r, x);                          /* x = S(r, Forward)        */
+  memcpy(res, r, sizeof(double) * (size_t)n);
+  orc_spmv(&lv->A, x, res, 1);                        /* res = r - A x            */
+  orc_spmv(&lv->R, res, rc, 0);                       /* R res                    */
+  orc_vcycle_at(levels, n_levels, co, l - 1, rc, xc); /* coarse_x                 */
+  orc_spmv_t(&lv->R, xc, tmp);                        /* correction = R^T coarse_x */
+  for (int32_t i = 0; i < n; ++i) x[i] = x[i] + tmp[i];
+  orc_spmv(&lv->A, tmp, res, 1);                      /* res -= A correction      */
+  orc_as_apply(lv, n, res, tmp);                      /* S(res, Reverse) == Forward for AS */
+  for (int32_t i = 0; i < n; ++i) x[i] = x[i] + tmp[i];
+  free(res);
+  free(tmp);
+  free(rc);
+  free(xc);
+  return IG_OK;
+}
+
+/* ------------------------------------------------------------------ PCG -- */
+
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+int orc_pcg(const ig_level *levels, int32_t n_levels, const ig_coarse *co, int mode,
+            const double *b, double tol, int32_t maxit, double *x, double *residuals,
+            int32_t *iterations, double *seconds) {
+  const ig_csr *A = &levels[n_levels - 1].A;
+  const int32_t n = A->n_rows;
+  if (A->n_rows != A->n_cols) return IG_INVALID_ARGUMENT;
+  const double t0 = now_s();
+  *iterations = 0;
+  for (int32_t i = 0; i < n; ++i) x[i] = 0.0;
+  const double bnorm = sqrt(orc_dot(mode, n, b, b));
+  if (bnorm == 0.0) {
+    residuals[0] = 0.0;
+    *seconds = now_s() - t0;
+    return IG_OK;
+  }
+  residuals[0] = 1.0;
+  if (1.0 <= tol) {
+    *seconds = now_s() - t0;
+    return IG_OK;
+  }
+  double *r = (double *)malloc(sizeof(double) * (size_t)n);
+  double *z = (double *)malloc(sizeof(double) * (size_t)n);
+  double *p = (double *)malloc(sizeof(double) * (size_t)n);
+  double *ap = (double *)malloc(sizeof(double) * (size_t)n);
+  memcpy(r, b, sizeof(double) * (size_t)n);
+  orc_vcycle_at(levels, n_levels, co, n_levels - 1, r, z);
+  memcpy(p, z, sizeof(double) * (size_t)n);
+  double rz = orc_dot(mode, n, r, z);
+  int status = IG_NOT_CONVERGED;
+  for (int32_t k = 0; k < maxit; ++k) {
+    orc_spmv(A, p, ap, 0);
+    const double pap = orc_dot(mode, n, p, ap);
+    if (pap <= 0.0) {
+      status = IG_BREAKDOWN;
+      break;
+    }
+    const double alpha = rz / pap;
+    for (int32_t i = 0; i < n; ++i) x[i] = x[i] + alpha * p[i];
+    for (int32_t i = 0; i < n; ++i) r[i] = r[i] - alpha * ap[i];
+    *iterations = k + 1;
+    const double rel = sqrt(orc_dot(mode, n, r, r)) / bnorm;
+    residuals[k + 1] = rel;
+    if (rel <= tol) {
+      status = IG_OK;
+      break;
+    }
+    orc_vcycle_at(levels, n_levels, co, n_levels - 1, r, z);
+    const double rz_next = orc_dot(mode, n, r, z);
+    const double beta = rz_next / rz;
+    for (int32_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+    rz = rz_next;
+  }
+  *seconds = now_s() - t0;
+  free(r);
+  free(z);
+  free(p);
+  free(ap);
+  return status;
+}

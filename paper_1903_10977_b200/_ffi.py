@@ -1,0 +1,135 @@
+"""ctypes declarations of the two C-ABIs (include/ig_gpu.h, include/ig_host.h).
+
+Plain structs and function prototypes only; the reference-shaped API lives in
+``paper_1903_10977_b200/__init__.py``.  Libraries are loaded from this package
+directory (built in-tree by ``make -C paper_1903_10977_b200``); a missing GPU
+library raises instead of falling back to anything.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+i32, i64, f64 = C.c_int32, C.c_int64, C.c_double
+P = C.POINTER
+
+
+class ig_csr(C.Structure):
+    _fields_ = [("n_rows", i32), ("n_cols", i32), ("nnz", i64),
+                ("row_ptr", P(i32)), ("col_idx", P(i32)), ("val", P(f64))]
+
+
+class ig_blocks(C.Structure):
+    _fields_ = [("n_blocks", i32), ("blk_ptr", P(i32)), ("blk_dofs", P(i32)),
+                ("fac_ptr", P(i64)), ("fac", P(f64))]
+
+
+class ig_level(C.Structure):
+    _fields_ = [("A", ig_csr), ("R", ig_csr), ("smoother_kind", i32),
+                ("gamma", f64), ("blocks", ig_blocks)]
+
+
+class ig_coarse(C.Structure):
+    _fields_ = [("n", i32), ("rank", i32), ("L", P(f64)), ("piv", P(i32))]
+
+
+class ig_info(C.Structure):
+    _fields_ = [("n_levels", i32), ("n", i32 * 16), ("nnz_A", i64 * 16),
+                ("nnz_R", i64 * 16), ("n_blocks", i32 * 16),
+                ("n_multi_blocks", i32 * 16), ("sum_s", i64 * 16),
+                ("sum_s2", i64 * 16), ("sell_slots_A", i64 * 16),
+                ("bytes_vcycle", i64), ("bytes_pcg_iter", i64),
+                ("bytes_spmv_finest", i64), ("device_bytes", i64),
+                ("kernels_vcycle", i32), ("kernels_pcg_iter", i32)]
+
+
+class igh_config(C.Structure):
+    _fields_ = [("dim", i32), ("geometry", C.c_char_p), ("origin", f64 * 3),
+                ("extent", f64 * 3), ("resolution", i32 * 3), ("family", i32),
+                ("degree", i32), ("levels", i32), ("quad_depth", i32),
+                ("gauss_order", i32), ("classify_depth", i32), ("edge_tol", f64),
+                ("body_force", f64), ("beta", f64), ("dirichlet_box_sides", i32),
+                ("smoother_kind", i32), ("gamma", f64), ("filter_ratio", f64),
+                ("threads", i32)]
+
+
+class igh_info(C.Structure):
+    _fields_ = [("n_levels", i32), ("n", i32 * 16), ("nnz", i64 * 16),
+                ("max_nk", i32 * 16), ("filtered_dofs", i64 * 16),
+                ("coarse_rank", i32), ("cut_elements", i64), ("eta", f64),
+                ("seconds_assemble", f64), ("seconds_mg_setup", f64)]
+
+
+IG_OK, IG_NOT_CONVERGED, IG_BREAKDOWN, IG_INVALID_ARGUMENT, IG_CUDA_ERROR, IG_UNSUPPORTED = range(6)
+IG_SMOOTHER_JACOBI, IG_SMOOTHER_GAUSS_SEIDEL, IG_SMOOTHER_ADDITIVE_SCHWARZ, IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ = range(4)
+IG_OPT_USE_GRAPH = 1
+
+_host = None
+_gpu = None
+
+
+def _lib(name: str) -> C.CDLL:
+    path = os.path.join(HERE, name)
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is not built; run `make -C {HERE}` (or __graft_entry__.build())")
+    return C.CDLL(path)
+
+
+def host() -> C.CDLL:
+    global _host
+    if _host is None:
+        lib = _lib("libig_host.so")
+        lib.igh_config_default.argtypes = [P(igh_config)]
+        lib.igh_config_default.restype = None
+        lib.igh_build.argtypes = [P(igh_config), P(C.c_void_p)]
+        lib.igh_levels.argtypes = [C.c_void_p, P(P(ig_level)), P(i32), P(P(ig_coarse))]
+        lib.igh_rhs.argtypes = [C.c_void_p, P(i32)]
+        lib.igh_rhs.restype = P(f64)
+        lib.igh_get_info.argtypes = [C.c_void_p, P(igh_info)]
+        lib.igh_anchors.argtypes = [C.c_void_p, i32, P(i32)]
+        lib.igh_write.argtypes = [C.c_void_p, C.c_char_p]
+        lib.igh_read.argtypes = [C.c_char_p, P(C.c_void_p)]
+        lib.igh_destroy.argtypes = [C.c_void_p]
+        lib.igh_destroy.restype = None
+        lib.igh_last_error.restype = C.c_char_p
+        lib.igh_pstrf.argtypes = [i32, P(f64), P(i32), f64]
+        lib.igh_pstrf.restype = i32
+        lib.igh_eta.argtypes = [P(igh_config), P(f64), P(i64), P(i32)]
+        _host = lib
+    return _host
+
+
+GPU_SYMBOLS = (
+    "ig_hier_create", "ig_hier_destroy", "ig_hier_info", "ig_hier_stream",
+    "ig_vcycle", "ig_vcycle_at", "ig_coarse_solve", "ig_smoother_apply",
+    "ig_level_spmv", "ig_pcg", "ig_vcycle_device", "ig_pcg_device",
+    "ig_pcg_result", "ig_last_error", "ig_set_option",
+)
+
+
+def gpu() -> C.CDLL:
+    global _gpu
+    if _gpu is None:
+        lib = _lib("libig_gpu.so")
+        vp, dp = C.c_void_p, P(f64)
+        lib.ig_hier_create.argtypes = [P(ig_level), i32, P(ig_coarse), P(vp)]
+        lib.ig_hier_destroy.argtypes = [vp]
+        lib.ig_hier_destroy.restype = None
+        lib.ig_hier_info.argtypes = [vp, P(ig_info)]
+        lib.ig_hier_stream.argtypes = [vp]
+        lib.ig_hier_stream.restype = vp
+        lib.ig_vcycle.argtypes = [vp, dp, dp]
+        lib.ig_vcycle_at.argtypes = [vp, i32, dp, dp]
+        lib.ig_coarse_solve.argtypes = [vp, dp, dp]
+        lib.ig_smoother_apply.argtypes = [vp, i32, dp, dp]
+        lib.ig_level_spmv.argtypes = [vp, i32, dp, dp, i32]
+        lib.ig_pcg.argtypes = [vp, dp, f64, i32, dp, dp, P(i32), dp]
+        lib.ig_vcycle_device.argtypes = [vp, vp, vp]
+        lib.ig_pcg_device.argtypes = [vp, vp, f64, i32, vp]
+        lib.ig_pcg_result.argtypes = [vp, dp, P(i32)]
+        lib.ig_last_error.restype = C.c_char_p
+        lib.ig_set_option.argtypes = [i32, i64]
+        _gpu = lib
+    return _gpu
