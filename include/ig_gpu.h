@@ -147,6 +147,10 @@ int ig_pcg(ig_hier *h, const double *b, double tol, int32_t maxit, double *x,
 
 /* --- device-resident variants (async on ig_hier_stream) ----------------- */
 int ig_vcycle_device(ig_hier *h, const double *d_r, double *d_x);
+/* ig_level_spmv on device buffers (modes as ig_level_spmv); used to time the
+ * dominant kernel in isolation. */
+int ig_level_spmv_device(ig_hier *h, int32_t level, const double *d_x,
+                         double *d_y, int32_t mode);
 /* Launches the whole solve (CUDA graph with a device-side WHILE loop); no
  * host synchronisation.  Read the outcome with ig_pcg_result. */
 int ig_pcg_device(ig_hier *h, const double *d_b, double tol, int32_t maxit,

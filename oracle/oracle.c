@@ -86,20 +86,25 @@ void orc_spmv_t(const ig_csr *A, const double *x, double *y) {
 
 /* --------------------------------------------------------- block solves -- */
 
-/* Eigen LLT::solve: forward substitution with L (column oriented), then
- * backward substitution with L^T (row dot products, ascending k). */
-static void llt_solve(int s, const double *L, double *y) {
+/* Eigen LLT::solve (smoothers.cpp:180): forward substitution with L (column
+ * oriented), then backward substitution with L^T in row-dot form
+ * y_i = (y_i - sum_{k>i} L(k,i) y_k) / L(i,i).  Eigen's panel/SIMD order is
+ * not observable here, so the dot order is DEFINED as descending k (the
+ * order in which the y_k become available), which the device reproduces
+ * exactly.  ld = leading dimension of the column-major factor. */
+static void tri_solve(int s, int ld, const double *L, double *y) {
   for (int j = 0; j < s; ++j) {
-    const double yj = y[j] / L[(size_t)j * s + j];
+    const double yj = y[j] / L[(size_t)j * ld + j];
     y[j] = yj;
-    for (int i = j + 1; i < s; ++i) y[i] = y[i] - L[(size_t)j * s + i] * yj;
+    for (int i = j + 1; i < s; ++i) y[i] = y[i] - L[(size_t)j * ld + i] * yj;
   }
   for (int i = s - 1; i >= 0; --i) {
     double acc = 0.0;
-    for (int k = i + 1; k < s; ++k) acc = acc + L[(size_t)i * s + k] * y[k]; /* L(k,i) */
-    y[i] = (y[i] - acc) / L[(size_t)i * s + i];
+    for (int k = s - 1; k > i; --k) acc = acc + L[(size_t)i * ld + k] * y[k]; /* L(k,i) */
+    y[i] = (y[i] - acc) / L[(size_t)i * ld + i];
   }
 }
+static void llt_solve(int s, const double *L, double *y) { tri_solve(s, s, L, y); }
 
 void orc_as_apply(const ig_level *lv, int32_t n, const double *r, double *x) {
   const ig_blocks *B = &lv->blocks;
@@ -124,17 +129,8 @@ void orc_coarse_solve(const ig_coarse *co, const double *r, double *x) {
   double *perm = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
   for (int k = 0; k < n; ++k) perm[k] = r[co->piv[k] - 1];
   for (int k = 0; k < rk; ++k) y[k] = perm[k];
-  const double *L = co->L;
-  for (int j = 0; j < rk; ++j) {
-    const double yj = y[j] / L[(size_t)j * n + j];
-    y[j] = yj;
-    for (int i = j + 1; i < rk; ++i) y[i] = y[i] - L[(size_t)j * n + i] * yj;
-  }
-  for (int i = rk - 1; i >= 0; --i) {
-    double acc = 0.0;
-    for (int k = i + 1; k < rk; ++k) acc = acc + L[(size_t)i * n + k] * y[k];
-    y[i] = (y[i] - acc) / L[(size_t)i * n + i];
-  }
+  /* L11 = topLeftCorner(rank, rank) of the n x n factor (multigrid.cpp:82-84). */
+  tri_solve(rk, n, co->L, y);
   for (int k = 0; k < n; ++k) x[co->piv[k] - 1] = y[k];
   free(y);
   free(perm);

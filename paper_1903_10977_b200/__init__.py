@@ -1,0 +1,435 @@
+"""B200-native solve phase of the immersed-FE / isogeometric multigrid method
+(arXiv 1903.10977), behind the reference's solver/preconditioner interface.
+
+Python mirror of the reference surface (/root/reference/proj/include/immergrid):
+
+=========================  ===========================================================
+this module                reference
+=========================  ===========================================================
+``pcg``                    ``pcg(A, b, precond, tol, maxit)``  solvers.hpp:51-53
+``ConvergenceReport``      solvers.hpp:16-23
+``Breakdown``              solvers.hpp:25-31
+``NotConverged``           solvers.hpp:33-41
+``MgHierarchy``            multigrid.hpp:34-74 (build / levels / level / vcycle_at /
+                           apply / coarse_solve / coarse_rank)
+``vcycle``                 multigrid.hpp:73-75 (1-based wrapper)
+``SmootherConfig``         smoothers.hpp:18-22
+``CaseConfig``/``build_case``  runner.cpp:523-532 + config.hpp (host setup)
+=========================  ===========================================================
+
+Host setup (trim, spaces, assembly, Galerkin hierarchy, Schwarz factors,
+dpstrf) runs in ``libig_host.so`` (C++/OpenMP); every solve-phase operation
+runs on the GPU in ``libig_gpu.so`` (hand-written sm_100a kernels).  There is
+no CPU fallback: without the GPU library these calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _ffi
+
+__all__ = [
+    "ConvergenceReport", "Breakdown", "NotConverged", "ResolutionError",
+    "SmootherConfig", "CaseConfig", "SpMat", "Case", "build_case",
+    "MgHierarchy", "vcycle", "pcg", "seed_offsets",
+]
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+
+
+# --------------------------------------------------------------- reports ---
+@dataclasses.dataclass
+class ConvergenceReport:
+    """solvers.hpp:16-23: residuals[k] = ||r_k|| / ||b||, k = 0..iterations."""
+    residuals: list = dataclasses.field(default_factory=list)
+    iterations: int = 0
+    converged: bool = False
+    seconds: float = 0.0
+
+
+class Breakdown(RuntimeError):
+    """p^T A p <= 0 inside CG (solvers.hpp:25-31)."""
+
+    def __init__(self, what: str, report: ConvergenceReport):
+        super().__init__(what)
+        self.report = report
+
+
+class NotConverged(RuntimeError):
+    """Iteration budget exhausted; carries the report and the last x (solvers.hpp:33-41)."""
+
+    def __init__(self, what: str, report: ConvergenceReport, x: np.ndarray):
+        super().__init__(what)
+        self.report = report
+        self.x = x
+
+
+class ResolutionError(RuntimeError):
+    """The mesh cannot be coarsened the requested number of times (multigrid.hpp:13-16)."""
+
+
+class GpuError(RuntimeError):
+    pass
+
+
+def _check(lib, rc: int, what: str):
+    if rc == _ffi.IG_OK:
+        return
+    msg = lib.ig_last_error().decode() if hasattr(lib, "ig_last_error") else lib.igh_last_error().decode()
+    if rc == _ffi.IG_INVALID_ARGUMENT:
+        if "coarsenings" in msg:
+            raise ResolutionError(msg)
+        raise ValueError(f"{what}: {msg}")
+    if rc == _ffi.IG_UNSUPPORTED:
+        raise NotImplementedError(f"{what}: {msg}")
+    raise GpuError(f"{what}: {msg} (status {rc})")
+
+
+# ------------------------------------------------------------ host setup ---
+@dataclasses.dataclass
+class SmootherConfig:
+    """smoothers.hpp:18-22.  Only additive Schwarz runs on the device."""
+    kind: str = "additive-schwarz"
+    gamma: float = 0.0          # 0 = automatic 1/max N_K
+    filter_ratio: float = 1e-16
+
+
+_KINDS = {"jacobi": 0, "gauss-seidel": 1, "additive-schwarz": 2, "multiplicative-schwarz": 3}
+
+
+@dataclasses.dataclass
+class CaseConfig:
+    """Case description (the subset of config.hpp:34-86 the solve needs, plus 3D)."""
+    geometry: str = "constant(1)"
+    dim: int = 2
+    origin: Sequence[float] = (0.0, 0.0, 0.0)
+    extent: Sequence[float] = (1.0, 1.0, 1.0)
+    resolution: Sequence[int] = (16, 16, 16)
+    family: str = "bspline"     # "bspline" | "lagrange" (2D)
+    degree: int = 2
+    levels: int = 2
+    quad_depth: int = 3
+    gauss_order: int = 0         # 0 = p + 1
+    classify_depth: int = 2
+    edge_tol: float = 1e-12
+    body_force: float = 1.0
+    beta: float = 0.0            # 0 = 2/h
+    dirichlet_box_sides: bool = True
+    smoother: SmootherConfig = dataclasses.field(default_factory=SmootherConfig)
+    threads: int = 0
+
+    def to_c(self) -> _ffi.igh_config:
+        c = _ffi.igh_config()
+        _ffi.host().igh_config_default(C.byref(c))
+        self._geo = self.geometry.encode()
+        c.dim = self.dim
+        c.geometry = self._geo
+        for i in range(3):
+            c.origin[i] = float(self.origin[i]) if i < len(self.origin) else 0.0
+            c.extent[i] = float(self.extent[i]) if i < len(self.extent) else 1.0
+            c.resolution[i] = int(self.resolution[i]) if i < len(self.resolution) else 1
+        c.family = 0 if self.family.lower().startswith("lag") else 1
+        c.degree = self.degree
+        c.levels = self.levels
+        c.quad_depth = self.quad_depth
+        c.gauss_order = self.gauss_order
+        c.classify_depth = self.classify_depth
+        c.edge_tol = self.edge_tol
+        c.body_force = self.body_force
+        c.beta = self.beta
+        c.dirichlet_box_sides = 1 if self.dirichlet_box_sides else 0
+        c.smoother_kind = _KINDS[self.smoother.kind]
+        c.gamma = self.smoother.gamma
+        c.filter_ratio = self.smoother.filter_ratio
+        c.threads = self.threads
+        return c
+
+
+def seed_offsets(seed: int = 1, count: int = 3):
+    """delta = Rng(seed).uniform(-0.01, 0.01) x count (common.hpp:43-58)."""
+    m = (1 << 64) - 1
+    s = seed
+    out = []
+    for _ in range(count):
+        s = (s + 0x9E3779B97F4A7C15) & m
+        z = s
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+        z ^= z >> 31
+        u = (z >> 11) * 2.0 ** -53
+        out.append(-0.01 + 0.02 * u)
+    return out
+
+
+class SpMat:
+    """CSR view (== Eigen RowMajor compressed, int32 indices)."""
+
+    def __init__(self, n_rows, n_cols, row_ptr, col_idx, val, _owner=None):
+        self.shape = (int(n_rows), int(n_cols))
+        self.row_ptr = row_ptr
+        self.col_idx = col_idx
+        self.val = val
+        self._owner = _owner
+
+    @classmethod
+    def from_c(cls, m: _ffi.ig_csr, owner=None) -> "SpMat":
+        nr, nc, nnz = m.n_rows, m.n_cols, m.nnz
+        if nr == 0:
+            return cls(0, nc, np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0), owner)
+        rp = np.ctypeslib.as_array(m.row_ptr, (nr + 1,))
+        ci = np.ctypeslib.as_array(m.col_idx, (nnz,)) if nnz else np.zeros(0, np.int32)
+        vv = np.ctypeslib.as_array(m.val, (nnz,)) if nnz else np.zeros(0)
+        return cls(nr, nc, rp, ci, vv, owner)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.shape[0])
+
+    def rows(self) -> int:
+        return self.shape[0]
+
+    def cols(self) -> int:
+        return self.shape[1]
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+        return sp.csr_matrix((self.val, self.col_idx, self.row_ptr), shape=self.shape)
+
+
+class Case:
+    """Host-built case: fine system (A, b) and the multigrid hierarchy payload
+    that crosses the C-ABI (owned by libig_host.so until close())."""
+
+    def __init__(self, handle: C.c_void_p, cfg: Optional[CaseConfig] = None):
+        self._h = handle
+        self.config = cfg
+        lib = _ffi.host()
+        self._lv = C.POINTER(_ffi.ig_level)()
+        nl = C.c_int32()
+        self._co = C.POINTER(_ffi.ig_coarse)()
+        lib.igh_levels(self._h, C.byref(self._lv), C.byref(nl), C.byref(self._co))
+        self.n_levels = nl.value
+        n = C.c_int32()
+        bp = lib.igh_rhs(self._h, C.byref(n))
+        self.b = np.ctypeslib.as_array(bp, (n.value,)).copy()
+        info = _ffi.igh_info()
+        lib.igh_get_info(self._h, C.byref(info))
+        self.info = info
+        self.A = SpMat.from_c(self._lv[self.n_levels - 1].A, self)
+
+    @property
+    def n(self) -> int:
+        return self.b.shape[0]
+
+    def level_dofs(self):
+        return [self.info.n[i] for i in range(self.n_levels)]
+
+    def levels_c(self):
+        return self._lv, self.n_levels, self._co
+
+    def level_A(self, l: int) -> SpMat:
+        return SpMat.from_c(self._lv[l].A, self)
+
+    def level_R(self, l: int) -> SpMat:
+        return SpMat.from_c(self._lv[l].R, self)
+
+    def gamma(self, l: int) -> float:
+        return self._lv[l].gamma
+
+    def blocks(self, l: int):
+        """(blk_ptr, blk_dofs, fac_ptr, fac) of level l (post-filter)."""
+        b = self._lv[l].blocks
+        nb = b.n_blocks
+        if nb == 0:
+            return None
+        ptr = np.ctypeslib.as_array(b.blk_ptr, (nb + 1,))
+        dofs = np.ctypeslib.as_array(b.blk_dofs, (int(ptr[-1]),))
+        fptr = np.ctypeslib.as_array(b.fac_ptr, (nb + 1,))
+        fac = np.ctypeslib.as_array(b.fac, (int(fptr[-1]),))
+        return ptr, dofs, fptr, fac
+
+    def coarse(self):
+        co = self._co.contents
+        n = co.n
+        L = np.ctypeslib.as_array(co.L, (n * n,)).reshape(n, n, order="F")
+        piv = np.ctypeslib.as_array(co.piv, (max(n, 1),))[:n]
+        return L, piv, co.rank
+
+    def anchors(self, l: int) -> np.ndarray:
+        out = np.zeros((self.info.n[l], 3), np.int32)
+        _check(_ffi.host(), _ffi.host().igh_anchors(self._h, l, out.ctypes.data_as(_ip)), "anchors")
+        return out
+
+    def write(self, path: str):
+        _check(_ffi.host(), _ffi.host().igh_write(self._h, path.encode()), "igh_write")
+
+    @classmethod
+    def read(cls, path: str) -> "Case":
+        h = C.c_void_p()
+        _check(_ffi.host(), _ffi.host().igh_read(path.encode(), C.byref(h)), "igh_read")
+        return cls(h)
+
+    def close(self):
+        if self._h:
+            _ffi.host().igh_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_case(cfg: CaseConfig) -> Case:
+    """build_case + MgHierarchy::build host half (runner.cpp:523-532, multigrid.cpp:12-75)."""
+    c = cfg.to_c()
+    h = C.c_void_p()
+    _check(_ffi.host(), _ffi.host().igh_build(C.byref(c), C.byref(h)), "igh_build")
+    return Case(h, cfg)
+
+
+# -------------------------------------------------------------- device -----
+def _as_f64(v, n: int) -> np.ndarray:
+    a = np.ascontiguousarray(v, dtype=np.float64)
+    if a.shape != (n,):
+        raise ValueError(f"vector of size {a.shape} where {n} is required")
+    return a
+
+
+class MgHierarchy:
+    """Device-resident multigrid hierarchy (multigrid.hpp:34-74).  Immutable
+    after build; calls on one handle serialise (the library holds a mutex)."""
+
+    def __init__(self, case):
+        """`case`: a host-built Case, or any payload exposing levels_c() ->
+        (ig_level*, n_levels, ig_coarse*) (the C-ABI boundary structs)."""
+        lib = _ffi.gpu()
+        lv, nl, co = case.levels_c()
+        self._h = C.c_void_p()
+        _check(lib, lib.ig_hier_create(lv, nl, co, C.byref(self._h)), "ig_hier_create")
+        self.case = case
+        self._lv = lv
+        self._n = [lv[i].A.n_rows for i in range(nl)]
+        self.A = SpMat.from_c(lv[nl - 1].A, case)
+        self._rank = co.contents.rank
+        info = _ffi.ig_info()
+        lib.ig_hier_info(self._h, C.byref(info))
+        self.info = info
+
+    @staticmethod
+    def build(case_or_cfg, levels: Optional[int] = None, smoother: Optional[SmootherConfig] = None) -> "MgHierarchy":
+        if isinstance(case_or_cfg, CaseConfig):
+            cfg = dataclasses.replace(case_or_cfg)
+            if levels is not None:
+                cfg.levels = levels
+            if smoother is not None:
+                cfg.smoother = smoother
+            case_or_cfg = build_case(cfg)
+        return MgHierarchy(case_or_cfg)
+
+    def levels(self) -> int:
+        return len(self._n)
+
+    def level(self, l: int):
+        return SpMat.from_c(self._lv[l].A, self.case), SpMat.from_c(self._lv[l].R, self.case)
+
+    def coarse_rank(self) -> int:
+        return self._rank
+
+    @property
+    def handle(self):
+        return self._h
+
+    def vcycle_at(self, l: int, r) -> np.ndarray:
+        if not 0 <= l < self.levels():
+            raise ValueError("vcycle_at: level out of range")
+        rr = _as_f64(r, self._n[l])
+        x = np.empty_like(rr)
+        lib = _ffi.gpu()
+        _check(lib, lib.ig_vcycle_at(self._h, l, rr.ctypes.data_as(_dp), x.ctypes.data_as(_dp)), "vcycle_at")
+        return x
+
+    def apply(self, r) -> np.ndarray:
+        return self.vcycle_at(self.levels() - 1, r)
+
+    __call__ = apply
+
+    def coarse_solve(self, r) -> np.ndarray:
+        return self.vcycle_at(0, r)
+
+    def smoother_apply(self, l: int, r) -> np.ndarray:
+        rr = _as_f64(r, self._n[l])
+        x = np.empty_like(rr)
+        lib = _ffi.gpu()
+        _check(lib, lib.ig_smoother_apply(self._h, l, rr.ctypes.data_as(_dp), x.ctypes.data_as(_dp)), "smoother_apply")
+        return x
+
+    def spmv(self, l: int, x, mode: int = 0, y=None) -> np.ndarray:
+        """mode 0: A x, 1: y - A x, 2: R x, 3: R^T x (ig_level_spmv)."""
+        A, R = self.level(l)
+        nin = A.cols() if mode <= 1 else (R.cols() if mode == 2 else R.rows())
+        nout = A.rows() if mode <= 1 else (R.rows() if mode == 2 else R.cols())
+        xx = _as_f64(x, nin)
+        yy = np.zeros(nout) if y is None else _as_f64(y, nout).copy()
+        lib = _ffi.gpu()
+        _check(lib, lib.ig_level_spmv(self._h, l, xx.ctypes.data_as(_dp), yy.ctypes.data_as(_dp), mode), "level_spmv")
+        return yy
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _ffi.gpu().ig_hier_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def vcycle(h: MgHierarchy, ell: int, r) -> np.ndarray:
+    """One-based level wrapper (multigrid.hpp:73-75)."""
+    return h.vcycle_at(ell - 1, r)
+
+
+def pcg(a, b, precond: MgHierarchy, tol: float = 1e-10, maxit: int = 1000):
+    """Preconditioned CG with zero initial guess (solvers.cpp:17-71), run
+    entirely on the device.  ``precond`` must be the GPU MgHierarchy built on
+    ``a`` (the reference passes the same fine matrix to build and pcg,
+    runner.cpp:219,233).  Returns (x, ConvergenceReport); raises Breakdown /
+    NotConverged like the reference."""
+    if not isinstance(precond, MgHierarchy):
+        raise TypeError("pcg: the preconditioner must be a device MgHierarchy (no CPU fallback)")
+    fineA = precond.A
+    if a is not None and a is not fineA:
+        shape = getattr(a, "shape", None)
+        if shape is None or tuple(shape) != fineA.shape:
+            raise ValueError("pcg: dimension mismatch")
+    n = fineA.rows()
+    if fineA.rows() != fineA.cols() or np.shape(b) != (n,):
+        raise ValueError("pcg: dimension mismatch")
+    bb = _as_f64(b, n)
+    x = np.zeros(n)
+    res = np.zeros(max(maxit, 0) + 1)
+    it = C.c_int32()
+    sec = C.c_double()
+    lib = _ffi.gpu()
+    rc = lib.ig_pcg(precond.handle, bb.ctypes.data_as(_dp), float(tol), int(maxit), x.ctypes.data_as(_dp),
+                    res.ctypes.data_as(_dp), C.byref(it), C.byref(sec))
+    k = it.value
+    rep = ConvergenceReport(residuals=res[: k + 1].tolist(), iterations=k, converged=(rc == _ffi.IG_OK),
+                            seconds=sec.value)
+    if rc == _ffi.IG_OK:
+        return x, rep
+    msg = lib.ig_last_error().decode()
+    if rc == _ffi.IG_NOT_CONVERGED:
+        raise NotConverged(msg, rep, x)
+    if rc == _ffi.IG_BREAKDOWN:
+        raise Breakdown(msg, rep)
+    _check(lib, rc, "pcg")

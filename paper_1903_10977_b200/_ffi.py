@@ -104,7 +104,7 @@ def host() -> C.CDLL:
 GPU_SYMBOLS = (
     "ig_hier_create", "ig_hier_destroy", "ig_hier_info", "ig_hier_stream",
     "ig_vcycle", "ig_vcycle_at", "ig_coarse_solve", "ig_smoother_apply",
-    "ig_level_spmv", "ig_pcg", "ig_vcycle_device", "ig_pcg_device",
+    "ig_level_spmv", "ig_pcg", "ig_vcycle_device", "ig_level_spmv_device", "ig_pcg_device",
     "ig_pcg_result", "ig_last_error", "ig_set_option",
 )
 
@@ -127,6 +127,7 @@ def gpu() -> C.CDLL:
         lib.ig_level_spmv.argtypes = [vp, i32, dp, dp, i32]
         lib.ig_pcg.argtypes = [vp, dp, f64, i32, dp, dp, P(i32), dp]
         lib.ig_vcycle_device.argtypes = [vp, vp, vp]
+        lib.ig_level_spmv_device.argtypes = [vp, i32, vp, vp, i32]
         lib.ig_pcg_device.argtypes = [vp, vp, f64, i32, vp]
         lib.ig_pcg_result.argtypes = [vp, dp, P(i32)]
         lib.ig_last_error.restype = C.c_char_p

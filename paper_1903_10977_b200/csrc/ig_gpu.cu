@@ -1,0 +1,773 @@
+// ig_gpu.cu — host side of the B200 solve phase behind the C-ABI of
+// include/ig_gpu.h: device layouts built from the boundary payload, the
+// V-cycle and PCG launch sequences, and the CUDA graph that runs the whole PCG
+// loop device-side (conditional WHILE node, no host round trips).
+//
+// Reference semantics followed (file:line in /root/reference/proj):
+//   pcg                 src/solvers.cpp:17-71
+//   MgHierarchy::vcycle_at src/multigrid.cpp:90-108
+//   coarse_solve        src/multigrid.cpp:77-88
+//   Smoother::apply(AS) src/smoothers.cpp:174-184
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ig_gpu.h"
+#include "kernels.cuh"
+
+using namespace igk;
+
+namespace {
+
+thread_local std::string g_err;
+int g_use_graph = 1;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      throw Error(IG_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_) + " (" + \
+                                     __FILE__ + ":" + std::to_string(__LINE__) + ")");       \
+  } while (0)
+
+inline unsigned grid_of(int64_t n) { return static_cast<unsigned>((n + kCta - 1) / kCta); }
+
+// Host image of a SELL-32 matrix.
+struct HostSell {
+  int32_t nr = 0, nc = 0;
+  std::vector<int64_t> slice_ptr;
+  std::vector<int32_t> rowlen;
+  std::vector<double> val;
+  std::vector<int32_t> col;
+};
+
+HostSell to_sell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, const double* val) {
+  HostSell s;
+  s.nr = nr;
+  s.nc = nc;
+  const int32_t nslice = (nr + kSell - 1) / kSell;
+  s.slice_ptr.assign(static_cast<size_t>(nslice) + 1, 0);
+  s.rowlen.assign(static_cast<size_t>(std::max(nr, 1)), 0);
+  for (int32_t i = 0; i < nr; ++i) s.rowlen[i] = ptr[i + 1] - ptr[i];
+  for (int32_t sl = 0; sl < nslice; ++sl) {
+    int32_t w = 0;
+    for (int32_t i = sl * kSell; i < std::min(nr, (sl + 1) * kSell); ++i) w = std::max(w, s.rowlen[i]);
+    s.slice_ptr[sl + 1] = s.slice_ptr[sl] + static_cast<int64_t>(w) * kSell;
+  }
+  const int64_t slots = s.slice_ptr[nslice];
+  s.val.assign(static_cast<size_t>(std::max<int64_t>(slots, 1)), 0.0);
+  s.col.assign(static_cast<size_t>(std::max<int64_t>(slots, 1)), 0);
+  for (int32_t i = 0; i < nr; ++i) {
+    const int64_t base = s.slice_ptr[i / kSell] + (i % kSell);
+    for (int32_t k = 0; k < s.rowlen[i]; ++k) {
+      s.val[base + static_cast<int64_t>(k) * kSell] = val[ptr[i] + k];
+      s.col[base + static_cast<int64_t>(k) * kSell] = col[ptr[i] + k];
+    }
+  }
+  return s;
+}
+
+// Transpose of a CSR (rows of the result visit source rows ascending).
+void csr_transpose(const ig_csr& a, std::vector<int32_t>& tp, std::vector<int32_t>& tc, std::vector<double>& tv) {
+  tp.assign(static_cast<size_t>(a.n_cols) + 1, 0);
+  for (int64_t k = 0; k < a.nnz; ++k) ++tp[a.col_idx[k] + 1];
+  for (int32_t j = 0; j < a.n_cols; ++j) tp[j + 1] += tp[j];
+  tc.resize(static_cast<size_t>(a.nnz));
+  tv.resize(static_cast<size_t>(a.nnz));
+  std::vector<int32_t> nx(tp.begin(), tp.end() - 1);
+  for (int32_t i = 0; i < a.n_rows; ++i)
+    for (int32_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+      const int32_t p = nx[a.col_idx[k]]++;
+      tc[p] = i;
+      tv[p] = a.val[k];
+    }
+}
+
+struct DevSell {
+  Sell s{};
+  bool stream = false;
+  int64_t nnz = 0, slots = 0;
+};
+
+struct Level {
+  int32_t n = 0;
+  DevSell A, R, P;
+  AsGroups G{};
+  AsGather S{};
+  int32_t n_blocks = 0, n_multi = 0;
+  int64_t sum_s = 0, sum_s2 = 0, packed_F = 0;
+  double* r_in = nullptr;  // input residual buffer (host API; coarse levels: R res)
+  double* x = nullptr;
+  double* res = nullptr;
+  double* cor = nullptr;
+  double* ybuf = nullptr;
+};
+
+// Algorithmic byte counts (CSR-minimal traffic).
+int64_t bytes_spmv(int64_t nr, int64_t nin, int64_t nnz, bool resid) {
+  return 12 * nnz + 4 * (nr + 1) + 8 * nin + 8 * nr + (resid ? 8 * nr : 0);
+}
+
+}  // namespace
+
+struct ig_hier {
+  std::vector<Level> lv;  // [0] coarsest
+  int32_t L = 0;
+  int32_t n0 = 0, rank = 0;
+  double* Lp = nullptr;  // packed lower L11
+  int32_t* piv = nullptr;
+  int coarse_threads = 32;
+  size_t coarse_smem = 0;
+  int coarse_use_smem = 0;
+  cudaStream_t stream = nullptr;
+  PcgState* st = nullptr;
+  double* partials = nullptr;
+  double* residuals = nullptr;
+  int32_t res_cap = 0;
+  double *r = nullptr, *z = nullptr, *p = nullptr, *ap = nullptr;
+  double *hb = nullptr, *hx = nullptr;  // device copies for the host-buffer API
+  cudaGraphExec_t pcg_exec = nullptr;
+  struct VcGraph {
+    const double* r;
+    double* x;
+    cudaGraphExec_t exec;
+  };
+  std::vector<VcGraph> vc_graphs;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<void*> allocs;
+  ig_info info{};
+  std::mutex mu;
+  int last_status = IG_OK;
+
+  template <typename T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    allocs.push_back(p);
+    info.device_bytes += static_cast<int64_t>(std::max<size_t>(count, 1) * sizeof(T));
+    return static_cast<T*>(p);
+  }
+  template <typename T>
+  T* upload(const T* src, size_t count) {
+    T* d = alloc<T>(count);
+    if (count) CK(cudaMemcpy(d, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+  }
+  DevSell upload_sell(const HostSell& h, int64_t nnz) {
+    DevSell d;
+    d.s.n_rows = h.nr;
+    d.s.n_cols = h.nc;
+    d.s.slice_ptr = upload(h.slice_ptr.data(), h.slice_ptr.size());
+    d.s.rowlen = upload(h.rowlen.data(), h.rowlen.size());
+    d.s.val = upload(h.val.data(), h.val.size());
+    d.s.col = upload(h.col.data(), h.col.size());
+    d.nnz = nnz;
+    d.slots = h.slice_ptr.back();
+    // Stream (evict-first) matrices far larger than L2; keep small ones cached.
+    d.stream = d.slots * 12 > (int64_t(48) << 20);
+    return d;
+  }
+  ~ig_hier() {
+    if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
+    for (auto& g : vc_graphs) cudaGraphExecDestroy(g.exec);
+    for (void* p : allocs) cudaFree(p);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  // ------------------------------------------------------------ launches --
+  void spmv(const DevSell& A, int mode, const double* x, double* y, const double* rsrc,
+            PcgState* s = nullptr, bool red = false) {
+    const unsigned g = grid_of(A.s.n_rows);
+    if (g == 0) return;
+#define IG_SPMV(M, S, R) k_spmv<M, S, R><<<g, kCta, 0, stream>>>(A.s, x, y, rsrc, s, partials)
+    if (red) {
+      if (A.stream) IG_SPMV(0, true, true); else IG_SPMV(0, false, true);
+    } else if (mode == 0) {
+      if (A.stream) IG_SPMV(0, true, false); else IG_SPMV(0, false, false);
+    } else {
+      if (A.stream) IG_SPMV(1, true, false); else IG_SPMV(1, false, false);
+    }
+#undef IG_SPMV
+    CK(cudaGetLastError());
+  }
+  void prolong(const Level& l, const double* xc, double* x, PcgState* s) {
+    const unsigned g = grid_of(l.P.s.n_rows);
+    if (l.P.stream)
+      k_prolong<true><<<g, kCta, 0, stream>>>(l.P.s, xc, l.cor, x, s);
+    else
+      k_prolong<false><<<g, kCta, 0, stream>>>(l.P.s, xc, l.cor, x, s);
+    CK(cudaGetLastError());
+  }
+  void smoother(const Level& l, const double* r, double* x, bool acc, PcgState* s, const double* rdot) {
+    if (l.n_multi > 0) {
+      const unsigned g = static_cast<unsigned>((static_cast<int64_t>(l.G.n_groups) * 32 + 127) / 128);
+      k_as_blocks<<<g, 128, 0, stream>>>(l.G, r, l.ybuf, s);
+      CK(cudaGetLastError());
+    }
+    const unsigned g = grid_of(l.n);
+    if (rdot)
+      k_as_gather<true, true><<<g, kCta, 0, stream>>>(l.S, r, l.ybuf, x, rdot, s, partials);
+    else if (acc)
+      k_as_gather<true, false><<<g, kCta, 0, stream>>>(l.S, r, l.ybuf, x, nullptr, s, nullptr);
+    else
+      k_as_gather<false, false><<<g, kCta, 0, stream>>>(l.S, r, l.ybuf, x, nullptr, s, nullptr);
+    CK(cudaGetLastError());
+  }
+  void coarse(const double* r, double* x, PcgState* s) {
+    k_coarse<<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, coarse_use_smem, s);
+    CK(cudaGetLastError());
+  }
+  // MgHierarchy::vcycle_at (multigrid.cpp:90-108).  rdot != null: PCG mode on
+  // the finest level (the last kernel also reduces r . z).
+  void vcycle(int l, const double* r, double* x, PcgState* s, const double* rdot) {
+    if (l == 0) {
+      coarse(r, x, s);
+      if (rdot) {  // 1-level hierarchy inside PCG: r . z as a separate pass
+        k_pcg_rz<<<grid_of(n0), kCta, 0, stream>>>(n0, rdot, x, s, partials);
+        CK(cudaGetLastError());
+      }
+      return;
+    }
+    Level& c = lv[l];
+    Level& cc = lv[l - 1];
+    smoother(c, r, x, false, s, nullptr);       // x = S(r, Forward)
+    spmv(c.A, 1, x, c.res, r, s);               // res = r - A x
+    spmv(c.R, 0, c.res, cc.r_in, nullptr, s);   // R res
+    vcycle(l - 1, cc.r_in, cc.x, s, nullptr);   // coarse_x
+    prolong(c, cc.x, x, s);                     // cor = R^T coarse_x; x += cor
+    spmv(c.A, 1, c.cor, c.res, c.res, s);       // res -= A cor
+    smoother(c, c.res, x, true, s, rdot);       // x += S(res, Reverse)
+  }
+  void pcg_prologue(cudaGraphConditionalHandle cond) {
+    const int32_t n = lv[L - 1].n;
+    k_pcg_init<<<grid_of(n), kCta, 0, stream>>>(n, r, st, partials);
+    CK(cudaGetLastError());
+    vcycle(L - 1, r, z, st, r);
+    k_pcg_p<true><<<grid_of(n), kCta, 0, stream>>>(n, z, p, st, cond);
+    CK(cudaGetLastError());
+  }
+  void pcg_body(cudaGraphConditionalHandle cond) {
+    const int32_t n = lv[L - 1].n;
+    spmv(lv[L - 1].A, 0, p, ap, nullptr, st, true);  // ap = A p; pap; alpha
+    k_pcg_update<<<grid_of(n), kCta, 0, stream>>>(n, p, ap, r, st, partials);
+    CK(cudaGetLastError());
+    vcycle(L - 1, r, z, st, r);                      // z = M r; rz; beta
+    k_pcg_p<false><<<grid_of(n), kCta, 0, stream>>>(n, z, p, st, cond);
+    CK(cudaGetLastError());
+  }
+  void build_pcg_graph() {
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle cond;
+    CK(cudaGraphConditionalHandleCreate(&cond, g, 0, cudaGraphCondAssignDefault));
+    CK(cudaStreamBeginCaptureToGraph(stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    pcg_prologue(cond);
+    // Conditional WHILE node appended after the captured prologue.
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    cudaGraph_t cap_graph;
+    CK(cudaStreamGetCaptureInfo(stream, &cs, nullptr, &cap_graph, &deps, &ndeps));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    CK(cudaGraphAddNode(&cnode, cap_graph, deps, ndeps, &cp));
+    CK(cudaStreamUpdateCaptureDependencies(stream, &cnode, 1, cudaStreamSetCaptureDependencies));
+    CK(cudaStreamEndCapture(stream, &g));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    pcg_body(cond);
+    CK(cudaStreamEndCapture(stream, &body));
+    CK(cudaGraphInstantiate(&pcg_exec, g, 0));
+    CK(cudaGraphDestroy(g));
+  }
+  void ensure_residuals(int32_t maxit) {
+    if (maxit + 1 > res_cap) {
+      res_cap = std::max(maxit + 1, 1024);
+      residuals = alloc<double>(static_cast<size_t>(res_cap));
+    }
+  }
+  // Enqueue a whole solve on the stream (no host synchronisation).
+  void pcg_launch(const double* d_b, double* d_x, double tol, int32_t maxit) {
+    ensure_residuals(maxit);
+    PcgState h{};
+    h.tol = tol;
+    h.maxit = maxit;
+    h.k = -1;
+    h.done = 0;
+    h.status = ST_RUNNING;
+    h.b = d_b;
+    h.x = d_x;
+    h.residuals = residuals;
+    CK(cudaMemcpyAsync(st, &h, sizeof(PcgState), cudaMemcpyHostToDevice, stream));
+    if (maxit <= 0) {
+      // Zero iterations allowed: still report the initial residual.
+      const int32_t n = lv[L - 1].n;
+      k_pcg_init<<<grid_of(n), kCta, 0, stream>>>(n, r, st, partials);
+      CK(cudaGetLastError());
+      return;
+    }
+    if (g_use_graph) {
+      if (!pcg_exec) build_pcg_graph();
+      CK(cudaGraphLaunch(pcg_exec, stream));
+    } else {
+      pcg_prologue(0);
+      for (int32_t it = 0; it < maxit; ++it) {
+        int32_t done = 0;
+        CK(cudaMemcpyAsync(&done, &st->done, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (done) break;
+        pcg_body(0);
+      }
+    }
+  }
+  int pcg_collect(double* res_out, int32_t* iters) {
+    CK(cudaStreamSynchronize(stream));
+    PcgState h{};
+    CK(cudaMemcpy(&h, st, sizeof(PcgState), cudaMemcpyDeviceToHost));
+    int status = h.status;
+    int32_t k = std::max(h.k, 0);
+    if (h.maxit <= 0) {
+      status = h.bnorm == 0.0 || 1.0 <= h.tol ? IG_OK : IG_NOT_CONVERGED;
+      k = 0;
+    }
+    if (status == ST_RUNNING) throw Error(IG_CUDA_ERROR, "pcg: solve did not terminate");
+    if (iters) *iters = k;
+    if (res_out) CK(cudaMemcpy(res_out, residuals, sizeof(double) * (static_cast<size_t>(k) + 1), cudaMemcpyDeviceToHost));
+    return status;
+  }
+};
+
+namespace {
+
+int fail(int code, const std::string& m) {
+  g_err = m;
+  return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const Error& e) {
+    return fail(e.code, e.what());
+  } catch (const std::exception& e) {
+    return fail(IG_CUDA_ERROR, e.what());
+  }
+}
+
+void check_csr(const ig_csr& a, const char* what) {
+  if (a.n_rows < 0 || a.n_cols < 0 || a.nnz < 0) throw Error(IG_INVALID_ARGUMENT, std::string(what) + ": negative size");
+  if (a.n_rows > 0 && (!a.row_ptr || (a.nnz > 0 && (!a.col_idx || !a.val))))
+    throw Error(IG_INVALID_ARGUMENT, std::string(what) + ": null array");
+  if (a.n_rows > 0 && (a.row_ptr[0] != 0 || a.row_ptr[a.n_rows] != a.nnz))
+    throw Error(IG_INVALID_ARGUMENT, std::string(what) + ": row_ptr inconsistent with nnz");
+  for (int32_t i = 0; i < a.n_rows; ++i)
+    for (int32_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k)
+      if (a.col_idx[k] < 0 || a.col_idx[k] >= a.n_cols || (k > a.row_ptr[i] && a.col_idx[k] <= a.col_idx[k - 1]))
+        throw Error(IG_INVALID_ARGUMENT, std::string(what) + ": column indices out of range or not ascending");
+}
+
+// Smoother layout for one level (see kernels.cuh: AsGroups / AsGather).
+void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
+  const ig_blocks& B = src.blocks;
+  const int32_t n = L.n, nb = B.n_blocks;
+  if (nb <= 0 || !B.blk_ptr || !B.blk_dofs || !B.fac_ptr || !B.fac)
+    throw Error(IG_INVALID_ARGUMENT, "smoother: empty block layout");
+  L.n_blocks = nb;
+  // Multi-DOF blocks: compact ybuf positions, sorted by size for grouping.
+  std::vector<int32_t> ypos(static_cast<size_t>(nb), -1);
+  std::vector<int32_t> multi;
+  int64_t yl = 0;
+  std::vector<double> sval(static_cast<size_t>(nb), 0.0);
+  for (int32_t b = 0; b < nb; ++b) {
+    const int32_t s = B.blk_ptr[b + 1] - B.blk_ptr[b];
+    if (s <= 0) throw Error(IG_INVALID_ARGUMENT, "smoother: empty block");
+    for (int32_t i = B.blk_ptr[b]; i < B.blk_ptr[b + 1]; ++i)
+      if (B.blk_dofs[i] < 0 || B.blk_dofs[i] >= n) throw Error(IG_INVALID_ARGUMENT, "smoother: DOF out of range");
+    L.sum_s += s;
+    L.sum_s2 += static_cast<int64_t>(s) * s;
+    L.packed_F += static_cast<int64_t>(s) * (s + 1) / 2;
+    if (s == 1) {
+      sval[b] = B.fac[B.fac_ptr[b]];
+    } else {
+      if (s > 128) throw Error(IG_INVALID_ARGUMENT, "smoother: block larger than 128 DOFs");
+      ypos[b] = static_cast<int32_t>(yl);
+      yl += s;
+      multi.push_back(b);
+    }
+  }
+  if (yl > INT32_MAX) throw Error(IG_INVALID_ARGUMENT, "smoother: too many block entries");
+  L.n_multi = static_cast<int32_t>(multi.size());
+  std::stable_sort(multi.begin(), multi.end(), [&](int32_t a, int32_t b) {
+    return (B.blk_ptr[a + 1] - B.blk_ptr[a]) > (B.blk_ptr[b + 1] - B.blk_ptr[b]);
+  });
+  const int32_t ng = (L.n_multi + 31) / 32;
+  std::vector<int32_t> gsmax(static_cast<size_t>(std::max(ng, 1)), 0), gsize(static_cast<size_t>(std::max(ng, 1)) * 32, 0),
+      gypos(static_cast<size_t>(std::max(ng, 1)) * 32, 0), gdofs;
+  std::vector<int64_t> gdoff(static_cast<size_t>(std::max(ng, 1)), 0), gfoff(static_cast<size_t>(std::max(ng, 1)), 0);
+  std::vector<double> gfac;
+  for (int32_t g = 0; g < ng; ++g) {
+    const int32_t b0 = multi[static_cast<size_t>(g) * 32];
+    const int32_t smax = B.blk_ptr[b0 + 1] - B.blk_ptr[b0];
+    gsmax[g] = smax;
+    gdoff[g] = static_cast<int64_t>(gdofs.size());
+    gfoff[g] = static_cast<int64_t>(gfac.size());
+    const int64_t np = static_cast<int64_t>(smax) * (smax + 1) / 2;
+    gdofs.resize(gdofs.size() + static_cast<size_t>(smax) * 32, 0);
+    gfac.resize(gfac.size() + static_cast<size_t>(np) * 32, 1.0);
+    for (int lane = 0; lane < 32; ++lane) {
+      const int64_t idx = static_cast<int64_t>(g) * 32 + lane;
+      if (idx >= L.n_multi) continue;
+      const int32_t b = multi[idx];
+      const int32_t s = B.blk_ptr[b + 1] - B.blk_ptr[b];
+      gsize[idx] = s;
+      gypos[idx] = ypos[b];
+      for (int i = 0; i < s; ++i) gdofs[gdoff[g] + static_cast<int64_t>(i) * 32 + lane] = B.blk_dofs[B.blk_ptr[b] + i];
+      const double* f = B.fac + B.fac_ptr[b];
+      for (int j = 0; j < s; ++j)
+        for (int i = j; i < s; ++i) {
+          const int64_t e = static_cast<int64_t>(j) * smax - (static_cast<int64_t>(j) * (j - 1)) / 2 + (i - j);
+          gfac[gfoff[g] + e * 32 + lane] = f[static_cast<size_t>(j) * s + i];
+        }
+    }
+  }
+  L.G.n_groups = ng;
+  L.G.smax = h.upload(gsmax.data(), gsmax.size());
+  L.G.dof_off = h.upload(gdoff.data(), gdoff.size());
+  L.G.fac_off = h.upload(gfoff.data(), gfoff.size());
+  L.G.size = h.upload(gsize.data(), gsize.size());
+  L.G.ypos = h.upload(gypos.data(), gypos.size());
+  L.G.dofs = h.upload(gdofs.data(), std::max<size_t>(gdofs.size(), 1));
+  L.G.fac = h.upload(gfac.data(), std::max<size_t>(gfac.size(), 1));
+  L.ybuf = h.alloc<double>(static_cast<size_t>(std::max<int64_t>(yl, 1)));
+  // Per-DOF contribution lists in ascending block order.
+  std::vector<int32_t> cnt(static_cast<size_t>(n) + 1, 0);
+  for (int32_t b = 0; b < nb; ++b)
+    for (int32_t i = B.blk_ptr[b]; i < B.blk_ptr[b + 1]; ++i) ++cnt[B.blk_dofs[i] + 1];
+  for (int32_t d = 0; d < n; ++d) cnt[d + 1] += cnt[d];
+  std::vector<int32_t> centry(static_cast<size_t>(cnt[n]));
+  std::vector<int32_t> nx(cnt.begin(), cnt.end() - 1);
+  for (int32_t b = 0; b < nb; ++b) {
+    const int32_t s = B.blk_ptr[b + 1] - B.blk_ptr[b];
+    for (int32_t i = 0; i < s; ++i) {
+      const int32_t d = B.blk_dofs[B.blk_ptr[b] + i];
+      centry[nx[d]++] = s == 1 ? -(b + 1) : ypos[b] + i;
+    }
+  }
+  L.S.n = n;
+  L.S.gamma = src.gamma;
+  L.S.cptr = h.upload(cnt.data(), cnt.size());
+  L.S.centry = h.upload(centry.data(), std::max<size_t>(centry.size(), 1));
+  L.S.sval = h.upload(sval.data(), sval.size());
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ig_last_error(void) { return g_err.c_str(); }
+
+int ig_set_option(int32_t option, int64_t value) {
+  if (option == IG_OPT_USE_GRAPH) {
+    g_use_graph = value != 0;
+    return IG_OK;
+  }
+  return fail(IG_INVALID_ARGUMENT, "ig_set_option: unknown option");
+}
+
+int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* coarse, ig_hier** out) {
+  if (!out) return fail(IG_INVALID_ARGUMENT, "ig_hier_create: null out");
+  *out = nullptr;
+  if (!levels || !coarse || n_levels < 1 || n_levels > 16)
+    return fail(IG_INVALID_ARGUMENT, "ig_hier_create: need 1..16 levels and a coarse factor");
+  return guarded([&] {
+    auto h = std::make_unique<ig_hier>();
+    h->L = n_levels;
+    h->lv.resize(n_levels);
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&h->ev0));
+    CK(cudaEventCreate(&h->ev1));
+    ig_info& I = h->info;
+    I.n_levels = n_levels;
+    for (int l = 0; l < n_levels; ++l) {
+      const ig_level& s = levels[l];
+      Level& L = h->lv[l];
+      check_csr(s.A, "A");
+      if (s.A.n_rows != s.A.n_cols) throw Error(IG_INVALID_ARGUMENT, "A must be square");
+      L.n = s.A.n_rows;
+      if (L.n <= 0) throw Error(IG_INVALID_ARGUMENT, "empty level");
+      I.n[l] = L.n;
+      I.nnz_A[l] = s.A.nnz;
+      L.r_in = h->alloc<double>(L.n);
+      L.x = h->alloc<double>(L.n);
+      if (l == 0) continue;
+      check_csr(s.R, "R");
+      if (s.R.n_cols != L.n || s.R.n_rows != levels[l - 1].A.n_rows)
+        throw Error(IG_INVALID_ARGUMENT, "R has the wrong shape");
+      if (s.smoother_kind != IG_SMOOTHER_ADDITIVE_SCHWARZ)
+        throw Error(IG_UNSUPPORTED, "device smoother: only additive Schwarz is implemented");
+      I.nnz_R[l] = s.R.nnz;
+      L.A = h->upload_sell(to_sell(s.A.n_rows, s.A.n_cols, s.A.row_ptr, s.A.col_idx, s.A.val), s.A.nnz);
+      L.R = h->upload_sell(to_sell(s.R.n_rows, s.R.n_cols, s.R.row_ptr, s.R.col_idx, s.R.val), s.R.nnz);
+      std::vector<int32_t> tp, tc;
+      std::vector<double> tv;
+      csr_transpose(s.R, tp, tc, tv);
+      L.P = h->upload_sell(to_sell(s.R.n_cols, s.R.n_rows, tp.data(), tc.data(), tv.data()), s.R.nnz);
+      L.res = h->alloc<double>(L.n);
+      L.cor = h->alloc<double>(L.n);
+      build_smoother(*h, L, s);
+      I.sell_slots_A[l] = L.A.slots;
+      I.n_blocks[l] = L.n_blocks;
+      I.n_multi_blocks[l] = L.n_multi;
+      I.sum_s[l] = L.sum_s;
+      I.sum_s2[l] = L.sum_s2;
+    }
+    // Finest A is used by PCG even with a single level.
+    Level& F = h->lv[n_levels - 1];
+    if (n_levels == 1) {
+      const ig_level& s = levels[0];
+      F.A = h->upload_sell(to_sell(s.A.n_rows, s.A.n_cols, s.A.row_ptr, s.A.col_idx, s.A.val), s.A.nnz);
+      I.sell_slots_A[0] = F.A.slots;
+    }
+    // Coarse factor.
+    h->n0 = coarse->n;
+    h->rank = coarse->rank;
+    if (h->n0 != h->lv[0].n) throw Error(IG_INVALID_ARGUMENT, "coarse factor size differs from level 0");
+    if (h->rank < 0 || h->rank > h->n0) throw Error(IG_INVALID_ARGUMENT, "coarse rank out of range");
+    if (h->rank > 1024) throw Error(IG_UNSUPPORTED, "coarse rank above 1024");
+    if (!coarse->L || !coarse->piv) throw Error(IG_INVALID_ARGUMENT, "coarse factor arrays are null");
+    for (int k = 0; k < h->n0; ++k)
+      if (coarse->piv[k] < 1 || coarse->piv[k] > h->n0) throw Error(IG_INVALID_ARGUMENT, "coarse pivot out of range");
+    const int64_t rk = h->rank, n0 = h->n0;
+    std::vector<double> packed(static_cast<size_t>(std::max<int64_t>(rk * (rk + 1) / 2, 1)), 0.0);
+    for (int64_t j = 0; j < rk; ++j)
+      for (int64_t i = j; i < rk; ++i) packed[j * rk - (j * (j - 1)) / 2 + (i - j)] = coarse->L[j * n0 + i];
+    h->Lp = h->upload(packed.data(), packed.size());
+    h->piv = h->upload(coarse->piv, static_cast<size_t>(n0));
+    h->coarse_threads = std::max(32, static_cast<int>((std::max<int64_t>(rk, 1) + 31) / 32 * 32));
+    const size_t smem = sizeof(double) * (static_cast<size_t>((rk + 1) & ~int64_t(1)) + packed.size());
+    int max_optin = 0;
+    CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
+    if (smem <= static_cast<size_t>(max_optin)) {
+      h->coarse_use_smem = 1;
+      h->coarse_smem = smem;
+      // Process-wide function attribute: raise it to the opt-in maximum so no
+      // handle created later can shrink it below another handle's need.
+      CK(cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+    } else {
+      h->coarse_use_smem = 0;
+      h->coarse_smem = sizeof(double) * static_cast<size_t>((rk + 2) & ~int64_t(1));
+    }
+    // PCG workspace.
+    const int32_t nf = F.n;
+    h->r = h->alloc<double>(nf);
+    h->z = h->alloc<double>(nf);
+    h->p = h->alloc<double>(nf);
+    h->ap = h->alloc<double>(nf);
+    h->hb = h->alloc<double>(nf);
+    h->hx = h->alloc<double>(nf);
+    h->partials = h->alloc<double>(grid_of(nf) + 1);
+    h->st = h->alloc<PcgState>(1);
+    CK(cudaMemset(h->st, 0, sizeof(PcgState)));
+    h->ensure_residuals(1000);
+    // Algorithmic bytes and launch counts.
+    int64_t vc = 0;
+    int kv = 1;  // coarse
+    for (int l = 1; l < n_levels; ++l) {
+      const Level& L = h->lv[l];
+      const int64_t n = L.n, nc = h->lv[l - 1].n;
+      const int64_t as = 8 * L.packed_F + 8 * L.sum_s + 4 * (L.n_blocks + 1) + 4 * (n + 1) + 16 * n;
+      vc += 2 * bytes_spmv(n, n, L.A.nnz, true);
+      vc += 2 * as + 8 * n;                                              // second application accumulates
+      vc += bytes_spmv(nc, n, L.R.nnz, false);                           // R
+      vc += 12 * L.R.nnz + 4 * (n + 1) + 8 * nc + 16 * n + 8 * n;        // P + x update
+      kv += 2 * (L.n_multi > 0 ? 2 : 1) + 4;
+    }
+    vc += 8 * static_cast<int64_t>(h->rank) * h->rank + 24 * static_cast<int64_t>(h->n0);
+    I.bytes_vcycle = vc;
+    I.bytes_spmv_finest = bytes_spmv(nf, nf, F.A.nnz, false);
+    I.bytes_pcg_iter = vc + I.bytes_spmv_finest + 80 * static_cast<int64_t>(nf);
+    I.kernels_vcycle = kv;
+    I.kernels_pcg_iter = kv + 3;
+    CK(cudaDeviceSynchronize());
+    *out = h.release();
+    return IG_OK;
+  });
+}
+
+void ig_hier_destroy(ig_hier* h) { delete h; }
+
+int ig_hier_info(const ig_hier* h, ig_info* out) {
+  if (!h || !out) return fail(IG_INVALID_ARGUMENT, "ig_hier_info: null argument");
+  *out = h->info;
+  return IG_OK;
+}
+
+void* ig_hier_stream(ig_hier* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int ig_vcycle_at(ig_hier* h, int32_t level, const double* r, double* x) {
+  if (!h || !r || !x) return fail(IG_INVALID_ARGUMENT, "vcycle_at: null argument");
+  if (level < 0 || level >= h->L) return fail(IG_INVALID_ARGUMENT, "vcycle_at: level out of range");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return guarded([&] {
+    Level& L = h->lv[level];
+    CK(cudaMemcpyAsync(L.r_in, r, sizeof(double) * L.n, cudaMemcpyHostToDevice, h->stream));
+    h->vcycle(level, L.r_in, h->hx, nullptr, nullptr);
+    CK(cudaMemcpyAsync(x, h->hx, sizeof(double) * L.n, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return IG_OK;
+  });
+}
+
+int ig_vcycle(ig_hier* h, const double* r, double* x) {
+  if (!h) return fail(IG_INVALID_ARGUMENT, "vcycle: null handle");
+  return ig_vcycle_at(h, h->L - 1, r, x);
+}
+
+int ig_coarse_solve(ig_hier* h, const double* r, double* x) {
+  if (!h) return fail(IG_INVALID_ARGUMENT, "coarse_solve: null handle");
+  return ig_vcycle_at(h, 0, r, x);
+}
+
+int ig_smoother_apply(ig_hier* h, int32_t level, const double* r, double* x) {
+  if (!h || !r || !x) return fail(IG_INVALID_ARGUMENT, "smoother_apply: null argument");
+  if (level < 1 || level >= h->L) return fail(IG_INVALID_ARGUMENT, "smoother_apply: level has no smoother");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return guarded([&] {
+    Level& L = h->lv[level];
+    CK(cudaMemcpyAsync(L.r_in, r, sizeof(double) * L.n, cudaMemcpyHostToDevice, h->stream));
+    h->smoother(L, L.r_in, h->hx, false, nullptr, nullptr);
+    CK(cudaMemcpyAsync(x, h->hx, sizeof(double) * L.n, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return IG_OK;
+  });
+}
+
+int ig_level_spmv(ig_hier* h, int32_t level, const double* x, double* y, int32_t mode) {
+  if (!h || !x || !y) return fail(IG_INVALID_ARGUMENT, "level_spmv: null argument");
+  if (level < 0 || level >= h->L) return fail(IG_INVALID_ARGUMENT, "level_spmv: level out of range");
+  if (mode < 0 || mode > 3) return fail(IG_INVALID_ARGUMENT, "level_spmv: bad mode");
+  if (mode >= 2 && level == 0) return fail(IG_INVALID_ARGUMENT, "level_spmv: coarsest level has no R");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return guarded([&] {
+    Level& L = h->lv[level];
+    const DevSell* M = nullptr;
+    if (mode <= 1) {
+      if (level == 0 && h->L > 1) throw Error(IG_UNSUPPORTED, "level_spmv: coarsest A is not resident (dense factor only)");
+      M = &L.A;
+    } else {
+      M = mode == 2 ? &L.R : &L.P;
+    }
+    const int32_t nin = M->s.n_cols, nout = M->s.n_rows;
+    double* din = h->hb;   // finest-sized scratch (every level fits)
+    double* dout = h->hx;
+    CK(cudaMemcpyAsync(din, x, sizeof(double) * nin, cudaMemcpyHostToDevice, h->stream));
+    if (mode == 1) CK(cudaMemcpyAsync(dout, y, sizeof(double) * nout, cudaMemcpyHostToDevice, h->stream));
+    h->spmv(*M, mode == 1 ? 1 : 0, din, dout, dout);
+    CK(cudaMemcpyAsync(y, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return IG_OK;
+  });
+}
+
+int ig_level_spmv_device(ig_hier* h, int32_t level, const double* d_x, double* d_y, int32_t mode) {
+  if (!h || !d_x || !d_y) return fail(IG_INVALID_ARGUMENT, "level_spmv_device: null argument");
+  if (level < 0 || level >= h->L || mode < 0 || mode > 3 || (mode >= 2 && level == 0))
+    return fail(IG_INVALID_ARGUMENT, "level_spmv_device: bad level or mode");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return guarded([&] {
+    Level& L = h->lv[level];
+    if (mode <= 1 && level == 0 && h->L > 1)
+      throw Error(IG_UNSUPPORTED, "level_spmv_device: coarsest A is not resident (dense factor only)");
+    const DevSell& M = mode <= 1 ? L.A : (mode == 2 ? L.R : L.P);
+    h->spmv(M, mode == 1 ? 1 : 0, d_x, d_y, d_y);
+    return IG_OK;
+  });
+}
+
+int ig_vcycle_device(ig_hier* h, const double* d_r, double* d_x) {
+  if (!h || !d_r || !d_x) return fail(IG_INVALID_ARGUMENT, "vcycle_device: null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return guarded([&] {
+    if (!g_use_graph) {
+      h->vcycle(h->L - 1, d_r, d_x, nullptr, nullptr);
+      return IG_OK;
+    }
+    cudaGraphExec_t ex = nullptr;
+    for (auto& g : h->vc_graphs)
+      if (g.r == d_r && g.x == d_x) ex = g.exec;
+    if (!ex) {
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+      h->vcycle(h->L - 1, d_r, d_x, nullptr, nullptr);
+      CK(cudaStreamEndCapture(h->stream, &g));
+      CK(cudaGraphInstantiate(&ex, g, 0));
+      CK(cudaGraphDestroy(g));
+      h->vc_graphs.push_back({d_r, d_x, ex});
+    }
+    CK(cudaGraphLaunch(ex, h->stream));
+    return IG_OK;
+  });
+}
+
+int ig_pcg_device(ig_hier* h, const double* d_b, double tol, int32_t maxit, double* d_x) {
+  if (!h || !d_b || !d_x) return fail(IG_INVALID_ARGUMENT, "pcg_device: null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return guarded([&] {
+    h->pcg_launch(d_b, d_x, tol, maxit);
+    return IG_OK;
+  });
+}
+
+int ig_pcg_result(ig_hier* h, double* residuals, int32_t* iterations) {
+  if (!h) return fail(IG_INVALID_ARGUMENT, "pcg_result: null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return guarded([&] {
+    const int s = h->pcg_collect(residuals, iterations);
+    if (s == IG_NOT_CONVERGED) g_err = "pcg: no convergence within the iteration budget";
+    if (s == IG_BREAKDOWN) g_err = "pcg: p^T A p <= 0 (operator not SPD)";
+    return s;
+  });
+}
+
+int ig_pcg(ig_hier* h, const double* b, double tol, int32_t maxit, double* x, double* residuals,
+           int32_t* iterations, double* seconds) {
+  if (!h || !b || !x || !residuals || !iterations) return fail(IG_INVALID_ARGUMENT, "pcg: null argument");
+  if (maxit < 0) return fail(IG_INVALID_ARGUMENT, "pcg: maxit must be >= 0");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return guarded([&] {
+    const int32_t n = h->lv[h->L - 1].n;
+    CK(cudaMemcpyAsync(h->hb, b, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaEventRecord(h->ev0, h->stream));
+    h->pcg_launch(h->hb, h->hx, tol, maxit);
+    CK(cudaEventRecord(h->ev1, h->stream));
+    CK(cudaMemcpyAsync(x, h->hx, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+    const int s = h->pcg_collect(residuals, iterations);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (seconds) *seconds = 1e-3 * ms;
+    if (s == IG_NOT_CONVERGED) g_err = "pcg: no convergence within " + std::to_string(maxit) + " iterations";
+    if (s == IG_BREAKDOWN) g_err = "pcg: p^T A p <= 0 (operator not SPD)";
+    return s;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,500 @@
+// Device kernels of the solve phase (sm_100a, FP64, HBM-bound; no tensor
+// cores -- every operation here is <= 0.25 flop/B).
+//
+// Arithmetic contract: the library is compiled with -fmad=false, so every
+// a*b+c rounds twice, exactly like the reference's default x86-64 build and
+// the oracle (-ffp-contract=off).  Every kernel fixes its summation order to
+// the one the oracle documents, so device results are bitwise reproducible
+// run to run and bitwise equal to oracle/oracle.c in ORC_GPU_ORDER mode.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace igk {
+
+constexpr int kCta = 256;   // threads per CTA == reduction chunk size
+constexpr int kSell = 32;   // SELL slice height == warp size
+
+// ----------------------------------------------------------- PCG state ----
+// Device-resident solver state: scalars, flags and the residual history.  The
+// whole PCG loop reads/writes it, so no host round trip is needed.
+struct PcgState {
+  double bnorm, rz, rz_new, pap, alpha, beta, tol;
+  int32_t k, maxit, done, status;
+  const double* b;   // right-hand side (device pointer, set per solve)
+  double* x;         // solution (device pointer, set per solve)
+  double* residuals; // maxit+1
+  unsigned int counter[8];
+};
+enum { ST_RUNNING = -1, ST_OK = 0, ST_NOT_CONVERGED = 1, ST_BREAKDOWN = 2 };
+
+// ------------------------------------------------------------ reduction ---
+// Canonical chunk reduction (oracle.c tree256): 32-lane xor butterfly per
+// warp, then ((w0+w1)+(w2+w3))+((w4+w5)+(w6+w7)).  Result valid in thread 0.
+__device__ __forceinline__ double cta_reduce(double v, double* sm8) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) sm8[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    t = ((sm8[0] + sm8[1]) + (sm8[2] + sm8[3])) + ((sm8[4] + sm8[5]) + (sm8[6] + sm8[7]));
+  return t;
+}
+
+// Reduce this CTA's chunk (one value per thread, cta_reduce) and publish the
+// partial; the last CTA to arrive reduces all partials (lane t sums P[t],
+// P[t+256], ... ascending, then cta_reduce) and returns true with *total set
+// (valid in every thread of that CTA).  Must be reached by all threads.
+__device__ __forceinline__ bool last_cta_total(double v, double* partials,
+                                               unsigned int* counter, double* total) {
+  __shared__ double sm8[8];
+  __shared__ bool is_last;
+  __shared__ double tot;
+  const double partial = cta_reduce(v, sm8);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = partial;
+    __threadfence();
+    const unsigned int prev = atomicAdd(counter, 1u);
+    is_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return false;
+  __threadfence();
+  double a = 0.0;
+  for (unsigned int k = threadIdx.x; k < gridDim.x; k += kCta) a = a + __ldcg(partials + k);
+  __syncthreads();  // sm8 reuse
+  const double t = cta_reduce(a, sm8);
+  if (threadIdx.x == 0) {
+    tot = t;
+    *counter = 0u;
+  }
+  __syncthreads();
+  *total = tot;
+  return true;
+}
+
+__device__ __forceinline__ bool pcg_done(const PcgState* st) {
+  return st != nullptr && *reinterpret_cast<const volatile int32_t*>(&st->done);
+}
+
+// ----------------------------------------------------------- SELL SpMV ----
+// Sliced ELLPACK, slice height 32, column-major within a slice: entry k of
+// row i sits at slice_ptr[i/32] + 32*k + (i%32).  One thread per row walks its
+// row in ascending column order (== Eigen RowMajor order), so warps load 32
+// consecutive doubles / ints per step (coalesced) and the x gathers of
+// neighbouring rows share sectors.
+struct Sell {
+  int32_t n_rows, n_cols;
+  const int64_t* slice_ptr;
+  const int32_t* rowlen;
+  const double* val;
+  const int32_t* col;
+};
+
+template <bool STREAM>
+__device__ __forceinline__ double ld_val(const double* p) {
+  if (STREAM) return __ldcs(p);
+  return __ldg(p);
+}
+template <bool STREAM>
+__device__ __forceinline__ int32_t ld_col(const int32_t* p) {
+  if (STREAM) return __ldcs(p);
+  return __ldg(p);
+}
+
+// Row dot product, ascending k, unrolled loads (the sum itself stays serial).
+template <bool STREAM>
+__device__ __forceinline__ double sell_row(const Sell& A, int row, const double* __restrict__ x) {
+  const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
+  const int len = A.rowlen[row];
+  const double* vp = A.val + base;
+  const int32_t* cp = A.col + base;
+  double acc = 0.0;
+  int k = 0;
+  constexpr int U = 8;
+  for (; k + U <= len; k += U) {
+    double v[U];
+    int32_t c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      v[u] = ld_val<STREAM>(vp + (k + u) * kSell);
+      c[u] = ld_col<STREAM>(cp + (k + u) * kSell);
+    }
+    double xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = acc + v[u] * xv[u];
+  }
+  for (; k < len; ++k) acc = acc + ld_val<STREAM>(vp + k * kSell) * __ldg(x + ld_col<STREAM>(cp + k * kSell));
+  return acc;
+}
+
+// MODE 0: y = A x.  MODE 1: y = r - A x with r read from y (in place allowed).
+// RED: also reduce x_i * y_i (p . Ap) into the PCG state.
+template <int MODE, bool STREAM, bool RED>
+__global__ void __launch_bounds__(kCta) k_spmv(Sell A, const double* __restrict__ x, double* y,
+                                               const double* rsrc, PcgState* st, double* partials) {
+  if (pcg_done(st)) return;
+  const int row = blockIdx.x * kCta + threadIdx.x;
+  double prod = 0.0;
+  if (row < A.n_rows) {
+    const double acc = sell_row<STREAM>(A, row, x);
+    double out;
+    if (MODE == 0)
+      out = acc;
+    else
+      out = rsrc[row] - acc;
+    y[row] = out;
+    if (RED) prod = x[row] * out;
+  }
+  if (RED) {
+    double pap;
+    if (last_cta_total(prod, partials, &st->counter[0], &pap)) {
+      if (threadIdx.x == 0) {
+        st->pap = pap;
+        if (pap <= 0.0) {  // solvers.cpp:47-50 (a NaN does not trigger it)
+          st->status = ST_BREAKDOWN;
+          st->done = 1;
+        } else {
+          st->alpha = st->rz / pap;
+        }
+      }
+    }
+  }
+}
+
+// Prolongation fused with the correction: cor = P xc (P = R^T stored as CSR
+// over fine rows, ascending coarse index == Eigen's column-major R^T product
+// order) and x += cor.
+template <bool STREAM>
+__global__ void __launch_bounds__(kCta) k_prolong(Sell P, const double* __restrict__ xc, double* cor,
+                                                  double* x, const PcgState* st) {
+  if (pcg_done(st)) return;
+  const int row = blockIdx.x * kCta + threadIdx.x;
+  if (row >= P.n_rows) return;
+  const double c = sell_row<STREAM>(P, row, xc);
+  cor[row] = c;
+  x[row] = x[row] + c;
+}
+
+// ------------------------------------------------- additive Schwarz -------
+// Phase 1: multi-DOF blocks (s >= 2), one thread per block.  Blocks are sorted
+// by size (descending) and grouped by 32 (one warp); per group the DOF lists,
+// output positions and packed lower factors are interleaved lane-fastest so
+// every load is coalesced.  Packed lower column-major with the group's
+// s_max as stride: e(i, j) = j*smax - j*(j-1)/2 + (i - j), i >= j.
+struct AsGroups {
+  int32_t n_groups;
+  const int32_t* smax;      // per group
+  const int64_t* dof_off;   // per group: base of [i][lane] dof table
+  const int64_t* fac_off;   // per group: base of [e][lane] factor table
+  const int32_t* size;      // [group*32 + lane], 0 for padding lanes
+  const int32_t* ypos;      // [group*32 + lane]: ybuf offset of the block
+  const int32_t* dofs;
+  const double* fac;
+};
+
+__device__ __forceinline__ int packed_idx(int i, int j, int smax) {
+  return j * smax - (j * (j - 1)) / 2 + (i - j);
+}
+
+template <int SM>
+__device__ __forceinline__ void block_solve(const AsGroups& G, int g, int lane, int s, int smax,
+                                            const double* __restrict__ r, double* ybuf) {
+  double y[SM];
+  const int32_t* dp = G.dofs + G.dof_off[g] + lane;
+  const double* fp = G.fac + G.fac_off[g] + lane;
+#pragma unroll
+  for (int i = 0; i < SM; ++i) y[i] = (i < s) ? __ldg(r + dp[i * 32]) : 0.0;
+  // forward: column oriented
+#pragma unroll
+  for (int j = 0; j < SM; ++j) {
+    if (j < s) {
+      const double yj = y[j] / fp[packed_idx(j, j, smax) * 32];
+      y[j] = yj;
+#pragma unroll
+      for (int i = j + 1; i < SM; ++i)
+        if (i < s) y[i] = y[i] - fp[packed_idx(i, j, smax) * 32] * yj;
+    }
+  }
+  // backward: y_i = (y_i - sum_{k desc} L(k,i) y_k) / L(i,i)
+#pragma unroll
+  for (int i = SM - 1; i >= 0; --i) {
+    if (i < s) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = SM - 1; k > i; --k)
+        if (k < s) acc = acc + fp[packed_idx(k, i, smax) * 32] * y[k];
+      y[i] = (y[i] - acc) / fp[packed_idx(i, i, smax) * 32];
+    }
+  }
+  const int pos = G.ypos[g * 32 + lane];
+#pragma unroll
+  for (int i = 0; i < SM; ++i)
+    if (i < s) ybuf[pos + i] = y[i];
+}
+
+// Generic (any size) fallback with local memory.
+__device__ __noinline__ void block_solve_any(const AsGroups& G, int g, int lane, int s, int smax,
+                                             const double* __restrict__ r, double* ybuf) {
+  double y[128];
+  const int32_t* dp = G.dofs + G.dof_off[g] + lane;
+  const double* fp = G.fac + G.fac_off[g] + lane;
+  for (int i = 0; i < s; ++i) y[i] = __ldg(r + dp[i * 32]);
+  for (int j = 0; j < s; ++j) {
+    const double yj = y[j] / fp[packed_idx(j, j, smax) * 32];
+    y[j] = yj;
+    for (int i = j + 1; i < s; ++i) y[i] = y[i] - fp[packed_idx(i, j, smax) * 32] * yj;
+  }
+  for (int i = s - 1; i >= 0; --i) {
+    double acc = 0.0;
+    for (int k = s - 1; k > i; --k) acc = acc + fp[packed_idx(k, i, smax) * 32] * y[k];
+    y[i] = (y[i] - acc) / fp[packed_idx(i, i, smax) * 32];
+  }
+  const int pos = G.ypos[g * 32 + lane];
+  for (int i = 0; i < s; ++i) ybuf[pos + i] = y[i];
+}
+
+__global__ void __launch_bounds__(128) k_as_blocks(AsGroups G, const double* __restrict__ r,
+                                                   double* ybuf, const PcgState* st) {
+  if (pcg_done(st)) return;
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= G.n_groups) return;
+  const int s = G.size[g * 32 + lane];
+  const int smax = G.smax[g];  // warp-uniform
+  if (s == 0) return;
+  if (smax <= 4)
+    block_solve<4>(G, g, lane, s, smax, r, ybuf);
+  else if (smax <= 8)
+    block_solve<8>(G, g, lane, s, smax, r, ybuf);
+  else if (smax <= 16)
+    block_solve<16>(G, g, lane, s, smax, r, ybuf);
+  else if (smax <= 32)
+    block_solve<32>(G, g, lane, s, smax, r, ybuf);
+  else
+    block_solve_any(G, g, lane, s, smax, r, ybuf);
+}
+
+// Phase 2: deterministic segmented reduction per DOF, contributions in
+// ascending block order starting from 0 (smoothers.cpp:176-183), then gamma.
+// Entry code >= 0: ybuf offset (multi-DOF block); code = -(b+1): singleton
+// block b whose only member is this DOF, y = (r_d / l) / l with l = sval[b]
+// (== the LLT solve of a 1x1 block: forward r/l, backward (y - 0)/l).
+// ACC: x += gamma*sum (post-smoother) else x = gamma*sum.
+// RED: also reduce rdot_i * x_i (r . z) into the PCG state (finest level).
+struct AsGather {
+  int32_t n;
+  double gamma;
+  const int32_t* cptr;
+  const int32_t* centry;
+  const double* sval;
+};
+
+// rz = r . z bookkeeping after a preconditioner application (solvers.cpp:41-43, :63-65).
+__device__ __forceinline__ void rz_update(PcgState* st, double rz) {
+  if (st->k < 0) {  // initial application: p = z, rz = r.z
+    st->rz = rz;
+    st->k = 0;
+  } else {
+    st->rz_new = rz;
+    st->beta = rz / st->rz;
+    st->rz = rz;
+  }
+}
+
+template <bool ACC, bool RED>
+__global__ void __launch_bounds__(kCta) k_as_gather(AsGather S, const double* __restrict__ r,
+                                                    const double* __restrict__ ybuf, double* x,
+                                                    const double* rdot, PcgState* st, double* partials) {
+  if (pcg_done(st)) return;
+  const int d = blockIdx.x * kCta + threadIdx.x;
+  double prod = 0.0;
+  if (d < S.n) {
+    double acc = 0.0;
+    const int q0 = S.cptr[d], q1 = S.cptr[d + 1];
+    for (int q = q0; q < q1; ++q) {
+      const int code = S.centry[q];
+      double v;
+      if (code < 0) {
+        const double l = S.sval[-code - 1];
+        v = (r[d] / l) / l;
+      } else {
+        v = ybuf[code];
+      }
+      acc = acc + v;
+    }
+    const double out = S.gamma * acc;
+    const double xn = ACC ? x[d] + out : out;
+    x[d] = xn;
+    if (RED) prod = rdot[d] * xn;
+  }
+  if (RED) {
+    double rz;
+    if (last_cta_total(prod, partials, &st->counter[2], &rz))
+      if (threadIdx.x == 0) rz_update(st, rz);
+  }
+}
+
+// r . z as its own pass, for a 1-level hierarchy whose preconditioner is the
+// coarse solve alone (no smoother kernel to fuse the reduction into).
+__global__ void __launch_bounds__(kCta) k_pcg_rz(int32_t n, const double* __restrict__ r,
+                                                 const double* __restrict__ z, PcgState* st,
+                                                 double* partials) {
+  if (pcg_done(st)) return;
+  const int i = blockIdx.x * kCta + threadIdx.x;
+  const double prod = i < n ? r[i] * z[i] : 0.0;
+  double rz;
+  if (last_cta_total(prod, partials, &st->counter[2], &rz))
+    if (threadIdx.x == 0) rz_update(st, rz);
+}
+
+// ------------------------------------------------------------ coarse ------
+// Permuted, rank-truncated L11 L11^T solve (multigrid.cpp:77-88), one CTA.
+// Thread t owns row t (rank <= blockDim).  Forward: column oriented, one
+// barrier per column.  Backward: row-dot form with descending k, the
+// accumulation advanced as each y_k is finalised.  L11 is staged packed in
+// shared memory when it fits.
+__global__ void k_coarse(int32_t n, int32_t rank, const double* __restrict__ Lp,
+                         const int32_t* __restrict__ piv, const double* __restrict__ r, double* x,
+                         int use_smem, const PcgState* st) {
+  if (pcg_done(st)) return;
+  extern __shared__ double smem[];
+  double* y = smem;                     // rank
+  double* Ls = smem + ((rank + 1) & ~1);  // packed lower, rank*(rank+1)/2
+  const int t = threadIdx.x;
+  const int64_t np = static_cast<int64_t>(rank) * (rank + 1) / 2;
+  const double* L = Lp;
+  if (use_smem) {
+    for (int64_t k = t; k < np; k += blockDim.x) Ls[k] = Lp[k];
+    L = Ls;
+  }
+  auto Lij = [&](int i, int j) { return L[static_cast<int64_t>(j) * rank - (static_cast<int64_t>(j) * (j - 1)) / 2 + (i - j)]; };
+  double yi = 0.0;
+  if (t < rank) yi = r[piv[t] - 1];
+  __syncthreads();
+  // forward
+  if (t == 0 && rank > 0) {
+    yi = yi / Lij(0, 0);
+    y[0] = yi;
+  }
+  for (int j = 0; j < rank; ++j) {
+    __syncthreads();
+    const double yj = y[j];
+    if (t > j && t < rank) {
+      yi = yi - Lij(t, j) * yj;
+      if (t == j + 1) {
+        yi = yi / Lij(t, t);
+        y[t] = yi;
+      }
+    }
+  }
+  __syncthreads();
+  // backward
+  double acc = 0.0;
+  if (t == rank - 1) {
+    yi = (yi - acc) / Lij(t, t);
+    y[t] = yi;
+  }
+  for (int k = rank - 1; k > 0; --k) {
+    __syncthreads();
+    const double yk = y[k];
+    if (t < k) {
+      acc = acc + Lij(k, t) * yk;
+      if (t == k - 1) {
+        yi = (yi - acc) / Lij(t, t);
+        y[t] = yi;
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = t; k < n; k += blockDim.x) x[piv[k] - 1] = (k < rank) ? y[k] : 0.0;
+}
+
+// ---------------------------------------------------------- PCG vectors ---
+
+// x = 0, r = b, bnorm from the canonical reduction (solvers.cpp:24-39).
+__global__ void __launch_bounds__(kCta) k_pcg_init(int32_t n, double* r, PcgState* st, double* partials) {
+  const int i = blockIdx.x * kCta + threadIdx.x;
+  double prod = 0.0;
+  if (i < n) {
+    const double bi = st->b[i];
+    st->x[i] = 0.0;
+    r[i] = bi;
+    prod = bi * bi;
+  }
+  double bb;
+  if (last_cta_total(prod, partials, &st->counter[3], &bb)) {
+    if (threadIdx.x == 0) {
+      const double bn = sqrt(bb);
+      st->bnorm = bn;
+      st->k = -1;
+      if (bn == 0.0) {
+        st->residuals[0] = 0.0;
+        st->status = ST_OK;
+        st->done = 1;
+      } else {
+        st->residuals[0] = 1.0;
+        if (1.0 <= st->tol) {
+          st->status = ST_OK;
+          st->done = 1;
+        }
+      }
+    }
+  }
+}
+
+// x += alpha p; r -= alpha Ap; rel = ||r|| / ||b|| (solvers.cpp:51-61).
+__global__ void __launch_bounds__(kCta) k_pcg_update(int32_t n, const double* __restrict__ p,
+                                                     const double* __restrict__ ap, double* r,
+                                                     PcgState* st, double* partials) {
+  if (pcg_done(st)) return;
+  const int i = blockIdx.x * kCta + threadIdx.x;
+  const double alpha = st->alpha;
+  double prod = 0.0;
+  if (i < n) {
+    double* x = st->x;
+    x[i] = x[i] + alpha * p[i];
+    const double ri = r[i] - alpha * ap[i];
+    r[i] = ri;
+    prod = ri * ri;
+  }
+  double rr;
+  if (last_cta_total(prod, partials, &st->counter[1], &rr)) {
+    if (threadIdx.x == 0) {
+      const int k = st->k;
+      const double rel = sqrt(rr) / st->bnorm;
+      st->residuals[k + 1] = rel;
+      st->k = k + 1;
+      if (rel <= st->tol) {
+        st->status = ST_OK;
+        st->done = 1;
+      } else if (k + 1 >= st->maxit) {
+        st->status = ST_NOT_CONVERGED;
+        st->done = 1;
+      }
+    }
+  }
+}
+
+// p = z (first) or p = z + beta p (solvers.cpp:42, :64); block 0 also sets
+// the graph's WHILE condition (handle != 0) to "not done".
+template <bool FIRST>
+__global__ void __launch_bounds__(kCta) k_pcg_p(int32_t n, const double* __restrict__ z, double* p,
+                                                PcgState* st, cudaGraphConditionalHandle cond) {
+  const bool done = pcg_done(st);
+  if (cond != 0 && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, done ? 0u : 1u);
+  if (done) return;
+  const int i = blockIdx.x * kCta + threadIdx.x;
+  if (i >= n) return;
+  if (FIRST)
+    p[i] = z[i];
+  else
+    p[i] = z[i] + st->beta * p[i];
+}
+
+}  // namespace igk

@@ -144,135 +144,122 @@ ElemData element2(const Space& s, int e, const ProblemConfig& prob, const QuadCo
 }
 
 // ------------------------------------------------------------------ 3D ----
+// Stable point evaluation: 1D local functions of an extraction class are
+// non-negative combinations of Bernstein polynomials (span_extraction), so
+// values/derivatives at a point carry no cancellation, and every diagonal
+// contribution w*|grad phi|^2 is >= 0 -- essential for slivers whose
+// diagonal is 1e-30 of the interior one.
 
-struct Moments {
-  double m[kMaxM][kMaxM][kMaxM];
-  void clear() { std::memset(m, 0, sizeof(m)); }
-};
-
-// Monomial coefficients of the local 1D functions of one extraction class:
-// f_i(u) = sum_k mono[i][k] u^k and f_i'(u) = sum_k dmono[i][k] u^k.
-struct Mono1D {
-  double mono[kMaxQ][kMaxQ];
-  double dmono[kMaxQ][kMaxQ];
-};
-
-Mono1D monomials(const Mat& Ext, int p) {
-  // Bernstein b_k(u) = C(p,k) u^k (1-u)^(p-k) in monomials.
-  double bm[kMaxQ][kMaxQ] = {{0}};
-  auto binom = [](int n, int k) {
-    double r = 1;
-    for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
-    return r;
-  };
-  for (int k = 0; k <= p; ++k)
-    for (int m = 0; m <= p - k; ++m)
-      bm[k][k + m] += binom(p, k) * binom(p - k, m) * ((m & 1) ? -1.0 : 1.0);
-  Mono1D r{};
+inline void eval1d(const Mat& E, int p, double u, double* v, double* d) {
+  double b[kMaxQ], db[kMaxQ];
+  spline::bernstein(p, u, b, db);
   for (int i = 0; i <= p; ++i) {
-    for (int t = 0; t <= p; ++t) {
-      double c = 0;
-      for (int k = 0; k <= p; ++k) c += Ext(i, k) * bm[k][t];
-      r.mono[i][t] = c;
+    double a = 0.0, c = 0.0;
+    for (int k = 0; k <= p; ++k) {
+      a += E(i, k) * b[k];
+      c += E(i, k) * db[k];
     }
-    for (int t = 0; t < p; ++t) r.dmono[i][t] = (t + 1) * r.mono[i][t + 1];
-    r.dmono[i][p] = 0.0;
+    v[i] = a;
+    d[i] = c;
   }
-  return r;
 }
 
-// Product polynomial coefficients c[t] of f*g (degree <= 2p).
-inline void polymul(const double* f, const double* g, int p, double* c) {
-  for (int t = 0; t <= 2 * p; ++t) c[t] = 0.0;
-  for (int a = 0; a <= p; ++a)
-    for (int b = 0; b <= p; ++b) c[a + b] += f[a] * g[b];
+struct Elem3 {
+  const Mat* E[3];
+  int p;
+  double h[3];
+  double beta, f;
+  double* K;  // nl x nl row-major (upper triangle accumulated, mirrored at the end)
+  double* F;
+  double vol;  // reference-units volume integrated (fraction of the cell)
+};
+
+// Volume point u (reference coords), reference weight w.
+void add_vol_point(Elem3& e, const double* u, double w) {
+  const int p = e.p, q = p + 1, nl = q * q * q;
+  double v[3][kMaxQ], d[3][kMaxQ];
+  for (int a = 0; a < 3; ++a) eval1d(*e.E[a], p, u[a], v[a], d[a]);
+  const double jac = e.h[0] * e.h[1] * e.h[2];
+  const double wp = w * jac;
+  double phi[kMaxQ * kMaxQ * kMaxQ], gx[kMaxQ * kMaxQ * kMaxQ], gy[kMaxQ * kMaxQ * kMaxQ],
+      gz[kMaxQ * kMaxQ * kMaxQ];
+  for (int ic = 0, i = 0; ic < q; ++ic)
+    for (int ib = 0; ib < q; ++ib)
+      for (int ia = 0; ia < q; ++ia, ++i) {
+        phi[i] = v[0][ia] * v[1][ib] * v[2][ic];
+        gx[i] = d[0][ia] * v[1][ib] * v[2][ic] / e.h[0];
+        gy[i] = v[0][ia] * d[1][ib] * v[2][ic] / e.h[1];
+        gz[i] = v[0][ia] * v[1][ib] * d[2][ic] / e.h[2];
+      }
+  for (int i = 0; i < nl; ++i) {
+    double* Ki = e.K + static_cast<size_t>(i) * nl;
+    const double a = wp * gx[i], b = wp * gy[i], c = wp * gz[i];
+    for (int j = i; j < nl; ++j) Ki[j] += a * gx[j] + b * gy[j] + c * gz[j];
+    if (e.f != 0.0) e.F[i] += wp * e.f * phi[i];
+  }
+  e.vol += w;
 }
 
-// Ke/Fe from volume moments M (reference coords), surface moments S.
-void element_from_moments(const Mono1D* mx, const Mono1D* my, const Mono1D* mz, int p,
-                          const Moments& M, const Moments* S, const double h[3], double beta,
-                          double f, ElemData& d) {
-  const int q = p + 1, nl = q * q * q, m = 2 * p + 1;
-  d.K.assign(static_cast<size_t>(nl) * nl, 0.0);
-  d.F.assign(nl, 0.0);
-  const double jac = h[0] * h[1] * h[2];
-  const double cg[3] = {jac / (h[0] * h[0]), jac / (h[1] * h[1]), jac / (h[2] * h[2])};
-  const double cs = beta * h[0] * h[0];  // cubic cells: surface measure scales h^2
-  // 1D product tables: pv[a][b][t] (value*value), pd[a][b][t] (der*der).
-  double pvx[kMaxQ][kMaxQ][kMaxM], pdx[kMaxQ][kMaxQ][kMaxM];
-  double pvy[kMaxQ][kMaxQ][kMaxM], pdy[kMaxQ][kMaxQ][kMaxM];
-  double pvz[kMaxQ][kMaxQ][kMaxM], pdz[kMaxQ][kMaxQ][kMaxM];
-  for (int a = 0; a < q; ++a)
-    for (int b = 0; b < q; ++b) {
-      polymul(mx->mono[a], mx->mono[b], p, pvx[a][b]);
-      polymul(mx->dmono[a], mx->dmono[b], p, pdx[a][b]);
-      polymul(my->mono[a], my->mono[b], p, pvy[a][b]);
-      polymul(my->dmono[a], my->dmono[b], p, pdy[a][b]);
-      polymul(mz->mono[a], mz->mono[b], p, pvz[a][b]);
-      polymul(mz->dmono[a], mz->dmono[b], p, pdz[a][b]);
+// Interface point (reference coords, reference-area weight w): penalty term.
+void add_surf_point(Elem3& e, const double* u, double w) {
+  const int p = e.p, q = p + 1, nl = q * q * q;
+  double v[3][kMaxQ], d[3][kMaxQ];
+  for (int a = 0; a < 3; ++a) eval1d(*e.E[a], p, u[a], v[a], d[a]);
+  const double wb = w * e.h[0] * e.h[0] * e.beta;  // cubic cells: dS = h^2 dS_ref
+  double phi[kMaxQ * kMaxQ * kMaxQ];
+  for (int ic = 0, i = 0; ic < q; ++ic)
+    for (int ib = 0; ib < q; ++ib)
+      for (int ia = 0; ia < q; ++ia, ++i) phi[i] = v[0][ia] * v[1][ib] * v[2][ic];
+  for (int i = 0; i < nl; ++i) {
+    double* Ki = e.K + static_cast<size_t>(i) * nl;
+    const double a = wb * phi[i];
+    for (int j = i; j < nl; ++j) Ki[j] += a * phi[j];
+  }
+}
+
+// Axis box [a, b] (reference coords): exact tensor integration with (p+1)-point
+// Gauss per axis (the 1D integrands have degree <= 2p).
+void add_box(Elem3& e, const double* a, const double* b) {
+  const int p = e.p, q = p + 1, nl = q * q * q;
+  std::vector<double> gn, gw;
+  gauss_legendre(q, gn, gw);
+  double Ivv[3][kMaxQ][kMaxQ] = {}, Idd[3][kMaxQ][kMaxQ] = {}, Iv[3][kMaxQ] = {};
+  for (int ax = 0; ax < 3; ++ax) {
+    const double L = b[ax] - a[ax];
+    if (!(L > 0.0)) return;
+    for (int g = 0; g < q; ++g) {
+      const double u = a[ax] + 0.5 * (gn[g] + 1.0) * L, w = 0.5 * gw[g] * L;
+      double v[kMaxQ], d[kMaxQ];
+      eval1d(*e.E[ax], p, u, v, d);
+      for (int i = 0; i < q; ++i) {
+        Iv[ax][i] += w * v[i];
+        for (int j = 0; j < q; ++j) {
+          Ivv[ax][i][j] += w * v[i] * v[j];
+          Idd[ax][i][j] += w * d[i] * d[j];
+        }
+      }
     }
+  }
+  const double jac = e.h[0] * e.h[1] * e.h[2];
+  const double cx = jac / (e.h[0] * e.h[0]), cy = jac / (e.h[1] * e.h[1]), cz = jac / (e.h[2] * e.h[2]);
   for (int i = 0; i < nl; ++i) {
     const int ia = i % q, ib = (i / q) % q, ic = i / (q * q);
+    double* Ki = e.K + static_cast<size_t>(i) * nl;
     for (int j = i; j < nl; ++j) {
       const int ja = j % q, jb = (j / q) % q, jc = j / (q * q);
-      double kx = 0, ky = 0, kz = 0, ks = 0;
-      for (int al = 0; al < m; ++al)
-        for (int be = 0; be < m; ++be)
-          for (int ga = 0; ga < m; ++ga) {
-            const double mm = M.m[al][be][ga];
-            kx += pdx[ia][ja][al] * pvy[ib][jb][be] * pvz[ic][jc][ga] * mm;
-            ky += pvx[ia][ja][al] * pdy[ib][jb][be] * pvz[ic][jc][ga] * mm;
-            kz += pvx[ia][ja][al] * pvy[ib][jb][be] * pdz[ic][jc][ga] * mm;
-            if (S) ks += pvx[ia][ja][al] * pvy[ib][jb][be] * pvz[ic][jc][ga] * S->m[al][be][ga];
-          }
-      const double v = cg[0] * kx + cg[1] * ky + cg[2] * kz + cs * ks;
-      d.K[static_cast<size_t>(i) * nl + j] = v;
-      d.K[static_cast<size_t>(j) * nl + i] = v;
+      Ki[j] += cx * Idd[0][ia][ja] * Ivv[1][ib][jb] * Ivv[2][ic][jc] +
+               cy * Ivv[0][ia][ja] * Idd[1][ib][jb] * Ivv[2][ic][jc] +
+               cz * Ivv[0][ia][ja] * Ivv[1][ib][jb] * Idd[2][ic][jc];
     }
-    if (f != 0.0) {
-      double fi = 0;
-      for (int al = 0; al <= p; ++al)
-        for (int be = 0; be <= p; ++be)
-          for (int ga = 0; ga <= p; ++ga)
-            fi += mx->mono[ia][al] * my->mono[ib][be] * mz->mono[ic][ga] * M.m[al][be][ga];
-      d.F[i] = f * jac * fi;
-    }
+    if (e.f != 0.0) e.F[i] += e.f * jac * Iv[0][ia] * Iv[1][ib] * Iv[2][ic];
   }
+  e.vol += (b[0] - a[0]) * (b[1] - a[1]) * (b[2] - a[2]);
 }
 
-// Exact moments of the reference box [u0,u1]x[v0,v1]x[w0,w1].
-void add_box_moments(const double* a, const double* b, int m, Moments& M) {
-  double px[kMaxM], py[kMaxM], pz[kMaxM];
-  auto oned = [&](double lo, double hi, double* o) {
-    double pl = lo, ph = hi;
-    for (int k = 0; k < m; ++k) {
-      o[k] = (ph - pl) / (k + 1);
-      pl *= lo;
-      ph *= hi;
-    }
-  };
-  oned(a[0], b[0], px);
-  oned(a[1], b[1], py);
-  oned(a[2], b[2], pz);
-  for (int i = 0; i < m; ++i)
-    for (int j = 0; j < m; ++j)
-      for (int k = 0; k < m; ++k) M.m[i][j][k] += px[i] * py[j] * pz[k];
-}
-
-inline void add_point(const double* u, double w, int m, Moments& M) {
-  double px[kMaxM], py[kMaxM], pz[kMaxM];
-  px[0] = py[0] = 1.0;
-  pz[0] = w;
-  for (int k = 1; k < m; ++k) {
-    px[k] = px[k - 1] * u[0];
-    py[k] = py[k - 1] * u[1];
-    pz[k] = pz[k - 1] * u[2];
-  }
-  for (int i = 0; i < m; ++i)
-    for (int j = 0; j < m; ++j) {
-      const double pij = px[i] * py[j];
-      for (int k = 0; k < m; ++k) M.m[i][j][k] += pij * pz[k];
-    }
+void finish3(Elem3& e) {
+  const int q = e.p + 1, nl = q * q * q;
+  for (int i = 0; i < nl; ++i)
+    for (int j = 0; j < i; ++j) e.K[static_cast<size_t>(i) * nl + j] = e.K[static_cast<size_t>(j) * nl + i];
 }
 
 struct Rule1 {
@@ -291,7 +278,7 @@ Rule1 gauss01(int n) {
 
 // Collapsed (Duffy) rule on tetrahedron v0..v3 (reference coords):
 // x = v0 + a[(v1-v0) + b((v2-v1) + c(v3-v2))], |J| = 6 V a^2 b.
-void tet_moments(const double v[4][3], const Rule1& g, int m, Moments& M) {
+void tet_points(Elem3& e, const double v[4][3], const Rule1& g) {
   double e1[3], e2[3], e3[3];
   for (int k = 0; k < 3; ++k) {
     e1[k] = v[1][k] - v[0][k];
@@ -309,12 +296,12 @@ void tet_moments(const double v[4][3], const Rule1& g, int m, Moments& M) {
         const double a = g.x[ia], b = g.x[ib], c = g.x[ic];
         double u[3];
         for (int k = 0; k < 3; ++k) u[k] = v[0][k] + a * (e1[k] + b * (e2[k] + c * e3[k]));
-        add_point(u, vol6 * a * a * b * g.w[ia] * g.w[ib] * g.w[ic], m, M);
+        add_vol_point(e, u, vol6 * a * a * b * g.w[ia] * g.w[ib] * g.w[ic]);
       }
 }
 
-// Triangle v0..v2 (reference coords; surface measure in reference units).
-void tri_moments(const double v[3][3], const Rule1& g, int m, Moments& S) {
+// Triangle v0..v2 (reference coords, area in reference units).
+void tri_points(Elem3& e, const double v[3][3], const Rule1& g) {
   double e1[3], e2[3];
   for (int k = 0; k < 3; ++k) {
     e1[k] = v[1][k] - v[0][k];
@@ -330,30 +317,32 @@ void tri_moments(const double v[3][3], const Rule1& g, int m, Moments& S) {
       const double a = g.x[ia], b = g.x[ib];
       double u[3];
       for (int k = 0; k < 3; ++k) u[k] = v[0][k] + a * (e1[k] + b * e2[k]);
-      add_point(u, area2 * a * g.w[ia] * g.w[ib], m, S);
+      add_surf_point(e, u, area2 * a * g.w[ia] * g.w[ib]);
     }
 }
 
 struct Cut3Ctx {
   const LevelSet* ls;
   const double* elo;  // element box lo (physical)
-  double h[3];
-  int m;
   QuadConfig qc;
-  Rule1 g;
-  Moments* M;
-  Moments* S;
-  double volume;  // reference-units volume accumulated
+  Rule1 gt, gs;  // tetrahedron / triangle 1D factors
+  Elem3* e;
 };
 
 void to_ref(const Cut3Ctx& c, const double* x, double* u) {
-  for (int k = 0; k < 3; ++k) u[k] = (x[k] - c.elo[k]) / c.h[k];
+  for (int k = 0; k < 3; ++k) u[k] = (x[k] - c.elo[k]) / c.e->h[k];
 }
 
-// Clip tetrahedron (physical vertices x, values f) to psi >= 0.
+// Clip tetrahedron (physical vertices x, values f) to psi >= 0; interface
+// facets are the clip planes through the (bisection) edge roots.
 void clip_tet(Cut3Ctx& c, const double x[4][3], const double f[4]) {
   int in[4], out[4], ni = 0, no = 0;
-  for (int k = 0; k < 4; ++k) (f[k] >= 0.0 ? in[ni++] : out[no++]) = k;
+  for (int k = 0; k < 4; ++k) {
+    if (f[k] >= 0.0)
+      in[ni++] = k;
+    else
+      out[no++] = k;
+  }
   if (ni == 0) return;
   auto ref = [&](const double* p, double* u) { to_ref(c, p, u); };
   auto cross = [&](int a, int b, double* u) {
@@ -364,18 +353,18 @@ void clip_tet(Cut3Ctx& c, const double x[4][3], const double f[4]) {
   double T[4][3];
   if (ni == 4) {
     for (int k = 0; k < 4; ++k) ref(x[k], T[k]);
-    tet_moments(T, c.g, c.m, *c.M);
+    tet_points(*c.e, T, c.gt);
     return;
   }
   if (ni == 1) {
     const int a = in[0];
-    double p[3][3];
-    for (int k = 0; k < 3; ++k) cross(a, out[k], p[k]);
+    double P[3][3];
+    for (int k = 0; k < 3; ++k) cross(a, out[k], P[k]);
     ref(x[a], T[0]);
     for (int k = 0; k < 3; ++k)
-      for (int d = 0; d < 3; ++d) T[k + 1][d] = p[k][d];
-    tet_moments(T, c.g, c.m, *c.M);
-    tri_moments(p, c.g, c.m, *c.S);
+      for (int d = 0; d < 3; ++d) T[k + 1][d] = P[k][d];
+    tet_points(*c.e, T, c.gt);
+    tri_points(*c.e, P, c.gs);
     return;
   }
   if (ni == 3) {
@@ -385,19 +374,17 @@ void clip_tet(Cut3Ctx& c, const double x[4][3], const double f[4]) {
       ref(x[in[k]], bot[k]);
       cross(in[k], a, top[k]);
     }
-    // Prism (bot -> top) as three tetrahedra.
-    const double* P[3][4] = {{bot[0], bot[1], bot[2], top[0]},
-                             {bot[1], bot[2], top[0], top[1]},
-                             {bot[2], top[0], top[1], top[2]}};
-    for (auto& t : P) {
+    const double* Pr[3][4] = {{bot[0], bot[1], bot[2], top[0]},
+                              {bot[1], bot[2], top[0], top[1]},
+                              {bot[2], top[0], top[1], top[2]}};
+    for (auto& t : Pr) {
       for (int k = 0; k < 4; ++k)
         for (int d = 0; d < 3; ++d) T[k][d] = t[k][d];
-      tet_moments(T, c.g, c.m, *c.M);
+      tet_points(*c.e, T, c.gt);
     }
-    tri_moments(top, c.g, c.m, *c.S);
+    tri_points(*c.e, top, c.gs);
     return;
   }
-  // ni == 2: wedge between edges (in0 -> out0/out1) and (in1 -> out0/out1).
   const int a = in[0], b = in[1];
   double pa[3], pb[3], xa0[3], xa1[3], xb0[3], xb1[3];
   ref(x[a], pa);
@@ -406,11 +393,11 @@ void clip_tet(Cut3Ctx& c, const double x[4][3], const double f[4]) {
   cross(a, out[1], xa1);
   cross(b, out[0], xb0);
   cross(b, out[1], xb1);
-  const double* P[3][4] = {{pa, xa0, xa1, pb}, {xa0, xa1, pb, xb0}, {xa1, pb, xb0, xb1}};
-  for (auto& t : P) {
+  const double* Pr[3][4] = {{pa, xa0, xa1, pb}, {xa0, xa1, pb, xb0}, {xa1, pb, xb0, xb1}};
+  for (auto& t : Pr) {
     for (int k = 0; k < 4; ++k)
       for (int d = 0; d < 3; ++d) T[k][d] = t[k][d];
-    tet_moments(T, c.g, c.m, *c.M);
+    tet_points(*c.e, T, c.gt);
   }
   double t1[3][3], t2[3][3];
   for (int d = 0; d < 3; ++d) {
@@ -421,12 +408,11 @@ void clip_tet(Cut3Ctx& c, const double x[4][3], const double f[4]) {
     t2[1][d] = xb1[d];
     t2[2][d] = xa1[d];
   }
-  tri_moments(t1, c.g, c.m, *c.S);
-  tri_moments(t2, c.g, c.m, *c.S);
+  tri_points(*c.e, t1, c.gs);
+  tri_points(*c.e, t2, c.gs);
 }
 
-// Kuhn decomposition: 6 tetrahedra sharing the main diagonal 0 -> 7,
-// corner index = x + 2y + 4z.
+// Kuhn decomposition: 6 tetrahedra sharing the diagonal 0 -> 7 (corner = x + 2y + 4z).
 const int kKuhn[6][4] = {{0, 1, 3, 7}, {0, 1, 5, 7}, {0, 2, 3, 7},
                          {0, 2, 6, 7}, {0, 4, 5, 7}, {0, 4, 6, 7}};
 
@@ -448,6 +434,7 @@ void cut_leaf3(Cut3Ctx& c, const double* lo, const double* hi) {
   }
 }
 
+// Octree analogue of recurse_cut (quadrature.cpp:266-290).
 void recurse3(Cut3Ctx& c, const double* lo, const double* hi, int depth) {
   switch (classify_cell(*c.ls, lo, hi, 3, c.qc.classify_depth)) {
     case CellClass::Outside: return;
@@ -455,7 +442,7 @@ void recurse3(Cut3Ctx& c, const double* lo, const double* hi, int depth) {
       double a[3], b[3];
       to_ref(c, lo, a);
       to_ref(c, hi, b);
-      add_box_moments(a, b, c.m, *c.M);
+      add_box(*c.e, a, b);
       return;
     }
     case CellClass::Cut: break;
@@ -477,6 +464,26 @@ void recurse3(Cut3Ctx& c, const double* lo, const double* hi, int depth) {
   }
 }
 
+// Element data for a 3D element: cut (octree + clipped tets) or full box.
+ElemData element3(const Space& s, int cx, int cy, int cz, const double* lo, const double* hi, bool cut,
+                  const QuadConfig& qc, double beta, double f) {
+  const int q = s.p + 1, nl = q * q * q;
+  ElemData d;
+  d.K.assign(static_cast<size_t>(nl) * nl, 0.0);
+  d.F.assign(nl, 0.0);
+  Elem3 e{{&s.ext[0][cx], &s.ext[1][cy], &s.ext[2][cz]}, s.p, {s.grid.h(0), s.grid.h(1), s.grid.h(2)},
+          beta, f, d.K.data(), d.F.data(), 0.0};
+  if (cut) {
+    Cut3Ctx c{&s.ls, lo, qc, gauss01(2), gauss01(3), &e};
+    recurse3(c, lo, hi, qc.depth);
+  } else {
+    const double a[3] = {0, 0, 0}, b[3] = {1, 1, 1};
+    add_box(e, a, b);
+  }
+  finish3(e);
+  d.volume = e.vol;
+  return d;
+}
 }  // namespace
 
 Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& qc, int threads) {
@@ -516,10 +523,6 @@ Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& 
   const int ncx = static_cast<int>(s.ext[0].size()), ncy = static_cast<int>(s.ext[1].size());
   const int ncz = dim == 3 ? static_cast<int>(s.ext[2].size()) : 1;
   std::vector<ElemData> cdata(static_cast<size_t>(ncx) * ncy * ncz);
-  std::vector<Mono1D> mono[3];
-  if (dim == 3)
-    for (int d = 0; d < 3; ++d)
-      for (const Mat& E : s.ext[d]) mono[d].push_back(monomials(E, p));
   const double h3[3] = {g.h(0), g.h(1), dim == 3 ? g.h(2) : 1.0};
   if (dim == 3 && (std::fabs(h3[0] - h3[1]) > 1e-14 * h3[0] || std::fabs(h3[0] - h3[2]) > 1e-14 * h3[0]))
     throw SetupError("assemble: 3D cells must be cubic");
@@ -555,12 +558,7 @@ Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& 
             for (int a = 0; a < nl; ++a) d.F[a] += w * prob.body_force * val[a];
         }
     } else {
-      Moments M;
-      M.clear();
-      const double a0[3] = {0, 0, 0}, a1[3] = {1, 1, 1};
-      add_box_moments(a0, a1, 2 * p + 1, M);
-      element_from_moments(&mono[0][cx], &mono[1][cy], &mono[2][cz], p, M, nullptr, h3, beta,
-                           prob.body_force, d);
+      d = element3(s, cx, cy, cz, nullptr, nullptr, false, qc, beta, prob.body_force);
     }
   }
 
@@ -580,16 +578,9 @@ Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& 
     } else {
       double lo[3], hi[3];
       g.cell_box(s.el_ix[e], s.el_iy[e], s.el_iz[e], lo, hi);
-      Moments M, S;
-      M.clear();
-      S.clear();
-      Cut3Ctx c{&s.ls, lo, {h3[0], h3[1], h3[2]}, 2 * p + 1, qc, gauss01(3), &M, &S, 0.0};
-      recurse3(c, lo, hi, qc.depth);
       const int cx = s.ext_cls[0][s.el_ix[e]], cy = s.ext_cls[1][s.el_iy[e]], cz = s.ext_cls[2][s.el_iz[e]];
-      element_from_moments(&mono[0][cx], &mono[1][cy], &mono[2][cz], p, M, &S, h3, beta,
-                           prob.body_force, sdata[k]);
-      sdata[k].volume = M.m[0][0][0];  // reference units: fraction of the cell
-      eta = std::min(eta, M.m[0][0][0]);
+      sdata[k] = element3(s, cx, cy, cz, lo, hi, true, qc, beta, prob.body_force);
+      eta = std::min(eta, sdata[k].volume);  // reference units: fraction of the cell
     }
   }
   out.eta = eta;
@@ -685,16 +676,21 @@ Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& 
 
   // --- symmetrise: A = 0.5 (A + A^T) (assembly.cpp:177-180) ----------------
   std::vector<double> sym(A.val.size());
-#pragma omp parallel for schedule(dynamic, 512) num_threads(threads)
+  int unsym = 0;
+#pragma omp parallel for schedule(dynamic, 512) num_threads(threads) reduction(+ : unsym)
   for (int i = 0; i < n; ++i)
     for (int32_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
       const int32_t j = A.col[k];
       const int32_t* b = A.col.data() + A.ptr[j];
       const int32_t* e = A.col.data() + A.ptr[j + 1];
       const int32_t* it = std::lower_bound(b, e, i);
-      if (it == e || *it != i) throw SetupError("assemble: unsymmetric pattern");
+      if (it == e || *it != i) {
+        ++unsym;
+        continue;
+      }
       sym[k] = 0.5 * (A.val[k] + A.val[it - A.col.data()]);
     }
+  if (unsym) throw SetupError("assemble: unsymmetric pattern");
   A.val.swap(sym);
   return out;
 }

@@ -1,0 +1,206 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same host-built hierarchy.
+
+The device kernels fix every summation order to the one oracle.c documents,
+so against the oracle in GPU-order mode the results must be BIT-IDENTICAL
+(np.array_equal); against the sequential-reduction oracle they must meet the
+north-star tolerances: iterations +-1, residual history within 1e-9 relative
+over the first 10 iterations, final x within 1e-8 relative L2.
+"""
+import numpy as np
+import pytest
+
+import oracle_ffi as orc
+from conftest import rng_vec
+
+pytestmark = pytest.mark.gpu
+
+RES_TOL = 1e-9   # north star: residual history, first 10 iterations
+X_TOL = 1e-8     # north star: final solution, relative L2
+
+
+@pytest.fixture(scope="module")
+def hier_c1(c1_case):
+    from paper_1903_10977_b200 import MgHierarchy
+    return MgHierarchy(c1_case)
+
+
+@pytest.fixture(scope="module")
+def hier_d3(d3_case):
+    from paper_1903_10977_b200 import MgHierarchy
+    return MgHierarchy(d3_case)
+
+
+@pytest.fixture(scope="module")
+def hier_star(star_case):
+    from paper_1903_10977_b200 import MgHierarchy
+    return MgHierarchy(star_case)
+
+
+CASES = ["hier_c1", "hier_d3", "hier_star"]
+
+
+def _pair(request, name):
+    h = request.getfixturevalue(name)
+    return h, h.case.levels_c()
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_level_spmv_bitwise(request, name):
+    h, lv = _pair(request, name)
+    for l in range(1, h.levels()):
+        A, R = h.level(l)
+        x = rng_vec(7 + l, A.cols())
+        y0 = rng_vec(8 + l, A.rows())
+        assert np.array_equal(h.spmv(l, x, 0), orc.spmv(lv, l, x, 0))
+        assert np.array_equal(h.spmv(l, x, 1, y0), orc.spmv(lv, l, x, 1, y0))
+        assert np.array_equal(h.spmv(l, x, 2), orc.spmv(lv, l, x, 2))
+        xc = rng_vec(9 + l, R.rows())
+        assert np.array_equal(h.spmv(l, xc, 3), orc.spmv(lv, l, xc, 3))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_smoother_bitwise(request, name):
+    h, lv = _pair(request, name)
+    for l in range(1, h.levels()):
+        r = rng_vec(11 + l, h._n[l])
+        assert np.array_equal(h.smoother_apply(l, r), orc.as_apply(lv, l, r))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_coarse_solve_bitwise(request, name):
+    h, lv = _pair(request, name)
+    r = rng_vec(13, h._n[0])
+    x = h.coarse_solve(r)
+    assert np.array_equal(x, orc.coarse_solve(lv, r))
+    assert np.all(np.isfinite(x))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_vcycle_bitwise(request, name):
+    h, lv = _pair(request, name)
+    for l in range(h.levels()):
+        r = rng_vec(17 + l, h._n[l])
+        assert np.array_equal(h.vcycle_at(l, r), orc.vcycle_at(lv, l, r))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_pcg_bitwise_vs_gpu_order_oracle(request, name):
+    from paper_1903_10977_b200 import pcg
+    h, lv = _pair(request, name)
+    b = h.case.b
+    x, rep = pcg(h.A, b, h, tol=1e-8, maxit=1000)
+    st, xo, ro, it, _ = orc.pcg(lv, b, tol=1e-8, maxit=1000, mode=orc.GPU_ORDER)
+    assert st == 0 and rep.converged
+    assert rep.iterations == it
+    assert np.array_equal(np.array(rep.residuals), ro)
+    assert np.array_equal(x, xo)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_pcg_tolerance_vs_sequential_oracle(request, name):
+    from paper_1903_10977_b200 import pcg
+    h, lv = _pair(request, name)
+    b = h.case.b
+    x, rep = pcg(h.A, b, h, tol=1e-8, maxit=1000)
+    st, xo, ro, it, _ = orc.pcg(lv, b, tol=1e-8, maxit=1000, mode=orc.SEQ)
+    assert st == 0
+    assert abs(rep.iterations - it) <= 1
+    k = min(11, len(ro), len(rep.residuals))
+    rg = np.array(rep.residuals[:k])
+    assert np.all(np.abs(rg - ro[:k]) <= RES_TOL * np.abs(ro[:k]))
+    assert np.linalg.norm(x - xo) <= X_TOL * np.linalg.norm(xo)
+    # The report must not flatter the residual (proj/tests/test_solvers.cpp:82).
+    A = h.A.to_scipy()
+    assert np.linalg.norm(b - A @ x) / np.linalg.norm(b) <= 2e-8
+
+
+def test_pcg_rerun_bit_identical(hier_c1):
+    """Determinism contract (proj/tests/test_runner.cpp:175-185)."""
+    from paper_1903_10977_b200 import pcg
+    b = hier_c1.case.b
+    x1, r1 = pcg(hier_c1.A, b, hier_c1, tol=1e-8)
+    x2, r2 = pcg(hier_c1.A, b, hier_c1, tol=1e-8)
+    assert np.array_equal(x1, x2) and r1.residuals == r2.residuals
+
+
+def test_graph_and_host_loop_agree(hier_c1):
+    from paper_1903_10977_b200 import _ffi, pcg
+    b = hier_c1.case.b
+    xg, rg = pcg(hier_c1.A, b, hier_c1, tol=1e-8)
+    _ffi.gpu().ig_set_option(_ffi.IG_OPT_USE_GRAPH, 0)
+    try:
+        xh, rh = pcg(hier_c1.A, b, hier_c1, tol=1e-8)
+    finally:
+        _ffi.gpu().ig_set_option(_ffi.IG_OPT_USE_GRAPH, 1)
+    assert np.array_equal(xg, xh) and rg.residuals == rh.residuals
+
+
+def test_identity_cg_one_step_and_zero_rhs():
+    """proj/tests/test_solvers.cpp:47-67 on the device path."""
+    from paper_1903_10977_b200 import MgHierarchy, pcg
+    n = 40
+    syn = orc.Synthetic(np.eye(n))
+    h = MgHierarchy(syn)
+    b = rng_vec(7, n)
+    x, rep = pcg(h.A, b, h)
+    assert rep.converged and rep.iterations == 1
+    assert len(rep.residuals) == 2 and rep.residuals[0] == 1.0 and rep.residuals[1] <= 1e-14
+    assert np.max(np.abs(x - b)) <= 1e-14
+    xz, repz = pcg(h.A, np.zeros(n), h)
+    assert repz.converged and np.max(np.abs(xz)) == 0.0 and repz.residuals == [0.0]
+
+
+def test_indefinite_breakdown():
+    """proj/tests/test_solvers.cpp:153-173."""
+    from paper_1903_10977_b200 import Breakdown, MgHierarchy, pcg
+    h = MgHierarchy(orc.Synthetic(np.diag([1.0, -1.0])))
+    with pytest.raises(Breakdown) as e:
+        pcg(h.A, np.array([0.0, 1.0]), h)
+    assert len(e.value.report.residuals) >= 1
+    with pytest.raises(ValueError):
+        pcg(h.A, np.zeros(3), h)
+
+
+def test_not_converged_carries_partial_state(hier_star):
+    """proj/tests/test_solvers.cpp:92-107."""
+    from paper_1903_10977_b200 import NotConverged, pcg
+    b = hier_star.case.b
+    with pytest.raises(NotConverged) as e:
+        pcg(hier_star.A, b, hier_star, tol=1e-10, maxit=5)
+    assert e.value.report.iterations == 5
+    assert len(e.value.report.residuals) == 6
+    assert not e.value.report.converged
+    assert e.value.x.shape == b.shape and np.max(np.abs(e.value.x)) > 0.0
+    st, xo, ro, it, _ = orc.pcg(hier_star.case.levels_c(), b, tol=1e-10, maxit=5, mode=orc.GPU_ORDER)
+    assert st == 1 and np.array_equal(e.value.x, xo) and np.array_equal(np.array(e.value.report.residuals), ro)
+
+
+def test_device_entry_points_match_host_api(hier_d3):
+    """ig_pcg_device / ig_vcycle_device on torch-owned device buffers."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1903_10977_b200 import _ffi, pcg
+    lib = _ffi.gpu()
+    h = hier_d3
+    b = h.case.b
+    x_ref, rep = pcg(h.A, b, h, tol=1e-8)
+    db = torch.from_numpy(b).cuda()
+    dx = torch.empty_like(db)
+    torch.cuda.synchronize()
+    assert lib.ig_pcg_device(h.handle, C.c_void_p(db.data_ptr()), 1e-8, 1000, C.c_void_p(dx.data_ptr())) == 0
+    res = np.zeros(1001)
+    it = C.c_int32()
+    assert lib.ig_pcg_result(h.handle, res.ctypes.data_as(C.POINTER(C.c_double)), C.byref(it)) == 0
+    assert it.value == rep.iterations
+    assert np.array_equal(dx.cpu().numpy(), x_ref)
+    r = torch.from_numpy(rng_vec(5, h._n[-1])).cuda()
+    z = torch.empty_like(r)
+    torch.cuda.synchronize()
+    for _ in range(2):  # second call replays the cached graph
+        assert lib.ig_vcycle_device(h.handle, C.c_void_p(r.data_ptr()), C.c_void_p(z.data_ptr())) == 0
+        C.c_void_p(lib.ig_hier_stream(h.handle))
+        torch.cuda.synchronize()
+        assert np.array_equal(z.cpu().numpy(), h.apply(r.cpu().numpy()))
