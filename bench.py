@@ -135,6 +135,9 @@ def main():
     ap.add_argument("--threads", type=int, default=0, help="host setup threads (0 = all)")
     ap.add_argument("--cpu-sample-iters", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch kernels directly instead of the CUDA graph (ncu cannot profile "
+                         "kernel nodes of graphs with conditional nodes)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -155,6 +158,8 @@ def main():
 
     from paper_1903_10977_b200 import MgHierarchy, _ffi
     lib = _ffi.gpu()
+    if args.no_graph:
+        lib.ig_set_option(_ffi.IG_OPT_USE_GRAPH, 0)
 
     case, desc, t_setup = build_workload(args.workload, args.threads)
     t0 = time.perf_counter()

@@ -106,7 +106,7 @@ struct Level {
   DevSell A, R, P;
   AsGroups G{};
   AsGather S{};
-  int32_t n_blocks = 0, n_multi = 0;
+  int32_t n_blocks = 0, n_multi = 0, n_complex = 0;
   int64_t sum_s = 0, sum_s2 = 0, packed_F = 0;
   double* r_in = nullptr;  // input residual buffer (host API; coarse levels: R res)
   double* x = nullptr;
@@ -214,7 +214,8 @@ struct ig_hier {
   }
   void smoother(const Level& l, const double* r, double* x, bool acc, PcgState* s, const double* rdot) {
     if (l.n_multi > 0) {
-      const unsigned g = static_cast<unsigned>((static_cast<int64_t>(l.G.n_groups) * 32 + 127) / 128);
+      const unsigned g =
+          static_cast<unsigned>((static_cast<int64_t>(l.G.n_groups + l.G.n_wblocks) * 32 + 127) / 128);
       k_as_blocks<<<g, 128, 0, stream>>>(l.G, r, l.ybuf, s);
       CK(cudaGetLastError());
     }
@@ -392,13 +393,15 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
   if (nb <= 0 || !B.blk_ptr || !B.blk_dofs || !B.fac_ptr || !B.fac)
     throw Error(IG_INVALID_ARGUMENT, "smoother: empty block layout");
   L.n_blocks = nb;
-  // Multi-DOF blocks: compact ybuf positions, sorted by size for grouping.
+  auto bsize = [&](int32_t b) { return B.blk_ptr[b + 1] - B.blk_ptr[b]; };
+  // Multi-DOF blocks: compact ybuf positions; thread-per-block groups for
+  // s <= 8 and s > 32, warp-per-block for 9 <= s <= 32.
   std::vector<int32_t> ypos(static_cast<size_t>(nb), -1);
-  std::vector<int32_t> multi;
+  std::vector<int32_t> grouped, warped;
   int64_t yl = 0;
   std::vector<double> sval(static_cast<size_t>(nb), 0.0);
   for (int32_t b = 0; b < nb; ++b) {
-    const int32_t s = B.blk_ptr[b + 1] - B.blk_ptr[b];
+    const int32_t s = bsize(b);
     if (s <= 0) throw Error(IG_INVALID_ARGUMENT, "smoother: empty block");
     for (int32_t i = B.blk_ptr[b]; i < B.blk_ptr[b + 1]; ++i)
       if (B.blk_dofs[i] < 0 || B.blk_dofs[i] >= n) throw Error(IG_INVALID_ARGUMENT, "smoother: DOF out of range");
@@ -407,26 +410,26 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
     L.packed_F += static_cast<int64_t>(s) * (s + 1) / 2;
     if (s == 1) {
       sval[b] = B.fac[B.fac_ptr[b]];
-    } else {
-      if (s > 128) throw Error(IG_INVALID_ARGUMENT, "smoother: block larger than 128 DOFs");
-      ypos[b] = static_cast<int32_t>(yl);
-      yl += s;
-      multi.push_back(b);
+      continue;
     }
+    if (s > 128) throw Error(IG_INVALID_ARGUMENT, "smoother: block larger than 128 DOFs");
+    ypos[b] = static_cast<int32_t>(yl);
+    yl += s;
+    if (s >= 9 && s <= 32)
+      warped.push_back(b);
+    else
+      grouped.push_back(b);
   }
   if (yl > INT32_MAX) throw Error(IG_INVALID_ARGUMENT, "smoother: too many block entries");
-  L.n_multi = static_cast<int32_t>(multi.size());
-  std::stable_sort(multi.begin(), multi.end(), [&](int32_t a, int32_t b) {
-    return (B.blk_ptr[a + 1] - B.blk_ptr[a]) > (B.blk_ptr[b + 1] - B.blk_ptr[b]);
-  });
-  const int32_t ng = (L.n_multi + 31) / 32;
-  std::vector<int32_t> gsmax(static_cast<size_t>(std::max(ng, 1)), 0), gsize(static_cast<size_t>(std::max(ng, 1)) * 32, 0),
-      gypos(static_cast<size_t>(std::max(ng, 1)) * 32, 0), gdofs;
-  std::vector<int64_t> gdoff(static_cast<size_t>(std::max(ng, 1)), 0), gfoff(static_cast<size_t>(std::max(ng, 1)), 0);
+  L.n_multi = static_cast<int32_t>(grouped.size() + warped.size());
+  std::stable_sort(grouped.begin(), grouped.end(), [&](int32_t a, int32_t b) { return bsize(a) > bsize(b); });
+  const int32_t ng = static_cast<int32_t>((grouped.size() + 31) / 32);
+  const size_t ng1 = static_cast<size_t>(std::max(ng, 1));
+  std::vector<int32_t> gsmax(ng1, 0), gsize(ng1 * 32, 0), gypos(ng1 * 32, 0), gdofs;
+  std::vector<int64_t> gdoff(ng1, 0), gfoff(ng1, 0);
   std::vector<double> gfac;
   for (int32_t g = 0; g < ng; ++g) {
-    const int32_t b0 = multi[static_cast<size_t>(g) * 32];
-    const int32_t smax = B.blk_ptr[b0 + 1] - B.blk_ptr[b0];
+    const int32_t smax = bsize(grouped[static_cast<size_t>(g) * 32]);
     gsmax[g] = smax;
     gdoff[g] = static_cast<int64_t>(gdofs.size());
     gfoff[g] = static_cast<int64_t>(gfac.size());
@@ -434,10 +437,10 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
     gdofs.resize(gdofs.size() + static_cast<size_t>(smax) * 32, 0);
     gfac.resize(gfac.size() + static_cast<size_t>(np) * 32, 1.0);
     for (int lane = 0; lane < 32; ++lane) {
-      const int64_t idx = static_cast<int64_t>(g) * 32 + lane;
-      if (idx >= L.n_multi) continue;
-      const int32_t b = multi[idx];
-      const int32_t s = B.blk_ptr[b + 1] - B.blk_ptr[b];
+      const size_t idx = static_cast<size_t>(g) * 32 + lane;
+      if (idx >= grouped.size()) continue;
+      const int32_t b = grouped[idx];
+      const int32_t s = bsize(b);
       gsize[idx] = s;
       gypos[idx] = ypos[b];
       for (int i = 0; i < s; ++i) gdofs[gdoff[g] + static_cast<int64_t>(i) * 32 + lane] = B.blk_dofs[B.blk_ptr[b] + i];
@@ -457,8 +460,33 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
   L.G.ypos = h.upload(gypos.data(), gypos.size());
   L.G.dofs = h.upload(gdofs.data(), std::max<size_t>(gdofs.size(), 1));
   L.G.fac = h.upload(gfac.data(), std::max<size_t>(gfac.size(), 1));
+  // Warp blocks: contiguous DOF lists and full column-major factors.
+  {
+    const size_t nw = warped.size();
+    std::vector<int32_t> wsize(std::max<size_t>(nw, 1), 0), wypos(std::max<size_t>(nw, 1), 0), wdofs;
+    std::vector<int64_t> wdoff(std::max<size_t>(nw, 1), 0), wfoff(std::max<size_t>(nw, 1), 0);
+    std::vector<double> wfac;
+    for (size_t k = 0; k < nw; ++k) {
+      const int32_t b = warped[k];
+      const int32_t s = bsize(b);
+      wsize[k] = s;
+      wypos[k] = ypos[b];
+      wdoff[k] = static_cast<int64_t>(wdofs.size());
+      wfoff[k] = static_cast<int64_t>(wfac.size());
+      wdofs.insert(wdofs.end(), B.blk_dofs + B.blk_ptr[b], B.blk_dofs + B.blk_ptr[b + 1]);
+      wfac.insert(wfac.end(), B.fac + B.fac_ptr[b], B.fac + B.fac_ptr[b] + static_cast<int64_t>(s) * s);
+    }
+    L.G.n_wblocks = static_cast<int32_t>(nw);
+    L.G.w_size = h.upload(wsize.data(), wsize.size());
+    L.G.w_ypos = h.upload(wypos.data(), wypos.size());
+    L.G.w_dof_off = h.upload(wdoff.data(), wdoff.size());
+    L.G.w_fac_off = h.upload(wfoff.data(), wfoff.size());
+    L.G.w_dofs = h.upload(wdofs.data(), std::max<size_t>(wdofs.size(), 1));
+    L.G.w_fac = h.upload(wfac.data(), std::max<size_t>(wfac.size(), 1));
+  }
   L.ybuf = h.alloc<double>(static_cast<size_t>(std::max<int64_t>(yl, 1)));
-  // Per-DOF contribution lists in ascending block order.
+  // Per-DOF contribution lists in ascending block order; DOFs whose only
+  // contribution is their own singleton take the head >= 0 fast path.
   std::vector<int32_t> cnt(static_cast<size_t>(n) + 1, 0);
   for (int32_t b = 0; b < nb; ++b)
     for (int32_t i = B.blk_ptr[b]; i < B.blk_ptr[b + 1]; ++i) ++cnt[B.blk_dofs[i] + 1];
@@ -466,17 +494,33 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
   std::vector<int32_t> centry(static_cast<size_t>(cnt[n]));
   std::vector<int32_t> nx(cnt.begin(), cnt.end() - 1);
   for (int32_t b = 0; b < nb; ++b) {
-    const int32_t s = B.blk_ptr[b + 1] - B.blk_ptr[b];
+    const int32_t s = bsize(b);
     for (int32_t i = 0; i < s; ++i) {
       const int32_t d = B.blk_dofs[B.blk_ptr[b] + i];
       centry[nx[d]++] = s == 1 ? -(b + 1) : ypos[b] + i;
     }
   }
+  std::vector<int32_t> head(static_cast<size_t>(n), 0), cptr{0}, cent;
+  std::vector<double> sdiag(static_cast<size_t>(n), 0.0);
+  for (int32_t d = 0; d < n; ++d) {
+    const int32_t q0 = cnt[d], q1 = cnt[d + 1];
+    if (q1 - q0 == 1 && centry[q0] < 0) {
+      head[d] = 0;
+      sdiag[d] = sval[-centry[q0] - 1];
+    } else {
+      head[d] = -static_cast<int32_t>(cptr.size());  // -(c+1), c = cptr.size()-1
+      cent.insert(cent.end(), centry.begin() + q0, centry.begin() + q1);
+      cptr.push_back(static_cast<int32_t>(cent.size()));
+    }
+  }
   L.S.n = n;
   L.S.gamma = src.gamma;
-  L.S.cptr = h.upload(cnt.data(), cnt.size());
-  L.S.centry = h.upload(centry.data(), std::max<size_t>(centry.size(), 1));
+  L.S.head = h.upload(head.data(), head.size());
+  L.S.sdiag = h.upload(sdiag.data(), sdiag.size());
+  L.S.cptr = h.upload(cptr.data(), cptr.size());
+  L.S.centry = h.upload(cent.data(), std::max<size_t>(cent.size(), 1));
   L.S.sval = h.upload(sval.data(), sval.size());
+  L.n_complex = static_cast<int32_t>(cptr.size() - 1);
 }
 
 }  // namespace

@@ -182,11 +182,19 @@ __global__ void __launch_bounds__(kCta) k_prolong(Sell P, const double* __restri
 }
 
 // ------------------------------------------------- additive Schwarz -------
-// Phase 1: multi-DOF blocks (s >= 2), one thread per block.  Blocks are sorted
-// by size (descending) and grouped by 32 (one warp); per group the DOF lists,
-// output positions and packed lower factors are interleaved lane-fastest so
-// every load is coalesced.  Packed lower column-major with the group's
-// s_max as stride: e(i, j) = j*smax - j*(j-1)/2 + (i - j), i >= j.
+// Phase 1: multi-DOF blocks (s >= 2).  Two layouts, one launch:
+//  * "groups": thread-per-block for small blocks (s <= 8) and the rare
+//    s > 32 fallback.  Blocks are sorted by size (descending) and grouped by
+//    32 (one warp); DOF lists, output positions and packed lower factors are
+//    interleaved lane-fastest so every load is coalesced.  Packed lower
+//    column-major with the group's s_max as stride:
+//    e(i, j) = j*smax - j*(j-1)/2 + (i - j), i >= j.
+//  * "warp blocks": warp-per-block for 9 <= s <= 32.  Lane i holds y_i and
+//    row i of L + L^T in registers; each substitution step is one division
+//    by the owning lane, a shuffle broadcast and one FMA-free update per lane,
+//    so the dependent chain is 2s short steps instead of s^2 loads.
+// Both perform exactly the oracle's operation sequence per entry (forward
+// column-oriented; backward y_i = (y_i - sum_{k desc} L(k,i) y_k) / L(i,i)).
 struct AsGroups {
   int32_t n_groups;
   const int32_t* smax;      // per group
@@ -196,6 +204,14 @@ struct AsGroups {
   const int32_t* ypos;      // [group*32 + lane]: ybuf offset of the block
   const int32_t* dofs;
   const double* fac;
+  // warp blocks
+  int32_t n_wblocks;
+  const int32_t* w_size;
+  const int32_t* w_ypos;
+  const int64_t* w_dof_off;
+  const int64_t* w_fac_off;  // full s x s column-major factor
+  const int32_t* w_dofs;
+  const double* w_fac;
 };
 
 __device__ __forceinline__ int packed_idx(int i, int j, int smax) {
@@ -205,31 +221,34 @@ __device__ __forceinline__ int packed_idx(int i, int j, int smax) {
 template <int SM>
 __device__ __forceinline__ void block_solve(const AsGroups& G, int g, int lane, int s, int smax,
                                             const double* __restrict__ r, double* ybuf) {
-  double y[SM];
+  double y[SM], Lp[SM * (SM + 1) / 2];
   const int32_t* dp = G.dofs + G.dof_off[g] + lane;
   const double* fp = G.fac + G.fac_off[g] + lane;
+  // All loads first (independent of the substitution chain).
 #pragma unroll
   for (int i = 0; i < SM; ++i) y[i] = (i < s) ? __ldg(r + dp[i * 32]) : 0.0;
-  // forward: column oriented
+#pragma unroll
+  for (int j = 0; j < SM; ++j)
+#pragma unroll
+    for (int i = j; i < SM; ++i) Lp[packed_idx(i, j, SM)] = (i < s) ? fp[packed_idx(i, j, smax) * 32] : 1.0;
 #pragma unroll
   for (int j = 0; j < SM; ++j) {
     if (j < s) {
-      const double yj = y[j] / fp[packed_idx(j, j, smax) * 32];
+      const double yj = y[j] / Lp[packed_idx(j, j, SM)];
       y[j] = yj;
 #pragma unroll
       for (int i = j + 1; i < SM; ++i)
-        if (i < s) y[i] = y[i] - fp[packed_idx(i, j, smax) * 32] * yj;
+        if (i < s) y[i] = y[i] - Lp[packed_idx(i, j, SM)] * yj;
     }
   }
-  // backward: y_i = (y_i - sum_{k desc} L(k,i) y_k) / L(i,i)
 #pragma unroll
   for (int i = SM - 1; i >= 0; --i) {
     if (i < s) {
       double acc = 0.0;
 #pragma unroll
       for (int k = SM - 1; k > i; --k)
-        if (k < s) acc = acc + fp[packed_idx(k, i, smax) * 32] * y[k];
-      y[i] = (y[i] - acc) / fp[packed_idx(i, i, smax) * 32];
+        if (k < s) acc = acc + Lp[packed_idx(k, i, SM)] * y[k];
+      y[i] = (y[i] - acc) / Lp[packed_idx(i, i, SM)];
     }
   }
   const int pos = G.ypos[g * 32 + lane];
@@ -259,37 +278,73 @@ __device__ __noinline__ void block_solve_any(const AsGroups& G, int g, int lane,
   for (int i = 0; i < s; ++i) ybuf[pos + i] = y[i];
 }
 
+__device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int lane,
+                                                 const double* __restrict__ r, double* ybuf) {
+  const int s = G.w_size[b];
+  const double* f = G.w_fac + G.w_fac_off[b];
+  const int32_t* dp = G.w_dofs + G.w_dof_off[b];
+  double m[32];  // m[t] = L(max(lane,t), min(lane,t)): row `lane` of L + L^T
+#pragma unroll
+  for (int t = 0; t < 32; ++t) {
+    const int hi = lane > t ? lane : t, lo = lane > t ? t : lane;
+    m[t] = (t < s && lane < s) ? __ldg(f + lo * s + hi) : 0.0;
+  }
+  double y = lane < s ? __ldg(r + dp[lane]) : 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    if (j < s) {
+      if (lane == j) y = y / m[j];
+      const double yj = __shfl_sync(0xffffffffu, y, j);
+      if (lane > j) y = y - m[j] * yj;
+    }
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 31; k >= 0; --k) {
+    if (k < s) {
+      if (lane == k) y = (y - acc) / m[k];
+      const double yk = __shfl_sync(0xffffffffu, y, k);
+      if (lane < k) acc = acc + m[k] * yk;
+    }
+  }
+  if (lane < s) ybuf[G.w_ypos[b] + lane] = y;
+}
+
 __global__ void __launch_bounds__(128) k_as_blocks(AsGroups G, const double* __restrict__ r,
                                                    double* ybuf, const PcgState* st) {
   if (pcg_done(st)) return;
-  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (g >= G.n_groups) return;
-  const int s = G.size[g * 32 + lane];
-  const int smax = G.smax[g];  // warp-uniform
-  if (s == 0) return;
-  if (smax <= 4)
-    block_solve<4>(G, g, lane, s, smax, r, ybuf);
-  else if (smax <= 8)
-    block_solve<8>(G, g, lane, s, smax, r, ybuf);
-  else if (smax <= 16)
-    block_solve<16>(G, g, lane, s, smax, r, ybuf);
-  else if (smax <= 32)
-    block_solve<32>(G, g, lane, s, smax, r, ybuf);
-  else
-    block_solve_any(G, g, lane, s, smax, r, ybuf);
+  if (w < G.n_groups) {
+    const int g = w;
+    const int s = G.size[g * 32 + lane];
+    const int smax = G.smax[g];  // warp-uniform
+    if (s == 0) return;
+    if (smax <= 4)
+      block_solve<4>(G, g, lane, s, smax, r, ybuf);
+    else if (smax <= 8)
+      block_solve<8>(G, g, lane, s, smax, r, ybuf);
+    else
+      block_solve_any(G, g, lane, s, smax, r, ybuf);
+  } else if (w - G.n_groups < G.n_wblocks) {
+    warp_block_solve(G, w - G.n_groups, lane, r, ybuf);
+  }
 }
 
 // Phase 2: deterministic segmented reduction per DOF, contributions in
 // ascending block order starting from 0 (smoothers.cpp:176-183), then gamma.
-// Entry code >= 0: ybuf offset (multi-DOF block); code = -(b+1): singleton
-// block b whose only member is this DOF, y = (r_d / l) / l with l = sval[b]
-// (== the LLT solve of a 1x1 block: forward r/l, backward (y - 0)/l).
+// Fast path (head[d] >= 0): the DOF's only contribution is its own singleton
+// block, y = (r_d / l) / l with l = sdiag[d] (== the LLT solve of a 1x1
+// block: forward r/l, backward (y - 0)/l).  Otherwise list c = -head[d]-1:
+// entry code >= 0 is a ybuf offset (multi-DOF block), code = -(b+1) a
+// singleton block b with factor sval[b].
 // ACC: x += gamma*sum (post-smoother) else x = gamma*sum.
 // RED: also reduce rdot_i * x_i (r . z) into the PCG state (finest level).
 struct AsGather {
   int32_t n;
   double gamma;
+  const int32_t* head;
+  const double* sdiag;
   const int32_t* cptr;
   const int32_t* centry;
   const double* sval;
@@ -315,21 +370,30 @@ __global__ void __launch_bounds__(kCta) k_as_gather(AsGather S, const double* __
   const int d = blockIdx.x * kCta + threadIdx.x;
   double prod = 0.0;
   if (d < S.n) {
+    const int h = S.head[d];
+    const double rd = r[d];
+    const double l = S.sdiag[d];
+    const double xo = ACC ? x[d] : 0.0;
     double acc = 0.0;
-    const int q0 = S.cptr[d], q1 = S.cptr[d + 1];
-    for (int q = q0; q < q1; ++q) {
-      const int code = S.centry[q];
-      double v;
-      if (code < 0) {
-        const double l = S.sval[-code - 1];
-        v = (r[d] / l) / l;
-      } else {
-        v = ybuf[code];
+    if (h >= 0) {
+      acc = acc + (rd / l) / l;
+    } else {
+      const int c = -h - 1;
+      const int q0 = S.cptr[c], q1 = S.cptr[c + 1];
+      for (int q = q0; q < q1; ++q) {
+        const int code = S.centry[q];
+        double v;
+        if (code < 0) {
+          const double ls = S.sval[-code - 1];
+          v = (rd / ls) / ls;
+        } else {
+          v = ybuf[code];
+        }
+        acc = acc + v;
       }
-      acc = acc + v;
     }
     const double out = S.gamma * acc;
-    const double xn = ACC ? x[d] + out : out;
+    const double xn = ACC ? xo + out : out;
     x[d] = xn;
     if (RED) prod = rdot[d] * xn;
   }
