@@ -299,7 +299,14 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "k_spmv (finest A p, SELL-32)", "achieved": achieved,
                          "peak": hbm, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic, "algorithmic_bytes_per_launch": int(info.bytes_spmv_finest),
-                         "launch_ms": spmv_ms},
+                         "launch_ms": spmv_ms,
+                         "layout_bytes_per_launch": int(info.bytes_spmv_finest_layout),
+                         "layout_gbs": info.bytes_spmv_finest_layout / (spmv_ms * 1e-3) / 1e9,
+                         "layout_frac": info.bytes_spmv_finest_layout / (spmv_ms * 1e-3) / 1e9 / hbm,
+                         "note": ("achieved counts CSR-minimal bytes (12 B/nnz, SURVEY.md App. C); the "
+                                  "row-dictionary SELL reads only layout_bytes_per_launch from HBM, so "
+                                  "frac > 1 is expected; layout_frac is the bandwidth efficiency")},
+            "vcycle_layout_gbs": info.bytes_vcycle_layout / (vc_ms * 1e-3) / 1e9,
             "cpu_baseline": cpu,
             "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n + 8 * (iters + 1), "ms_per_step": e2e_ms},

@@ -117,6 +117,13 @@ typedef struct {
   int64_t device_bytes;       /* device memory held by the handle */
   int32_t kernels_vcycle;     /* kernel launches per V-cycle */
   int32_t kernels_pcg_iter;   /* kernel launches per PCG iteration */
+  /* Row-dictionary SELL (kernels.cuh): matrix entries whose value / column
+   * is actually read from HBM, per level, and the bytes one finest SpMV must
+   * move with that layout (vs. the CSR-minimal bytes_spmv_finest). */
+  int64_t explicit_vals_A[16];
+  int64_t explicit_cols_A[16];
+  int64_t bytes_spmv_finest_layout;
+  int64_t bytes_vcycle_layout;
 } ig_info;
 
 /* Upload a hierarchy (copied; the host arrays may be freed afterwards).
@@ -164,6 +171,8 @@ const char *ig_last_error(void);
 
 /* Build options (set before ig_hier_create; process-wide). 0 = default. */
 #define IG_OPT_USE_GRAPH 1 /* 1 (default): CUDA-graph PCG loop; 0: host loop */
+#define IG_OPT_ROW_DICT 2  /* 1 (default): row-dictionary SELL; 0: plain SELL */
+#define IG_OPT_SPMV_VARIANT 3 /* SpMV batch/prefetch variant 0..3 (kernels.cuh SpmvVar) */
 int ig_set_option(int32_t option, int64_t value);
 
 #ifdef __cplusplus

@@ -42,7 +42,9 @@ class ig_info(C.Structure):
                 ("sum_s2", i64 * 16), ("sell_slots_A", i64 * 16),
                 ("bytes_vcycle", i64), ("bytes_pcg_iter", i64),
                 ("bytes_spmv_finest", i64), ("device_bytes", i64),
-                ("kernels_vcycle", i32), ("kernels_pcg_iter", i32)]
+                ("kernels_vcycle", i32), ("kernels_pcg_iter", i32),
+                ("explicit_vals_A", i64 * 16), ("explicit_cols_A", i64 * 16),
+                ("bytes_spmv_finest_layout", i64), ("bytes_vcycle_layout", i64)]
 
 
 class igh_config(C.Structure):
@@ -65,6 +67,8 @@ class igh_info(C.Structure):
 IG_OK, IG_NOT_CONVERGED, IG_BREAKDOWN, IG_INVALID_ARGUMENT, IG_CUDA_ERROR, IG_UNSUPPORTED = range(6)
 IG_SMOOTHER_JACOBI, IG_SMOOTHER_GAUSS_SEIDEL, IG_SMOOTHER_ADDITIVE_SCHWARZ, IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ = range(4)
 IG_OPT_USE_GRAPH = 1
+IG_OPT_ROW_DICT = 2
+IG_OPT_SPMV_VARIANT = 3
 
 _host = None
 _gpu = None

@@ -44,14 +44,58 @@ struct Error : std::runtime_error {
 
 inline unsigned grid_of(int64_t n) { return static_cast<unsigned>((n + kCta - 1) / kCta); }
 
-// Host image of a SELL-32 matrix.
+// Host image of a SELL-32 matrix with its row dictionary (kernels.cuh: Sell).
 struct HostSell {
   int32_t nr = 0, nc = 0;
   std::vector<int64_t> slice_ptr;
-  std::vector<int32_t> rowlen;
+  std::vector<int32_t> rowinfo;
   std::vector<double> val;
   std::vector<int32_t> col;
+  int32_t dict_w = 1;
+  std::vector<double> dval;
+  std::vector<int32_t> doff;
+  int64_t explicit_vals = 0;  // nnz whose value is read from HBM
+  int64_t explicit_cols = 0;  // nnz whose column is read from HBM
 };
+
+int g_use_dict = 1;
+int g_spmv_variant = 3;  // profiles/spmv_variants.py: best full-PCG time on C4
+constexpr int kDictEntries = 8;
+
+uint64_t fnv(const void* p, size_t bytes, uint64_t h = 1469598103934665603ULL) {
+  const unsigned char* c = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < bytes; ++i) h = (h ^ c[i]) * 1099511628211ULL;
+  return h;
+}
+
+// Up to kDictEntries most frequent bit-exact row patterns (count >= min_count).
+template <typename KeyFn, typename EqFn>
+std::vector<int32_t> top_patterns(int32_t nr, const std::vector<uint8_t>& eligible, KeyFn key, EqFn eq,
+                                  int64_t min_count) {
+  std::vector<std::pair<uint64_t, int32_t>> keys;  // (hash, row)
+  keys.reserve(static_cast<size_t>(nr));
+  for (int32_t i = 0; i < nr; ++i)
+    if (eligible[i]) keys.push_back({key(i), i});
+  std::sort(keys.begin(), keys.end());
+  std::vector<std::pair<int64_t, int32_t>> groups;  // (count, representative row)
+  for (size_t a = 0; a < keys.size();) {
+    size_t b = a;
+    while (b < keys.size() && keys[b].first == keys[a].first) ++b;
+    int64_t c = 0;
+    for (size_t k = a; k < b; ++k) c += eq(keys[k].second, keys[a].second) ? 1 : 0;
+    groups.push_back({c, keys[a].second});
+    a = b;
+  }
+  std::sort(groups.begin(), groups.end(), [](const auto& x, const auto& y) {
+    return x.first != y.first ? x.first > y.first : x.second < y.second;
+  });
+  std::vector<int32_t> reps;
+  for (const auto& g : groups) {
+    if (static_cast<int>(reps.size()) >= kDictEntries || g.first < min_count) break;
+    reps.push_back(g.second);
+  }
+  return reps;
+}
 
 HostSell to_sell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, const double* val) {
   HostSell s;
@@ -59,11 +103,13 @@ HostSell to_sell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col,
   s.nc = nc;
   const int32_t nslice = (nr + kSell - 1) / kSell;
   s.slice_ptr.assign(static_cast<size_t>(nslice) + 1, 0);
-  s.rowlen.assign(static_cast<size_t>(std::max(nr, 1)), 0);
-  for (int32_t i = 0; i < nr; ++i) s.rowlen[i] = ptr[i + 1] - ptr[i];
+  s.rowinfo.assign(static_cast<size_t>(std::max(nr, 1)), 0);
+  auto len = [&](int32_t i) { return ptr[i + 1] - ptr[i]; };
+  for (int32_t i = 0; i < nr; ++i)
+    if (len(i) > 0xffff) throw Error(IG_UNSUPPORTED, "SELL: row longer than 65535 entries");
   for (int32_t sl = 0; sl < nslice; ++sl) {
     int32_t w = 0;
-    for (int32_t i = sl * kSell; i < std::min(nr, (sl + 1) * kSell); ++i) w = std::max(w, s.rowlen[i]);
+    for (int32_t i = sl * kSell; i < std::min(nr, (sl + 1) * kSell); ++i) w = std::max(w, len(i));
     s.slice_ptr[sl + 1] = s.slice_ptr[sl] + static_cast<int64_t>(w) * kSell;
   }
   const int64_t slots = s.slice_ptr[nslice];
@@ -71,10 +117,71 @@ HostSell to_sell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col,
   s.col.assign(static_cast<size_t>(std::max<int64_t>(slots, 1)), 0);
   for (int32_t i = 0; i < nr; ++i) {
     const int64_t base = s.slice_ptr[i / kSell] + (i % kSell);
-    for (int32_t k = 0; k < s.rowlen[i]; ++k) {
+    for (int32_t k = 0; k < len(i); ++k) {
       s.val[base + static_cast<int64_t>(k) * kSell] = val[ptr[i] + k];
       s.col[base + static_cast<int64_t>(k) * kSell] = col[ptr[i] + k];
     }
+  }
+  // Row dictionary: value sequences, then column-offset patterns among them.
+  std::vector<int32_t> vd(static_cast<size_t>(std::max(nr, 1)), 0), od(static_cast<size_t>(std::max(nr, 1)), 0);
+  std::vector<int32_t> vreps, oreps;
+  if (g_use_dict && nr >= 256) {
+    const int64_t min_count = std::max<int64_t>(64, nr / 200);
+    std::vector<uint8_t> all(static_cast<size_t>(nr), 1);
+    auto vkey = [&](int32_t i) {
+      const uint64_t l = static_cast<uint64_t>(len(i));
+      return fnv(val + ptr[i], sizeof(double) * static_cast<size_t>(len(i)), fnv(&l, sizeof(l)));
+    };
+    auto veq = [&](int32_t a, int32_t b) {
+      return len(a) == len(b) && std::memcmp(val + ptr[a], val + ptr[b], sizeof(double) * len(a)) == 0;
+    };
+    vreps = top_patterns(nr, all, vkey, veq, min_count);
+    for (int32_t i = 0; i < nr; ++i)
+      for (size_t e = 0; e < vreps.size(); ++e)
+        if (veq(i, vreps[e])) {
+          vd[i] = static_cast<int32_t>(e) + 1;
+          break;
+        }
+    std::vector<uint8_t> has_v(static_cast<size_t>(nr), 0);
+    for (int32_t i = 0; i < nr; ++i) has_v[i] = vd[i] > 0;
+    auto off_eq = [&](int32_t a, int32_t b) {
+      if (len(a) != len(b)) return false;
+      for (int32_t k = 0; k < len(a); ++k)
+        if (col[ptr[a] + k] - a != col[ptr[b] + k] - b) return false;
+      return true;
+    };
+    auto okey = [&](int32_t i) {
+      uint64_t h = fnv(&vd[i], sizeof(int32_t));
+      for (int32_t k = 0; k < len(i); ++k) {
+        const int32_t o = col[ptr[i] + k] - i;
+        h = fnv(&o, sizeof(o), h);
+      }
+      return h;
+    };
+    auto oeq = [&](int32_t a, int32_t b) { return vd[a] == vd[b] && off_eq(a, b); };
+    oreps = top_patterns(nr, has_v, okey, oeq, min_count);
+    for (int32_t i = 0; i < nr; ++i) {
+      if (!has_v[i]) continue;
+      for (size_t e = 0; e < oreps.size(); ++e)
+        if (off_eq(i, oreps[e])) {
+          od[i] = static_cast<int32_t>(e) + 1;
+          break;
+        }
+    }
+  }
+  int32_t W = 1;
+  for (int32_t r : vreps) W = std::max(W, len(r));
+  s.dict_w = W;
+  s.dval.assign(static_cast<size_t>(W) * std::max<size_t>(vreps.size(), 1), 0.0);
+  s.doff.assign(static_cast<size_t>(W) * std::max<size_t>(oreps.size(), 1), 0);
+  for (size_t e = 0; e < vreps.size(); ++e)
+    for (int32_t k = 0; k < len(vreps[e]); ++k) s.dval[e * W + k] = val[ptr[vreps[e]] + k];
+  for (size_t e = 0; e < oreps.size(); ++e)
+    for (int32_t k = 0; k < len(oreps[e]); ++k) s.doff[e * W + k] = col[ptr[oreps[e]] + k] - oreps[e];
+  for (int32_t i = 0; i < nr; ++i) {
+    s.rowinfo[i] = len(i) | (vd[i] << 16) | (od[i] << 24);
+    if (!vd[i]) s.explicit_vals += len(i);
+    if (!od[i]) s.explicit_cols += len(i);
   }
   return s;
 }
@@ -99,6 +206,7 @@ struct DevSell {
   Sell s{};
   bool stream = false;
   int64_t nnz = 0, slots = 0;
+  int64_t explicit_vals = 0, explicit_cols = 0;
 };
 
 struct Level {
@@ -162,7 +270,7 @@ struct ig_hier {
   template <typename T>
   T* upload(const T* src, size_t count) {
     T* d = alloc<T>(count);
-    if (count) CK(cudaMemcpy(d, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    if (count && src) CK(cudaMemcpy(d, src, count * sizeof(T), cudaMemcpyHostToDevice));
     return d;
   }
   DevSell upload_sell(const HostSell& h, int64_t nnz) {
@@ -170,11 +278,16 @@ struct ig_hier {
     d.s.n_rows = h.nr;
     d.s.n_cols = h.nc;
     d.s.slice_ptr = upload(h.slice_ptr.data(), h.slice_ptr.size());
-    d.s.rowlen = upload(h.rowlen.data(), h.rowlen.size());
+    d.s.rowinfo = upload(h.rowinfo.data(), h.rowinfo.size());
     d.s.val = upload(h.val.data(), h.val.size());
     d.s.col = upload(h.col.data(), h.col.size());
+    d.s.dict_w = h.dict_w;
+    d.s.dval = upload(h.dval.data(), h.dval.size());
+    d.s.doff = upload(h.doff.data(), h.doff.size());
     d.nnz = nnz;
     d.slots = h.slice_ptr.back();
+    d.explicit_vals = h.explicit_vals;
+    d.explicit_cols = h.explicit_cols;
     // Stream (evict-first) matrices far larger than L2; keep small ones cached.
     d.stream = d.slots * 12 > (int64_t(48) << 20);
     return d;
@@ -189,27 +302,43 @@ struct ig_hier {
   }
 
   // ------------------------------------------------------------ launches --
+  template <int M, bool S, bool R>
+  void spmv_var(unsigned g, const DevSell& A, const double* x, double* y, const double* rsrc, PcgState* s) {
+    switch (g_spmv_variant) {
+      case 1: k_spmv<M, S, R, 1><<<g, kCta, 0, stream>>>(A.s, x, y, rsrc, s, partials); break;
+      case 2: k_spmv<M, S, R, 2><<<g, kCta, 0, stream>>>(A.s, x, y, rsrc, s, partials); break;
+      case 3: k_spmv<M, S, R, 3><<<g, kCta, 0, stream>>>(A.s, x, y, rsrc, s, partials); break;
+      default: k_spmv<M, S, R, 0><<<g, kCta, 0, stream>>>(A.s, x, y, rsrc, s, partials); break;
+    }
+  }
   void spmv(const DevSell& A, int mode, const double* x, double* y, const double* rsrc,
             PcgState* s = nullptr, bool red = false) {
     const unsigned g = grid_of(A.s.n_rows);
     if (g == 0) return;
-#define IG_SPMV(M, S, R) k_spmv<M, S, R><<<g, kCta, 0, stream>>>(A.s, x, y, rsrc, s, partials)
     if (red) {
-      if (A.stream) IG_SPMV(0, true, true); else IG_SPMV(0, false, true);
+      if (A.stream) spmv_var<0, true, true>(g, A, x, y, rsrc, s); else spmv_var<0, false, true>(g, A, x, y, rsrc, s);
     } else if (mode == 0) {
-      if (A.stream) IG_SPMV(0, true, false); else IG_SPMV(0, false, false);
+      if (A.stream) spmv_var<0, true, false>(g, A, x, y, rsrc, s); else spmv_var<0, false, false>(g, A, x, y, rsrc, s);
     } else {
-      if (A.stream) IG_SPMV(1, true, false); else IG_SPMV(1, false, false);
+      if (A.stream) spmv_var<1, true, false>(g, A, x, y, rsrc, s); else spmv_var<1, false, false>(g, A, x, y, rsrc, s);
     }
-#undef IG_SPMV
     CK(cudaGetLastError());
+  }
+  template <bool S>
+  void prolong_var(unsigned g, const Level& l, const double* xc, double* x, PcgState* s) {
+    switch (g_spmv_variant) {
+      case 1: k_prolong<S, 1><<<g, kCta, 0, stream>>>(l.P.s, xc, l.cor, x, s); break;
+      case 2: k_prolong<S, 2><<<g, kCta, 0, stream>>>(l.P.s, xc, l.cor, x, s); break;
+      case 3: k_prolong<S, 3><<<g, kCta, 0, stream>>>(l.P.s, xc, l.cor, x, s); break;
+      default: k_prolong<S, 0><<<g, kCta, 0, stream>>>(l.P.s, xc, l.cor, x, s); break;
+    }
   }
   void prolong(const Level& l, const double* xc, double* x, PcgState* s) {
     const unsigned g = grid_of(l.P.s.n_rows);
     if (l.P.stream)
-      k_prolong<true><<<g, kCta, 0, stream>>>(l.P.s, xc, l.cor, x, s);
+      prolong_var<true>(g, l, xc, x, s);
     else
-      k_prolong<false><<<g, kCta, 0, stream>>>(l.P.s, xc, l.cor, x, s);
+      prolong_var<false>(g, l, xc, x, s);
     CK(cudaGetLastError());
   }
   void smoother(const Level& l, const double* r, double* x, bool acc, PcgState* s, const double* rdot) {
@@ -458,8 +587,8 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
   L.G.fac_off = h.upload(gfoff.data(), gfoff.size());
   L.G.size = h.upload(gsize.data(), gsize.size());
   L.G.ypos = h.upload(gypos.data(), gypos.size());
-  L.G.dofs = h.upload(gdofs.data(), std::max<size_t>(gdofs.size(), 1));
-  L.G.fac = h.upload(gfac.data(), std::max<size_t>(gfac.size(), 1));
+  L.G.dofs = h.upload(gdofs.data(), gdofs.size());  // empty -> 1-element placeholder
+  L.G.fac = h.upload(gfac.data(), gfac.size());
   // Warp blocks: contiguous DOF lists and full column-major factors.
   {
     const size_t nw = warped.size();
@@ -481,8 +610,8 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
     L.G.w_ypos = h.upload(wypos.data(), wypos.size());
     L.G.w_dof_off = h.upload(wdoff.data(), wdoff.size());
     L.G.w_fac_off = h.upload(wfoff.data(), wfoff.size());
-    L.G.w_dofs = h.upload(wdofs.data(), std::max<size_t>(wdofs.size(), 1));
-    L.G.w_fac = h.upload(wfac.data(), std::max<size_t>(wfac.size(), 1));
+    L.G.w_dofs = h.upload(wdofs.data(), wdofs.size());
+    L.G.w_fac = h.upload(wfac.data(), wfac.size());
   }
   L.ybuf = h.alloc<double>(static_cast<size_t>(std::max<int64_t>(yl, 1)));
   // Per-DOF contribution lists in ascending block order; DOFs whose only
@@ -518,7 +647,7 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
   L.S.head = h.upload(head.data(), head.size());
   L.S.sdiag = h.upload(sdiag.data(), sdiag.size());
   L.S.cptr = h.upload(cptr.data(), cptr.size());
-  L.S.centry = h.upload(cent.data(), std::max<size_t>(cent.size(), 1));
+  L.S.centry = h.upload(cent.data(), cent.size());
   L.S.sval = h.upload(sval.data(), sval.size());
   L.n_complex = static_cast<int32_t>(cptr.size() - 1);
 }
@@ -532,6 +661,15 @@ const char* ig_last_error(void) { return g_err.c_str(); }
 int ig_set_option(int32_t option, int64_t value) {
   if (option == IG_OPT_USE_GRAPH) {
     g_use_graph = value != 0;
+    return IG_OK;
+  }
+  if (option == IG_OPT_ROW_DICT) {
+    g_use_dict = value != 0;
+    return IG_OK;
+  }
+  if (option == IG_OPT_SPMV_VARIANT) {
+    if (value < 0 || value > 3) return fail(IG_INVALID_ARGUMENT, "ig_set_option: SpMV variant in 0..3");
+    g_spmv_variant = static_cast<int>(value);
     return IG_OK;
   }
   return fail(IG_INVALID_ARGUMENT, "ig_set_option: unknown option");
@@ -633,7 +771,12 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     CK(cudaMemset(h->st, 0, sizeof(PcgState)));
     h->ensure_residuals(1000);
     // Algorithmic bytes and launch counts.
-    int64_t vc = 0;
+    // layout_bytes: the same, counting only the matrix words the row
+    // dictionary leaves in HBM (8 B per explicit value, 4 B per explicit column).
+    auto layout_spmv = [](const DevSell& M, int64_t nr, int64_t nin, bool resid) {
+      return 8 * M.explicit_vals + 4 * M.explicit_cols + 4 * nr + 8 * nin + 8 * nr + (resid ? 8 * nr : 0);
+    };
+    int64_t vc = 0, vcl = 0;
     int kv = 1;  // coarse
     for (int l = 1; l < n_levels; ++l) {
       const Level& L = h->lv[l];
@@ -643,11 +786,20 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       vc += 2 * as + 8 * n;                                              // second application accumulates
       vc += bytes_spmv(nc, n, L.R.nnz, false);                           // R
       vc += 12 * L.R.nnz + 4 * (n + 1) + 8 * nc + 16 * n + 8 * n;        // P + x update
+      vcl += 2 * layout_spmv(L.A, n, n, true) + 2 * as + 8 * n + layout_spmv(L.R, nc, n, false) +
+             layout_spmv(L.P, n, nc, false) + 16 * n;
       kv += 2 * (L.n_multi > 0 ? 2 : 1) + 4;
+      I.explicit_vals_A[l] = L.A.explicit_vals;
+      I.explicit_cols_A[l] = L.A.explicit_cols;
     }
     vc += 8 * static_cast<int64_t>(h->rank) * h->rank + 24 * static_cast<int64_t>(h->n0);
+    vcl += 8 * static_cast<int64_t>(h->rank) * h->rank + 24 * static_cast<int64_t>(h->n0);
     I.bytes_vcycle = vc;
+    I.bytes_vcycle_layout = vcl;
     I.bytes_spmv_finest = bytes_spmv(nf, nf, F.A.nnz, false);
+    I.bytes_spmv_finest_layout = layout_spmv(F.A, nf, nf, false);
+    I.explicit_vals_A[n_levels - 1] = F.A.explicit_vals;
+    I.explicit_cols_A[n_levels - 1] = F.A.explicit_cols;
     I.bytes_pcg_iter = vc + I.bytes_spmv_finest + 80 * static_cast<int64_t>(nf);
     I.kernels_vcycle = kv;
     I.kernels_pcg_iter = kv + 3;

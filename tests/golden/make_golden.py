@@ -33,8 +33,13 @@ def hexes(a):
 
 def solve_record(case, mode, full_x):
     st, x, res, it, sec = orc.pcg(case.levels_c(), case.b, tol=configs.TOL, maxit=configs.MAXIT, mode=mode)
+    import hashlib
+    import math
+    # Machine-independent checksums: sha256 of the raw doubles and an exactly
+    # rounded sum of squares (math.fsum); BLAS dot/sum orders vary by CPU.
     rec = {"status": st, "iterations": it, "residuals": hexes(res),
-           "x_norm2": float(np.dot(x, x)).hex(), "x_sum": float(np.sum(x)).hex(),
+           "x_sha256": hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest(),
+           "x_fsum2": math.fsum((x * x).tolist()).hex(),
            "x_sample_idx": list(range(0, x.shape[0], max(1, x.shape[0] // 64))),
            "cpu_seconds": sec}
     rec["x_sample"] = hexes(x[rec["x_sample_idx"]])
@@ -45,9 +50,11 @@ def solve_record(case, mode, full_x):
 
 def case_record(case):
     i = case.info
+    import hashlib
     return {"n": case.n, "level_dofs": [int(i.n[k]) for k in range(case.n_levels)],
             "nnz": [int(i.nnz[k]) for k in range(case.n_levels)], "coarse_rank": int(i.coarse_rank),
-            "b_sum": float(np.sum(case.b)).hex(), "A_val_sum": float(np.sum(case.A.val)).hex(),
+            "b_sha256": hashlib.sha256(case.b.tobytes()).hexdigest(),
+            "A_val_sha256": hashlib.sha256(np.ascontiguousarray(case.A.val).tobytes()).hexdigest(),
             "eta": float(i.eta).hex()}
 
 
