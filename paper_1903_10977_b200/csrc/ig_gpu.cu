@@ -357,8 +357,14 @@ struct ig_hier {
       k_as_gather<false, false><<<g, kCta, 0, stream>>>(l.S, r, l.ybuf, x, nullptr, s, nullptr);
     CK(cudaGetLastError());
   }
+  void coarse_launch(bool sm, const double* r, double* x, PcgState* s) {
+    if (sm)
+      k_coarse<true><<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, s);
+    else
+      k_coarse<false><<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, s);
+  }
   void coarse(const double* r, double* x, PcgState* s) {
-    k_coarse<<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, coarse_use_smem, s);
+    coarse_launch(coarse_use_smem != 0, r, x, s);
     CK(cudaGetLastError());
   }
   // MgHierarchy::vcycle_at (multigrid.cpp:90-108).  rdot != null: PCG mode on
@@ -739,24 +745,28 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     for (int k = 0; k < h->n0; ++k)
       if (coarse->piv[k] < 1 || coarse->piv[k] > h->n0) throw Error(IG_INVALID_ARGUMENT, "coarse pivot out of range");
     const int64_t rk = h->rank, n0 = h->n0;
-    std::vector<double> packed(static_cast<size_t>(std::max<int64_t>(rk * (rk + 1) / 2, 1)), 0.0);
+    // Packed lower L11, padded to an even count (16-byte TMA bulk copies).
+    const int64_t np = rk * (rk + 1) / 2, np_al = (np + 1) & ~int64_t(1);
+    std::vector<double> packed(static_cast<size_t>(std::max<int64_t>(np_al, 2)), 0.0);
     for (int64_t j = 0; j < rk; ++j)
       for (int64_t i = j; i < rk; ++i) packed[j * rk - (j * (j - 1)) / 2 + (i - j)] = coarse->L[j * n0 + i];
     h->Lp = h->upload(packed.data(), packed.size());
     h->piv = h->upload(coarse->piv, static_cast<size_t>(n0));
-    h->coarse_threads = std::max(32, static_cast<int>((std::max<int64_t>(rk, 1) + 31) / 32 * 32));
-    const size_t smem = sizeof(double) * (static_cast<size_t>((rk + 1) & ~int64_t(1)) + packed.size());
+    h->coarse_threads = static_cast<int>(std::max<int64_t>(32, (rk + 31) / 32 * 32));  // one row per thread
+    // [packed L11][y: rank doubles][flags: rank ints]
+    const size_t smem = sizeof(double) * static_cast<size_t>(np_al + rk + 1) + sizeof(int) * static_cast<size_t>(rk + 1);
     int max_optin = 0;
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
-    if (smem <= static_cast<size_t>(max_optin)) {
+    const int dyn_cap = max_optin - 1024;  // headroom for the kernel's static shared memory
+    if (smem <= static_cast<size_t>(dyn_cap)) {
       h->coarse_use_smem = 1;
       h->coarse_smem = smem;
-      // Process-wide function attribute: raise it to the opt-in maximum so no
-      // handle created later can shrink it below another handle's need.
-      CK(cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+      // Process-wide function attributes: raised to the cap once so no handle
+      // created later can shrink them below another handle's need.
+      CK(cudaFuncSetAttribute(k_coarse<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_cap));
     } else {
       h->coarse_use_smem = 0;
-      h->coarse_smem = sizeof(double) * static_cast<size_t>((rk + 2) & ~int64_t(1));
+      h->coarse_smem = sizeof(double) * static_cast<size_t>(rk + 1) + sizeof(int) * static_cast<size_t>(rk + 1);
     }
     // PCG workspace.
     const int32_t nf = F.n;

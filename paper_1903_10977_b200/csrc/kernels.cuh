@@ -63,8 +63,20 @@ __device__ __forceinline__ bool last_cta_total(double v, double* partials,
   __syncthreads();
   if (!is_last) return false;
   __threadfence();
+  // Lane t: P[t] + P[t+256] + ... in ascending order.  Loads are issued 8 at a
+  // time ahead of the (serial) adds so the tail is one L2 round trip per 8
+  // partials, not per partial.
   double a = 0.0;
-  for (unsigned int k = threadIdx.x; k < gridDim.x; k += kCta) a = a + __ldcg(partials + k);
+  const unsigned int nb = gridDim.x;
+  unsigned int k = threadIdx.x;
+  for (; k + 7 * kCta < nb; k += 8 * kCta) {
+    double q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) q[u] = __ldcg(partials + k + u * kCta);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a = a + q[u];
+  }
+  for (; k < nb; k += kCta) a = a + __ldcg(partials + k);
   __syncthreads();  // sm8 reuse
   const double t = cta_reduce(a, sm8);
   if (threadIdx.x == 0) {
@@ -516,65 +528,115 @@ __global__ void __launch_bounds__(kCta) k_pcg_rz(int32_t n, const double* __rest
 }
 
 // ------------------------------------------------------------ coarse ------
-// Permuted, rank-truncated L11 L11^T solve (multigrid.cpp:77-88), one CTA.
-// Thread t owns row t (rank <= blockDim).  Forward: column oriented, one
-// barrier per column.  Backward: row-dot form with descending k, the
-// accumulation advanced as each y_k is finalised.  L11 is staged packed in
-// shared memory when it fits.
+// Permuted, rank-truncated L11 L11^T solve (multigrid.cpp:77-88).
+// L11 (packed lower, column-major) is staged into shared memory with TMA bulk
+// copies (cp.async.bulk + mbarrier); the substitutions run pipelined across
+// warps (k_coarse below).  Operation order per row is the oracle's: forward
+// column-oriented, backward dot in descending k.
+
+__device__ __forceinline__ void bulk_copy_to_smem(double* dst, const double* src, size_t bytes,
+                                                  unsigned long long* mbar) {
+  const unsigned int m = static_cast<unsigned int>(__cvta_generic_to_shared(mbar));
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(m));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(static_cast<unsigned int>(bytes)));
+    const size_t kChunk = 32768;
+    for (size_t off = 0; off < bytes; off += kChunk) {
+      const unsigned int sz = static_cast<unsigned int>(bytes - off < kChunk ? bytes - off : kChunk);
+      const unsigned int d = static_cast<unsigned int>(__cvta_generic_to_shared(reinterpret_cast<char*>(dst) + off));
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+          "l"(reinterpret_cast<const char*>(src) + off), "r"(sz), "r"(m)
+          : "memory");
+    }
+  }
+  __syncthreads();
+  unsigned int done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(m)
+        : "memory");
+  }
+}
+
+// Pipelined multi-warp substitution: warp w owns rows 32w..32w+31 (one per
+// lane).  Within a block the chain runs by shuffles; across blocks, finished
+// rows are published in shared memory with a per-row flag, and later warps
+// apply those columns while earlier blocks are still solving, so the
+// critical path is ~rank x (mul + sub + div) instead of rank x CTA barriers.
+template <bool SM>
 __global__ void k_coarse(int32_t n, int32_t rank, const double* __restrict__ Lp,
                          const int32_t* __restrict__ piv, const double* __restrict__ r, double* x,
-                         int use_smem, const PcgState* st) {
+                         const PcgState* st) {
   if (pcg_done(st)) return;
-  extern __shared__ double smem[];
-  double* y = smem;                     // rank
-  double* Ls = smem + ((rank + 1) & ~1);  // packed lower, rank*(rank+1)/2
-  const int t = threadIdx.x;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ unsigned long long mbar;
   const int64_t np = static_cast<int64_t>(rank) * (rank + 1) / 2;
-  const double* L = Lp;
-  if (use_smem) {
-    for (int64_t k = t; k < np; k += blockDim.x) Ls[k] = Lp[k];
-    L = Ls;
-  }
-  auto Lij = [&](int i, int j) { return L[static_cast<int64_t>(j) * rank - (static_cast<int64_t>(j) * (j - 1)) / 2 + (i - j)]; };
-  double yi = 0.0;
-  if (t < rank) yi = r[piv[t] - 1];
-  __syncthreads();
-  // forward
-  if (t == 0 && rank > 0) {
-    yi = yi / Lij(0, 0);
-    y[0] = yi;
-  }
-  for (int j = 0; j < rank; ++j) {
+  const int64_t np_al = (np + 1) & ~int64_t(1);  // 16-byte aligned region
+  volatile double* ysh = smem + (SM ? np_al : 0);
+  volatile int* flag = reinterpret_cast<volatile int*>(smem + (SM ? np_al : 0) + rank);
+  for (int k = threadIdx.x; k < rank; k += blockDim.x) flag[k] = 0;
+  if (SM && np > 0)
+    bulk_copy_to_smem(smem, Lp, static_cast<size_t>(np_al) * sizeof(double), &mbar);  // has a barrier
+  else
     __syncthreads();
-    const double yj = y[j];
-    if (t > j && t < rank) {
-      yi = yi - Lij(t, j) * yj;
-      if (t == j + 1) {
-        yi = yi / Lij(t, t);
-        y[t] = yi;
-      }
+  const double* L = SM ? smem : Lp;  // compile-time: LDS from shared, LDG otherwise
+  // Packed column-major lower: L(i, j) = L[off(j) + i], off(j) = j*rank - j(j-1)/2 - j.
+  auto off = [&](int j) { return j * rank - (j * (j - 1)) / 2 - j; };
+  const int i = threadIdx.x;  // one row per thread; warp w owns rows 32w..32w+31
+  const bool own = i < rank;
+  const int b0 = threadIdx.x & ~31;
+  const int bend = min(b0 + 32, rank);
+  const int oi = own ? off(i) : 0;
+  double y = own ? r[piv[i] - 1] : 0.0;
+  // ---- forward: y_j = y_j / L_jj ; y_i -= L_ij y_j (i > j), j ascending ----
+  // Columns of earlier blocks: consumed as their owners publish them.
+  int oj = 0;  // off(j)
+  for (int j = 0; j < b0; ++j) {
+    while (flag[j] == 0) {
     }
+    __threadfence_block();
+    const double yj = ysh[j];
+    if (own) y = y - L[oj + i] * yj;
+    oj += rank - j - 1;
   }
-  __syncthreads();
-  // backward
+  // Own block: the owner of row j divides, publishes, and hands y_j to the
+  // warp by shuffle.
+  for (int j = b0; j < bend; ++j) {
+    if (i == j) {
+      y = y / L[oi + i];
+      ysh[j] = y;
+      __threadfence_block();
+      flag[j] = 1;
+    }
+    const double yj = __shfl_sync(0xffffffffu, y, j - b0);
+    if (own && i > j) y = y - L[oj + i] * yj;
+    oj += rank - j - 1;
+  }
+  // ---- backward: y_i = (y_i - sum_{k desc > i} L_ki y_k) / L_ii ----------
   double acc = 0.0;
-  if (t == rank - 1) {
-    yi = (yi - acc) / Lij(t, t);
-    y[t] = yi;
-  }
-  for (int k = rank - 1; k > 0; --k) {
-    __syncthreads();
-    const double yk = y[k];
-    if (t < k) {
-      acc = acc + Lij(k, t) * yk;
-      if (t == k - 1) {
-        yi = (yi - acc) / Lij(t, t);
-        y[t] = yi;
-      }
+  for (int k = rank - 1; k >= bend; --k) {
+    while (flag[k] != 2) {
     }
+    __threadfence_block();
+    const double yk = ysh[k];
+    if (own) acc = acc + L[oi + k] * yk;
   }
-  __syncthreads();
-  for (int k = t; k < n; k += blockDim.x) x[piv[k] - 1] = (k < rank) ? y[k] : 0.0;
+  for (int k = bend - 1; k >= b0; --k) {
+    if (i == k) {
+      y = (y - acc) / L[oi + i];
+      ysh[k] = y;
+      __threadfence_block();
+      flag[k] = 2;
+    }
+    const double yk = __shfl_sync(0xffffffffu, y, k - b0);
+    if (own && i < k) acc = acc + L[oi + k] * yk;
+  }
+  if (own) x[piv[i] - 1] = y;
+  for (int k = rank + threadIdx.x; k < n; k += blockDim.x) x[piv[k] - 1] = 0.0;
 }
 
 // ---------------------------------------------------------- PCG vectors ---
