@@ -240,6 +240,8 @@ struct ig_hier {
   size_t coarse_smem = 0;
   int coarse_use_smem = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // block solves, forked from / joined into `stream`
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   PcgState* st = nullptr;
   double* partials = nullptr;
   double* residuals = nullptr;
@@ -298,6 +300,9 @@ struct ig_hier {
     for (void* p : allocs) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -341,20 +346,39 @@ struct ig_hier {
       prolong_var<false>(g, l, xc, x, s);
     CK(cudaGetLastError());
   }
+  // Smoother::apply (AS).  Fork: the block solves run on the side stream while
+  // the singleton fast path runs on the main stream; join; then the DOFs with
+  // contribution lists (and, in PCG on the finest level, r . z).
   void smoother(const Level& l, const double* r, double* x, bool acc, PcgState* s, const double* rdot) {
-    if (l.n_multi > 0) {
-      const unsigned g =
+    const bool multi = l.n_multi > 0;
+    if (multi) {
+      CK(cudaEventRecord(ev_fork, stream));
+      CK(cudaStreamWaitEvent(side, ev_fork, 0));
+      const unsigned gb =
           static_cast<unsigned>((static_cast<int64_t>(l.G.n_groups + l.G.n_wblocks) * 32 + 127) / 128);
-      k_as_blocks<<<g, 128, 0, stream>>>(l.G, r, l.ybuf, s);
+      k_as_blocks<<<gb, 128, 0, side>>>(l.G, r, l.ybuf, s);
       CK(cudaGetLastError());
+      CK(cudaEventRecord(ev_join, side));
     }
     const unsigned g = grid_of(l.n);
-    if (rdot)
-      k_as_gather<true, true><<<g, kCta, 0, stream>>>(l.S, r, l.ybuf, x, rdot, s, partials);
-    else if (acc)
-      k_as_gather<true, false><<<g, kCta, 0, stream>>>(l.S, r, l.ybuf, x, nullptr, s, nullptr);
+    if (acc)
+      k_as_simple<true><<<g, kCta, 0, stream>>>(l.S, r, x, s);
     else
-      k_as_gather<false, false><<<g, kCta, 0, stream>>>(l.S, r, l.ybuf, x, nullptr, s, nullptr);
+      k_as_simple<false><<<g, kCta, 0, stream>>>(l.S, r, x, s);
+    CK(cudaGetLastError());
+    if (multi) CK(cudaStreamWaitEvent(stream, ev_join, 0));
+    if (rdot) {
+      if (acc)
+        k_as_finish_red<true><<<g, kCta, 0, stream>>>(l.S, r, l.ybuf, x, rdot, s, partials);
+      else
+        k_as_finish_red<false><<<g, kCta, 0, stream>>>(l.S, r, l.ybuf, x, rdot, s, partials);
+    } else if (l.S.n_complex > 0) {
+      const unsigned gc = grid_of(l.S.n_complex);
+      if (acc)
+        k_as_complex<true><<<gc, kCta, 0, stream>>>(l.S, r, l.ybuf, x, s);
+      else
+        k_as_complex<false><<<gc, kCta, 0, stream>>>(l.S, r, l.ybuf, x, s);
+    }
     CK(cudaGetLastError());
   }
   void coarse_launch(bool sm, const double* r, double* x, PcgState* s) {
@@ -388,31 +412,32 @@ struct ig_hier {
     spmv(c.A, 1, c.cor, c.res, c.res, s);       // res -= A cor
     smoother(c, c.res, x, true, s, rdot);       // x += S(res, Reverse)
   }
-  void pcg_prologue(cudaGraphConditionalHandle cond) {
+  // PCG pieces (solvers.cpp:24-66).  head: init (+ conditions); tail: the
+  // preconditioner application and the direction update, which are skipped
+  // (IF node / host check) once the solve has stopped.
+  void pcg_init(cudaGraphConditionalHandle c_if, cudaGraphConditionalHandle c_loop) {
     const int32_t n = lv[L - 1].n;
-    k_pcg_init<<<grid_of(n), kCta, 0, stream>>>(n, r, st, partials);
-    CK(cudaGetLastError());
-    vcycle(L - 1, r, z, st, r);
-    k_pcg_p<true><<<grid_of(n), kCta, 0, stream>>>(n, z, p, st, cond);
+    k_pcg_init<<<grid_of(n), kCta, 0, stream>>>(n, r, st, partials, c_if, c_loop);
     CK(cudaGetLastError());
   }
-  void pcg_body(cudaGraphConditionalHandle cond) {
+  void pcg_precond(bool first) {
     const int32_t n = lv[L - 1].n;
-    spmv(lv[L - 1].A, 0, p, ap, nullptr, st, true);  // ap = A p; pap; alpha
-    k_pcg_update<<<grid_of(n), kCta, 0, stream>>>(n, p, ap, r, st, partials);
-    CK(cudaGetLastError());
-    vcycle(L - 1, r, z, st, r);                      // z = M r; rz; beta
-    k_pcg_p<false><<<grid_of(n), kCta, 0, stream>>>(n, z, p, st, cond);
+    vcycle(L - 1, r, z, st, r);  // z = M r; r . z; beta
+    if (first)
+      k_pcg_p<true><<<grid_of(n), kCta, 0, stream>>>(n, z, p, st);
+    else
+      k_pcg_p<false><<<grid_of(n), kCta, 0, stream>>>(n, z, p, st);
     CK(cudaGetLastError());
   }
-  void build_pcg_graph() {
-    cudaGraph_t g;
-    CK(cudaGraphCreate(&g, 0));
-    cudaGraphConditionalHandle cond;
-    CK(cudaGraphConditionalHandleCreate(&cond, g, 0, cudaGraphCondAssignDefault));
-    CK(cudaStreamBeginCaptureToGraph(stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    pcg_prologue(cond);
-    // Conditional WHILE node appended after the captured prologue.
+  void pcg_step(cudaGraphConditionalHandle c_if, cudaGraphConditionalHandle c_loop) {
+    const int32_t n = lv[L - 1].n;
+    spmv(lv[L - 1].A, 0, p, ap, nullptr, st, true);  // ap = A p; pap; alpha / breakdown
+    k_pcg_update<<<grid_of(n), kCta, 0, stream>>>(n, p, ap, r, st, partials, c_if, c_loop);
+    CK(cudaGetLastError());
+  }
+  // Append a conditional node of `type` after the current capture frontier
+  // of `stream`; returns its body graph (capture continues after the node).
+  cudaGraph_t add_conditional(cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type) {
     cudaStreamCaptureStatus cs;
     const cudaGraphNode_t* deps = nullptr;
     size_t ndeps = 0;
@@ -420,17 +445,41 @@ struct ig_hier {
     CK(cudaStreamGetCaptureInfo(stream, &cs, nullptr, &cap_graph, &deps, &ndeps));
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = cond;
-    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.handle = h;
+    cp.conditional.type = type;
     cp.conditional.size = 1;
-    cudaGraphNode_t cnode;
-    CK(cudaGraphAddNode(&cnode, cap_graph, deps, ndeps, &cp));
-    CK(cudaStreamUpdateCaptureDependencies(stream, &cnode, 1, cudaStreamSetCaptureDependencies));
-    CK(cudaStreamEndCapture(stream, &g));
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, cap_graph, deps, ndeps, &cp));
+    CK(cudaStreamUpdateCaptureDependencies(stream, &node, 1, cudaStreamSetCaptureDependencies));
+    return cp.conditional.phGraph_out[0];
+  }
+  // Capture `fn` into an (empty) conditional body graph.
+  template <typename F>
+  void capture_into(cudaGraph_t body, F&& fn) {
     CK(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    pcg_body(cond);
+    fn();
     CK(cudaStreamEndCapture(stream, &body));
+  }
+  // init -> IF(go){ precond(first) } -> WHILE(go){ step -> IF(go){ precond } }
+  void build_pcg_graph() {
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle c_if0, c_loop, c_if1;
+    CK(cudaGraphConditionalHandleCreate(&c_if0, g, 0, cudaGraphCondAssignDefault));
+    CK(cudaGraphConditionalHandleCreate(&c_loop, g, 0, cudaGraphCondAssignDefault));
+    CK(cudaGraphConditionalHandleCreate(&c_if1, g, 0, cudaGraphCondAssignDefault));
+    CK(cudaStreamBeginCaptureToGraph(stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    pcg_init(c_if0, c_loop);
+    cudaGraph_t pro = add_conditional(c_if0, cudaGraphCondTypeIf);
+    cudaGraph_t body = add_conditional(c_loop, cudaGraphCondTypeWhile);
+    CK(cudaStreamEndCapture(stream, &g));
+    capture_into(pro, [&] { pcg_precond(true); });
+    cudaGraph_t tail = nullptr;
+    capture_into(body, [&] {
+      pcg_step(c_if1, c_loop);
+      tail = add_conditional(c_if1, cudaGraphCondTypeIf);
+    });
+    capture_into(tail, [&] { pcg_precond(false); });
     CK(cudaGraphInstantiate(&pcg_exec, g, 0));
     CK(cudaGraphDestroy(g));
   }
@@ -455,22 +504,27 @@ struct ig_hier {
     CK(cudaMemcpyAsync(st, &h, sizeof(PcgState), cudaMemcpyHostToDevice, stream));
     if (maxit <= 0) {
       // Zero iterations allowed: still report the initial residual.
-      const int32_t n = lv[L - 1].n;
-      k_pcg_init<<<grid_of(n), kCta, 0, stream>>>(n, r, st, partials);
-      CK(cudaGetLastError());
+      pcg_init(0, 0);
       return;
     }
     if (g_use_graph) {
       if (!pcg_exec) build_pcg_graph();
       CK(cudaGraphLaunch(pcg_exec, stream));
     } else {
-      pcg_prologue(0);
-      for (int32_t it = 0; it < maxit; ++it) {
+      // Host-loop fallback (debug / ncu): same kernels, host checks the flag.
+      auto stopped = [&] {
         int32_t done = 0;
         CK(cudaMemcpyAsync(&done, &st->done, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
-        if (done) break;
-        pcg_body(0);
+        return done != 0;
+      };
+      pcg_init(0, 0);
+      if (stopped()) return;
+      pcg_precond(true);
+      for (int32_t it = 0; it < maxit; ++it) {
+        pcg_step(0, 0);
+        if (stopped()) break;
+        pcg_precond(false);
       }
     }
   }
@@ -635,7 +689,7 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
       centry[nx[d]++] = s == 1 ? -(b + 1) : ypos[b] + i;
     }
   }
-  std::vector<int32_t> head(static_cast<size_t>(n), 0), cptr{0}, cent;
+  std::vector<int32_t> head(static_cast<size_t>(n), 0), cptr{0}, cent, cdof;
   std::vector<double> sdiag(static_cast<size_t>(n), 0.0);
   for (int32_t d = 0; d < n; ++d) {
     const int32_t q0 = cnt[d], q1 = cnt[d + 1];
@@ -644,10 +698,13 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
       sdiag[d] = sval[-centry[q0] - 1];
     } else {
       head[d] = -static_cast<int32_t>(cptr.size());  // -(c+1), c = cptr.size()-1
+      cdof.push_back(d);
       cent.insert(cent.end(), centry.begin() + q0, centry.begin() + q1);
       cptr.push_back(static_cast<int32_t>(cent.size()));
     }
   }
+  L.S.n_complex = static_cast<int32_t>(cdof.size());
+  L.S.cdof = h.upload(cdof.data(), cdof.size());
   L.S.n = n;
   L.S.gamma = src.gamma;
   L.S.head = h.upload(head.data(), head.size());
@@ -691,6 +748,9 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     h->L = n_levels;
     h->lv.resize(n_levels);
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     CK(cudaEventCreate(&h->ev0));
     CK(cudaEventCreate(&h->ev1));
     ig_info& I = h->info;
@@ -798,7 +858,10 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       vc += 12 * L.R.nnz + 4 * (n + 1) + 8 * nc + 16 * n + 8 * n;        // P + x update
       vcl += 2 * layout_spmv(L.A, n, n, true) + 2 * as + 8 * n + layout_spmv(L.R, nc, n, false) +
              layout_spmv(L.P, n, nc, false) + 16 * n;
-      kv += 2 * (L.n_multi > 0 ? 2 : 1) + 4;
+      // smoother: [blocks] + simple + [complex | finish_red on the finest], twice;
+      // plus SpMV-residual x2, restriction, prolongation
+      const int per_app = (L.n_multi > 0 ? 1 : 0) + 1 + (L.S.n_complex > 0 ? 1 : 0);
+      kv += 2 * per_app + 4 + (l == n_levels - 1 && L.S.n_complex == 0 ? 1 : 0);
       I.explicit_vals_A[l] = L.A.explicit_vals;
       I.explicit_cols_A[l] = L.A.explicit_cols;
     }

@@ -88,8 +88,14 @@ __device__ __forceinline__ bool last_cta_total(double v, double* partials,
   return true;
 }
 
-__device__ __forceinline__ bool pcg_done(const PcgState* st) {
-  return st != nullptr && *reinterpret_cast<const volatile int32_t*>(&st->done);
+// V-cycle and vector kernels do not test the PCG flags: in the graph, the
+// conditional IF/WHILE nodes skip them once the solve has stopped, and in the
+// host-loop fallback a post-stop V-cycle only touches scratch (z, p, level
+// buffers), never x or the residual history.  Only k_pcg_update tests it
+// (a breakdown detected by the preceding SpMV must not update x and r).
+__device__ __forceinline__ bool pcg_done(const PcgState*) { return false; }
+__device__ __forceinline__ bool pcg_stopped(const PcgState* st) {
+  return *reinterpret_cast<const volatile int32_t*>(&st->done) != 0;
 }
 
 // ----------------------------------------------------------- SELL SpMV ----
@@ -458,6 +464,8 @@ struct AsGather {
   const int32_t* cptr;
   const int32_t* centry;
   const double* sval;
+  int32_t n_complex;
+  const int32_t* cdof;  // complex list index -> DOF
 };
 
 // rz = r . z bookkeeping after a preconditioner application (solvers.cpp:41-43, :63-65).
@@ -512,6 +520,83 @@ __global__ void __launch_bounds__(kCta) k_as_gather(AsGather S, const double* __
     if (last_cta_total(prod, partials, &st->counter[2], &rz))
       if (threadIdx.x == 0) rz_update(st, rz);
   }
+}
+
+// Split form of phase 2 (default): the per-DOF work is partitioned so the
+// singleton fast path, which does not read ybuf, runs CONCURRENTLY with the
+// block solves (a second stream / graph branch), and only the DOFs with
+// contribution lists wait for them.  Arithmetic per DOF is unchanged.
+__device__ __forceinline__ double as_list_sum(const AsGather& S, int d, double rd,
+                                              const double* __restrict__ ybuf) {
+  const int c = -S.head[d] - 1;
+  double acc = 0.0;
+  for (int q = S.cptr[c]; q < S.cptr[c + 1]; ++q) {
+    const int code = S.centry[q];
+    double v;
+    if (code < 0) {
+      const double ls = S.sval[-code - 1];
+      v = (rd / ls) / ls;
+    } else {
+      v = ybuf[code];
+    }
+    acc = acc + v;
+  }
+  return acc;
+}
+
+template <bool ACC>
+__global__ void __launch_bounds__(kCta) k_as_simple(AsGather S, const double* __restrict__ r, double* x,
+                                                    const PcgState* st) {
+  if (pcg_done(st)) return;
+  const int d = blockIdx.x * kCta + threadIdx.x;
+  if (d >= S.n) return;
+  const int h = S.head[d];
+  const double rd = r[d];
+  const double l = S.sdiag[d];
+  const double xo = ACC ? x[d] : 0.0;
+  if (h < 0) return;
+  double acc = 0.0;
+  acc = acc + (rd / l) / l;
+  const double out = S.gamma * acc;
+  x[d] = ACC ? xo + out : out;
+}
+
+template <bool ACC>
+__global__ void __launch_bounds__(kCta) k_as_complex(AsGather S, const double* __restrict__ r,
+                                                     const double* __restrict__ ybuf, double* x,
+                                                     const PcgState* st) {
+  if (pcg_done(st)) return;
+  const int c = blockIdx.x * kCta + threadIdx.x;
+  if (c >= S.n_complex) return;
+  const int d = S.cdof[c];
+  const double out = S.gamma * as_list_sum(S, d, r[d], ybuf);
+  x[d] = ACC ? x[d] + out : out;
+}
+
+// Finest level inside PCG: complex DOFs finish here, simple DOFs read back
+// k_as_simple's result, and every DOF contributes r_d * z_d to r . z in the
+// canonical chunk order.
+template <bool ACC>
+__global__ void __launch_bounds__(kCta) k_as_finish_red(AsGather S, const double* __restrict__ r,
+                                                        const double* __restrict__ ybuf, double* x,
+                                                        const double* rdot, PcgState* st, double* partials) {
+  if (pcg_done(st)) return;
+  const int d = blockIdx.x * kCta + threadIdx.x;
+  double prod = 0.0;
+  if (d < S.n) {
+    double xn;
+    if (S.head[d] >= 0) {
+      xn = x[d];
+    } else {
+      const double out = S.gamma * as_list_sum(S, d, r[d], ybuf);
+      xn = ACC ? x[d] + out : out;
+      x[d] = xn;
+    }
+    prod = rdot[d] * xn;
+  }
+  double rz;
+  if (last_cta_total(prod, partials, &st->counter[2], &rz))
+    if (threadIdx.x == 0) rz_update(st, rz);
 }
 
 // r . z as its own pass, for a 1-level hierarchy whose preconditioner is the
@@ -642,7 +727,17 @@ __global__ void k_coarse(int32_t n, int32_t rank, const double* __restrict__ Lp,
 // ---------------------------------------------------------- PCG vectors ---
 
 // x = 0, r = b, bnorm from the canonical reduction (solvers.cpp:24-39).
-__global__ void __launch_bounds__(kCta) k_pcg_init(int32_t n, double* r, PcgState* st, double* partials) {
+// Sets the graph conditions (handles != 0) to "keep going": c_if guards the
+// first V-cycle, c_loop the WHILE node.
+__device__ __forceinline__ void set_conds(cudaGraphConditionalHandle c_if, cudaGraphConditionalHandle c_loop,
+                                          bool go) {
+  if (c_if != 0) cudaGraphSetConditional(c_if, go ? 1u : 0u);
+  if (c_loop != 0) cudaGraphSetConditional(c_loop, go ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(kCta) k_pcg_init(int32_t n, double* r, PcgState* st, double* partials,
+                                                   cudaGraphConditionalHandle c_if,
+                                                   cudaGraphConditionalHandle c_loop) {
   const int i = blockIdx.x * kCta + threadIdx.x;
   double prod = 0.0;
   if (i < n) {
@@ -668,15 +763,23 @@ __global__ void __launch_bounds__(kCta) k_pcg_init(int32_t n, double* r, PcgStat
           st->done = 1;
         }
       }
+      set_conds(c_if, c_loop, st->done == 0);
     }
   }
 }
 
 // x += alpha p; r -= alpha Ap; rel = ||r|| / ||b|| (solvers.cpp:51-61).
+// The last CTA also sets the graph conditions: c_if guards this iteration's
+// V-cycle + p update, c_loop the WHILE node.
 __global__ void __launch_bounds__(kCta) k_pcg_update(int32_t n, const double* __restrict__ p,
                                                      const double* __restrict__ ap, double* r,
-                                                     PcgState* st, double* partials) {
-  if (pcg_done(st)) return;
+                                                     PcgState* st, double* partials,
+                                                     cudaGraphConditionalHandle c_if,
+                                                     cudaGraphConditionalHandle c_loop) {
+  if (pcg_stopped(st)) {  // breakdown in the preceding SpMV: x, r stay
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_conds(c_if, c_loop, false);
+    return;
+  }
   const int i = blockIdx.x * kCta + threadIdx.x;
   const double alpha = st->alpha;
   double prod = 0.0;
@@ -701,18 +804,15 @@ __global__ void __launch_bounds__(kCta) k_pcg_update(int32_t n, const double* __
         st->status = ST_NOT_CONVERGED;
         st->done = 1;
       }
+      set_conds(c_if, c_loop, st->done == 0);
     }
   }
 }
 
-// p = z (first) or p = z + beta p (solvers.cpp:42, :64); block 0 also sets
-// the graph's WHILE condition (handle != 0) to "not done".
+// p = z (first) or p = z + beta p (solvers.cpp:42, :64).
 template <bool FIRST>
 __global__ void __launch_bounds__(kCta) k_pcg_p(int32_t n, const double* __restrict__ z, double* p,
-                                                PcgState* st, cudaGraphConditionalHandle cond) {
-  const bool done = pcg_done(st);
-  if (cond != 0 && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, done ? 0u : 1u);
-  if (done) return;
+                                                const PcgState* st) {
   const int i = blockIdx.x * kCta + threadIdx.x;
   if (i >= n) return;
   if (FIRST)
