@@ -1,0 +1,42 @@
+"""BASELINE.json configs[1] (C2, p = 1..4, 512^2) and configs[2] (C3, 1024^2
+perforated plate) at FULL size: device PCG bit-identical to the GPU-order
+oracle and within the north-star tolerances of the sequential oracle."""
+import numpy as np
+import pytest
+
+import oracle_ffi as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(case):
+    from paper_1903_10977_b200 import MgHierarchy, pcg
+    h = MgHierarchy(case)
+    x, rep = pcg(h.A, case.b, h, tol=1e-8, maxit=1000)
+    assert rep.converged
+    st, xo, ro, it, _ = orc.pcg(case.levels_c(), case.b, tol=1e-8, maxit=1000, mode=orc.GPU_ORDER)
+    assert st == 0 and it == rep.iterations
+    assert np.array_equal(np.array(rep.residuals), ro)
+    assert np.array_equal(x, xo)
+    st, xs, rs, its, _ = orc.pcg(case.levels_c(), case.b, tol=1e-8, maxit=1000, mode=orc.SEQ)
+    assert st == 0 and abs(its - rep.iterations) <= 1
+    k = min(11, len(rs))
+    assert np.all(np.abs(np.array(rep.residuals[:k]) - rs[:k]) <= 1e-9 * rs[:k])
+    assert np.linalg.norm(x - xs) <= 1e-8 * np.linalg.norm(xs)
+    h.close()
+    return rep.iterations
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_c2_degree_sweep_full_size(p):
+    from paper_1903_10977_b200 import build_case, configs
+    case = build_case(configs.c2(p=p, seed=configs.c2_seed()))
+    assert case.info.eta < 1e-4  # the seed rule of configs[1]
+    _check(case)
+
+
+def test_c3_perforated_plate_full_size():
+    from paper_1903_10977_b200 import build_case, configs
+    case = build_case(configs.c3())
+    assert case.level_dofs()[-1] == 830708
+    _check(case)
