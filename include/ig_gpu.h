@@ -166,6 +166,13 @@ int ig_pcg_device(ig_hier *h, const double *d_b, double tol, int32_t maxit,
  * ig_pcg_device; residuals (maxit+1, may be NULL), iterations. */
 int ig_pcg_result(ig_hier *h, double *residuals, int32_t *iterations);
 
+/* Debug: run one V-cycle with direct launches and an event after every step
+ * (smoother, residual, restriction, prolongation, coarse solve); writes the
+ * elapsed ms per step, its level and a label (label_len bytes each). */
+int ig_debug_vcycle_timeline(ig_hier *h, const double *d_r, double *d_x,
+                             int32_t max_steps, float *ms, int32_t *levels,
+                             char *labels, int32_t label_len, int32_t *count);
+
 /* Thread-local message for the last non-OK status. */
 const char *ig_last_error(void);
 
@@ -173,6 +180,7 @@ const char *ig_last_error(void);
 #define IG_OPT_USE_GRAPH 1 /* 1 (default): CUDA-graph PCG loop; 0: host loop */
 #define IG_OPT_ROW_DICT 2  /* 1 (default): row-dictionary SELL; 0: plain SELL */
 #define IG_OPT_SPMV_VARIANT 3 /* SpMV batch/prefetch variant 0..3 (kernels.cuh SpmvVar) */
+#define IG_OPT_SMALL_ROWS 4   /* matrices with <= this many rows use the 8-lanes-per-row SpMV */
 int ig_set_option(int32_t option, int64_t value);
 
 #ifdef __cplusplus

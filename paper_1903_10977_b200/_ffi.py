@@ -69,6 +69,7 @@ IG_SMOOTHER_JACOBI, IG_SMOOTHER_GAUSS_SEIDEL, IG_SMOOTHER_ADDITIVE_SCHWARZ, IG_S
 IG_OPT_USE_GRAPH = 1
 IG_OPT_ROW_DICT = 2
 IG_OPT_SPMV_VARIANT = 3
+IG_OPT_SMALL_ROWS = 4
 
 _host = None
 _gpu = None
@@ -132,6 +133,7 @@ def gpu() -> C.CDLL:
         lib.ig_pcg.argtypes = [vp, dp, f64, i32, dp, dp, P(i32), dp]
         lib.ig_vcycle_device.argtypes = [vp, vp, vp]
         lib.ig_level_spmv_device.argtypes = [vp, i32, vp, vp, i32]
+        lib.ig_debug_vcycle_timeline.argtypes = [vp, vp, vp, i32, P(C.c_float), P(i32), C.c_char_p, i32, P(i32)]
         lib.ig_pcg_device.argtypes = [vp, vp, f64, i32, vp]
         lib.ig_pcg_result.argtypes = [vp, dp, P(i32)]
         lib.ig_last_error.restype = C.c_char_p

