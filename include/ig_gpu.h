@@ -181,6 +181,8 @@ const char *ig_last_error(void);
 #define IG_OPT_ROW_DICT 2  /* 1 (default): row-dictionary SELL; 0: plain SELL */
 #define IG_OPT_SPMV_VARIANT 3 /* SpMV batch/prefetch variant 0..3 (kernels.cuh SpmvVar) */
 #define IG_OPT_SMALL_ROWS 4   /* matrices with <= this many rows use the 8-lanes-per-row SpMV */
+#define IG_OPT_TMA_ROWS 5     /* matrices with >= this many rows use the compact SELL (0: never) */
+#define IG_OPT_TSELL_KERNEL 6 /* compact-SELL kernel: 0 direct thread-per-row, 1 TMA-staged */
 int ig_set_option(int32_t option, int64_t value);
 
 #ifdef __cplusplus

@@ -70,6 +70,7 @@ IG_OPT_USE_GRAPH = 1
 IG_OPT_ROW_DICT = 2
 IG_OPT_SPMV_VARIANT = 3
 IG_OPT_SMALL_ROWS = 4
+IG_OPT_TMA_ROWS = 5
 
 _host = None
 _gpu = None

@@ -21,6 +21,7 @@
 
 #include "ig_gpu.h"
 #include "kernels.cuh"
+#include "spmv_tma.cuh"
 
 using namespace igk;
 
@@ -61,6 +62,11 @@ struct HostSell {
 int g_use_dict = 1;
 int g_spmv_variant = 3;  // profiles/spmv_variants.py: best full-PCG time on C4
 int g_small_rows = 40000;  // matrices up to this many rows use k_spmv_grp (profiles/option_sweep.py)
+// Compact-SELL layouts (spmv_tma.cuh) measured SLOWER than the row-dictionary
+// SELL on C4 (finest SpMV 442 us direct / 410 us TMA-staged vs 303 us;
+// profiles/spmv_layouts.py), so they are off by default.
+int g_tma_rows = 0;        // matrices with at least this many rows use the compact layout (0 = never)
+int g_tsell_kernel = 0;    // compact layout kernel: 0 thread-per-row direct, 1 TMA-staged
 constexpr int kDictEntries = 8;
 
 uint64_t fnv(const void* p, size_t bytes, uint64_t h = 1469598103934665603ULL) {
@@ -208,7 +214,62 @@ struct DevSell {
   bool stream = false;
   int64_t nnz = 0, slots = 0;
   int64_t explicit_vals = 0, explicit_cols = 0;
+  bool has_t = false;  // TMA-staged compact layout present (large matrices)
+  TSell t{};
+  int64_t t_bytes = 0;  // matrix bytes of the compact layout (cols + vals)
 };
+
+// Compact TMA layout from the SELL image (spmv_tma.cuh: TSell).
+struct HostTSell {
+  std::vector<TSliceMeta> meta;
+  std::vector<int32_t> cols;
+  std::vector<double> vals;
+};
+
+HostTSell to_tsell(const HostSell& s) {
+  HostTSell t;
+  const int32_t nslice = (s.nr + kSell - 1) / kSell;
+  t.meta.resize(static_cast<size_t>(std::max(nslice, 1)));
+  for (int32_t sl = 0; sl < nslice; ++sl) {
+    TSliceMeta m{};
+    const int64_t w = (s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell;
+    m.nch = static_cast<int32_t>((w + kKC - 1) / kKC);
+    std::vector<int> cl, vl;  // lanes needing explicit cols / vals
+    for (int lane = 0; lane < kSell; ++lane) {
+      const int32_t row = sl * kSell + lane;
+      if (row >= s.nr) continue;
+      const int info = s.rowinfo[row];
+      if ((info & 0xffff) == 0) continue;
+      if (((info >> 24) & 0xff) == 0) {
+        m.cmask |= 1u << lane;
+        cl.push_back(lane);
+      }
+      if (((info >> 16) & 0xff) == 0) {
+        m.vmask |= 1u << lane;
+        vl.push_back(lane);
+      }
+    }
+    m.col_off = static_cast<int64_t>(t.cols.size());
+    m.val_off = static_cast<int64_t>(t.vals.size());
+    const int64_t kpad = static_cast<int64_t>(m.nch) * kKC;
+    t.cols.resize(t.cols.size() + static_cast<size_t>(kpad * cl.size()), 0);
+    t.vals.resize(t.vals.size() + static_cast<size_t>(kpad * vl.size()), 0.0);
+    for (int64_t k = 0; k < kpad; ++k) {
+      for (size_t j = 0; j < cl.size(); ++j) {
+        const int32_t row = sl * kSell + cl[j];
+        if (k < (s.rowinfo[row] & 0xffff))
+          t.cols[m.col_off + k * static_cast<int64_t>(cl.size()) + j] = s.col[s.slice_ptr[sl] + k * kSell + cl[j]];
+      }
+      for (size_t j = 0; j < vl.size(); ++j) {
+        const int32_t row = sl * kSell + vl[j];
+        if (k < (s.rowinfo[row] & 0xffff))
+          t.vals[m.val_off + k * static_cast<int64_t>(vl.size()) + j] = s.val[s.slice_ptr[sl] + k * kSell + vl[j]];
+      }
+    }
+    t.meta[sl] = m;
+  }
+  return t;
+}
 
 struct Level {
   int32_t n = 0;
@@ -242,6 +303,7 @@ struct ig_hier {
   int coarse_use_smem = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // block solves, forked from / joined into `stream`
+  int num_sms = 148;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   PcgState* st = nullptr;
   double* partials = nullptr;
@@ -291,6 +353,29 @@ struct ig_hier {
     d.slots = h.slice_ptr.back();
     d.explicit_vals = h.explicit_vals;
     d.explicit_cols = h.explicit_cols;
+    if (g_tma_rows > 0 && h.nr >= g_tma_rows) {
+      const HostTSell t = to_tsell(h);
+      d.has_t = true;
+      d.t.n_rows = h.nr;
+      d.t.n_slices = (h.nr + kSell - 1) / kSell;
+      d.t.n_chunks = static_cast<int32_t>((static_cast<int64_t>(h.nr) + kCta - 1) / kCta);
+      d.t.meta = upload(t.meta.data(), t.meta.size());
+      d.t.rowinfo = d.s.rowinfo;
+      d.t.cols = upload(t.cols.data(), t.cols.size());
+      d.t.vals = upload(t.vals.data(), t.vals.size());
+      d.t.dict_w = d.s.dict_w;
+      d.t.dval = d.s.dval;
+      d.t.doff = d.s.doff;
+      d.t_bytes = static_cast<int64_t>(t.cols.size()) * 4 + static_cast<int64_t>(t.vals.size()) * 8;
+      static bool attr_done = false;
+      if (!attr_done) {
+        CK(cudaFuncSetAttribute(k_spmv_tma<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem));
+        CK(cudaFuncSetAttribute(k_spmv_tma<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem));
+        CK(cudaFuncSetAttribute(k_spmv_tma<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem));
+        CK(cudaFuncSetAttribute(k_spmv_tma<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem));
+        attr_done = true;
+      }
+    }
     // Stream (evict-first) matrices far larger than L2; keep small ones cached.
     d.stream = d.slots * 12 > (int64_t(48) << 20);
     return d;
@@ -321,6 +406,27 @@ struct ig_hier {
             PcgState* s = nullptr, bool red = false) {
     const unsigned g = grid_of(A.s.n_rows);
     if (g == 0) return;
+    if (A.has_t && g_tsell_kernel == 0) {  // large matrix: compact SELL, thread per row
+      if (red)
+        k_spmv_cmp<0, true><<<g, kCta, 0, stream>>>(A.t, x, y, rsrc, s, partials);
+      else if (mode == 0)
+        k_spmv_cmp<0, false><<<g, kCta, 0, stream>>>(A.t, x, y, rsrc, s, partials);
+      else
+        k_spmv_cmp<1, false><<<g, kCta, 0, stream>>>(A.t, x, y, rsrc, s, partials);
+      CK(cudaGetLastError());
+      return;
+    }
+    if (A.has_t) {  // large matrix: TMA-staged compact SELL, persistent grid
+      const unsigned gt = static_cast<unsigned>(std::min<int64_t>(A.t.n_chunks, static_cast<int64_t>(num_sms) * 2));
+      if (red)
+        k_spmv_tma<0, true><<<gt, kCta, kTSmem, stream>>>(A.t, x, y, rsrc, s, partials);
+      else if (mode == 0)
+        k_spmv_tma<0, false><<<gt, kCta, kTSmem, stream>>>(A.t, x, y, rsrc, s, partials);
+      else
+        k_spmv_tma<1, false><<<gt, kCta, kTSmem, stream>>>(A.t, x, y, rsrc, s, partials);
+      CK(cudaGetLastError());
+      return;
+    }
     if (!red && A.s.n_rows <= g_small_rows) {  // latency-bound level: 8 lanes per row
       const unsigned gg = grid_of(static_cast<int64_t>(A.s.n_rows) * 8);
       if (mode == 0)
@@ -761,6 +867,15 @@ int ig_set_option(int32_t option, int64_t value) {
     g_use_dict = value != 0;
     return IG_OK;
   }
+  if (option == IG_OPT_TSELL_KERNEL) {
+    g_tsell_kernel = value != 0;
+    return IG_OK;
+  }
+  if (option == IG_OPT_TMA_ROWS) {
+    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: bad row threshold");
+    g_tma_rows = static_cast<int>(value);
+    return IG_OK;
+  }
   if (option == IG_OPT_SMALL_ROWS) {
     if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: bad row threshold");
     g_small_rows = static_cast<int>(value);
@@ -785,6 +900,7 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     h->lv.resize(n_levels);
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, 0));
     CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     CK(cudaEventCreate(&h->ev0));

@@ -44,6 +44,46 @@ __device__ __forceinline__ double cta_reduce(double v, double* sm8) {
   return t;
 }
 
+// Arrive once per CTA (after this CTA wrote its chunk partials); the last CTA
+// to arrive reduces all nparts partials (lane t sums P[t], P[t+256], ...
+// ascending, then cta_reduce) and returns true with *total set (valid in every
+// thread of that CTA).  Must be reached by all threads of every CTA.
+__device__ __forceinline__ bool grid_finish(unsigned int nparts, const double* partials, unsigned int* counter,
+                                            double* total) {
+  __shared__ double sm8f[8];
+  __shared__ bool is_last;
+  __shared__ double tot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int prev = atomicAdd(counter, 1u);
+    is_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return false;
+  __threadfence();
+  // Loads are issued 8 at a time ahead of the (serial) adds so the tail is
+  // one L2 round trip per 8 partials, not per partial.
+  double a = 0.0;
+  unsigned int k = threadIdx.x;
+  for (; k + 7 * kCta < nparts; k += 8 * kCta) {
+    double q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) q[u] = __ldcg(partials + k + u * kCta);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a = a + q[u];
+  }
+  for (; k < nparts; k += kCta) a = a + __ldcg(partials + k);
+  const double t = cta_reduce(a, sm8f);
+  if (threadIdx.x == 0) {
+    tot = t;
+    *counter = 0u;
+  }
+  __syncthreads();
+  *total = tot;
+  return true;
+}
+
 // Reduce this CTA's chunk (one value per thread, cta_reduce) and publish the
 // partial; the last CTA to arrive reduces all partials (lane t sums P[t],
 // P[t+256], ... ascending, then cta_reduce) and returns true with *total set
