@@ -102,6 +102,10 @@ def build_workload(name: str, threads: int):
     elif name == "c3":
         cfg = configs.c3(threads=threads)
         desc = "C3: 2D plate minus 64 holes, 1024^2, p=2, 9 levels, additive Schwarz"
+    elif name == "c5":
+        cfg = configs.c5(threads=threads)
+        desc = ("C5: 2D THB p=2, base 128^2 + 2 local refinement passes within 0.05 of the circle r=0.4, "
+                "6 levels, additive Schwarz")
     elif name.startswith("c2"):
         p = int(name[3:]) if len(name) > 3 else 2
         cfg = configs.c2(p=p, seed=configs.c2_seed(), threads=threads)
@@ -326,10 +330,9 @@ def run_reference(args, world, rank):
     case, desc, t_setup = build_workload(args.workload, args.threads)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_ffi as orc
-    # Full-solve iteration count of the oracle itself is needed for the
-    # extrapolation; it equals the device count (bit-identical paths), taken
-    # from a short reference probe of the residual decay is not possible, so
-    # the known count is measured once on a cheaper sample: run the sample.
+    # Each step times a bounded sample (the first iterations of the same
+    # solve); the per-iteration cost is extrapolated to the full solve's
+    # iteration count, which the oracle reaches on the same hierarchy.
     iters_full = int(os.environ.get("IG_REF_ITERS", "0")) or None
     samples = []
     sample_iters = max(1, args.cpu_sample_iters // 2)
@@ -339,7 +342,10 @@ def run_reference(args, world, rank):
             samples.append(sec / (it + 1))
     per_unit = statistics.median(samples)
     if iters_full is None:
-        iters_full = {"c4": 105, "c1": 25}.get(args.workload, 30)
+        # Oracle (sequential-order) iteration counts of the full solves,
+        # pinned by tests/test_thb.py, tests/test_gpu_configs.py and the C4 golden.
+        iters_full = {"c1": 25, "c2": 27, "c2-1": 18, "c2-2": 27, "c2-3": 55, "c2-4": 106,
+                      "c3": 38, "c4": 115, "c5": 37}[args.workload]
     t_full = per_unit * (iters_full + 1)
     v = case.n / t_full
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,

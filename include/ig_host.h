@@ -26,7 +26,7 @@ typedef struct {
   double origin[3];
   double extent[3];
   int32_t resolution[3];   /* background cells per axis (finest level)        */
-  int32_t family;          /* 0 Lagrange (2D), 1 B-spline                     */
+  int32_t family;          /* 0 Lagrange (2D), 1 B-spline, 2 THB (2D)         */
   int32_t degree;          /* 1..4                                            */
   int32_t levels;          /* total MG levels, >= 1                           */
   int32_t quad_depth;      /* cut-cell bisection depth (QuadratureConfig)     */
@@ -40,6 +40,15 @@ typedef struct {
   double gamma;            /* 0 = automatic (smoothers.cpp:234-239)           */
   double filter_ratio;     /* block eigen-filter ratio (default 1e-16)        */
   int32_t threads;         /* host threads for setup; 0 = all                 */
+  /* THB (family 2, 2D) local refinement of the finest mesh, applied in order:
+   * refine-by-box passes (mesh.cpp:51-56), then refine_passes passes of
+   * "elements of the current finest level within refine_dist of the circle
+   * (cx, cy, r)" (configs[4]; HierarchicalMesh::refine, mesh.cpp:35-49). */
+  int32_t n_refine_boxes;
+  const double *refine_boxes; /* 4 per box: x0, y0, x1, y1 */
+  int32_t refine_passes;
+  double refine_circle[3];
+  double refine_dist;
 } igh_config;
 
 typedef struct igh_case igh_case;

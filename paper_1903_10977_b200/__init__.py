@@ -122,6 +122,12 @@ class CaseConfig:
     dirichlet_box_sides: bool = True
     smoother: SmootherConfig = dataclasses.field(default_factory=SmootherConfig)
     threads: int = 0
+    # THB local refinement (family="thb", 2D): refine-by-box passes, then
+    # `refine_passes` passes near the circle (cx, cy, r) within refine_dist.
+    refine_boxes: Sequence[Sequence[float]] = ()
+    refine_passes: int = 0
+    refine_circle: Sequence[float] = (0.0, 0.0, 0.0)
+    refine_dist: float = 0.0
 
     def to_c(self) -> _ffi.igh_config:
         c = _ffi.igh_config()
@@ -133,7 +139,15 @@ class CaseConfig:
             c.origin[i] = float(self.origin[i]) if i < len(self.origin) else 0.0
             c.extent[i] = float(self.extent[i]) if i < len(self.extent) else 1.0
             c.resolution[i] = int(self.resolution[i]) if i < len(self.resolution) else 1
-        c.family = 0 if self.family.lower().startswith("lag") else 1
+        fam = self.family.lower()
+        c.family = 0 if fam.startswith("lag") else (2 if fam == "thb" else 1)
+        self._boxes = np.ascontiguousarray(np.array(self.refine_boxes, dtype=np.float64).reshape(-1))
+        c.n_refine_boxes = len(self.refine_boxes)
+        c.refine_boxes = self._boxes.ctypes.data_as(_dp) if len(self.refine_boxes) else None
+        c.refine_passes = self.refine_passes
+        for i in range(3):
+            c.refine_circle[i] = float(self.refine_circle[i])
+        c.refine_dist = self.refine_dist
         c.degree = self.degree
         c.levels = self.levels
         c.quad_depth = self.quad_depth

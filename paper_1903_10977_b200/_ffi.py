@@ -54,7 +54,8 @@ class igh_config(C.Structure):
                 ("gauss_order", i32), ("classify_depth", i32), ("edge_tol", f64),
                 ("body_force", f64), ("beta", f64), ("dirichlet_box_sides", i32),
                 ("smoother_kind", i32), ("gamma", f64), ("filter_ratio", f64),
-                ("threads", i32)]
+                ("threads", i32), ("n_refine_boxes", i32), ("refine_boxes", P(f64)),
+                ("refine_passes", i32), ("refine_circle", f64 * 3), ("refine_dist", f64)]
 
 
 class igh_info(C.Structure):

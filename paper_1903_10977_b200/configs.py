@@ -6,7 +6,8 @@ Deviations from the config text, all forced by the reference:
     implements only the penalty method, assembly.cpp:106-131);
   * additive Schwarz with gamma = 1/max N_K (D4);
   * levels for C3/C4 chosen so the coarsest grid is 4 cells per axis (D7).
-C5 (THB) needs a THB space, which is not built yet (next rows).
+C5 uses the THB space (host/thb.cpp) with a hierarchy that follows the
+refinement levels (the reference's Algorithm-2 coarsening).
 """
 from __future__ import annotations
 
@@ -95,4 +96,17 @@ def c4(res: int = 128, levels: int = 6, threads: int = 0) -> CaseConfig:
                       threads=threads)
 
 
-CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4}
+def c5(threads: int = 0, base: int = 128, levels: int = 6) -> CaseConfig:
+    """2D THB (configs[4]): p=2, base 128^2 on [0,1]^2, two passes of local
+    dyadic refinement on elements within 0.05 of the circle r=0.4 centred at
+    (0.5+d, 0.5+d) (the same seed-1 delta on both axes as
+    the config text), Dirichlet on the circle, hierarchy following the
+    refinement levels (coarsen keeps the 2 local levels, base down to 4)."""
+    d = seed_offsets(1)[0]
+    c = 0.5 + d
+    return CaseConfig(geometry=f"disc({c!r}, {c!r}, 0.4)", dim=2, resolution=(base, base, 1), family="thb",
+                      degree=2, levels=levels, smoother=SmootherConfig("additive-schwarz"), threads=threads,
+                      refine_passes=2, refine_circle=(c, c, 0.4), refine_dist=0.05)
+
+
+CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}

@@ -16,6 +16,7 @@
 
 #include "../../include/ig_host.h"
 #include "host.hpp"
+#include "thb.hpp"
 
 #ifdef _OPENMP
 #include <omp.h>
@@ -470,6 +471,7 @@ struct igh_case {
   igh_config cfg{};
   std::string geometry;
   std::vector<std::unique_ptr<Space>> spaces;  // [0] = coarsest (empty when read from file)
+  std::vector<std::unique_ptr<GSpace>> gspaces;  // THB levels
   std::vector<Csr> A, R;
   std::vector<Blocks> B;
   std::vector<double> gamma;
@@ -594,6 +596,8 @@ int igh_build(const igh_config* cfg, igh_case** out) {
       g.res[d] = d < dim ? cfg->resolution[d] : 1;
     }
     const LevelSet ls = parse_levelset(c->geometry);
+    const bool thb = cfg->family == 2;
+    if (thb && dim != 2) return fail("igh_build: THB is 2D only");
     const Family fam = cfg->family == 0 ? Family::Lagrange : Family::Bspline;
     QuadConfig qc;
     qc.depth = cfg->quad_depth;
@@ -606,31 +610,57 @@ int igh_build(const igh_config* cfg, igh_case** out) {
     prob.dirichlet_box_sides = cfg->dirichlet_box_sides != 0;
 
     const double t0 = now();
-    std::vector<std::unique_ptr<Space>> down;
-    down.push_back(build_space(g, ls, fam, cfg->degree, cfg->classify_depth, threads));
-    Assembled as = assemble(*down[0], prob, qc, threads);
-    const double t1 = now();
+    const int L = cfg->levels;
     std::vector<Csr> Adown, Rdown;
-    Adown.push_back(std::move(as.A));
-    for (int l = 1; l < cfg->levels; ++l) {
-      Grid cg = down.back()->grid;
-      for (int d = 0; d < dim; ++d) {
-        if (cg.res[d] % 2 != 0)
-          return fail("mesh does not support " + std::to_string(cfg->levels - 1) + " coarsenings");
-        cg.res[d] /= 2;
-      }
-      down.push_back(build_space(cg, ls, fam, cfg->degree, cfg->classify_depth, threads));
-      Csr r = restriction_matrix(*down[l - 1], *down[l]);
+    Assembled as;
+    double t1 = 0.0;
+    std::vector<std::unique_ptr<Space>> down;
+    std::vector<std::unique_ptr<GSpace>> gdown;
+    auto galerkin = [&](Csr r) {  // A_c = R (A R^T) (multigrid.cpp:39-41)
       const Csr rt = transpose(r);
       Csr ap = spgemm(Adown.back(), rt, threads);
       Adown.push_back(spgemm(r, ap, threads));
       Rdown.push_back(std::move(r));
+    };
+    if (thb) {
+      HMesh mesh = HMesh::uniform(g);
+      for (int k = 0; k < cfg->n_refine_boxes; ++k) mesh.refine_by_box(cfg->refine_boxes + 4 * k);
+      for (int k = 0; k < cfg->refine_passes; ++k)
+        mesh.refine_near_circle(cfg->refine_circle[0], cfg->refine_circle[1], cfg->refine_circle[2], cfg->refine_dist);
+      gdown.push_back(build_thb(mesh, ls, cfg->degree, cfg->classify_depth, threads));
+      as = assemble_g(*gdown[0], prob, qc, threads);
+      t1 = now();
+      Adown.push_back(std::move(as.A));
+      for (int l = 1; l < L; ++l) {
+        const HMesh& fm = gdown.back()->mesh;
+        if (fm.g.res[0] % 2 != 0 || fm.g.res[1] % 2 != 0)
+          return fail("mesh does not support " + std::to_string(L - 1) + " coarsenings");
+        gdown.push_back(build_thb(coarsen(fm), ls, cfg->degree, cfg->classify_depth, threads));
+        galerkin(restriction_thb(*gdown[l - 1], *gdown[l], threads));
+      }
+    } else {
+      down.push_back(build_space(g, ls, fam, cfg->degree, cfg->classify_depth, threads));
+      as = assemble(*down[0], prob, qc, threads);
+      t1 = now();
+      Adown.push_back(std::move(as.A));
+      for (int l = 1; l < L; ++l) {
+        Grid cg = down.back()->grid;
+        for (int d = 0; d < dim; ++d) {
+          if (cg.res[d] % 2 != 0)
+            return fail("mesh does not support " + std::to_string(L - 1) + " coarsenings");
+          cg.res[d] /= 2;
+        }
+        down.push_back(build_space(cg, ls, fam, cfg->degree, cfg->classify_depth, threads));
+        galerkin(restriction_matrix(*down[l - 1], *down[l]));
+      }
     }
     Rdown.push_back(Csr{});  // coarsest: empty R
     // Reverse: [0] = coarsest (multigrid.cpp:47-50).
-    const int L = cfg->levels;
     for (int l = L - 1; l >= 0; --l) {
-      c->spaces.push_back(std::move(down[l]));
+      if (thb)
+        c->gspaces.push_back(std::move(gdown[l]));
+      else
+        c->spaces.push_back(std::move(down[l]));
       c->A.push_back(std::move(Adown[l]));
       c->R.push_back(std::move(Rdown[l]));
     }
@@ -641,8 +671,14 @@ int igh_build(const igh_config* cfg, igh_case** out) {
     c->gamma.assign(L, 0.0);
     c->kind.assign(L, cfg->smoother_kind);
     for (int l = 1; l < L; ++l) {
-      Blocks b = select_blocks(*c->spaces[l], threads);
-      b.max_nk = max_blocks_per_element(b, *c->spaces[l]);
+      Blocks b;
+      if (thb) {
+        b = select_blocks_g(*c->gspaces[l]);
+        b.max_nk = max_blocks_per_element_g(b, *c->gspaces[l]);
+      } else {
+        b = select_blocks(*c->spaces[l], threads);
+        b.max_nk = max_blocks_per_element(b, *c->spaces[l]);
+      }
       factorize_blocks(c->A[l], b, cfg->filter_ratio, threads);
       double gm = cfg->gamma;
       if (gm <= 0.0) {
@@ -667,6 +703,16 @@ int igh_build(const igh_config* cfg, igh_case** out) {
     c->b = std::move(as.b);
     c->xyz.resize(L);
     for (int l = 0; l < L; ++l) {
+      if (thb) {  // (ax, ay, hierarchy level)
+        const GSpace& s = *c->gspaces[l];
+        c->xyz[l].resize(static_cast<size_t>(s.n()) * 3);
+        for (int a = 0; a < s.n(); ++a) {
+          c->xyz[l][3 * a] = s.anchors[a][1];
+          c->xyz[l][3 * a + 1] = s.anchors[a][2];
+          c->xyz[l][3 * a + 2] = s.anchors[a][0];
+        }
+        continue;
+      }
       const Space& s = *c->spaces[l];
       c->xyz[l].resize(static_cast<size_t>(s.n()) * 3);
       for (int a = 0; a < s.n(); ++a) anchor_xyz(s, a, &c->xyz[l][static_cast<size_t>(a) * 3]);
@@ -724,6 +770,19 @@ int igh_eta(const igh_config* cfg, double* eta, int64_t* cut, int32_t* n_dofs) {
       g.res[d] = d < cfg->dim ? cfg->resolution[d] : 1;
     }
     const LevelSet ls = parse_levelset(cfg->geometry ? cfg->geometry : "constant(1)");
+    if (cfg->family == 2) {  // THB: DOF count of the trimmed hierarchical space
+      HMesh mesh = HMesh::uniform(g);
+      for (int k = 0; k < cfg->n_refine_boxes; ++k) mesh.refine_by_box(cfg->refine_boxes + 4 * k);
+      for (int k = 0; k < cfg->refine_passes; ++k)
+        mesh.refine_near_circle(cfg->refine_circle[0], cfg->refine_circle[1], cfg->refine_circle[2], cfg->refine_dist);
+      auto gs = build_thb(mesh, ls, cfg->degree, cfg->classify_depth, threads);
+      int64_t nc = 0;
+      for (const auto& e : gs->el) nc += e.tag == kCut;
+      if (eta) *eta = -1.0;  // not computed for THB here
+      if (cut) *cut = nc;
+      if (n_dofs) *n_dofs = gs->n();
+      return IG_OK;
+    }
     auto s = build_space(g, ls, cfg->family == 0 ? Family::Lagrange : Family::Bspline, cfg->degree,
                          cfg->classify_depth, threads);
     QuadConfig qc;

@@ -40,3 +40,10 @@ def test_c3_perforated_plate_full_size():
     case = build_case(configs.c3())
     assert case.level_dofs()[-1] == 830708
     _check(case)
+
+
+def test_c5_thb_full_size():
+    from paper_1903_10977_b200 import build_case, configs
+    case = build_case(configs.c5())
+    assert case.level_dofs()[-1] == 40211
+    assert _check(case) == 37
