@@ -183,6 +183,7 @@ const char *ig_last_error(void);
 #define IG_OPT_SMALL_ROWS 4   /* matrices with <= this many rows use the 8-lanes-per-row SpMV */
 #define IG_OPT_TMA_ROWS 5     /* matrices with >= this many rows use the compact SELL (0: never) */
 #define IG_OPT_TSELL_KERNEL 6 /* compact-SELL kernel: 0 direct thread-per-row, 1 TMA-staged */
+#define IG_OPT_PSELL 7        /* 1 (default): pattern SELL for matrices above IG_OPT_SMALL_ROWS rows */
 int ig_set_option(int32_t option, int64_t value);
 
 #ifdef __cplusplus

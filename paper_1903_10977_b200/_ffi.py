@@ -72,6 +72,8 @@ IG_OPT_ROW_DICT = 2
 IG_OPT_SPMV_VARIANT = 3
 IG_OPT_SMALL_ROWS = 4
 IG_OPT_TMA_ROWS = 5
+IG_OPT_TSELL_KERNEL = 6
+IG_OPT_PSELL = 7
 
 _host = None
 _gpu = None

@@ -17,10 +17,12 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "ig_gpu.h"
 #include "kernels.cuh"
+#include "spmv_psell.cuh"
 #include "spmv_tma.cuh"
 
 using namespace igk;
@@ -193,6 +195,197 @@ HostSell to_sell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col,
   return s;
 }
 
+// ------------------------------------------------ pattern SELL (host) ------
+// Host image of spmv_psell.cuh's PSell.  See that header for the layout.
+int g_use_psell = 1;
+constexpr int kPDictEntries = 32;
+
+struct HostPSell {
+  std::vector<PSliceMeta> meta;
+  std::vector<uint32_t> rowinfo;
+  std::vector<double> V;
+  std::vector<int32_t> O;
+  int32_t dict_w = 1;
+  int64_t layout_bytes = 0;  // matrix words read from HBM per product (sequences shared by slices once)
+  int64_t n_fast = 0, n_general = 0;
+};
+
+inline uint64_t mix64(uint64_t h, uint64_t w) {
+  h ^= w + 0x9E3779B97F4A7C15ULL + (h << 6) + (h >> 2);
+  return h * 0xff51afd7ed558ccdULL;
+}
+
+// Returns false when the matrix does not fit the format (row longer than
+// kPMaxLen, pools beyond 2^32 entries); the caller keeps the plain SELL.
+bool to_psell(int32_t nr, const int32_t* ptr, const int32_t* col, const double* val, HostPSell& s) {
+  auto len = [&](int32_t i) { return ptr[i + 1] - ptr[i]; };
+  for (int32_t i = 0; i < nr; ++i)
+    if (len(i) > kPMaxLen) return false;
+  std::vector<uint64_t> hv(static_cast<size_t>(nr)), ho(static_cast<size_t>(nr));
+  for (int32_t i = 0; i < nr; ++i) {
+    uint64_t a = static_cast<uint64_t>(len(i)), b = a;
+    for (int32_t k = ptr[i]; k < ptr[i + 1]; ++k) {
+      uint64_t w;
+      std::memcpy(&w, val + k, 8);
+      a = mix64(a, w);
+      b = mix64(b, static_cast<uint64_t>(static_cast<int64_t>(col[k]) - i));
+    }
+    hv[i] = a;
+    ho[i] = b;
+  }
+  auto veq = [&](int32_t a, int32_t b) {
+    return len(a) == len(b) && std::memcmp(val + ptr[a], val + ptr[b], sizeof(double) * len(a)) == 0;
+  };
+  auto oeq = [&](int32_t a, int32_t b) {
+    if (len(a) != len(b)) return false;
+    for (int32_t k = 0; k < len(a); ++k)
+      if (col[ptr[a] + k] - a != col[ptr[b] + k] - b) return false;
+    return true;
+  };
+  // Global value dictionary: the most frequent sequences (>= 32 rows each).
+  std::vector<int32_t> dict_rows;
+  {
+    std::vector<std::pair<uint64_t, int32_t>> keys(static_cast<size_t>(nr));
+    for (int32_t i = 0; i < nr; ++i) keys[i] = {hv[i], i};
+    std::sort(keys.begin(), keys.end());
+    std::vector<std::pair<int64_t, int32_t>> groups;
+    for (size_t a = 0; a < keys.size();) {
+      size_t b = a;
+      while (b < keys.size() && keys[b].first == keys[a].first) ++b;
+      int64_t c = 0;
+      for (size_t k = a; k < b; ++k) c += veq(keys[k].second, keys[a].second) ? 1 : 0;
+      groups.push_back({c, keys[a].second});
+      a = b;
+    }
+    std::sort(groups.begin(), groups.end(), [](const auto& x, const auto& y) {
+      return x.first != y.first ? x.first > y.first : x.second < y.second;
+    });
+    for (const auto& g : groups) {
+      if (static_cast<int>(dict_rows.size()) >= kPDictEntries || g.first < 32) break;
+      dict_rows.push_back(g.second);
+    }
+  }
+  int32_t W = 1;
+  for (int32_t r : dict_rows) W = std::max(W, len(r));
+  s.dict_w = W;
+  s.V.assign(static_cast<size_t>(W) * dict_rows.size(), 0.0);
+  for (size_t e = 0; e < dict_rows.size(); ++e)
+    std::memcpy(s.V.data() + e * W, val + ptr[dict_rows[e]], sizeof(double) * len(dict_rows[e]));
+  s.layout_bytes += static_cast<int64_t>(s.V.size()) * 8;
+  auto dict_of = [&](int32_t i) -> int {  // 1-based dictionary entry, 0 = none
+    for (size_t e = 0; e < dict_rows.size(); ++e)
+      if (hv[i] == hv[dict_rows[e]] && veq(i, dict_rows[e])) return static_cast<int>(e) + 1;
+    return 0;
+  };
+  // Deduplicated stride-1 sequences of FAST slices.
+  std::unordered_map<uint64_t, std::vector<std::pair<uint32_t, int32_t>>> vseq, oseq;  // hash -> (start, row)
+  auto v_start = [&](int32_t i) -> uint32_t {
+    auto& b = vseq[hv[i]];
+    for (const auto& [st, r] : b)
+      if (veq(i, r)) return st;
+    const uint32_t st = static_cast<uint32_t>(s.V.size());
+    s.V.insert(s.V.end(), val + ptr[i], val + ptr[i + 1]);
+    s.layout_bytes += 8 * static_cast<int64_t>(len(i));
+    b.push_back({st, i});
+    return st;
+  };
+  auto o_start = [&](int32_t i) -> uint32_t {
+    auto& b = oseq[ho[i]];
+    for (const auto& [st, r] : b)
+      if (oeq(i, r)) return st;
+    const uint32_t st = static_cast<uint32_t>(s.O.size());
+    for (int32_t k = ptr[i]; k < ptr[i + 1]; ++k) s.O.push_back(col[k] - i);
+    s.layout_bytes += 4 * static_cast<int64_t>(len(i));
+    b.push_back({st, i});
+    return st;
+  };
+  const int32_t nslice = (nr + kSell - 1) / kSell;
+  const int32_t nslice_pad = static_cast<int32_t>((static_cast<int64_t>(nr) + kCta - 1) / kCta) * (kCta / kSell);
+  s.meta.assign(static_cast<size_t>(std::max(nslice_pad, 1)), PSliceMeta{0, 0, 0, 0, 0, 0});
+  s.rowinfo.assign(static_cast<size_t>(std::max(nr, 1)), 0u);
+  int lmax_all = 0;
+  for (int32_t sl = 0; sl < nslice; ++sl) {
+    const int32_t r0 = sl * kSell, r1 = std::min(nr, r0 + kSell);
+    PSliceMeta m{0, 0, 0, 0, 0, 0};
+    int lmax = 0;
+    bool ulen = r1 - r0 == kSell;
+    for (int32_t i = r0; i < r1; ++i) {
+      lmax = std::max(lmax, len(i));
+      ulen = ulen && len(i) == len(r0);
+    }
+    lmax_all = std::max(lmax_all, lmax);
+    m.lmax = static_cast<uint16_t>(lmax);
+    bool fast = ulen;
+    for (int32_t i = r0 + 1; fast && i < r1; ++i)
+      fast = hv[i] == hv[r0] && ho[i] == ho[r0] && veq(i, r0) && oeq(i, r0);
+    if (fast) {
+      const int e = dict_of(r0);
+      m.vbase = e ? static_cast<uint32_t>((e - 1) * W) : v_start(r0);
+      m.obase = o_start(r0);
+      m.flags = kPFast;
+      s.layout_bytes += 16;
+      ++s.n_fast;
+    } else {
+      std::vector<int32_t> opat, vpat;  // representative rows of the table columns
+      std::vector<uint32_t> info(static_cast<size_t>(r1 - r0));
+      for (int32_t i = r0; i < r1; ++i) {
+        int oi = -1;
+        for (size_t j = 0; j < opat.size(); ++j)
+          if (ho[i] == ho[opat[j]] && oeq(i, opat[j])) {
+            oi = static_cast<int>(j);
+            break;
+          }
+        if (oi < 0) {
+          oi = static_cast<int>(opat.size());
+          opat.push_back(i);
+        }
+        const int e = dict_of(i);
+        int vi = 0;
+        if (!e) {
+          vi = -1;
+          for (size_t j = 0; j < vpat.size(); ++j)
+            if (hv[i] == hv[vpat[j]] && veq(i, vpat[j])) {
+              vi = static_cast<int>(j);
+              break;
+            }
+          if (vi < 0) {
+            vi = static_cast<int>(vpat.size());
+            vpat.push_back(i);
+          }
+        }
+        info[i - r0] = static_cast<uint32_t>(len(i)) | static_cast<uint32_t>(e) << 11 |
+                       static_cast<uint32_t>(vi) << 17 | static_cast<uint32_t>(oi) << 22;
+      }
+      const int wo = static_cast<int>(opat.size()), wv = static_cast<int>(vpat.size());
+      m.wo = static_cast<uint8_t>(wo);
+      m.wv = static_cast<uint8_t>(wv);
+      m.obase = static_cast<uint32_t>(s.O.size());
+      s.O.resize(s.O.size() + static_cast<size_t>(lmax) * wo, 0);
+      for (int j = 0; j < wo; ++j) {
+        const int32_t r = opat[j];
+        for (int32_t k = 0; k < len(r); ++k) s.O[m.obase + static_cast<size_t>(k) * wo + j] = col[ptr[r] + k] - r;
+      }
+      m.vbase = static_cast<uint32_t>(s.V.size());
+      s.V.resize(s.V.size() + static_cast<size_t>(lmax) * wv, 0.0);
+      for (int j = 0; j < wv; ++j) {
+        const int32_t r = vpat[j];
+        for (int32_t k = 0; k < len(r); ++k) s.V[m.vbase + static_cast<size_t>(k) * wv + j] = val[ptr[r] + k];
+      }
+      for (int32_t i = r0; i < r1; ++i) s.rowinfo[i] = info[i - r0];
+      m.flags = ulen ? kPUlen : 0u;
+      s.layout_bytes += 16 + 4 * static_cast<int64_t>(r1 - r0) + static_cast<int64_t>(lmax) * (4 * wo + 8 * wv);
+      ++s.n_general;
+    }
+    s.meta[sl] = m;
+    if (s.V.size() > 0xF0000000ull || s.O.size() > 0xF0000000ull) return false;
+  }
+  // Padding: dictionary rows read up to lmax past their start; the last
+  // slice's table columns are read by the out-of-range lanes.
+  s.V.resize(s.V.size() + static_cast<size_t>(lmax_all) + 8, 0.0);
+  s.O.resize(s.O.size() + static_cast<size_t>(lmax_all) + 8, 0);
+  return true;
+}
+
 // Transpose of a CSR (rows of the result visit source rows ascending).
 void csr_transpose(const ig_csr& a, std::vector<int32_t>& tp, std::vector<int32_t>& tc, std::vector<double>& tv) {
   tp.assign(static_cast<size_t>(a.n_cols) + 1, 0);
@@ -217,6 +410,11 @@ struct DevSell {
   bool has_t = false;  // TMA-staged compact layout present (large matrices)
   TSell t{};
   int64_t t_bytes = 0;  // matrix bytes of the compact layout (cols + vals)
+  bool has_p = false;   // pattern-SELL layout present (spmv_psell.cuh)
+  PSell p{};
+  int64_t p_bytes = 0;  // HostPSell::layout_bytes
+  int64_t n_fast = 0, n_general = 0;
+  int64_t layout_matrix_bytes() const { return has_p ? p_bytes : 8 * explicit_vals + 4 * explicit_cols + 4 * int64_t(s.n_rows); }
 };
 
 // Compact TMA layout from the SELL image (spmv_tma.cuh: TSell).
@@ -380,6 +578,37 @@ struct ig_hier {
     d.stream = d.slots * 12 > (int64_t(48) << 20);
     return d;
   }
+  // Device layout of one operator: pattern SELL for the large matrices (when
+  // it fits), the row-dictionary SELL otherwise (and for the small levels,
+  // which run k_spmv_grp on it).
+  DevSell make_matrix(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, const double* val, int64_t nnz) {
+    if (g_use_psell && nr > g_small_rows) {
+      HostPSell hp;
+      if (to_psell(nr, ptr, col, val, hp)) {
+        DevSell d;
+        d.s.n_rows = nr;
+        d.s.n_cols = nc;
+        d.nnz = nnz;
+        d.has_p = true;
+        d.p.n_rows = nr;
+        d.p.n_cols = nc;
+        d.p.meta = upload(hp.meta.data(), hp.meta.size());
+        d.p.rowinfo = upload(hp.rowinfo.data(), hp.rowinfo.size());
+        d.p.V = upload(hp.V.data(), hp.V.size());
+        d.p.O = upload(hp.O.data(), hp.O.size());
+        d.p.dict_w = hp.dict_w;
+        d.p_bytes = hp.layout_bytes;
+        d.n_fast = hp.n_fast;
+        d.n_general = hp.n_general;
+        d.explicit_vals = static_cast<int64_t>(hp.V.size());
+        d.explicit_cols = static_cast<int64_t>(hp.O.size());
+        d.slots = static_cast<int64_t>(hp.V.size());
+        d.stream = static_cast<int64_t>(hp.O.size()) * 4 > (int64_t(48) << 20);
+        return d;
+      }
+    }
+    return upload_sell(to_sell(nr, nc, ptr, col, val), nnz);
+  }
   ~ig_hier() {
     if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
     for (auto& g : vc_graphs) cudaGraphExecDestroy(g.exec);
@@ -406,6 +635,20 @@ struct ig_hier {
             PcgState* s = nullptr, bool red = false) {
     const unsigned g = grid_of(A.s.n_rows);
     if (g == 0) return;
+    if (A.has_p) {
+      if (red) {
+        if (A.stream) k_pspmv<0, true, true><<<g, kCta, 0, stream>>>(A.p, x, y, rsrc, s, partials);
+        else k_pspmv<0, false, true><<<g, kCta, 0, stream>>>(A.p, x, y, rsrc, s, partials);
+      } else if (mode == 0) {
+        if (A.stream) k_pspmv<0, true, false><<<g, kCta, 0, stream>>>(A.p, x, y, rsrc, s, partials);
+        else k_pspmv<0, false, false><<<g, kCta, 0, stream>>>(A.p, x, y, rsrc, s, partials);
+      } else {
+        if (A.stream) k_pspmv<1, true, false><<<g, kCta, 0, stream>>>(A.p, x, y, rsrc, s, partials);
+        else k_pspmv<1, false, false><<<g, kCta, 0, stream>>>(A.p, x, y, rsrc, s, partials);
+      }
+      CK(cudaGetLastError());
+      return;
+    }
     if (A.has_t && g_tsell_kernel == 0) {  // large matrix: compact SELL, thread per row
       if (red)
         k_spmv_cmp<0, true><<<g, kCta, 0, stream>>>(A.t, x, y, rsrc, s, partials);
@@ -456,6 +699,12 @@ struct ig_hier {
   }
   void prolong(const Level& l, const double* xc, double* x, PcgState* s) {
     const unsigned g = grid_of(l.P.s.n_rows);
+    if (l.P.has_p) {
+      if (l.P.stream) k_pprolong<true><<<g, kCta, 0, stream>>>(l.P.p, xc, l.cor, x, s);
+      else k_pprolong<false><<<g, kCta, 0, stream>>>(l.P.p, xc, l.cor, x, s);
+      CK(cudaGetLastError());
+      return;
+    }
     if (l.P.stream)
       prolong_var<true>(g, l, xc, x, s);
     else
@@ -867,6 +1116,10 @@ int ig_set_option(int32_t option, int64_t value) {
     g_use_dict = value != 0;
     return IG_OK;
   }
+  if (option == IG_OPT_PSELL) {
+    g_use_psell = value != 0;
+    return IG_OK;
+  }
   if (option == IG_OPT_TSELL_KERNEL) {
     g_tsell_kernel = value != 0;
     return IG_OK;
@@ -925,12 +1178,12 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       if (s.smoother_kind != IG_SMOOTHER_ADDITIVE_SCHWARZ)
         throw Error(IG_UNSUPPORTED, "device smoother: only additive Schwarz is implemented");
       I.nnz_R[l] = s.R.nnz;
-      L.A = h->upload_sell(to_sell(s.A.n_rows, s.A.n_cols, s.A.row_ptr, s.A.col_idx, s.A.val), s.A.nnz);
-      L.R = h->upload_sell(to_sell(s.R.n_rows, s.R.n_cols, s.R.row_ptr, s.R.col_idx, s.R.val), s.R.nnz);
+      L.A = h->make_matrix(s.A.n_rows, s.A.n_cols, s.A.row_ptr, s.A.col_idx, s.A.val, s.A.nnz);
+      L.R = h->make_matrix(s.R.n_rows, s.R.n_cols, s.R.row_ptr, s.R.col_idx, s.R.val, s.R.nnz);
       std::vector<int32_t> tp, tc;
       std::vector<double> tv;
       csr_transpose(s.R, tp, tc, tv);
-      L.P = h->upload_sell(to_sell(s.R.n_cols, s.R.n_rows, tp.data(), tc.data(), tv.data()), s.R.nnz);
+      L.P = h->make_matrix(s.R.n_cols, s.R.n_rows, tp.data(), tc.data(), tv.data(), s.R.nnz);
       L.res = h->alloc<double>(L.n);
       L.cor = h->alloc<double>(L.n);
       build_smoother(*h, L, s);
@@ -944,7 +1197,7 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     Level& F = h->lv[n_levels - 1];
     if (n_levels == 1) {
       const ig_level& s = levels[0];
-      F.A = h->upload_sell(to_sell(s.A.n_rows, s.A.n_cols, s.A.row_ptr, s.A.col_idx, s.A.val), s.A.nnz);
+      F.A = h->make_matrix(s.A.n_rows, s.A.n_cols, s.A.row_ptr, s.A.col_idx, s.A.val, s.A.nnz);
       I.sell_slots_A[0] = F.A.slots;
     }
     // Coarse factor.
@@ -993,10 +1246,10 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     CK(cudaMemset(h->st, 0, sizeof(PcgState)));
     h->ensure_residuals(1000);
     // Algorithmic bytes and launch counts.
-    // layout_bytes: the same, counting only the matrix words the row
-    // dictionary leaves in HBM (8 B per explicit value, 4 B per explicit column).
+    // layout_bytes: the same, counting only the matrix words the device
+    // layout leaves in HBM (row dictionary / pattern SELL).
     auto layout_spmv = [](const DevSell& M, int64_t nr, int64_t nin, bool resid) {
-      return 8 * M.explicit_vals + 4 * M.explicit_cols + 4 * nr + 8 * nin + 8 * nr + (resid ? 8 * nr : 0);
+      return M.layout_matrix_bytes() + 8 * nin + 8 * nr + (resid ? 8 * nr : 0);
     };
     int64_t vc = 0, vcl = 0;
     int kv = 1;  // coarse

@@ -20,7 +20,8 @@ def main():
     opt = int(sys.argv[1])
     vals = [int(v) for v in sys.argv[2].split(",")]
     wls = sys.argv[3].split(",") if len(sys.argv) > 3 else ["c4"]
-    mk = {"c1": configs.c1, "c2": lambda: configs.c2(2, configs.c2_seed()), "c3": configs.c3, "c4": configs.c4}
+    mk = {"c1": configs.c1, "c2": lambda: configs.c2(2, configs.c2_seed()), "c3": configs.c3, "c4": configs.c4,
+          "c5": configs.c5}
     vp = C.c_void_p
     for wl in wls:
         case = build_case(mk[wl]())
@@ -42,11 +43,14 @@ def main():
                 torch.cuda.synchronize()
                 return e0.elapsed_time(e1) / n
 
+            L = h.info.n_levels
+            ts = timeit(lambda: lib.ig_level_spmv_device(h.handle, L - 1, vp(db.data_ptr()), vp(dx.data_ptr()), 0), 20)
             tv = timeit(lambda: lib.ig_vcycle_device(h.handle, vp(db.data_ptr()), vp(dx.data_ptr())), 20)
             tp = timeit(lambda: lib.ig_pcg_device(h.handle, vp(db.data_ptr()), 1e-8, 1000, vp(dx.data_ptr())), 3)
             it = C.c_int32()
             lib.ig_pcg_result(h.handle, None, C.byref(it))
-            print(f"{wl} option {opt}={v}: vcycle {tv * 1e3:8.1f} us  pcg {tp:8.3f} ms  iters {it.value}", flush=True)
+            print(f"{wl} option {opt}={v}: spmv {ts * 1e3:7.1f} us ({h.info.bytes_spmv_finest_layout / 1e6:.0f} MB layout)"
+                  f"  vcycle {tv * 1e3:8.1f} us  pcg {tp:8.3f} ms  iters {it.value}", flush=True)
             h.close()
             torch.cuda.synchronize()
 

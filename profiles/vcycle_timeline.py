@@ -16,7 +16,8 @@ def main():
 
     from paper_1903_10977_b200 import MgHierarchy, _ffi, build_case, configs
     wl = sys.argv[1] if len(sys.argv) > 1 else "c4"
-    mk = {"c1": configs.c1, "c2": lambda: configs.c2(2, configs.c2_seed()), "c3": configs.c3, "c4": configs.c4}
+    mk = {"c1": configs.c1, "c2": lambda: configs.c2(2, configs.c2_seed()), "c3": configs.c3, "c4": configs.c4,
+          "c5": configs.c5}
     lib = _ffi.gpu()
     case = build_case(mk[wl]())
     h = MgHierarchy(case)
