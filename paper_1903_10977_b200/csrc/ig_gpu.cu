@@ -199,15 +199,18 @@ HostSell to_sell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col,
 // Host image of spmv_psell.cuh's PSell.  See that header for the layout.
 int g_use_psell = 1;
 constexpr int kPDictEntries = 32;
+constexpr int kPMinRun = 8;  // shorter runs of identical rows go to GENERAL slices
 
 struct HostPSell {
   std::vector<PSliceMeta> meta;
-  std::vector<uint32_t> rowinfo;
+  std::vector<int32_t> rlist;
+  std::vector<uint32_t> ginfo;
   std::vector<double> V;
   std::vector<int32_t> O;
-  int32_t dict_w = 1;
-  int64_t layout_bytes = 0;  // matrix words read from HBM per product (sequences shared by slices once)
-  int64_t n_fast = 0, n_general = 0;
+  int32_t dict_w = 2;
+  int32_t smul = 1, sshift = 0;
+  int64_t layout_bytes = 0;  // matrix words read from HBM per product (shared sequences once)
+  int64_t n_fast = 0, n_general = 0, fast_rows = 0;
 };
 
 inline uint64_t mix64(uint64_t h, uint64_t w) {
@@ -217,36 +220,71 @@ inline uint64_t mix64(uint64_t h, uint64_t w) {
 
 // Returns false when the matrix does not fit the format (row longer than
 // kPMaxLen, pools beyond 2^32 entries); the caller keeps the plain SELL.
-bool to_psell(int32_t nr, const int32_t* ptr, const int32_t* col, const double* val, HostPSell& s) {
+bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, const double* val, HostPSell& s) {
   auto len = [&](int32_t i) { return ptr[i + 1] - ptr[i]; };
   for (int32_t i = 0; i < nr; ++i)
     if (len(i) > kPMaxLen) return false;
+  // Offset base per matrix: the scale (1, 2 or 1/2 of the row index) under
+  // which the column-offset sequences repeat most (A: 1, R: 2, P: 1/2).
   std::vector<uint64_t> hv(static_cast<size_t>(nr)), ho(static_cast<size_t>(nr));
   for (int32_t i = 0; i < nr; ++i) {
-    uint64_t a = static_cast<uint64_t>(len(i)), b = a;
+    uint64_t a = static_cast<uint64_t>(len(i));
     for (int32_t k = ptr[i]; k < ptr[i + 1]; ++k) {
       uint64_t w;
       std::memcpy(&w, val + k, 8);
       a = mix64(a, w);
-      b = mix64(b, static_cast<uint64_t>(static_cast<int64_t>(col[k]) - i));
     }
     hv[i] = a;
-    ho[i] = b;
   }
+  const int cand[3][2] = {{1, 0}, {2, 0}, {1, 1}};
+  size_t best_runs = SIZE_MAX;
+  std::vector<uint64_t> hcur(static_cast<size_t>(nr));
+  for (const auto& c : cand) {
+    if (c[0] == 2 && nc < nr) continue;  // scaling up only for wide (restriction-shaped) matrices
+    if (c[1] == 1 && nc > nr) continue;
+    for (int32_t i = 0; i < nr; ++i) {
+      const int64_t b = (static_cast<int64_t>(i) * c[0]) >> c[1];
+      uint64_t h = static_cast<uint64_t>(len(i));
+      for (int32_t k = ptr[i]; k < ptr[i + 1]; ++k) h = mix64(h, static_cast<uint64_t>(col[k] - b));
+      hcur[i] = h;
+    }
+    size_t runs = 0;  // consecutive-row changes of (values, offsets)
+    for (int32_t i = 1; i < nr; ++i) runs += (hv[i] != hv[i - 1] || hcur[i] != hcur[i - 1]) ? 1 : 0;
+    if (runs < best_runs) {
+      best_runs = runs;
+      s.smul = c[0];
+      s.sshift = c[1];
+      ho.swap(hcur);
+      hcur.resize(static_cast<size_t>(nr));
+    }
+  }
+  auto base = [&](int32_t i) { return static_cast<int32_t>((static_cast<int64_t>(i) * s.smul) >> s.sshift); };
   auto veq = [&](int32_t a, int32_t b) {
     return len(a) == len(b) && std::memcmp(val + ptr[a], val + ptr[b], sizeof(double) * len(a)) == 0;
   };
   auto oeq = [&](int32_t a, int32_t b) {
     if (len(a) != len(b)) return false;
+    const int32_t ba = base(a), bb = base(b);
     for (int32_t k = 0; k < len(a); ++k)
-      if (col[ptr[a] + k] - a != col[ptr[b] + k] - b) return false;
+      if (col[ptr[a] + k] - ba != col[ptr[b] + k] - bb) return false;
     return true;
   };
-  // Global value dictionary: the most frequent sequences (>= 32 rows each).
+  // Runs of identical consecutive rows.
+  std::vector<int32_t> run_start;
+  for (int32_t i = 0; i < nr; ++i)
+    if (i == 0 || hv[i] != hv[i - 1] || ho[i] != ho[i - 1] || !veq(i, i - 1) || !oeq(i, i - 1)) run_start.push_back(i);
+  run_start.push_back(nr);
+  std::vector<uint8_t> in_fast(static_cast<size_t>(nr), 0);
+  for (size_t r = 0; r + 1 < run_start.size(); ++r)
+    if (run_start[r + 1] - run_start[r] >= kPMinRun)
+      for (int32_t i = run_start[r]; i < run_start[r + 1]; ++i) in_fast[i] = 1;
+  // Global value dictionary (GENERAL rows): the most frequent sequences among
+  // the rows left to GENERAL slices, >= 32 rows each.
   std::vector<int32_t> dict_rows;
   {
-    std::vector<std::pair<uint64_t, int32_t>> keys(static_cast<size_t>(nr));
-    for (int32_t i = 0; i < nr; ++i) keys[i] = {hv[i], i};
+    std::vector<std::pair<uint64_t, int32_t>> keys;
+    for (int32_t i = 0; i < nr; ++i)
+      if (!in_fast[i]) keys.push_back({hv[i], i});
     std::sort(keys.begin(), keys.end());
     std::vector<std::pair<int64_t, int32_t>> groups;
     for (size_t a = 0; a < keys.size();) {
@@ -265,8 +303,9 @@ bool to_psell(int32_t nr, const int32_t* ptr, const int32_t* col, const double* 
       dict_rows.push_back(g.second);
     }
   }
-  int32_t W = 1;
+  int32_t W = 2;
   for (int32_t r : dict_rows) W = std::max(W, len(r));
+  W = (W + 1) & ~1;  // entries 16-byte aligned (double2 loads)
   s.dict_w = W;
   s.V.assign(static_cast<size_t>(W) * dict_rows.size(), 0.0);
   for (size_t e = 0; e < dict_rows.size(); ++e)
@@ -277,12 +316,13 @@ bool to_psell(int32_t nr, const int32_t* ptr, const int32_t* col, const double* 
       if (hv[i] == hv[dict_rows[e]] && veq(i, dict_rows[e])) return static_cast<int>(e) + 1;
     return 0;
   };
-  // Deduplicated stride-1 sequences of FAST slices.
+  // Deduplicated stride-1 sequences of FAST slices (16-byte aligned starts).
   std::unordered_map<uint64_t, std::vector<std::pair<uint32_t, int32_t>>> vseq, oseq;  // hash -> (start, row)
   auto v_start = [&](int32_t i) -> uint32_t {
     auto& b = vseq[hv[i]];
     for (const auto& [st, r] : b)
       if (veq(i, r)) return st;
+    s.V.resize((s.V.size() + 1) & ~size_t(1), 0.0);
     const uint32_t st = static_cast<uint32_t>(s.V.size());
     s.V.insert(s.V.end(), val + ptr[i], val + ptr[i + 1]);
     s.layout_bytes += 8 * static_cast<int64_t>(len(i));
@@ -293,96 +333,119 @@ bool to_psell(int32_t nr, const int32_t* ptr, const int32_t* col, const double* 
     auto& b = oseq[ho[i]];
     for (const auto& [st, r] : b)
       if (oeq(i, r)) return st;
+    s.O.resize((s.O.size() + 3) & ~size_t(3), 0);
     const uint32_t st = static_cast<uint32_t>(s.O.size());
-    for (int32_t k = ptr[i]; k < ptr[i + 1]; ++k) s.O.push_back(col[k] - i);
+    for (int32_t k = ptr[i]; k < ptr[i + 1]; ++k) s.O.push_back(col[k] - base(i));
     s.layout_bytes += 4 * static_cast<int64_t>(len(i));
     b.push_back({st, i});
     return st;
   };
-  const int32_t nslice = (nr + kSell - 1) / kSell;
-  const int32_t nslice_pad = static_cast<int32_t>((static_cast<int64_t>(nr) + kCta - 1) / kCta) * (kCta / kSell);
-  s.meta.assign(static_cast<size_t>(std::max(nslice_pad, 1)), PSliceMeta{0, 0, 0, 0, 0, 0});
-  s.rowinfo.assign(static_cast<size_t>(std::max(nr, 1)), 0u);
+  auto pack = [](int lmax, int count, bool fast, bool ulen, int wv, int wo) {
+    return static_cast<uint32_t>(lmax) | static_cast<uint32_t>(count) << 11 | (fast ? 1u << 17 : 0u) |
+           (ulen ? 1u << 18 : 0u) | static_cast<uint32_t>(wv) << 19 | static_cast<uint32_t>(wo) << 25;
+  };
   int lmax_all = 0;
-  for (int32_t sl = 0; sl < nslice; ++sl) {
-    const int32_t r0 = sl * kSell, r1 = std::min(nr, r0 + kSell);
-    PSliceMeta m{0, 0, 0, 0, 0, 0};
+  // GENERAL slice over the leftover rows g[0..cnt).
+  auto emit_general = [&](const std::vector<int32_t>& g) {
+    const int cnt = static_cast<int>(g.size());
     int lmax = 0;
-    bool ulen = r1 - r0 == kSell;
-    for (int32_t i = r0; i < r1; ++i) {
+    bool ulen = true;
+    for (int32_t i : g) {
       lmax = std::max(lmax, len(i));
-      ulen = ulen && len(i) == len(r0);
+      ulen = ulen && len(i) == len(g[0]);
     }
     lmax_all = std::max(lmax_all, lmax);
-    m.lmax = static_cast<uint16_t>(lmax);
-    bool fast = ulen;
-    for (int32_t i = r0 + 1; fast && i < r1; ++i)
-      fast = hv[i] == hv[r0] && ho[i] == ho[r0] && veq(i, r0) && oeq(i, r0);
-    if (fast) {
-      const int e = dict_of(r0);
-      m.vbase = e ? static_cast<uint32_t>((e - 1) * W) : v_start(r0);
-      m.obase = o_start(r0);
-      m.flags = kPFast;
-      s.layout_bytes += 16;
-      ++s.n_fast;
-    } else {
-      std::vector<int32_t> opat, vpat;  // representative rows of the table columns
-      std::vector<uint32_t> info(static_cast<size_t>(r1 - r0));
-      for (int32_t i = r0; i < r1; ++i) {
-        int oi = -1;
-        for (size_t j = 0; j < opat.size(); ++j)
-          if (ho[i] == ho[opat[j]] && oeq(i, opat[j])) {
-            oi = static_cast<int>(j);
+    std::vector<int32_t> opat, vpat;  // representative rows of the table columns
+    const uint32_t a = static_cast<uint32_t>(s.rlist.size());
+    for (int32_t i : g) {
+      int oi = -1;
+      for (size_t j = 0; j < opat.size(); ++j)
+        if (ho[i] == ho[opat[j]] && oeq(i, opat[j])) {
+          oi = static_cast<int>(j);
+          break;
+        }
+      if (oi < 0) {
+        oi = static_cast<int>(opat.size());
+        opat.push_back(i);
+      }
+      const int e = dict_of(i);
+      int vi = 0;
+      if (!e) {
+        vi = -1;
+        for (size_t j = 0; j < vpat.size(); ++j)
+          if (hv[i] == hv[vpat[j]] && veq(i, vpat[j])) {
+            vi = static_cast<int>(j);
             break;
           }
-        if (oi < 0) {
-          oi = static_cast<int>(opat.size());
-          opat.push_back(i);
+        if (vi < 0) {
+          vi = static_cast<int>(vpat.size());
+          vpat.push_back(i);
         }
-        const int e = dict_of(i);
-        int vi = 0;
-        if (!e) {
-          vi = -1;
-          for (size_t j = 0; j < vpat.size(); ++j)
-            if (hv[i] == hv[vpat[j]] && veq(i, vpat[j])) {
-              vi = static_cast<int>(j);
-              break;
-            }
-          if (vi < 0) {
-            vi = static_cast<int>(vpat.size());
-            vpat.push_back(i);
-          }
-        }
-        info[i - r0] = static_cast<uint32_t>(len(i)) | static_cast<uint32_t>(e) << 11 |
-                       static_cast<uint32_t>(vi) << 17 | static_cast<uint32_t>(oi) << 22;
       }
-      const int wo = static_cast<int>(opat.size()), wv = static_cast<int>(vpat.size());
-      m.wo = static_cast<uint8_t>(wo);
-      m.wv = static_cast<uint8_t>(wv);
-      m.obase = static_cast<uint32_t>(s.O.size());
-      s.O.resize(s.O.size() + static_cast<size_t>(lmax) * wo, 0);
-      for (int j = 0; j < wo; ++j) {
-        const int32_t r = opat[j];
-        for (int32_t k = 0; k < len(r); ++k) s.O[m.obase + static_cast<size_t>(k) * wo + j] = col[ptr[r] + k] - r;
-      }
-      m.vbase = static_cast<uint32_t>(s.V.size());
-      s.V.resize(s.V.size() + static_cast<size_t>(lmax) * wv, 0.0);
-      for (int j = 0; j < wv; ++j) {
-        const int32_t r = vpat[j];
-        for (int32_t k = 0; k < len(r); ++k) s.V[m.vbase + static_cast<size_t>(k) * wv + j] = val[ptr[r] + k];
-      }
-      for (int32_t i = r0; i < r1; ++i) s.rowinfo[i] = info[i - r0];
-      m.flags = ulen ? kPUlen : 0u;
-      s.layout_bytes += 16 + 4 * static_cast<int64_t>(r1 - r0) + static_cast<int64_t>(lmax) * (4 * wo + 8 * wv);
-      ++s.n_general;
+      s.rlist.push_back(i);
+      s.ginfo.push_back(static_cast<uint32_t>(len(i)) | static_cast<uint32_t>(e) << 11 |
+                        static_cast<uint32_t>(vi) << 17 | static_cast<uint32_t>(oi) << 22);
     }
-    s.meta[sl] = m;
+    const int wo = static_cast<int>(opat.size()), wv = static_cast<int>(vpat.size());
+    // k-blocked tables, zero-padded to a multiple of 8 entries.
+    const size_t l8 = static_cast<size_t>((lmax + 7) & ~7);
+    s.O.resize((s.O.size() + 3) & ~size_t(3), 0);
+    const uint32_t obase = static_cast<uint32_t>(s.O.size());
+    s.O.resize(s.O.size() + l8 * wo, 0);
+    for (int j = 0; j < wo; ++j) {
+      const int32_t r = opat[j];
+      for (int32_t k = 0; k < len(r); ++k)
+        s.O[obase + (k / 4) * 4 * static_cast<size_t>(wo) + 4 * j + k % 4] = col[ptr[r] + k] - base(r);
+    }
+    s.V.resize((s.V.size() + 1) & ~size_t(1), 0.0);
+    const uint32_t vbase = static_cast<uint32_t>(s.V.size());
+    s.V.resize(s.V.size() + l8 * wv, 0.0);
+    for (int j = 0; j < wv; ++j) {
+      const int32_t r = vpat[j];
+      for (int32_t k = 0; k < len(r); ++k)
+        s.V[vbase + (k / 2) * 2 * static_cast<size_t>(wv) + 2 * j + k % 2] = val[ptr[r] + k];
+    }
+    s.meta.push_back(PSliceMeta{a, vbase, obase, pack(lmax, cnt, false, ulen, wv, wo)});
+    s.layout_bytes += 16 + 8 * static_cast<int64_t>(cnt) + static_cast<int64_t>(l8) * (4 * wo + 8 * wv);
+    ++s.n_general;
+  };
+  // Slices in row order: FAST pieces of the long runs; leftover rows are
+  // collected 32 at a time into GENERAL slices.
+  std::vector<int32_t> pending;
+  for (size_t r = 0; r + 1 < run_start.size(); ++r) {
+    const int32_t r0 = run_start[r], r1 = run_start[r + 1];
+    if (r1 - r0 < kPMinRun) {
+      for (int32_t i = r0; i < r1; ++i) {
+        pending.push_back(i);
+        if (pending.size() == 32) {
+          emit_general(pending);
+          pending.clear();
+        }
+      }
+      continue;
+    }
+    lmax_all = std::max(lmax_all, len(r0));
+    const uint32_t vb = v_start(r0), ob = o_start(r0);
+    for (int32_t i = r0; i < r1; i += 32) {
+      const int cnt = std::min(32, r1 - i);
+      s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, ob, pack(len(r0), cnt, true, true, 0, 0)});
+      s.layout_bytes += 16;
+      ++s.n_fast;
+      s.fast_rows += cnt;
+    }
     if (s.V.size() > 0xF0000000ull || s.O.size() > 0xF0000000ull) return false;
   }
-  // Padding: dictionary rows read up to lmax past their start; the last
-  // slice's table columns are read by the out-of-range lanes.
-  s.V.resize(s.V.size() + static_cast<size_t>(lmax_all) + 8, 0.0);
-  s.O.resize(s.O.size() + static_cast<size_t>(lmax_all) + 8, 0);
+  if (!pending.empty()) emit_general(pending);
+  if (s.V.size() > 0xF0000000ull || s.O.size() > 0xF0000000ull) return false;
+  // Pad to whole CTAs (count 0 = empty slice); dictionary rows of GENERAL
+  // slices read up to the slice's padded length past their start.
+  while (s.meta.size() % (kCta / 32) != 0 || s.meta.empty()) s.meta.push_back(PSliceMeta{0, 0, 0, 0});
+  s.V.resize(s.V.size() + static_cast<size_t>(lmax_all) + 16, 0.0);
+  s.O.resize(s.O.size() + static_cast<size_t>(lmax_all) + 16, 0);
+  if (s.rlist.empty()) {
+    s.rlist.push_back(0);
+    s.ginfo.push_back(0);
+  }
   return true;
 }
 
@@ -584,7 +647,7 @@ struct ig_hier {
   DevSell make_matrix(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, const double* val, int64_t nnz) {
     if (g_use_psell && nr > g_small_rows) {
       HostPSell hp;
-      if (to_psell(nr, ptr, col, val, hp)) {
+      if (to_psell(nr, nc, ptr, col, val, hp)) {
         DevSell d;
         d.s.n_rows = nr;
         d.s.n_cols = nc;
@@ -592,8 +655,12 @@ struct ig_hier {
         d.has_p = true;
         d.p.n_rows = nr;
         d.p.n_cols = nc;
+        d.p.n_slices = static_cast<int32_t>(hp.meta.size());
         d.p.meta = upload(hp.meta.data(), hp.meta.size());
-        d.p.rowinfo = upload(hp.rowinfo.data(), hp.rowinfo.size());
+        d.p.rlist = upload(hp.rlist.data(), hp.rlist.size());
+        d.p.ginfo = upload(hp.ginfo.data(), hp.ginfo.size());
+        d.p.smul = hp.smul;
+        d.p.sshift = hp.sshift;
         d.p.V = upload(hp.V.data(), hp.V.size());
         d.p.O = upload(hp.O.data(), hp.O.size());
         d.p.dict_w = hp.dict_w;
@@ -636,17 +703,19 @@ struct ig_hier {
     const unsigned g = grid_of(A.s.n_rows);
     if (g == 0) return;
     if (A.has_p) {
-      if (red) {
-        if (A.stream) k_pspmv<0, true, true><<<g, kCta, 0, stream>>>(A.p, x, y, rsrc, s, partials);
-        else k_pspmv<0, false, true><<<g, kCta, 0, stream>>>(A.p, x, y, rsrc, s, partials);
-      } else if (mode == 0) {
-        if (A.stream) k_pspmv<0, true, false><<<g, kCta, 0, stream>>>(A.p, x, y, rsrc, s, partials);
-        else k_pspmv<0, false, false><<<g, kCta, 0, stream>>>(A.p, x, y, rsrc, s, partials);
+      const unsigned gp = static_cast<unsigned>(A.p.n_slices / (kCta / 32));
+      if (mode == 0) {
+        if (A.stream) k_pspmv<0, true><<<gp, kCta, 0, stream>>>(A.p, x, y, rsrc, s);
+        else k_pspmv<0, false><<<gp, kCta, 0, stream>>>(A.p, x, y, rsrc, s);
       } else {
-        if (A.stream) k_pspmv<1, true, false><<<g, kCta, 0, stream>>>(A.p, x, y, rsrc, s, partials);
-        else k_pspmv<1, false, false><<<g, kCta, 0, stream>>>(A.p, x, y, rsrc, s, partials);
+        if (A.stream) k_pspmv<1, true><<<gp, kCta, 0, stream>>>(A.p, x, y, rsrc, s);
+        else k_pspmv<1, false><<<gp, kCta, 0, stream>>>(A.p, x, y, rsrc, s);
       }
       CK(cudaGetLastError());
+      if (red) {  // p . Ap over the canonical chunks, alpha / Breakdown
+        k_pap<<<g, kCta, 0, stream>>>(A.s.n_rows, x, y, s, partials);
+        CK(cudaGetLastError());
+      }
       return;
     }
     if (A.has_t && g_tsell_kernel == 0) {  // large matrix: compact SELL, thread per row
@@ -700,8 +769,9 @@ struct ig_hier {
   void prolong(const Level& l, const double* xc, double* x, PcgState* s) {
     const unsigned g = grid_of(l.P.s.n_rows);
     if (l.P.has_p) {
-      if (l.P.stream) k_pprolong<true><<<g, kCta, 0, stream>>>(l.P.p, xc, l.cor, x, s);
-      else k_pprolong<false><<<g, kCta, 0, stream>>>(l.P.p, xc, l.cor, x, s);
+      const unsigned gp = static_cast<unsigned>(l.P.p.n_slices / (kCta / 32));
+      if (l.P.stream) k_pprolong<true><<<gp, kCta, 0, stream>>>(l.P.p, xc, l.cor, x, s);
+      else k_pprolong<false><<<gp, kCta, 0, stream>>>(l.P.p, xc, l.cor, x, s);
       CK(cudaGetLastError());
       return;
     }
@@ -747,10 +817,15 @@ struct ig_hier {
     CK(cudaGetLastError());
   }
   void coarse_launch(bool sm, const double* r, double* x, PcgState* s) {
-    if (sm)
-      k_coarse<true><<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, s);
+    const bool big = coarse_threads > 256;
+    if (sm && !big)
+      k_coarse<true, false><<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, s);
+    else if (sm)
+      k_coarse<true, true><<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, s);
+    else if (!big)
+      k_coarse<false, false><<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, s);
     else
-      k_coarse<false><<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, s);
+      k_coarse<false, true><<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, s);
   }
   void coarse(const double* r, double* x, PcgState* s) {
     coarse_launch(coarse_use_smem != 0, r, x, s);
@@ -1218,8 +1293,8 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     h->Lp = h->upload(packed.data(), packed.size());
     h->piv = h->upload(coarse->piv, static_cast<size_t>(n0));
     h->coarse_threads = static_cast<int>(std::max<int64_t>(32, (rk + 31) / 32 * 32));  // one row per thread
-    // [packed L11][y: rank doubles][flags: rank ints]
-    const size_t smem = sizeof(double) * static_cast<size_t>(np_al + rk + 1) + sizeof(int) * static_cast<size_t>(rk + 1);
+    // [packed L11][forward results: rank][backward results: rank]
+    const size_t smem = sizeof(double) * static_cast<size_t>(np_al + 2 * rk + 2);
     int max_optin = 0;
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
     const int dyn_cap = max_optin - 1024;  // headroom for the kernel's static shared memory
@@ -1228,10 +1303,11 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       h->coarse_smem = smem;
       // Process-wide function attributes: raised to the cap once so no handle
       // created later can shrink them below another handle's need.
-      CK(cudaFuncSetAttribute(k_coarse<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_cap));
+      CK(cudaFuncSetAttribute(k_coarse<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_cap));
+      CK(cudaFuncSetAttribute(k_coarse<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_cap));
     } else {
       h->coarse_use_smem = 0;
-      h->coarse_smem = sizeof(double) * static_cast<size_t>(rk + 1) + sizeof(int) * static_cast<size_t>(rk + 1);
+      h->coarse_smem = sizeof(double) * static_cast<size_t>(2 * rk + 2);
     }
     // PCG workspace.
     const int32_t nf = F.n;
@@ -1280,7 +1356,7 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     I.explicit_cols_A[n_levels - 1] = F.A.explicit_cols;
     I.bytes_pcg_iter = vc + I.bytes_spmv_finest + 80 * static_cast<int64_t>(nf);
     I.kernels_vcycle = kv;
-    I.kernels_pcg_iter = kv + 3;
+    I.kernels_pcg_iter = kv + 3 + (F.A.has_p ? 1 : 0);  // + k_pap after a pattern-SELL A p
     CK(cudaDeviceSynchronize());
     *out = h.release();
     return IG_OK;

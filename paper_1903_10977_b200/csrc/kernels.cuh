@@ -764,21 +764,44 @@ __device__ __forceinline__ void bulk_copy_to_smem(double* dst, const double* src
 
 // Pipelined multi-warp substitution: warp w owns rows 32w..32w+31 (one per
 // lane).  Within a block the chain runs by shuffles; across blocks, finished
-// rows are published in shared memory with a per-row flag, and later warps
-// apply those columns while earlier blocks are still solving, so the
-// critical path is ~rank x (mul + sub + div) instead of rank x CTA barriers.
-template <bool SM>
-__global__ void k_coarse(int32_t n, int32_t rank, const double* __restrict__ Lp,
-                         const int32_t* __restrict__ piv, const double* __restrict__ r, double* x,
-                         const PcgState* st) {
+// rows are published in shared memory and later warps apply those columns
+// while earlier blocks are still solving, so the critical path is
+// ~rank x (div + shuffle + mul + sub) instead of rank x CTA barriers.
+// Publication is the value itself: the slots start as a signalling-NaN
+// sentinel that no arithmetic result can equal (IEEE operations return quiet
+// NaNs), and a 64-bit shared store is single-copy atomic, so readers spin on
+// the slot and no fence sits on the chain.  (A variant where every lane of
+// the owning warp solves the whole block redundantly, with no shuffle on the
+// chain, measured 2x slower: the 31-t updates per step are then issued by one
+// warp in order ahead of the next division.)
+constexpr unsigned long long kCoarseSentinel = 0x7FF4C0A45E5E0001ull;
+
+__device__ __forceinline__ double wait_slot(const volatile double* p) {
+  unsigned long long v;
+  do {
+    v = static_cast<unsigned long long>(__double_as_longlong(*p));
+  } while (v == kCoarseSentinel);
+  return __longlong_as_double(static_cast<long long>(v));
+}
+
+// BIG: ranks above 256 (up to 1024 threads).
+template <bool SM, bool BIG = false>
+__global__ void __launch_bounds__(BIG ? 1024 : 256, 1) k_coarse(int32_t n, int32_t rank, const double* __restrict__ Lp,
+                                                               const int32_t* __restrict__ piv,
+                                                               const double* __restrict__ r, double* x,
+                                                               const PcgState* st) {
   if (pcg_done(st)) return;
   extern __shared__ __align__(16) double smem[];
   __shared__ unsigned long long mbar;
   const int64_t np = static_cast<int64_t>(rank) * (rank + 1) / 2;
   const int64_t np_al = (np + 1) & ~int64_t(1);  // 16-byte aligned region
-  volatile double* ysh = smem + (SM ? np_al : 0);
-  volatile int* flag = reinterpret_cast<volatile int*>(smem + (SM ? np_al : 0) + rank);
-  for (int k = threadIdx.x; k < rank; k += blockDim.x) flag[k] = 0;
+  volatile double* yf = smem + (SM ? np_al : 0);  // forward results
+  volatile double* yb = yf + rank;                 // backward results
+  const double sent = __longlong_as_double(static_cast<long long>(kCoarseSentinel));
+  for (int k = threadIdx.x; k < rank; k += blockDim.x) {
+    yf[k] = sent;
+    yb[k] = sent;
+  }
   if (SM && np > 0)
     bulk_copy_to_smem(smem, Lp, static_cast<size_t>(np_al) * sizeof(double), &mbar);  // has a barrier
   else
@@ -794,48 +817,63 @@ __global__ void k_coarse(int32_t n, int32_t rank, const double* __restrict__ Lp,
   double y = own ? r[piv[i] - 1] : 0.0;
   const double dg = own ? L[oi + i] : 1.0;  // own pivot L(i, i)
   const double rdg = safe_rcp(dg);
+  // Fast path (every pivot of the warp has a usable reciprocal): branch-free
+  // steps -- every lane forms the quotient, the shuffle picks the owner's,
+  // selects keep each lane's own operation sequence exactly the oracle's.
+  const bool fast = __all_sync(0xffffffffu, !own || (isfinite(rdg) && rdg != 0.0));
   // ---- forward: y_j = y_j / L_jj ; y_i -= L_ij y_j (i > j), j ascending ----
   // Columns of earlier blocks: consumed as their owners publish them.
   int oj = 0;  // off(j)
   for (int j = 0; j < b0; ++j) {
-    while (flag[j] == 0) {
-    }
-    __threadfence_block();
-    const double yj = ysh[j];
+    const double yj = wait_slot(yf + j);
     if (own) y = y - L[oj + i] * yj;
     oj += rank - j - 1;
   }
-  // Own block: the owner of row j divides, publishes, and hands y_j to the
-  // warp by shuffle.
-  for (int j = b0; j < bend; ++j) {
-    if (i == j) {
-      y = div_rb(y, dg, rdg);
-      ysh[j] = y;
-      __threadfence_block();
-      flag[j] = 1;
+  // Own block: the owner of row j divides and hands y_j to the warp by
+  // shuffle; the shared-memory publication for later warps is off the chain.
+  if (fast) {
+    for (int j = b0; j < bend; ++j) {
+      const double q = exact_div(y, dg, rdg);
+      const double yj = __shfl_sync(0xffffffffu, q, j - b0);
+      const double lij = L[oj + (own ? i : j)];
+      const double upd = y - lij * yj;
+      y = (i == j) ? yj : ((own && i > j) ? upd : y);
+      if (i == j) yf[j] = yj;
+      oj += rank - j - 1;
     }
-    const double yj = __shfl_sync(0xffffffffu, y, j - b0);
-    if (own && i > j) y = y - L[oj + i] * yj;
-    oj += rank - j - 1;
+  } else {
+    for (int j = b0; j < bend; ++j) {
+      if (i == j) y = div_rb(y, dg, rdg);
+      const double yj = __shfl_sync(0xffffffffu, y, j - b0);
+      if (i == j) yf[j] = yj;
+      if (own && i > j) y = y - L[oj + i] * yj;
+      oj += rank - j - 1;
+    }
   }
   // ---- backward: y_i = (y_i - sum_{k desc > i} L_ki y_k) / L_ii ----------
   double acc = 0.0;
   for (int k = rank - 1; k >= bend; --k) {
-    while (flag[k] != 2) {
-    }
-    __threadfence_block();
-    const double yk = ysh[k];
+    const double yk = wait_slot(yb + k);
     if (own) acc = acc + L[oi + k] * yk;
   }
-  for (int k = bend - 1; k >= b0; --k) {
-    if (i == k) {
-      y = div_rb(y - acc, dg, rdg);
-      ysh[k] = y;
-      __threadfence_block();
-      flag[k] = 2;
+  if (fast) {
+    for (int k = bend - 1; k >= b0; --k) {
+      const double q = exact_div(y - acc, dg, rdg);
+      const double yk = __shfl_sync(0xffffffffu, q, k - b0);
+      const double nacc = acc + L[oi + k] * yk;
+      if (i == k) {
+        y = yk;
+        yb[k] = yk;
+      }
+      acc = (own && i < k) ? nacc : acc;
     }
-    const double yk = __shfl_sync(0xffffffffu, y, k - b0);
-    if (own && i < k) acc = acc + L[oi + k] * yk;
+  } else {
+    for (int k = bend - 1; k >= b0; --k) {
+      if (i == k) y = div_rb(y - acc, dg, rdg);
+      const double yk = __shfl_sync(0xffffffffu, y, k - b0);
+      if (i == k) yb[k] = yk;
+      if (own && i < k) acc = acc + L[oi + k] * yk;
+    }
   }
   if (own) x[piv[i] - 1] = y;
   for (int k = rank + threadIdx.x; k < n; k += blockDim.x) x[piv[k] - 1] = 0.0;

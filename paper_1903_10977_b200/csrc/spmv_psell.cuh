@@ -2,30 +2,35 @@
 //
 // Why: the row-dictionary SELL (kernels.cuh: Sell) removed most value bytes
 // but the finest C4 SpMV stayed at ~300 us, 57 % issue-busy at 26 SASS
-// instructions per matrix slot (per-lane selects between dictionary and
-// explicit streams, predicated batches) with 4 B of column index per slot
-// still streamed for 56 % of the rows.  The operators of an immersed
-// B-spline discretisation are far more regular than that: 61 % of the 32-row
-// slices of C4's finest level have ONE value sequence, ONE column-offset
-// sequence (col - row) and one length for all 32 rows, and most of the rest
-// have a handful of distinct offset sequences (slices crossing an x-line end).
+// instructions per matrix slot, with 4 B of column index per slot still
+// streamed for 56 % of the rows.  The operators of an immersed B-spline
+// discretisation are far more regular than a general sparse matrix: on C4's
+// finest level 91 % of the rows lie in RUNS of consecutive rows with the same
+// value sequence and the same column-offset sequence (an x-line interior: the
+// typical run is 124 rows); the rest are single rows (line ends, cut cells).
 //
-// Layout, per slice of 32 consecutive rows (one warp):
-//   * FAST slices (all rows: same length, same values, same offsets): the warp
-//     reads one value sequence V[vbase + k] and one offset sequence
-//     O[obase + k] with warp-uniform addresses (one L1 wavefront each, the
-//     sequences deduplicated across the matrix, the most frequent value
-//     sequences shared through the global dictionary at the start of V), and
-//     gathers x[row + o_k] coalesced: 6 instructions per slot, no predication;
-//   * general slices: per-slice column-major tables of the DISTINCT offset
-//     sequences (width wo) and of the distinct non-dictionary value sequences
-//     (width wv); rowinfo[row] selects the row's columns and its value source
-//     (dictionary entry or table column).  Table entries past a row's length
-//     are zero (offset 0 keeps the gather in bounds; the product is never
-//     added).
+// Layout: a list of warp-sized slices, each one warp:
+//   * FAST slice = up to 32 consecutive rows of one run: the warp reads ONE
+//     value sequence V[vbase + k] and ONE offset sequence O[obase + k] with
+//     warp-uniform 16-byte loads (one L1 wavefront per 2 values / 4 offsets;
+//     sequences deduplicated over the matrix) and gathers x[base(row) + o_k]
+//     coalesced -- no per-row matrix bytes at all;
+//   * GENERAL slice = up to 32 leftover rows (in row order): per-slice tables
+//     of their DISTINCT offset sequences (wo columns) and distinct
+//     non-dictionary value sequences (wv columns), k-blocked for vector loads
+//     (offsets [k/4][col][k%4], values [k/2][col][k%2]); ginfo selects each
+//     row's offset column and value source (global dictionary entry at the
+//     start of V, or table column).  Entries past a row's length are zero
+//     (offset 0 keeps the gather in bounds; the product is never added).
+// Offsets are taken against base(row) = (row * smul) >> sshift, chosen per
+// matrix (A: row; restriction R: 2 row -- coarse x-lines map to every other
+// fine column; prolongation P: row / 2) so that runs and tables repeat.
+//
 // The sum is the same serial ascending-k chain as every other SpMV here
 // (Eigen RowMajor order), and values/offsets are stored bit-exactly, so the
-// results are identical to kernels.cuh's k_spmv and to the oracle.
+// results are identical to kernels.cuh's k_spmv and to the oracle.  Slices
+// are not aligned to the 256-row reduction chunks, so p . Ap is reduced by
+// k_pap (same canonical chunk tree) after the product.
 #pragma once
 
 #include <cstdint>
@@ -34,165 +39,149 @@
 
 namespace igk {
 
-constexpr uint32_t kPFast = 1u;  // slice: one length/value/offset sequence for all rows
-constexpr uint32_t kPUlen = 2u;  // slice: all 32 rows have length lmax
-
+// pk: lmax (11 bits) | count << 11 (6) | fast << 17 | ulen << 18 | wv << 19 (6) | wo << 25 (6)
 struct PSliceMeta {
-  uint32_t vbase;  // FAST: start of the value sequence; general: value table
-  uint32_t obase;  // FAST: start of the offset sequence; general: offset table
-  uint16_t lmax;
-  uint8_t wv, wo;  // general: table widths (column-major strides)
-  uint32_t flags;
+  uint32_t a;      // FAST: first row; GENERAL: index of the slice's entries in rlist/ginfo
+  uint32_t vbase;  // FAST: value sequence; GENERAL: value table
+  uint32_t obase;  // FAST: offset sequence; GENERAL: offset table
+  uint32_t pk;
 };
 
-// rowinfo (general slices): len | vsel << 11 | vi << 17 | oi << 22;
-// vsel > 0: values = dictionary entry vsel-1 (V[(vsel-1)*dict_w + k]),
-// vsel = 0: values = table column vi.  oi: offset-table column.
 constexpr int kPLenBits = 11;
 constexpr int kPMaxLen = (1 << kPLenBits) - 1;
-constexpr int kPMaxDict = 63;
 
+// ginfo (GENERAL rows): len | vsel << 11 | vi << 17 | oi << 22; vsel > 0:
+// values = dictionary entry vsel-1 (V[(vsel-1)*dict_w + k]); vsel = 0: table column vi.
 struct PSell {
-  int32_t n_rows, n_cols;
+  int32_t n_rows, n_cols, n_slices;
   const PSliceMeta* meta;
-  const uint32_t* rowinfo;
+  const int32_t* rlist;
+  const uint32_t* ginfo;
   const double* V;
   const int32_t* O;
   int32_t dict_w;
+  int32_t smul, sshift;  // base(row) = (row * smul) >> sshift
 };
 
-__device__ __forceinline__ PSliceMeta load_meta(const PSliceMeta* p) {
-  const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
-  PSliceMeta m;
-  m.vbase = u.x;
-  m.obase = u.y;
-  m.lmax = static_cast<uint16_t>(u.z & 0xffffu);
-  m.wv = static_cast<uint8_t>((u.z >> 16) & 0xffu);
-  m.wo = static_cast<uint8_t>(u.z >> 24);
-  m.flags = u.w;
-  return m;
-}
-
 template <bool STREAM>
-__device__ __forceinline__ int32_t ld_off(const int32_t* p) {
+__device__ __forceinline__ int4 ld_off4(const int4* p) {
   if (STREAM) return __ldcs(p);
   return __ldg(p);
 }
 
-// Row sum of one row of a pattern-SELL matrix (warp = slice; `row` < n_rows
-// for every lane that calls it with a valid row, others pass valid=false and
-// still follow the warp-uniform branches).
+// One warp, one slice.  Returns the row this lane owns (-1: none) and its sum.
 template <bool STREAM>
-__device__ __forceinline__ double psell_row(const PSell& A, int row, bool valid, const double* __restrict__ x) {
-  const PSliceMeta m = load_meta(A.meta + (row >> 5));
-  const double* xr = x + row;
-  double acc = 0.0;
-  constexpr int U = 8;
-  if (m.flags & kPFast) {  // warp-uniform branch
-    const double* vp = A.V + m.vbase;
-    const int32_t* op = A.O + m.obase;
-    const int L = m.lmax;
+__device__ __forceinline__ int psell_slice(const PSell& A, int slice, const double* __restrict__ x, double& acc) {
+  acc = 0.0;
+  const int lane = threadIdx.x & 31;
+  const uint4 mu = __ldg(reinterpret_cast<const uint4*>(A.meta + slice));
+  const uint32_t pk = mu.w;
+  const int count = static_cast<int>((pk >> 11) & 0x3f);
+  if (count == 0) return -1;  // padding slice (warp-uniform)
+  const int L = static_cast<int>(pk & kPMaxLen);
+  const int cl = min(lane, count - 1);  // surplus lanes recompute the last row, store nothing
+  if (pk & (1u << 17)) {                // FAST (warp-uniform branch)
+    const int row = static_cast<int>(mu.x) + cl;
+    const double* xr = x + ((row * A.smul) >> A.sshift);
+    const double* vp = A.V + mu.y;
+    const int32_t* op = A.O + mu.z;
+    const double2* vp2 = reinterpret_cast<const double2*>(vp);
+    const int4* op4 = reinterpret_cast<const int4*>(op);
     int k = 0;
-    for (; k + U <= L; k += U) {
-      double v[U], xv[U];
-      int32_t o[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        v[u] = __ldg(vp + k + u);
-        o[u] = __ldg(op + k + u);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = __ldg(xr + o[u]);
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc = acc + v[u] * xv[u];
+    for (; k + 8 <= L; k += 8) {
+      const double2 a0 = __ldg(vp2 + (k >> 1)), a1 = __ldg(vp2 + (k >> 1) + 1);
+      const double2 a2 = __ldg(vp2 + (k >> 1) + 2), a3 = __ldg(vp2 + (k >> 1) + 3);
+      const int4 b0 = __ldg(op4 + (k >> 2)), b1 = __ldg(op4 + (k >> 2) + 1);
+      const double x0 = __ldg(xr + b0.x), x1 = __ldg(xr + b0.y), x2 = __ldg(xr + b0.z), x3 = __ldg(xr + b0.w);
+      const double x4 = __ldg(xr + b1.x), x5 = __ldg(xr + b1.y), x6 = __ldg(xr + b1.z), x7 = __ldg(xr + b1.w);
+      acc = acc + a0.x * x0;
+      acc = acc + a0.y * x1;
+      acc = acc + a1.x * x2;
+      acc = acc + a1.y * x3;
+      acc = acc + a2.x * x4;
+      acc = acc + a2.y * x5;
+      acc = acc + a3.x * x6;
+      acc = acc + a3.y * x7;
     }
     for (; k < L; ++k) acc = acc + __ldg(vp + k) * __ldg(xr + __ldg(op + k));
-    return acc;
+    return lane < count ? row : -1;
   }
-  const uint32_t info = valid ? __ldg(A.rowinfo + row) : 0u;
+  const int idx = static_cast<int>(mu.x) + cl;
+  const int row = __ldg(A.rlist + idx);
+  const uint32_t info = __ldg(A.ginfo + idx);
   const int len = static_cast<int>(info & kPMaxLen);
   const int vsel = static_cast<int>((info >> 11) & 0x3f);
   const int vi = static_cast<int>((info >> 17) & 0x1f);
   const int oi = static_cast<int>((info >> 22) & 0x1f);
-  const double* vp = vsel ? A.V + static_cast<int64_t>(vsel - 1) * A.dict_w : A.V + m.vbase + vi;
-  const int vs = vsel ? 1 : m.wv;
-  const int32_t* op = A.O + m.obase + oi;
-  const int os = m.wo;
-  const int L = m.lmax;
-  // Out-of-range lanes of the last slice read table column 0 (the slice's
-  // first row): relative to that row, the discarded gathers stay in bounds.
-  if (!valid) xr = x + (row & ~31);
-  if (m.flags & kPUlen) {  // warp-uniform branch: every row has length L
-    int k = 0;
-    for (; k + U <= L; k += U) {
-      double v[U], xv[U];
-      int32_t o[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        v[u] = __ldg(vp + (k + u) * vs);
-        o[u] = ld_off<STREAM>(op + (k + u) * os);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = __ldg(xr + o[u]);
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc = acc + v[u] * xv[u];
-    }
-    for (; k < L; ++k) acc = acc + __ldg(vp + k * vs) * __ldg(xr + ld_off<STREAM>(op + k * os));
-    return acc;
-  }
-  // Mixed lengths: run to the slice maximum, add only k < len.  Entries past
-  // len are zero in the tables; dictionary rows past their length read the
-  // zero padding after the dictionary (V is padded by the host).
+  const int wv = static_cast<int>((pk >> 19) & 0x3f), wo = static_cast<int>((pk >> 25) & 0x3f);
+  const double* xr = x + ((row * A.smul) >> A.sshift);
+  const double2* vp2 = reinterpret_cast<const double2*>(
+      vsel ? A.V + static_cast<int64_t>(vsel - 1) * A.dict_w : A.V + mu.y + 2 * vi);
+  const int vs = vsel ? 1 : wv;  // double2 stride per 2 k
+  const int4* op4 = reinterpret_cast<const int4*>(A.O + mu.z + 4 * oi);
+  const int L8 = (L + 7) & ~7;
+  const int lfull = (pk & (1u << 18)) ? (L & ~7) : 0;  // blocks every row fills
   int k = 0;
-  for (; k + U <= L; k += U) {
-    double v[U], xv[U];
-    int32_t o[U];
+  for (; k < lfull; k += 8) {
+    const double2 a0 = __ldg(vp2 + (k >> 1) * vs), a1 = __ldg(vp2 + ((k >> 1) + 1) * vs);
+    const double2 a2 = __ldg(vp2 + ((k >> 1) + 2) * vs), a3 = __ldg(vp2 + ((k >> 1) + 3) * vs);
+    const int4 b0 = ld_off4<STREAM>(op4 + (k >> 2) * wo), b1 = ld_off4<STREAM>(op4 + ((k >> 2) + 1) * wo);
+    const double x0 = __ldg(xr + b0.x), x1 = __ldg(xr + b0.y), x2 = __ldg(xr + b0.z), x3 = __ldg(xr + b0.w);
+    const double x4 = __ldg(xr + b1.x), x5 = __ldg(xr + b1.y), x6 = __ldg(xr + b1.z), x7 = __ldg(xr + b1.w);
+    acc = acc + a0.x * x0;
+    acc = acc + a0.y * x1;
+    acc = acc + a1.x * x2;
+    acc = acc + a1.y * x3;
+    acc = acc + a2.x * x4;
+    acc = acc + a2.y * x5;
+    acc = acc + a3.x * x6;
+    acc = acc + a3.y * x7;
+  }
+  for (; k < L8; k += 8) {
+    const double2 a0 = __ldg(vp2 + (k >> 1) * vs), a1 = __ldg(vp2 + ((k >> 1) + 1) * vs);
+    const double2 a2 = __ldg(vp2 + ((k >> 1) + 2) * vs), a3 = __ldg(vp2 + ((k >> 1) + 3) * vs);
+    const int4 b0 = ld_off4<STREAM>(op4 + (k >> 2) * wo), b1 = ld_off4<STREAM>(op4 + ((k >> 2) + 1) * wo);
+    const double xv[8] = {__ldg(xr + b0.x), __ldg(xr + b0.y), __ldg(xr + b0.z), __ldg(xr + b0.w),
+                          __ldg(xr + b1.x), __ldg(xr + b1.y), __ldg(xr + b1.z), __ldg(xr + b1.w)};
+    const double av[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      v[u] = __ldg(vp + (k + u) * vs);
-      o[u] = ld_off<STREAM>(op + (k + u) * os);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) xv[u] = __ldg(xr + o[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const double t = acc + v[u] * xv[u];
+    for (int u = 0; u < 8; ++u) {
+      const double t = acc + av[u] * xv[u];
       acc = (k + u < len) ? t : acc;
     }
   }
-  for (; k < L; ++k) {
-    const double t = acc + __ldg(vp + k * vs) * __ldg(xr + ld_off<STREAM>(op + k * os));
-    acc = (k < len) ? t : acc;
-  }
-  return acc;
+  return lane < count ? row : -1;
 }
 
-// MODE 0: y = A x.  MODE 1: y = r - A x (r read from rsrc; in place allowed).
-// RED: p . Ap chunk partials, last CTA -> alpha / Breakdown (as k_spmv).
-template <int MODE, bool STREAM, bool RED>
+// MODE 0: y = A x.  MODE 1: y = r - A x (r read from rsrc; in place allowed:
+// every row is read and written by its own lane only).
+template <int MODE, bool STREAM>
 __global__ void __launch_bounds__(kCta) k_pspmv(PSell A, const double* __restrict__ x, double* y,
-                                               const double* rsrc, PcgState* st, double* partials) {
+                                               const double* rsrc, const PcgState* st) {
+  if (pcg_done(st)) return;
+  const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
+  double acc;
+  const int row = psell_slice<STREAM>(A, slice, x, acc);
+  if (row < 0) return;
+  y[row] = (MODE == 0) ? acc : rsrc[row] - acc;
+}
+
+// p . Ap over the canonical 256-row chunks (kernels.cuh: last_cta_total), then
+// alpha / Breakdown exactly as the fused k_spmv<...,RED> does.
+__global__ void __launch_bounds__(kCta) k_pap(int n, const double* __restrict__ p, const double* __restrict__ ap,
+                                             PcgState* st, double* partials) {
   if (pcg_done(st)) return;
   const int row = blockIdx.x * kCta + threadIdx.x;
-  const bool valid = row < A.n_rows;
-  double prod = 0.0;
-  const double acc = psell_row<STREAM>(A, row, valid, x);
-  if (valid) {
-    const double out = (MODE == 0) ? acc : rsrc[row] - acc;
-    y[row] = out;
-    if (RED) prod = x[row] * out;
-  }
-  if (RED) {
-    double pap;
-    if (last_cta_total(prod, partials, &st->counter[0], &pap)) {
-      if (threadIdx.x == 0) {
-        st->pap = pap;
-        if (pap <= 0.0) {  // solvers.cpp:47-50 (a NaN does not trigger it)
-          st->status = ST_BREAKDOWN;
-          st->done = 1;
-        } else {
-          st->alpha = st->rz / pap;
-        }
+  const double prod = row < n ? p[row] * ap[row] : 0.0;
+  double pap;
+  if (last_cta_total(prod, partials, &st->counter[0], &pap)) {
+    if (threadIdx.x == 0) {
+      st->pap = pap;
+      if (pap <= 0.0) {  // solvers.cpp:47-50 (a NaN does not trigger it)
+        st->status = ST_BREAKDOWN;
+        st->done = 1;
+      } else {
+        st->alpha = st->rz / pap;
       }
     }
   }
@@ -203,10 +192,10 @@ template <bool STREAM>
 __global__ void __launch_bounds__(kCta) k_pprolong(PSell P, const double* __restrict__ xc, double* cor, double* x,
                                                   const PcgState* st) {
   if (pcg_done(st)) return;
-  const int row = blockIdx.x * kCta + threadIdx.x;
-  const bool valid = row < P.n_rows;
-  const double c = psell_row<STREAM>(P, row, valid, xc);
-  if (!valid) return;
+  const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
+  double c;
+  const int row = psell_slice<STREAM>(P, slice, xc, c);
+  if (row < 0) return;
   cor[row] = c;
   x[row] = x[row] + c;
 }
