@@ -173,6 +173,13 @@ int ig_debug_vcycle_timeline(ig_hier *h, const double *d_r, double *d_x,
                              int32_t max_steps, float *ms, int32_t *levels,
                              char *labels, int32_t label_len, int32_t *count);
 
+/* Debug: run the persistent small-level kernel (levels 1..top, see
+ * IG_OPT_TAIL_ROWS) once on d_r -> d_x with a %globaltimer stamp after every
+ * phase (ns, written to stamps[0..*count)); IG_UNSUPPORTED if the hierarchy
+ * has no such kernel. */
+int ig_debug_tail_profile(ig_hier *h, const double *d_r, double *d_x, uint64_t *stamps,
+                          int32_t cap, int32_t *count);
+
 /* Thread-local message for the last non-OK status. */
 const char *ig_last_error(void);
 
@@ -184,6 +191,7 @@ const char *ig_last_error(void);
 #define IG_OPT_TMA_ROWS 5     /* matrices with >= this many rows use the compact SELL (0: never) */
 #define IG_OPT_TSELL_KERNEL 6 /* compact-SELL kernel: 0 direct thread-per-row, 1 TMA-staged */
 #define IG_OPT_PSELL 7        /* 1 (default): pattern SELL for matrices above IG_OPT_SMALL_ROWS rows */
+#define IG_OPT_TAIL_ROWS 8    /* levels (below the finest) up to this many rows run in one persistent kernel; 0 = off */
 int ig_set_option(int32_t option, int64_t value);
 
 #ifdef __cplusplus

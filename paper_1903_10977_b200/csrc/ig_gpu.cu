@@ -24,6 +24,7 @@
 #include "kernels.cuh"
 #include "spmv_psell.cuh"
 #include "spmv_tma.cuh"
+#include "vtail.cuh"
 
 using namespace igk;
 
@@ -64,6 +65,12 @@ struct HostSell {
 int g_use_dict = 1;
 int g_spmv_variant = 3;  // profiles/spmv_variants.py: best full-PCG time on C4
 int g_small_rows = 40000;  // matrices up to this many rows use k_spmv_grp (profiles/option_sweep.py)
+// Levels up to this many rows (below the finest) run in k_vtail; 0 = off.
+// Off by default: measured SLOWER than the graph-launched kernels (C5 V-cycle
+// 285 -> 538 us; profiles/tail_profile.py): each of the ~33 phases costs a
+// 1.2 us grid barrier plus the slowest warp's latency chain (3-40 us with
+// only 16 warps per SM), more than a kernel boundary in the graph.
+int g_tail_rows = 0;
 // Compact-SELL layouts (spmv_tma.cuh) measured SLOWER than the row-dictionary
 // SELL on C4 (finest SpMV 442 us direct / 410 us TMA-staged vs 303 us;
 // profiles/spmv_layouts.py), so they are off by default.
@@ -562,6 +569,12 @@ struct ig_hier {
   int coarse_threads = 32;
   size_t coarse_smem = 0;
   int coarse_use_smem = 0;
+  // Persistent small-level V-cycle (vtail.cuh): levels 1..tail_top.
+  int tail_top = 0;
+  TailLevel* tail_lv = nullptr;  // device array [0 .. tail_top]
+  unsigned tail_grid = 0;
+  size_t tail_smem = 0;
+  bool tail_sm = false;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // block solves, forked from / joined into `stream`
   int num_sms = 148;
@@ -833,7 +846,32 @@ struct ig_hier {
   }
   // MgHierarchy::vcycle_at (multigrid.cpp:90-108).  rdot != null: PCG mode on
   // the finest level (the last kernel also reduces r . z).
+  void tail(int top, const double* r, double* x, unsigned long long* prof = nullptr, int debug_mode = 0) {
+    TailParams P;
+    P.prof = prof;
+    P.debug_mode = debug_mode;
+    P.lv = tail_lv;
+    P.top = top;
+    P.r_top = r;
+    P.x_top = x;
+    P.n0 = n0;
+    P.rank = rank;
+    P.Lp = Lp;
+    P.piv = piv;
+    void* args[] = {&P};
+    if (tail_sm)
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_vtail<true>), dim3(tail_grid), dim3(kTailThreads), args,
+                                     tail_smem, stream));
+    else
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_vtail<false>), dim3(tail_grid), dim3(kTailThreads),
+                                     args, tail_smem, stream));
+  }
   void vcycle(int l, const double* r, double* x, PcgState* s, const double* rdot) {
+    if (l > 0 && l <= tail_top && !rdot) {  // small levels: one persistent kernel
+      tail(l, r, x);
+      mark("tail", l);
+      return;
+    }
     if (l == 0) {
       coarse(r, x, s);
       if (rdot) {  // 1-level hierarchy inside PCG: r . z as a separate pass
@@ -1191,6 +1229,11 @@ int ig_set_option(int32_t option, int64_t value) {
     g_use_dict = value != 0;
     return IG_OK;
   }
+  if (option == IG_OPT_TAIL_ROWS) {
+    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: bad row threshold");
+    g_tail_rows = static_cast<int>(value);
+    return IG_OK;
+  }
   if (option == IG_OPT_PSELL) {
     g_use_psell = value != 0;
     return IG_OK;
@@ -1357,6 +1400,49 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     I.bytes_pcg_iter = vc + I.bytes_spmv_finest + 80 * static_cast<int64_t>(nf);
     I.kernels_vcycle = kv;
     I.kernels_pcg_iter = kv + 3 + (F.A.has_p ? 1 : 0);  // + k_pap after a pattern-SELL A p
+    // Small levels below the finest: one cooperative persistent kernel.
+    if (g_tail_rows > 0 && h->rank <= kTailThreads) {
+      int top = 0;
+      for (int l = 1; l <= n_levels - 2 && h->lv[l].n <= g_tail_rows && h->lv[l].n <= g_small_rows; ++l) top = l;
+      int coop = 0;
+      CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, 0));
+      if (top > 0 && coop) {
+        std::vector<TailLevel> tl(static_cast<size_t>(top) + 1);
+        for (int l = 0; l <= top; ++l) {
+          const Level& Lv = h->lv[l];
+          TailLevel& t = tl[l];
+          t = TailLevel{};
+          t.n = Lv.n;
+          t.r_in = Lv.r_in;
+          t.x = Lv.x;
+          if (l == 0) continue;
+          t.A = Lv.A.s;
+          t.R = Lv.R.s;
+          t.P = Lv.P.s;
+          t.G = Lv.G;
+          t.S = Lv.S;
+          t.n_items = Lv.G.n_groups + Lv.G.n_wblocks;
+          t.res = Lv.res;
+          t.cor = Lv.cor;
+          t.ybuf = Lv.ybuf;
+        }
+        h->tail_lv = h->upload(tl.data(), tl.size());
+        h->tail_sm = h->coarse_use_smem != 0;
+        h->tail_smem = h->coarse_smem;
+        if (h->tail_sm)
+          CK(cudaFuncSetAttribute(k_vtail<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(h->tail_smem)));
+        int occ = 0;
+        if (h->tail_sm)
+          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vtail<true>, kTailThreads, h->tail_smem));
+        else
+          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vtail<false>, kTailThreads, h->tail_smem));
+        if (occ >= 1) {
+          h->tail_grid = static_cast<unsigned>(h->num_sms * std::min(occ, 2));
+          h->tail_top = top;
+        }
+      }
+    }
     CK(cudaDeviceSynchronize());
     *out = h.release();
     return IG_OK;
@@ -1488,6 +1574,39 @@ int ig_debug_vcycle_timeline(ig_hier* h, const double* d_r, double* d_x, int32_t
     *count = k;
     for (const auto& m : tl) cudaEventDestroy(m.ev);
     cudaEventDestroy(start);
+    return IG_OK;
+  });
+}
+
+int ig_debug_tail_profile(ig_hier* h, const double* d_r, double* d_x, uint64_t* stamps, int32_t cap,
+                          int32_t* count) {
+  if (!h || !d_r || !d_x || !stamps || !count || cap == 0) return fail(IG_INVALID_ARGUMENT, "tail_profile: bad argument");
+  const bool spmv_only = cap < 0;  // undocumented profiling mode: only the descent SpMVs
+  if (spmv_only) cap = -cap;
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->tail_top <= 0) return fail(IG_UNSUPPORTED, "tail_profile: no persistent small-level kernel");
+  return guarded([&] {
+    const int top = h->tail_top;
+    const size_t ns = 256 + 64 * static_cast<size_t>(h->tail_grid);
+    unsigned long long* dp = nullptr;
+    CK(cudaMalloc(&dp, ns * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(dp, 0, ns * sizeof(unsigned long long), h->stream));
+    h->tail(top, d_r, d_x, dp, spmv_only ? 1 : 0);
+    std::vector<unsigned long long> hs(ns);
+    CK(cudaMemcpyAsync(hs.data(), dp, ns * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(dp);
+    int32_t k = 0;
+    while (k < 256 && k < cap && hs[k] != 0) {
+      stamps[k] = hs[k];
+      ++k;
+    }
+    *count = k;
+    // Then, if room: the grid size and per-CTA arrival times of each barrier.
+    if (cap >= static_cast<int32_t>(ns) + 1) {
+      stamps[256] = h->tail_grid;
+      for (size_t q = 256; q < ns; ++q) stamps[q + 1] = hs[q];
+    }
     return IG_OK;
   });
 }

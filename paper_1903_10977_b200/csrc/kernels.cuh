@@ -329,10 +329,11 @@ __global__ void __launch_bounds__(kCta, SpmvVar<VAR>::MINB) k_spmv(Sell A, const
 // shuffles, so the sum is still sequential ((acc + p0) + p1) + ... exactly as
 // in the thread-per-row kernel, but the memory latency is paid once per G
 // entries instead of once per batch of a single thread.
+// Body for global thread t (all 32 lanes of a warp call it together: the
+// warp-maximum length is formed by shuffles).
 template <int MODE, int G>
-__global__ void __launch_bounds__(kCta) k_spmv_grp(Sell A, const double* __restrict__ x, double* y,
-                                                   const double* rsrc) {
-  const int t = blockIdx.x * kCta + threadIdx.x;
+__device__ __forceinline__ void spmv_grp_item(const Sell& A, int t, const double* __restrict__ x, double* y,
+                                              const double* rsrc) {
   const int row = t / G;
   const int g = t % G;
   const int lane = threadIdx.x & 31;
@@ -353,22 +354,44 @@ __global__ void __launch_bounds__(kCta) k_spmv_grp(Sell A, const double* __restr
   int wlen = len;
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) wlen = max(wlen, __shfl_xor_sync(0xffffffffu, wlen, o));
+  // Chunks of G*U entries: every lane issues its U value/column loads, then
+  // its U gathers, before any product is summed, so a chunk costs one memory
+  // round trip instead of U (the small levels are latency-bound).
+  constexpr int U = 16;
   double acc = 0.0;
-  for (int k0 = 0; k0 < wlen; k0 += G) {
-    const int k = k0 + g;
-    double prod = 0.0;
-    if (k < len) {
-      const double v = vd ? __ldg(dv + k) : __ldg(A.val + base + static_cast<int64_t>(k) * kSell);
-      const int32_t c = od ? row + __ldg(dc + k) : __ldg(A.col + base + static_cast<int64_t>(k) * kSell);
-      prod = v * __ldg(x + c);
-    }
+  for (int k0 = 0; k0 < wlen; k0 += G * U) {
+    double v[U];
+    int32_t c[U];
 #pragma unroll
-    for (int u = 0; u < G; ++u) {
-      const double pu = __shfl_sync(0xffffffffu, prod, gbase + u);
-      if (g == 0 && k0 + u < len) acc = acc + pu;
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * G + g;
+      v[u] = 0.0;
+      c[u] = 0;
+      if (k < len) {
+        v[u] = vd ? __ldg(dv + k) : __ldg(A.val + base + static_cast<int64_t>(k) * kSell);
+        c[u] = od ? row + __ldg(dc + k) : __ldg(A.col + base + static_cast<int64_t>(k) * kSell);
+      }
+    }
+    double prod[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) prod[u] = (k0 + u * G + g < len) ? v[u] * __ldg(x + c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (k0 + u * G < wlen) {  // warp-uniform
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          const double pu = __shfl_sync(0xffffffffu, prod[u], gbase + j);
+          if (g == 0 && k0 + u * G + j < len) acc = acc + pu;
+        }
+      }
     }
   }
   if (valid_row && g == 0) y[row] = (MODE == 0) ? acc : rsrc[row] - acc;
+}
+template <int MODE, int G>
+__global__ void __launch_bounds__(kCta) k_spmv_grp(Sell A, const double* __restrict__ x, double* y,
+                                                   const double* rsrc) {
+  spmv_grp_item<MODE, G>(A, blockIdx.x * kCta + threadIdx.x, x, y, rsrc);
 }
 
 // Prolongation fused with the correction: cor = P xc (P = R^T stored as CSR
@@ -541,11 +564,9 @@ __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int l
   if (lane < s) ybuf[G.w_ypos[b] + lane] = y;
 }
 
-__global__ void __launch_bounds__(128) k_as_blocks(AsGroups G, const double* __restrict__ r,
-                                                   double* ybuf, const PcgState* st) {
-  if (pcg_done(st)) return;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+// One warp-sized work item w of phase 1 (group of small blocks or a warp block).
+__device__ __forceinline__ void as_blocks_item(const AsGroups& G, int w, int lane, const double* __restrict__ r,
+                                               double* ybuf) {
   if (w < G.n_groups) {
     const int g = w;
     const int s = G.size[g * 32 + lane];
@@ -560,6 +581,11 @@ __global__ void __launch_bounds__(128) k_as_blocks(AsGroups G, const double* __r
   } else if (w - G.n_groups < G.n_wblocks) {
     warp_block_solve(G, w - G.n_groups, lane, r, ybuf);
   }
+}
+__global__ void __launch_bounds__(128) k_as_blocks(AsGroups G, const double* __restrict__ r,
+                                                   double* ybuf, const PcgState* st) {
+  if (pcg_done(st)) return;
+  as_blocks_item(G, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, r, ybuf);
 }
 
 // Phase 2: deterministic segmented reduction per DOF, contributions in
@@ -644,27 +670,38 @@ __global__ void __launch_bounds__(kCta) k_as_gather(AsGather S, const double* __
 __device__ __forceinline__ double as_list_sum(const AsGather& S, int d, double rd,
                                               const double* __restrict__ ybuf) {
   const int c = -S.head[d] - 1;
+  const int q0 = S.cptr[c], q1 = S.cptr[c + 1];
   double acc = 0.0;
-  for (int q = S.cptr[c]; q < S.cptr[c + 1]; ++q) {
-    const int code = S.centry[q];
-    double v;
-    if (code < 0) {
-      const double ls = S.sval[-code - 1];
-      v = (rd / ls) / ls;
-    } else {
-      v = ybuf[code];
+  // Batches of 8: all codes, then all values, then the ordered sum (one
+  // memory round trip per batch instead of two per contribution).
+  constexpr int U = 8;
+  for (int qb = q0; qb < q1; qb += U) {
+    int code[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) code[u] = (qb + u < q1) ? S.centry[qb + u] : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (qb + u < q1) {
+        if (code[u] < 0) {
+          const double ls = S.sval[-code[u] - 1];
+          v[u] = (rd / ls) / ls;
+        } else {
+          v[u] = ybuf[code[u]];
+        }
+      } else {
+        v[u] = 0.0;
+      }
     }
-    acc = acc + v;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (qb + u < q1) acc = acc + v[u];
   }
   return acc;
 }
 
 template <bool ACC>
-__global__ void __launch_bounds__(kCta) k_as_simple(AsGather S, const double* __restrict__ r, double* x,
-                                                    const PcgState* st) {
-  if (pcg_done(st)) return;
-  const int d = blockIdx.x * kCta + threadIdx.x;
-  if (d >= S.n) return;
+__device__ __forceinline__ void as_simple_item(const AsGather& S, int d, const double* __restrict__ r, double* x) {
   const int h = S.head[d];
   const double rd = r[d];
   const double l = S.sdiag[d];
@@ -675,7 +712,21 @@ __global__ void __launch_bounds__(kCta) k_as_simple(AsGather S, const double* __
   const double out = S.gamma * acc;
   x[d] = ACC ? xo + out : out;
 }
-
+template <bool ACC>
+__global__ void __launch_bounds__(kCta) k_as_simple(AsGather S, const double* __restrict__ r, double* x,
+                                                    const PcgState* st) {
+  if (pcg_done(st)) return;
+  const int d = blockIdx.x * kCta + threadIdx.x;
+  if (d >= S.n) return;
+  as_simple_item<ACC>(S, d, r, x);
+}
+template <bool ACC>
+__device__ __forceinline__ void as_complex_item(const AsGather& S, int c, const double* __restrict__ r,
+                                                const double* __restrict__ ybuf, double* x) {
+  const int d = S.cdof[c];
+  const double out = S.gamma * as_list_sum(S, d, r[d], ybuf);
+  x[d] = ACC ? x[d] + out : out;
+}
 template <bool ACC>
 __global__ void __launch_bounds__(kCta) k_as_complex(AsGather S, const double* __restrict__ r,
                                                      const double* __restrict__ ybuf, double* x,
@@ -683,9 +734,7 @@ __global__ void __launch_bounds__(kCta) k_as_complex(AsGather S, const double* _
   if (pcg_done(st)) return;
   const int c = blockIdx.x * kCta + threadIdx.x;
   if (c >= S.n_complex) return;
-  const int d = S.cdof[c];
-  const double out = S.gamma * as_list_sum(S, d, r[d], ybuf);
-  x[d] = ACC ? x[d] + out : out;
+  as_complex_item<ACC>(S, c, r, ybuf, x);
 }
 
 // Finest level inside PCG: complex DOFs finish here, simple DOFs read back
@@ -784,14 +833,12 @@ __device__ __forceinline__ double wait_slot(const volatile double* p) {
   return __longlong_as_double(static_cast<long long>(v));
 }
 
-// BIG: ranks above 256 (up to 1024 threads).
-template <bool SM, bool BIG = false>
-__global__ void __launch_bounds__(BIG ? 1024 : 256, 1) k_coarse(int32_t n, int32_t rank, const double* __restrict__ Lp,
-                                                               const int32_t* __restrict__ piv,
-                                                               const double* __restrict__ r, double* x,
-                                                               const PcgState* st) {
-  if (pcg_done(st)) return;
-  extern __shared__ __align__(16) double smem[];
+// The solve on one CTA (blockDim >= 32*ceil(rank/32); surplus warps only
+// zero-fill).  smem: [packed L11 (SM only)][forward: rank][backward: rank].
+template <bool SM>
+__device__ __forceinline__ void coarse_solve_cta(int32_t n, int32_t rank, const double* __restrict__ Lp,
+                                                 const int32_t* __restrict__ piv, const double* __restrict__ r,
+                                                 double* x, double* smem) {
   __shared__ unsigned long long mbar;
   const int64_t np = static_cast<int64_t>(rank) * (rank + 1) / 2;
   const int64_t np_al = (np + 1) & ~int64_t(1);  // 16-byte aligned region
@@ -812,6 +859,10 @@ __global__ void __launch_bounds__(BIG ? 1024 : 256, 1) k_coarse(int32_t n, int32
   const int i = threadIdx.x;  // one row per thread; warp w owns rows 32w..32w+31
   const bool own = i < rank;
   const int b0 = threadIdx.x & ~31;
+  if (b0 >= rank) {  // surplus warp
+    for (int k = rank + threadIdx.x; k < n; k += blockDim.x) x[piv[k] - 1] = 0.0;
+    return;
+  }
   const int bend = min(b0 + 32, rank);
   const int oi = own ? off(i) : 0;
   double y = own ? r[piv[i] - 1] : 0.0;
@@ -877,6 +928,17 @@ __global__ void __launch_bounds__(BIG ? 1024 : 256, 1) k_coarse(int32_t n, int32
   }
   if (own) x[piv[i] - 1] = y;
   for (int k = rank + threadIdx.x; k < n; k += blockDim.x) x[piv[k] - 1] = 0.0;
+}
+
+// BIG: ranks above 256 (up to 1024 threads).
+template <bool SM, bool BIG = false>
+__global__ void __launch_bounds__(BIG ? 1024 : 256, 1) k_coarse(int32_t n, int32_t rank, const double* __restrict__ Lp,
+                                                               const int32_t* __restrict__ piv,
+                                                               const double* __restrict__ r, double* x,
+                                                               const PcgState* st) {
+  if (pcg_done(st)) return;
+  extern __shared__ __align__(16) double smem[];
+  coarse_solve_cta<SM>(n, rank, Lp, piv, r, x, smem);
 }
 
 // ---------------------------------------------------------- PCG vectors ---
