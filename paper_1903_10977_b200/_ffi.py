@@ -75,6 +75,7 @@ IG_OPT_TMA_ROWS = 5
 IG_OPT_TSELL_KERNEL = 6
 IG_OPT_PSELL = 7
 IG_OPT_TAIL_ROWS = 8
+IG_OPT_PDL = 9
 
 _host = None
 _gpu = None

@@ -18,6 +18,7 @@
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
+#include <utility>
 #include <vector>
 
 #include "ig_gpu.h"
@@ -47,6 +48,28 @@ struct Error : std::runtime_error {
   } while (0)
 
 inline unsigned grid_of(int64_t n) { return static_cast<unsigned>((n + kCta - 1) / kCta); }
+
+int g_use_pdl = 1;  // programmatic dependent launch for every kernel (kernels.cuh: pdl_entry)
+
+// Every kernel launch of the library: cudaLaunchKernelEx with programmatic
+// stream serialization, so consecutive kernels on a stream (and in the
+// captured graphs) overlap launch latency with the predecessor's execution.
+template <typename... KArgs, typename... Args>
+void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_use_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) throw Error(IG_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
 
 // Host image of a SELL-32 matrix with its row dictionary (kernels.cuh: Sell).
 struct HostSell {
@@ -705,10 +728,10 @@ struct ig_hier {
   template <int M, bool S, bool R>
   void spmv_var(unsigned g, const DevSell& A, const double* x, double* y, const double* rsrc, PcgState* s) {
     switch (g_spmv_variant) {
-      case 1: k_spmv<M, S, R, 1><<<g, kCta, 0, stream>>>(A.s, x, y, rsrc, s, partials); break;
-      case 2: k_spmv<M, S, R, 2><<<g, kCta, 0, stream>>>(A.s, x, y, rsrc, s, partials); break;
-      case 3: k_spmv<M, S, R, 3><<<g, kCta, 0, stream>>>(A.s, x, y, rsrc, s, partials); break;
-      default: k_spmv<M, S, R, 0><<<g, kCta, 0, stream>>>(A.s, x, y, rsrc, s, partials); break;
+      case 1: launch(k_spmv<M, S, R, 1>, g, kCta, 0, stream, A.s, x, y, rsrc, s, partials); break;
+      case 2: launch(k_spmv<M, S, R, 2>, g, kCta, 0, stream, A.s, x, y, rsrc, s, partials); break;
+      case 3: launch(k_spmv<M, S, R, 3>, g, kCta, 0, stream, A.s, x, y, rsrc, s, partials); break;
+      default: launch(k_spmv<M, S, R, 0>, g, kCta, 0, stream, A.s, x, y, rsrc, s, partials); break;
     }
   }
   void spmv(const DevSell& A, int mode, const double* x, double* y, const double* rsrc,
@@ -718,46 +741,46 @@ struct ig_hier {
     if (A.has_p) {
       const unsigned gp = static_cast<unsigned>(A.p.n_slices / (kCta / 32));
       if (mode == 0) {
-        if (A.stream) k_pspmv<0, true><<<gp, kCta, 0, stream>>>(A.p, x, y, rsrc, s);
-        else k_pspmv<0, false><<<gp, kCta, 0, stream>>>(A.p, x, y, rsrc, s);
+        if (A.stream) launch(k_pspmv<0, true>, gp, kCta, 0, stream, A.p, x, y, rsrc, s);
+        else launch(k_pspmv<0, false>, gp, kCta, 0, stream, A.p, x, y, rsrc, s);
       } else {
-        if (A.stream) k_pspmv<1, true><<<gp, kCta, 0, stream>>>(A.p, x, y, rsrc, s);
-        else k_pspmv<1, false><<<gp, kCta, 0, stream>>>(A.p, x, y, rsrc, s);
+        if (A.stream) launch(k_pspmv<1, true>, gp, kCta, 0, stream, A.p, x, y, rsrc, s);
+        else launch(k_pspmv<1, false>, gp, kCta, 0, stream, A.p, x, y, rsrc, s);
       }
       CK(cudaGetLastError());
       if (red) {  // p . Ap over the canonical chunks, alpha / Breakdown
-        k_pap<<<g, kCta, 0, stream>>>(A.s.n_rows, x, y, s, partials);
+        launch(k_pap, g, kCta, 0, stream, A.s.n_rows, x, y, s, partials);
         CK(cudaGetLastError());
       }
       return;
     }
     if (A.has_t && g_tsell_kernel == 0) {  // large matrix: compact SELL, thread per row
       if (red)
-        k_spmv_cmp<0, true><<<g, kCta, 0, stream>>>(A.t, x, y, rsrc, s, partials);
+        launch(k_spmv_cmp<0, true>, g, kCta, 0, stream, A.t, x, y, rsrc, s, partials);
       else if (mode == 0)
-        k_spmv_cmp<0, false><<<g, kCta, 0, stream>>>(A.t, x, y, rsrc, s, partials);
+        launch(k_spmv_cmp<0, false>, g, kCta, 0, stream, A.t, x, y, rsrc, s, partials);
       else
-        k_spmv_cmp<1, false><<<g, kCta, 0, stream>>>(A.t, x, y, rsrc, s, partials);
+        launch(k_spmv_cmp<1, false>, g, kCta, 0, stream, A.t, x, y, rsrc, s, partials);
       CK(cudaGetLastError());
       return;
     }
     if (A.has_t) {  // large matrix: TMA-staged compact SELL, persistent grid
       const unsigned gt = static_cast<unsigned>(std::min<int64_t>(A.t.n_chunks, static_cast<int64_t>(num_sms) * 2));
       if (red)
-        k_spmv_tma<0, true><<<gt, kCta, kTSmem, stream>>>(A.t, x, y, rsrc, s, partials);
+        launch(k_spmv_tma<0, true>, gt, kCta, kTSmem, stream, A.t, x, y, rsrc, s, partials);
       else if (mode == 0)
-        k_spmv_tma<0, false><<<gt, kCta, kTSmem, stream>>>(A.t, x, y, rsrc, s, partials);
+        launch(k_spmv_tma<0, false>, gt, kCta, kTSmem, stream, A.t, x, y, rsrc, s, partials);
       else
-        k_spmv_tma<1, false><<<gt, kCta, kTSmem, stream>>>(A.t, x, y, rsrc, s, partials);
+        launch(k_spmv_tma<1, false>, gt, kCta, kTSmem, stream, A.t, x, y, rsrc, s, partials);
       CK(cudaGetLastError());
       return;
     }
     if (!red && A.s.n_rows <= g_small_rows) {  // latency-bound level: 8 lanes per row
       const unsigned gg = grid_of(static_cast<int64_t>(A.s.n_rows) * 8);
       if (mode == 0)
-        k_spmv_grp<0, 8><<<gg, kCta, 0, stream>>>(A.s, x, y, rsrc);
+        launch(k_spmv_grp<0, 8>, gg, kCta, 0, stream, A.s, x, y, rsrc);
       else
-        k_spmv_grp<1, 8><<<gg, kCta, 0, stream>>>(A.s, x, y, rsrc);
+        launch(k_spmv_grp<1, 8>, gg, kCta, 0, stream, A.s, x, y, rsrc);
       CK(cudaGetLastError());
       return;
     }
@@ -773,18 +796,18 @@ struct ig_hier {
   template <bool S>
   void prolong_var(unsigned g, const Level& l, const double* xc, double* x, PcgState* s) {
     switch (g_spmv_variant) {
-      case 1: k_prolong<S, 1><<<g, kCta, 0, stream>>>(l.P.s, xc, l.cor, x, s); break;
-      case 2: k_prolong<S, 2><<<g, kCta, 0, stream>>>(l.P.s, xc, l.cor, x, s); break;
-      case 3: k_prolong<S, 3><<<g, kCta, 0, stream>>>(l.P.s, xc, l.cor, x, s); break;
-      default: k_prolong<S, 0><<<g, kCta, 0, stream>>>(l.P.s, xc, l.cor, x, s); break;
+      case 1: launch(k_prolong<S, 1>, g, kCta, 0, stream, l.P.s, xc, l.cor, x, s); break;
+      case 2: launch(k_prolong<S, 2>, g, kCta, 0, stream, l.P.s, xc, l.cor, x, s); break;
+      case 3: launch(k_prolong<S, 3>, g, kCta, 0, stream, l.P.s, xc, l.cor, x, s); break;
+      default: launch(k_prolong<S, 0>, g, kCta, 0, stream, l.P.s, xc, l.cor, x, s); break;
     }
   }
   void prolong(const Level& l, const double* xc, double* x, PcgState* s) {
     const unsigned g = grid_of(l.P.s.n_rows);
     if (l.P.has_p) {
       const unsigned gp = static_cast<unsigned>(l.P.p.n_slices / (kCta / 32));
-      if (l.P.stream) k_pprolong<true><<<gp, kCta, 0, stream>>>(l.P.p, xc, l.cor, x, s);
-      else k_pprolong<false><<<gp, kCta, 0, stream>>>(l.P.p, xc, l.cor, x, s);
+      if (l.P.stream) launch(k_pprolong<true>, gp, kCta, 0, stream, l.P.p, xc, l.cor, x, s);
+      else launch(k_pprolong<false>, gp, kCta, 0, stream, l.P.p, xc, l.cor, x, s);
       CK(cudaGetLastError());
       return;
     }
@@ -804,41 +827,41 @@ struct ig_hier {
       CK(cudaStreamWaitEvent(side, ev_fork, 0));
       const unsigned gb =
           static_cast<unsigned>((static_cast<int64_t>(l.G.n_groups + l.G.n_wblocks) * 32 + 127) / 128);
-      k_as_blocks<<<gb, 128, 0, side>>>(l.G, r, l.ybuf, s);
+      launch(k_as_blocks, gb, 128, 0, side, l.G, r, l.ybuf, s);
       CK(cudaGetLastError());
       CK(cudaEventRecord(ev_join, side));
     }
     const unsigned g = grid_of(l.n);
     if (acc)
-      k_as_simple<true><<<g, kCta, 0, stream>>>(l.S, r, x, s);
+      launch(k_as_simple<true>, g, kCta, 0, stream, l.S, r, x, s);
     else
-      k_as_simple<false><<<g, kCta, 0, stream>>>(l.S, r, x, s);
+      launch(k_as_simple<false>, g, kCta, 0, stream, l.S, r, x, s);
     CK(cudaGetLastError());
     if (multi) CK(cudaStreamWaitEvent(stream, ev_join, 0));
     if (rdot) {
       if (acc)
-        k_as_finish_red<true><<<g, kCta, 0, stream>>>(l.S, r, l.ybuf, x, rdot, s, partials);
+        launch(k_as_finish_red<true>, g, kCta, 0, stream, l.S, r, l.ybuf, x, rdot, s, partials);
       else
-        k_as_finish_red<false><<<g, kCta, 0, stream>>>(l.S, r, l.ybuf, x, rdot, s, partials);
+        launch(k_as_finish_red<false>, g, kCta, 0, stream, l.S, r, l.ybuf, x, rdot, s, partials);
     } else if (l.S.n_complex > 0) {
       const unsigned gc = grid_of(l.S.n_complex);
       if (acc)
-        k_as_complex<true><<<gc, kCta, 0, stream>>>(l.S, r, l.ybuf, x, s);
+        launch(k_as_complex<true>, gc, kCta, 0, stream, l.S, r, l.ybuf, x, s);
       else
-        k_as_complex<false><<<gc, kCta, 0, stream>>>(l.S, r, l.ybuf, x, s);
+        launch(k_as_complex<false>, gc, kCta, 0, stream, l.S, r, l.ybuf, x, s);
     }
     CK(cudaGetLastError());
   }
   void coarse_launch(bool sm, const double* r, double* x, PcgState* s) {
     const bool big = coarse_threads > 256;
     if (sm && !big)
-      k_coarse<true, false><<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, s);
+      launch(k_coarse<true, false>, 1, coarse_threads, coarse_smem, stream, n0, rank, Lp, piv, r, x, s);
     else if (sm)
-      k_coarse<true, true><<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, s);
+      launch(k_coarse<true, true>, 1, coarse_threads, coarse_smem, stream, n0, rank, Lp, piv, r, x, s);
     else if (!big)
-      k_coarse<false, false><<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, s);
+      launch(k_coarse<false, false>, 1, coarse_threads, coarse_smem, stream, n0, rank, Lp, piv, r, x, s);
     else
-      k_coarse<false, true><<<1, coarse_threads, coarse_smem, stream>>>(n0, rank, Lp, piv, r, x, s);
+      launch(k_coarse<false, true>, 1, coarse_threads, coarse_smem, stream, n0, rank, Lp, piv, r, x, s);
   }
   void coarse(const double* r, double* x, PcgState* s) {
     coarse_launch(coarse_use_smem != 0, r, x, s);
@@ -875,7 +898,7 @@ struct ig_hier {
     if (l == 0) {
       coarse(r, x, s);
       if (rdot) {  // 1-level hierarchy inside PCG: r . z as a separate pass
-        k_pcg_rz<<<grid_of(n0), kCta, 0, stream>>>(n0, rdot, x, s, partials);
+        launch(k_pcg_rz, grid_of(n0), kCta, 0, stream, n0, rdot, x, s, partials);
         CK(cudaGetLastError());
       }
       mark("coarse", 0);
@@ -916,22 +939,22 @@ struct ig_hier {
   // (IF node / host check) once the solve has stopped.
   void pcg_init(cudaGraphConditionalHandle c_if, cudaGraphConditionalHandle c_loop) {
     const int32_t n = lv[L - 1].n;
-    k_pcg_init<<<grid_of(n), kCta, 0, stream>>>(n, r, st, partials, c_if, c_loop);
+    launch(k_pcg_init, grid_of(n), kCta, 0, stream, n, r, st, partials, c_if, c_loop);
     CK(cudaGetLastError());
   }
   void pcg_precond(bool first) {
     const int32_t n = lv[L - 1].n;
     vcycle(L - 1, r, z, st, r);  // z = M r; r . z; beta
     if (first)
-      k_pcg_p<true><<<grid_of(n), kCta, 0, stream>>>(n, z, p, st);
+      launch(k_pcg_p<true>, grid_of(n), kCta, 0, stream, n, z, p, st);
     else
-      k_pcg_p<false><<<grid_of(n), kCta, 0, stream>>>(n, z, p, st);
+      launch(k_pcg_p<false>, grid_of(n), kCta, 0, stream, n, z, p, st);
     CK(cudaGetLastError());
   }
   void pcg_step(cudaGraphConditionalHandle c_if, cudaGraphConditionalHandle c_loop) {
     const int32_t n = lv[L - 1].n;
     spmv(lv[L - 1].A, 0, p, ap, nullptr, st, true);  // ap = A p; pap; alpha / breakdown
-    k_pcg_update<<<grid_of(n), kCta, 0, stream>>>(n, p, ap, r, st, partials, c_if, c_loop);
+    launch(k_pcg_update, grid_of(n), kCta, 0, stream, n, p, ap, r, st, partials, c_if, c_loop);
     CK(cudaGetLastError());
   }
   // Append a conditional node of `type` after the current capture frontier
@@ -1227,6 +1250,10 @@ int ig_set_option(int32_t option, int64_t value) {
   }
   if (option == IG_OPT_ROW_DICT) {
     g_use_dict = value != 0;
+    return IG_OK;
+  }
+  if (option == IG_OPT_PDL) {
+    g_use_pdl = value != 0;
     return IG_OK;
   }
   if (option == IG_OPT_TAIL_ROWS) {

@@ -13,6 +13,18 @@
 
 namespace igk {
 
+// Programmatic dependent launch (PDL): every kernel is launched with
+// programmatic stream serialization, so the next kernel's CTAs are scheduled
+// while this one runs and the launch latency of a dependent chain overlaps
+// the work.  Each kernel first waits for its predecessor grid to complete
+// (griddepcontrol.wait: full completion + memory flush, transitively), then
+// lets its own dependents launch.  Without the launch attribute both are
+// no-ops.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 constexpr int kCta = 256;   // threads per CTA == reduction chunk size
 constexpr int kSell = 32;   // SELL slice height == warp size
 
@@ -294,6 +306,7 @@ __device__ __forceinline__ double sell_row(const Sell& A, int row, const double*
 template <int MODE, bool STREAM, bool RED, int VAR>
 __global__ void __launch_bounds__(kCta, SpmvVar<VAR>::MINB) k_spmv(Sell A, const double* __restrict__ x, double* y,
                                                const double* rsrc, PcgState* st, double* partials) {
+  pdl_entry();
   if (pcg_done(st)) return;
   const int row = blockIdx.x * kCta + threadIdx.x;
   double prod = 0.0;
@@ -391,6 +404,7 @@ __device__ __forceinline__ void spmv_grp_item(const Sell& A, int t, const double
 template <int MODE, int G>
 __global__ void __launch_bounds__(kCta) k_spmv_grp(Sell A, const double* __restrict__ x, double* y,
                                                    const double* rsrc) {
+  pdl_entry();
   spmv_grp_item<MODE, G>(A, blockIdx.x * kCta + threadIdx.x, x, y, rsrc);
 }
 
@@ -400,6 +414,7 @@ __global__ void __launch_bounds__(kCta) k_spmv_grp(Sell A, const double* __restr
 template <bool STREAM, int VAR>
 __global__ void __launch_bounds__(kCta, SpmvVar<VAR>::MINB) k_prolong(Sell P, const double* __restrict__ xc, double* cor,
                                                   double* x, const PcgState* st) {
+  pdl_entry();
   if (pcg_done(st)) return;
   const int row = blockIdx.x * kCta + threadIdx.x;
   if (row >= P.n_rows) return;
@@ -544,21 +559,44 @@ __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int l
   double y = lane < s ? __ldg(r + dp[lane]) : 0.0;
   const double dg = lane < s ? __ldg(f + lane * s + lane) : 1.0;  // own pivot L(lane, lane)
   const double rdg = safe_rcp(dg);
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    if (j < s) {
-      if (lane == j) y = div_rb(y, dg, rdg);
-      const double yj = __shfl_sync(0xffffffffu, y, j);
-      if (lane > j) y = y - m[j] * yj;
-    }
-  }
   double acc = 0.0;
+  if (__all_sync(0xffffffffu, isfinite(rdg) && rdg != 0.0)) {
+    // Branch-free steps (as in the coarse solve): every lane forms the
+    // quotient, the shuffle picks the owner's, selects keep each lane's own
+    // operation sequence.
 #pragma unroll
-  for (int k = 31; k >= 0; --k) {
-    if (k < s) {
-      if (lane == k) y = div_rb(y - acc, dg, rdg);
-      const double yk = __shfl_sync(0xffffffffu, y, k);
-      if (lane < k) acc = acc + m[k] * yk;
+    for (int j = 0; j < 32; ++j) {
+      if (j < s) {
+        const double yj = __shfl_sync(0xffffffffu, exact_div(y, dg, rdg), j);
+        const double upd = y - m[j] * yj;
+        y = (lane == j) ? yj : ((lane > j) ? upd : y);
+      }
+    }
+#pragma unroll
+    for (int k = 31; k >= 0; --k) {
+      if (k < s) {
+        const double yk = __shfl_sync(0xffffffffu, exact_div(y - acc, dg, rdg), k);
+        const double nacc = acc + m[k] * yk;
+        y = (lane == k) ? yk : y;
+        acc = (lane < k) ? nacc : acc;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j < s) {
+        if (lane == j) y = div_rb(y, dg, rdg);
+        const double yj = __shfl_sync(0xffffffffu, y, j);
+        if (lane > j) y = y - m[j] * yj;
+      }
+    }
+#pragma unroll
+    for (int k = 31; k >= 0; --k) {
+      if (k < s) {
+        if (lane == k) y = div_rb(y - acc, dg, rdg);
+        const double yk = __shfl_sync(0xffffffffu, y, k);
+        if (lane < k) acc = acc + m[k] * yk;
+      }
     }
   }
   if (lane < s) ybuf[G.w_ypos[b] + lane] = y;
@@ -584,6 +622,7 @@ __device__ __forceinline__ void as_blocks_item(const AsGroups& G, int w, int lan
 }
 __global__ void __launch_bounds__(128) k_as_blocks(AsGroups G, const double* __restrict__ r,
                                                    double* ybuf, const PcgState* st) {
+  pdl_entry();
   if (pcg_done(st)) return;
   as_blocks_item(G, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, r, ybuf);
 }
@@ -625,6 +664,7 @@ template <bool ACC, bool RED>
 __global__ void __launch_bounds__(kCta) k_as_gather(AsGather S, const double* __restrict__ r,
                                                     const double* __restrict__ ybuf, double* x,
                                                     const double* rdot, PcgState* st, double* partials) {
+  pdl_entry();
   if (pcg_done(st)) return;
   const int d = blockIdx.x * kCta + threadIdx.x;
   double prod = 0.0;
@@ -667,9 +707,9 @@ __global__ void __launch_bounds__(kCta) k_as_gather(AsGather S, const double* __
 // singleton fast path, which does not read ybuf, runs CONCURRENTLY with the
 // block solves (a second stream / graph branch), and only the DOFs with
 // contribution lists wait for them.  Arithmetic per DOF is unchanged.
-__device__ __forceinline__ double as_list_sum(const AsGather& S, int d, double rd,
-                                              const double* __restrict__ ybuf) {
-  const int c = -S.head[d] - 1;
+// Contribution list c (== complex item c: head[cdof[c]] = -(c+1)).
+__device__ __forceinline__ double as_list_sum_c(const AsGather& S, int c, double rd,
+                                                const double* __restrict__ ybuf) {
   const int q0 = S.cptr[c], q1 = S.cptr[c + 1];
   double acc = 0.0;
   // Batches of 8: all codes, then all values, then the ordered sum (one
@@ -699,6 +739,10 @@ __device__ __forceinline__ double as_list_sum(const AsGather& S, int d, double r
   }
   return acc;
 }
+__device__ __forceinline__ double as_list_sum(const AsGather& S, int d, double rd,
+                                              const double* __restrict__ ybuf) {
+  return as_list_sum_c(S, -S.head[d] - 1, rd, ybuf);
+}
 
 template <bool ACC>
 __device__ __forceinline__ void as_simple_item(const AsGather& S, int d, const double* __restrict__ r, double* x) {
@@ -715,6 +759,7 @@ __device__ __forceinline__ void as_simple_item(const AsGather& S, int d, const d
 template <bool ACC>
 __global__ void __launch_bounds__(kCta) k_as_simple(AsGather S, const double* __restrict__ r, double* x,
                                                     const PcgState* st) {
+  pdl_entry();
   if (pcg_done(st)) return;
   const int d = blockIdx.x * kCta + threadIdx.x;
   if (d >= S.n) return;
@@ -724,13 +769,14 @@ template <bool ACC>
 __device__ __forceinline__ void as_complex_item(const AsGather& S, int c, const double* __restrict__ r,
                                                 const double* __restrict__ ybuf, double* x) {
   const int d = S.cdof[c];
-  const double out = S.gamma * as_list_sum(S, d, r[d], ybuf);
+  const double out = S.gamma * as_list_sum_c(S, c, r[d], ybuf);
   x[d] = ACC ? x[d] + out : out;
 }
 template <bool ACC>
 __global__ void __launch_bounds__(kCta) k_as_complex(AsGather S, const double* __restrict__ r,
                                                      const double* __restrict__ ybuf, double* x,
                                                      const PcgState* st) {
+  pdl_entry();
   if (pcg_done(st)) return;
   const int c = blockIdx.x * kCta + threadIdx.x;
   if (c >= S.n_complex) return;
@@ -744,6 +790,7 @@ template <bool ACC>
 __global__ void __launch_bounds__(kCta) k_as_finish_red(AsGather S, const double* __restrict__ r,
                                                         const double* __restrict__ ybuf, double* x,
                                                         const double* rdot, PcgState* st, double* partials) {
+  pdl_entry();
   if (pcg_done(st)) return;
   const int d = blockIdx.x * kCta + threadIdx.x;
   double prod = 0.0;
@@ -768,6 +815,7 @@ __global__ void __launch_bounds__(kCta) k_as_finish_red(AsGather S, const double
 __global__ void __launch_bounds__(kCta) k_pcg_rz(int32_t n, const double* __restrict__ r,
                                                  const double* __restrict__ z, PcgState* st,
                                                  double* partials) {
+  pdl_entry();
   if (pcg_done(st)) return;
   const int i = blockIdx.x * kCta + threadIdx.x;
   const double prod = i < n ? r[i] * z[i] : 0.0;
@@ -936,6 +984,7 @@ __global__ void __launch_bounds__(BIG ? 1024 : 256, 1) k_coarse(int32_t n, int32
                                                                const int32_t* __restrict__ piv,
                                                                const double* __restrict__ r, double* x,
                                                                const PcgState* st) {
+  pdl_entry();
   if (pcg_done(st)) return;
   extern __shared__ __align__(16) double smem[];
   coarse_solve_cta<SM>(n, rank, Lp, piv, r, x, smem);
@@ -955,6 +1004,7 @@ __device__ __forceinline__ void set_conds(cudaGraphConditionalHandle c_if, cudaG
 __global__ void __launch_bounds__(kCta) k_pcg_init(int32_t n, double* r, PcgState* st, double* partials,
                                                    cudaGraphConditionalHandle c_if,
                                                    cudaGraphConditionalHandle c_loop) {
+  pdl_entry();
   const int i = blockIdx.x * kCta + threadIdx.x;
   double prod = 0.0;
   if (i < n) {
@@ -993,6 +1043,7 @@ __global__ void __launch_bounds__(kCta) k_pcg_update(int32_t n, const double* __
                                                      PcgState* st, double* partials,
                                                      cudaGraphConditionalHandle c_if,
                                                      cudaGraphConditionalHandle c_loop) {
+  pdl_entry();
   if (pcg_stopped(st)) {  // breakdown in the preceding SpMV: x, r stay
     if (blockIdx.x == 0 && threadIdx.x == 0) set_conds(c_if, c_loop, false);
     return;
@@ -1030,6 +1081,7 @@ __global__ void __launch_bounds__(kCta) k_pcg_update(int32_t n, const double* __
 template <bool FIRST>
 __global__ void __launch_bounds__(kCta) k_pcg_p(int32_t n, const double* __restrict__ z, double* p,
                                                 const PcgState* st) {
+  pdl_entry();
   const int i = blockIdx.x * kCta + threadIdx.x;
   if (i >= n) return;
   if (FIRST)

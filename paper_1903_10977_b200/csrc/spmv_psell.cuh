@@ -158,6 +158,7 @@ __device__ __forceinline__ int psell_slice(const PSell& A, int slice, const doub
 template <int MODE, bool STREAM>
 __global__ void __launch_bounds__(kCta) k_pspmv(PSell A, const double* __restrict__ x, double* y,
                                                const double* rsrc, const PcgState* st) {
+  pdl_entry();
   if (pcg_done(st)) return;
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   double acc;
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(kCta) k_pspmv(PSell A, const double* __restric
 // alpha / Breakdown exactly as the fused k_spmv<...,RED> does.
 __global__ void __launch_bounds__(kCta) k_pap(int n, const double* __restrict__ p, const double* __restrict__ ap,
                                              PcgState* st, double* partials) {
+  pdl_entry();
   if (pcg_done(st)) return;
   const int row = blockIdx.x * kCta + threadIdx.x;
   const double prod = row < n ? p[row] * ap[row] : 0.0;
@@ -191,6 +193,7 @@ __global__ void __launch_bounds__(kCta) k_pap(int n, const double* __restrict__ 
 template <bool STREAM>
 __global__ void __launch_bounds__(kCta) k_pprolong(PSell P, const double* __restrict__ xc, double* cor, double* x,
                                                   const PcgState* st) {
+  pdl_entry();
   if (pcg_done(st)) return;
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   double c;

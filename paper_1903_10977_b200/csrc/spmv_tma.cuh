@@ -72,6 +72,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 template <int MODE, bool RED>
 __global__ void __launch_bounds__(kCta) k_spmv_tma(TSell A, const double* __restrict__ x, double* y,
                                                    const double* rsrc, PcgState* st, double* partials) {
+  pdl_entry();
   extern __shared__ __align__(128) unsigned char tsm[];
   __shared__ unsigned long long mbar[8][2];
   __shared__ double sm8[8];
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(kCta) k_spmv_tma(TSell A, const double* __rest
 template <int MODE, bool RED>
 __global__ void __launch_bounds__(kCta) k_spmv_cmp(TSell A, const double* __restrict__ x, double* y,
                                                    const double* rsrc, PcgState* st, double* partials) {
+  pdl_entry();
   const int row = blockIdx.x * kCta + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int s = row >> 5;
