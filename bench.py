@@ -117,13 +117,42 @@ def build_workload(name: str, threads: int):
     return case, desc, time.perf_counter() - t0
 
 
+def host_cpu():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def pinned_core0(fn):
+    """Run fn() pinned to host core 0 (taskset -c 0), then
+    restore the affinity."""
+    try:
+        old = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {sorted(old)[0]})
+    except (AttributeError, OSError):
+        old = None
+    try:
+        return fn()
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
+
+
 def cpu_sample(case, iters_full: int, sample_iters: int):
     """Oracle (single-threaded C restatement) on the first `sample_iters` PCG
     iterations, extrapolated to the full solve: the prologue costs one
     preconditioner application, every iteration one SpMV + one V-cycle."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_ffi as orc
-    st, x, res, it, sec = orc.pcg(case.levels_c(), case.b, tol=1e-8, maxit=sample_iters, mode=orc.SEQ)
+    st, x, res, it, sec = pinned_core0(
+        lambda: orc.pcg(case.levels_c(), case.b, tol=1e-8, maxit=sample_iters, mode=orc.SEQ))
     per_unit = sec / (it + 1)
     t_full = per_unit * (iters_full + 1)
     return case.n / t_full, sec, it
@@ -228,13 +257,15 @@ def main():
     spmv_ms = e0.elapsed_time(e1) / nspmv
     hbm, peak_src = peaks()
     achieved = info.bytes_spmv_finest / (spmv_ms * 1e-3) / 1e9
+    kernel_name = ("k_pspmv (finest A p, pattern SELL; spmv_psell.cuh)" if n > 40000
+                   else "k_spmv_grp (finest A p, row-dictionary SELL)")
 
     # --- V-cycles/s and V-cycle GB/s (graph-replayed V-cycle) -----------------
     dz = torch.empty_like(db)
     for _ in range(3):
         lib.ig_vcycle_device(h.handle, vp(db.data_ptr()), vp(dz.data_ptr()))
     torch.cuda.synchronize()
-    nv = 20
+    nv = 100  # >= 100 back-to-back V-cycles
     e0.record(stream)
     for _ in range(nv):
         lib.ig_vcycle_device(h.handle, vp(db.data_ptr()), vp(dz.data_ptr()))
@@ -270,22 +301,23 @@ def main():
     assert np.array_equal(hx.numpy(), dx.cpu().numpy()), "host-buffer and device solves differ"
 
     kv = info.kernels_vcycle
-    launches_per_solve = (kv + 2) + iters * (kv + 3)
+    launches_per_solve = (kv + 2) + iters * info.kernels_pcg_iter  # init + V-cycle + p; per iteration
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, sec, sit = cpu_sample(case, iters, args.cpu_sample_iters)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": (f"oracle/liboracle.so (C restatement of solvers.cpp/multigrid.cpp/smoothers.cpp, "
-                          f"single-threaded like the reference, -O3 -ffp-contract=off): first {sit} PCG "
-                          f"iterations of the same {args.workload.upper()} hierarchy took {sec:.2f} s, "
-                          f"extrapolated to the {iters}-iteration solve")}
+                          f"single-threaded like the reference, -O3 -ffp-contract=off, pinned to host core 0): "
+                          f"first {sit} PCG iterations of the same {args.workload.upper()} hierarchy took "
+                          f"{sec:.2f} s, extrapolated to the {iters}-iteration solve"),
+               "host": host_cpu()}
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "spmv_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("bytes_per_launch")
+            traffic = json.load(f).get(args.workload, {}).get("bytes_per_launch")
 
     if rank == 0:
         line = {
@@ -300,7 +332,7 @@ def main():
             "iterations": iters,
             "vcycles_per_s": 1e3 / vc_ms, "vcycle_ms": vc_ms, "vcycle_gbs": vc_gbs,
             "vcycle_frac_of_hbm": vc_gbs / hbm,
-            "roofline": {"bound": "hbm", "kernel": "k_spmv (finest A p, SELL-32)", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": achieved,
                          "peak": hbm, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic, "algorithmic_bytes_per_launch": int(info.bytes_spmv_finest),
                          "launch_ms": spmv_ms,
@@ -308,8 +340,9 @@ def main():
                          "layout_gbs": info.bytes_spmv_finest_layout / (spmv_ms * 1e-3) / 1e9,
                          "layout_frac": info.bytes_spmv_finest_layout / (spmv_ms * 1e-3) / 1e9 / hbm,
                          "note": ("achieved counts CSR-minimal bytes (12 B/nnz, SURVEY.md App. C); the "
-                                  "row-dictionary SELL reads only layout_bytes_per_launch from HBM, so "
-                                  "frac > 1 is expected; layout_frac is the bandwidth efficiency")},
+                                  "pattern SELL reads only layout_bytes_per_launch from HBM (matrix words "
+                                  "shared by runs of identical rows are read once), so frac > 1 is expected; "
+                                  "traffic is ncu dram read+write bytes per launch (profiles/)")},
             "vcycle_layout_gbs": info.bytes_vcycle_layout / (vc_ms * 1e-3) / 1e9,
             "cpu_baseline": cpu,
             "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
