@@ -78,6 +78,11 @@ typedef struct {
   const int32_t *blk_dofs; /* blk_ptr[n_blocks] */
   const int64_t *fac_ptr;  /* n_blocks+1 */
   const double *fac;
+  /* Multiplicative sweeps only (ColorClasses, smoothers.hpp:35-42): greedy
+   * colour of each block (pre-filter supports), colours 0..n_colors-1.  Same-
+   * colour blocks have disjoint DOFs.  NULL / 0 for additive Schwarz. */
+  int32_t n_colors;
+  const int32_t *color_of; /* n_blocks */
 } ig_blocks;
 
 /* One level.  levels[0] is the coarsest (A only; R empty, no smoother),
@@ -86,7 +91,7 @@ typedef struct {
 typedef struct {
   ig_csr A;
   ig_csr R;
-  int32_t smoother_kind; /* ig_smoother_kind; only ADDITIVE_SCHWARZ on device */
+  int32_t smoother_kind; /* ig_smoother_kind: ADDITIVE_ or MULTIPLICATIVE_SCHWARZ on the device */
   double gamma;          /* damping, already resolved (smoothers.cpp:234-239) */
   ig_blocks blocks;
 } ig_level;

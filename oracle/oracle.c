@@ -123,6 +123,53 @@ void orc_as_apply(const ig_level *lv, int32_t n, const double *r, double *x) {
   for (int32_t i = 0; i < n; ++i) x[i] = lv->gamma * x[i];
 }
 
+/* Colored multiplicative sweep (smoothers.cpp:186-208).  The residual `cur`
+ * is frozen within a colour; same-colour blocks touch disjoint DOFs; the
+ * residual update `cur -= A * delta` runs after every colour but the last,
+ * as a full Eigen RowMajor product (per-row ascending sum) subtracted from
+ * cur.  Colours without blocks are skipped (`if (!any) continue`). */
+void orc_ms_apply(const ig_level *lv, int32_t n, const double *r, double *x, int dir) {
+  const ig_blocks *B = &lv->blocks;
+  const int C = B->n_colors;
+  double *cur = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  double *delta = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  double y[1024];
+  for (int32_t i = 0; i < n; ++i) {
+    x[i] = 0.0;
+    cur[i] = r[i];
+  }
+  for (int step = 0; step < C; ++step) {
+    const int col = dir == 0 ? C - 1 - step : step;
+    int any = 0;
+    for (int32_t i = 0; i < n; ++i) delta[i] = 0.0;
+    for (int32_t b = 0; b < B->n_blocks; ++b) {
+      if (B->color_of[b] != col) continue;
+      const int32_t o = B->blk_ptr[b];
+      const int s = B->blk_ptr[b + 1] - o;
+      for (int i = 0; i < s; ++i) y[i] = cur[B->blk_dofs[o + i]];
+      llt_solve(s, B->fac + B->fac_ptr[b], y);
+      for (int i = 0; i < s; ++i) {
+        const int32_t d = B->blk_dofs[o + i];
+        delta[d] = delta[d] + y[i];
+      }
+      any = 1;
+    }
+    if (!any) continue;
+    for (int32_t i = 0; i < n; ++i) x[i] = x[i] + delta[i];
+    if (step + 1 < C) orc_spmv(&lv->A, delta, cur, 1); /* cur -= A * delta */
+  }
+  for (int32_t i = 0; i < n; ++i) x[i] = lv->gamma * x[i];
+  free(cur);
+  free(delta);
+}
+
+void orc_smoother_apply(const ig_level *lv, int32_t n, const double *r, double *x, int dir) {
+  if (lv->smoother_kind == IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ)
+    orc_ms_apply(lv, n, r, x, dir);
+  else
+    orc_as_apply(lv, n, r, x); /* additive: both directions agree (smoothers.cpp:174-184) */
+}
+
 void orc_coarse_solve(const ig_coarse *co, const double *r, double *x) {
   const int n = co->n, rk = co->rank;
   double *y = (double *)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
@@ -152,7 +199,7 @@ int orc_vcycle_at(const ig_level *levels, int32_t n_levels, const ig_coarse *co,
   double *rc = (double *)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1));
   double *xc = (double *)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1));
 
-  orc_as_apply(lv, n, r, x);                          /* x = S(r, Forward)        */
+  orc_smoother_apply(lv, n, r, x, 0);                 /* x = S(r, Forward)        */
   memcpy(res, r, sizeof(double) * (size_t)n);
   orc_spmv(&lv->A, x, res, 1);                        /* res = r - A x            */
   orc_spmv(&lv->R, res, rc, 0);                       /* R res                    */
@@ -160,7 +207,7 @@ int orc_vcycle_at(const ig_level *levels, int32_t n_levels, const ig_coarse *co,
   orc_spmv_t(&lv->R, xc, tmp);                        /* correction = R^T coarse_x */
   for (int32_t i = 0; i < n; ++i) x[i] = x[i] + tmp[i];
   orc_spmv(&lv->A, tmp, res, 1);                      /* res -= A correction      */
-  orc_as_apply(lv, n, res, tmp);                      /* S(res, Reverse) == Forward for AS */
+  orc_smoother_apply(lv, n, res, tmp, 1);             /* S(res, Reverse)          */
   for (int32_t i = 0; i < n; ++i) x[i] = x[i] + tmp[i];
   free(res);
   free(tmp);

@@ -11,7 +11,8 @@
  *   pcg              proj/src/solvers.cpp:17-71
  *   vcycle_at        proj/src/multigrid.cpp:90-108
  *   coarse_solve     proj/src/multigrid.cpp:77-88
- *   Smoother::apply  proj/src/smoothers.cpp:169-184 (additive Schwarz)
+ *   Smoother::apply  proj/src/smoothers.cpp:169-184 (additive Schwarz),
+ *                    :186-208 (colored multiplicative Schwarz sweep)
  *   LLT::solve       Eigen (forward column-oriented with L, backward row-dot with L^T)
  *   SpMV             Eigen RowMajor sparse*dense: per-row ascending sum
  *
@@ -49,6 +50,11 @@ void orc_spmv(const ig_csr *A, const double *x, double *y, int resid);
 void orc_spmv_t(const ig_csr *A, const double *x, double *y);
 /* Smoother::apply for additive Schwarz: x = gamma * sum_b P_b L_b^-T L_b^-1 P_b^T r. */
 void orc_as_apply(const ig_level *lv, int32_t n, const double *r, double *x);
+/* Smoother::apply for multiplicative Schwarz (colored sweep): dir 0 =
+ * Forward (colours descending), 1 = Reverse (ascending). */
+void orc_ms_apply(const ig_level *lv, int32_t n, const double *r, double *x, int dir);
+/* The level's smoother (additive or multiplicative by smoother_kind). */
+void orc_smoother_apply(const ig_level *lv, int32_t n, const double *r, double *x, int dir);
 void orc_coarse_solve(const ig_coarse *co, const double *r, double *x);
 /* MgHierarchy::vcycle_at(l, r). Returns 0, or 3 on bad arguments. */
 int orc_vcycle_at(const ig_level *levels, int32_t n_levels, const ig_coarse *co,

@@ -93,7 +93,7 @@ def _check(lib, rc: int, what: str):
 # ------------------------------------------------------------ host setup ---
 @dataclasses.dataclass
 class SmootherConfig:
-    """smoothers.hpp:18-22.  Only additive Schwarz runs on the device."""
+    """smoothers.hpp:18-22.  Additive and multiplicative Schwarz run on the device."""
     kind: str = "additive-schwarz"
     gamma: float = 0.0          # 0 = automatic 1/max N_K
     filter_ratio: float = 1e-16
@@ -266,6 +266,13 @@ class Case:
         fptr = np.ctypeslib.as_array(b.fac_ptr, (nb + 1,))
         fac = np.ctypeslib.as_array(b.fac, (int(fptr[-1]),))
         return ptr, dofs, fptr, fac
+
+    def colors(self, l: int):
+        """(color_of per block, n_colors) of level l (multiplicative sweeps; None otherwise)."""
+        b = self._lv[l].blocks
+        if b.n_colors == 0 or not b.color_of:
+            return None
+        return np.ctypeslib.as_array(b.color_of, (b.n_blocks,)), b.n_colors
 
     def coarse(self):
         co = self._co.contents

@@ -23,7 +23,7 @@ class ig_csr(C.Structure):
 
 class ig_blocks(C.Structure):
     _fields_ = [("n_blocks", i32), ("blk_ptr", P(i32)), ("blk_dofs", P(i32)),
-                ("fac_ptr", P(i64)), ("fac", P(f64))]
+                ("fac_ptr", P(i64)), ("fac", P(f64)), ("n_colors", i32), ("color_of", P(i32))]
 
 
 class ig_level(C.Structure):

@@ -574,6 +574,18 @@ struct Level {
   double* res = nullptr;
   double* cor = nullptr;
   double* ybuf = nullptr;
+  // Multiplicative Schwarz (smoother_kind MULTIPLICATIVE_SCHWARZ).
+  bool ms = false;
+  double gamma = 1.0;
+  struct MsColor {
+    AsGroups G{};
+    int32_t n_items = 0;   // warp work items of the block solves
+    DevSell S;             // the colour's columns of A over the rows they touch
+    int32_t* rowmap = nullptr;
+    int64_t n_dofs = 0;    // DOFs solved in this colour
+  };
+  std::vector<MsColor> colors;  // [colour]; empty colours have n_items == 0
+  double *ms_cur = nullptr, *ms_delta = nullptr, *ms_x = nullptr;
 };
 
 // Algorithmic byte counts (CSR-minimal traffic).
@@ -820,7 +832,14 @@ struct ig_hier {
   // Smoother::apply (AS).  Fork: the block solves run on the side stream while
   // the singleton fast path runs on the main stream; join; then the DOFs with
   // contribution lists (and, in PCG on the finest level, r . z).
-  void smoother(const Level& l, const double* r, double* x, bool acc, PcgState* s, const double* rdot) {
+  // Smoother::apply(r, dir) (smoothers.cpp:169-208); dir < 0: Forward for the
+  // pre-smoother (acc = false), Reverse for the post-smoother (acc = true),
+  // as vcycle_at uses them (multigrid.cpp:99, :106).
+  void smoother(const Level& l, const double* r, double* x, bool acc, PcgState* s, const double* rdot, int dir = -1) {
+    if (l.ms) {
+      ms_smoother(l, r, x, acc, s, rdot, dir < 0 ? (acc ? 1 : 0) : dir);
+      return;
+    }
     const bool multi = l.n_multi > 0;
     if (multi) {
       CK(cudaEventRecord(ev_fork, stream));
@@ -851,6 +870,27 @@ struct ig_hier {
         launch(k_as_complex<false>, gc, kCta, 0, stream, l.S, r, l.ybuf, x, s);
     }
     CK(cudaGetLastError());
+  }
+  void ms_smoother(const Level& l, const double* r, double* out, bool acc, PcgState* s, const double* rdot, int dir) {
+    const int32_t n = l.n;
+    const int C = static_cast<int>(l.colors.size());
+    launch(k_ms_init, grid_of(n), kCta, 0, stream, n, r, l.ms_cur, l.ms_x, s);
+    for (int step = 0; step < C; ++step) {
+      const int c = dir == 0 ? C - 1 - step : step;
+      const Level::MsColor& mc = l.colors[c];
+      if (mc.n_items == 0) continue;  // `if (!any) continue;`
+      const unsigned gb = static_cast<unsigned>((static_cast<int64_t>(mc.n_items) * 32 + 127) / 128);
+      launch(k_ms_blocks, gb, 128, 0, stream, mc.G, l.ms_cur, l.ms_delta, l.ms_x, s);
+      if (step + 1 < C)
+        launch(k_ms_update, grid_of(mc.S.s.n_rows), kCta, 0, stream, mc.S.s, mc.rowmap, l.ms_delta, l.ms_cur, s);
+    }
+    if (rdot) {
+      if (acc) launch(k_ms_finish<true, true>, grid_of(n), kCta, 0, stream, n, l.gamma, l.ms_x, out, rdot, s, partials);
+      else launch(k_ms_finish<false, true>, grid_of(n), kCta, 0, stream, n, l.gamma, l.ms_x, out, rdot, s, partials);
+    } else {
+      if (acc) launch(k_ms_finish<true, false>, grid_of(n), kCta, 0, stream, n, l.gamma, l.ms_x, out, rdot, s, partials);
+      else launch(k_ms_finish<false, false>, grid_of(n), kCta, 0, stream, n, l.gamma, l.ms_x, out, rdot, s, partials);
+    }
   }
   void coarse_launch(bool sm, const double* r, double* x, PcgState* s) {
     const bool big = coarse_threads > 256;
@@ -1097,6 +1137,11 @@ void check_csr(const ig_csr& a, const char* what) {
         throw Error(IG_INVALID_ARGUMENT, std::string(what) + ": column indices out of range or not ascending");
 }
 
+AsGroups build_groups(ig_hier& h, const ig_blocks& B, std::vector<int32_t> grouped, const std::vector<int32_t>& warped,
+                      const std::vector<int32_t>& ypos);
+void build_gather(ig_hier& h, Level& L, const ig_level& src, const std::vector<int32_t>& ypos,
+                  const std::vector<double>& sval);
+
 // Smoother layout for one level (see kernels.cuh: AsGroups / AsGather).
 void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
   const ig_blocks& B = src.blocks;
@@ -1133,6 +1178,19 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
   }
   if (yl > INT32_MAX) throw Error(IG_INVALID_ARGUMENT, "smoother: too many block entries");
   L.n_multi = static_cast<int32_t>(grouped.size() + warped.size());
+  L.G = build_groups(h, B, grouped, warped, ypos);
+  L.ybuf = h.alloc<double>(static_cast<size_t>(std::max<int64_t>(yl, 1)));
+  build_gather(h, L, src, ypos, sval);
+}
+
+// Batched block-solve layout (kernels.cuh AsGroups) for a subset of blocks:
+// `grouped` thread-per-block (sorted by size, descending, stable), `warped`
+// warp-per-block.  ypos: ybuf offsets (additive) -- unused by the
+// multiplicative sweep, which writes by DOF.
+AsGroups build_groups(ig_hier& h, const ig_blocks& B, std::vector<int32_t> grouped, const std::vector<int32_t>& warped,
+                      const std::vector<int32_t>& ypos) {
+  auto bsize = [&](int32_t b) { return B.blk_ptr[b + 1] - B.blk_ptr[b]; };
+  AsGroups G{};
   std::stable_sort(grouped.begin(), grouped.end(), [&](int32_t a, int32_t b) { return bsize(a) > bsize(b); });
   const int32_t ng = static_cast<int32_t>((grouped.size() + 31) / 32);
   const size_t ng1 = static_cast<size_t>(std::max(ng, 1));
@@ -1153,7 +1211,7 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
       const int32_t b = grouped[idx];
       const int32_t s = bsize(b);
       gsize[idx] = s;
-      gypos[idx] = ypos[b];
+      gypos[idx] = ypos.empty() ? 0 : ypos[b];
       for (int i = 0; i < s; ++i) gdofs[gdoff[g] + static_cast<int64_t>(i) * 32 + lane] = B.blk_dofs[B.blk_ptr[b] + i];
       const double* f = B.fac + B.fac_ptr[b];
       for (int j = 0; j < s; ++j)
@@ -1163,14 +1221,14 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
         }
     }
   }
-  L.G.n_groups = ng;
-  L.G.smax = h.upload(gsmax.data(), gsmax.size());
-  L.G.dof_off = h.upload(gdoff.data(), gdoff.size());
-  L.G.fac_off = h.upload(gfoff.data(), gfoff.size());
-  L.G.size = h.upload(gsize.data(), gsize.size());
-  L.G.ypos = h.upload(gypos.data(), gypos.size());
-  L.G.dofs = h.upload(gdofs.data(), gdofs.size());  // empty -> 1-element placeholder
-  L.G.fac = h.upload(gfac.data(), gfac.size());
+  G.n_groups = ng;
+  G.smax = h.upload(gsmax.data(), gsmax.size());
+  G.dof_off = h.upload(gdoff.data(), gdoff.size());
+  G.fac_off = h.upload(gfoff.data(), gfoff.size());
+  G.size = h.upload(gsize.data(), gsize.size());
+  G.ypos = h.upload(gypos.data(), gypos.size());
+  G.dofs = h.upload(gdofs.data(), gdofs.size());  // empty -> 1-element placeholder
+  G.fac = h.upload(gfac.data(), gfac.size());
   // Warp blocks: contiguous DOF lists and full column-major factors.
   {
     const size_t nw = warped.size();
@@ -1181,21 +1239,29 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
       const int32_t b = warped[k];
       const int32_t s = bsize(b);
       wsize[k] = s;
-      wypos[k] = ypos[b];
+      wypos[k] = ypos.empty() ? 0 : ypos[b];
       wdoff[k] = static_cast<int64_t>(wdofs.size());
       wfoff[k] = static_cast<int64_t>(wfac.size());
       wdofs.insert(wdofs.end(), B.blk_dofs + B.blk_ptr[b], B.blk_dofs + B.blk_ptr[b + 1]);
       wfac.insert(wfac.end(), B.fac + B.fac_ptr[b], B.fac + B.fac_ptr[b] + static_cast<int64_t>(s) * s);
     }
-    L.G.n_wblocks = static_cast<int32_t>(nw);
-    L.G.w_size = h.upload(wsize.data(), wsize.size());
-    L.G.w_ypos = h.upload(wypos.data(), wypos.size());
-    L.G.w_dof_off = h.upload(wdoff.data(), wdoff.size());
-    L.G.w_fac_off = h.upload(wfoff.data(), wfoff.size());
-    L.G.w_dofs = h.upload(wdofs.data(), wdofs.size());
-    L.G.w_fac = h.upload(wfac.data(), wfac.size());
+    G.n_wblocks = static_cast<int32_t>(nw);
+    G.w_size = h.upload(wsize.data(), wsize.size());
+    G.w_ypos = h.upload(wypos.data(), wypos.size());
+    G.w_dof_off = h.upload(wdoff.data(), wdoff.size());
+    G.w_fac_off = h.upload(wfoff.data(), wfoff.size());
+    G.w_dofs = h.upload(wdofs.data(), wdofs.size());
+    G.w_fac = h.upload(wfac.data(), wfac.size());
   }
-  L.ybuf = h.alloc<double>(static_cast<size_t>(std::max<int64_t>(yl, 1)));
+  return G;
+}
+
+// Per-DOF gather of the additive smoother (kernels.cuh AsGather).
+void build_gather(ig_hier& h, Level& L, const ig_level& src, const std::vector<int32_t>& ypos,
+                  const std::vector<double>& sval) {
+  const ig_blocks& B = src.blocks;
+  const int32_t n = L.n, nb = B.n_blocks;
+  auto bsize = [&](int32_t b) { return B.blk_ptr[b + 1] - B.blk_ptr[b]; };
   // Per-DOF contribution lists in ascending block order; DOFs whose only
   // contribution is their own singleton take the head >= 0 fast path.
   std::vector<int32_t> cnt(static_cast<size_t>(n) + 1, 0);
@@ -1235,6 +1301,81 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
   L.S.centry = h.upload(cent.data(), cent.size());
   L.S.sval = h.upload(sval.data(), sval.size());
   L.n_complex = static_cast<int32_t>(cptr.size() - 1);
+}
+
+// Multiplicative (colored) Schwarz layout (kernels.cuh k_ms_*): per colour,
+// the batched block solves of its blocks and the colour's columns of A over
+// the rows they touch (ascending row, ascending column: A's own order).
+void build_ms(ig_hier& h, Level& L, const ig_level& src, const ig_csr& A) {
+  const ig_blocks& B = src.blocks;
+  const int32_t n = L.n, nb = B.n_blocks;
+  if (nb <= 0 || !B.blk_ptr || !B.blk_dofs || !B.fac_ptr || !B.fac)
+    throw Error(IG_INVALID_ARGUMENT, "smoother: empty block layout");
+  if (B.n_colors <= 0 || !B.color_of) throw Error(IG_INVALID_ARGUMENT, "multiplicative smoother: no block colours");
+  const int C = B.n_colors;
+  L.ms = true;
+  L.gamma = src.gamma;
+  L.n_blocks = nb;
+  auto bsize = [&](int32_t b) { return B.blk_ptr[b + 1] - B.blk_ptr[b]; };
+  std::vector<std::vector<int32_t>> cb(static_cast<size_t>(C));
+  for (int32_t b = 0; b < nb; ++b) {
+    const int32_t s = bsize(b);
+    if (s <= 0) throw Error(IG_INVALID_ARGUMENT, "smoother: empty block");
+    if (s > 128) throw Error(IG_INVALID_ARGUMENT, "smoother: block larger than 128 DOFs");
+    if (B.color_of[b] < 0 || B.color_of[b] >= C) throw Error(IG_INVALID_ARGUMENT, "smoother: colour out of range");
+    for (int32_t i = B.blk_ptr[b]; i < B.blk_ptr[b + 1]; ++i)
+      if (B.blk_dofs[i] < 0 || B.blk_dofs[i] >= n) throw Error(IG_INVALID_ARGUMENT, "smoother: DOF out of range");
+    L.sum_s += s;
+    L.sum_s2 += static_cast<int64_t>(s) * s;
+    L.packed_F += static_cast<int64_t>(s) * (s + 1) / 2;
+    if (s > 1) ++L.n_multi;
+    cb[B.color_of[b]].push_back(b);
+  }
+  std::vector<int32_t> mark(static_cast<size_t>(n), -1);
+  L.colors.resize(static_cast<size_t>(C));
+  std::vector<int32_t> ptr, col, rowmap;
+  std::vector<double> val;
+  for (int c = 0; c < C; ++c) {
+    Level::MsColor& mc = L.colors[c];
+    if (cb[c].empty()) continue;
+    std::vector<int32_t> grouped, warped;
+    for (int32_t b : cb[c]) {
+      const int32_t s = bsize(b);
+      if (s >= 9 && s <= 32)
+        warped.push_back(b);
+      else
+        grouped.push_back(b);
+      for (int32_t i = B.blk_ptr[b]; i < B.blk_ptr[b + 1]; ++i) {
+        if (mark[B.blk_dofs[i]] == c) throw Error(IG_INVALID_ARGUMENT, "smoother: same-colour blocks share a DOF");
+        mark[B.blk_dofs[i]] = c;
+        ++mc.n_dofs;
+      }
+    }
+    mc.G = build_groups(h, B, grouped, warped, {});
+    mc.n_items = mc.G.n_groups + mc.G.n_wblocks;
+    ptr.assign(1, 0);
+    col.clear();
+    val.clear();
+    rowmap.clear();
+    for (int32_t i = 0; i < n; ++i) {
+      const size_t before = col.size();
+      for (int32_t k = A.row_ptr[i]; k < A.row_ptr[i + 1]; ++k)
+        if (mark[A.col_idx[k]] == c) {
+          col.push_back(A.col_idx[k]);
+          val.push_back(A.val[k]);
+        }
+      if (col.size() > before) {
+        rowmap.push_back(i);
+        ptr.push_back(static_cast<int32_t>(col.size()));
+      }
+    }
+    const int32_t nr = static_cast<int32_t>(rowmap.size());
+    mc.S = h.upload_sell(to_sell(nr, n, ptr.data(), col.data(), val.data()), static_cast<int64_t>(col.size()));
+    mc.rowmap = h.upload(rowmap.data(), rowmap.size());
+  }
+  L.ms_cur = h.alloc<double>(n);
+  L.ms_delta = h.alloc<double>(n);
+  L.ms_x = h.alloc<double>(n);
 }
 
 }  // namespace
@@ -1320,8 +1461,8 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       check_csr(s.R, "R");
       if (s.R.n_cols != L.n || s.R.n_rows != levels[l - 1].A.n_rows)
         throw Error(IG_INVALID_ARGUMENT, "R has the wrong shape");
-      if (s.smoother_kind != IG_SMOOTHER_ADDITIVE_SCHWARZ)
-        throw Error(IG_UNSUPPORTED, "device smoother: only additive Schwarz is implemented");
+      if (s.smoother_kind != IG_SMOOTHER_ADDITIVE_SCHWARZ && s.smoother_kind != IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ)
+        throw Error(IG_UNSUPPORTED, "device smoother: additive or multiplicative Schwarz only");
       I.nnz_R[l] = s.R.nnz;
       L.A = h->make_matrix(s.A.n_rows, s.A.n_cols, s.A.row_ptr, s.A.col_idx, s.A.val, s.A.nnz);
       L.R = h->make_matrix(s.R.n_rows, s.R.n_cols, s.R.row_ptr, s.R.col_idx, s.R.val, s.R.nnz);
@@ -1331,7 +1472,10 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       L.P = h->make_matrix(s.R.n_cols, s.R.n_rows, tp.data(), tc.data(), tv.data(), s.R.nnz);
       L.res = h->alloc<double>(L.n);
       L.cor = h->alloc<double>(L.n);
-      build_smoother(*h, L, s);
+      if (s.smoother_kind == IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ)
+        build_ms(*h, L, s, s.A);
+      else
+        build_smoother(*h, L, s);
       I.sell_slots_A[l] = L.A.slots;
       I.n_blocks[l] = L.n_blocks;
       I.n_multi_blocks[l] = L.n_multi;
@@ -1402,7 +1546,11 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     for (int l = 1; l < n_levels; ++l) {
       const Level& L = h->lv[l];
       const int64_t n = L.n, nc = h->lv[l - 1].n;
-      const int64_t as = 8 * L.packed_F + 8 * L.sum_s + 4 * (L.n_blocks + 1) + 4 * (n + 1) + 16 * n;
+      int64_t as = 8 * L.packed_F + 8 * L.sum_s + 4 * (L.n_blocks + 1) + 4 * (n + 1) + 16 * n;
+      if (L.ms) {  // colored sweep: block solves + the colours' residual updates + init/finish
+        as = 8 * L.packed_F + 16 * L.sum_s + 40 * n;
+        for (const auto& mc : L.colors) as += 12 * mc.S.nnz + 16 * mc.n_dofs;
+      }
       vc += 2 * bytes_spmv(n, n, L.A.nnz, true);
       vc += 2 * as + 8 * n;                                              // second application accumulates
       vc += bytes_spmv(nc, n, L.R.nnz, false);                           // R
@@ -1411,7 +1559,12 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
              layout_spmv(L.P, n, nc, false) + 16 * n;
       // smoother: [blocks] + simple + [complex | finish_red on the finest], twice;
       // plus SpMV-residual x2, restriction, prolongation
-      const int per_app = (L.n_multi > 0 ? 1 : 0) + 1 + (L.S.n_complex > 0 ? 1 : 0);
+      int per_app = (L.n_multi > 0 ? 1 : 0) + 1 + (L.S.n_complex > 0 ? 1 : 0);
+      if (L.ms) {
+        int ne = 0;
+        for (const auto& mc : L.colors) ne += mc.n_items > 0 ? 1 : 0;
+        per_app = 2 + 2 * ne - 1;  // init, blocks + update per colour (last: none), finish
+      }
       kv += 2 * per_app + 4 + (l == n_levels - 1 && L.S.n_complex == 0 ? 1 : 0);
       I.explicit_vals_A[l] = L.A.explicit_vals;
       I.explicit_cols_A[l] = L.A.explicit_cols;

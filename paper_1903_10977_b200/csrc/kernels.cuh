@@ -482,9 +482,23 @@ __device__ __forceinline__ int packed_idx(int i, int j, int smax) {
   return j * smax - (j * (j - 1)) / 2 + (i - j);
 }
 
-template <int SM>
+// Output: additive (MS = false) -> ybuf[pos + i]; multiplicative sweep
+// (MS = true) -> ybuf is the colour's delta vector: delta[d] = 0 + y_i and
+// xms[d] += delta[d] (smoothers.cpp:199-204; same-colour blocks are disjoint).
+template <bool MS>
+__device__ __forceinline__ void block_out(double* ybuf, double* xms, int pos_or_dof, double y) {
+  if (MS) {
+    const double dv = 0.0 + y;
+    ybuf[pos_or_dof] = dv;
+    xms[pos_or_dof] = xms[pos_or_dof] + dv;
+  } else {
+    ybuf[pos_or_dof] = y;
+  }
+}
+
+template <int SM, bool MS = false>
 __device__ __forceinline__ void block_solve(const AsGroups& G, int g, int lane, int s, int smax,
-                                            const double* __restrict__ r, double* ybuf) {
+                                            const double* __restrict__ r, double* ybuf, double* xms = nullptr) {
   double y[SM], Lp[SM * (SM + 1) / 2];
   const int32_t* dp = G.dofs + G.dof_off[g] + lane;
   const double* fp = G.fac + G.fac_off[g] + lane;
@@ -521,12 +535,13 @@ __device__ __forceinline__ void block_solve(const AsGroups& G, int g, int lane, 
   const int pos = G.ypos[g * 32 + lane];
 #pragma unroll
   for (int i = 0; i < SM; ++i)
-    if (i < s) ybuf[pos + i] = y[i];
+    if (i < s) block_out<MS>(ybuf, xms, MS ? dp[i * 32] : pos + i, y[i]);
 }
 
 // Generic (any size) fallback with local memory.
+template <bool MS = false>
 __device__ __noinline__ void block_solve_any(const AsGroups& G, int g, int lane, int s, int smax,
-                                             const double* __restrict__ r, double* ybuf) {
+                                             const double* __restrict__ r, double* ybuf, double* xms = nullptr) {
   double y[128];
   const int32_t* dp = G.dofs + G.dof_off[g] + lane;
   const double* fp = G.fac + G.fac_off[g] + lane;
@@ -542,11 +557,12 @@ __device__ __noinline__ void block_solve_any(const AsGroups& G, int g, int lane,
     y[i] = (y[i] - acc) / fp[packed_idx(i, i, smax) * 32];
   }
   const int pos = G.ypos[g * 32 + lane];
-  for (int i = 0; i < s; ++i) ybuf[pos + i] = y[i];
+  for (int i = 0; i < s; ++i) block_out<MS>(ybuf, xms, MS ? dp[i * 32] : pos + i, y[i]);
 }
 
+template <bool MS = false>
 __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int lane,
-                                                 const double* __restrict__ r, double* ybuf) {
+                                                 const double* __restrict__ r, double* ybuf, double* xms = nullptr) {
   const int s = G.w_size[b];
   const double* f = G.w_fac + G.w_fac_off[b];
   const int32_t* dp = G.w_dofs + G.w_dof_off[b];
@@ -599,25 +615,26 @@ __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int l
       }
     }
   }
-  if (lane < s) ybuf[G.w_ypos[b] + lane] = y;
+  if (lane < s) block_out<MS>(ybuf, xms, MS ? dp[lane] : G.w_ypos[b] + lane, y);
 }
 
 // One warp-sized work item w of phase 1 (group of small blocks or a warp block).
+template <bool MS = false>
 __device__ __forceinline__ void as_blocks_item(const AsGroups& G, int w, int lane, const double* __restrict__ r,
-                                               double* ybuf) {
+                                               double* ybuf, double* xms = nullptr) {
   if (w < G.n_groups) {
     const int g = w;
     const int s = G.size[g * 32 + lane];
     const int smax = G.smax[g];  // warp-uniform
     if (s == 0) return;
     if (smax <= 4)
-      block_solve<4>(G, g, lane, s, smax, r, ybuf);
+      block_solve<4, MS>(G, g, lane, s, smax, r, ybuf, xms);
     else if (smax <= 8)
-      block_solve<8>(G, g, lane, s, smax, r, ybuf);
+      block_solve<8, MS>(G, g, lane, s, smax, r, ybuf, xms);
     else
-      block_solve_any(G, g, lane, s, smax, r, ybuf);
+      block_solve_any<MS>(G, g, lane, s, smax, r, ybuf, xms);
   } else if (w - G.n_groups < G.n_wblocks) {
-    warp_block_solve(G, w - G.n_groups, lane, r, ybuf);
+    warp_block_solve<MS>(G, w - G.n_groups, lane, r, ybuf, xms);
   }
 }
 __global__ void __launch_bounds__(128) k_as_blocks(AsGroups G, const double* __restrict__ r,
@@ -822,6 +839,68 @@ __global__ void __launch_bounds__(kCta) k_pcg_rz(int32_t n, const double* __rest
   double rz;
   if (last_cta_total(prod, partials, &st->counter[2], &rz))
     if (threadIdx.x == 0) rz_update(st, rz);
+}
+
+// ------------------------------------------ multiplicative Schwarz -------
+// Colored multiplicative sweep (smoothers.cpp:186-208), one colour at a time:
+//   k_ms_init    cur = r, xms = 0
+//   per colour   k_ms_blocks: the colour's block solves on the frozen cur,
+//                  delta[d] = 0 + y, xms[d] += delta[d] (disjoint DOFs);
+//                k_ms_update (all colours but the last): cur_i -= sum over
+//                  the colour's columns of A_ik delta_k, ascending k
+//   k_ms_finish  out = gamma * xms (ACC: out += gamma * xms); RED: r . z.
+// The reference's update is a full product A * delta; every column outside
+// the colour holds +0 there, and adding the +-0 products leaves a running
+// sum that starts at +0 unchanged (it can never be -0), so summing only the
+// colour's columns in ascending order gives the same bits.  x += delta for
+// DOFs outside the colour adds +0 to a value that is never -0: also a no-op.
+__global__ void __launch_bounds__(kCta) k_ms_init(int32_t n, const double* __restrict__ r, double* cur,
+                                                  double* xms, const PcgState* st) {
+  pdl_entry();
+  if (pcg_done(st)) return;
+  const int i = blockIdx.x * kCta + threadIdx.x;
+  if (i >= n) return;
+  cur[i] = r[i];
+  xms[i] = 0.0;
+}
+__global__ void __launch_bounds__(128) k_ms_blocks(AsGroups G, const double* __restrict__ cur, double* delta,
+                                                   double* xms, const PcgState* st) {
+  pdl_entry();
+  if (pcg_done(st)) return;
+  as_blocks_item<true>(G, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, cur, delta, xms);
+}
+// S: the colour's columns of A over the rows they touch (compact row j is
+// row rowmap[j] of A; entries keep A's ascending column order).
+__global__ void __launch_bounds__(kCta) k_ms_update(Sell S, const int32_t* __restrict__ rowmap,
+                                                    const double* __restrict__ delta, double* cur,
+                                                    const PcgState* st) {
+  pdl_entry();
+  if (pcg_done(st)) return;
+  const int j = blockIdx.x * kCta + threadIdx.x;
+  if (j >= S.n_rows) return;
+  const double acc = sell_row<false, 3>(S, j, delta);
+  const int i = rowmap[j];
+  cur[i] = cur[i] - acc;
+}
+template <bool ACC, bool RED>
+__global__ void __launch_bounds__(kCta) k_ms_finish(int32_t n, double gamma, const double* __restrict__ xms,
+                                                    double* out, const double* rdot, PcgState* st,
+                                                    double* partials) {
+  pdl_entry();
+  if (pcg_done(st)) return;
+  const int i = blockIdx.x * kCta + threadIdx.x;
+  double prod = 0.0;
+  if (i < n) {
+    const double v = gamma * xms[i];
+    const double o = ACC ? out[i] + v : v;
+    out[i] = o;
+    if (RED) prod = rdot[i] * o;
+  }
+  if (RED) {
+    double rz;
+    if (last_cta_total(prod, partials, &st->counter[2], &rz))
+      if (threadIdx.x == 0) rz_update(st, rz);
+  }
 }
 
 // ------------------------------------------------------------ coarse ------

@@ -393,6 +393,8 @@ void factorize_blocks(const Csr& A, Blocks& b, double filter_ratio, int threads)
   Blocks out;
   out.owners = b.owners;
   out.max_nk = b.max_nk;
+  out.color = std::move(b.color);  // colours stay with the pre-filter block indices
+  out.n_colors = b.n_colors;
   out.ptr.reserve(static_cast<size_t>(nb) + 1);
   out.fptr.reserve(static_cast<size_t>(nb) + 1);
   int64_t filtered = 0;
@@ -530,6 +532,8 @@ void igh_case::wire() {
     bb.blk_dofs = B[l].dofs.data();
     bb.fac_ptr = B[l].fptr.data();
     bb.fac = B[l].fac.data();
+    bb.n_colors = B[l].n_colors;
+    bb.color_of = B[l].color.empty() ? nullptr : B[l].color.data();
   }
   co.n = A.empty() ? 0 : A[0].nr;
   co.rank = rank;
@@ -679,6 +683,21 @@ int igh_build(const igh_config* cfg, igh_case** out) {
         b = select_blocks(*c->spaces[l], threads);
         b.max_nk = max_blocks_per_element(b, *c->spaces[l]);
       }
+      // Colours of the pre-filter layout (make_smoother: color_blocks runs
+      // before factorize_blocks, smoothers.cpp:228-232).
+      if (cfg->smoother_kind == IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ) {
+        if (thb) {
+          const GSpace& gs = *c->gspaces[l];
+          color_blocks(b, static_cast<int>(gs.el.size()), [&](int d, auto&& f) {
+            for (int e : gs.supp[d]) f(e);
+          });
+        } else {
+          const Space& sp = *c->spaces[l];
+          color_blocks(b, static_cast<int>(sp.el_ix.size()), [&](int d, auto&& f) {
+            for (int64_t t = sp.supp_ptr[d]; t < sp.supp_ptr[d + 1]; ++t) f(sp.supp_el[t]);
+          });
+        }
+      }
       factorize_blocks(c->A[l], b, cfg->filter_ratio, threads);
       double gm = cfg->gamma;
       if (gm <= 0.0) {
@@ -814,7 +833,7 @@ int igh_eta(const igh_config* cfg, double* eta, int64_t* cut, int32_t* n_dofs) {
 
 }  // extern "C"
 
-// ---- .igh file: little-endian binary, version 1 ---------------------------
+// ---- .igh file: little-endian binary, version 2 (v1 = no block colours) ----
 namespace {
 template <typename T>
 void wr(std::ofstream& f, const T* p, size_t n) {
@@ -853,7 +872,7 @@ void rcsr(std::ifstream& f, Csr& m) {
   rv(f, m.col);
   rv(f, m.val);
 }
-const char kMagic[8] = {'I', 'G', 'H', '1', 0, 0, 0, 1};
+const char kMagic[8] = {'I', 'G', 'H', '1', 0, 0, 0, 2};  // last byte: version
 }  // namespace
 
 extern "C" {
@@ -878,6 +897,8 @@ int igh_write(const igh_case* c, const char* path) {
       wv(f, c->B[l].fac);
       wr(f, &c->B[l].max_nk, 1);
       wv(f, c->xyz[l]);
+      wv(f, c->B[l].color);
+      wr(f, &c->B[l].n_colors, 1);
     }
     wv(f, c->coarseL);
     wv(f, c->piv);
@@ -896,7 +917,8 @@ int igh_read(const char* path, igh_case** out) {
     if (!f) return fail(std::string("igh_read: cannot open ") + path);
     char mg[8];
     rd(f, mg, 8);
-    if (std::memcmp(mg, kMagic, 8) != 0) return fail("igh_read: bad magic");
+    if (std::memcmp(mg, kMagic, 7) != 0 || (mg[7] != 1 && mg[7] != 2)) return fail("igh_read: bad magic");
+    const int version = mg[7];
     auto c = std::make_unique<igh_case>();
     int32_t L = 0;
     rd(f, &L, 1);
@@ -921,6 +943,10 @@ int igh_read(const char* path, igh_case** out) {
       rv(f, c->B[l].fac);
       rd(f, &c->B[l].max_nk, 1);
       rv(f, c->xyz[l]);
+      if (version >= 2) {
+        rv(f, c->B[l].color);
+        rd(f, &c->B[l].n_colors, 1);
+      }
     }
     rv(f, c->coarseL);
     rv(f, c->piv);

@@ -240,9 +240,36 @@ struct Blocks {
   std::vector<double> fac;  // s x s column-major lower factors
   int max_nk = 0;
   int64_t filtered_dofs = 0;
+  std::vector<int32_t> color;  // multiplicative sweeps: colour per block (pre-filter)
+  int n_colors = 0;
 };
 Blocks select_blocks(const Space& s, int threads);
 int max_blocks_per_element(const Blocks& b, const Space& s);
+// Greedy colouring in block (owner) order; blocks are adjacent when the
+// physical supports of their members share an element (smoothers.cpp:99-122).
+// supp(d, f) calls f(e) for every element of DOF d's physical support.
+template <typename SuppFn>
+void color_blocks(Blocks& b, int n_elements, SuppFn supp) {
+  constexpr int kW = 8;  // up to 512 colours
+  std::vector<uint64_t> used(static_cast<size_t>(n_elements) * kW, 0);
+  const int nb = static_cast<int>(b.owners.size());
+  b.color.assign(static_cast<size_t>(nb), 0);
+  b.n_colors = 0;
+  std::vector<int> els;
+  for (int k = 0; k < nb; ++k) {
+    els.clear();
+    for (int32_t q = b.ptr[k]; q < b.ptr[k + 1]; ++q) supp(b.dofs[q], [&](int e) { els.push_back(e); });
+    uint64_t m[kW] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int e : els)
+      for (int w = 0; w < kW; ++w) m[w] |= used[static_cast<size_t>(e) * kW + w];
+    int col = 0;
+    while (col < kW * 64 && ((m[col >> 6] >> (col & 63)) & 1u)) ++col;
+    if (col >= kW * 64) throw std::runtime_error("color_blocks: more than 512 colours");
+    b.color[k] = col;
+    b.n_colors = std::max(b.n_colors, col + 1);
+    for (int e : els) used[static_cast<size_t>(e) * kW + (col >> 6)] |= uint64_t(1) << (col & 63);
+  }
+}
 void factorize_blocks(const Csr& A, Blocks& b, double filter_ratio, int threads);
 
 // LAPACK dpstrf('L') restatement (unblocked dpstf2 order).  a: n x n col-major,

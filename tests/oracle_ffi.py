@@ -30,6 +30,8 @@ def lib():
         L.orc_spmv.argtypes = [C.POINTER(_ffi.ig_csr), _dp, _dp, C.c_int]
         L.orc_spmv_t.argtypes = [C.POINTER(_ffi.ig_csr), _dp, _dp]
         L.orc_as_apply.argtypes = [lvp, C.c_int32, _dp, _dp]
+        L.orc_ms_apply.argtypes = [lvp, C.c_int32, _dp, _dp, C.c_int]
+        L.orc_smoother_apply.argtypes = [lvp, C.c_int32, _dp, _dp, C.c_int]
         L.orc_coarse_solve.argtypes = [cop, _dp, _dp]
         L.orc_vcycle_at.argtypes = [lvp, C.c_int32, cop, C.c_int32, _dp, _dp]
         L.orc_pcg.argtypes = [lvp, C.c_int32, cop, C.c_int, _dp, C.c_double, C.c_int32, _dp, _dp,
@@ -72,6 +74,15 @@ def as_apply(levels, l, r):
     r = np.ascontiguousarray(r, np.float64)
     x = np.zeros_like(r)
     lib().orc_as_apply(C.byref(lv[l]), r.shape[0], _p(r), _p(x))
+    return x
+
+
+def smoother_apply(levels, l, r, direction=0):
+    """The level's smoother (additive or multiplicative); direction 0 Forward, 1 Reverse."""
+    lv, nl, co = levels
+    r = np.ascontiguousarray(r, np.float64)
+    x = np.zeros_like(r)
+    lib().orc_smoother_apply(C.byref(lv[l]), r.shape[0], _p(r), _p(x), direction)
     return x
 
 
