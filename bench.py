@@ -90,8 +90,8 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def build_workload(name: str, threads: int):
-    from paper_1903_10977_b200 import build_case, configs
+def build_workload(name: str, threads: int, smoother: str = "as"):
+    from paper_1903_10977_b200 import SmootherConfig, build_case, configs
     if name == "c4":
         cfg = configs.c4(threads=threads)
         desc = ("C4: 3D [0,1]^3 128^3 minus sphere r=0.3 (seed-1 offset), p=2 B-splines, 6 levels, "
@@ -112,6 +112,10 @@ def build_workload(name: str, threads: int):
         desc = f"C2: 2D disc r=0.4 on 512^2, p={p}, 8 levels, additive Schwarz, seed with eta<1e-4"
     else:
         raise SystemExit(f"unknown workload {name}")
+    if smoother == "ms":  # the reference's default smoother (smoothers.hpp:17), SURVEY.md 8(f) row 1
+        cfg.smoother = SmootherConfig("multiplicative-schwarz")
+        desc = desc.replace("additive Schwarz gamma=1/27", "multiplicative (colored) Schwarz")
+        desc = desc.replace("additive Schwarz", "multiplicative (colored) Schwarz")
     t0 = time.perf_counter()
     case = build_case(cfg)
     return case, desc, time.perf_counter() - t0
@@ -166,6 +170,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4")
     ap.add_argument("--threads", type=int, default=0, help="host setup threads (0 = all)")
+    ap.add_argument("--smoother", default="as", choices=["as", "ms"],
+                    help="as: additive Schwarz (the BASELINE configs); ms: multiplicative colored Schwarz")
     ap.add_argument("--cpu-sample-iters", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
@@ -194,7 +200,7 @@ def main():
     if args.no_graph:
         lib.ig_set_option(_ffi.IG_OPT_USE_GRAPH, 0)
 
-    case, desc, t_setup = build_workload(args.workload, args.threads)
+    case, desc, t_setup = build_workload(args.workload, args.threads, args.smoother)
     t0 = time.perf_counter()
     h = MgHierarchy(case)
     t_upload = time.perf_counter() - t0
@@ -360,7 +366,7 @@ def main():
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    case, desc, t_setup = build_workload(args.workload, args.threads)
+    case, desc, t_setup = build_workload(args.workload, args.threads, args.smoother)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_ffi as orc
     # Each step times a bounded sample (the first iterations of the same
@@ -379,6 +385,8 @@ def run_reference(args, world, rank):
         # pinned by tests/test_thb.py, tests/test_gpu_configs.py and the C4 golden.
         iters_full = {"c1": 25, "c2": 27, "c2-1": 18, "c2-2": 27, "c2-3": 55, "c2-4": 106,
                       "c3": 38, "c4": 115, "c5": 37}[args.workload]
+        if args.smoother == "ms":
+            st, _, _, iters_full, _ = orc.pcg(case.levels_c(), case.b, tol=1e-8, maxit=1000, mode=orc.SEQ)
     t_full = per_unit * (iters_full + 1)
     v = case.n / t_full
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
