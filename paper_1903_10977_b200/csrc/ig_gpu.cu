@@ -87,7 +87,7 @@ struct HostSell {
 
 int g_use_dict = 1;
 int g_spmv_variant = 3;  // profiles/spmv_variants.py: best full-PCG time on C4
-int g_small_rows = 40000;  // matrices up to this many rows use k_spmv_grp (profiles/option_sweep.py)
+int g_small_rows = 10000;  // matrices up to this many rows use k_spmv_grp (profiles/option_sweep.py: C4 173.2 -> 169.5 ms, C2 8.0 -> 7.3 ms vs 40000)
 // Levels up to this many rows (below the finest) run in k_vtail; 0 = off.
 // Off by default: measured SLOWER than the graph-launched kernels (C5 V-cycle
 // 285 -> 538 us; profiles/tail_profile.py): each of the ~33 phases costs a

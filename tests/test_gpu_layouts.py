@@ -24,11 +24,21 @@ def layout(request):
     lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, small)
     lib.ig_set_option(_ffi.IG_OPT_PSELL, psell)
     yield request.param
-    lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 40000)
+    lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 10000)
     lib.ig_set_option(_ffi.IG_OPT_PSELL, 1)
 
 
-@pytest.mark.parametrize("case_name", ["c1_case", "d3_case", "star_case"])
+@pytest.fixture(scope="module")
+def c3_small_case():
+    """A C3-like perforated plate (Dirichlet on the box edges) at 128^2, 6
+    levels: restriction/prolongation shapes whose scaled offset bases exceed
+    the column range (regression for the padded-gather bound)."""
+    from paper_1903_10977_b200 import CaseConfig, SmootherConfig, build_case, configs
+    return build_case(CaseConfig(geometry=configs.c3_geometry(1, holes=8), resolution=(128, 128, 1), degree=2, levels=6,
+                                 dirichlet_box_sides=True, smoother=SmootherConfig("additive-schwarz")))
+
+
+@pytest.mark.parametrize("case_name", ["c1_case", "d3_case", "star_case", "c3_small_case"])
 def test_layout_bitwise(request, layout, case_name):
     from paper_1903_10977_b200 import MgHierarchy, pcg
     case = request.getfixturevalue(case_name)
@@ -62,7 +72,7 @@ def test_pattern_sell_nonfinite_and_signed_zero(star_case):
     try:
         h = MgHierarchy(star_case)
     finally:
-        lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 40000)
+        lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 10000)
     lv = star_case.levels_c()
     try:
         l = h.levels() - 1
