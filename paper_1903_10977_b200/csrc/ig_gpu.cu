@@ -87,7 +87,7 @@ struct HostSell {
 
 int g_use_dict = 1;
 int g_spmv_variant = 3;  // profiles/spmv_variants.py: best full-PCG time on C4
-int g_small_rows = 10000;  // matrices up to this many rows use k_spmv_grp (profiles/option_sweep.py: C4 173.2 -> 169.5 ms, C2 8.0 -> 7.3 ms vs 40000)
+int g_small_rows = 12000;  // matrices up to this many rows use k_spmv_grp (profiles/option_sweep.py)
 // Levels up to this many rows (below the finest) run in k_vtail; 0 = off.
 // Off by default: measured SLOWER than the graph-launched kernels (C5 V-cycle
 // 285 -> 538 us; profiles/tail_profile.py): each of the ~33 phases costs a
@@ -389,7 +389,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
     const uint32_t a = static_cast<uint32_t>(s.rlist.size());
     for (int32_t i : g) {
       int oi = -1;
-      for (size_t j = 0; j < opat.size(); ++j)
+      for (size_t j = 0; j < opat.size() && len(i) > 0; ++j)  // empty rows: own column (padding is per row)
         if (ho[i] == ho[opat[j]] && oeq(i, opat[j])) {
           oi = static_cast<int>(j);
           break;
@@ -424,8 +424,12 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
     s.O.resize(s.O.size() + l8 * wo, 0);
     for (int j = 0; j < wo; ++j) {
       const int32_t r = opat[j];
-      for (int32_t k = 0; k < len(r); ++k)
-        s.O[obase + (k / 4) * 4 * static_cast<size_t>(wo) + 4 * j + k % 4] = col[ptr[r] + k] - base(r);
+      // Padding past the row's end repeats its first offset (gathers stay in
+      // x for every row sharing the column); an empty row points at x[0].
+      const int32_t pad = len(r) > 0 ? col[ptr[r]] - base(r) : -base(r);
+      for (size_t k = 0; k < l8; ++k)
+        s.O[obase + (k / 4) * 4 * static_cast<size_t>(wo) + 4 * j + k % 4] =
+            static_cast<int32_t>(k) < len(r) ? col[ptr[r] + k] - base(r) : pad;
     }
     s.V.resize((s.V.size() + 1) & ~size_t(1), 0.0);
     const uint32_t vbase = static_cast<uint32_t>(s.V.size());

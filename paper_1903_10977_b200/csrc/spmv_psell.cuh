@@ -20,8 +20,10 @@
 //     non-dictionary value sequences (wv columns), k-blocked for vector loads
 //     (offsets [k/4][col][k%4], values [k/2][col][k%2]); ginfo selects each
 //     row's offset column and value source (global dictionary entry at the
-//     start of V, or table column).  Entries past a row's length are zero and
-//     never added (their gathers read x[0]).
+//     start of V, or table column).  Entries past a row's length are never
+//     added; their offsets repeat the row's first one (an empty row gets its
+//     own column pointing at x[0]), so every gather stays inside x whatever
+//     base(row) is.
 // Offsets are taken against base(row) = (row * smul) >> sshift, chosen per
 // matrix (A: row; restriction R: 2 row -- coarse x-lines map to every other
 // fine column; prolongation P: row / 2) so that runs and tables repeat.
@@ -141,13 +143,8 @@ __device__ __forceinline__ int psell_slice(const PSell& A, int slice, const doub
     const double2 a0 = __ldg(vp2 + (k >> 1) * vs), a1 = __ldg(vp2 + ((k >> 1) + 1) * vs);
     const double2 a2 = __ldg(vp2 + ((k >> 1) + 2) * vs), a3 = __ldg(vp2 + ((k >> 1) + 3) * vs);
     const int4 b0 = ld_off4<STREAM>(op4 + (k >> 2) * wo), b1 = ld_off4<STREAM>(op4 + ((k >> 2) + 1) * wo);
-    // Entries past a row's end gather x[0]: the zero padding of the tables is
-    // relative to base(row), which for scaled bases (R: 2 row, P: row / 2)
-    // can lie outside x.
-    const int ob[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-    double xv[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) xv[u] = __ldg(k + u < len ? xr + ob[u] : x);
+    const double xv[8] = {__ldg(xr + b0.x), __ldg(xr + b0.y), __ldg(xr + b0.z), __ldg(xr + b0.w),
+                          __ldg(xr + b1.x), __ldg(xr + b1.y), __ldg(xr + b1.z), __ldg(xr + b1.w)};
     const double av[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
 #pragma unroll
     for (int u = 0; u < 8; ++u) {

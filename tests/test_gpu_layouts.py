@@ -24,7 +24,7 @@ def layout(request):
     lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, small)
     lib.ig_set_option(_ffi.IG_OPT_PSELL, psell)
     yield request.param
-    lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 10000)
+    lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
     lib.ig_set_option(_ffi.IG_OPT_PSELL, 1)
 
 
@@ -72,7 +72,7 @@ def test_pattern_sell_nonfinite_and_signed_zero(star_case):
     try:
         h = MgHierarchy(star_case)
     finally:
-        lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 10000)
+        lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
     lv = star_case.levels_c()
     try:
         l = h.levels() - 1
