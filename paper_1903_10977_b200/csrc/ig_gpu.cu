@@ -228,10 +228,12 @@ HostSell to_sell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col,
 // ------------------------------------------------ pattern SELL (host) ------
 // Host image of spmv_psell.cuh's PSell.  See that header for the layout.
 int g_use_psell = 1;
+int g_psell_pairs = 1;  // FAST slices with two rows per lane (x reuse across a column run)
 constexpr int kPDictEntries = 32;
 constexpr int kPMinRun = 8;  // shorter runs of identical rows go to GENERAL slices
 
 struct HostPSell {
+  std::vector<int2> seg;  // FAST2 segment lists: (first offset, run length), m = 0 terminates
   std::vector<PSliceMeta> meta;
   std::vector<int32_t> rlist;
   std::vector<uint32_t> ginfo;
@@ -370,6 +372,26 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
     b.push_back({st, i});
     return st;
   };
+  // FAST2 segment list of a row's offsets: maximal runs of consecutive
+  // columns, split at 8 entries; deduplicated like the offset sequences.
+  std::unordered_map<uint64_t, std::vector<std::pair<uint32_t, int32_t>>> sseq;
+  auto seg_start = [&](int32_t i) -> uint32_t {
+    auto& b = sseq[ho[i]];
+    for (const auto& [st, r] : b)
+      if (oeq(i, r)) return st;
+    const uint32_t st = static_cast<uint32_t>(s.seg.size());
+    const int32_t bi = base(i);
+    for (int32_t k = ptr[i]; k < ptr[i + 1];) {
+      int32_t m = 1;
+      while (k + m < ptr[i + 1] && m < 8 && col[k + m] == col[k] + m) ++m;
+      s.seg.push_back(make_int2(col[k] - bi, m));
+      k += m;
+    }
+    s.seg.push_back(make_int2(0, 0));
+    s.layout_bytes += 8 * static_cast<int64_t>(s.seg.size() - st);
+    b.push_back({st, i});
+    return st;
+  };
   auto pack = [](int lmax, int count, bool fast, bool ulen, int wv, int wo) {
     return static_cast<uint32_t>(lmax) | static_cast<uint32_t>(count) << 11 | (fast ? 1u << 17 : 0u) |
            (ulen ? 1u << 18 : 0u) | static_cast<uint32_t>(wv) << 19 | static_cast<uint32_t>(wo) << 25;
@@ -459,13 +481,30 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       continue;
     }
     lmax_all = std::max(lmax_all, len(r0));
-    const uint32_t vb = v_start(r0), ob = o_start(r0);
-    for (int32_t i = r0; i < r1; i += 32) {
-      const int cnt = std::min(32, r1 - i);
-      s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, ob, pack(len(r0), cnt, true, true, 0, 0)});
-      s.layout_bytes += 16;
-      ++s.n_fast;
-      s.fast_rows += cnt;
+    const uint32_t vb = v_start(r0);
+    int32_t i = r0;
+    // FAST2 (unscaled base only: rows r and r+1 then see the same column run
+    // shifted by one): pieces of up to 64 rows, an even count.
+    if (g_psell_pairs && s.smul == 1 && s.sshift == 0 && r1 - r0 >= 2) {
+      const uint32_t sg = seg_start(r0);
+      for (; r1 - i >= 2; ) {
+        const int cnt = std::min(64, (r1 - i) & ~1);
+        s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, sg, pack(len(r0), cnt / 2, true, true, 1, 0)});
+        s.layout_bytes += 16;
+        ++s.n_fast;
+        s.fast_rows += cnt;
+        i += cnt;
+      }
+    }
+    if (i < r1) {
+      const uint32_t ob = o_start(r0);
+      for (; i < r1; i += 32) {
+        const int cnt = std::min(32, r1 - i);
+        s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, ob, pack(len(r0), cnt, true, true, 0, 0)});
+        s.layout_bytes += 16;
+        ++s.n_fast;
+        s.fast_rows += cnt;
+      }
     }
     if (s.V.size() > 0xF0000000ull || s.O.size() > 0xF0000000ull) return false;
   }
@@ -713,6 +752,8 @@ struct ig_hier {
         d.p.ginfo = upload(hp.ginfo.data(), hp.ginfo.size());
         d.p.smul = hp.smul;
         d.p.sshift = hp.sshift;
+        if (hp.seg.empty()) hp.seg.push_back(make_int2(0, 0));
+        d.p.seg = upload(hp.seg.data(), hp.seg.size());
         d.p.V = upload(hp.V.data(), hp.V.size());
         d.p.O = upload(hp.O.data(), hp.O.size());
         d.p.dict_w = hp.dict_w;

@@ -63,6 +63,7 @@ struct PSell {
   const int32_t* O;
   int32_t dict_w;
   int32_t smul, sshift;  // base(row) = (row * smul) >> sshift
+  const int2* seg;       // FAST2 segment lists (first offset, length); length 0 ends a list
 };
 
 template <bool STREAM>
@@ -71,10 +72,59 @@ __device__ __forceinline__ int4 ld_off4(const int4* p) {
   return __ldg(p);
 }
 
-// One warp, one slice.  Returns the row this lane owns (-1: none) and its sum.
+// FAST2: one segment (m consecutive offsets starting at o) for the two rows
+// ra = r0 + 2 lane and ra + 1 (base(row) = row).  Both rows need the m+1
+// values x[ra+o .. ra+o+m]; they are loaded once, as 16-byte pairs from the
+// even index below (P = parity of r0 + o, warp-uniform), and each row adds
+// its m products in ascending order.  Loads are 16-byte aligned (x is).
+template <int P, int M>
+__device__ __forceinline__ void fast2_segment(const double* __restrict__ x, int a, const double* __restrict__ vp,
+                                              double& acc0, double& acc1) {
+  constexpr int C = M + 1 + P;  // values needed from base = a - P
+  const double* xb = x + (a - P);
+  const double2* xb2 = reinterpret_cast<const double2*>(xb);
+  double X[C + 1], v[M];
+#pragma unroll
+  for (int q = 0; 2 * q < C; ++q) {
+    if (2 * q + 1 < C) {
+      const double2 t = __ldg(xb2 + q);
+      X[2 * q] = t.x;
+      X[2 * q + 1] = t.y;
+    } else {
+      X[2 * q] = __ldg(xb + 2 * q);  // last value only: never read past x[a+M]
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < M; ++j) v[j] = __ldg(vp + j);
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    acc0 = acc0 + v[j] * X[P + j];
+    acc1 = acc1 + v[j] * X[P + j + 1];
+  }
+}
+template <int P>
+__device__ __forceinline__ void fast2_dispatch(const double* __restrict__ x, int a, int m,
+                                               const double* __restrict__ vp, double& acc0, double& acc1) {
+  switch (m) {  // warp-uniform
+    case 1: fast2_segment<P, 1>(x, a, vp, acc0, acc1); break;
+    case 2: fast2_segment<P, 2>(x, a, vp, acc0, acc1); break;
+    case 3: fast2_segment<P, 3>(x, a, vp, acc0, acc1); break;
+    case 4: fast2_segment<P, 4>(x, a, vp, acc0, acc1); break;
+    case 5: fast2_segment<P, 5>(x, a, vp, acc0, acc1); break;
+    case 6: fast2_segment<P, 6>(x, a, vp, acc0, acc1); break;
+    case 7: fast2_segment<P, 7>(x, a, vp, acc0, acc1); break;
+    default: fast2_segment<P, 8>(x, a, vp, acc0, acc1); break;
+  }
+}
+
+// One warp, one slice.  Returns the row this lane owns (-1: none) and its
+// sum; FAST2 slices give each lane a second row (row2 / acc2, else -1).
 template <bool STREAM>
-__device__ __forceinline__ int psell_slice(const PSell& A, int slice, const double* __restrict__ x, double& acc) {
+__device__ __forceinline__ int psell_slice(const PSell& A, int slice, const double* __restrict__ x, double& acc,
+                                           int& row2, double& acc2) {
   acc = 0.0;
+  acc2 = 0.0;
+  row2 = -1;
   const int lane = threadIdx.x & 31;
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(A.meta + slice));
   const uint32_t pk = mu.w;
@@ -82,6 +132,23 @@ __device__ __forceinline__ int psell_slice(const PSell& A, int slice, const doub
   if (count == 0) return -1;  // padding slice (warp-uniform)
   const int L = static_cast<int>(pk & kPMaxLen);
   const int cl = min(lane, count - 1);  // surplus lanes recompute the last row, store nothing
+  if ((pk & (1u << 17)) && ((pk >> 19) & 0x3f) == 1) {  // FAST2: `count` row pairs (warp-uniform)
+    const int ra = static_cast<int>(mu.x) + 2 * cl;
+    const double* vp = A.V + mu.y;
+    const int p0 = static_cast<int>(mu.x) & 1;
+    for (const int2* sg = A.seg + mu.z;; ++sg) {
+      const int2 e = __ldg(sg);
+      if (e.y == 0) break;
+      if (((p0 + e.x) & 1) == 0)
+        fast2_dispatch<0>(x, ra + e.x, e.y, vp, acc, acc2);
+      else
+        fast2_dispatch<1>(x, ra + e.x, e.y, vp, acc, acc2);
+      vp += e.y;
+    }
+    if (lane >= count) return -1;
+    row2 = ra + 1;
+    return ra;
+  }
   if (pk & (1u << 17)) {                // FAST (warp-uniform branch)
     const int row = static_cast<int>(mu.x) + cl;
     const double* xr = x + ((row * A.smul) >> A.sshift);
@@ -163,10 +230,12 @@ __global__ void __launch_bounds__(kCta) k_pspmv(PSell A, const double* __restric
   pdl_entry();
   if (pcg_done(st)) return;
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
-  double acc;
-  const int row = psell_slice<STREAM>(A, slice, x, acc);
+  double acc, acc2;
+  int row2;
+  const int row = psell_slice<STREAM>(A, slice, x, acc, row2, acc2);
   if (row < 0) return;
   y[row] = (MODE == 0) ? acc : rsrc[row] - acc;
+  if (row2 >= 0) y[row2] = (MODE == 0) ? acc2 : rsrc[row2] - acc2;
 }
 
 // p . Ap over the canonical 256-row chunks (kernels.cuh: last_cta_total), then
@@ -198,11 +267,16 @@ __global__ void __launch_bounds__(kCta) k_pprolong(PSell P, const double* __rest
   pdl_entry();
   if (pcg_done(st)) return;
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
-  double c;
-  const int row = psell_slice<STREAM>(P, slice, xc, c);
+  double c, c2;
+  int row2;
+  const int row = psell_slice<STREAM>(P, slice, xc, c, row2, c2);
   if (row < 0) return;
   cor[row] = c;
   x[row] = x[row] + c;
+  if (row2 >= 0) {
+    cor[row2] = c2;
+    x[row2] = x[row2] + c2;
+  }
 }
 
 }  // namespace igk
