@@ -48,7 +48,8 @@ enum ig_status {
   IG_BREAKDOWN = 2,         /* Breakdown{report}        (solvers.cpp:47-50)  */
   IG_INVALID_ARGUMENT = 3,  /* std::invalid_argument    (solvers.cpp:20-21)  */
   IG_CUDA_ERROR = 4,        /* device failure (no reference counterpart)     */
-  IG_UNSUPPORTED = 5        /* smoother kind not implemented on the device   */
+  IG_UNSUPPORTED = 5,       /* smoother kind not implemented on the device   */
+  IG_DIVERGED = 6           /* Diverged{report}         (solvers.cpp:108-112)*/
 };
 
 /* SmootherKind order of proj/include/immergrid/smoothers.hpp:15. */
@@ -170,6 +171,13 @@ int ig_pcg_device(ig_hier *h, const double *d_b, double tol, int32_t maxit,
 /* Synchronises the stream and returns the status of the last
  * ig_pcg_device; residuals (maxit+1, may be NULL), iterations. */
 int ig_pcg_result(ig_hier *h, double *residuals, int32_t *iterations);
+
+/* richardson(A = finest A, b, V-cycle, tol, maxit) — solvers.hpp:55-59,
+ * solvers.cpp:73-120: x <- x + M^{-1}(b - A x) from x = 0; residuals has
+ * room for maxit+1 entries.  IG_OK, IG_NOT_CONVERGED (x = last iterate) or
+ * IG_DIVERGED (residual grew 10 steps in a row). */
+int ig_richardson(ig_hier *h, const double *b, double tol, int32_t maxit, double *x,
+                  double *residuals, int32_t *iterations, double *seconds);
 
 /* Debug: run one V-cycle with direct launches and an event after every step
  * (smoother, residual, restriction, prolongation, coarse solve); writes the

@@ -283,3 +283,57 @@ int orc_pcg(const ig_level *levels, int32_t n_levels, const ig_coarse *co, int m
   free(ap);
   return status;
 }
+
+/* ----------------------------------------------------------- Richardson -- */
+
+/* richardson (solvers.cpp:73-120).  Status 0 converged, 1 NotConverged,
+ * 6 Diverged (10 consecutive growths). */
+int orc_richardson(const ig_level *levels, int32_t n_levels, const ig_coarse *co, int mode,
+                   const double *b, double tol, int32_t maxit, double *x, double *residuals,
+                   int32_t *iterations, double *seconds) {
+  const ig_csr *A = &levels[n_levels - 1].A;
+  const int32_t n = A->n_rows;
+  if (A->n_rows != A->n_cols) return IG_INVALID_ARGUMENT;
+  const double t0 = now_s();
+  for (int32_t i = 0; i < n; ++i) x[i] = 0.0;
+  *iterations = 0;
+  const double bnorm = sqrt(orc_dot(mode, n, b, b));
+  if (bnorm == 0.0) {
+    residuals[0] = 0.0;
+    *seconds = now_s() - t0;
+    return IG_OK;
+  }
+  double *r = (double *)malloc(sizeof(double) * (size_t)n);
+  double *dx = (double *)malloc(sizeof(double) * (size_t)n);
+  memcpy(r, b, sizeof(double) * (size_t)n);
+  int growth = 0, status = IG_NOT_CONVERGED;
+  for (int32_t k = 0; k <= maxit; ++k) {
+    const double rel = sqrt(orc_dot(mode, n, r, r)) / bnorm;
+    residuals[k] = rel;
+    if (k > 0 && rel > residuals[k - 1])
+      ++growth;
+    else
+      growth = 0;
+    if (rel <= tol) {
+      *iterations = k;
+      status = IG_OK;
+      break;
+    }
+    if (growth >= 10) {
+      *iterations = k;
+      status = 6; /* Diverged */
+      break;
+    }
+    if (k == maxit) {
+      *iterations = maxit;
+      break;
+    }
+    orc_vcycle_at(levels, n_levels, co, n_levels - 1, r, dx);
+    for (int32_t i = 0; i < n; ++i) x[i] = x[i] + dx[i];
+    orc_spmv(A, dx, r, 1); /* r -= A dx */
+  }
+  *seconds = now_s() - t0;
+  free(r);
+  free(dx);
+  return status;
+}

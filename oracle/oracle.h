@@ -9,6 +9,7 @@
  * It consumes exactly the payload that crosses the drop-in boundary
  * (include/ig_gpu.h: ig_level[], ig_coarse) and restates, single-threaded:
  *   pcg              proj/src/solvers.cpp:17-71
+ *   richardson       proj/src/solvers.cpp:73-120
  *   vcycle_at        proj/src/multigrid.cpp:90-108
  *   coarse_solve     proj/src/multigrid.cpp:77-88
  *   Smoother::apply  proj/src/smoothers.cpp:169-184 (additive Schwarz),
@@ -64,6 +65,12 @@ int orc_vcycle_at(const ig_level *levels, int32_t n_levels, const ig_coarse *co,
 int orc_pcg(const ig_level *levels, int32_t n_levels, const ig_coarse *co,
             int mode, const double *b, double tol, int32_t maxit, double *x,
             double *residuals, int32_t *iterations, double *seconds);
+
+/* richardson(A = levels[n_levels-1].A, b, V-cycle, tol, maxit)
+ * (solvers.cpp:73-120).  Returns 0, 1 (NotConverged) or 6 (Diverged). */
+int orc_richardson(const ig_level *levels, int32_t n_levels, const ig_coarse *co, int mode,
+                   const double *b, double tol, int32_t maxit, double *x, double *residuals,
+                   int32_t *iterations, double *seconds);
 
 #ifdef __cplusplus
 }

@@ -60,6 +60,14 @@ class Breakdown(RuntimeError):
         self.report = report
 
 
+class Diverged(RuntimeError):
+    """Richardson residual grew for 10 consecutive steps (solvers.hpp:42-48)."""
+
+    def __init__(self, what: str, report: ConvergenceReport):
+        super().__init__(what)
+        self.report = report
+
+
 class NotConverged(RuntimeError):
     """Iteration budget exhausted; carries the report and the last x (solvers.hpp:33-41)."""
 
@@ -454,3 +462,36 @@ def pcg(a, b, precond: MgHierarchy, tol: float = 1e-10, maxit: int = 1000):
     if rc == _ffi.IG_BREAKDOWN:
         raise Breakdown(msg, rep)
     _check(lib, rc, "pcg")
+
+
+def richardson(a, b, precond: MgHierarchy, tol: float = 1e-10, maxit: int = 1000):
+    """Preconditioned Richardson x <- x + M^{-1}(b - A x) from x = 0
+    (solvers.cpp:73-120) on the device, M = one V-cycle.  Returns
+    (x, ConvergenceReport); raises Diverged / NotConverged like the reference."""
+    if not isinstance(precond, MgHierarchy):
+        raise TypeError("richardson: the preconditioner must be a device MgHierarchy (no CPU fallback)")
+    fineA = precond.A
+    n = fineA.rows()
+    if a is not None and a is not fineA and tuple(getattr(a, "shape", ())) != fineA.shape:
+        raise ValueError("richardson: dimension mismatch")
+    if np.shape(b) != (n,):
+        raise ValueError("richardson: dimension mismatch")
+    bb = _as_f64(b, n)
+    x = np.zeros(n)
+    res = np.zeros(max(maxit, 0) + 1)
+    it = C.c_int32()
+    sec = C.c_double()
+    lib = _ffi.gpu()
+    rc = lib.ig_richardson(precond.handle, bb.ctypes.data_as(_dp), float(tol), int(maxit), x.ctypes.data_as(_dp),
+                           res.ctypes.data_as(_dp), C.byref(it), C.byref(sec))
+    k = it.value
+    rep = ConvergenceReport(residuals=res[: k + 1].tolist(), iterations=k, converged=(rc == _ffi.IG_OK),
+                            seconds=sec.value)
+    if rc == _ffi.IG_OK:
+        return x, rep
+    msg = lib.ig_last_error().decode()
+    if rc == _ffi.IG_NOT_CONVERGED:
+        raise NotConverged(msg, rep, x)
+    if rc == _ffi.IG_DIVERGED:
+        raise Diverged(msg, rep)
+    _check(lib, rc, "richardson")

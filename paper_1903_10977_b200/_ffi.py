@@ -65,7 +65,7 @@ class igh_info(C.Structure):
                 ("seconds_assemble", f64), ("seconds_mg_setup", f64)]
 
 
-IG_OK, IG_NOT_CONVERGED, IG_BREAKDOWN, IG_INVALID_ARGUMENT, IG_CUDA_ERROR, IG_UNSUPPORTED = range(6)
+IG_OK, IG_NOT_CONVERGED, IG_BREAKDOWN, IG_INVALID_ARGUMENT, IG_CUDA_ERROR, IG_UNSUPPORTED, IG_DIVERGED = range(7)
 IG_SMOOTHER_JACOBI, IG_SMOOTHER_GAUSS_SEIDEL, IG_SMOOTHER_ADDITIVE_SCHWARZ, IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ = range(4)
 IG_OPT_USE_GRAPH = 1
 IG_OPT_ROW_DICT = 2
@@ -116,7 +116,7 @@ GPU_SYMBOLS = (
     "ig_hier_create", "ig_hier_destroy", "ig_hier_info", "ig_hier_stream",
     "ig_vcycle", "ig_vcycle_at", "ig_coarse_solve", "ig_smoother_apply",
     "ig_level_spmv", "ig_pcg", "ig_vcycle_device", "ig_level_spmv_device", "ig_pcg_device",
-    "ig_pcg_result", "ig_last_error", "ig_set_option",
+    "ig_pcg_result", "ig_last_error", "ig_set_option", "ig_richardson",
 )
 
 
@@ -137,6 +137,7 @@ def gpu() -> C.CDLL:
         lib.ig_smoother_apply.argtypes = [vp, i32, dp, dp]
         lib.ig_level_spmv.argtypes = [vp, i32, dp, dp, i32]
         lib.ig_pcg.argtypes = [vp, dp, f64, i32, dp, dp, P(i32), dp]
+        lib.ig_richardson.argtypes = [vp, dp, f64, i32, dp, dp, P(i32), dp]
         lib.ig_vcycle_device.argtypes = [vp, vp, vp]
         lib.ig_level_spmv_device.argtypes = [vp, i32, vp, vp, i32]
         lib.ig_debug_vcycle_timeline.argtypes = [vp, vp, vp, i32, P(C.c_float), P(i32), C.c_char_p, i32, P(i32)]

@@ -664,6 +664,7 @@ struct ig_hier {
   double *r = nullptr, *z = nullptr, *p = nullptr, *ap = nullptr;
   double *hb = nullptr, *hx = nullptr;  // device copies for the host-buffer API
   cudaGraphExec_t pcg_exec = nullptr;
+  cudaGraphExec_t rich_exec = nullptr;
   struct VcGraph {
     const double* r;
     double* x;
@@ -771,6 +772,7 @@ struct ig_hier {
   }
   ~ig_hier() {
     if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
+    if (rich_exec) cudaGraphExecDestroy(rich_exec);
     for (auto& g : vc_graphs) cudaGraphExecDestroy(g.exec);
     for (void* p : allocs) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
@@ -1089,6 +1091,64 @@ struct ig_hier {
     capture_into(tail, [&] { pcg_precond(false); });
     CK(cudaGraphInstantiate(&pcg_exec, g, 0));
     CK(cudaGraphDestroy(g));
+  }
+  // Richardson (solvers.cpp:73-120): WHILE node whose body is
+  // z = V-cycle(r); r -= A z; x += z and the residual tests.
+  void rich_body(cudaGraphConditionalHandle c_loop) {
+    const int32_t n = lv[L - 1].n;
+    vcycle(L - 1, r, z, st, nullptr);
+    spmv(lv[L - 1].A, 1, z, r, r, st);
+    launch(k_rich_step, grid_of(n), kCta, 0, stream, n, z, r, st, partials, c_loop);
+  }
+  void build_rich_graph() {
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle c_loop;
+    CK(cudaGraphConditionalHandleCreate(&c_loop, g, 0, cudaGraphCondAssignDefault));
+    CK(cudaStreamBeginCaptureToGraph(stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    const int32_t n = lv[L - 1].n;
+    launch(k_rich_init, grid_of(n), kCta, 0, stream, n, r, st, partials, c_loop);
+    cudaGraph_t body = add_conditional(c_loop, cudaGraphCondTypeWhile);
+    CK(cudaStreamEndCapture(stream, &g));
+    capture_into(body, [&] { rich_body(c_loop); });
+    CK(cudaGraphInstantiate(&rich_exec, g, 0));
+    CK(cudaGraphDestroy(g));
+  }
+  void rich_launch(const double* d_b, double* d_x, double tol, int32_t maxit) {
+    ensure_residuals(maxit);
+    PcgState hs{};
+    hs.tol = tol;
+    hs.maxit = maxit;
+    hs.k = 0;
+    hs.status = ST_RUNNING;
+    hs.b = d_b;
+    hs.x = d_x;
+    hs.residuals = residuals;
+    CK(cudaMemcpyAsync(st, &hs, sizeof(PcgState), cudaMemcpyHostToDevice, stream));
+    const int32_t n = lv[L - 1].n;
+    if (g_use_graph) {
+      if (!rich_exec) build_rich_graph();
+      CK(cudaGraphLaunch(rich_exec, stream));
+      return;
+    }
+    auto stopped = [&] {
+      int32_t done = 0;
+      CK(cudaMemcpyAsync(&done, &st->done, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      return done != 0;
+    };
+    launch(k_rich_init, grid_of(n), kCta, 0, stream, n, r, st, partials, cudaGraphConditionalHandle(0));
+    while (!stopped()) rich_body(0);
+  }
+  int rich_collect(double* res_out, int32_t* iters) {
+    CK(cudaStreamSynchronize(stream));
+    PcgState hs{};
+    CK(cudaMemcpy(&hs, st, sizeof(PcgState), cudaMemcpyDeviceToHost));
+    if (hs.status == ST_RUNNING) throw Error(IG_CUDA_ERROR, "richardson: solve did not terminate");
+    const int32_t k = std::max(hs.k, 0);
+    if (iters) *iters = k;
+    if (res_out) CK(cudaMemcpy(res_out, residuals, sizeof(double) * (static_cast<size_t>(k) + 1), cudaMemcpyDeviceToHost));
+    return hs.status;
   }
   void ensure_residuals(int32_t maxit) {
     if (maxit + 1 > res_cap) {
@@ -1899,6 +1959,28 @@ int ig_pcg(ig_hier* h, const double* b, double tol, int32_t maxit, double* x, do
     if (seconds) *seconds = 1e-3 * ms;
     if (s == IG_NOT_CONVERGED) g_err = "pcg: no convergence within " + std::to_string(maxit) + " iterations";
     if (s == IG_BREAKDOWN) g_err = "pcg: p^T A p <= 0 (operator not SPD)";
+    return s;
+  });
+}
+
+int ig_richardson(ig_hier* h, const double* b, double tol, int32_t maxit, double* x, double* residuals,
+                  int32_t* iterations, double* seconds) {
+  if (!h || !b || !x || !residuals || !iterations) return fail(IG_INVALID_ARGUMENT, "richardson: null argument");
+  if (maxit < 0) return fail(IG_INVALID_ARGUMENT, "richardson: maxit must be >= 0");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return guarded([&] {
+    const int32_t n = h->lv[h->L - 1].n;
+    CK(cudaMemcpyAsync(h->hb, b, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaEventRecord(h->ev0, h->stream));
+    h->rich_launch(h->hb, h->hx, tol, maxit);
+    CK(cudaEventRecord(h->ev1, h->stream));
+    CK(cudaMemcpyAsync(x, h->hx, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+    const int s = h->rich_collect(residuals, iterations);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (seconds) *seconds = 1e-3 * ms;
+    if (s == IG_NOT_CONVERGED) g_err = "richardson: no convergence within " + std::to_string(maxit) + " iterations";
+    if (s == IG_DIVERGED) g_err = "richardson: residual grew for 10 consecutive steps";
     return s;
   });
 }

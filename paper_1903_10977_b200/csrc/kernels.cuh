@@ -34,12 +34,13 @@ constexpr int kSell = 32;   // SELL slice height == warp size
 struct PcgState {
   double bnorm, rz, rz_new, pap, alpha, beta, tol;
   int32_t k, maxit, done, status;
+  int32_t streak;    // Richardson: consecutive residual growths
   const double* b;   // right-hand side (device pointer, set per solve)
   double* x;         // solution (device pointer, set per solve)
   double* residuals; // maxit+1
   unsigned int counter[8];
 };
-enum { ST_RUNNING = -1, ST_OK = 0, ST_NOT_CONVERGED = 1, ST_BREAKDOWN = 2 };
+enum { ST_RUNNING = -1, ST_OK = 0, ST_NOT_CONVERGED = 1, ST_BREAKDOWN = 2, ST_DIVERGED = 6 };
 
 // ------------------------------------------------------------ reduction ---
 // Canonical chunk reduction (oracle.c tree256): 32-lane xor butterfly per
@@ -1152,6 +1153,85 @@ __global__ void __launch_bounds__(kCta) k_pcg_update(int32_t n, const double* __
         st->done = 1;
       }
       set_conds(c_if, c_loop, st->done == 0);
+    }
+  }
+}
+
+// ------------------------------------------------------------ Richardson --
+// richardson (solvers.cpp:73-120): x = 0, r = b; at every k the relative
+// residual is recorded, a growth streak counted, then tol, streak >= 10
+// (Diverged) and k == maxit are tested in that order; otherwise
+// dx = M r, x += dx, r -= A dx.
+// Init: x = 0, r = b, ||b|| (canonical reduction), the k = 0 test.
+__global__ void __launch_bounds__(kCta) k_rich_init(int32_t n, double* r, PcgState* st, double* partials,
+                                                    cudaGraphConditionalHandle c_loop) {
+  pdl_entry();
+  const int i = blockIdx.x * kCta + threadIdx.x;
+  double prod = 0.0;
+  if (i < n) {
+    const double bi = st->b[i];
+    st->x[i] = 0.0;
+    r[i] = bi;
+    prod = bi * bi;
+  }
+  double bb;
+  if (last_cta_total(prod, partials, &st->counter[3], &bb)) {
+    if (threadIdx.x == 0) {
+      const double bn = sqrt(bb);
+      st->bnorm = bn;
+      st->k = 0;
+      st->streak = 0;
+      if (bn == 0.0) {
+        st->residuals[0] = 0.0;
+        st->status = ST_OK;
+        st->done = 1;
+      } else {
+        const double rel = sqrt(bb) / bn;  // r == b: the reference's r.norm() / bnorm
+        st->residuals[0] = rel;
+        if (rel <= st->tol) {
+          st->status = ST_OK;
+          st->done = 1;
+        } else if (st->maxit <= 0) {
+          st->status = ST_NOT_CONVERGED;
+          st->done = 1;
+        }
+      }
+      if (c_loop != 0) cudaGraphSetConditional(c_loop, st->done == 0 ? 1u : 0u);
+    }
+  }
+}
+// After dx = M r (in z) and r -= A dx: x += dx, ||r|| -> residual, the tests.
+__global__ void __launch_bounds__(kCta) k_rich_step(int32_t n, const double* __restrict__ z,
+                                                    const double* __restrict__ r, PcgState* st, double* partials,
+                                                    cudaGraphConditionalHandle c_loop) {
+  pdl_entry();
+  const int i = blockIdx.x * kCta + threadIdx.x;
+  double prod = 0.0;
+  if (i < n) {
+    double* x = st->x;
+    x[i] = x[i] + z[i];
+    const double ri = r[i];
+    prod = ri * ri;
+  }
+  double rr;
+  if (last_cta_total(prod, partials, &st->counter[1], &rr)) {
+    if (threadIdx.x == 0) {
+      const int k = st->k + 1;
+      const double rel = sqrt(rr) / st->bnorm;
+      st->residuals[k] = rel;
+      st->k = k;
+      st->streak = rel > st->residuals[k - 1] ? st->streak + 1 : 0;
+      if (rel <= st->tol) {
+        st->status = ST_OK;
+        st->done = 1;
+      } else if (st->streak >= 10) {
+        st->status = ST_DIVERGED;
+        st->done = 1;
+      } else if (k >= st->maxit) {
+        st->status = ST_NOT_CONVERGED;
+        st->done = 1;
+      }
+      if (c_loop != 0) cudaGraphSetConditional(c_loop, st->done == 0 ? 1u : 0u);
     }
   }
 }

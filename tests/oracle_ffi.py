@@ -36,6 +36,7 @@ def lib():
         L.orc_vcycle_at.argtypes = [lvp, C.c_int32, cop, C.c_int32, _dp, _dp]
         L.orc_pcg.argtypes = [lvp, C.c_int32, cop, C.c_int, _dp, C.c_double, C.c_int32, _dp, _dp,
                               C.POINTER(C.c_int32), _dp]
+        L.orc_richardson.argtypes = L.orc_pcg.argtypes
         _lib = L
     return _lib
 
@@ -101,6 +102,17 @@ def vcycle_at(levels, l, r):
     rc = lib().orc_vcycle_at(lv, nl, co, l, _p(r), _p(x))
     assert rc == 0
     return x
+
+
+def richardson(levels, b, tol=1e-10, maxit=1000, mode=SEQ):
+    """(status, x, residuals[:it+1], iterations, seconds)."""
+    lv, nl, co = levels
+    b = np.ascontiguousarray(b, np.float64)
+    x = np.zeros_like(b)
+    res = np.zeros(maxit + 1)
+    it, sec = C.c_int32(), C.c_double()
+    st = lib().orc_richardson(lv, nl, co, mode, _p(b), tol, maxit, _p(x), _p(res), C.byref(it), C.byref(sec))
+    return st, x, res[:it.value + 1].copy(), it.value, sec.value
 
 
 def pcg(levels, b, tol=1e-10, maxit=1000, mode=SEQ):
