@@ -42,6 +42,12 @@ struct NotConverged : std::runtime_error {
   Vec x;
 };
 
+// solvers.hpp:42-48.
+struct Diverged : std::runtime_error {
+  Diverged(const std::string& what, ConvergenceReport r) : std::runtime_error(what), report(std::move(r)) {}
+  ConvergenceReport report;
+};
+
 struct DeviceError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
@@ -113,6 +119,28 @@ inline std::pair<Vec, ConvergenceReport> pcg(const ig_csr& a, const Vec& b, cons
   if (st == IG_NOT_CONVERGED) throw NotConverged(ig_last_error(), std::move(rep), std::move(x));
   if (st == IG_BREAKDOWN) throw Breakdown(ig_last_error(), std::move(rep));
   check(st, "pcg");
+  return {};
+}
+
+// richardson (solvers.hpp:55-59, solvers.cpp:73-120), M = one device V-cycle.
+inline std::pair<Vec, ConvergenceReport> richardson(const ig_csr& a, const Vec& b, const MgHierarchy& precond,
+                                                    double tol = 1e-10, int maxit = 1000) {
+  const int n = precond.n(precond.levels() - 1);
+  if (a.n_rows != a.n_cols || a.n_rows != static_cast<int>(b.size()) || n != a.n_rows)
+    throw std::invalid_argument("richardson: dimension mismatch");
+  Vec x(b.size()), res(static_cast<size_t>(maxit) + 1);
+  int32_t it = 0;
+  double sec = 0.0;
+  const int st = ig_richardson(precond.handle(), b.data(), tol, maxit, x.data(), res.data(), &it, &sec);
+  ConvergenceReport rep;
+  rep.residuals.assign(res.begin(), res.begin() + it + 1);
+  rep.iterations = it;
+  rep.converged = st == IG_OK;
+  rep.seconds = sec;
+  if (st == IG_OK) return {std::move(x), std::move(rep)};
+  if (st == IG_NOT_CONVERGED) throw NotConverged(ig_last_error(), std::move(rep), std::move(x));
+  if (st == IG_DIVERGED) throw Diverged(ig_last_error(), std::move(rep));
+  check(st, "richardson");
   return {};
 }
 
