@@ -76,6 +76,7 @@ IG_OPT_TSELL_KERNEL = 6
 IG_OPT_PSELL = 7
 IG_OPT_TAIL_ROWS = 8
 IG_OPT_PDL = 9
+IG_OPT_TAIL_CLUSTER = 10
 
 _host = None
 _gpu = None

@@ -89,11 +89,15 @@ int g_use_dict = 1;
 int g_spmv_variant = 3;  // profiles/spmv_variants.py: best full-PCG time on C4
 int g_small_rows = 12000;  // matrices up to this many rows use k_spmv_grp (profiles/option_sweep.py)
 // Levels up to this many rows (below the finest) run in k_vtail; 0 = off.
-// Off by default: measured SLOWER than the graph-launched kernels (C5 V-cycle
-// 285 -> 538 us; profiles/tail_profile.py): each of the ~33 phases costs a
-// 1.2 us grid barrier plus the slowest warp's latency chain (3-40 us with
-// only 16 warps per SM), more than a kernel boundary in the graph.
+// Off by default: measured SLOWER than the graph-launched kernels with
+// programmatic dependent launch, both as a cooperative grid (C5 V-cycle 285
+// -> 538 us: 1.2 us grid barriers plus the slowest warp's latency chain per
+// phase) and as one 16-CTA cluster (0.6 us cluster barriers, but every phase
+// still waits for its slowest row: C5 243 -> 300 us, C4 1029 -> 1097 us with
+// only L1 + coarse inside; profiles/tail_profile.py, option_sweep.py 8).
+// In the graph consecutive small kernels overlap their launch and drain.
 int g_tail_rows = 0;
+int g_tail_cluster = 1;  // 1: the small levels run in one 16-CTA cluster (cluster barriers); 0: cooperative grid
 // Compact-SELL layouts (spmv_tma.cuh) measured SLOWER than the row-dictionary
 // SELL on C4 (finest SpMV 442 us direct / 410 us TMA-staged vs 303 us;
 // profiles/spmv_layouts.py), so they are off by default.
@@ -651,6 +655,7 @@ struct ig_hier {
   int tail_top = 0;
   TailLevel* tail_lv = nullptr;  // device array [0 .. tail_top]
   unsigned tail_grid = 0;
+  bool tail_cluster = false;
   size_t tail_smem = 0;
   bool tail_sm = false;
   cudaStream_t stream = nullptr;
@@ -969,12 +974,31 @@ struct ig_hier {
     P.Lp = Lp;
     P.piv = piv;
     void* args[] = {&P};
+    if (tail_cluster) {  // one thread-block cluster, cluster barriers
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(kTailCluster);
+      cfg.blockDim = dim3(kTailThreads);
+      cfg.dynamicSmemBytes = tail_smem;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = kTailCluster;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (tail_sm)
+        CK(cudaLaunchKernelEx(&cfg, k_vtail<true, true>, P));
+      else
+        CK(cudaLaunchKernelEx(&cfg, k_vtail<false, true>, P));
+      return;
+    }
     if (tail_sm)
-      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_vtail<true>), dim3(tail_grid), dim3(kTailThreads), args,
-                                     tail_smem, stream));
-    else
-      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_vtail<false>), dim3(tail_grid), dim3(kTailThreads),
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_vtail<true, false>), dim3(tail_grid), dim3(kTailThreads),
                                      args, tail_smem, stream));
+    else
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_vtail<false, false>), dim3(tail_grid),
+                                     dim3(kTailThreads), args, tail_smem, stream));
   }
   void vcycle(int l, const double* r, double* x, PcgState* s, const double* rdot) {
     if (l > 0 && l <= tail_top && !rdot) {  // small levels: one persistent kernel
@@ -1498,6 +1522,10 @@ int ig_set_option(int32_t option, int64_t value) {
     g_use_dict = value != 0;
     return IG_OK;
   }
+  if (option == IG_OPT_TAIL_CLUSTER) {
+    g_tail_cluster = value != 0;
+    return IG_OK;
+  }
   if (option == IG_OPT_PDL) {
     g_use_pdl = value != 0;
     return IG_OK;
@@ -1714,17 +1742,44 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
         h->tail_lv = h->upload(tl.data(), tl.size());
         h->tail_sm = h->coarse_use_smem != 0;
         h->tail_smem = h->coarse_smem;
-        if (h->tail_sm)
-          CK(cudaFuncSetAttribute(k_vtail<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(h->tail_smem)));
-        int occ = 0;
-        if (h->tail_sm)
-          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vtail<true>, kTailThreads, h->tail_smem));
-        else
-          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vtail<false>, kTailThreads, h->tail_smem));
-        if (occ >= 1) {
-          h->tail_grid = static_cast<unsigned>(h->num_sms * std::min(occ, 2));
-          h->tail_top = top;
+        int max_optin = 0;
+        CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
+        const int cap = max_optin - 2048;  // headroom for the kernels' static shared memory
+        CK(cudaFuncSetAttribute(k_vtail<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+        CK(cudaFuncSetAttribute(k_vtail<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+        CK(cudaFuncSetAttribute(k_vtail<true, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CK(cudaFuncSetAttribute(k_vtail<false, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        if (g_tail_cluster) {
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3(kTailCluster);
+          cfg.blockDim = dim3(kTailThreads);
+          cfg.dynamicSmemBytes = h->tail_smem;
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeClusterDimension;
+          attr[0].val.clusterDim.x = kTailCluster;
+          attr[0].val.clusterDim.y = 1;
+          attr[0].val.clusterDim.z = 1;
+          cfg.attrs = attr;
+          cfg.numAttrs = 1;
+          int nclusters = 0;
+          const cudaError_t e = h->tail_sm ? cudaOccupancyMaxActiveClusters(&nclusters, k_vtail<true, true>, &cfg)
+                                           : cudaOccupancyMaxActiveClusters(&nclusters, k_vtail<false, true>, &cfg);
+          if (e == cudaSuccess && nclusters >= 1) {
+            h->tail_cluster = true;
+            h->tail_grid = kTailCluster;
+            h->tail_top = top;
+          }
+          cudaGetLastError();
+        } else {
+          int occ = 0;
+          if (h->tail_sm)
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vtail<true, false>, kTailThreads, h->tail_smem));
+          else
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vtail<false, false>, kTailThreads, h->tail_smem));
+          if (occ >= 1) {
+            h->tail_grid = static_cast<unsigned>(h->num_sms * std::min(occ, 2));
+            h->tail_top = top;
+          }
         }
       }
     }

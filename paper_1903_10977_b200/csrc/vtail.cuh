@@ -80,17 +80,87 @@ __device__ __forceinline__ void tail_smooth_p2(const TailLevel& L, const double*
 }
 
 template <int MODE>
-__device__ __forceinline__ void tail_spmv(const Sell& A, const double* x, double* y, const double* rsrc,
-                                          const TailIdx& ix) {
+__device__ __forceinline__ void tail_spmv_grp(const Sell& A, const double* x, double* y, const double* rsrc,
+                                              const TailIdx& ix) {
   const int total = ((A.n_rows * 8) + 31) & ~31;  // whole warps (shuffles inside)
   for (int base = ix.gw * 32; base < total; base += ix.nw * 32) spmv_grp_item<MODE, 8>(A, base + ix.lane, x, y, rsrc);
 }
 
-template <bool SM>
+// Thread-per-row row sum for latency: batches of 16 entries, the next
+// batch's values/columns loaded before this batch's ordered adds.
+__device__ __forceinline__ double sell_row_lat(const Sell& A, int row, const double* __restrict__ x) {
+  constexpr int U = 16;
+  const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
+  const int info = A.rowinfo[row];
+  const int len = info & 0xffff;
+  const int vd = (info >> 16) & 0xff;
+  const int od = (info >> 24) & 0xff;
+  const double* vp = A.val + base;
+  const int32_t* cp = A.col + base;
+  const double* dv = A.dval + (vd > 0 ? (vd - 1) * A.dict_w : 0);
+  const int32_t* dc = A.doff + (od > 0 ? (od - 1) * A.dict_w : 0);
+  auto val_at = [&](int k) { return vd ? __ldg(dv + k) : __ldg(vp + static_cast<int64_t>(k) * kSell); };
+  auto col_at = [&](int k) { return od ? row + __ldg(dc + k) : __ldg(cp + static_cast<int64_t>(k) * kSell); };
+  double v[U];
+  int32_t c[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    v[u] = u < len ? val_at(u) : 0.0;
+    c[u] = u < len ? col_at(u) : row;
+  }
+  double acc = 0.0;
+  for (int k0 = 0; k0 < len; k0 += U) {
+    double xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = __ldg(x + c[u]);
+    double vn[U];
+    int32_t cn[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + U + u;
+      vn[u] = k < len ? val_at(k) : 0.0;
+      cn[u] = k < len ? col_at(k) : row;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k0 + u < len) acc = acc + v[u] * xv[u];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      v[u] = vn[u];
+      c[u] = cn[u];
+    }
+  }
+  return acc;
+}
+
+template <int MODE>
+__device__ __forceinline__ void tail_spmv(const Sell& A, const double* x, double* y, const double* rsrc,
+                                          const TailIdx& ix) {
+  for (int row = ix.gt; row < A.n_rows; row += ix.nt) {
+    const double acc = sell_row_lat(A, row, x);
+    y[row] = (MODE == 0) ? acc : rsrc[row] - acc;
+  }
+}
+
+// CL: launched as ONE thread-block cluster (kTailCluster CTAs; barriers are
+// cluster barriers), else as a cooperative grid (grid barriers).
+constexpr int kTailCluster = 16;
+
+template <bool CL>
+struct TailBarrier {
+  __device__ __forceinline__ void sync() {
+    namespace cg = cooperative_groups;
+    if (CL)
+      cg::this_cluster().sync();
+    else
+      cg::this_grid().sync();
+  }
+};
+
+template <bool SM, bool CL>
 __global__ void __launch_bounds__(kTailThreads, 1) k_vtail(TailParams T) {
   extern __shared__ __align__(16) double smem[];
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
+  TailBarrier<CL> grid;
   TailIdx ix;
   ix.gt = blockIdx.x * blockDim.x + threadIdx.x;
   ix.nt = gridDim.x * blockDim.x;

@@ -1,7 +1,7 @@
 """Per-phase timing of the persistent small-level kernel (vtail.cuh) via the
 %globaltimer stamps of ig_debug_tail_profile (CTA 0 after every barrier).
 
-  python profiles/tail_profile.py [workload]     (c5 default)
+  IG_TAIL_ROWS=6000 IG_TAIL_CLUSTER=1 python profiles/tail_profile.py [workload]     (c5 default)
 """
 import ctypes as C
 import os
@@ -23,6 +23,9 @@ def main():
     lib.ig_debug_tail_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_int32,
                                           C.POINTER(C.c_int32)]
     case = build_case(mk[wl]())
+    rows = int(os.environ.get("IG_TAIL_ROWS", "6000"))
+    lib.ig_set_option(_ffi.IG_OPT_TAIL_ROWS, rows)
+    lib.ig_set_option(_ffi.IG_OPT_TAIL_CLUSTER, int(os.environ.get("IG_TAIL_CLUSTER", "1")))
     h = MgHierarchy(case)
     r = torch.from_numpy(case.b).cuda()
     x = torch.empty_like(r)

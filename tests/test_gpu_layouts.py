@@ -88,3 +88,32 @@ def test_pattern_sell_nonfinite_and_signed_zero(star_case):
         assert np.array_equal(yg[m], yo[m])
     finally:
         h.close()
+
+
+@pytest.mark.parametrize("cluster", [1, 0])
+@pytest.mark.parametrize("case_name", ["c1_case", "d3_case", "star_case", "c3_small_case"])
+def test_small_level_tail_kernel_bitwise(request, case_name, cluster):
+    """The persistent small-level V-cycle kernel (vtail.cuh; one thread-block
+    cluster or a cooperative grid) gives the same bits as the kernel-per-step
+    V-cycle: V-cycles from every level and the whole PCG solve."""
+    from paper_1903_10977_b200 import MgHierarchy, _ffi, pcg
+    lib = _ffi.gpu()
+    case = request.getfixturevalue(case_name)
+    lib.ig_set_option(_ffi.IG_OPT_TAIL_ROWS, 12000)
+    lib.ig_set_option(_ffi.IG_OPT_TAIL_CLUSTER, cluster)
+    try:
+        h = MgHierarchy(case)
+    finally:
+        lib.ig_set_option(_ffi.IG_OPT_TAIL_ROWS, 0)
+        lib.ig_set_option(_ffi.IG_OPT_TAIL_CLUSTER, 1)
+    lv = case.levels_c()
+    try:
+        for l in range(h.levels()):
+            r = rng_vec(17 + l, h._n[l])
+            assert np.array_equal(h.vcycle_at(l, r), orc.vcycle_at(lv, l, r))
+        x, rep = pcg(h.A, case.b, h, tol=1e-8, maxit=1000)
+        st, xo, ro, it, _ = orc.pcg(lv, case.b, tol=1e-8, maxit=1000, mode=orc.GPU_ORDER)
+        assert st == 0 and rep.iterations == it
+        assert np.array_equal(np.array(rep.residuals), ro) and np.array_equal(x, xo)
+    finally:
+        h.close()
