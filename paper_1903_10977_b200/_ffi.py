@@ -77,6 +77,7 @@ IG_OPT_PSELL = 7
 IG_OPT_TAIL_ROWS = 8
 IG_OPT_PDL = 9
 IG_OPT_TAIL_CLUSTER = 10
+IG_OPT_MS_LAZY = 11
 
 _host = None
 _gpu = None

@@ -97,7 +97,12 @@ int g_small_rows = 12000;  // matrices up to this many rows use k_spmv_grp (prof
 // only L1 + coarse inside; profiles/tail_profile.py, option_sweep.py 8).
 // In the graph consecutive small kernels overlap their launch and drain.
 int g_tail_rows = 0;
-int g_tail_cluster = 1;  // 1: the small levels run in one 16-CTA cluster (cluster barriers); 0: cooperative grid
+int g_tail_cluster = 1;
+// Multiplicative sweep: 1 lazily updated residual (k_msl_*), 0 classic
+// per-colour updates (default).  The lazy form halves the kernel count but
+// each DOF walks its own row's colour groups with indirect Delta gathers
+// (uncoalesced): C4 V-cycle 9.3 -> 77 ms, C5 1.6 -> 7.1 ms.  Kept, off.
+int g_ms_lazy = 0;  // 1: the small levels run in one 16-CTA cluster (cluster barriers); 0: cooperative grid
 // Compact-SELL layouts (spmv_tma.cuh) measured SLOWER than the row-dictionary
 // SELL on C4 (finest SpMV 442 us direct / 410 us TMA-staged vs 303 us;
 // profiles/spmv_layouts.py), so they are off by default.
@@ -633,6 +638,13 @@ struct Level {
   };
   std::vector<MsColor> colors;  // [colour]; empty colours have n_items == 0
   double *ms_cur = nullptr, *ms_delta = nullptr, *ms_x = nullptr;
+  // Lazily updated sweep (kernels.cuh LazyLoad / k_msl_*).
+  bool msl = false;
+  MslRows msl_rows{};
+  int32_t* msl_dptr = nullptr;
+  int2* msl_dlist = nullptr;
+  double* msl_delta = nullptr;
+  int64_t msl_entries = 0;
 };
 
 // Algorithmic byte counts (CSR-minimal traffic).
@@ -926,6 +938,30 @@ struct ig_hier {
   void ms_smoother(const Level& l, const double* r, double* out, bool acc, PcgState* s, const double* rdot, int dir) {
     const int32_t n = l.n;
     const int C = static_cast<int>(l.colors.size());
+    if (l.msl) {
+      for (int step = 0; step < C; ++step) {
+        const int c = dir == 0 ? C - 1 - step : step;
+        const Level::MsColor& mc = l.colors[c];
+        if (mc.n_items == 0) continue;
+        LazyLoad ld;
+        ld.r = r;
+        ld.R = l.msl_rows;
+        ld.delta = l.msl_delta;
+        ld.color = c;
+        ld.dir = dir;
+        const unsigned gb = static_cast<unsigned>((static_cast<int64_t>(mc.n_items) * 32 + 127) / 128);
+        launch(k_msl_blocks, gb, 128, 0, stream, mc.G, ld, l.msl_delta, s);
+      }
+      const unsigned g = grid_of(n);
+      if (rdot) {
+        if (acc) launch(k_msl_finish<true, true>, g, kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
+        else launch(k_msl_finish<false, true>, g, kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
+      } else {
+        if (acc) launch(k_msl_finish<true, false>, g, kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
+        else launch(k_msl_finish<false, false>, g, kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
+      }
+      return;
+    }
     launch(k_ms_init, grid_of(n), kCta, 0, stream, n, r, l.ms_cur, l.ms_x, s);
     for (int step = 0; step < C; ++step) {
       const int c = dir == 0 ? C - 1 - step : step;
@@ -1507,6 +1543,107 @@ void build_ms(ig_hier& h, Level& L, const ig_level& src, const ig_csr& A) {
   L.ms_x = h.alloc<double>(n);
 }
 
+// Lazily updated multiplicative sweep (kernels.cuh LazyLoad): per colour the
+// block solves with their Delta positions in one pool; per row its entries
+// grouped by the colours of their columns (ascending colour, ascending
+// column); per DOF its (colour, pool position) list.
+void build_msl(ig_hier& h, Level& L, const ig_level& src, const ig_csr& A) {
+  const ig_blocks& B = src.blocks;
+  const int32_t n = L.n, nb = B.n_blocks;
+  if (nb <= 0 || !B.blk_ptr || !B.blk_dofs || !B.fac_ptr || !B.fac)
+    throw Error(IG_INVALID_ARGUMENT, "smoother: empty block layout");
+  if (B.n_colors <= 0 || !B.color_of) throw Error(IG_INVALID_ARGUMENT, "multiplicative smoother: no block colours");
+  const int C = B.n_colors;
+  L.ms = true;
+  L.msl = true;
+  L.gamma = src.gamma;
+  L.n_blocks = nb;
+  auto bsize = [&](int32_t b) { return B.blk_ptr[b + 1] - B.blk_ptr[b]; };
+  std::vector<std::vector<int32_t>> cb(static_cast<size_t>(C));
+  for (int32_t b = 0; b < nb; ++b) {
+    const int32_t s = bsize(b);
+    if (s <= 0) throw Error(IG_INVALID_ARGUMENT, "smoother: empty block");
+    if (s > 128) throw Error(IG_INVALID_ARGUMENT, "smoother: block larger than 128 DOFs");
+    if (B.color_of[b] < 0 || B.color_of[b] >= C) throw Error(IG_INVALID_ARGUMENT, "smoother: colour out of range");
+    for (int32_t i = B.blk_ptr[b]; i < B.blk_ptr[b + 1]; ++i)
+      if (B.blk_dofs[i] < 0 || B.blk_dofs[i] >= n) throw Error(IG_INVALID_ARGUMENT, "smoother: DOF out of range");
+    L.sum_s += s;
+    L.sum_s2 += static_cast<int64_t>(s) * s;
+    L.packed_F += static_cast<int64_t>(s) * (s + 1) / 2;
+    if (s > 1) ++L.n_multi;
+    cb[B.color_of[b]].push_back(b);
+  }
+  // Pool positions: colour by colour, blocks ascending, members in order.
+  std::vector<int32_t> ypos(static_cast<size_t>(nb), 0);
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> dl(static_cast<size_t>(n));  // DOF -> (colour, pos)
+  int64_t pool = 0;
+  std::vector<int32_t> mark(static_cast<size_t>(n), -1);
+  L.colors.resize(static_cast<size_t>(C));
+  for (int c = 0; c < C; ++c) {
+    Level::MsColor& mc = L.colors[c];
+    if (cb[c].empty()) continue;
+    std::vector<int32_t> grouped, warped;
+    for (int32_t b : cb[c]) {
+      const int32_t s = bsize(b);
+      (s >= 9 && s <= 32 ? warped : grouped).push_back(b);
+      ypos[b] = static_cast<int32_t>(pool);
+      for (int32_t i = 0; i < s; ++i) {
+        const int32_t d = B.blk_dofs[B.blk_ptr[b] + i];
+        if (mark[d] == c) throw Error(IG_INVALID_ARGUMENT, "smoother: same-colour blocks share a DOF");
+        mark[d] = c;
+        dl[d].push_back({c, static_cast<int32_t>(pool + i)});
+      }
+      pool += s;
+      mc.n_dofs += s;
+    }
+    if (pool > INT32_MAX) throw Error(IG_INVALID_ARGUMENT, "smoother: too many block entries");
+    mc.G = build_groups(h, B, grouped, warped, ypos);
+    mc.n_items = mc.G.n_groups + mc.G.n_wblocks;
+  }
+  // Per DOF: (colour, pos) ascending colour (filled in colour order already).
+  std::vector<int32_t> dptr(static_cast<size_t>(n) + 1, 0);
+  std::vector<int2> dlist;
+  for (int32_t d = 0; d < n; ++d) {
+    for (const auto& [c, q] : dl[d]) dlist.push_back(make_int2(c, q));
+    dptr[d + 1] = static_cast<int32_t>(dlist.size());
+  }
+  // Per row: entries grouped by colour (ascending), columns ascending.
+  std::vector<int32_t> gptr(static_cast<size_t>(n) + 1, 0), epos;
+  std::vector<int4> ghead;
+  std::vector<double> eval;
+  std::vector<std::vector<std::pair<int32_t, double>>> bucket(static_cast<size_t>(C));
+  std::vector<int32_t> used;
+  for (int32_t d = 0; d < n; ++d) {
+    used.clear();
+    for (int32_t k = A.row_ptr[d]; k < A.row_ptr[d + 1]; ++k) {
+      const int32_t col = A.col_idx[k];
+      for (const auto& [c, q] : dl[col]) {
+        if (bucket[c].empty()) used.push_back(c);
+        bucket[c].push_back({q, A.val[k]});
+      }
+    }
+    std::sort(used.begin(), used.end());
+    for (int32_t c : used) {
+      ghead.push_back(make_int4(c, static_cast<int>(epos.size()), static_cast<int>(bucket[c].size()), 0));
+      for (const auto& [q, v] : bucket[c]) {
+        epos.push_back(q);
+        eval.push_back(v);
+      }
+      bucket[c].clear();
+    }
+    gptr[d + 1] = static_cast<int32_t>(ghead.size());
+    if (epos.size() > static_cast<size_t>(INT32_MAX)) throw Error(IG_UNSUPPORTED, "lazy sweep: too many entries");
+  }
+  L.msl_rows.gptr = h.upload(gptr.data(), gptr.size());
+  L.msl_rows.ghead = h.upload(ghead.data(), ghead.size());
+  L.msl_rows.epos = h.upload(epos.data(), epos.size());
+  L.msl_rows.eval = h.upload(eval.data(), eval.size());
+  L.msl_dptr = h.upload(dptr.data(), dptr.size());
+  L.msl_dlist = h.upload(dlist.data(), dlist.size());
+  L.msl_delta = h.alloc<double>(static_cast<size_t>(std::max<int64_t>(pool, 1)));
+  L.msl_entries = static_cast<int64_t>(epos.size());
+}
+
 }  // namespace
 
 extern "C" {
@@ -1520,6 +1657,10 @@ int ig_set_option(int32_t option, int64_t value) {
   }
   if (option == IG_OPT_ROW_DICT) {
     g_use_dict = value != 0;
+    return IG_OK;
+  }
+  if (option == IG_OPT_MS_LAZY) {
+    g_ms_lazy = value != 0;
     return IG_OK;
   }
   if (option == IG_OPT_TAIL_CLUSTER) {
@@ -1605,7 +1746,9 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       L.P = h->make_matrix(s.R.n_cols, s.R.n_rows, tp.data(), tc.data(), tv.data(), s.R.nnz);
       L.res = h->alloc<double>(L.n);
       L.cor = h->alloc<double>(L.n);
-      if (s.smoother_kind == IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ)
+      if (s.smoother_kind == IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ && g_ms_lazy)
+        build_msl(*h, L, s, s.A);
+      else if (s.smoother_kind == IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ)
         build_ms(*h, L, s, s.A);
       else
         build_smoother(*h, L, s);
@@ -1683,6 +1826,7 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       if (L.ms) {  // colored sweep: block solves + the colours' residual updates + init/finish
         as = 8 * L.packed_F + 16 * L.sum_s + 40 * n;
         for (const auto& mc : L.colors) as += 12 * mc.S.nnz + 16 * mc.n_dofs;
+        if (L.msl) as = 8 * L.packed_F + 16 * L.sum_s + 16 * L.msl_entries / 2 + 24 * n;  // ~half the entries per sweep
       }
       vc += 2 * bytes_spmv(n, n, L.A.nnz, true);
       vc += 2 * as + 8 * n;                                              // second application accumulates
@@ -1696,7 +1840,7 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       if (L.ms) {
         int ne = 0;
         for (const auto& mc : L.colors) ne += mc.n_items > 0 ? 1 : 0;
-        per_app = 2 + 2 * ne - 1;  // init, blocks + update per colour (last: none), finish
+        per_app = L.msl ? ne + 1 : 2 + 2 * ne - 1;  // lazy: blocks per colour + finish
       }
       kv += 2 * per_app + 4 + (l == n_levels - 1 && L.S.n_complex == 0 ? 1 : 0);
       I.explicit_vals_A[l] = L.A.explicit_vals;

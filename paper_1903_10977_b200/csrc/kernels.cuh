@@ -483,6 +483,19 @@ __device__ __forceinline__ int packed_idx(int i, int j, int smax) {
   return j * smax - (j * (j - 1)) / 2 + (i - j);
 }
 
+// Residual gather of the block solves: r[d] (additive and classic
+// multiplicative sweep) or, for the lazily updated multiplicative sweep, a
+// functor computing the frozen residual of DOF d (LazyLoad below).
+template <class T>
+struct NoDeduce {
+  using type = T;
+};
+struct RLoad {
+  const double* r;
+  __device__ __forceinline__ RLoad(const double* p) : r(p) {}
+  __device__ __forceinline__ double operator()(int d) const { return __ldg(r + d); }
+};
+
 // Output: additive (MS = false) -> ybuf[pos + i]; multiplicative sweep
 // (MS = true) -> ybuf is the colour's delta vector: delta[d] = 0 + y_i and
 // xms[d] += delta[d] (smoothers.cpp:199-204; same-colour blocks are disjoint).
@@ -497,15 +510,15 @@ __device__ __forceinline__ void block_out(double* ybuf, double* xms, int pos_or_
   }
 }
 
-template <int SM, bool MS = false>
+template <int SM, bool MS = false, class LD = RLoad>
 __device__ __forceinline__ void block_solve(const AsGroups& G, int g, int lane, int s, int smax,
-                                            const double* __restrict__ r, double* ybuf, double* xms = nullptr) {
+                                            typename NoDeduce<LD>::type r, double* ybuf, double* xms = nullptr) {
   double y[SM], Lp[SM * (SM + 1) / 2];
   const int32_t* dp = G.dofs + G.dof_off[g] + lane;
   const double* fp = G.fac + G.fac_off[g] + lane;
   // All loads first (independent of the substitution chain).
 #pragma unroll
-  for (int i = 0; i < SM; ++i) y[i] = (i < s) ? __ldg(r + dp[i * 32]) : 0.0;
+  for (int i = 0; i < SM; ++i) y[i] = (i < s) ? r(dp[i * 32]) : 0.0;
 #pragma unroll
   for (int j = 0; j < SM; ++j)
 #pragma unroll
@@ -540,13 +553,13 @@ __device__ __forceinline__ void block_solve(const AsGroups& G, int g, int lane, 
 }
 
 // Generic (any size) fallback with local memory.
-template <bool MS = false>
+template <bool MS = false, class LD = RLoad>
 __device__ __noinline__ void block_solve_any(const AsGroups& G, int g, int lane, int s, int smax,
-                                             const double* __restrict__ r, double* ybuf, double* xms = nullptr) {
+                                             typename NoDeduce<LD>::type r, double* ybuf, double* xms = nullptr) {
   double y[128];
   const int32_t* dp = G.dofs + G.dof_off[g] + lane;
   const double* fp = G.fac + G.fac_off[g] + lane;
-  for (int i = 0; i < s; ++i) y[i] = __ldg(r + dp[i * 32]);
+  for (int i = 0; i < s; ++i) y[i] = r(dp[i * 32]);
   for (int j = 0; j < s; ++j) {
     const double yj = y[j] / fp[packed_idx(j, j, smax) * 32];
     y[j] = yj;
@@ -561,9 +574,9 @@ __device__ __noinline__ void block_solve_any(const AsGroups& G, int g, int lane,
   for (int i = 0; i < s; ++i) block_out<MS>(ybuf, xms, MS ? dp[i * 32] : pos + i, y[i]);
 }
 
-template <bool MS = false>
+template <bool MS = false, class LD = RLoad>
 __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int lane,
-                                                 const double* __restrict__ r, double* ybuf, double* xms = nullptr) {
+                                                 typename NoDeduce<LD>::type r, double* ybuf, double* xms = nullptr) {
   const int s = G.w_size[b];
   const double* f = G.w_fac + G.w_fac_off[b];
   const int32_t* dp = G.w_dofs + G.w_dof_off[b];
@@ -573,7 +586,7 @@ __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int l
     const int hi = lane > t ? lane : t, lo = lane > t ? t : lane;
     m[t] = (t < s && lane < s) ? __ldg(f + lo * s + hi) : 0.0;
   }
-  double y = lane < s ? __ldg(r + dp[lane]) : 0.0;
+  double y = lane < s ? r(dp[lane]) : 0.0;
   const double dg = lane < s ? __ldg(f + lane * s + lane) : 1.0;  // own pivot L(lane, lane)
   const double rdg = safe_rcp(dg);
   double acc = 0.0;
@@ -620,8 +633,8 @@ __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int l
 }
 
 // One warp-sized work item w of phase 1 (group of small blocks or a warp block).
-template <bool MS = false>
-__device__ __forceinline__ void as_blocks_item(const AsGroups& G, int w, int lane, const double* __restrict__ r,
+template <bool MS = false, class LD = RLoad>
+__device__ __forceinline__ void as_blocks_item(const AsGroups& G, int w, int lane, typename NoDeduce<LD>::type r,
                                                double* ybuf, double* xms = nullptr) {
   if (w < G.n_groups) {
     const int g = w;
@@ -629,13 +642,13 @@ __device__ __forceinline__ void as_blocks_item(const AsGroups& G, int w, int lan
     const int smax = G.smax[g];  // warp-uniform
     if (s == 0) return;
     if (smax <= 4)
-      block_solve<4, MS>(G, g, lane, s, smax, r, ybuf, xms);
+      block_solve<4, MS, LD>(G, g, lane, s, smax, r, ybuf, xms);
     else if (smax <= 8)
-      block_solve<8, MS>(G, g, lane, s, smax, r, ybuf, xms);
+      block_solve<8, MS, LD>(G, g, lane, s, smax, r, ybuf, xms);
     else
-      block_solve_any<MS>(G, g, lane, s, smax, r, ybuf, xms);
+      block_solve_any<MS, LD>(G, g, lane, s, smax, r, ybuf, xms);
   } else if (w - G.n_groups < G.n_wblocks) {
-    warp_block_solve<MS>(G, w - G.n_groups, lane, r, ybuf, xms);
+    warp_block_solve<MS, LD>(G, w - G.n_groups, lane, r, ybuf, xms);
   }
 }
 __global__ void __launch_bounds__(128) k_as_blocks(AsGroups G, const double* __restrict__ r,
@@ -893,6 +906,100 @@ __global__ void __launch_bounds__(kCta) k_ms_finish(int32_t n, double gamma, con
   double prod = 0.0;
   if (i < n) {
     const double v = gamma * xms[i];
+    const double o = ACC ? out[i] + v : v;
+    out[i] = o;
+    if (RED) prod = rdot[i] * o;
+  }
+  if (RED) {
+    double rz;
+    if (last_cta_total(prod, partials, &st->counter[2], &rz))
+      if (threadIdx.x == 0) rz_update(st, rz);
+  }
+}
+
+// Lazily updated multiplicative sweep (IG_OPT_MS_LAZY; measured slower, off
+// by default -- see ig_gpu.cu g_ms_lazy).  The classic sweep above
+// updates the frozen residual of EVERY row after every colour; here a block
+// of colour c' forms the residual of its own DOFs when it needs it:
+//   cur_d = ((r_d - t_{c1,d}) - t_{c2,d}) - ...,  t_{c,d} = sum_{k in D_c} A_dk Delta_c(k)
+// over the colours c processed before c', in processing order, each sum in
+// ascending k -- the same operations, in the same order, as the reference's
+// incremental `cur -= A * delta` on row d (colours without neighbours of d
+// add +0 there and are skipped).  x is assembled at the end from the
+// colours' Delta of each DOF, in processing order, as x += delta does.
+// One kernel per colour plus one finish, instead of two per colour.
+struct MslRows {
+  const int32_t* gptr;  // n+1: row d's colour groups [gptr[d], gptr[d+1])
+  const int4* ghead;    // (colour, first entry, count, 0), colours ascending
+  const int32_t* epos;  // entry: position of Delta_c(k) in the delta pool
+  const double* eval;   // entry: A_dk
+};
+struct LazyLoad {
+  const double* r;
+  MslRows R;
+  const double* delta;
+  int color;  // the colour being solved
+  int dir;    // 0 Forward (processed before: higher colours), 1 Reverse (lower)
+  __device__ __forceinline__ double gsum(int4 h) const {
+    constexpr int U = 8;
+    double t = 0.0;
+    for (int e0 = h.y; e0 < h.y + h.z; e0 += U) {
+      double v[U], dv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool in = e0 + u < h.y + h.z;
+        v[u] = in ? __ldg(R.eval + e0 + u) : 0.0;
+        dv[u] = in ? __ldg(delta + __ldg(R.epos + e0 + u)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (e0 + u < h.y + h.z) t = t + v[u] * dv[u];
+    }
+    return t;
+  }
+  __device__ __forceinline__ double operator()(int d) const {
+    double cur = __ldg(r + d);
+    const int g0 = __ldg(R.gptr + d), g1 = __ldg(R.gptr + d + 1);
+    if (dir == 0) {
+      for (int g = g1 - 1; g >= g0; --g) {
+        const int4 h = __ldg(R.ghead + g);
+        if (h.x <= color) break;
+        cur = cur - gsum(h);
+      }
+    } else {
+      for (int g = g0; g < g1; ++g) {
+        const int4 h = __ldg(R.ghead + g);
+        if (h.x >= color) break;
+        cur = cur - gsum(h);
+      }
+    }
+    return cur;
+  }
+};
+__global__ void __launch_bounds__(128) k_msl_blocks(AsGroups G, LazyLoad ld, double* delta, const PcgState* st) {
+  pdl_entry();
+  if (pcg_done(st)) return;
+  as_blocks_item<false, LazyLoad>(G, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, ld, delta,
+                                  nullptr);
+}
+// x_d = sum of Delta_c(d) over d's colours in processing order (from 0), then
+// out = gamma * x (ACC: out += gamma * x); RED: r . z (finest level in PCG).
+template <bool ACC, bool RED>
+__global__ void __launch_bounds__(kCta) k_msl_finish(int32_t n, double gamma, int dir, const int32_t* __restrict__ dptr,
+                                                     const int2* __restrict__ dlist, const double* __restrict__ delta,
+                                                     double* out, const double* rdot, PcgState* st, double* partials) {
+  pdl_entry();
+  if (pcg_done(st)) return;
+  const int i = blockIdx.x * kCta + threadIdx.x;
+  double prod = 0.0;
+  if (i < n) {
+    const int q0 = dptr[i], q1 = dptr[i + 1];
+    double x = 0.0;
+    if (dir == 0)
+      for (int q = q1 - 1; q >= q0; --q) x = x + delta[dlist[q].y];
+    else
+      for (int q = q0; q < q1; ++q) x = x + delta[dlist[q].y];
+    const double v = gamma * x;
     const double o = ACC ? out[i] + v : v;
     out[i] = o;
     if (RED) prod = rdot[i] * o;
