@@ -208,6 +208,7 @@ const char *ig_last_error(void);
 #define IG_OPT_PDL 9          /* 1 (default): programmatic dependent launch for every kernel; 0: plain stream order */
 #define IG_OPT_TAIL_CLUSTER 10 /* persistent small-level kernel: 1 one 16-CTA cluster, 0 cooperative grid */
 #define IG_OPT_MS_LAZY 11     /* multiplicative sweep: 1 lazily updated residual, 0 (default) classic per-colour updates */
+#define IG_OPT_AS_SPLIT 12    /* additive smoother: 1 (default) small blocks fused with singletons, 0 all blocks on the side stream */
 int ig_set_option(int32_t option, int64_t value);
 
 #ifdef __cplusplus

@@ -102,7 +102,8 @@ int g_tail_cluster = 1;
 // per-colour updates (default).  The lazy form halves the kernel count but
 // each DOF walks its own row's colour groups with indirect Delta gathers
 // (uncoalesced): C4 V-cycle 9.3 -> 77 ms, C5 1.6 -> 7.1 ms.  Kept, off.
-int g_ms_lazy = 0;  // 1: the small levels run in one 16-CTA cluster (cluster barriers); 0: cooperative grid
+int g_ms_lazy = 0;
+int g_split = 1;  // additive smoother: small groups (smax <= 4) with the singleton DOFs, big ones on the side stream  // 1: the small levels run in one 16-CTA cluster (cluster barriers); 0: cooperative grid
 // Compact-SELL layouts (spmv_tma.cuh) measured SLOWER than the row-dictionary
 // SELL on C4 (finest SpMV 442 us direct / 410 us TMA-staged vs 303 us;
 // profiles/spmv_layouts.py), so they are off by default.
@@ -619,6 +620,7 @@ struct Level {
   DevSell A, R, P;
   AsGroups G{};
   AsGather S{};
+  int32_t g_small = 0;  // first group with smax <= 4 (groups are sorted by size, descending)
   int32_t n_blocks = 0, n_multi = 0, n_complex = 0;
   int64_t sum_s = 0, sum_s2 = 0, packed_F = 0;
   double* r_in = nullptr;  // input residual buffer (host API; coarse levels: R res)
@@ -904,21 +906,26 @@ struct ig_hier {
       ms_smoother(l, r, x, acc, s, rdot, dir < 0 ? (acc ? 1 : 0) : dir);
       return;
     }
-    const bool multi = l.n_multi > 0;
+    // Big groups (smax > 4) and warp blocks on the side stream; the small
+    // groups fused with the singleton DOFs on the main stream.
+    AsGroups big = l.G;
+    big.n_groups = g_split ? l.g_small : l.G.n_groups;
+    const int32_t n_small = l.G.n_groups - big.n_groups;
+    const bool multi = big.n_groups + big.n_wblocks > 0;
     if (multi) {
       CK(cudaEventRecord(ev_fork, stream));
       CK(cudaStreamWaitEvent(side, ev_fork, 0));
-      const unsigned gb =
-          static_cast<unsigned>((static_cast<int64_t>(l.G.n_groups + l.G.n_wblocks) * 32 + 127) / 128);
-      launch(k_as_blocks, gb, 128, 0, side, l.G, r, l.ybuf, s);
+      const unsigned gb = static_cast<unsigned>((static_cast<int64_t>(big.n_groups + big.n_wblocks) * 32 + 127) / 128);
+      launch(k_as_blocks, gb, 128, 0, side, big, r, l.ybuf, s);
       CK(cudaGetLastError());
       CK(cudaEventRecord(ev_join, side));
     }
     const unsigned g = grid_of(l.n);
+    const int32_t gctas = static_cast<int32_t>((static_cast<int64_t>(n_small) * 32 + kCta - 1) / kCta);
     if (acc)
-      launch(k_as_simple<true>, g, kCta, 0, stream, l.S, r, x, s);
+      launch(k_as_small_simple<true>, g + gctas, kCta, 0, stream, l.G, big.n_groups, gctas, l.S, r, l.ybuf, x, s);
     else
-      launch(k_as_simple<false>, g, kCta, 0, stream, l.S, r, x, s);
+      launch(k_as_small_simple<false>, g + gctas, kCta, 0, stream, l.G, big.n_groups, gctas, l.S, r, l.ybuf, x, s);
     CK(cudaGetLastError());
     if (multi) CK(cudaStreamWaitEvent(stream, ev_join, 0));
     if (rdot) {
@@ -1344,6 +1351,18 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
   if (yl > INT32_MAX) throw Error(IG_INVALID_ARGUMENT, "smoother: too many block entries");
   L.n_multi = static_cast<int32_t>(grouped.size() + warped.size());
   L.G = build_groups(h, B, grouped, warped, ypos);
+  {
+    std::vector<int32_t> gs(grouped.size());
+    for (size_t k = 0; k < grouped.size(); ++k) gs[k] = bsize(grouped[k]);
+    std::stable_sort(gs.begin(), gs.end(), [](int32_t a, int32_t b) { return a > b; });
+    int32_t first = static_cast<int32_t>((grouped.size() + 31) / 32);
+    for (int32_t g = 0; g < static_cast<int32_t>((grouped.size() + 31) / 32); ++g)
+      if (gs[static_cast<size_t>(g) * 32] <= 4) {
+        first = g;
+        break;
+      }
+    L.g_small = first;
+  }
   L.ybuf = h.alloc<double>(static_cast<size_t>(std::max<int64_t>(yl, 1)));
   build_gather(h, L, src, ypos, sval);
 }
@@ -1657,6 +1676,10 @@ int ig_set_option(int32_t option, int64_t value) {
   }
   if (option == IG_OPT_ROW_DICT) {
     g_use_dict = value != 0;
+    return IG_OK;
+  }
+  if (option == IG_OPT_AS_SPLIT) {
+    g_split = value != 0;
     return IG_OK;
   }
   if (option == IG_OPT_MS_LAZY) {

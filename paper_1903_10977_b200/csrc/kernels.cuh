@@ -796,6 +796,31 @@ __global__ void __launch_bounds__(kCta) k_as_simple(AsGather S, const double* __
   if (d >= S.n) return;
   as_simple_item<ACC>(S, d, r, x);
 }
+// Small groups (smax <= 4: faces of the box, most multi-DOF blocks) fused
+// with the singleton DOFs: CTAs [0, n_gctas) run groups g_begin.. of G with
+// the lean 4-wide solve (4 warps per CTA), the rest the singleton DOFs.
+// Registers stay low (no 8-wide or warp-block code), so it runs at full
+// occupancy next to the big groups and warp blocks on the side stream.
+template <bool ACC>
+__global__ void __launch_bounds__(kCta) k_as_small_simple(AsGroups G, int32_t g_begin, int32_t n_gctas, AsGather S,
+                                                          const double* __restrict__ r, double* ybuf, double* x,
+                                                          const PcgState* st) {
+  pdl_entry();
+  if (pcg_done(st)) return;
+  if (static_cast<int32_t>(blockIdx.x) < n_gctas) {
+    const int g = g_begin + static_cast<int>((blockIdx.x * kCta + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (g >= G.n_groups) return;
+    const int s = G.size[g * 32 + lane];
+    if (s == 0) return;
+    block_solve<4>(G, g, lane, s, G.smax[g], r, ybuf);
+    return;
+  }
+  const int d = (blockIdx.x - n_gctas) * kCta + threadIdx.x;
+  if (d >= S.n) return;
+  as_simple_item<ACC>(S, d, r, x);
+}
+
 template <bool ACC>
 __device__ __forceinline__ void as_complex_item(const AsGather& S, int c, const double* __restrict__ r,
                                                 const double* __restrict__ ybuf, double* x) {
