@@ -827,7 +827,7 @@ struct ig_hier {
       }
       CK(cudaGetLastError());
       if (red) {  // p . Ap over the canonical chunks, alpha / Breakdown
-        launch(k_pap, g, kCta, 0, stream, A.s.n_rows, x, y, s, partials);
+        launch(k_pap, red_grid(A.s.n_rows), kCta, 0, stream, A.s.n_rows, x, y, s, partials);
         CK(cudaGetLastError());
       }
       return;
@@ -930,9 +930,9 @@ struct ig_hier {
     if (multi) CK(cudaStreamWaitEvent(stream, ev_join, 0));
     if (rdot) {
       if (acc)
-        launch(k_as_finish_red<true>, g, kCta, 0, stream, l.S, r, l.ybuf, x, rdot, s, partials);
+        launch(k_as_finish_red<true>, red_grid(l.n), kCta, 0, stream, l.S, r, l.ybuf, x, rdot, s, partials);
       else
-        launch(k_as_finish_red<false>, g, kCta, 0, stream, l.S, r, l.ybuf, x, rdot, s, partials);
+        launch(k_as_finish_red<false>, red_grid(l.n), kCta, 0, stream, l.S, r, l.ybuf, x, rdot, s, partials);
     } else if (l.S.n_complex > 0) {
       const unsigned gc = grid_of(l.S.n_complex);
       if (acc)
@@ -942,6 +942,9 @@ struct ig_hier {
     }
     CK(cudaGetLastError());
   }
+  // Grid of the canonical-reduction kernels (kernels.cuh chunk_reduce): at
+  // most 4 CTAs per SM, each looping over 256-element chunks.
+  unsigned red_grid(int64_t n) const { return static_cast<unsigned>(std::min<int64_t>(grid_of(n), 4 * num_sms)); }
   void ms_smoother(const Level& l, const double* r, double* out, bool acc, PcgState* s, const double* rdot, int dir) {
     const int32_t n = l.n;
     const int C = static_cast<int>(l.colors.size());
@@ -961,8 +964,8 @@ struct ig_hier {
       }
       const unsigned g = grid_of(n);
       if (rdot) {
-        if (acc) launch(k_msl_finish<true, true>, g, kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
-        else launch(k_msl_finish<false, true>, g, kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
+        if (acc) launch(k_msl_finish<true, true>, red_grid(n), kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
+        else launch(k_msl_finish<false, true>, red_grid(n), kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
       } else {
         if (acc) launch(k_msl_finish<true, false>, g, kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
         else launch(k_msl_finish<false, false>, g, kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
@@ -980,8 +983,8 @@ struct ig_hier {
         launch(k_ms_update, grid_of(mc.S.s.n_rows), kCta, 0, stream, mc.S.s, mc.rowmap, l.ms_delta, l.ms_cur, s);
     }
     if (rdot) {
-      if (acc) launch(k_ms_finish<true, true>, grid_of(n), kCta, 0, stream, n, l.gamma, l.ms_x, out, rdot, s, partials);
-      else launch(k_ms_finish<false, true>, grid_of(n), kCta, 0, stream, n, l.gamma, l.ms_x, out, rdot, s, partials);
+      if (acc) launch(k_ms_finish<true, true>, red_grid(n), kCta, 0, stream, n, l.gamma, l.ms_x, out, rdot, s, partials);
+      else launch(k_ms_finish<false, true>, red_grid(n), kCta, 0, stream, n, l.gamma, l.ms_x, out, rdot, s, partials);
     } else {
       if (acc) launch(k_ms_finish<true, false>, grid_of(n), kCta, 0, stream, n, l.gamma, l.ms_x, out, rdot, s, partials);
       else launch(k_ms_finish<false, false>, grid_of(n), kCta, 0, stream, n, l.gamma, l.ms_x, out, rdot, s, partials);
@@ -1052,7 +1055,7 @@ struct ig_hier {
     if (l == 0) {
       coarse(r, x, s);
       if (rdot) {  // 1-level hierarchy inside PCG: r . z as a separate pass
-        launch(k_pcg_rz, grid_of(n0), kCta, 0, stream, n0, rdot, x, s, partials);
+        launch(k_pcg_rz, red_grid(n0), kCta, 0, stream, n0, rdot, x, s, partials);
         CK(cudaGetLastError());
       }
       mark("coarse", 0);
@@ -1093,7 +1096,7 @@ struct ig_hier {
   // (IF node / host check) once the solve has stopped.
   void pcg_init(cudaGraphConditionalHandle c_if, cudaGraphConditionalHandle c_loop) {
     const int32_t n = lv[L - 1].n;
-    launch(k_pcg_init, grid_of(n), kCta, 0, stream, n, r, st, partials, c_if, c_loop);
+    launch(k_pcg_init, red_grid(n), kCta, 0, stream, n, r, st, partials, c_if, c_loop);
     CK(cudaGetLastError());
   }
   void pcg_precond(bool first) {
@@ -1108,7 +1111,7 @@ struct ig_hier {
   void pcg_step(cudaGraphConditionalHandle c_if, cudaGraphConditionalHandle c_loop) {
     const int32_t n = lv[L - 1].n;
     spmv(lv[L - 1].A, 0, p, ap, nullptr, st, true);  // ap = A p; pap; alpha / breakdown
-    launch(k_pcg_update, grid_of(n), kCta, 0, stream, n, p, ap, r, st, partials, c_if, c_loop);
+    launch(k_pcg_update, red_grid(n), kCta, 0, stream, n, p, ap, r, st, partials, c_if, c_loop);
     CK(cudaGetLastError());
   }
   // Append a conditional node of `type` after the current capture frontier
@@ -1165,7 +1168,7 @@ struct ig_hier {
     const int32_t n = lv[L - 1].n;
     vcycle(L - 1, r, z, st, nullptr);
     spmv(lv[L - 1].A, 1, z, r, r, st);
-    launch(k_rich_step, grid_of(n), kCta, 0, stream, n, z, r, st, partials, c_loop);
+    launch(k_rich_step, red_grid(n), kCta, 0, stream, n, z, r, st, partials, c_loop);
   }
   void build_rich_graph() {
     cudaGraph_t g;
@@ -1174,7 +1177,7 @@ struct ig_hier {
     CK(cudaGraphConditionalHandleCreate(&c_loop, g, 0, cudaGraphCondAssignDefault));
     CK(cudaStreamBeginCaptureToGraph(stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     const int32_t n = lv[L - 1].n;
-    launch(k_rich_init, grid_of(n), kCta, 0, stream, n, r, st, partials, c_loop);
+    launch(k_rich_init, red_grid(n), kCta, 0, stream, n, r, st, partials, c_loop);
     cudaGraph_t body = add_conditional(c_loop, cudaGraphCondTypeWhile);
     CK(cudaStreamEndCapture(stream, &g));
     capture_into(body, [&] { rich_body(c_loop); });
@@ -1204,7 +1207,7 @@ struct ig_hier {
       CK(cudaStreamSynchronize(stream));
       return done != 0;
     };
-    launch(k_rich_init, grid_of(n), kCta, 0, stream, n, r, st, partials, cudaGraphConditionalHandle(0));
+    launch(k_rich_init, red_grid(n), kCta, 0, stream, n, r, st, partials, cudaGraphConditionalHandle(0));
     while (!stopped()) rich_body(0);
   }
   int rich_collect(double* res_out, int32_t* iters) {

@@ -244,10 +244,8 @@ __global__ void __launch_bounds__(kCta) k_pap(int n, const double* __restrict__ 
                                              PcgState* st, double* partials) {
   pdl_entry();
   if (pcg_done(st)) return;
-  const int row = blockIdx.x * kCta + threadIdx.x;
-  const double prod = row < n ? p[row] * ap[row] : 0.0;
   double pap;
-  if (last_cta_total(prod, partials, &st->counter[0], &pap)) {
+  if (chunk_reduce(n, [&](int row) { return p[row] * ap[row]; }, partials, &st->counter[0], &pap)) {
     if (threadIdx.x == 0) {
       st->pap = pap;
       if (pap <= 0.0) {  // solvers.cpp:47-50 (a NaN does not trigger it)
