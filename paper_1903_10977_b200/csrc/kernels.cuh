@@ -107,12 +107,26 @@ template <class F>
 __device__ __forceinline__ bool chunk_reduce(int n, F f, double* partials, unsigned int* counter, double* total) {
   __shared__ double sm8c[8];
   const unsigned int nchunks = static_cast<unsigned int>((n + kCta - 1) / kCta);
-  for (unsigned int c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const int i = static_cast<int>(c) * kCta + threadIdx.x;
-    const double prod = i < n ? f(i) : 0.0;
-    const double part = cta_reduce(prod, sm8c);
-    if (threadIdx.x == 0) partials[c] = part;
-    __syncthreads();  // sm8c reuse
+  // Up to 4 chunks' element work first (their loads in flight together),
+  // then their per-chunk trees in chunk order.
+  constexpr int B = 4;
+  for (unsigned int c0 = blockIdx.x; c0 < nchunks; c0 += B * gridDim.x) {
+    double prod[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const unsigned int c = c0 + u * gridDim.x;
+      const int i = static_cast<int>(c) * kCta + threadIdx.x;
+      prod[u] = (c < nchunks && i < n) ? f(i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const unsigned int c = c0 + u * gridDim.x;
+      if (c < nchunks) {  // CTA-uniform
+        const double part = cta_reduce(prod[u], sm8c);
+        if (threadIdx.x == 0) partials[c] = part;
+        __syncthreads();  // sm8c reuse
+      }
+    }
   }
   return grid_finish(nchunks, partials, counter, total);
 }
