@@ -79,6 +79,7 @@ IG_OPT_PDL = 9
 IG_OPT_TAIL_CLUSTER = 10
 IG_OPT_MS_LAZY = 11
 IG_OPT_AS_SPLIT = 12
+IG_OPT_RED_CTAS = 13
 
 _host = None
 _gpu = None

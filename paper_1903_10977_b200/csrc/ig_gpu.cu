@@ -103,6 +103,7 @@ int g_tail_cluster = 1;
 // each DOF walks its own row's colour groups with indirect Delta gathers
 // (uncoalesced): C4 V-cycle 9.3 -> 77 ms, C5 1.6 -> 7.1 ms.  Kept, off.
 int g_ms_lazy = 0;
+int g_red_ctas = 8;  // CTAs per SM of the canonical-reduction kernels (profiles/option_sweep.py 13)
 int g_split = 1;  // additive smoother: small groups (smax <= 4) with the singleton DOFs, big ones on the side stream  // 1: the small levels run in one 16-CTA cluster (cluster barriers); 0: cooperative grid
 // Compact-SELL layouts (spmv_tma.cuh) measured SLOWER than the row-dictionary
 // SELL on C4 (finest SpMV 442 us direct / 410 us TMA-staged vs 303 us;
@@ -951,7 +952,8 @@ struct ig_hier {
   }
   // Grid of the canonical-reduction kernels (kernels.cuh chunk_reduce): at
   // most 4 CTAs per SM, each looping over 256-element chunks.
-  unsigned red_grid(int64_t n) const { return static_cast<unsigned>(std::min<int64_t>(grid_of(n), 4 * num_sms)); }
+  int red_ctas = g_red_ctas;
+  unsigned red_grid(int64_t n) const { return static_cast<unsigned>(std::min<int64_t>(grid_of(n), red_ctas * num_sms)); }
   void ms_smoother(const Level& l, const double* r, double* out, bool acc, PcgState* s, const double* rdot, int dir) {
     const int32_t n = l.n;
     const int C = static_cast<int>(l.colors.size());
@@ -1686,6 +1688,11 @@ int ig_set_option(int32_t option, int64_t value) {
   }
   if (option == IG_OPT_ROW_DICT) {
     g_use_dict = value != 0;
+    return IG_OK;
+  }
+  if (option == IG_OPT_RED_CTAS) {
+    if (value < 1 || value > 64) return fail(IG_INVALID_ARGUMENT, "ig_set_option: reduction CTAs per SM in 1..64");
+    g_red_ctas = static_cast<int>(value);
     return IG_OK;
   }
   if (option == IG_OPT_AS_SPLIT) {
