@@ -225,6 +225,10 @@ def main():
         st = lib.ig_pcg_result(h.handle, res.ctypes.data_as(C.POINTER(C.c_double)), C.byref(it))
         return st, it.value
 
+    # The clock sampler runs from the warm-up through the timed region (short
+    # workloads finish the timed region faster than nvidia-smi can sample).
+    clk = Clocks(local)
+    clk.__enter__()
     for _ in range(max(args.warmup, 3) if args.warmup > 0 else 0):
         solve()
     st, iters = result() if args.warmup > 0 else (None, None)
@@ -234,12 +238,12 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            solve()
-        ev1.record(stream)
-        torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        solve()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk.__exit__(None, None, None)
     ms = ev0.elapsed_time(ev1) / args.steps
     st, iters = result()
     assert st == 0, f"solve did not converge (status {st})"
