@@ -146,6 +146,12 @@ int ig_vcycle(ig_hier *h, const double *r, double *x);
 int ig_vcycle_at(ig_hier *h, int32_t level, const double *r, double *x);
 int ig_coarse_solve(ig_hier *h, const double *r, double *x);
 int ig_smoother_apply(ig_hier *h, int32_t level, const double *r, double *x);
+/* Smoother::apply(r, dir) (smoothers.hpp:70-73): dir 0 Forward, 1 Reverse
+ * (multiplicative sweeps: colours descending / ascending). */
+int ig_smoother_apply_dir(ig_hier *h, int32_t level, const double *r, double *x, int32_t dir);
+/* Smoother::apply_symmetric (smoothers.cpp:211-214):
+ * x1 = S(r, Forward); x = x1 + S(r - A x1, Reverse). */
+int ig_smoother_apply_symmetric(ig_hier *h, int32_t level, const double *r, double *x);
 /* mode 0: y = A x; 1: y = r - A x (r passed in y); 2: y = R x; 3: y = R^T x */
 int ig_level_spmv(ig_hier *h, int32_t level, const double *x, double *y,
                   int32_t mode);

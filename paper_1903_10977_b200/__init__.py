@@ -392,11 +392,22 @@ class MgHierarchy:
     def coarse_solve(self, r) -> np.ndarray:
         return self.vcycle_at(0, r)
 
-    def smoother_apply(self, l: int, r) -> np.ndarray:
+    def smoother_apply(self, l: int, r, direction: int = 0) -> np.ndarray:
+        """Smoother::apply(r, dir) of level l: direction 0 Forward, 1 Reverse."""
         rr = _as_f64(r, self._n[l])
         x = np.empty_like(rr)
         lib = _ffi.gpu()
-        _check(lib, lib.ig_smoother_apply(self._h, l, rr.ctypes.data_as(_dp), x.ctypes.data_as(_dp)), "smoother_apply")
+        _check(lib, lib.ig_smoother_apply_dir(self._h, l, rr.ctypes.data_as(_dp), x.ctypes.data_as(_dp),
+                                              int(direction)), "smoother_apply")
+        return x
+
+    def smoother_apply_symmetric(self, l: int, r) -> np.ndarray:
+        """Smoother::apply_symmetric (smoothers.cpp:211-214)."""
+        rr = _as_f64(r, self._n[l])
+        x = np.empty_like(rr)
+        lib = _ffi.gpu()
+        _check(lib, lib.ig_smoother_apply_symmetric(self._h, l, rr.ctypes.data_as(_dp), x.ctypes.data_as(_dp)),
+               "smoother_apply_symmetric")
         return x
 
     def spmv(self, l: int, x, mode: int = 0, y=None) -> np.ndarray:

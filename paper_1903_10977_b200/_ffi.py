@@ -121,6 +121,7 @@ GPU_SYMBOLS = (
     "ig_vcycle", "ig_vcycle_at", "ig_coarse_solve", "ig_smoother_apply",
     "ig_level_spmv", "ig_pcg", "ig_vcycle_device", "ig_level_spmv_device", "ig_pcg_device",
     "ig_pcg_result", "ig_last_error", "ig_set_option", "ig_richardson",
+    "ig_smoother_apply_dir", "ig_smoother_apply_symmetric",
 )
 
 
@@ -139,6 +140,8 @@ def gpu() -> C.CDLL:
         lib.ig_vcycle_at.argtypes = [vp, i32, dp, dp]
         lib.ig_coarse_solve.argtypes = [vp, dp, dp]
         lib.ig_smoother_apply.argtypes = [vp, i32, dp, dp]
+        lib.ig_smoother_apply_dir.argtypes = [vp, i32, dp, dp, i32]
+        lib.ig_smoother_apply_symmetric.argtypes = [vp, i32, dp, dp]
         lib.ig_level_spmv.argtypes = [vp, i32, dp, dp, i32]
         lib.ig_pcg.argtypes = [vp, dp, f64, i32, dp, dp, P(i32), dp]
         lib.ig_richardson.argtypes = [vp, dp, f64, i32, dp, dp, P(i32), dp]

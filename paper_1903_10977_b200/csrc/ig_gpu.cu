@@ -2021,6 +2021,37 @@ int ig_smoother_apply(ig_hier* h, int32_t level, const double* r, double* x) {
   });
 }
 
+int ig_smoother_apply_dir(ig_hier* h, int32_t level, const double* r, double* x, int32_t dir) {
+  if (!h || !r || !x) return fail(IG_INVALID_ARGUMENT, "smoother_apply: null argument");
+  if (level < 1 || level >= h->L) return fail(IG_INVALID_ARGUMENT, "smoother_apply: level has no smoother");
+  if (dir != 0 && dir != 1) return fail(IG_INVALID_ARGUMENT, "smoother_apply: dir must be 0 (Forward) or 1 (Reverse)");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return guarded([&] {
+    Level& L = h->lv[level];
+    CK(cudaMemcpyAsync(L.r_in, r, sizeof(double) * L.n, cudaMemcpyHostToDevice, h->stream));
+    h->smoother(L, L.r_in, h->hx, false, nullptr, nullptr, dir);
+    CK(cudaMemcpyAsync(x, h->hx, sizeof(double) * L.n, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return IG_OK;
+  });
+}
+
+int ig_smoother_apply_symmetric(ig_hier* h, int32_t level, const double* r, double* x) {
+  if (!h || !r || !x) return fail(IG_INVALID_ARGUMENT, "smoother_apply_symmetric: null argument");
+  if (level < 1 || level >= h->L) return fail(IG_INVALID_ARGUMENT, "smoother_apply_symmetric: level has no smoother");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return guarded([&] {
+    Level& L = h->lv[level];
+    CK(cudaMemcpyAsync(L.r_in, r, sizeof(double) * L.n, cudaMemcpyHostToDevice, h->stream));
+    h->smoother(L, L.r_in, h->hx, false, nullptr, nullptr, 0);   // x1 = S(r, Forward)
+    h->spmv(L.A, 1, h->hx, L.cor, L.r_in, nullptr);            // r - A x1
+    h->smoother(L, L.cor, h->hx, true, nullptr, nullptr, 1);    // x1 + S(., Reverse)
+    CK(cudaMemcpyAsync(x, h->hx, sizeof(double) * L.n, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return IG_OK;
+  });
+}
+
 int ig_level_spmv(ig_hier* h, int32_t level, const double* x, double* y, int32_t mode) {
   if (!h || !x || !y) return fail(IG_INVALID_ARGUMENT, "level_spmv: null argument");
   if (level < 0 || level >= h->L) return fail(IG_INVALID_ARGUMENT, "level_spmv: level out of range");

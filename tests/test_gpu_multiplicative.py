@@ -72,3 +72,17 @@ def test_pcg_bitwise(ms_hier):
     assert st == 0 and rep.converged and rep.iterations == it
     assert np.array_equal(np.array(rep.residuals), ro)
     assert np.array_equal(x, xo)
+
+
+def test_smoother_reverse_and_symmetric_bitwise(ms_hier):
+    """Smoother::apply(r, Reverse) and apply_symmetric (smoothers.cpp:211-214)
+    on the device against the oracle's pieces."""
+    h = ms_hier
+    lv = h.case.levels_c()
+    for l in range(1, h.levels()):
+        r = rng_vec(61 + l, h._n[l])
+        assert np.array_equal(h.smoother_apply(l, r, 1), orc.smoother_apply(lv, l, r, 1))
+        x1 = orc.smoother_apply(lv, l, r, 0)
+        res = orc.spmv(lv, l, x1, 1, r.copy())
+        want = x1 + orc.smoother_apply(lv, l, res, 1)
+        assert np.array_equal(h.smoother_apply_symmetric(l, r), want)

@@ -237,3 +237,16 @@ def test_c4_full_size_matches_golden():
     # true residual through the device SpMV (mode 1: b - A x)
     r = h.spmv(h.levels() - 1, x, 1, case.b)
     assert np.linalg.norm(r) / np.linalg.norm(case.b) <= 2e-8
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_additive_reverse_and_symmetric_bitwise(request, name):
+    """Additive Schwarz: Reverse == Forward (smoothers.cpp:174-184) and
+    apply_symmetric (smoothers.cpp:211-214) bit-identical to the oracle."""
+    h, lv = _pair(request, name)
+    for l in range(1, h.levels()):
+        r = rng_vec(71 + l, h._n[l])
+        assert np.array_equal(h.smoother_apply(l, r, 1), h.smoother_apply(l, r, 0))
+        x1 = orc.smoother_apply(lv, l, r, 0)
+        want = x1 + orc.smoother_apply(lv, l, orc.spmv(lv, l, x1, 1, r.copy()), 1)
+        assert np.array_equal(h.smoother_apply_symmetric(l, r), want)
