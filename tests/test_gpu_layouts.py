@@ -117,3 +117,22 @@ def test_small_level_tail_kernel_bitwise(request, case_name, cluster):
         assert np.array_equal(np.array(rep.residuals), ro) and np.array_equal(x, xo)
     finally:
         h.close()
+
+
+def test_breakdown_through_pattern_sell():
+    """proj/tests/test_solvers.cpp:153-173 with the finest A in the pattern
+    layout: p.Ap <= 0 is detected by k_pap (the separate canonical reduction)
+    and reported as Breakdown."""
+    from paper_1903_10977_b200 import Breakdown, MgHierarchy, _ffi, pcg
+    lib = _ffi.gpu()
+    lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 0)
+    try:
+        h = MgHierarchy(orc.Synthetic(np.diag([1.0, -1.0])))
+    finally:
+        lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
+    try:
+        with pytest.raises(Breakdown) as e:
+            pcg(h.A, np.array([0.0, 1.0]), h)
+        assert len(e.value.report.residuals) >= 1
+    finally:
+        h.close()
