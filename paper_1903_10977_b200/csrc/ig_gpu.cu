@@ -11,12 +11,17 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <utility>
 #include <vector>
@@ -256,6 +261,24 @@ struct HostPSell {
   int64_t n_fast = 0, n_general = 0, fast_rows = 0;
 };
 
+// Host-side data-parallel loop over [0, n) in contiguous ranges (layout
+// construction of the large levels; results do not depend on the split).
+template <typename F>
+void parallel_rows(int32_t n, F fn) {
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (n < 65536 || hw == 1) {
+    fn(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int32_t step = (n + static_cast<int32_t>(hw) - 1) / static_cast<int32_t>(hw);
+  for (unsigned t = 0; t < hw; ++t) {
+    const int32_t a = static_cast<int32_t>(t) * step, b = std::min(n, a + step);
+    if (a < b) th.emplace_back(fn, a, b);
+  }
+  for (auto& x : th) x.join();
+}
+
 inline uint64_t mix64(uint64_t h, uint64_t w) {
   h ^= w + 0x9E3779B97F4A7C15ULL + (h << 6) + (h >> 2);
   return h * 0xff51afd7ed558ccdULL;
@@ -270,27 +293,31 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
   // Offset base per matrix: the scale (1, 2 or 1/2 of the row index) under
   // which the column-offset sequences repeat most (A: 1, R: 2, P: 1/2).
   std::vector<uint64_t> hv(static_cast<size_t>(nr)), ho(static_cast<size_t>(nr));
-  for (int32_t i = 0; i < nr; ++i) {
-    uint64_t a = static_cast<uint64_t>(len(i));
-    for (int32_t k = ptr[i]; k < ptr[i + 1]; ++k) {
-      uint64_t w;
-      std::memcpy(&w, val + k, 8);
-      a = mix64(a, w);
+  parallel_rows(nr, [&](int32_t i0, int32_t i1) {
+    for (int32_t i = i0; i < i1; ++i) {
+      uint64_t a = static_cast<uint64_t>(len(i));
+      for (int32_t k = ptr[i]; k < ptr[i + 1]; ++k) {
+        uint64_t w;
+        std::memcpy(&w, val + k, 8);
+        a = mix64(a, w);
+      }
+      hv[i] = a;
     }
-    hv[i] = a;
-  }
+  });
   const int cand[3][2] = {{1, 0}, {2, 0}, {1, 1}};
   size_t best_runs = SIZE_MAX;
   std::vector<uint64_t> hcur(static_cast<size_t>(nr));
   for (const auto& c : cand) {
     if (c[0] == 2 && nc < nr) continue;  // scaling up only for wide (restriction-shaped) matrices
     if (c[1] == 1 && nc > nr) continue;
-    for (int32_t i = 0; i < nr; ++i) {
-      const int64_t b = (static_cast<int64_t>(i) * c[0]) >> c[1];
-      uint64_t h = static_cast<uint64_t>(len(i));
-      for (int32_t k = ptr[i]; k < ptr[i + 1]; ++k) h = mix64(h, static_cast<uint64_t>(col[k] - b));
-      hcur[i] = h;
-    }
+    parallel_rows(nr, [&](int32_t i0, int32_t i1) {
+      for (int32_t i = i0; i < i1; ++i) {
+        const int64_t b = (static_cast<int64_t>(i) * c[0]) >> c[1];
+        uint64_t h = static_cast<uint64_t>(len(i));
+        for (int32_t k = ptr[i]; k < ptr[i + 1]; ++k) h = mix64(h, static_cast<uint64_t>(col[k] - b));
+        hcur[i] = h;
+      }
+    });
     size_t runs = 0;  // consecutive-row changes of (values, offsets)
     for (int32_t i = 1; i < nr; ++i) runs += (hv[i] != hv[i - 1] || hcur[i] != hcur[i - 1]) ? 1 : 0;
     if (runs < best_runs) {
@@ -313,9 +340,14 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
     return true;
   };
   // Runs of identical consecutive rows.
+  std::vector<uint8_t> brk(static_cast<size_t>(nr), 0);
+  parallel_rows(nr, [&](int32_t i0, int32_t i1) {
+    for (int32_t i = i0; i < i1; ++i)
+      brk[i] = (i == 0 || hv[i] != hv[i - 1] || ho[i] != ho[i - 1] || !veq(i, i - 1) || !oeq(i, i - 1)) ? 1 : 0;
+  });
   std::vector<int32_t> run_start;
   for (int32_t i = 0; i < nr; ++i)
-    if (i == 0 || hv[i] != hv[i - 1] || ho[i] != ho[i - 1] || !veq(i, i - 1) || !oeq(i, i - 1)) run_start.push_back(i);
+    if (brk[i]) run_start.push_back(i);
   run_start.push_back(nr);
   std::vector<uint8_t> in_fast(static_cast<size_t>(nr), 0);
   for (size_t r = 0; r + 1 < run_start.size(); ++r)
@@ -1316,9 +1348,17 @@ void check_csr(const ig_csr& a, const char* what) {
   if (a.n_rows > 0 && (a.row_ptr[0] != 0 || a.row_ptr[a.n_rows] != a.nnz))
     throw Error(IG_INVALID_ARGUMENT, std::string(what) + ": row_ptr inconsistent with nnz");
   for (int32_t i = 0; i < a.n_rows; ++i)
-    for (int32_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k)
-      if (a.col_idx[k] < 0 || a.col_idx[k] >= a.n_cols || (k > a.row_ptr[i] && a.col_idx[k] <= a.col_idx[k - 1]))
-        throw Error(IG_INVALID_ARGUMENT, std::string(what) + ": column indices out of range or not ascending");
+    if (a.row_ptr[i + 1] < a.row_ptr[i]) throw Error(IG_INVALID_ARGUMENT, std::string(what) + ": row_ptr decreasing");
+  std::atomic<int> bad{0};
+  parallel_rows(a.n_rows, [&](int32_t i0, int32_t i1) {
+    for (int32_t i = i0; i < i1 && !bad.load(std::memory_order_relaxed); ++i)
+      for (int32_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k)
+        if (a.col_idx[k] < 0 || a.col_idx[k] >= a.n_cols || (k > a.row_ptr[i] && a.col_idx[k] <= a.col_idx[k - 1])) {
+          bad.store(1);
+          break;
+        }
+  });
+  if (bad.load()) throw Error(IG_INVALID_ARGUMENT, std::string(what) + ": column indices out of range or not ascending");
 }
 
 AsGroups build_groups(ig_hier& h, const ig_blocks& B, std::vector<int32_t> grouped, const std::vector<int32_t>& warped,
@@ -1778,12 +1818,19 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       if (s.smoother_kind != IG_SMOOTHER_ADDITIVE_SCHWARZ && s.smoother_kind != IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ)
         throw Error(IG_UNSUPPORTED, "device smoother: additive or multiplicative Schwarz only");
       I.nnz_R[l] = s.R.nnz;
+      const bool timing = std::getenv("IG_TIMING") != nullptr;
+      auto tnow = [] { return std::chrono::steady_clock::now(); };
+      auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+      const auto t0 = tnow();
       L.A = h->make_matrix(s.A.n_rows, s.A.n_cols, s.A.row_ptr, s.A.col_idx, s.A.val, s.A.nnz);
+      const auto t1 = tnow();
       L.R = h->make_matrix(s.R.n_rows, s.R.n_cols, s.R.row_ptr, s.R.col_idx, s.R.val, s.R.nnz);
+      const auto t2 = tnow();
       std::vector<int32_t> tp, tc;
       std::vector<double> tv;
       csr_transpose(s.R, tp, tc, tv);
       L.P = h->make_matrix(s.R.n_cols, s.R.n_rows, tp.data(), tc.data(), tv.data(), s.R.nnz);
+      const auto t3 = tnow();
       L.res = h->alloc<double>(L.n);
       L.cor = h->alloc<double>(L.n);
       if (s.smoother_kind == IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ && g_ms_lazy)
@@ -1792,6 +1839,10 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
         build_ms(*h, L, s, s.A);
       else
         build_smoother(*h, L, s);
+      const auto t4 = tnow();
+      if (timing)
+        std::fprintf(stderr, "[ig_hier_create] level %d n=%d: A %.3f s, R %.3f s, P %.3f s, smoother %.3f s\n", l, L.n,
+                     secs(t0, t1), secs(t1, t2), secs(t2, t3), secs(t3, t4));
       I.sell_slots_A[l] = L.A.slots;
       I.n_blocks[l] = L.n_blocks;
       I.n_multi_blocks[l] = L.n_multi;
