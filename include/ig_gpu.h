@@ -216,6 +216,7 @@ const char *ig_last_error(void);
 #define IG_OPT_MS_LAZY 11     /* multiplicative sweep: 1 lazily updated residual, 0 (default) classic per-colour updates */
 #define IG_OPT_AS_SPLIT 12    /* additive smoother: 1 (default) small blocks fused with singletons, 0 all blocks on the side stream */
 #define IG_OPT_RED_CTAS 13    /* CTAs per SM of the canonical-reduction kernels (default 8) */
+#define IG_OPT_PSELL_CTAS 15  /* pattern-SELL SpMV occupancy cap, CTAs per SM (0 = registers decide) */
 int ig_set_option(int32_t option, int64_t value);
 
 #ifdef __cplusplus

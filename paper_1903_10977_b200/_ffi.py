@@ -80,6 +80,7 @@ IG_OPT_TAIL_CLUSTER = 10
 IG_OPT_MS_LAZY = 11
 IG_OPT_AS_SPLIT = 12
 IG_OPT_RED_CTAS = 13
+IG_OPT_PSELL_CTAS = 15
 
 _host = None
 _gpu = None
@@ -128,7 +129,7 @@ GPU_SYMBOLS = (
 def gpu() -> C.CDLL:
     global _gpu
     if _gpu is None:
-        lib = _lib("libig_gpu.so")
+        lib = _lib(os.environ.get("IG_GPU_LIB", "libig_gpu.so"))  # variant builds for profiling only
         vp, dp = C.c_void_p, P(f64)
         lib.ig_hier_create.argtypes = [P(ig_level), i32, P(ig_coarse), P(vp)]
         lib.ig_hier_destroy.argtypes = [vp]

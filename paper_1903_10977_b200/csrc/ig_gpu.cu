@@ -245,6 +245,14 @@ HostSell to_sell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col,
 // Host image of spmv_psell.cuh's PSell.  See that header for the layout.
 int g_use_psell = 1;
 int g_psell_pairs = 1;  // FAST slices with two rows per lane (x reuse across a column run)
+// Occupancy cap of the pattern-SELL kernels (CTAs per SM, 0 = registers
+// decide), applied as unused dynamic shared memory: fewer resident warps keep
+// more of each warp's x lines in L1 (the gathers are L1-hit-rate bound).
+int g_psell_ctas = 0;
+size_t psell_smem() {
+  if (g_psell_ctas <= 0) return 0;
+  return static_cast<size_t>(std::max(0, 233472 / g_psell_ctas - 1024 - 1024)) & ~size_t(1023);
+}
 constexpr int kPDictEntries = 32;
 constexpr int kPMinRun = 8;  // shorter runs of identical rows go to GENERAL slices
 
@@ -851,12 +859,13 @@ struct ig_hier {
     if (g == 0) return;
     if (A.has_p) {
       const unsigned gp = static_cast<unsigned>(A.p.n_slices / (kCta / 32));
+      const size_t sm = psell_smem();
       if (mode == 0) {
-        if (A.stream) launch(k_pspmv<0, true>, gp, kCta, 0, stream, A.p, x, y, rsrc, s);
-        else launch(k_pspmv<0, false>, gp, kCta, 0, stream, A.p, x, y, rsrc, s);
+        if (A.stream) launch(k_pspmv<0, true>, gp, kCta, sm, stream, A.p, x, y, rsrc, s);
+        else launch(k_pspmv<0, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s);
       } else {
-        if (A.stream) launch(k_pspmv<1, true>, gp, kCta, 0, stream, A.p, x, y, rsrc, s);
-        else launch(k_pspmv<1, false>, gp, kCta, 0, stream, A.p, x, y, rsrc, s);
+        if (A.stream) launch(k_pspmv<1, true>, gp, kCta, sm, stream, A.p, x, y, rsrc, s);
+        else launch(k_pspmv<1, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s);
       }
       CK(cudaGetLastError());
       if (red) {  // p . Ap over the canonical chunks, alpha / Breakdown
@@ -917,8 +926,9 @@ struct ig_hier {
     const unsigned g = grid_of(l.P.s.n_rows);
     if (l.P.has_p) {
       const unsigned gp = static_cast<unsigned>(l.P.p.n_slices / (kCta / 32));
-      if (l.P.stream) launch(k_pprolong<true>, gp, kCta, 0, stream, l.P.p, xc, l.cor, x, s);
-      else launch(k_pprolong<false>, gp, kCta, 0, stream, l.P.p, xc, l.cor, x, s);
+      const size_t sm = psell_smem();
+      if (l.P.stream) launch(k_pprolong<true>, gp, kCta, sm, stream, l.P.p, xc, l.cor, x, s);
+      else launch(k_pprolong<false>, gp, kCta, sm, stream, l.P.p, xc, l.cor, x, s);
       CK(cudaGetLastError());
       return;
     }
@@ -1733,6 +1743,17 @@ int ig_set_option(int32_t option, int64_t value) {
   if (option == IG_OPT_RED_CTAS) {
     if (value < 1 || value > 64) return fail(IG_INVALID_ARGUMENT, "ig_set_option: reduction CTAs per SM in 1..64");
     g_red_ctas = static_cast<int>(value);
+    return IG_OK;
+  }
+  if (option == IG_OPT_PSELL_CTAS) {
+    if (value < 0 || value > 8) return fail(IG_INVALID_ARGUMENT, "ig_set_option: pattern-SELL CTAs per SM in 0..8");
+    g_psell_ctas = static_cast<int>(value);
+    const int sm = static_cast<int>(psell_smem());
+    void (*ks[])(PSell, const double*, double*, const double*, const PcgState*) = {
+        k_pspmv<0, true>, k_pspmv<0, false>, k_pspmv<1, true>, k_pspmv<1, false>};
+    for (auto k : ks) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_pprolong<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_pprolong<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     return IG_OK;
   }
   if (option == IG_OPT_AS_SPLIT) {

@@ -26,6 +26,35 @@ __device__ __forceinline__ void pdl_entry() {
 }
 
 constexpr int kCta = 256;   // threads per CTA == reduction chunk size
+// Register budgets (min CTAs per SM) of the smoother and small-level SpMV
+// kernels; variant builds override them (profiles/build_variants.sh).
+// (An explicit minimum of 1 is NOT the same as none: it lets ptxas use up to
+// 255 registers.)  0 = no hint.
+#ifndef IG_ASB_MINB
+#define IG_ASB_MINB 0
+#endif
+#ifndef IG_AS_MINB
+#define IG_AS_MINB 0
+#endif
+#ifndef IG_GRP_MINB
+#define IG_GRP_MINB 0
+#endif
+#if IG_ASB_MINB > 0
+#define IG_ASB_BOUNDS __launch_bounds__(128, IG_ASB_MINB)
+#else
+#define IG_ASB_BOUNDS __launch_bounds__(128)
+#endif
+#if IG_AS_MINB > 0
+#define IG_AS_BOUNDS __launch_bounds__(kCta, IG_AS_MINB)
+#else
+#define IG_AS_BOUNDS __launch_bounds__(kCta)
+#endif
+#if IG_GRP_MINB > 0
+#define IG_GRP_BOUNDS __launch_bounds__(kCta, IG_GRP_MINB)
+#else
+#define IG_GRP_BOUNDS __launch_bounds__(kCta)
+#endif
+
 constexpr int kSell = 32;   // SELL slice height == warp size
 
 // ----------------------------------------------------------- PCG state ----
@@ -437,7 +466,7 @@ __device__ __forceinline__ void spmv_grp_item(const Sell& A, int t, const double
   if (valid_row && g == 0) y[row] = (MODE == 0) ? acc : rsrc[row] - acc;
 }
 template <int MODE, int G>
-__global__ void __launch_bounds__(kCta) k_spmv_grp(Sell A, const double* __restrict__ x, double* y,
+__global__ void IG_GRP_BOUNDS k_spmv_grp(Sell A, const double* __restrict__ x, double* y,
                                                    const double* rsrc) {
   pdl_entry();
   spmv_grp_item<MODE, G>(A, blockIdx.x * kCta + threadIdx.x, x, y, rsrc);
@@ -685,7 +714,7 @@ __device__ __forceinline__ void as_blocks_item(const AsGroups& G, int w, int lan
     warp_block_solve<MS, LD>(G, w - G.n_groups, lane, r, ybuf, xms);
   }
 }
-__global__ void __launch_bounds__(128) k_as_blocks(AsGroups G, const double* __restrict__ r,
+__global__ void IG_ASB_BOUNDS k_as_blocks(AsGroups G, const double* __restrict__ r,
                                                    double* ybuf, const PcgState* st) {
   pdl_entry();
   if (pcg_done(st)) return;
@@ -836,7 +865,7 @@ __global__ void __launch_bounds__(kCta) k_as_simple(AsGather S, const double* __
 // Registers stay low (no 8-wide or warp-block code), so it runs at full
 // occupancy next to the big groups and warp blocks on the side stream.
 template <bool ACC>
-__global__ void __launch_bounds__(kCta) k_as_small_simple(AsGroups G, int32_t g_begin, int32_t n_gctas, AsGather S,
+__global__ void IG_AS_BOUNDS k_as_small_simple(AsGroups G, int32_t g_begin, int32_t n_gctas, AsGather S,
                                                           const double* __restrict__ r, double* ybuf, double* x,
                                                           const PcgState* st) {
   pdl_entry();
@@ -863,7 +892,7 @@ __device__ __forceinline__ void as_complex_item(const AsGather& S, int c, const 
   x[d] = ACC ? x[d] + out : out;
 }
 template <bool ACC>
-__global__ void __launch_bounds__(kCta) k_as_complex(AsGather S, const double* __restrict__ r,
+__global__ void IG_AS_BOUNDS k_as_complex(AsGather S, const double* __restrict__ r,
                                                      const double* __restrict__ ybuf, double* x,
                                                      const PcgState* st) {
   pdl_entry();

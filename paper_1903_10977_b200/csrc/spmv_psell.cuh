@@ -224,8 +224,19 @@ __device__ __forceinline__ int psell_slice(const PSell& A, int slice, const doub
 
 // MODE 0: y = A x.  MODE 1: y = r - A x (r read from rsrc; in place allowed:
 // every row is read and written by its own lane only).
+// Register budget: 256 threads x 4 CTAs per SM (<= 64 registers).  Measured
+// on C4 (profiles/psell_sweep.py, variant builds): the compiler's default
+// (40 registers, 6 CTAs) 172 us for the finest A p and 1036 us per V-cycle;
+// with this bound 161 us and 904 us -- the extra registers hoist more gathers
+// ahead of each serial chain, and 32 resident warps keep their x lines in L1.
+#ifndef IG_PSPMV_MINB
+#define IG_PSPMV_MINB 4
+#endif
+#ifndef IG_PPROLONG_MINB
+#define IG_PPROLONG_MINB 4
+#endif
 template <int MODE, bool STREAM>
-__global__ void __launch_bounds__(kCta) k_pspmv(PSell A, const double* __restrict__ x, double* y,
+__global__ void __launch_bounds__(kCta, IG_PSPMV_MINB) k_pspmv(PSell A, const double* __restrict__ x, double* y,
                                                const double* rsrc, const PcgState* st) {
   pdl_entry();
   if (pcg_done(st)) return;
@@ -260,7 +271,7 @@ __global__ void __launch_bounds__(kCta) k_pap(int n, const double* __restrict__ 
 
 // Prolongation fused with the correction (k_prolong on the pattern layout).
 template <bool STREAM>
-__global__ void __launch_bounds__(kCta) k_pprolong(PSell P, const double* __restrict__ xc, double* cor, double* x,
+__global__ void __launch_bounds__(kCta, IG_PPROLONG_MINB) k_pprolong(PSell P, const double* __restrict__ xc, double* cor, double* x,
                                                   const PcgState* st) {
   pdl_entry();
   if (pcg_done(st)) return;

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <string>
@@ -620,7 +621,10 @@ int igh_build(const igh_config* cfg, igh_case** out) {
     double t1 = 0.0;
     std::vector<std::unique_ptr<Space>> down;
     std::vector<std::unique_ptr<GSpace>> gdown;
+    double t_gal = 0.0, t_fac = 0.0;
     auto galerkin = [&](Csr r) {  // A_c = R (A R^T) (multigrid.cpp:39-41)
+      const double tg = now();
+      struct Acc { double& t; double t0; ~Acc() { t += now() - t0; } } acc_{t_gal, tg};
       const Csr rt = transpose(r);
       Csr ap = spgemm(Adown.back(), rt, threads);
       Adown.push_back(spgemm(r, ap, threads));
@@ -698,7 +702,9 @@ int igh_build(const igh_config* cfg, igh_case** out) {
           });
         }
       }
+      const double tf = now();
       factorize_blocks(c->A[l], b, cfg->filter_ratio, threads);
+      t_fac += now() - tf;
       double gm = cfg->gamma;
       if (gm <= 0.0) {
         const bool damped = cfg->smoother_kind == IG_SMOOTHER_ADDITIVE_SCHWARZ;
@@ -741,6 +747,9 @@ int igh_build(const igh_config* cfg, igh_case** out) {
     c->info.eta = as.eta;
     c->info.seconds_assemble = t1 - t0;
     c->info.seconds_mg_setup = t2 - t1;
+    if (std::getenv("IG_TIMING"))
+      std::fprintf(stderr, "igh_build: assemble %.3f s, mg setup %.3f s (galerkin %.3f, block factorization %.3f)\n",
+                   t1 - t0, t2 - t1, t_gal, t_fac);
     *out = c.release();
     return IG_OK;
   } catch (const std::exception& e) {

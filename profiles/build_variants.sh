@@ -1,0 +1,17 @@
+#!/bin/bash
+# Profiling-only variant builds of the device library:
+#   profiles/build_variants.sh name1:"-DFLAG ..." name2:"..." ...
+# -> paper_1903_10977_b200/libig_gpu_<name>.so (load with IG_GPU_LIB=libig_gpu_<name>.so).
+set -e
+cd "$(dirname "$0")/../paper_1903_10977_b200"
+for spec in "$@"; do
+  name="${spec%%:*}"; flags="${spec#*:}"
+  nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -fmad=false -Xcompiler -fPIC \
+    --expt-relaxed-constexpr -I../include $flags -shared -o "libig_gpu_$name.so" csrc/ig_gpu.cu -lcudart \
+    2> "/tmp/ptxas_$name.log" &
+done
+wait
+for spec in "$@"; do
+  name="${spec%%:*}"
+  echo "$name $(cuobjdump -res-usage libig_gpu_$name.so | grep -A1 'k_pspmvILi0ELb0\|k_pprolongILb0' | grep -o 'REG:[0-9]*\|STACK:[0-9]*' | paste -s -d' ')"
+done
