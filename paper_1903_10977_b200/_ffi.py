@@ -81,6 +81,7 @@ IG_OPT_MS_LAZY = 11
 IG_OPT_AS_SPLIT = 12
 IG_OPT_RED_CTAS = 13
 IG_OPT_PSELL_CTAS = 15
+IG_OPT_FUSED_AS_ROWS = 16
 
 _host = None
 _gpu = None

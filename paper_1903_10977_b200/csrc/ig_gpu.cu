@@ -249,6 +249,13 @@ int g_psell_pairs = 1;  // FAST slices with two rows per lane (x reuse across a 
 // decide), applied as unused dynamic shared memory: fewer resident warps keep
 // more of each warp's x lines in L1 (the gathers are L1-hit-rate bound).
 int g_psell_ctas = 0;
+// Levels with at most this many DOFs run the additive smoother as one fused
+// kernel (kernels.cuh k_as_fused) instead of the fork/join split.  Off by
+// default: measured slower on every workload (C2 V-cycle 228 -> 272 us, C4
+// 907 -> 936 us with levels <= 300k rows fused): the split kernels already
+// overlap under PDL and the graph fork, and the fused kernel's phase-1 fence
+// + arrival + wait sits on the critical path of every application.
+int32_t g_fused_rows = 0;
 size_t psell_smem() {
   if (g_psell_ctas <= 0) return 0;
   return static_cast<size_t>(std::max(0, 233472 / g_psell_ctas - 1024 - 1024)) & ~size_t(1023);
@@ -719,6 +726,9 @@ struct ig_hier {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   PcgState* st = nullptr;
   double* partials = nullptr;
+  unsigned int* fused_ctr = nullptr;  // k_as_fused arrival counters (2)
+  unsigned fused_cap = 0;             // co-resident CTAs of k_as_fused (occupancy x SMs)
+  int32_t fused_rows = 0;             // levels with n <= this use k_as_fused
   double* residuals = nullptr;
   int32_t res_cap = 0;
   double *r = nullptr, *z = nullptr, *p = nullptr, *ap = nullptr;
@@ -947,6 +957,18 @@ struct ig_hier {
   void smoother(const Level& l, const double* r, double* x, bool acc, PcgState* s, const double* rdot, int dir = -1) {
     if (l.ms) {
       ms_smoother(l, r, x, acc, s, rdot, dir < 0 ? (acc ? 1 : 0) : dir);
+      return;
+    }
+    if (l.n <= fused_rows) {  // one kernel: blocks, singletons, then lists (k_as_fused)
+      const int64_t need = std::max<int64_t>((static_cast<int64_t>(l.G.n_groups + l.G.n_wblocks) + 7) / 8,
+                                             (static_cast<int64_t>(l.n) + kCta - 1) / kCta);
+      const unsigned gf = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(need, fused_cap)));
+      if (acc)
+        launch(k_as_fused<true>, gf, kCta, 0, stream, l.G, l.S, r, l.ybuf, x, fused_ctr, s);
+      else
+        launch(k_as_fused<false>, gf, kCta, 0, stream, l.G, l.S, r, l.ybuf, x, fused_ctr, s);
+      CK(cudaGetLastError());
+      if (rdot) launch(k_pcg_rz, red_grid(l.n), kCta, 0, stream, l.n, rdot, x, s, partials);
       return;
     }
     // Big groups (smax > 4) and warp blocks on the side stream; the small
@@ -1745,6 +1767,11 @@ int ig_set_option(int32_t option, int64_t value) {
     g_red_ctas = static_cast<int>(value);
     return IG_OK;
   }
+  if (option == IG_OPT_FUSED_AS_ROWS) {
+    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: fused smoother rows out of range");
+    g_fused_rows = static_cast<int32_t>(value);
+    return IG_OK;
+  }
   if (option == IG_OPT_PSELL_CTAS) {
     if (value < 0 || value > 8) return fail(IG_INVALID_ARGUMENT, "ig_set_option: pattern-SELL CTAs per SM in 0..8");
     g_psell_ctas = static_cast<int>(value);
@@ -1920,6 +1947,15 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     h->hb = h->alloc<double>(nf);
     h->hx = h->alloc<double>(nf);
     h->partials = h->alloc<double>(grid_of(nf) + 1);
+    h->fused_ctr = h->alloc<unsigned int>(2);
+    CK(cudaMemset(h->fused_ctr, 0, 2 * sizeof(unsigned int)));
+    {
+      int occ0 = 0, occ1 = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, k_as_fused<false>, kCta, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_as_fused<true>, kCta, 0));
+      h->fused_cap = static_cast<unsigned>(std::max(1, std::min(occ0, occ1)) * h->num_sms);
+      h->fused_rows = g_fused_rows;
+    }
     h->st = h->alloc<PcgState>(1);
     CK(cudaMemset(h->st, 0, sizeof(PcgState)));
     h->ensure_residuals(1000);
@@ -1949,6 +1985,7 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       // smoother: [blocks] + simple + [complex | finish_red on the finest], twice;
       // plus SpMV-residual x2, restriction, prolongation
       int per_app = (L.n_multi > 0 ? 1 : 0) + 1 + (L.S.n_complex > 0 ? 1 : 0);
+      if (L.n <= h->fused_rows) per_app = 1;  // k_as_fused
       if (L.ms) {
         int ne = 0;
         for (const auto& mc : L.colors) ne += mc.n_items > 0 ? 1 : 0;

@@ -902,6 +902,96 @@ __global__ void IG_AS_BOUNDS k_as_complex(AsGather S, const double* __restrict__
   as_complex_item<ACC>(S, c, r, ybuf, x);
 }
 
+// ---------------------------------------------- fused additive smoother ----
+// The whole AS application of one level in ONE kernel (levels up to
+// IG_OPT_FUSED_AS_ROWS rows), replacing fork -> {k_as_blocks ||
+// k_as_small_simple} -> join -> k_as_complex.  On the small levels those
+// three dependent launches plus the graph's fork/join cost ~22 us per
+// application for a few microseconds of work.
+//   phase 1  block items (groups of small blocks, warp blocks) -> ybuf
+//            (warps of the bounded grid stride over the items);
+//            then the CTA arrives on ctr[0]
+//   phase 2  singleton DOFs (no ybuf dependency) while others finish phase 1
+//   phase 3  wait for all CTAs' phase-1 arrivals, then the DOFs with
+//            contribution lists (ybuf read through L2: written by other SMs
+//            in this launch)
+// The grid never exceeds the co-resident capacity (host: occupancy x SMs),
+// so the wait cannot starve; with PDL the dependents launch only after every
+// CTA of this grid has started.  The last CTA to leave resets both counters.
+// Per-DOF arithmetic and order are those of the split kernels (bit-identical).
+struct YbufL2 {
+  const double* p;
+  __device__ __forceinline__ double operator()(int i) const { return __ldcg(p + i); }
+};
+template <class YB>
+__device__ __forceinline__ double as_list_sum_y(const AsGather& S, int c, double rd, YB yb) {
+  const int q0 = S.cptr[c], q1 = S.cptr[c + 1];
+  double acc = 0.0;
+  constexpr int U = 8;
+  for (int qb = q0; qb < q1; qb += U) {
+    int code[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) code[u] = (qb + u < q1) ? S.centry[qb + u] : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (qb + u < q1) {
+        if (code[u] < 0) {
+          const double ls = S.sval[-code[u] - 1];
+          v[u] = (rd / ls) / ls;
+        } else {
+          v[u] = yb(code[u]);
+        }
+      } else {
+        v[u] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (qb + u < q1) acc = acc + v[u];
+  }
+  return acc;
+}
+template <bool ACC>
+__global__ void __launch_bounds__(kCta) k_as_fused(AsGroups G, AsGather S, const double* __restrict__ r,
+                                                  double* ybuf, double* x, unsigned int* ctr, const PcgState* st) {
+  pdl_entry();
+  if (pcg_done(st)) return;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = static_cast<int>(gridDim.x) * (kCta / 32);
+  const int nitems = G.n_groups + G.n_wblocks;
+  for (int w = static_cast<int>(blockIdx.x) * (kCta / 32) + (threadIdx.x >> 5); w < nitems; w += nwarps)
+    as_blocks_item(G, w, lane, r, ybuf);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(&ctr[0], 1u);
+  const int nthreads = static_cast<int>(gridDim.x) * kCta;
+  for (int d = static_cast<int>(blockIdx.x) * kCta + threadIdx.x; d < S.n; d += nthreads)
+    as_simple_item<ACC>(S, d, r, x);
+  if (threadIdx.x == 0) {
+    unsigned int seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
+    } while (seen < gridDim.x);
+  }
+  __syncthreads();
+  const YbufL2 yb{ybuf};
+  for (int c = static_cast<int>(blockIdx.x) * kCta + threadIdx.x; c < S.n_complex; c += nthreads) {
+    const int d = S.cdof[c];
+    const double out = S.gamma * as_list_sum_y(S, c, r[d], yb);
+    x[d] = ACC ? x[d] + out : out;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(&ctr[1], 1u);
+    if (prev == gridDim.x - 1) {  // everyone has passed the wait: reset for the next launch
+      ctr[0] = 0u;
+      ctr[1] = 0u;
+      __threadfence();
+    }
+  }
+}
+
 // Finest level inside PCG: complex DOFs finish here, simple DOFs read back
 // k_as_simple's result, and every DOF contributes r_d * z_d to r . z in the
 // canonical chunk order.

@@ -136,3 +136,32 @@ def test_breakdown_through_pattern_sell():
         assert len(e.value.report.residuals) >= 1
     finally:
         h.close()
+
+
+@pytest.mark.parametrize("case_name", ["c1_case", "d3_case", "star_case", "c3_small_case"])
+def test_fused_smoother_bitwise(request, case_name):
+    """The single-kernel additive smoother (k_as_fused, IG_OPT_FUSED_AS_ROWS;
+    off by default) on every level gives the same bits as the fork/join split:
+    smoother applications, V-cycles and the whole PCG solve vs the oracle."""
+    from paper_1903_10977_b200 import MgHierarchy, _ffi, pcg
+    lib = _ffi.gpu()
+    case = request.getfixturevalue(case_name)
+    lib.ig_set_option(_ffi.IG_OPT_FUSED_AS_ROWS, 1 << 30)
+    try:
+        h = MgHierarchy(case)
+    finally:
+        lib.ig_set_option(_ffi.IG_OPT_FUSED_AS_ROWS, 0)
+    lv = case.levels_c()
+    try:
+        for l in range(1, h.levels()):
+            r = rng_vec(27 + l, h._n[l])
+            assert np.array_equal(h.smoother_apply(l, r), orc.smoother_apply(lv, l, r))
+        for l in range(h.levels()):
+            r = rng_vec(37 + l, h._n[l])
+            assert np.array_equal(h.vcycle_at(l, r), orc.vcycle_at(lv, l, r))
+        x, rep = pcg(h.A, case.b, h, tol=1e-8, maxit=1000)
+        st, xo, ro, it, _ = orc.pcg(lv, case.b, tol=1e-8, maxit=1000, mode=orc.GPU_ORDER)
+        assert st == 0 and rep.iterations == it
+        assert np.array_equal(np.array(rep.residuals), ro) and np.array_equal(x, xo)
+    finally:
+        h.close()
