@@ -199,6 +199,23 @@ int ig_debug_vcycle_timeline(ig_hier *h, const double *d_r, double *d_x,
 int ig_debug_tail_profile(ig_hier *h, const double *d_r, double *d_x, uint64_t *stamps,
                           int32_t cap, int32_t *count);
 
+/* --- device-side hierarchy setup ---------------- */
+/* Galerkin coarse operators on the device: starting from A_fine (the finest
+ * level's A), A_{l-1} = R_l (A_l R_l^T) for l = n_levels-1 .. 1, exactly the
+ * products of MgHierarchy::build (proj/src/multigrid.cpp:37-41,
+ * `r * (down.back().A * rt)`), bit-identical to Eigen's sparse-product
+ * summation order (each entry summed over the inner index ascending, first
+ * product assigned).  R[l] (l >= 1) is the restriction of level l (rows
+ * n_{l-1}, cols n_l), as ig_level.R; R[0] is ignored.  A_out[l] for
+ * l = 0 .. n_levels-2 receives the coarse operators in host arrays owned by
+ * the library (release each with ig_csr_free).  seconds (may be NULL) gets
+ * 2 doubles: [0] wall time of the call (uploads and downloads included),
+ * [1] device time of the transposes and products (CUDA events).
+ * IG_UNSUPPORTED if a product row has more than 768 distinct columns. */
+int ig_galerkin_hierarchy(const ig_csr *A_fine, const ig_csr *R, int32_t n_levels, ig_csr *A_out,
+                          double *seconds);
+void ig_csr_free(ig_csr *m);
+
 /* Thread-local message for the last non-OK status. */
 const char *ig_last_error(void);
 

@@ -223,6 +223,45 @@ class SpMat:
         return sp.csr_matrix((self.val, self.col_idx, self.row_ptr), shape=self.shape)
 
 
+def galerkin_hierarchy(A_fine: "SpMat", R: Sequence[Optional["SpMat"]]):
+    """Device-side Galerkin products of MgHierarchy::build
+    (proj/src/multigrid.cpp:37-41, `r * (A * r.transpose())` level by level):
+    A_{l-1} = R_l (A_l R_l^T) for l = L-1 .. 1 on the GPU, bit-identical to the
+    host (Eigen-order) products.  `R[l]` is level l's restriction (R[0] unused).
+    Returns ([A_0 .. A_{L-2}] as SpMat with numpy-owned arrays,
+    (wall_seconds, device_seconds))."""
+    lib = _ffi.gpu()
+    L = len(R)
+
+    keep = []  # arrays referenced by the C structs stay alive until the call returns
+
+    def to_c(m: SpMat):
+        rp = np.ascontiguousarray(m.row_ptr, np.int32)
+        ci = np.ascontiguousarray(m.col_idx, np.int32)
+        vv = np.ascontiguousarray(m.val, np.float64)
+        keep.extend((rp, ci, vv))
+        return _ffi.ig_csr(m.shape[0], m.shape[1], m.nnz, rp.ctypes.data_as(C.POINTER(C.c_int32)),
+                           ci.ctypes.data_as(C.POINTER(C.c_int32)), vv.ctypes.data_as(C.POINTER(C.c_double)))
+
+    a = to_c(A_fine)
+    rs = (_ffi.ig_csr * L)()
+    for l in range(1, L):
+        rs[l] = to_c(R[l])
+    out = (_ffi.ig_csr * max(L - 1, 1))()
+    sec = (C.c_double * 2)()
+    _check(lib, lib.ig_galerkin_hierarchy(C.byref(a), rs, L, out, sec), "ig_galerkin_hierarchy")
+    res = []
+    try:
+        for l in range(L - 1):
+            m = SpMat.from_c(out[l])
+            res.append(SpMat(m.shape[0], m.shape[1], m.row_ptr.copy(), m.col_idx.copy(), m.val.copy()))
+    finally:
+        for l in range(L - 1):
+            lib.ig_csr_free(C.byref(out[l]))
+    del keep
+    return res, (sec[0], sec[1])
+
+
 class Case:
     """Host-built case: fine system (A, b) and the multigrid hierarchy payload
     that crosses the C-ABI (owned by libig_host.so until close())."""

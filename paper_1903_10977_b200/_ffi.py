@@ -123,7 +123,7 @@ GPU_SYMBOLS = (
     "ig_vcycle", "ig_vcycle_at", "ig_coarse_solve", "ig_smoother_apply",
     "ig_level_spmv", "ig_pcg", "ig_vcycle_device", "ig_level_spmv_device", "ig_pcg_device",
     "ig_pcg_result", "ig_last_error", "ig_set_option", "ig_richardson",
-    "ig_smoother_apply_dir", "ig_smoother_apply_symmetric",
+    "ig_smoother_apply_dir", "ig_smoother_apply_symmetric", "ig_galerkin_hierarchy", "ig_csr_free",
 )
 
 
@@ -133,6 +133,9 @@ def gpu() -> C.CDLL:
         lib = _lib(os.environ.get("IG_GPU_LIB", "libig_gpu.so"))  # variant builds for profiling only
         vp, dp = C.c_void_p, P(f64)
         lib.ig_hier_create.argtypes = [P(ig_level), i32, P(ig_coarse), P(vp)]
+        lib.ig_galerkin_hierarchy.argtypes = [P(ig_csr), P(ig_csr), i32, P(ig_csr), dp]
+        lib.ig_csr_free.argtypes = [P(ig_csr)]
+        lib.ig_csr_free.restype = None
         lib.ig_hier_destroy.argtypes = [vp]
         lib.ig_hier_destroy.restype = None
         lib.ig_hier_info.argtypes = [vp, P(ig_info)]

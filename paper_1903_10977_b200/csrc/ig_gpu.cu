@@ -29,6 +29,7 @@
 #include "ig_gpu.h"
 #include "kernels.cuh"
 #include "spmv_psell.cuh"
+#include "galerkin.cuh"
 #include "spmv_tma.cuh"
 #include "vtail.cuh"
 
@@ -2362,6 +2363,216 @@ int ig_richardson(ig_hier* h, const double* b, double tol, int32_t maxit, double
     if (s == IG_DIVERGED) g_err = "richardson: residual grew for 10 consecutive steps";
     return s;
   });
+}
+
+}  // extern "C"
+
+// ----------------------------------------------------- device Galerkin -----
+namespace {
+
+// Device CSR owned by the Galerkin driver (int64 row offsets while building).
+struct GalMat {
+  int32_t nr = 0, nc = 0;
+  int64_t nnz = 0;
+  int32_t* ptr = nullptr;  // int32 row offsets (kernels' input form)
+  int32_t* col = nullptr;
+  double* val = nullptr;
+  GalCsr view() const { return GalCsr{nr, nc, ptr, col, val}; }
+  void free_all() {
+    cudaFree(ptr);
+    cudaFree(col);
+    cudaFree(val);
+    ptr = nullptr;
+    col = nullptr;
+    val = nullptr;
+  }
+};
+
+template <typename T>
+T* dmalloc(size_t n) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+__global__ void k_i64_to_i32(int64_t n, const int64_t* a, int32_t* b) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = static_cast<int32_t>(a[i]);
+}
+
+GalMat gal_upload(const ig_csr& a, cudaStream_t st) {
+  GalMat m;
+  m.nr = a.n_rows;
+  m.nc = a.n_cols;
+  m.nnz = a.nnz;
+  m.ptr = dmalloc<int32_t>(static_cast<size_t>(a.n_rows) + 1);
+  m.col = dmalloc<int32_t>(static_cast<size_t>(a.nnz));
+  m.val = dmalloc<double>(static_cast<size_t>(a.nnz));
+  CK(cudaMemcpyAsync(m.ptr, a.row_ptr, sizeof(int32_t) * (a.n_rows + 1), cudaMemcpyHostToDevice, st));
+  if (a.nnz) {
+    CK(cudaMemcpyAsync(m.col, a.col_idx, sizeof(int32_t) * a.nnz, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m.val, a.val, sizeof(double) * a.nnz, cudaMemcpyHostToDevice, st));
+  }
+  return m;
+}
+
+// Offsets from per-row counts; returns the total (synchronises).
+int64_t gal_offsets(int32_t n, const int32_t* cnt, int64_t* off64, int32_t* off32, cudaStream_t st) {
+  k_scan_counts<<<1, 1024, 0, st>>>(n, cnt, off64);
+  CK(cudaGetLastError());
+  int64_t tot = 0;
+  CK(cudaMemcpyAsync(&tot, off64 + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (tot > INT32_MAX) throw Error(IG_UNSUPPORTED, "galerkin: product has more than 2^31 nonzeros (int32 CSR)");
+  const int64_t n1 = static_cast<int64_t>(n) + 1;
+  k_i64_to_i32<<<static_cast<unsigned>((n1 + 255) / 256), 256, 0, st>>>(n1, off64, off32);
+  CK(cudaGetLastError());
+  return tot;
+}
+
+GalMat gal_transpose(const GalMat& m, cudaStream_t st) {
+  GalMat t;
+  t.nr = m.nc;
+  t.nc = m.nr;
+  t.nnz = m.nnz;
+  int32_t* cnt = dmalloc<int32_t>(static_cast<size_t>(t.nr));
+  int64_t* off = dmalloc<int64_t>(static_cast<size_t>(t.nr) + 1);
+  t.ptr = dmalloc<int32_t>(static_cast<size_t>(t.nr) + 1);
+  t.col = dmalloc<int32_t>(static_cast<size_t>(t.nnz));
+  t.val = dmalloc<double>(static_cast<size_t>(t.nnz));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * t.nr, st));
+  const unsigned g = static_cast<unsigned>((m.nr + 255) / 256);
+  if (g) k_tr_count<<<g, 256, 0, st>>>(m.view(), cnt);
+  CK(cudaGetLastError());
+  gal_offsets(t.nr, cnt, off, t.ptr, st);
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * t.nr, st));
+  if (g) k_tr_scatter<<<g, 256, 0, st>>>(m.view(), off, cnt, t.col, t.val);
+  const unsigned gt = static_cast<unsigned>((t.nr + 255) / 256);
+  if (gt) k_tr_sort<<<gt, 256, 0, st>>>(t.nr, off, t.col, t.val);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  cudaFree(cnt);
+  cudaFree(off);
+  return t;
+}
+
+// C = A B with the host spgemm's summation order (galerkin.cuh).
+GalMat gal_spgemm(const GalMat& a, const GalMat& b, cudaStream_t st) {
+  if (a.nc != b.nr) throw Error(IG_INVALID_ARGUMENT, "galerkin: inner dimension mismatch");
+  GalMat c;
+  c.nr = a.nr;
+  c.nc = b.nc;
+  int32_t* cnt = dmalloc<int32_t>(static_cast<size_t>(c.nr));
+  int64_t* off = dmalloc<int64_t>(static_cast<size_t>(c.nr) + 1);
+  c.ptr = dmalloc<int32_t>(static_cast<size_t>(c.nr) + 1);
+  const unsigned g = static_cast<unsigned>((c.nr + kGalWarps - 1) / kGalWarps);
+  if (g) k_gal_count<<<g, 32 * kGalWarps, kGalCountSmem, st>>>(a.view(), b.view(), cnt);
+  CK(cudaGetLastError());
+  // Rows that do not fit the per-warp table: fail loudly.
+  {
+    int32_t mx = 0;
+    std::vector<int32_t> hc(static_cast<size_t>(c.nr));
+    if (c.nr) CK(cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * c.nr, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int32_t v : hc) mx = std::max(mx, v);
+    if (mx > kGalLoad)
+      throw Error(IG_UNSUPPORTED, "galerkin: a product row has more than " + std::to_string(kGalLoad) +
+                                      " distinct columns (device table limit)");
+  }
+  c.nnz = gal_offsets(c.nr, cnt, off, c.ptr, st);
+  c.col = dmalloc<int32_t>(static_cast<size_t>(c.nnz));
+  c.val = dmalloc<double>(static_cast<size_t>(c.nnz));
+  if (g) k_gal_fill<<<g, 32 * kGalWarps, kGalFillSmem, st>>>(a.view(), b.view(), off, c.col, c.val);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  cudaFree(cnt);
+  cudaFree(off);
+  return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ig_galerkin_hierarchy(const ig_csr* A_fine, const ig_csr* R, int32_t n_levels, ig_csr* A_out, double* seconds) {
+  if (!A_fine || !R || !A_out || n_levels < 1) return fail(IG_INVALID_ARGUMENT, "galerkin: null argument");
+  for (int32_t l = 0; l + 1 < n_levels; ++l) A_out[l] = ig_csr{};
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  GalMat A, Rd, Rt, C;
+  const auto t0 = std::chrono::steady_clock::now();
+  const int rc = guarded([&] {
+    check_csr(*A_fine, "galerkin: A");
+    for (int32_t l = 1; l < n_levels; ++l) check_csr(R[l], "galerkin: R");
+    CK(cudaFuncSetAttribute(k_gal_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGalFillSmem)));
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    A = gal_upload(*A_fine, st);
+    float dev_ms = 0.f;
+    for (int32_t l = n_levels - 1; l >= 1; --l) {
+      const ig_csr& r = R[l];
+      if (r.n_cols != A.nr || r.n_rows <= 0)
+        throw Error(IG_INVALID_ARGUMENT, "galerkin: R[" + std::to_string(l) + "] does not match level " +
+                                             std::to_string(l));
+      Rd = gal_upload(r, st);
+      CK(cudaStreamSynchronize(st));
+      CK(cudaEventRecord(e0, st));
+      Rt = gal_transpose(Rd, st);
+      C = gal_spgemm(A, Rt, st);  // A R^T
+      Rt.free_all();
+      GalMat Ac = gal_spgemm(Rd, C, st);  // R (A R^T)
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      dev_ms += ms;
+      C.free_all();
+      Rd.free_all();
+      A.free_all();
+      A = Ac;
+      ig_csr& o = A_out[l - 1];
+      o.n_rows = A.nr;
+      o.n_cols = A.nc;
+      o.nnz = A.nnz;
+      int32_t* hp = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * (A.nr + 1)));
+      int32_t* hc = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * std::max<int64_t>(A.nnz, 1)));
+      double* hv = static_cast<double*>(std::malloc(sizeof(double) * std::max<int64_t>(A.nnz, 1)));
+      o.row_ptr = hp;
+      o.col_idx = hc;
+      o.val = hv;
+      if (!hp || !hc || !hv) throw Error(IG_CUDA_ERROR, "galerkin: host allocation failed");
+      CK(cudaMemcpyAsync(hp, A.ptr, sizeof(int32_t) * (A.nr + 1), cudaMemcpyDeviceToHost, st));
+      if (A.nnz) {
+        CK(cudaMemcpyAsync(hc, A.col, sizeof(int32_t) * A.nnz, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hv, A.val, sizeof(double) * A.nnz, cudaMemcpyDeviceToHost, st));
+      }
+      CK(cudaStreamSynchronize(st));
+    }
+    if (seconds) {
+      seconds[1] = 1e-3 * dev_ms;
+    }
+    return IG_OK;
+  });
+  A.free_all();
+  Rd.free_all();
+  Rt.free_all();
+  C.free_all();
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (st) cudaStreamDestroy(st);
+  if (seconds) seconds[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (rc != IG_OK)
+    for (int32_t l = 0; l + 1 < n_levels; ++l) ig_csr_free(&A_out[l]);
+  return rc;
+}
+
+void ig_csr_free(ig_csr* m) {
+  if (!m) return;
+  std::free(const_cast<int32_t*>(m->row_ptr));
+  std::free(const_cast<int32_t*>(m->col_idx));
+  std::free(const_cast<double*>(m->val));
+  *m = ig_csr{};
 }
 
 }  // extern "C"
