@@ -215,6 +215,20 @@ int ig_debug_tail_profile(ig_hier *h, const double *d_r, double *d_x, uint64_t *
 int ig_galerkin_hierarchy(const ig_csr *A_fine, const ig_csr *R, int32_t n_levels, ig_csr *A_out,
                           double *seconds);
 void ig_csr_free(ig_csr *m);
+/* Batched Schwarz block factorisation on the device (factorize_blocks of
+ * make_smoother, proj/src/smoothers.cpp:131-162): for each pre-filter block
+ * (blk_ptr / blk_dofs: blocks in owner order, DOFs ascending) gather A_b from
+ * A, drop the DOF with the largest |component| of the lowest eigenvector
+ * while lambda_min < filter_ratio * max diag (no filtering when
+ * filter_ratio <= 0), then the lower Cholesky factor (Eigen::LLT).  Output:
+ * the post-filter layout in `out` (host arrays owned by the library; release
+ * with ig_blocks_free; n_colors = 0), bit-identical to the host factorisation.
+ * *filtered_dofs (may be NULL) = DOFs removed.  seconds (may be NULL): [0]
+ * wall time, [1] device time.  IG_INVALID_ARGUMENT if a block loses every DOF
+ * (the reference's std::runtime_error). */
+int ig_factorize_blocks(const ig_csr *A, int32_t n_blocks, const int32_t *blk_ptr, const int32_t *blk_dofs,
+                        double filter_ratio, ig_blocks *out, int64_t *filtered_dofs, double *seconds);
+void ig_blocks_free(ig_blocks *b);
 
 /* Thread-local message for the last non-OK status. */
 const char *ig_last_error(void);

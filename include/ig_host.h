@@ -72,6 +72,11 @@ int igh_build(const igh_config *cfg, igh_case **out);
 int igh_levels(const igh_case *c, const ig_level **levels, int32_t *n_levels,
                const ig_coarse **coarse);
 const double *igh_rhs(const igh_case *c, int32_t *n);
+/* Pre-filter Schwarz layout of level >= 1 (select_blocks output, the input of
+ * factorize_blocks, smoothers.cpp:131-162): blocks in owner order, DOFs
+ * ascending.  Owned by the case; built cases only (not igh_read). */
+int igh_prefilter_blocks(const igh_case *c, int32_t level, int32_t *n_blocks,
+                         const int32_t **blk_ptr, const int32_t **blk_dofs);
 int igh_get_info(const igh_case *c, igh_info *out);
 /* Kept anchors of level l as untrimmed tensor indices (ax, ay, az) -> n x 3. */
 int igh_anchors(const igh_case *c, int32_t level, int32_t *out_xyz);

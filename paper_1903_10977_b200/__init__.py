@@ -262,6 +262,37 @@ def galerkin_hierarchy(A_fine: "SpMat", R: Sequence[Optional["SpMat"]]):
     return res, (sec[0], sec[1])
 
 
+def factorize_blocks(A: "SpMat", blk_ptr, blk_dofs, filter_ratio: float = 1e-16):
+    """Device batched Schwarz block factorisation (make_smoother's
+    factorize_blocks, proj/src/smoothers.cpp:131-162): eigen-filter + LLT of
+    every pre-filter block.  Returns (blk_ptr, blk_dofs, fac_ptr, fac,
+    filtered_dofs, (wall_seconds, device_seconds)) of the post-filter layout,
+    bit-identical to the host factorisation."""
+    lib = _ffi.gpu()
+    rp = np.ascontiguousarray(A.row_ptr, np.int32)
+    ci = np.ascontiguousarray(A.col_idx, np.int32)
+    vv = np.ascontiguousarray(A.val, np.float64)
+    a = _ffi.ig_csr(A.shape[0], A.shape[1], A.nnz, rp.ctypes.data_as(C.POINTER(C.c_int32)),
+                    ci.ctypes.data_as(C.POINTER(C.c_int32)), vv.ctypes.data_as(C.POINTER(C.c_double)))
+    bp = np.ascontiguousarray(blk_ptr, np.int32)
+    bd = np.ascontiguousarray(blk_dofs, np.int32)
+    nb = bp.shape[0] - 1
+    out = _ffi.ig_blocks()
+    filt = C.c_int64()
+    sec = (C.c_double * 2)()
+    _check(lib, lib.ig_factorize_blocks(C.byref(a), nb, bp.ctypes.data_as(C.POINTER(C.c_int32)),
+                                        bd.ctypes.data_as(C.POINTER(C.c_int32)), float(filter_ratio),
+                                        C.byref(out), C.byref(filt), sec), "ig_factorize_blocks")
+    try:
+        optr = np.ctypeslib.as_array(out.blk_ptr, (nb + 1,)).copy()
+        odofs = np.ctypeslib.as_array(out.blk_dofs, (max(int(optr[-1]), 1),))[:int(optr[-1])].copy()
+        ofp = np.ctypeslib.as_array(out.fac_ptr, (nb + 1,)).copy()
+        ofac = np.ctypeslib.as_array(out.fac, (max(int(ofp[-1]), 1),))[:int(ofp[-1])].copy()
+    finally:
+        lib.ig_blocks_free(C.byref(out))
+    return optr, odofs, ofp, ofac, int(filt.value), (sec[0], sec[1])
+
+
 class Case:
     """Host-built case: fine system (A, b) and the multigrid hierarchy payload
     that crosses the C-ABI (owned by libig_host.so until close())."""
@@ -295,6 +326,16 @@ class Case:
 
     def level_A(self, l: int) -> SpMat:
         return SpMat.from_c(self._lv[l].A, self)
+
+    def prefilter_blocks(self, l: int):
+        """(blk_ptr, blk_dofs) of level l's pre-filter Schwarz layout (select_blocks)."""
+        nb = C.c_int32()
+        bp = C.POINTER(C.c_int32)()
+        bd = C.POINTER(C.c_int32)()
+        _check(_ffi.host(), _ffi.host().igh_prefilter_blocks(self._h, l, C.byref(nb), C.byref(bp), C.byref(bd)),
+               "igh_prefilter_blocks")
+        ptr = np.ctypeslib.as_array(bp, (nb.value + 1,)).copy()
+        return ptr, np.ctypeslib.as_array(bd, (max(int(ptr[-1]), 1),))[:int(ptr[-1])].copy()
 
     def level_R(self, l: int) -> SpMat:
         return SpMat.from_c(self._lv[l].R, self)

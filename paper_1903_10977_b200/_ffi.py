@@ -104,6 +104,7 @@ def host() -> C.CDLL:
         lib.igh_levels.argtypes = [C.c_void_p, P(P(ig_level)), P(i32), P(P(ig_coarse))]
         lib.igh_rhs.argtypes = [C.c_void_p, P(i32)]
         lib.igh_rhs.restype = P(f64)
+        lib.igh_prefilter_blocks.argtypes = [C.c_void_p, i32, P(i32), P(P(i32)), P(P(i32))]
         lib.igh_get_info.argtypes = [C.c_void_p, P(igh_info)]
         lib.igh_anchors.argtypes = [C.c_void_p, i32, P(i32)]
         lib.igh_write.argtypes = [C.c_void_p, C.c_char_p]
@@ -124,6 +125,7 @@ GPU_SYMBOLS = (
     "ig_level_spmv", "ig_pcg", "ig_vcycle_device", "ig_level_spmv_device", "ig_pcg_device",
     "ig_pcg_result", "ig_last_error", "ig_set_option", "ig_richardson",
     "ig_smoother_apply_dir", "ig_smoother_apply_symmetric", "ig_galerkin_hierarchy", "ig_csr_free",
+    "ig_factorize_blocks", "ig_blocks_free",
 )
 
 
@@ -136,6 +138,9 @@ def gpu() -> C.CDLL:
         lib.ig_galerkin_hierarchy.argtypes = [P(ig_csr), P(ig_csr), i32, P(ig_csr), dp]
         lib.ig_csr_free.argtypes = [P(ig_csr)]
         lib.ig_csr_free.restype = None
+        lib.ig_factorize_blocks.argtypes = [P(ig_csr), i32, P(i32), P(i32), f64, P(ig_blocks), P(i64), dp]
+        lib.ig_blocks_free.argtypes = [P(ig_blocks)]
+        lib.ig_blocks_free.restype = None
         lib.ig_hier_destroy.argtypes = [vp]
         lib.ig_hier_destroy.restype = None
         lib.ig_hier_info.argtypes = [vp, P(ig_info)]

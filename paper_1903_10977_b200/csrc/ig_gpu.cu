@@ -30,6 +30,7 @@
 #include "kernels.cuh"
 #include "spmv_psell.cuh"
 #include "galerkin.cuh"
+#include "blockfac.cuh"
 #include "spmv_tma.cuh"
 #include "vtail.cuh"
 
@@ -2573,6 +2574,130 @@ void ig_csr_free(ig_csr* m) {
   std::free(const_cast<int32_t*>(m->col_idx));
   std::free(const_cast<double*>(m->val));
   *m = ig_csr{};
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int ig_factorize_blocks(const ig_csr* A, int32_t n_blocks, const int32_t* blk_ptr, const int32_t* blk_dofs,
+                        double filter_ratio, ig_blocks* out, int64_t* filtered_dofs, double* seconds) {
+  if (!A || !blk_ptr || (n_blocks > 0 && !blk_dofs) || !out || n_blocks < 0)
+    return fail(IG_INVALID_ARGUMENT, "factorize_blocks: null argument");
+  *out = ig_blocks{};
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  GalMat Ad;
+  std::vector<void*> dev;
+  auto dal = [&](size_t bytes) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
+    dev.push_back(p);
+    return p;
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  const int rc = guarded([&] {
+    check_csr(*A, "factorize_blocks: A");
+    if (blk_ptr[0] != 0) throw Error(IG_INVALID_ARGUMENT, "factorize_blocks: blk_ptr[0] != 0");
+    std::vector<int64_t> soff(static_cast<size_t>(n_blocks) + 1, 0);
+    for (int32_t b = 0; b < n_blocks; ++b) {
+      const int64_t sb = blk_ptr[b + 1] - blk_ptr[b];
+      if (sb < 1) throw Error(IG_INVALID_ARGUMENT, "factorize_blocks: empty block");
+      for (int32_t i = blk_ptr[b]; i < blk_ptr[b + 1]; ++i)
+        if (blk_dofs[i] < 0 || blk_dofs[i] >= A->n_rows) throw Error(IG_INVALID_ARGUMENT, "factorize_blocks: DOF out of range");
+      soff[b + 1] = soff[b] + 3 * sb * sb;
+    }
+    const int64_t nd = n_blocks ? blk_ptr[n_blocks] : 0;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    Ad = gal_upload(*A, st);
+    auto* dptr = static_cast<int32_t*>(dal(sizeof(int32_t) * (n_blocks + 1)));
+    auto* ddofs = static_cast<int32_t*>(dal(sizeof(int32_t) * nd));
+    auto* dsoff = static_cast<int64_t*>(dal(sizeof(int64_t) * (n_blocks + 1)));
+    auto* scratch = static_cast<double*>(dal(sizeof(double) * soff[n_blocks]));
+    auto* kdofs = static_cast<int32_t*>(dal(sizeof(int32_t) * nd));
+    auto* ksize = static_cast<int32_t*>(dal(sizeof(int32_t) * n_blocks));
+    CK(cudaMemcpyAsync(dptr, blk_ptr, sizeof(int32_t) * (n_blocks + 1), cudaMemcpyHostToDevice, st));
+    if (nd) CK(cudaMemcpyAsync(ddofs, blk_dofs, sizeof(int32_t) * nd, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dsoff, soff.data(), sizeof(int64_t) * (n_blocks + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaEventRecord(e0, st));
+    std::vector<int32_t> big;
+    for (int32_t b = 0; b < n_blocks; ++b) {
+      const int sb = blk_ptr[b + 1] - blk_ptr[b];
+      if (sb >= kBfWarpMin && sb <= 32) big.push_back(b);
+    }
+    auto* dbig = static_cast<int32_t*>(dal(sizeof(int32_t) * big.size()));
+    if (!big.empty())
+      CK(cudaMemcpyAsync(dbig, big.data(), sizeof(int32_t) * big.size(), cudaMemcpyHostToDevice, st));
+    BlockFacArgs fa{Ad.view(), n_blocks, dptr, ddofs, dsoff, scratch, kdofs, ksize, filter_ratio, 1};
+    const unsigned g = static_cast<unsigned>((n_blocks + 127) / 128);
+    CK(cudaFuncSetAttribute(k_block_factor_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(kBfWarpSmem)));
+    if (!big.empty())
+      k_block_factor_warp<<<static_cast<unsigned>((big.size() + kBfWarps - 1) / kBfWarps), 32 * kBfWarps, kBfWarpSmem,
+                            st>>>(fa, dbig, static_cast<int32_t>(big.size()));
+    if (g) k_block_factor<<<g, 128, 0, st>>>(fa);
+    CK(cudaGetLastError());
+    std::vector<int32_t> hs(static_cast<size_t>(n_blocks));
+    if (n_blocks) CK(cudaMemcpyAsync(hs.data(), ksize, sizeof(int32_t) * n_blocks, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int64_t> optr(static_cast<size_t>(n_blocks) + 1, 0), ofptr(static_cast<size_t>(n_blocks) + 1, 0);
+    for (int32_t b = 0; b < n_blocks; ++b) {
+      if (hs[b] < 0) throw Error(IG_INVALID_ARGUMENT, "factorize_blocks: all DOFs filtered from a block");
+      optr[b + 1] = optr[b] + hs[b];
+      ofptr[b + 1] = ofptr[b] + static_cast<int64_t>(hs[b]) * hs[b];
+    }
+    auto* doptr = static_cast<int64_t*>(dal(sizeof(int64_t) * (n_blocks + 1)));
+    auto* dofptr = static_cast<int64_t*>(dal(sizeof(int64_t) * (n_blocks + 1)));
+    auto* odofs = static_cast<int32_t*>(dal(sizeof(int32_t) * optr[n_blocks]));
+    auto* ofac = static_cast<double*>(dal(sizeof(double) * ofptr[n_blocks]));
+    CK(cudaMemcpyAsync(doptr, optr.data(), sizeof(int64_t) * (n_blocks + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dofptr, ofptr.data(), sizeof(int64_t) * (n_blocks + 1), cudaMemcpyHostToDevice, st));
+    if (g) k_block_compact<<<g, 128, 0, st>>>(n_blocks, dptr, kdofs, ksize, dsoff, scratch, doptr, dofptr, odofs, ofac);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e1, st));
+    auto* hp = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * (n_blocks + 1)));
+    auto* hd = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * std::max<int64_t>(optr[n_blocks], 1)));
+    auto* hfp = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (n_blocks + 1)));
+    auto* hf = static_cast<double*>(std::malloc(sizeof(double) * std::max<int64_t>(ofptr[n_blocks], 1)));
+    out->n_blocks = n_blocks;
+    out->blk_ptr = hp;
+    out->blk_dofs = hd;
+    out->fac_ptr = hfp;
+    out->fac = hf;
+    if (!hp || !hd || !hfp || !hf) throw Error(IG_CUDA_ERROR, "factorize_blocks: host allocation failed");
+    for (int32_t b = 0; b <= n_blocks; ++b) {
+      hp[b] = static_cast<int32_t>(optr[b]);
+      hfp[b] = ofptr[b];
+    }
+    if (optr[n_blocks]) CK(cudaMemcpyAsync(hd, odofs, sizeof(int32_t) * optr[n_blocks], cudaMemcpyDeviceToHost, st));
+    if (ofptr[n_blocks]) CK(cudaMemcpyAsync(hf, ofac, sizeof(double) * ofptr[n_blocks], cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (filtered_dofs) *filtered_dofs = nd - optr[n_blocks];
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (seconds) seconds[1] = 1e-3 * ms;
+    return IG_OK;
+  });
+  Ad.free_all();
+  for (void* p : dev) cudaFree(p);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (st) cudaStreamDestroy(st);
+  if (seconds) seconds[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (rc != IG_OK) ig_blocks_free(out);
+  return rc;
+}
+
+void ig_blocks_free(ig_blocks* b) {
+  if (!b) return;
+  std::free(const_cast<int32_t*>(b->blk_ptr));
+  std::free(const_cast<int32_t*>(b->blk_dofs));
+  std::free(const_cast<int64_t*>(b->fac_ptr));
+  std::free(const_cast<double*>(b->fac));
+  *b = ig_blocks{};
 }
 
 }  // extern "C"

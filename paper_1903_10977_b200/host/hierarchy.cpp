@@ -477,6 +477,9 @@ struct igh_case {
   std::vector<std::unique_ptr<GSpace>> gspaces;  // THB levels
   std::vector<Csr> A, R;
   std::vector<Blocks> B;
+  // Pre-filter Schwarz layouts (block pointers, DOFs) as select_blocks made
+  // them: the input of factorize_blocks, kept for the device factorisation.
+  std::vector<std::vector<int32_t>> pre_ptr, pre_dofs;
   std::vector<double> gamma;
   std::vector<int32_t> kind;
   std::vector<double> coarseL;
@@ -702,6 +705,12 @@ int igh_build(const igh_config* cfg, igh_case** out) {
           });
         }
       }
+      if (c->pre_ptr.size() < static_cast<size_t>(L)) {
+        c->pre_ptr.resize(L);
+        c->pre_dofs.resize(L);
+      }
+      c->pre_ptr[l] = b.ptr;
+      c->pre_dofs[l] = b.dofs;
       const double tf = now();
       factorize_blocks(c->A[l], b, cfg->filter_ratio, threads);
       t_fac += now() - tf;
@@ -755,6 +764,17 @@ int igh_build(const igh_config* cfg, igh_case** out) {
   } catch (const std::exception& e) {
     return fail(e.what());
   }
+}
+
+int igh_prefilter_blocks(const igh_case* c, int32_t level, int32_t* n_blocks, const int32_t** blk_ptr,
+                         const int32_t** blk_dofs) {
+  if (!c || !n_blocks || !blk_ptr || !blk_dofs) return fail("igh_prefilter_blocks: null argument");
+  if (level < 1 || static_cast<size_t>(level) >= c->pre_ptr.size() || c->pre_ptr[level].empty())
+    return fail("igh_prefilter_blocks: no pre-filter layout for this level (levels 1.., built cases only)");
+  *n_blocks = static_cast<int32_t>(c->pre_ptr[level].size()) - 1;
+  *blk_ptr = c->pre_ptr[level].data();
+  *blk_dofs = c->pre_dofs[level].data();
+  return IG_OK;
 }
 
 int igh_levels(const igh_case* c, const ig_level** levels, int32_t* n_levels, const ig_coarse** coarse) {
