@@ -229,6 +229,11 @@ void ig_csr_free(ig_csr *m);
 int ig_factorize_blocks(const ig_csr *A, int32_t n_blocks, const int32_t *blk_ptr, const int32_t *blk_dofs,
                         double filter_ratio, ig_blocks *out, int64_t *filtered_dofs, double *seconds);
 void ig_blocks_free(ig_blocks *b);
+/* Coarsest-level pivoted Cholesky on the device (LAPACK dpstf2, UPLO 'L', as
+ * MgHierarchy::build calls dpstrf, proj/src/multigrid.cpp:57-73): a is n x n
+ * column-major (host buffer, factored in place), piv 1-based, *rank the
+ * accepted pivots; bit-identical to the host restatement igh_pstrf. */
+int ig_pstrf(int32_t n, double *a, int32_t *piv, double tol, int32_t *rank);
 
 /* Thread-local message for the last non-OK status. */
 const char *ig_last_error(void);

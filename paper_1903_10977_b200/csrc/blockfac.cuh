@@ -357,3 +357,114 @@ __global__ void __launch_bounds__(128) k_block_compact(int32_t n_blocks, const i
 }
 
 }  // namespace igk
+
+namespace igk {
+
+// Coarsest-level pivoted Cholesky on the device: LAPACK dpstf2 with
+// UPLO = 'L' (MgHierarchy::build, proj/src/multigrid.cpp:57-73), restated
+// step for step as the host's pstrf_lower (host/hierarchy.cpp): one CTA,
+// row-parallel updates of WORK, the swaps and the DGEMV column update (each
+// entry accumulates over k ascending, reference-BLAS column order), the
+// MAXLOC pivot search (first maximum) by thread 0.  a: n x n column-major in
+// global memory (in place); piv 1-based; *rank_out = returned rank.
+__global__ void __launch_bounds__(1024) k_pstrf(int32_t n, double* a, int32_t* piv, double tol, double* work,
+                                               int32_t* rank_out) {
+  __shared__ int s_pvt;
+  __shared__ double s_ajj;
+  __shared__ int s_ret;
+  auto A = [&](int i, int j) -> double& { return a[static_cast<size_t>(j) * n + i]; };
+  const int t = threadIdx.x, nt = blockDim.x;
+  for (int i = t; i < n; i += nt) piv[i] = i + 1;
+  if (n == 0) {
+    if (t == 0) *rank_out = 0;
+    return;
+  }
+  if (t == 0) {
+    int pvt = 0;
+    double ajj = A(0, 0);
+    for (int i = 1; i < n; ++i)
+      if (A(i, i) > ajj) {
+        pvt = i;
+        ajj = A(pvt, pvt);
+      }
+    s_pvt = pvt;
+    s_ajj = ajj;
+    s_ret = (ajj <= 0.0 || isnan(ajj)) ? 0 : -1;
+  }
+  for (int i = t; i < 2 * n; i += nt) work[i] = 0.0;
+  __syncthreads();
+  if (s_ret == 0) {
+    if (t == 0) *rank_out = 0;
+    return;
+  }
+  const double dstop = tol >= 0.0 ? tol : n * 2.220446049250313e-16 * s_ajj;
+  for (int j = 0; j < n; ++j) {
+    for (int i = j + t; i < n; i += nt) {
+      if (j > 0) work[i] = work[i] + A(i, j - 1) * A(i, j - 1);
+      work[n + i] = A(i, i) - work[i];
+    }
+    __syncthreads();
+    if (j > 0) {
+      if (t == 0) {
+        int pvt = j;
+        for (int i = j + 1; i < n; ++i)
+          if (work[n + i] > work[n + pvt]) pvt = i;
+        s_pvt = pvt;
+        s_ajj = work[n + pvt];
+        if (s_ajj <= dstop || isnan(s_ajj)) {
+          A(j, j) = s_ajj;
+          s_ret = j;
+        }
+      }
+      __syncthreads();
+      if (s_ret >= 0) {
+        if (t == 0) *rank_out = s_ret;
+        return;
+      }
+    }
+    const int pvt = s_pvt;
+    if (j != pvt) {
+      // Same entries as the host's serial swaps: the three index sets are
+      // disjoint, so their order does not matter.
+      if (t == 0) {
+        A(pvt, pvt) = A(j, j);
+        const double w = work[j];
+        work[j] = work[pvt];
+        work[pvt] = w;
+        const int p = piv[j];
+        piv[j] = piv[pvt];
+        piv[pvt] = p;
+      }
+      for (int k = t; k < j; k += nt) {
+        const double x = A(j, k);
+        A(j, k) = A(pvt, k);
+        A(pvt, k) = x;
+      }
+      for (int k = pvt + 1 + t; k < n; k += nt) {
+        const double x = A(k, j);
+        A(k, j) = A(k, pvt);
+        A(k, pvt) = x;
+      }
+      for (int k = t; k < pvt - j - 1; k += nt) {
+        const double x = A(j + 1 + k, j);
+        A(j + 1 + k, j) = A(pvt, j + 1 + k);
+        A(pvt, j + 1 + k) = x;
+      }
+    }
+    __syncthreads();
+    const double ajj = sqrt(s_ajj);
+    if (t == 0) A(j, j) = ajj;
+    if (j < n - 1) {
+      const double r = 1.0 / ajj;
+      for (int i = j + 1 + t; i < n; i += nt) {
+        double v = A(i, j);
+        for (int k = 0; k < j; ++k) v = v + (-A(j, k)) * A(i, k);
+        A(i, j) = v * r;
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) *rank_out = n;
+}
+
+}  // namespace igk

@@ -2701,3 +2701,36 @@ void ig_blocks_free(ig_blocks* b) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int ig_pstrf(int32_t n, double* a, int32_t* piv, double tol, int32_t* rank) {
+  if (n < 0 || (n > 0 && (!a || !piv)) || !rank) return fail(IG_INVALID_ARGUMENT, "pstrf: bad argument");
+  double* da = nullptr;
+  double* dw = nullptr;
+  int32_t* dp = nullptr;
+  int32_t* dr = nullptr;
+  const int rc = guarded([&] {
+    const size_t nn = static_cast<size_t>(n) * n;
+    CK(cudaMalloc(&da, std::max<size_t>(nn, 1) * sizeof(double)));
+    CK(cudaMalloc(&dw, std::max<size_t>(2 * static_cast<size_t>(n), 1) * sizeof(double)));
+    CK(cudaMalloc(&dp, std::max<int32_t>(n, 1) * sizeof(int32_t)));
+    CK(cudaMalloc(&dr, sizeof(int32_t)));
+    if (nn) CK(cudaMemcpy(da, a, nn * sizeof(double), cudaMemcpyHostToDevice));
+    const int threads = std::max(32, std::min(1024, ((n + 31) / 32) * 32));
+    k_pstrf<<<1, threads>>>(n, da, dp, tol, dw, dr);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    if (nn) CK(cudaMemcpy(a, da, nn * sizeof(double), cudaMemcpyDeviceToHost));
+    if (n) CK(cudaMemcpy(piv, dp, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rank, dr, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    return IG_OK;
+  });
+  cudaFree(da);
+  cudaFree(dw);
+  cudaFree(dp);
+  cudaFree(dr);
+  return rc;
+}
+
+}  // extern "C"

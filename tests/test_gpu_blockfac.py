@@ -64,3 +64,50 @@ def test_blockfac_all_filtered_is_an_error(c1_case):
     A = c1_case.level_A(c1_case.n_levels - 1)
     with pytest.raises(ValueError):
         factorize_blocks(A, np.array([0, 2], np.int32), np.array([0, 1], np.int32), 1e300)
+
+
+def _pstrf_both(A, tol):
+    import ctypes as C
+    from paper_1903_10977_b200 import _ffi
+    n = A.shape[0]
+    ah = np.asfortranarray(A.copy())
+    ad = np.asfortranarray(A.copy())
+    ph = np.zeros(max(n, 1), np.int32)
+    pd = np.zeros(max(n, 1), np.int32)
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+    rh = _ffi.host().igh_pstrf(n, ah.ctypes.data_as(dp), ph.ctypes.data_as(ip), tol)
+    rd = C.c_int32(-7)
+    assert _ffi.gpu().ig_pstrf(n, ad.ctypes.data_as(dp), pd.ctypes.data_as(ip), tol, C.byref(rd)) == 0
+    return (rh, ah, ph), (rd.value, ad, pd)
+
+
+@pytest.mark.parametrize("n,r", [(1, 1), (30, 30), (216, 216), (40, 33), (12, 5), (300, 120)])
+def test_device_pstrf_bitwise(n, r):
+    """Device dpstf2 (k_pstrf) vs the host restatement igh_pstrf: rank, pivots
+    and every entry of the factored array (including the untouched trailing
+    part of a rank-deficient factorisation) bit for bit."""
+    rng = np.random.default_rng(n * 1000 + r)
+    B = rng.standard_normal((n, r))
+    A = B @ B.T
+    (rh, ah, ph), (rd, ad, pd) = _pstrf_both(A, 1e-14 * np.max(np.diag(A)))
+    assert rh == rd
+    assert np.array_equal(ph, pd)
+    assert np.array_equal(ah.view(np.uint64), ad.view(np.uint64))
+
+
+def test_device_pstrf_edge_cases():
+    for A, tol in ((np.zeros((0, 0)), 0.0), (-np.eye(3), 0.0), (np.full((2, 2), np.nan), 0.0),
+                   (np.diag([4.0, 0.0, 1.0]), -1.0)):
+        (rh, ah, ph), (rd, ad, pd) = _pstrf_both(A, tol)
+        assert rh == rd and np.array_equal(ph, pd)
+        assert np.array_equal(ah.view(np.uint64), ad.view(np.uint64))
+
+
+@pytest.mark.parametrize("case_name", ["c1_case", "d3_case"])
+def test_device_pstrf_coarse_levels(request, case_name):
+    """The hierarchies' own coarsest operators (sliver cuts: rank-deficient)."""
+    case = request.getfixturevalue(case_name)
+    A0 = case.level_A(0).to_scipy().toarray()
+    (rh, ah, ph), (rd, ad, pd) = _pstrf_both(A0, 1e-14 * np.max(np.diag(A0)))
+    assert rh == rd == case.info.coarse_rank
+    assert np.array_equal(ph, pd) and np.array_equal(ah.view(np.uint64), ad.view(np.uint64))
