@@ -234,6 +234,20 @@ void ig_blocks_free(ig_blocks *b);
  * column-major (host buffer, factored in place), piv 1-based, *rank the
  * accepted pivots; bit-identical to the host restatement igh_pstrf. */
 int ig_pstrf(int32_t n, double *a, int32_t *piv, double tol, int32_t *rank);
+/* MgHierarchy::build's algebraic half on the device (multigrid.cpp:12-75 from
+ * the fine matrix on): the Galerkin chain (ig_galerkin_hierarchy), every
+ * level's block factorisation (ig_factorize_blocks) and the coarsest pivoted
+ * Cholesky (ig_pstrf, tol 1e-14 max diag), then ig_hier_create.  Inputs: the
+ * finest A, R[l] (l >= 1, as ig_level.R), prefilter[l] (l >= 1: the
+ * pre-filter layouts of select_blocks in blk_ptr / blk_dofs, fac ignored;
+ * n_colors / color_of for multiplicative sweeps), gamma[l] (resolved damping),
+ * the smoother kind and filter ratio of every level.  The result is the same
+ * handle the host-built payload gives (bit-identical operators, factors and
+ * solves).  seconds (may be NULL): [0] wall time, [1] device time of the
+ * Galerkin / factorisation / pstrf kernels, [2] of which ig_hier_create. */
+int ig_hier_build(const ig_csr *A_fine, const ig_csr *R, const ig_blocks *prefilter, const double *gamma,
+                  int32_t smoother_kind, double filter_ratio, int32_t n_levels, ig_hier **out,
+                  double *seconds);
 
 /* Thread-local message for the last non-OK status. */
 const char *ig_last_error(void);

@@ -432,6 +432,51 @@ class MgHierarchy:
         self.info = info
 
     @staticmethod
+    def build_on_device(case) -> "MgHierarchy":
+        """MgHierarchy::build's algebraic half on the GPU (ig_hier_build): the
+        Galerkin chain, the Schwarz block factorisations and the coarsest
+        pivoted Cholesky are computed on the device from the finest operator,
+        the restrictions and the pre-filter block layouts of the host-built
+        `case` (its own coarse operators and factors are NOT used).  The
+        handle is bit-identical to MgHierarchy(case).  self.setup_seconds =
+        (wall, device kernels, ig_hier_create)."""
+        lib = _ffi.gpu()
+        lv, nl, co = case.levels_c()
+        sm = case.config.smoother if case.config is not None else SmootherConfig()
+        R = (_ffi.ig_csr * nl)()
+        pre = (_ffi.ig_blocks * nl)()
+        gam = (C.c_double * nl)()
+        keep = []
+        for l in range(nl):
+            gam[l] = lv[l].gamma
+            if l == 0:
+                continue
+            R[l] = lv[l].R
+            bp, bd = case.prefilter_blocks(l)
+            keep += [bp, bd]
+            pre[l].n_blocks = bp.shape[0] - 1
+            pre[l].blk_ptr = bp.ctypes.data_as(C.POINTER(C.c_int32))
+            pre[l].blk_dofs = bd.ctypes.data_as(C.POINTER(C.c_int32))
+            pre[l].n_colors = lv[l].blocks.n_colors
+            pre[l].color_of = lv[l].blocks.color_of
+        self = MgHierarchy.__new__(MgHierarchy)
+        self._h = C.c_void_p()
+        sec = (C.c_double * 3)()
+        _check(lib, lib.ig_hier_build(C.byref(lv[nl - 1].A), R, pre, gam, lv[nl - 1].smoother_kind if nl > 1 else 2,
+                                      float(sm.filter_ratio), nl, C.byref(self._h), sec), "ig_hier_build")
+        del keep
+        self.case = case
+        self._lv = lv
+        self._n = [lv[i].A.n_rows for i in range(nl)]
+        self.A = SpMat.from_c(lv[nl - 1].A, case)
+        self._rank = co.contents.rank
+        info = _ffi.ig_info()
+        lib.ig_hier_info(self._h, C.byref(info))
+        self.info = info
+        self.setup_seconds = (sec[0], sec[1], sec[2])
+        return self
+
+    @staticmethod
     def build(case_or_cfg, levels: Optional[int] = None, smoother: Optional[SmootherConfig] = None) -> "MgHierarchy":
         if isinstance(case_or_cfg, CaseConfig):
             cfg = dataclasses.replace(case_or_cfg)

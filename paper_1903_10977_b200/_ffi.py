@@ -125,7 +125,7 @@ GPU_SYMBOLS = (
     "ig_level_spmv", "ig_pcg", "ig_vcycle_device", "ig_level_spmv_device", "ig_pcg_device",
     "ig_pcg_result", "ig_last_error", "ig_set_option", "ig_richardson",
     "ig_smoother_apply_dir", "ig_smoother_apply_symmetric", "ig_galerkin_hierarchy", "ig_csr_free",
-    "ig_factorize_blocks", "ig_blocks_free", "ig_pstrf",
+    "ig_factorize_blocks", "ig_blocks_free", "ig_pstrf", "ig_hier_build",
 )
 
 
@@ -142,6 +142,7 @@ def gpu() -> C.CDLL:
         lib.ig_blocks_free.argtypes = [P(ig_blocks)]
         lib.ig_blocks_free.restype = None
         lib.ig_pstrf.argtypes = [i32, dp, P(i32), f64, P(i32)]
+        lib.ig_hier_build.argtypes = [P(ig_csr), P(ig_csr), P(ig_blocks), dp, i32, f64, i32, P(vp), dp]
         lib.ig_hier_destroy.argtypes = [vp]
         lib.ig_hier_destroy.restype = None
         lib.ig_hier_info.argtypes = [vp, P(ig_info)]

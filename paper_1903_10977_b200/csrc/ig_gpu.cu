@@ -2578,6 +2578,116 @@ void ig_csr_free(ig_csr* m) {
 
 }  // extern "C"
 
+namespace {
+
+// Host-owned post-filter layout produced by the device factorisation.
+struct HostBlocks {
+  std::vector<int32_t> ptr, dofs;
+  std::vector<int64_t> fptr;
+  std::vector<double> fac;
+  int64_t filtered = 0;
+};
+
+// factorize_blocks on a device-resident A (blockfac.cuh); synchronous on st.
+// dev_ms accumulates the kernels' device time.
+HostBlocks fac_blocks_dev(const GalMat& Ad, int32_t n_blocks, const int32_t* blk_ptr, const int32_t* blk_dofs,
+                          double filter_ratio, cudaStream_t st, float* dev_ms) {
+  HostBlocks hb;
+  std::vector<void*> dev;
+  struct Free {
+    std::vector<void*>& v;
+    ~Free() {
+      for (void* p : v) cudaFree(p);
+    }
+  } fr{dev};
+  auto dal = [&](size_t bytes) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
+    dev.push_back(p);
+    return p;
+  };
+  if (blk_ptr[0] != 0) throw Error(IG_INVALID_ARGUMENT, "factorize_blocks: blk_ptr[0] != 0");
+  std::vector<int64_t> soff(static_cast<size_t>(n_blocks) + 1, 0);
+  std::vector<int32_t> big;
+  for (int32_t b = 0; b < n_blocks; ++b) {
+    const int64_t sb = blk_ptr[b + 1] - blk_ptr[b];
+    if (sb < 1) throw Error(IG_INVALID_ARGUMENT, "factorize_blocks: empty block");
+    for (int32_t i = blk_ptr[b]; i < blk_ptr[b + 1]; ++i)
+      if (blk_dofs[i] < 0 || blk_dofs[i] >= Ad.nr) throw Error(IG_INVALID_ARGUMENT, "factorize_blocks: DOF out of range");
+    soff[b + 1] = soff[b] + 3 * sb * sb;
+    if (sb >= kBfWarpMin && sb <= 32) big.push_back(b);
+  }
+  const int64_t nd = n_blocks ? blk_ptr[n_blocks] : 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  struct Ev {
+    cudaEvent_t a, b;
+    ~Ev() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  } ev{e0, e1};
+  auto* dptr = static_cast<int32_t*>(dal(sizeof(int32_t) * (n_blocks + 1)));
+  auto* ddofs = static_cast<int32_t*>(dal(sizeof(int32_t) * nd));
+  auto* dsoff = static_cast<int64_t*>(dal(sizeof(int64_t) * (n_blocks + 1)));
+  auto* scratch = static_cast<double*>(dal(sizeof(double) * soff[n_blocks]));
+  auto* kdofs = static_cast<int32_t*>(dal(sizeof(int32_t) * nd));
+  auto* ksize = static_cast<int32_t*>(dal(sizeof(int32_t) * n_blocks));
+  auto* dbig = static_cast<int32_t*>(dal(sizeof(int32_t) * big.size()));
+  CK(cudaMemcpyAsync(dptr, blk_ptr, sizeof(int32_t) * (n_blocks + 1), cudaMemcpyHostToDevice, st));
+  if (nd) CK(cudaMemcpyAsync(ddofs, blk_dofs, sizeof(int32_t) * nd, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dsoff, soff.data(), sizeof(int64_t) * (n_blocks + 1), cudaMemcpyHostToDevice, st));
+  if (!big.empty()) CK(cudaMemcpyAsync(dbig, big.data(), sizeof(int32_t) * big.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaEventRecord(e0, st));
+  BlockFacArgs fa{Ad.view(), n_blocks, dptr, ddofs, dsoff, scratch, kdofs, ksize, filter_ratio, 1};
+  const unsigned g = static_cast<unsigned>((n_blocks + 127) / 128);
+  CK(cudaFuncSetAttribute(k_block_factor_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(kBfWarpSmem)));
+  if (!big.empty())
+    k_block_factor_warp<<<static_cast<unsigned>((big.size() + kBfWarps - 1) / kBfWarps), 32 * kBfWarps, kBfWarpSmem,
+                          st>>>(fa, dbig, static_cast<int32_t>(big.size()));
+  if (g) k_block_factor<<<g, 128, 0, st>>>(fa);
+  CK(cudaGetLastError());
+  std::vector<int32_t> hs(static_cast<size_t>(n_blocks));
+  if (n_blocks) CK(cudaMemcpyAsync(hs.data(), ksize, sizeof(int32_t) * n_blocks, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int64_t> optr(static_cast<size_t>(n_blocks) + 1, 0);
+  hb.fptr.assign(static_cast<size_t>(n_blocks) + 1, 0);
+  for (int32_t b = 0; b < n_blocks; ++b) {
+    if (hs[b] < 0) throw Error(IG_INVALID_ARGUMENT, "factorize_blocks: all DOFs filtered from a block");
+    optr[b + 1] = optr[b] + hs[b];
+    hb.fptr[b + 1] = hb.fptr[b] + static_cast<int64_t>(hs[b]) * hs[b];
+  }
+  if (optr[n_blocks] > INT32_MAX) throw Error(IG_UNSUPPORTED, "factorize_blocks: more than 2^31 DOF entries");
+  auto* doptr = static_cast<int64_t*>(dal(sizeof(int64_t) * (n_blocks + 1)));
+  auto* dofptr = static_cast<int64_t*>(dal(sizeof(int64_t) * (n_blocks + 1)));
+  auto* odofs = static_cast<int32_t*>(dal(sizeof(int32_t) * optr[n_blocks]));
+  auto* ofac = static_cast<double*>(dal(sizeof(double) * hb.fptr[n_blocks]));
+  CK(cudaMemcpyAsync(doptr, optr.data(), sizeof(int64_t) * (n_blocks + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dofptr, hb.fptr.data(), sizeof(int64_t) * (n_blocks + 1), cudaMemcpyHostToDevice, st));
+  if (g) k_block_compact<<<g, 128, 0, st>>>(n_blocks, dptr, kdofs, ksize, dsoff, scratch, doptr, dofptr, odofs, ofac);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(e1, st));
+  hb.ptr.resize(static_cast<size_t>(n_blocks) + 1);
+  for (int32_t b = 0; b <= n_blocks; ++b) hb.ptr[b] = static_cast<int32_t>(optr[b]);
+  hb.dofs.resize(static_cast<size_t>(optr[n_blocks]));
+  hb.fac.resize(static_cast<size_t>(hb.fptr[n_blocks]));
+  if (!hb.dofs.empty())
+    CK(cudaMemcpyAsync(hb.dofs.data(), odofs, sizeof(int32_t) * hb.dofs.size(), cudaMemcpyDeviceToHost, st));
+  if (!hb.fac.empty())
+    CK(cudaMemcpyAsync(hb.fac.data(), ofac, sizeof(double) * hb.fac.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  hb.filtered = nd - optr[n_blocks];
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  if (dev_ms) *dev_ms += ms;
+  return hb;
+}
+
+}  // namespace
+
 extern "C" {
 
 int ig_factorize_blocks(const ig_csr* A, int32_t n_blocks, const int32_t* blk_ptr, const int32_t* blk_dofs,
@@ -2586,105 +2696,33 @@ int ig_factorize_blocks(const ig_csr* A, int32_t n_blocks, const int32_t* blk_pt
     return fail(IG_INVALID_ARGUMENT, "factorize_blocks: null argument");
   *out = ig_blocks{};
   cudaStream_t st = nullptr;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
   GalMat Ad;
-  std::vector<void*> dev;
-  auto dal = [&](size_t bytes) {
-    void* p = nullptr;
-    CK(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
-    dev.push_back(p);
-    return p;
-  };
   const auto t0 = std::chrono::steady_clock::now();
   const int rc = guarded([&] {
     check_csr(*A, "factorize_blocks: A");
-    if (blk_ptr[0] != 0) throw Error(IG_INVALID_ARGUMENT, "factorize_blocks: blk_ptr[0] != 0");
-    std::vector<int64_t> soff(static_cast<size_t>(n_blocks) + 1, 0);
-    for (int32_t b = 0; b < n_blocks; ++b) {
-      const int64_t sb = blk_ptr[b + 1] - blk_ptr[b];
-      if (sb < 1) throw Error(IG_INVALID_ARGUMENT, "factorize_blocks: empty block");
-      for (int32_t i = blk_ptr[b]; i < blk_ptr[b + 1]; ++i)
-        if (blk_dofs[i] < 0 || blk_dofs[i] >= A->n_rows) throw Error(IG_INVALID_ARGUMENT, "factorize_blocks: DOF out of range");
-      soff[b + 1] = soff[b] + 3 * sb * sb;
-    }
-    const int64_t nd = n_blocks ? blk_ptr[n_blocks] : 0;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
     Ad = gal_upload(*A, st);
-    auto* dptr = static_cast<int32_t*>(dal(sizeof(int32_t) * (n_blocks + 1)));
-    auto* ddofs = static_cast<int32_t*>(dal(sizeof(int32_t) * nd));
-    auto* dsoff = static_cast<int64_t*>(dal(sizeof(int64_t) * (n_blocks + 1)));
-    auto* scratch = static_cast<double*>(dal(sizeof(double) * soff[n_blocks]));
-    auto* kdofs = static_cast<int32_t*>(dal(sizeof(int32_t) * nd));
-    auto* ksize = static_cast<int32_t*>(dal(sizeof(int32_t) * n_blocks));
-    CK(cudaMemcpyAsync(dptr, blk_ptr, sizeof(int32_t) * (n_blocks + 1), cudaMemcpyHostToDevice, st));
-    if (nd) CK(cudaMemcpyAsync(ddofs, blk_dofs, sizeof(int32_t) * nd, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dsoff, soff.data(), sizeof(int64_t) * (n_blocks + 1), cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));
-    CK(cudaEventRecord(e0, st));
-    std::vector<int32_t> big;
-    for (int32_t b = 0; b < n_blocks; ++b) {
-      const int sb = blk_ptr[b + 1] - blk_ptr[b];
-      if (sb >= kBfWarpMin && sb <= 32) big.push_back(b);
-    }
-    auto* dbig = static_cast<int32_t*>(dal(sizeof(int32_t) * big.size()));
-    if (!big.empty())
-      CK(cudaMemcpyAsync(dbig, big.data(), sizeof(int32_t) * big.size(), cudaMemcpyHostToDevice, st));
-    BlockFacArgs fa{Ad.view(), n_blocks, dptr, ddofs, dsoff, scratch, kdofs, ksize, filter_ratio, 1};
-    const unsigned g = static_cast<unsigned>((n_blocks + 127) / 128);
-    CK(cudaFuncSetAttribute(k_block_factor_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(kBfWarpSmem)));
-    if (!big.empty())
-      k_block_factor_warp<<<static_cast<unsigned>((big.size() + kBfWarps - 1) / kBfWarps), 32 * kBfWarps, kBfWarpSmem,
-                            st>>>(fa, dbig, static_cast<int32_t>(big.size()));
-    if (g) k_block_factor<<<g, 128, 0, st>>>(fa);
-    CK(cudaGetLastError());
-    std::vector<int32_t> hs(static_cast<size_t>(n_blocks));
-    if (n_blocks) CK(cudaMemcpyAsync(hs.data(), ksize, sizeof(int32_t) * n_blocks, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    std::vector<int64_t> optr(static_cast<size_t>(n_blocks) + 1, 0), ofptr(static_cast<size_t>(n_blocks) + 1, 0);
-    for (int32_t b = 0; b < n_blocks; ++b) {
-      if (hs[b] < 0) throw Error(IG_INVALID_ARGUMENT, "factorize_blocks: all DOFs filtered from a block");
-      optr[b + 1] = optr[b] + hs[b];
-      ofptr[b + 1] = ofptr[b] + static_cast<int64_t>(hs[b]) * hs[b];
-    }
-    auto* doptr = static_cast<int64_t*>(dal(sizeof(int64_t) * (n_blocks + 1)));
-    auto* dofptr = static_cast<int64_t*>(dal(sizeof(int64_t) * (n_blocks + 1)));
-    auto* odofs = static_cast<int32_t*>(dal(sizeof(int32_t) * optr[n_blocks]));
-    auto* ofac = static_cast<double*>(dal(sizeof(double) * ofptr[n_blocks]));
-    CK(cudaMemcpyAsync(doptr, optr.data(), sizeof(int64_t) * (n_blocks + 1), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dofptr, ofptr.data(), sizeof(int64_t) * (n_blocks + 1), cudaMemcpyHostToDevice, st));
-    if (g) k_block_compact<<<g, 128, 0, st>>>(n_blocks, dptr, kdofs, ksize, dsoff, scratch, doptr, dofptr, odofs, ofac);
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(e1, st));
-    auto* hp = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * (n_blocks + 1)));
-    auto* hd = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * std::max<int64_t>(optr[n_blocks], 1)));
-    auto* hfp = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (n_blocks + 1)));
-    auto* hf = static_cast<double*>(std::malloc(sizeof(double) * std::max<int64_t>(ofptr[n_blocks], 1)));
+    float ms = 0.f;
+    HostBlocks hb = fac_blocks_dev(Ad, n_blocks, blk_ptr, blk_dofs, filter_ratio, st, &ms);
+    auto* hp = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * hb.ptr.size()));
+    auto* hd = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * std::max<size_t>(hb.dofs.size(), 1)));
+    auto* hfp = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * hb.fptr.size()));
+    auto* hf = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(hb.fac.size(), 1)));
     out->n_blocks = n_blocks;
     out->blk_ptr = hp;
     out->blk_dofs = hd;
     out->fac_ptr = hfp;
     out->fac = hf;
     if (!hp || !hd || !hfp || !hf) throw Error(IG_CUDA_ERROR, "factorize_blocks: host allocation failed");
-    for (int32_t b = 0; b <= n_blocks; ++b) {
-      hp[b] = static_cast<int32_t>(optr[b]);
-      hfp[b] = ofptr[b];
-    }
-    if (optr[n_blocks]) CK(cudaMemcpyAsync(hd, odofs, sizeof(int32_t) * optr[n_blocks], cudaMemcpyDeviceToHost, st));
-    if (ofptr[n_blocks]) CK(cudaMemcpyAsync(hf, ofac, sizeof(double) * ofptr[n_blocks], cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (filtered_dofs) *filtered_dofs = nd - optr[n_blocks];
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
+    std::memcpy(hp, hb.ptr.data(), sizeof(int32_t) * hb.ptr.size());
+    std::memcpy(hd, hb.dofs.data(), sizeof(int32_t) * hb.dofs.size());
+    std::memcpy(hfp, hb.fptr.data(), sizeof(int64_t) * hb.fptr.size());
+    std::memcpy(hf, hb.fac.data(), sizeof(double) * hb.fac.size());
+    if (filtered_dofs) *filtered_dofs = hb.filtered;
     if (seconds) seconds[1] = 1e-3 * ms;
     return IG_OK;
   });
   Ad.free_all();
-  for (void* p : dev) cudaFree(p);
-  if (e0) cudaEventDestroy(e0);
-  if (e1) cudaEventDestroy(e1);
   if (st) cudaStreamDestroy(st);
   if (seconds) seconds[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (rc != IG_OK) ig_blocks_free(out);
@@ -2730,6 +2768,163 @@ int ig_pstrf(int32_t n, double* a, int32_t* piv, double tol, int32_t* rank) {
   cudaFree(dw);
   cudaFree(dp);
   cudaFree(dr);
+  return rc;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int ig_hier_build(const ig_csr* A_fine, const ig_csr* R, const ig_blocks* prefilter, const double* gamma,
+                  int32_t smoother_kind, double filter_ratio, int32_t n_levels, ig_hier** out, double* seconds) {
+  if (!A_fine || !R || !prefilter || !gamma || !out || n_levels < 1)
+    return fail(IG_INVALID_ARGUMENT, "hier_build: null argument");
+  *out = nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  std::vector<GalMat> Ad(static_cast<size_t>(n_levels));
+  GalMat Rd, Rt, Cm;
+  double t_create = 0.0;
+  float dev_ms = 0.f;
+  const int rc = guarded([&] {
+    check_csr(*A_fine, "hier_build: A");
+    for (int32_t l = 1; l < n_levels; ++l) check_csr(R[l], "hier_build: R");
+    CK(cudaFuncSetAttribute(k_gal_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGalFillSmem)));
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    // 1. Galerkin chain (multigrid.cpp:37-41), every level kept on the device.
+    Ad[n_levels - 1] = gal_upload(*A_fine, st);
+    for (int32_t l = n_levels - 1; l >= 1; --l) {
+      if (R[l].n_cols != Ad[l].nr || R[l].n_rows <= 0)
+        throw Error(IG_INVALID_ARGUMENT, "hier_build: R[" + std::to_string(l) + "] does not match level " +
+                                             std::to_string(l));
+      Rd = gal_upload(R[l], st);
+      CK(cudaStreamSynchronize(st));
+      CK(cudaEventRecord(e0, st));
+      Rt = gal_transpose(Rd, st);
+      Cm = gal_spgemm(Ad[l], Rt, st);
+      Rt.free_all();
+      Ad[l - 1] = gal_spgemm(Rd, Cm, st);
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      dev_ms += ms;
+      Cm.free_all();
+      Rd.free_all();
+    }
+    // 2. Schwarz blocks of levels >= 1 (make_smoother: factorize_blocks).
+    std::vector<HostBlocks> hb(static_cast<size_t>(n_levels));
+    for (int32_t l = 1; l < n_levels; ++l) {
+      const ig_blocks& pb = prefilter[l];
+      if (pb.n_blocks < 0 || (pb.n_blocks > 0 && (!pb.blk_ptr || !pb.blk_dofs)))
+        throw Error(IG_INVALID_ARGUMENT, "hier_build: bad pre-filter layout");
+      hb[l] = fac_blocks_dev(Ad[l], pb.n_blocks, pb.blk_ptr, pb.blk_dofs, filter_ratio, st, &dev_ms);
+    }
+    // 3. Coarse operators back to the host (the layouts are built there).
+    std::vector<std::vector<int32_t>> hp(static_cast<size_t>(n_levels)), hc(static_cast<size_t>(n_levels));
+    std::vector<std::vector<double>> hv(static_cast<size_t>(n_levels));
+    for (int32_t l = 0; l + 1 < n_levels; ++l) {
+      const GalMat& m = Ad[l];
+      hp[l].resize(static_cast<size_t>(m.nr) + 1);
+      hc[l].resize(static_cast<size_t>(m.nnz));
+      hv[l].resize(static_cast<size_t>(m.nnz));
+      CK(cudaMemcpyAsync(hp[l].data(), m.ptr, sizeof(int32_t) * (m.nr + 1), cudaMemcpyDeviceToHost, st));
+      if (m.nnz) {
+        CK(cudaMemcpyAsync(hc[l].data(), m.col, sizeof(int32_t) * m.nnz, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hv[l].data(), m.val, sizeof(double) * m.nnz, cudaMemcpyDeviceToHost, st));
+      }
+    }
+    CK(cudaStreamSynchronize(st));
+    for (auto& m : Ad) m.free_all();
+    // 4. Coarsest pivoted Cholesky on the device (multigrid.cpp:57-73).
+    const int32_t n0 = n_levels > 1 ? static_cast<int32_t>(hp[0].size()) - 1 : A_fine->n_rows;
+    const int32_t* p0 = n_levels > 1 ? hp[0].data() : A_fine->row_ptr;
+    const int32_t* c0 = n_levels > 1 ? hc[0].data() : A_fine->col_idx;
+    const double* v0 = n_levels > 1 ? hv[0].data() : A_fine->val;
+    std::vector<double> L(static_cast<size_t>(n0) * n0, 0.0);
+    for (int32_t i = 0; i < n0; ++i)
+      for (int32_t k = p0[i]; k < p0[i + 1]; ++k) L[static_cast<size_t>(c0[k]) * n0 + i] = v0[k];
+    double max_diag = 0.0;
+    for (int32_t i = 0; i < n0; ++i) max_diag = std::max(max_diag, L[static_cast<size_t>(i) * n0 + i]);
+    std::vector<int32_t> piv(static_cast<size_t>(std::max(n0, 1)), 0);
+    int32_t rank = 0;
+    {
+      double *da = nullptr, *dw = nullptr;
+      int32_t *dp = nullptr, *dr = nullptr;
+      struct F {
+        double*& a;
+        double*& w;
+        int32_t*& p;
+        int32_t*& r;
+        ~F() {
+          cudaFree(a);
+          cudaFree(w);
+          cudaFree(p);
+          cudaFree(r);
+        }
+      } fr{da, dw, dp, dr};
+      CK(cudaMalloc(&da, std::max<size_t>(L.size(), 1) * sizeof(double)));
+      CK(cudaMalloc(&dw, std::max<size_t>(2 * static_cast<size_t>(n0), 1) * sizeof(double)));
+      CK(cudaMalloc(&dp, piv.size() * sizeof(int32_t)));
+      CK(cudaMalloc(&dr, sizeof(int32_t)));
+      if (!L.empty()) CK(cudaMemcpyAsync(da, L.data(), L.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+      CK(cudaEventRecord(e0, st));
+      k_pstrf<<<1, std::max(32, std::min(1024, ((n0 + 31) / 32) * 32)), 0, st>>>(n0, da, dp, 1e-14 * max_diag, dw, dr);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(e1, st));
+      if (!L.empty()) CK(cudaMemcpyAsync(L.data(), da, L.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+      if (n0) CK(cudaMemcpyAsync(piv.data(), dp, n0 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&rank, dr, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      dev_ms += ms;
+    }
+    // 5. The device hierarchy (layouts, upload): ig_hier_create.
+    std::vector<ig_level> lv(static_cast<size_t>(n_levels));
+    for (int32_t l = 0; l < n_levels; ++l) {
+      ig_level& v = lv[l];
+      if (l + 1 < n_levels) {
+        v.A = ig_csr{static_cast<int32_t>(hp[l].size()) - 1, static_cast<int32_t>(hp[l].size()) - 1,
+                     static_cast<int64_t>(hc[l].size()), hp[l].data(), hc[l].data(), hv[l].data()};
+      } else {
+        v.A = *A_fine;
+      }
+      v.R = l >= 1 ? R[l] : ig_csr{};
+      v.smoother_kind = smoother_kind;
+      v.gamma = gamma[l];
+      if (l >= 1) {
+        const HostBlocks& b = hb[l];
+        v.blocks.n_blocks = prefilter[l].n_blocks;
+        v.blocks.blk_ptr = b.ptr.data();
+        v.blocks.blk_dofs = b.dofs.data();
+        v.blocks.fac_ptr = b.fptr.data();
+        v.blocks.fac = b.fac.data();
+        v.blocks.n_colors = prefilter[l].n_colors;
+        v.blocks.color_of = prefilter[l].color_of;
+      }
+    }
+    ig_coarse co{n0, rank, L.data(), piv.data()};
+    const auto tc = std::chrono::steady_clock::now();
+    const int c = ig_hier_create(lv.data(), n_levels, &co, out);
+    t_create = std::chrono::duration<double>(std::chrono::steady_clock::now() - tc).count();
+    return c;
+  });
+  for (auto& m : Ad) m.free_all();
+  Rd.free_all();
+  Rt.free_all();
+  Cm.free_all();
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (st) cudaStreamDestroy(st);
+  if (seconds) {
+    seconds[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    seconds[1] = 1e-3 * dev_ms;
+    seconds[2] = t_create;
+  }
   return rc;
 }
 

@@ -111,3 +111,55 @@ def test_device_pstrf_coarse_levels(request, case_name):
     (rh, ah, ph), (rd, ad, pd) = _pstrf_both(A0, 1e-14 * np.max(np.diag(A0)))
     assert rh == rd == case.info.coarse_rank
     assert np.array_equal(ph, pd) and np.array_equal(ah.view(np.uint64), ad.view(np.uint64))
+
+
+def _same_solve(case):
+    import oracle_ffi as orc
+    from paper_1903_10977_b200 import MgHierarchy, pcg
+    hd = MgHierarchy.build_on_device(case)
+    try:
+        x, rep = pcg(hd.A, case.b, hd, tol=1e-8, maxit=1000)
+        st, xo, ro, it, _ = orc.pcg(case.levels_c(), case.b, tol=1e-8, maxit=1000, mode=orc.GPU_ORDER)
+        assert st == 0 and rep.iterations == it
+        assert np.array_equal(np.array(rep.residuals), ro) and np.array_equal(x, xo)
+        for l in range(hd.levels()):
+            from conftest import rng_vec
+            r = rng_vec(3 + l, hd._n[l])
+            assert np.array_equal(hd.vcycle_at(l, r), orc.vcycle_at(case.levels_c(), l, r))
+        return hd.setup_seconds
+    finally:
+        hd.close()
+
+
+@pytest.mark.parametrize("case_name", ["c1_case", "d3_case", "star_case"])
+def test_device_hierarchy_build_solves_identically(request, case_name):
+    """ig_hier_build (Galerkin + block factorisation + pstrf on the device,
+    then the layouts) gives the host-built hierarchy's V-cycles and PCG solve
+    bit for bit (the oracle runs on the host-built payload)."""
+    _same_solve(request.getfixturevalue(case_name))
+
+
+def test_device_hierarchy_build_multiplicative():
+    from paper_1903_10977_b200 import CaseConfig, SmootherConfig, build_case, configs
+    cfg = configs.c1()
+    case = build_case(CaseConfig(**{**cfg.__dict__, "smoother": SmootherConfig("multiplicative-schwarz")}))
+    _same_solve(case)
+
+
+def test_device_hierarchy_build_c4_full_size():
+    """Full-size C4: the device-built handle solves exactly like the handle
+    built from the host payload (both on the GPU; the C4 oracle solve is
+    covered by test_gpu_parity)."""
+    from paper_1903_10977_b200 import MgHierarchy, build_case, configs, pcg
+    case = build_case(configs.c4())
+    hd = MgHierarchy.build_on_device(case)
+    wall, dev, create = hd.setup_seconds
+    xd, rd = pcg(hd.A, case.b, hd, tol=1e-8, maxit=1000)
+    hd.close()
+    hh = MgHierarchy(case)
+    xh, rh = pcg(hh.A, case.b, hh, tol=1e-8, maxit=1000)
+    hh.close()
+    assert rd.iterations == rh.iterations == 115
+    assert np.array_equal(np.array(rd.residuals), np.array(rh.residuals)) and np.array_equal(xd, xh)
+    print(f"C4 device hierarchy build: wall {wall:.2f} s (device kernels {dev * 1e3:.0f} ms, "
+          f"ig_hier_create {create:.2f} s); host mg setup {case.info.seconds_mg_setup:.2f} s")
