@@ -174,6 +174,7 @@ def main():
                     help="as: additive Schwarz (the BASELINE configs); ms: multiplicative colored Schwarz")
     ap.add_argument("--cpu-sample-iters", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-device-setup", action="store_true", help="skip the ig_hier_build setup measurement")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch kernels directly instead of the CUDA graph (ncu cannot profile "
                          "kernel nodes of graphs with conditional nodes)")
@@ -310,6 +311,24 @@ def main():
         e2e_ms = float(t.item())
     assert np.array_equal(hx.numpy(), dx.cpu().numpy()), "host-buffer and device solves differ"
 
+    # --- device-side hierarchy setup: ig_hier_build --
+    dsetup = None
+    if not args.no_device_setup:
+        hd = MgHierarchy.build_on_device(case)
+        wall, kern, create = hd.setup_seconds
+        xd = torch.empty_like(db)
+        rc = lib.ig_pcg_device(hd.handle, vp(db.data_ptr()), 1e-8, 1000, vp(xd.data_ptr()))
+        assert rc == 0 and lib.ig_pcg_result(hd.handle, None, None) == 0
+        same = bool(torch.equal(xd, dx))
+        hd.close()
+        assert same, "device-built hierarchy solves differently from the host-built one"
+        dsetup = {"wall_s": wall, "device_kernels_s": kern, "hier_create_s": create,
+                  "host_mg_setup_s": case.info.seconds_mg_setup,
+                  "what": ("Galerkin chain + Schwarz block eigen-filter/LLT + coarsest pstrf on the device "
+                           "(ig_hier_build), vs the host's multithreaded Galerkin/factorisation/pstrf "
+                           "(host_mg_setup_s); hier_create_s = layout construction + upload in both paths"),
+                  "solve_bit_identical": same}
+
     kv = info.kernels_vcycle
     launches_per_solve = (kv + 2) + iters * info.kernels_pcg_iter  # init + V-cycle + p; per iteration
 
@@ -359,7 +378,7 @@ def main():
                     "d2h_bytes_per_step": 8 * n + 8 * (iters + 1), "ms_per_step": e2e_ms},
             "gpu_launches": launches_per_solve * args.steps,
             "clocks": clk.summary(),
-            "setup_seconds": {"host_setup": t_setup, "upload": t_upload},
+            "setup_seconds": {"host_setup": t_setup, "upload": t_upload, "device_setup": dsetup},
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -183,3 +183,24 @@ def test_3d_hierarchy_shapes(d3_case):
         R = d3_case.level_R(l)
         assert R.shape == (d3_case.level_dofs()[l - 1], d3_case.level_dofs()[l])
     assert 0 < d3_case.info.eta < 1
+
+
+def test_prefilter_layout_matches_post_filter(c1_case):
+    """igh_prefilter_blocks (the input of the device factorisation): same block
+    count as the post-filter layout, every kept DOF list a subsequence of its
+    pre-filter list, and the difference is exactly the filtered-DOF count."""
+    for l in range(1, c1_case.n_levels):
+        bp, bd = c1_case.prefilter_blocks(l)
+        hp, hd, _, _ = c1_case.blocks(l)
+        assert bp.shape == hp.shape and bp[0] == 0
+        removed = 0
+        for b in range(bp.shape[0] - 1):
+            pre = list(bd[bp[b]:bp[b + 1]])
+            post = list(hd[hp[b]:hp[b + 1]])
+            it = iter(pre)
+            assert all(d in it for d in post)  # ordered subsequence
+            assert pre == sorted(pre)
+            removed += len(pre) - len(post)
+        assert removed == c1_case.info.filtered_dofs[l]
+    with pytest.raises(ValueError):
+        c1_case.prefilter_blocks(0)
