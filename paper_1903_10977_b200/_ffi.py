@@ -82,6 +82,8 @@ IG_OPT_AS_SPLIT = 12
 IG_OPT_RED_CTAS = 13
 IG_OPT_PSELL_CTAS = 15
 IG_OPT_FUSED_AS_ROWS = 16
+IG_OPT_L2_ROWS = 18
+IG_OPT_L2_MB = 19
 
 _host = None
 _gpu = None

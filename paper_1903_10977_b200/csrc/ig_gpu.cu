@@ -258,6 +258,13 @@ int g_psell_ctas = 0;
 // overlap under PDL and the graph fork, and the fused kernel's phase-1 fence
 // + arrival + wait sits on the critical path of every application.
 int32_t g_fused_rows = 0;
+// Levels below the finest with at most this many DOFs live in the L2-persisting
+// arena (ig_hier::alloc); 0 = off.  Arena size g_l2_bytes.
+// Measured (profiles/option_sweep.py 18/19): C4 V-cycle 903 -> 881 us, C3
+// 424 -> 395 us; an arena above the device's persisting maximum (83 MB on
+// B200) thrashes and gains nothing.
+int32_t g_l2_rows = 300000;
+size_t g_l2_bytes = size_t(64) << 20;
 size_t psell_smem() {
   if (g_psell_ctas <= 0) return 0;
   return static_cast<size_t>(std::max(0, 233472 / g_psell_ctas - 1024 - 1024)) & ~size_t(1023);
@@ -749,12 +756,27 @@ struct ig_hier {
   std::mutex mu;
   int last_status = IG_OK;
 
+  // L2-resident arena for the small levels (IG_OPT_L2_ROWS): their arrays
+  // are sub-allocated from one block so a single persisting access-policy
+  // window on the streams covers them (the finest level's streaming would
+  // otherwise evict them between V-cycles).
+  char* arena = nullptr;
+  size_t arena_cap = 0, arena_used = 0;
+  bool arena_on = false;
   template <typename T>
   T* alloc(size_t count) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    info.device_bytes += static_cast<int64_t>(bytes);
+    if (arena_on && arena) {
+      const size_t off = (arena_used + 255) & ~size_t(255);
+      if (off + bytes <= arena_cap) {
+        arena_used = off + bytes;
+        return reinterpret_cast<T*>(arena + off);
+      }
+    }
     void* p = nullptr;
-    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    CK(cudaMalloc(&p, bytes));
     allocs.push_back(p);
-    info.device_bytes += static_cast<int64_t>(std::max<size_t>(count, 1) * sizeof(T));
     return static_cast<T*>(p);
   }
   template <typename T>
@@ -1769,6 +1791,16 @@ int ig_set_option(int32_t option, int64_t value) {
     g_red_ctas = static_cast<int>(value);
     return IG_OK;
   }
+  if (option == IG_OPT_L2_MB) {
+    if (value < 1 || value > 4096) return fail(IG_INVALID_ARGUMENT, "ig_set_option: L2 arena MB in 1..4096");
+    g_l2_bytes = static_cast<size_t>(value) << 20;
+    return IG_OK;
+  }
+  if (option == IG_OPT_L2_ROWS) {
+    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: L2 rows out of range");
+    g_l2_rows = static_cast<int32_t>(value);
+    return IG_OK;
+  }
   if (option == IG_OPT_FUSED_AS_ROWS) {
     if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: fused smoother rows out of range");
     g_fused_rows = static_cast<int32_t>(value);
@@ -1850,9 +1882,17 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     CK(cudaEventCreate(&h->ev1));
     ig_info& I = h->info;
     I.n_levels = n_levels;
+    if (g_l2_rows > 0 && n_levels > 1) {
+      void* p = nullptr;
+      CK(cudaMalloc(&p, g_l2_bytes));
+      h->allocs.push_back(p);
+      h->arena = static_cast<char*>(p);
+      h->arena_cap = g_l2_bytes;
+    }
     for (int l = 0; l < n_levels; ++l) {
       const ig_level& s = levels[l];
       Level& L = h->lv[l];
+      h->arena_on = l < n_levels - 1 && s.A.n_rows <= g_l2_rows;
       check_csr(s.A, "A");
       if (s.A.n_rows != s.A.n_cols) throw Error(IG_INVALID_ARGUMENT, "A must be square");
       L.n = s.A.n_rows;
@@ -1921,8 +1961,30 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     std::vector<double> packed(static_cast<size_t>(std::max<int64_t>(np_al, 2)), 0.0);
     for (int64_t j = 0; j < rk; ++j)
       for (int64_t i = j; i < rk; ++i) packed[j * rk - (j * (j - 1)) / 2 + (i - j)] = coarse->L[j * n0 + i];
+    h->arena_on = h->arena != nullptr;
     h->Lp = h->upload(packed.data(), packed.size());
     h->piv = h->upload(coarse->piv, static_cast<size_t>(n0));
+    h->arena_on = false;
+    if (h->arena && h->arena_used > 0) {
+      size_t lim = 0;
+      int maxp = 0;
+      CK(cudaDeviceGetLimit(&lim, cudaLimitPersistingL2CacheSize));
+      CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, 0));
+      const size_t want = std::min<size_t>(h->arena_used, static_cast<size_t>(maxp));
+      if (lim < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+      cudaGetLastError();
+      if (std::getenv("IG_TIMING"))
+        std::fprintf(stderr, "[ig_hier_create] L2 arena: %zu bytes used, persisting max %d\n", h->arena_used, maxp);
+      cudaStreamAttrValue av = {};
+      av.accessPolicyWindow.base_ptr = h->arena;
+      av.accessPolicyWindow.num_bytes = h->arena_used;
+      av.accessPolicyWindow.hitRatio =
+          std::min(1.0f, static_cast<float>(static_cast<double>(std::max(maxp, 1)) / static_cast<double>(h->arena_used)));
+      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      CK(cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &av));
+      CK(cudaStreamSetAttribute(h->side, cudaStreamAttributeAccessPolicyWindow, &av));
+    }
     h->coarse_threads = static_cast<int>(std::max<int64_t>(32, (rk + 31) / 32 * 32));  // one row per thread
     // [packed L11][forward results: rank][backward results: rank]
     const size_t smem = sizeof(double) * static_cast<size_t>(np_al + 2 * rk + 2);

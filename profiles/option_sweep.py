@@ -1,7 +1,7 @@
 """Sweep one ig_set_option over values on several workloads: V-cycle and full
 PCG device time (CUDA events on the library stream).
 
-  python profiles/option_sweep.py OPTION v1,v2,... [workloads]
+  [IG_PRESET=opt=val,...] python profiles/option_sweep.py OPTION v1,v2,... [workloads]
   e.g.  python profiles/option_sweep.py 4 0,50000,300000 c4,c3,c2
 """
 import ctypes as C
@@ -17,6 +17,9 @@ def main():
 
     from paper_1903_10977_b200 import MgHierarchy, _ffi, build_case, configs
     lib = _ffi.gpu()
+    for kv in filter(None, os.environ.get("IG_PRESET", "").split(",")):  # e.g. IG_PRESET=19=96,18=300000
+        k, v = kv.split("=")
+        assert lib.ig_set_option(int(k), int(v)) == 0
     opt = int(sys.argv[1])
     vals = [int(v) for v in sys.argv[2].split(",")]
     wls = sys.argv[3].split(",") if len(sys.argv) > 3 else ["c4"]
