@@ -199,6 +199,18 @@ int ig_debug_vcycle_timeline(ig_hier *h, const double *d_r, double *d_x,
 int ig_debug_tail_profile(ig_hier *h, const double *d_r, double *d_x, uint64_t *stamps,
                           int32_t cap, int32_t *count);
 
+/* --- composed spectral operators ---------------- */
+/* Columns j0 .. j0+count-1 of a composed operator on the finest level, the
+ * LinOps proj/src/runner.cpp:84-122 hands to dense_spectrum
+ * (proj/src/spectral.cpp:28-50 materialises them column by column from unit
+ * vectors): IG_OP_A = A e_j; IG_OP_VCYCLE = MgHierarchy::apply(A e_j)
+ * ("vcycle"); IG_OP_SMOOTHER_SYMMETRIC = Smoother::apply_symmetric(A e_j) of
+ * the finest smoother ("as2" / "ms2").  out: n x count, column-major, host. */
+#define IG_OP_A 0
+#define IG_OP_VCYCLE 1
+#define IG_OP_SMOOTHER_SYMMETRIC 2
+int ig_operator_columns(ig_hier *h, int32_t kind, int32_t j0, int32_t count, double *out);
+
 /* --- device-side hierarchy setup ---------------- */
 /* Galerkin coarse operators on the device: starting from A_fine (the finest
  * level's A), A_{l-1} = R_l (A_l R_l^T) for l = n_levels-1 .. 1, exactly the

@@ -293,6 +293,73 @@ def factorize_blocks(A: "SpMat", blk_ptr, blk_dofs, filter_ratio: float = 1e-16)
     return optr, odofs, ofp, ofac, int(filt.value), (sec[0], sec[1])
 
 
+class TooLarge(RuntimeError):
+    """spectral.hpp:16 TooLarge."""
+
+
+@dataclasses.dataclass
+class SpectrumResult:
+    """spectral.hpp:24-31."""
+    eigenvalues: np.ndarray
+    vectors: Optional[np.ndarray]
+    lambda_min: float
+    lambda_max: float
+    kappa: float
+
+
+def dense_spectrum(h: "MgHierarchy", name: str = "vcycle", want_vectors: bool = False,
+                   dense_limit: int = 6000) -> SpectrumResult:
+    """dense_spectrum of a composed operator (runner.cpp:84-122 + spectral.cpp:28-91):
+    the operator is materialised column by column ON THE DEVICE
+    (ig_operator_columns: A e_j, then the V-cycle / symmetric smoother), the
+    dense nonsymmetric eigenproblem runs on the host (the reference calls
+    LAPACK dgeev there too).  name: "vcycle" (M A), "as2" / "ms2" (the finest
+    smoother's apply_symmetric(A v); must match the hierarchy's smoother kind),
+    "jacobi" (D^-1 A)."""
+    n = h.A.rows()
+    if n < 1:
+        raise ValueError("dense_spectrum: n must be positive")
+    if n > dense_limit:
+        raise TooLarge(f"dense_spectrum: n = {n} exceeds dense limit {dense_limit}")
+    lib = _ffi.gpu()
+    if name == "vcycle":
+        kind = _ffi.IG_OP_VCYCLE
+    elif name in ("as2", "ms2"):
+        want = 2 if name == "as2" else 3
+        if h.levels() < 2 or h._lv[h.levels() - 1].smoother_kind != want:
+            raise ValueError(f"dense_spectrum: {name} needs a hierarchy built with that smoother")
+        kind = _ffi.IG_OP_SMOOTHER_SYMMETRIC
+    elif name in ("jacobi", "A"):
+        kind = _ffi.IG_OP_A
+    else:
+        raise ValueError(f'spectrum: unknown operator "{name}" (one of: jacobi, as2, ms2, vcycle)')
+    m = np.empty((n, n), order="F")
+    _check(lib, lib.ig_operator_columns(h.handle, kind, 0, n, m.ctypes.data_as(C.POINTER(C.c_double))),
+           "ig_operator_columns")
+    if name == "jacobi":
+        d = h.A.to_scipy().diagonal()
+        if np.any(d <= 0.0):
+            raise RuntimeError("spectrum: operator diagonal is not positive")
+        m = m / d[:, None]
+    if want_vectors:
+        wr_c, vr = np.linalg.eig(m)
+    else:
+        wr_c, vr = np.linalg.eigvals(m), None
+    wr, wi = wr_c.real, wr_c.imag
+    scale = np.max(np.abs(wr))
+    if np.max(np.abs(wi)) > 1e-8 * max(scale, 1e-300):
+        raise RuntimeError("dense_spectrum: eigenvalues have imaginary parts beyond tolerance "
+                           "(operator not similar to a symmetric one)")
+    order = np.argsort(wr, kind="stable")
+    ev = wr[order]
+    vecs = vr[:, order].real if want_vectors else None
+    lmax = float(ev[-1])
+    cutoff = 1e-12 * abs(lmax)
+    nz = ev[ev > cutoff]
+    smallest = float(nz[0]) if nz.size else lmax
+    return SpectrumResult(ev, vecs, float(ev[0]), lmax, lmax / smallest)
+
+
 class Case:
     """Host-built case: fine system (A, b) and the multigrid hierarchy payload
     that crosses the C-ABI (owned by libig_host.so until close())."""

@@ -67,6 +67,9 @@ class igh_info(C.Structure):
 
 IG_OK, IG_NOT_CONVERGED, IG_BREAKDOWN, IG_INVALID_ARGUMENT, IG_CUDA_ERROR, IG_UNSUPPORTED, IG_DIVERGED = range(7)
 IG_SMOOTHER_JACOBI, IG_SMOOTHER_GAUSS_SEIDEL, IG_SMOOTHER_ADDITIVE_SCHWARZ, IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ = range(4)
+IG_OP_A = 0
+IG_OP_VCYCLE = 1
+IG_OP_SMOOTHER_SYMMETRIC = 2
 IG_OPT_USE_GRAPH = 1
 IG_OPT_ROW_DICT = 2
 IG_OPT_SPMV_VARIANT = 3
@@ -128,6 +131,7 @@ GPU_SYMBOLS = (
     "ig_pcg_result", "ig_last_error", "ig_set_option", "ig_richardson",
     "ig_smoother_apply_dir", "ig_smoother_apply_symmetric", "ig_galerkin_hierarchy", "ig_csr_free",
     "ig_factorize_blocks", "ig_blocks_free", "ig_pstrf", "ig_hier_build",
+    "ig_operator_columns",
 )
 
 
@@ -144,6 +148,7 @@ def gpu() -> C.CDLL:
         lib.ig_blocks_free.argtypes = [P(ig_blocks)]
         lib.ig_blocks_free.restype = None
         lib.ig_pstrf.argtypes = [i32, dp, P(i32), f64, P(i32)]
+        lib.ig_operator_columns.argtypes = [vp, i32, i32, i32, dp]
         lib.ig_hier_build.argtypes = [P(ig_csr), P(ig_csr), P(ig_blocks), dp, i32, f64, i32, P(vp), dp]
         lib.ig_hier_destroy.argtypes = [vp]
         lib.ig_hier_destroy.restype = None

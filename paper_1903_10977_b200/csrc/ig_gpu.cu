@@ -2991,3 +2991,63 @@ int ig_hier_build(const ig_csr* A_fine, const ig_csr* R, const ig_blocks* prefil
 }
 
 }  // extern "C"
+
+namespace {
+__global__ void k_set_unit(double* e, int32_t prev, int32_t j) {
+  if (threadIdx.x == 0) {
+    if (prev >= 0) e[prev] = 0.0;
+    e[j] = 1.0;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int ig_operator_columns(ig_hier* h, int32_t kind, int32_t j0, int32_t count, double* out) {
+  if (!h || !out) return fail(IG_INVALID_ARGUMENT, "operator_columns: null argument");
+  if (kind < IG_OP_A || kind > IG_OP_SMOOTHER_SYMMETRIC) return fail(IG_INVALID_ARGUMENT, "operator_columns: bad kind");
+  std::lock_guard<std::mutex> lk(h->mu);
+  const int32_t top = h->L - 1;
+  const int32_t n = h->lv[top].n;
+  if (j0 < 0 || count < 0 || j0 + static_cast<int64_t>(count) > n)
+    return fail(IG_INVALID_ARGUMENT, "operator_columns: column range outside the operator");
+  if (kind == IG_OP_SMOOTHER_SYMMETRIC && top < 1)
+    return fail(IG_INVALID_ARGUMENT, "operator_columns: a 1-level hierarchy has no smoother");
+  double *e = nullptr, *u = nullptr, *cols = nullptr;
+  const int rc = guarded([&] {
+    if (count == 0) return IG_OK;
+    CK(cudaMalloc(&e, sizeof(double) * n));
+    CK(cudaMalloc(&u, sizeof(double) * n));
+    CK(cudaMalloc(&cols, sizeof(double) * static_cast<size_t>(n) * count));
+    CK(cudaMemsetAsync(e, 0, sizeof(double) * n, h->stream));
+    Level& F = h->lv[top];
+    for (int32_t c = 0; c < count; ++c) {
+      const int32_t j = j0 + c;
+      k_set_unit<<<1, 32, 0, h->stream>>>(e, c == 0 ? -1 : j - 1, j);
+      CK(cudaGetLastError());
+      double* col = cols + static_cast<size_t>(c) * n;
+      if (kind == IG_OP_A) {
+        h->spmv(F.A, 0, e, col, col);
+        continue;
+      }
+      h->spmv(F.A, 0, e, u, u);  // A e_j
+      if (kind == IG_OP_VCYCLE) {
+        h->vcycle(top, u, col, nullptr, nullptr);  // MgHierarchy::apply(A e_j)
+      } else {                                      // Smoother::apply_symmetric(A e_j)
+        h->smoother(F, u, col, false, nullptr, nullptr, 0);
+        h->spmv(F.A, 1, col, F.cor, u, nullptr);
+        h->smoother(F, F.cor, col, true, nullptr, nullptr, 1);
+      }
+    }
+    CK(cudaMemcpyAsync(out, cols, sizeof(double) * static_cast<size_t>(n) * count, cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return IG_OK;
+  });
+  cudaFree(e);
+  cudaFree(u);
+  cudaFree(cols);
+  return rc;
+}
+
+}  // extern "C"
