@@ -86,7 +86,37 @@ class MgHierarchy {
   ig_hier* handle() const { return h_.get(); }
   int n(int l) const { return n_[l]; }
 
+  // MgHierarchy::build's algebraic half on the device (ig_hier_build): the
+  // Galerkin chain, block factorisations and coarse pstrf from the finest A,
+  // the restrictions R[1..L-1] and the pre-filter block layouts
+  // prefilter[1..L-1] (fac ignored); gamma[l] resolved per level.
+  static MgHierarchy build_on_device(const ig_csr& a_fine, const ig_csr* R, const ig_blocks* prefilter,
+                                     const double* gamma, int smoother_kind, double filter_ratio, int n_levels,
+                                     double* seconds = nullptr) {
+    ig_hier* h = nullptr;
+    check(ig_hier_build(&a_fine, R, prefilter, gamma, smoother_kind, filter_ratio, n_levels, &h, seconds),
+          "MgHierarchy::build_on_device");
+    MgHierarchy m;
+    m.h_.reset(h);
+    m.n_levels_ = n_levels;
+    ig_info info{};
+    check(ig_hier_info(h, &info), "MgHierarchy::build_on_device");
+    for (int l = 0; l < n_levels; ++l) m.n_.push_back(info.n[l]);
+    m.rank_ = -1;  // not reported by the device build; see ig_pstrf for the factor itself
+    return m;
+  }
+
+  // Dense columns j0.. of the composed operator (IG_OP_A / IG_OP_VCYCLE /
+  // IG_OP_SMOOTHER_SYMMETRIC) for dense_spectrum (runner.cpp:84-122),
+  // column-major n x count.
+  Vec operator_columns(int kind, int j0, int count) const {
+    Vec out(static_cast<size_t>(n_[n_levels_ - 1]) * count);
+    check(ig_operator_columns(h_.get(), kind, j0, count, out.data()), "operator_columns");
+    return out;
+  }
+
  private:
+  MgHierarchy() = default;
   struct Del {
     void operator()(ig_hier* h) const { ig_hier_destroy(h); }
   };
