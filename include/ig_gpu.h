@@ -104,6 +104,25 @@ typedef struct {
   const int32_t *piv; /* n, 1-based (dpstrf) */
 } ig_coarse;
 
+/* Finest-level assembly payload (the reference's assemble(),
+ * proj/src/assembly.cpp:36-183, after the element loop): element matrices
+ * and load vectors in tables, the uniform space's element cells, physical
+ * supports and anchor numbering.  ig_assemble runs the global assembly (the
+ * setFromTriplets summation, :164-176) and the symmetrisation (:177-180). */
+typedef struct {
+  int32_t dim, p, family;  /* family 1: B-spline (first anchor = cell), 0: Lagrange (p * cell) */
+  int32_t n, n_elements, n_tables;
+  int32_t nf[3];                                /* untrimmed functions per axis */
+  const int32_t *el_ix, *el_iy, *el_iz;         /* element cells (el_iz NULL in 2D) */
+  const int32_t *el_table;                      /* element -> table */
+  const double *K;                              /* n_tables x nloc x nloc, row-major */
+  const double *F;                              /* n_tables x nloc */
+  const int64_t *anchors;                       /* DOF -> untrimmed linear anchor */
+  const int64_t *supp_ptr;                      /* n + 1 */
+  const int32_t *supp_el;                       /* physical support, elements ascending */
+  const int32_t *kept;                          /* untrimmed -> DOF or -1 */
+} ig_assembly;
+
 typedef struct ig_hier ig_hier;
 
 /* Device-side sizes and algorithmic byte counts. */
@@ -198,6 +217,14 @@ int ig_debug_vcycle_timeline(ig_hier *h, const double *d_r, double *d_x,
  * has no such kernel. */
 int ig_debug_tail_profile(ig_hier *h, const double *d_r, double *d_x, uint64_t *stamps,
                           int32_t cap, int32_t *count);
+
+/* --- the step before the path: global assembly -- */
+/* A = 0.5 (K + K^T) and b from the element tables on the device, bit-identical
+ * to the host assembly (each entry sums its element contributions in
+ * ascending element order, exact zeros dropped, as setFromTriplets does;
+ * assembly.cpp:164-180).  A_out: library-owned host CSR (ig_csr_free);
+ * b_out: n doubles.  seconds (may be NULL): [0] wall, [1] device time. */
+int ig_assemble(const ig_assembly *a, ig_csr *A_out, double *b_out, double *seconds);
 
 /* --- composed spectral operators ---------------- */
 /* Columns j0 .. j0+count-1 of a composed operator on the finest level, the

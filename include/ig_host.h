@@ -72,6 +72,9 @@ int igh_build(const igh_config *cfg, igh_case **out);
 int igh_levels(const igh_case *c, const ig_level **levels, int32_t *n_levels,
                const ig_coarse **coarse);
 const double *igh_rhs(const igh_case *c, int32_t *n);
+/* Finest-level assembly payload for ig_assemble (uniform B-spline / Lagrange
+ * cases; owned by the case). */
+int igh_assembly_payload(const igh_case *c, ig_assembly *out);
 /* Pre-filter Schwarz layout of level >= 1 (select_blocks output, the input of
  * factorize_blocks, smoothers.cpp:131-162): blocks in owner order, DOFs
  * ascending.  Owned by the case; built cases only (not igh_read). */

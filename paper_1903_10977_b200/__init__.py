@@ -293,6 +293,29 @@ def factorize_blocks(A: "SpMat", blk_ptr, blk_dofs, filter_ratio: float = 1e-16)
     return optr, odofs, ofp, ofac, int(filt.value), (sec[0], sec[1])
 
 
+def assemble_on_device(case):
+    """The finest level's global assembly on the GPU:
+    the host case's element tables (cut-cell quadrature stays on the host)
+    go through ig_assemble, which sums the element contributions in the
+    reference's setFromTriplets order and symmetrises (assembly.cpp:164-180).
+    Returns (A as SpMat, b, (wall_seconds, device_seconds)), bit-identical to
+    the host assembly (case.A, case.b)."""
+    lib = _ffi.gpu()
+    pay = _ffi.ig_assembly()
+    _check(_ffi.host(), _ffi.host().igh_assembly_payload(case._h, C.byref(pay)), "igh_assembly_payload")
+    out = _ffi.ig_csr()
+    b = np.empty(pay.n)
+    sec = (C.c_double * 2)()
+    _check(lib, lib.ig_assemble(C.byref(pay), C.byref(out), b.ctypes.data_as(C.POINTER(C.c_double)), sec),
+           "ig_assemble")
+    try:
+        m = SpMat.from_c(out)
+        A = SpMat(m.shape[0], m.shape[1], m.row_ptr.copy(), m.col_idx.copy(), m.val.copy())
+    finally:
+        lib.ig_csr_free(C.byref(out))
+    return A, b, (sec[0], sec[1])
+
+
 class TooLarge(RuntimeError):
     """spectral.hpp:16 TooLarge."""
 

@@ -31,6 +31,13 @@ class ig_level(C.Structure):
                 ("gamma", f64), ("blocks", ig_blocks)]
 
 
+class ig_assembly(C.Structure):
+    _fields_ = [("dim", i32), ("p", i32), ("family", i32), ("n", i32), ("n_elements", i32), ("n_tables", i32),
+                ("nf", i32 * 3), ("el_ix", P(i32)), ("el_iy", P(i32)), ("el_iz", P(i32)), ("el_table", P(i32)),
+                ("K", P(f64)), ("F", P(f64)), ("anchors", P(i64)), ("supp_ptr", P(i64)), ("supp_el", P(i32)),
+                ("kept", P(i32))]
+
+
 class ig_coarse(C.Structure):
     _fields_ = [("n", i32), ("rank", i32), ("L", P(f64)), ("piv", P(i32))]
 
@@ -109,6 +116,7 @@ def host() -> C.CDLL:
         lib.igh_levels.argtypes = [C.c_void_p, P(P(ig_level)), P(i32), P(P(ig_coarse))]
         lib.igh_rhs.argtypes = [C.c_void_p, P(i32)]
         lib.igh_rhs.restype = P(f64)
+        lib.igh_assembly_payload.argtypes = [C.c_void_p, P(ig_assembly)]
         lib.igh_prefilter_blocks.argtypes = [C.c_void_p, i32, P(i32), P(P(i32)), P(P(i32))]
         lib.igh_get_info.argtypes = [C.c_void_p, P(igh_info)]
         lib.igh_anchors.argtypes = [C.c_void_p, i32, P(i32)]
@@ -131,7 +139,7 @@ GPU_SYMBOLS = (
     "ig_pcg_result", "ig_last_error", "ig_set_option", "ig_richardson",
     "ig_smoother_apply_dir", "ig_smoother_apply_symmetric", "ig_galerkin_hierarchy", "ig_csr_free",
     "ig_factorize_blocks", "ig_blocks_free", "ig_pstrf", "ig_hier_build",
-    "ig_operator_columns",
+    "ig_operator_columns", "ig_assemble",
 )
 
 
@@ -149,6 +157,7 @@ def gpu() -> C.CDLL:
         lib.ig_blocks_free.restype = None
         lib.ig_pstrf.argtypes = [i32, dp, P(i32), f64, P(i32)]
         lib.ig_operator_columns.argtypes = [vp, i32, i32, i32, dp]
+        lib.ig_assemble.argtypes = [P(ig_assembly), P(ig_csr), dp, dp]
         lib.ig_hier_build.argtypes = [P(ig_csr), P(ig_csr), P(ig_blocks), dp, i32, f64, i32, P(vp), dp]
         lib.ig_hier_destroy.argtypes = [vp]
         lib.ig_hier_destroy.restype = None

@@ -31,6 +31,7 @@
 #include "spmv_psell.cuh"
 #include "galerkin.cuh"
 #include "blockfac.cuh"
+#include "assemble.cuh"
 #include "spmv_tma.cuh"
 #include "vtail.cuh"
 
@@ -3047,6 +3048,124 @@ int ig_operator_columns(ig_hier* h, int32_t kind, int32_t j0, int32_t count, dou
   cudaFree(e);
   cudaFree(u);
   cudaFree(cols);
+  return rc;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int ig_assemble(const ig_assembly* a, ig_csr* A_out, double* b_out, double* seconds) {
+  if (!a || !A_out || !b_out) return fail(IG_INVALID_ARGUMENT, "assemble: null argument");
+  *A_out = ig_csr{};
+  std::vector<void*> dev;
+  auto dal = [&](size_t bytes) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
+    dev.push_back(p);
+    return p;
+  };
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  const int rc = guarded([&] {
+    if (a->dim != 2 && a->dim != 3) throw Error(IG_INVALID_ARGUMENT, "assemble: dim must be 2 or 3");
+    if (a->p < 1 || a->n < 1 || a->n_elements < 1 || a->n_tables < 1)
+      throw Error(IG_INVALID_ARGUMENT, "assemble: empty payload");
+    if (!a->el_ix || !a->el_iy || (a->dim == 3 && !a->el_iz) || !a->el_table || !a->K || !a->F || !a->anchors ||
+        !a->supp_ptr || !a->supp_el || !a->kept)
+      throw Error(IG_INVALID_ARGUMENT, "assemble: null array");
+    int nl = 1;
+    for (int d = 0; d < a->dim; ++d) nl *= a->p + 1;
+    const int W = 2 * a->p + 1;
+    const int wsize = a->dim == 3 ? W * W * W : W * W;
+    const int64_t nun = static_cast<int64_t>(a->nf[0]) * a->nf[1] * (a->dim == 3 ? a->nf[2] : 1);
+    const int64_t nsupp = a->supp_ptr[a->n];
+    const size_t smem = static_cast<size_t>(kAsmWarps) * wsize * (sizeof(double) + 1);
+    if (smem > 200 * 1024) throw Error(IG_UNSUPPORTED, "assemble: window too large for shared memory");
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    auto up = [&](const void* src, size_t bytes) {
+      void* d = dal(bytes);
+      if (bytes) CK(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st));
+      return d;
+    };
+    const size_t ne = static_cast<size_t>(a->n_elements);
+    AsmArgs g{};
+    g.dim = a->dim;
+    g.p = a->p;
+    g.family = a->family;
+    g.n = a->n;
+    g.nloc = nl;
+    g.W = W;
+    g.wsize = wsize;
+    g.nf0 = a->nf[0];
+    g.nf1 = a->nf[1];
+    g.nf2 = a->dim == 3 ? a->nf[2] : 1;
+    g.el_ix = static_cast<const int32_t*>(up(a->el_ix, 4 * ne));
+    g.el_iy = static_cast<const int32_t*>(up(a->el_iy, 4 * ne));
+    g.el_iz = a->dim == 3 ? static_cast<const int32_t*>(up(a->el_iz, 4 * ne)) : nullptr;
+    g.el_table = static_cast<const int32_t*>(up(a->el_table, 4 * ne));
+    g.K = static_cast<const double*>(up(a->K, sizeof(double) * static_cast<size_t>(a->n_tables) * nl * nl));
+    g.F = static_cast<const double*>(up(a->F, sizeof(double) * static_cast<size_t>(a->n_tables) * nl));
+    g.anchors = static_cast<const int64_t*>(up(a->anchors, 8 * static_cast<size_t>(a->n)));
+    g.supp_ptr = static_cast<const int64_t*>(up(a->supp_ptr, 8 * (static_cast<size_t>(a->n) + 1)));
+    g.supp_el = static_cast<const int32_t*>(up(a->supp_el, 4 * static_cast<size_t>(nsupp)));
+    g.kept = static_cast<const int32_t*>(up(a->kept, 4 * static_cast<size_t>(nun)));
+    auto* cnt = static_cast<int32_t*>(dal(4 * static_cast<size_t>(a->n)));
+    auto* off = static_cast<int64_t*>(dal(8 * (static_cast<size_t>(a->n) + 1)));
+    auto* ptr = static_cast<int32_t*>(dal(4 * (static_cast<size_t>(a->n) + 1)));
+    auto* db = static_cast<double*>(dal(8 * static_cast<size_t>(a->n)));
+    auto* bad = static_cast<int*>(dal(sizeof(int)));
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    CK(cudaFuncSetAttribute(k_asm_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    CK(cudaFuncSetAttribute(k_asm_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaEventRecord(e0, st));
+    const unsigned gr = static_cast<unsigned>((a->n + kAsmWarps - 1) / kAsmWarps);
+    k_asm_rows<false><<<gr, 32 * kAsmWarps, smem, st>>>(g, cnt, nullptr, nullptr, nullptr, nullptr);
+    CK(cudaGetLastError());
+    const int64_t nnz = gal_offsets(a->n, cnt, off, ptr, st);
+    auto* col = static_cast<int32_t*>(dal(4 * static_cast<size_t>(nnz)));
+    auto* val = static_cast<double*>(dal(8 * static_cast<size_t>(nnz)));
+    auto* sym = static_cast<double*>(dal(8 * static_cast<size_t>(nnz)));
+    k_asm_rows<true><<<gr, 32 * kAsmWarps, smem, st>>>(g, nullptr, off, col, val, db);
+    CK(cudaGetLastError());
+    k_asm_sym<<<static_cast<unsigned>((a->n + 255) / 256), 256, 0, st>>>(a->n, ptr, col, val, sym, bad);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e1, st));
+    int hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hbad) throw Error(IG_INVALID_ARGUMENT, "assemble: unsymmetric pattern");
+    auto* hp = static_cast<int32_t*>(std::malloc(4 * (static_cast<size_t>(a->n) + 1)));
+    auto* hc = static_cast<int32_t*>(std::malloc(4 * std::max<size_t>(static_cast<size_t>(nnz), 1)));
+    auto* hv = static_cast<double*>(std::malloc(8 * std::max<size_t>(static_cast<size_t>(nnz), 1)));
+    A_out->n_rows = A_out->n_cols = a->n;
+    A_out->nnz = nnz;
+    A_out->row_ptr = hp;
+    A_out->col_idx = hc;
+    A_out->val = hv;
+    if (!hp || !hc || !hv) throw Error(IG_CUDA_ERROR, "assemble: host allocation failed");
+    CK(cudaMemcpyAsync(hp, ptr, 4 * (static_cast<size_t>(a->n) + 1), cudaMemcpyDeviceToHost, st));
+    if (nnz) {
+      CK(cudaMemcpyAsync(hc, col, 4 * static_cast<size_t>(nnz), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hv, sym, 8 * static_cast<size_t>(nnz), cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaMemcpyAsync(b_out, db, 8 * static_cast<size_t>(a->n), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (seconds) seconds[1] = 1e-3 * ms;
+    return IG_OK;
+  });
+  for (void* p : dev) cudaFree(p);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (st) cudaStreamDestroy(st);
+  if (seconds) seconds[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (rc != IG_OK) ig_csr_free(A_out);
   return rc;
 }
 

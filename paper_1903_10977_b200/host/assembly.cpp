@@ -17,6 +17,9 @@
 // ascending element order -- the order in which Eigen's setFromTriplets sums
 // the reference's duplicate triplets -- dropping exact zeros (assembly.cpp:171).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 
@@ -492,6 +495,10 @@ Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& 
   const double beta = prob.beta > 0.0 ? prob.beta : default_penalty(g);
   const int ne = static_cast<int>(s.el_ix.size());
   Assembled out;
+  const bool timing = std::getenv("IG_TIMING") != nullptr;
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+  const auto ta0 = tnow();
 
   // --- element data -------------------------------------------------------
   // Elements needing individual treatment: cut, or (2D) box-boundary sides.
@@ -584,6 +591,33 @@ Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& 
     }
   }
   out.eta = eta;
+  const auto ta1 = tnow();
+
+  // Element tables for the device row gather (same data, flattened).
+  {
+    const int ncls = static_cast<int>(cdata.size());
+    out.n_tables = ncls + static_cast<int32_t>(sdata.size());
+    out.tabK.assign(static_cast<size_t>(out.n_tables) * nl * nl, 0.0);
+    out.tabF.assign(static_cast<size_t>(out.n_tables) * nl, 0.0);
+    auto put = [&](int t, const ElemData& d) {
+      if (d.K.size() == static_cast<size_t>(nl) * nl)
+        std::copy(d.K.begin(), d.K.end(), out.tabK.begin() + static_cast<size_t>(t) * nl * nl);
+      if (d.F.size() == static_cast<size_t>(nl)) std::copy(d.F.begin(), d.F.end(), out.tabF.begin() + static_cast<size_t>(t) * nl);
+    };
+    for (int t = 0; t < ncls; ++t)
+      if (class_used[t]) put(t, cdata[t]);
+    for (size_t k = 0; k < sdata.size(); ++k) put(ncls + static_cast<int>(k), sdata[k]);
+    out.el_table.resize(static_cast<size_t>(ne));
+    for (int e = 0; e < ne; ++e) {
+      if (special[e] >= 0) {
+        out.el_table[e] = ncls + special[e];
+      } else {
+        const int cx = s.ext_cls[0][s.el_ix[e]], cy = s.ext_cls[1][s.el_iy[e]];
+        const int cz = dim == 3 ? s.ext_cls[2][s.el_iz[e]] : 0;
+        out.el_table[e] = (cz * ncy + cy) * ncx + cx;
+      }
+    }
+  }
 
   auto elem = [&](int e) -> const ElemData& {
     if (special[e] >= 0) return sdata[special[e]];
@@ -674,6 +708,7 @@ Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& 
   // Columns come out in window order; kept numbering is monotone in
   // (az, ay, ax), so window order is ascending column order.
 
+  const auto ta2 = tnow();
   // --- symmetrise: A = 0.5 (A + A^T) (assembly.cpp:177-180) ----------------
   std::vector<double> sym(A.val.size());
   int unsym = 0;
@@ -692,6 +727,9 @@ Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& 
     }
   if (unsym) throw SetupError("assemble: unsymmetric pattern");
   A.val.swap(sym);
+  if (timing)
+    std::fprintf(stderr, "assemble: element data %.3f s (%zu special), row gather %.3f s, symmetrise %.3f s\n",
+                 secs(ta0, ta1), special_list.size(), secs(ta1, ta2), secs(ta2, tnow()));
   return out;
 }
 

@@ -480,6 +480,10 @@ struct igh_case {
   // Pre-filter Schwarz layouts (block pointers, DOFs) as select_blocks made
   // them: the input of factorize_blocks, kept for the device factorisation.
   std::vector<std::vector<int32_t>> pre_ptr, pre_dofs;
+  // Finest-level element tables (device assembly payload; uniform spaces).
+  std::vector<double> tabK, tabF;
+  std::vector<int32_t> el_table;
+  int32_t n_tables = 0;
   std::vector<double> gamma;
   std::vector<int32_t> kind;
   std::vector<double> coarseL;
@@ -652,6 +656,10 @@ int igh_build(const igh_config* cfg, igh_case** out) {
     } else {
       down.push_back(build_space(g, ls, fam, cfg->degree, cfg->classify_depth, threads));
       as = assemble(*down[0], prob, qc, threads);
+      c->tabK = std::move(as.tabK);
+      c->tabF = std::move(as.tabF);
+      c->el_table = std::move(as.el_table);
+      c->n_tables = as.n_tables;
       t1 = now();
       Adown.push_back(std::move(as.A));
       for (int l = 1; l < L; ++l) {
@@ -774,6 +782,32 @@ int igh_prefilter_blocks(const igh_case* c, int32_t level, int32_t* n_blocks, co
   *n_blocks = static_cast<int32_t>(c->pre_ptr[level].size()) - 1;
   *blk_ptr = c->pre_ptr[level].data();
   *blk_dofs = c->pre_dofs[level].data();
+  return IG_OK;
+}
+
+int igh_assembly_payload(const igh_case* c, ig_assembly* out) {
+  if (!c || !out) return fail("igh_assembly_payload: null argument");
+  if (c->spaces.empty() || c->el_table.empty())
+    return fail("igh_assembly_payload: only built uniform (B-spline / Lagrange) cases carry the element tables");
+  const Space& s = *c->spaces.back();
+  *out = ig_assembly{};
+  out->dim = s.grid.dim;
+  out->p = s.p;
+  out->family = s.family == Family::Bspline ? 1 : 0;
+  out->n = s.n();
+  out->n_elements = static_cast<int32_t>(s.el_ix.size());
+  out->n_tables = c->n_tables;
+  for (int d = 0; d < 3; ++d) out->nf[d] = s.nf[d];
+  out->el_ix = s.el_ix.data();
+  out->el_iy = s.el_iy.data();
+  out->el_iz = s.grid.dim == 3 ? s.el_iz.data() : nullptr;
+  out->el_table = c->el_table.data();
+  out->K = c->tabK.data();
+  out->F = c->tabF.data();
+  out->anchors = s.anchors.data();
+  out->supp_ptr = s.supp_ptr.data();
+  out->supp_el = s.supp_el.data();
+  out->kept = s.kept.data();
   return IG_OK;
 }
 

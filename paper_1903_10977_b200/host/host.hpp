@@ -210,6 +210,13 @@ struct Assembled {
   std::vector<double> b;
   double eta = 1.0;  // min volume fraction (quadrature.cpp:363-371)
   int64_t cut_elements = 0;
+  // Element tables the row gather consumed (device assembly payload,
+  // ig_assembly): table t holds K (nloc x nloc, row-major) and F (nloc);
+  // element e uses table el_table[e] (Inside classes first, then the
+  // individually integrated elements).
+  std::vector<double> tabK, tabF;
+  std::vector<int32_t> el_table;
+  int32_t n_tables = 0;
 };
 
 Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& q,
