@@ -259,6 +259,7 @@ int g_psell_ctas = 0;
 // overlap under PDL and the graph fork, and the fused kernel's phase-1 fence
 // + arrival + wait sits on the critical path of every application.
 int32_t g_fused_rows = 0;
+int32_t g_fork_rows = 0;  // IG_OPT_FORK_ROWS
 // Levels below the finest with at most this many DOFs live in the L2-persisting
 // arena (ig_hier::alloc); 0 = off.  Arena size g_l2_bytes.
 // Measured (profiles/option_sweep.py 18/19): C4 V-cycle 903 -> 881 us, C3
@@ -1002,7 +1003,15 @@ struct ig_hier {
     big.n_groups = g_split ? l.g_small : l.G.n_groups;
     const int32_t n_small = l.G.n_groups - big.n_groups;
     const bool multi = big.n_groups + big.n_wblocks > 0;
-    if (multi) {
+    // Levels below g_fork_rows DOFs keep the block solves on the main stream
+    // (a serial PDL chain) instead of forking them onto the side stream.
+    const bool fork = multi && l.n >= g_fork_rows;
+    if (multi && !fork) {
+      const unsigned gb = static_cast<unsigned>((static_cast<int64_t>(big.n_groups + big.n_wblocks) * 32 + 127) / 128);
+      launch(k_as_blocks, gb, 128, 0, stream, big, r, l.ybuf, s);
+      CK(cudaGetLastError());
+    }
+    if (fork) {
       CK(cudaEventRecord(ev_fork, stream));
       CK(cudaStreamWaitEvent(side, ev_fork, 0));
       const unsigned gb = static_cast<unsigned>((static_cast<int64_t>(big.n_groups + big.n_wblocks) * 32 + 127) / 128);
@@ -1017,7 +1026,7 @@ struct ig_hier {
     else
       launch(k_as_small_simple<false>, g + gctas, kCta, 0, stream, l.G, big.n_groups, gctas, l.S, r, l.ybuf, x, s);
     CK(cudaGetLastError());
-    if (multi) CK(cudaStreamWaitEvent(stream, ev_join, 0));
+    if (fork) CK(cudaStreamWaitEvent(stream, ev_join, 0));
     if (rdot) {
       // Complex DOFs, then r . z as a plain streaming reduction (the fused
       // k_as_finish_red keeps the list walks inside the reduction chunks and
@@ -1790,6 +1799,11 @@ int ig_set_option(int32_t option, int64_t value) {
   if (option == IG_OPT_RED_CTAS) {
     if (value < 1 || value > 64) return fail(IG_INVALID_ARGUMENT, "ig_set_option: reduction CTAs per SM in 1..64");
     g_red_ctas = static_cast<int>(value);
+    return IG_OK;
+  }
+  if (option == IG_OPT_FORK_ROWS) {
+    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: fork rows out of range");
+    g_fork_rows = static_cast<int32_t>(value);
     return IG_OK;
   }
   if (option == IG_OPT_L2_MB) {
