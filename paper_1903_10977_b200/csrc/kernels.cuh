@@ -24,6 +24,17 @@ __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// Split form: a kernel first loads what no earlier kernel writes (matrix
+// layouts, block factors and DOF lists, contribution lists -- built once at
+// ig_hier_create), THEN waits for its predecessor, so those loads overlap the
+// predecessor's tail instead of sitting on the chain.  Waiters are passed to
+// the shared device helpers; NoWait where the caller already waited.
+struct NoWait {
+  __device__ __forceinline__ void operator()() const {}
+};
+struct PdlWait {
+  __device__ __forceinline__ void operator()() const { pdl_entry(); }
+};
 
 constexpr int kCta = 256;   // threads per CTA == reduction chunk size
 // Register budgets (min CTAs per SM) of the smoother and small-level SpMV
@@ -573,19 +584,25 @@ __device__ __forceinline__ void block_out(double* ybuf, double* xms, int pos_or_
   }
 }
 
-template <int SM, bool MS = false, class LD = RLoad>
+template <int SM, bool MS = false, class LD = RLoad, class WT = NoWait>
 __device__ __forceinline__ void block_solve(const AsGroups& G, int g, int lane, int s, int smax,
-                                            typename NoDeduce<LD>::type r, double* ybuf, double* xms = nullptr) {
+                                            typename NoDeduce<LD>::type r, double* ybuf, double* xms = nullptr,
+                                            WT wt = WT{}) {
   double y[SM], Lp[SM * (SM + 1) / 2];
+  int dof[SM];
   const int32_t* dp = G.dofs + G.dof_off[g] + lane;
   const double* fp = G.fac + G.fac_off[g] + lane;
-  // All loads first (independent of the substitution chain).
+  // All loads first (independent of the substitution chain): the static DOF
+  // list and factor before the predecessor wait, the residual gathers after.
 #pragma unroll
-  for (int i = 0; i < SM; ++i) y[i] = (i < s) ? r(dp[i * 32]) : 0.0;
+  for (int i = 0; i < SM; ++i) dof[i] = (i < s) ? dp[i * 32] : 0;
 #pragma unroll
   for (int j = 0; j < SM; ++j)
 #pragma unroll
     for (int i = j; i < SM; ++i) Lp[packed_idx(i, j, SM)] = (i < s) ? fp[packed_idx(i, j, smax) * 32] : 1.0;
+  wt();
+#pragma unroll
+  for (int i = 0; i < SM; ++i) y[i] = (i < s) ? r(dof[i]) : 0.0;
   double rd[SM];  // reciprocal pivots, computed off the substitution chain
 #pragma unroll
   for (int j = 0; j < SM; ++j) rd[j] = safe_rcp(Lp[packed_idx(j, j, SM)]);
@@ -612,13 +629,15 @@ __device__ __forceinline__ void block_solve(const AsGroups& G, int g, int lane, 
   const int pos = G.ypos[g * 32 + lane];
 #pragma unroll
   for (int i = 0; i < SM; ++i)
-    if (i < s) block_out<MS>(ybuf, xms, MS ? dp[i * 32] : pos + i, y[i]);
+    if (i < s) block_out<MS>(ybuf, xms, MS ? dof[i] : pos + i, y[i]);
 }
 
 // Generic (any size) fallback with local memory.
-template <bool MS = false, class LD = RLoad>
+template <bool MS = false, class LD = RLoad, class WT = NoWait>
 __device__ __noinline__ void block_solve_any(const AsGroups& G, int g, int lane, int s, int smax,
-                                             typename NoDeduce<LD>::type r, double* ybuf, double* xms = nullptr) {
+                                             typename NoDeduce<LD>::type r, double* ybuf, double* xms = nullptr,
+                                             WT wt = WT{}) {
+  wt();
   double y[128];
   const int32_t* dp = G.dofs + G.dof_off[g] + lane;
   const double* fp = G.fac + G.fac_off[g] + lane;
@@ -637,9 +656,10 @@ __device__ __noinline__ void block_solve_any(const AsGroups& G, int g, int lane,
   for (int i = 0; i < s; ++i) block_out<MS>(ybuf, xms, MS ? dp[i * 32] : pos + i, y[i]);
 }
 
-template <bool MS = false, class LD = RLoad>
+template <bool MS = false, class LD = RLoad, class WT = NoWait>
 __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int lane,
-                                                 typename NoDeduce<LD>::type r, double* ybuf, double* xms = nullptr) {
+                                                 typename NoDeduce<LD>::type r, double* ybuf, double* xms = nullptr,
+                                                 WT wt = WT{}) {
   const int s = G.w_size[b];
   const double* f = G.w_fac + G.w_fac_off[b];
   const int32_t* dp = G.w_dofs + G.w_dof_off[b];
@@ -649,8 +669,10 @@ __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int l
     const int hi = lane > t ? lane : t, lo = lane > t ? t : lane;
     m[t] = (t < s && lane < s) ? __ldg(f + lo * s + hi) : 0.0;
   }
-  double y = lane < s ? r(dp[lane]) : 0.0;
+  const int mydof = lane < s ? dp[lane] : 0;
   const double dg = lane < s ? __ldg(f + lane * s + lane) : 1.0;  // own pivot L(lane, lane)
+  wt();
+  double y = lane < s ? r(mydof) : 0.0;
   const double rdg = safe_rcp(dg);
   double acc = 0.0;
   if (__all_sync(0xffffffffu, isfinite(rdg) && rdg != 0.0)) {
@@ -692,33 +714,34 @@ __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int l
       }
     }
   }
-  if (lane < s) block_out<MS>(ybuf, xms, MS ? dp[lane] : G.w_ypos[b] + lane, y);
+  if (lane < s) block_out<MS>(ybuf, xms, MS ? mydof : G.w_ypos[b] + lane, y);
 }
 
 // One warp-sized work item w of phase 1 (group of small blocks or a warp block).
-template <bool MS = false, class LD = RLoad>
+template <bool MS = false, class LD = RLoad, class WT = NoWait>
 __device__ __forceinline__ void as_blocks_item(const AsGroups& G, int w, int lane, typename NoDeduce<LD>::type r,
-                                               double* ybuf, double* xms = nullptr) {
+                                               double* ybuf, double* xms = nullptr, WT wt = WT{}) {
   if (w < G.n_groups) {
     const int g = w;
     const int s = G.size[g * 32 + lane];
     const int smax = G.smax[g];  // warp-uniform
     if (s == 0) return;
     if (smax <= 4)
-      block_solve<4, MS, LD>(G, g, lane, s, smax, r, ybuf, xms);
+      block_solve<4, MS, LD, WT>(G, g, lane, s, smax, r, ybuf, xms, wt);
     else if (smax <= 8)
-      block_solve<8, MS, LD>(G, g, lane, s, smax, r, ybuf, xms);
+      block_solve<8, MS, LD, WT>(G, g, lane, s, smax, r, ybuf, xms, wt);
     else
-      block_solve_any<MS, LD>(G, g, lane, s, smax, r, ybuf, xms);
+      block_solve_any<MS, LD, WT>(G, g, lane, s, smax, r, ybuf, xms, wt);
   } else if (w - G.n_groups < G.n_wblocks) {
-    warp_block_solve<MS, LD>(G, w - G.n_groups, lane, r, ybuf, xms);
+    warp_block_solve<MS, LD, WT>(G, w - G.n_groups, lane, r, ybuf, xms, wt);
   }
 }
 __global__ void IG_ASB_BOUNDS k_as_blocks(AsGroups G, const double* __restrict__ r,
                                                    double* ybuf, const PcgState* st) {
-  pdl_entry();
-  if (pcg_done(st)) return;
-  as_blocks_item(G, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, r, ybuf);
+  // pcg_done is a compile-time no-op for V-cycle kernels (see above); the
+  // predecessor wait happens inside, after the static loads.
+  as_blocks_item<false, RLoad, PdlWait>(G, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, r,
+                                        ybuf, nullptr, PdlWait{});
 }
 
 // Phase 2: deterministic segmented reduction per DOF, contributions in
@@ -868,20 +891,27 @@ template <bool ACC>
 __global__ void IG_AS_BOUNDS k_as_small_simple(AsGroups G, int32_t g_begin, int32_t n_gctas, AsGather S,
                                                           const double* __restrict__ r, double* ybuf, double* x,
                                                           const PcgState* st) {
-  pdl_entry();
-  if (pcg_done(st)) return;
   if (static_cast<int32_t>(blockIdx.x) < n_gctas) {
     const int g = g_begin + static_cast<int>((blockIdx.x * kCta + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (g >= G.n_groups) return;
     const int s = G.size[g * 32 + lane];
     if (s == 0) return;
-    block_solve<4>(G, g, lane, s, G.smax[g], r, ybuf);
+    block_solve<4, false, RLoad, PdlWait>(G, g, lane, s, G.smax[g], r, ybuf, nullptr, PdlWait{});
     return;
   }
   const int d = (blockIdx.x - n_gctas) * kCta + threadIdx.x;
   if (d >= S.n) return;
-  as_simple_item<ACC>(S, d, r, x);
+  const int h = S.head[d];  // static: before the predecessor wait
+  if (h < 0) return;
+  const double l = S.sdiag[d];
+  pdl_entry();
+  const double rd = r[d];
+  const double xo = ACC ? x[d] : 0.0;
+  double acc = 0.0;
+  acc = acc + (rd / l) / l;
+  const double out = S.gamma * acc;
+  x[d] = ACC ? xo + out : out;
 }
 
 template <bool ACC>
@@ -895,11 +925,52 @@ template <bool ACC>
 __global__ void IG_AS_BOUNDS k_as_complex(AsGather S, const double* __restrict__ r,
                                                      const double* __restrict__ ybuf, double* x,
                                                      const PcgState* st) {
-  pdl_entry();
-  if (pcg_done(st)) return;
   const int c = blockIdx.x * kCta + threadIdx.x;
   if (c >= S.n_complex) return;
-  as_complex_item<ACC>(S, c, r, ybuf, x);
+  // Static part of the list walk (DOF, bounds, first batch of codes and
+  // singleton factors) before the predecessor wait.
+  constexpr int U = 8;
+  const int d = S.cdof[c];
+  const int q0 = S.cptr[c], q1 = S.cptr[c + 1];
+  int code[U];
+  double ls[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) code[u] = (q0 + u < q1) ? S.centry[q0 + u] : 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) ls[u] = (q0 + u < q1 && code[u] < 0) ? S.sval[-code[u] - 1] : 1.0;
+  pdl_entry();
+  const double rd = r[d];
+  double v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) v[u] = (q0 + u < q1) ? (code[u] < 0 ? (rd / ls[u]) / ls[u] : ybuf[code[u]]) : 0.0;
+  double acc = 0.0;
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (q0 + u < q1) acc = acc + v[u];
+  for (int qb = q0 + U; qb < q1; qb += U) {  // longer lists: as_list_sum_c's batches
+    int cd[U];
+    double w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cd[u] = (qb + u < q1) ? S.centry[qb + u] : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (qb + u < q1) {
+        if (cd[u] < 0) {
+          const double l2 = S.sval[-cd[u] - 1];
+          w[u] = (rd / l2) / l2;
+        } else {
+          w[u] = ybuf[cd[u]];
+        }
+      } else {
+        w[u] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (qb + u < q1) acc = acc + w[u];
+  }
+  const double out = S.gamma * acc;
+  x[d] = ACC ? x[d] + out : out;
 }
 
 // ---------------------------------------------- fused additive smoother ----
