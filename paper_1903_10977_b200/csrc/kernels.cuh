@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kCta, SpmvVar<VAR>::MINB) k_spmv(Sell A, const
 // warp-maximum length is formed by shuffles).
 template <int MODE, int G>
 __device__ __forceinline__ void spmv_grp_item(const Sell& A, int t, const double* __restrict__ x, double* y,
-                                              const double* rsrc) {
+                                              const double* rsrc, bool pdl = false) {
   const int row = t / G;
   const int g = t % G;
   const int lane = threadIdx.x & 31;
@@ -460,6 +460,7 @@ __device__ __forceinline__ void spmv_grp_item(const Sell& A, int t, const double
         c[u] = od ? row + __ldg(dc + k) : __ldg(A.col + base + static_cast<int64_t>(k) * kSell);
       }
     }
+    if (pdl && k0 == 0) pdl_entry();  // values / columns are static: loaded before the predecessor wait
     double prod[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) prod[u] = (k0 + u * G + g < len) ? v[u] * __ldg(x + c[u]) : 0.0;
@@ -474,13 +475,13 @@ __device__ __forceinline__ void spmv_grp_item(const Sell& A, int t, const double
       }
     }
   }
+  if (pdl && wlen == 0) pdl_entry();
   if (valid_row && g == 0) y[row] = (MODE == 0) ? acc : rsrc[row] - acc;
 }
 template <int MODE, int G>
 __global__ void IG_GRP_BOUNDS k_spmv_grp(Sell A, const double* __restrict__ x, double* y,
                                                    const double* rsrc) {
-  pdl_entry();
-  spmv_grp_item<MODE, G>(A, blockIdx.x * kCta + threadIdx.x, x, y, rsrc);
+  spmv_grp_item<MODE, G>(A, blockIdx.x * kCta + threadIdx.x, x, y, rsrc, true);
 }
 
 // Prolongation fused with the correction: cor = P xc (P = R^T stored as CSR
@@ -489,9 +490,15 @@ __global__ void IG_GRP_BOUNDS k_spmv_grp(Sell A, const double* __restrict__ x, d
 template <bool STREAM, int VAR>
 __global__ void __launch_bounds__(kCta, SpmvVar<VAR>::MINB) k_prolong(Sell P, const double* __restrict__ xc, double* cor,
                                                   double* x, const PcgState* st) {
+  const int row = blockIdx.x * kCta + threadIdx.x;
+  if (row < P.n_rows) {  // static layout words into L1 while the predecessor finishes
+    const int64_t base = P.slice_ptr[row >> 5] + (row & 31);
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(P.val + base));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(P.col + base));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(P.rowinfo + row));
+  }
   pdl_entry();
   if (pcg_done(st)) return;
-  const int row = blockIdx.x * kCta + threadIdx.x;
   if (row >= P.n_rows) return;
   const double c = sell_row<STREAM, VAR>(P, row, xc);
   cor[row] = c;
@@ -1314,10 +1321,10 @@ __device__ __forceinline__ double wait_slot(const volatile double* p) {
 
 // The solve on one CTA (blockDim >= 32*ceil(rank/32); surplus warps only
 // zero-fill).  smem: [packed L11 (SM only)][forward: rank][backward: rank].
-template <bool SM>
+template <bool SM, class WT = NoWait>
 __device__ __forceinline__ void coarse_solve_cta(int32_t n, int32_t rank, const double* __restrict__ Lp,
                                                  const int32_t* __restrict__ piv, const double* __restrict__ r,
-                                                 double* x, double* smem) {
+                                                 double* x, double* smem, WT wt = WT{}) {
   __shared__ unsigned long long mbar;
   const int64_t np = static_cast<int64_t>(rank) * (rank + 1) / 2;
   const int64_t np_al = (np + 1) & ~int64_t(1);  // 16-byte aligned region
@@ -1332,6 +1339,7 @@ __device__ __forceinline__ void coarse_solve_cta(int32_t n, int32_t rank, const 
     bulk_copy_to_smem(smem, Lp, static_cast<size_t>(np_al) * sizeof(double), &mbar);  // has a barrier
   else
     __syncthreads();
+  wt();  // L11 is static: its staging overlaps the predecessor; r is read after the wait
   const double* L = SM ? smem : Lp;  // compile-time: LDS from shared, LDG otherwise
   // Packed column-major lower: L(i, j) = L[off(j) + i], off(j) = j*rank - j(j-1)/2 - j.
   auto off = [&](int j) { return j * rank - (j * (j - 1)) / 2 - j; };
@@ -1415,10 +1423,8 @@ __global__ void __launch_bounds__(BIG ? 1024 : 256, 1) k_coarse(int32_t n, int32
                                                                const int32_t* __restrict__ piv,
                                                                const double* __restrict__ r, double* x,
                                                                const PcgState* st) {
-  pdl_entry();
-  if (pcg_done(st)) return;
   extern __shared__ __align__(16) double smem[];
-  coarse_solve_cta<SM>(n, rank, Lp, piv, r, x, smem);
+  coarse_solve_cta<SM, PdlWait>(n, rank, Lp, piv, r, x, smem, PdlWait{});
 }
 
 // ---------------------------------------------------------- PCG vectors ---

@@ -120,13 +120,12 @@ __device__ __forceinline__ void fast2_dispatch(const double* __restrict__ x, int
 // One warp, one slice.  Returns the row this lane owns (-1: none) and its
 // sum; FAST2 slices give each lane a second row (row2 / acc2, else -1).
 template <bool STREAM>
-__device__ __forceinline__ int psell_slice(const PSell& A, int slice, const double* __restrict__ x, double& acc,
+__device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const double* __restrict__ x, double& acc,
                                            int& row2, double& acc2) {
   acc = 0.0;
   acc2 = 0.0;
   row2 = -1;
   const int lane = threadIdx.x & 31;
-  const uint4 mu = __ldg(reinterpret_cast<const uint4*>(A.meta + slice));
   const uint32_t pk = mu.w;
   const int count = static_cast<int>((pk >> 11) & 0x3f);
   if (count == 0) return -1;  // padding slice (warp-uniform)
@@ -238,12 +237,13 @@ __device__ __forceinline__ int psell_slice(const PSell& A, int slice, const doub
 template <int MODE, bool STREAM>
 __global__ void __launch_bounds__(kCta, IG_PSPMV_MINB) k_pspmv(PSell A, const double* __restrict__ x, double* y,
                                                const double* rsrc, const PcgState* st) {
+  const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
+  const uint4 mu = __ldg(reinterpret_cast<const uint4*>(A.meta + slice));  // static: before the wait
   pdl_entry();
   if (pcg_done(st)) return;
-  const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   double acc, acc2;
   int row2;
-  const int row = psell_slice<STREAM>(A, slice, x, acc, row2, acc2);
+  const int row = psell_slice<STREAM>(A, mu, x, acc, row2, acc2);
   if (row < 0) return;
   y[row] = (MODE == 0) ? acc : rsrc[row] - acc;
   if (row2 >= 0) y[row2] = (MODE == 0) ? acc2 : rsrc[row2] - acc2;
@@ -273,12 +273,13 @@ __global__ void __launch_bounds__(kCta) k_pap(int n, const double* __restrict__ 
 template <bool STREAM>
 __global__ void __launch_bounds__(kCta, IG_PPROLONG_MINB) k_pprolong(PSell P, const double* __restrict__ xc, double* cor, double* x,
                                                   const PcgState* st) {
+  const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
+  const uint4 mu = __ldg(reinterpret_cast<const uint4*>(P.meta + slice));  // static: before the wait
   pdl_entry();
   if (pcg_done(st)) return;
-  const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   double c, c2;
   int row2;
-  const int row = psell_slice<STREAM>(P, slice, xc, c, row2, c2);
+  const int row = psell_slice<STREAM>(P, mu, xc, c, row2, c2);
   if (row < 0) return;
   cor[row] = c;
   x[row] = x[row] + c;
