@@ -1130,18 +1130,24 @@ __global__ void __launch_bounds__(kCta) k_ms_init(int32_t n, const double* __res
 }
 __global__ void __launch_bounds__(128) k_ms_blocks(AsGroups G, const double* __restrict__ cur, double* delta,
                                                    double* xms, const PcgState* st) {
-  pdl_entry();
-  if (pcg_done(st)) return;
-  as_blocks_item<true>(G, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, cur, delta, xms);
+  as_blocks_item<true, RLoad, PdlWait>(G, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, cur, delta,
+                                       xms, PdlWait{});
 }
 // S: the colour's columns of A over the rows they touch (compact row j is
 // row rowmap[j] of A; entries keep A's ascending column order).
 __global__ void __launch_bounds__(kCta) k_ms_update(Sell S, const int32_t* __restrict__ rowmap,
                                                     const double* __restrict__ delta, double* cur,
                                                     const PcgState* st) {
+  const int j = blockIdx.x * kCta + threadIdx.x;
+  if (j < S.n_rows) {  // static layout words into L1 while the predecessor finishes
+    const int64_t base = S.slice_ptr[j >> 5] + (j & 31);
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(S.val + base));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(S.col + base));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(S.rowinfo + j));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(rowmap + j));
+  }
   pdl_entry();
   if (pcg_done(st)) return;
-  const int j = blockIdx.x * kCta + threadIdx.x;
   if (j >= S.n_rows) return;
   const double acc = sell_row<false, 3>(S, j, delta);
   const int i = rowmap[j];
