@@ -24,6 +24,13 @@ __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// Kernels that set a CUDA-graph conditional (the PCG / Richardson IF and
+// WHILE handles) wait but never trigger their dependents early: the node
+// after them may be a conditional node, which must not be evaluated before
+// the value is written (the implicit trigger at grid completion is safe).
+// (Triggering before the wait -- measured as a variant -- let conditional
+// nodes read stale handles: PCG ran to maxit.)
+__device__ __forceinline__ void pdl_wait_only() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // Split form: a kernel first loads what no earlier kernel writes (matrix
 // layouts, block factors and DOF lists, contribution lists -- built once at
 // ig_hier_create), THEN waits for its predecessor, so those loads overlap the
@@ -1447,7 +1454,7 @@ __device__ __forceinline__ void set_conds(cudaGraphConditionalHandle c_if, cudaG
 __global__ void __launch_bounds__(kCta) k_pcg_init(int32_t n, double* r, PcgState* st, double* partials,
                                                    cudaGraphConditionalHandle c_if,
                                                    cudaGraphConditionalHandle c_loop) {
-  pdl_entry();
+  pdl_wait_only();
   double bb;
   const bool last = chunk_reduce(n, [&](int i) {
     const double bi = st->b[i];
@@ -1484,7 +1491,7 @@ __global__ void __launch_bounds__(kCta) k_pcg_update(int32_t n, const double* __
                                                      PcgState* st, double* partials,
                                                      cudaGraphConditionalHandle c_if,
                                                      cudaGraphConditionalHandle c_loop) {
-  pdl_entry();
+  pdl_wait_only();
   if (pcg_stopped(st)) {  // breakdown in the preceding SpMV: x, r stay
     if (blockIdx.x == 0 && threadIdx.x == 0) set_conds(c_if, c_loop, false);
     return;
@@ -1524,7 +1531,7 @@ __global__ void __launch_bounds__(kCta) k_pcg_update(int32_t n, const double* __
 // Init: x = 0, r = b, ||b|| (canonical reduction), the k = 0 test.
 __global__ void __launch_bounds__(kCta) k_rich_init(int32_t n, double* r, PcgState* st, double* partials,
                                                     cudaGraphConditionalHandle c_loop) {
-  pdl_entry();
+  pdl_wait_only();
   double bb;
   const bool last = chunk_reduce(n, [&](int i) {
     const double bi = st->b[i];
@@ -1561,7 +1568,7 @@ __global__ void __launch_bounds__(kCta) k_rich_init(int32_t n, double* r, PcgSta
 __global__ void __launch_bounds__(kCta) k_rich_step(int32_t n, const double* __restrict__ z,
                                                     const double* __restrict__ r, PcgState* st, double* partials,
                                                     cudaGraphConditionalHandle c_loop) {
-  pdl_entry();
+  pdl_wait_only();
   double* x = st->x;
   double rr;
   const bool last = chunk_reduce(n, [&](int i) {

@@ -7,7 +7,7 @@ cd "$(dirname "$0")/../paper_1903_10977_b200"
 for spec in "$@"; do
   name="${spec%%:*}"; flags="${spec#*:}"
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -fmad=false -Xcompiler -fPIC \
-    --expt-relaxed-constexpr -I../include $flags -shared -o "libig_gpu_$name.so" csrc/ig_gpu.cu -lcudart \
+    --expt-relaxed-constexpr -I../include $flags -shared -o "libig_gpu_$name.so" csrc/*.cu -lcudart \
     2> "/tmp/ptxas_$name.log" &
 done
 wait
