@@ -916,9 +916,9 @@ __global__ void IG_AS_BOUNDS k_as_small_simple(AsGroups G, int32_t g_begin, int3
   }
   const int d = (blockIdx.x - n_gctas) * kCta + threadIdx.x;
   if (d >= S.n) return;
-  const int h = S.head[d];  // static: before the predecessor wait
-  if (h < 0) return;
+  const int h = S.head[d];  // static: both loads in flight before the predecessor wait
   const double l = S.sdiag[d];
+  if (h < 0) return;
   pdl_entry();
   const double rd = r[d];
   const double xo = ACC ? x[d] : 0.0;
