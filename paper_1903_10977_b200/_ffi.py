@@ -95,6 +95,7 @@ IG_OPT_FUSED_AS_ROWS = 16
 IG_OPT_L2_ROWS = 18
 IG_OPT_L2_MB = 19
 IG_OPT_FORK_ROWS = 20
+IG_OPT_GAL_SHORT = 21
 
 _host = None
 _gpu = None

@@ -139,6 +139,97 @@ __global__ void __launch_bounds__(32 * kGalWarps) k_gal_fill(GalCsr A, GalCsr B,
   }
 }
 
+// Short-B-row variant (every row of B has <= 32 entries: B = R^T in A R^T,
+// a fine DOF's coarse parents).  The warp first loads 32 entries of row i of
+// A and their B-row bounds in parallel (one lane each), then walks them in
+// ascending order with B row t+1's columns / values already in flight while
+// row t is inserted -- the per-step chain is the shared-memory insert only,
+// not three dependent global loads.  Same per-entry order (k ascending,
+// first product assigned): same bits as k_gal_fill / k_gal_count.
+template <bool FILL>
+__global__ void __launch_bounds__(32 * kGalWarps) k_gal_short(GalCsr A, GalCsr B, int32_t* cnt, const int64_t* cptr,
+                                                             int32_t* ccol, double* cval) {
+  extern __shared__ uint32_t gsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* keys = gsm + w * kGalHS;
+  double* vals = reinterpret_cast<double*>(gsm + kGalWarps * kGalHS) + w * kGalHS;
+  uint32_t* ck = gsm + kGalWarps * kGalHS * 3 + w * kGalLoad;
+  double* cv = reinterpret_cast<double*>(gsm + kGalWarps * kGalHS * 3 + kGalWarps * kGalLoad) + w * kGalLoad;
+  const int row = blockIdx.x * kGalWarps + w;
+  if (row >= A.n_rows) return;
+  for (int s = lane; s < kGalHS; s += 32) keys[s] = kGalEmpty;
+  __syncwarp();
+  const int32_t a0 = A.ptr[row], a1 = A.ptr[row + 1];
+  int n = 0;
+  bool full = false;
+  for (int32_t c0 = a0; c0 < a1; c0 += 32) {
+    const int32_t t = c0 + lane;
+    const int32_t k = t < a1 ? A.col[t] : 0;
+    const double av = (FILL && t < a1) ? A.val[t] : 0.0;
+    const int32_t q0 = t < a1 ? B.ptr[k] : 0;
+    const int32_t q1 = t < a1 ? B.ptr[k + 1] : 0;
+    const int steps = min(32, a1 - c0);
+    // Step j's B entries, one per lane: prefetched one step ahead.
+    int32_t nb0 = __shfl_sync(0xffffffffu, q0, 0), ne0 = __shfl_sync(0xffffffffu, q1, 0);
+    int32_t bc = nb0 + lane < ne0 ? B.col[nb0 + lane] : 0;
+    double bv = (FILL && nb0 + lane < ne0) ? B.val[nb0 + lane] : 0.0;
+    for (int j = 0; j < steps; ++j) {
+      const int32_t b0 = nb0, b1 = ne0;
+      const int32_t cc = bc;
+      const double cvv = bv;
+      const double a = __shfl_sync(0xffffffffu, av, j);
+      if (j + 1 < steps) {
+        nb0 = __shfl_sync(0xffffffffu, q0, j + 1);
+        ne0 = __shfl_sync(0xffffffffu, q1, j + 1);
+        bc = nb0 + lane < ne0 ? B.col[nb0 + lane] : 0;
+        if (FILL) bv = nb0 + lane < ne0 ? B.val[nb0 + lane] : 0.0;
+      }
+      if (b0 + lane < b1) {
+        bool fresh;
+        const int s = gal_insert(keys, static_cast<uint32_t>(cc), fresh);
+        if (s < 0) {
+          full = true;
+        } else {
+          n += fresh ? 1 : 0;
+          if (FILL) {
+            const double prod = a * cvv;
+            vals[s] = fresh ? prod : vals[s] + prod;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (!FILL) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    full = __any_sync(0xffffffffu, full);
+    if (lane == 0) cnt[row] = (full || n > kGalLoad) ? kGalLoad + 1 : n;
+    return;
+  }
+  int base = 0;
+  for (int s0 = 0; s0 < kGalHS; s0 += 32) {
+    const uint32_t kk = keys[s0 + lane];
+    const bool used = kk != kGalEmpty;
+    const unsigned m = __ballot_sync(0xffffffffu, used);
+    if (used) {
+      const int pos = base + __popc(m & ((1u << lane) - 1u));
+      ck[pos] = kk;
+      cv[pos] = vals[s0 + lane];
+    }
+    base += __popc(m);
+  }
+  __syncwarp();
+  const int64_t o = cptr[row];
+  for (int e = lane; e < base; e += 32) {
+    const uint32_t key = ck[e];
+    int rank = 0;
+    for (int f = 0; f < base; ++f) rank += ck[f] < key ? 1 : 0;
+    ccol[o + rank] = static_cast<int32_t>(key);
+    cval[o + rank] = cv[e];
+  }
+}
+
 constexpr size_t kGalFillSmem =
     static_cast<size_t>(kGalWarps) * (kGalHS * (4 + 8) + kGalLoad * (4 + 8));
 constexpr size_t kGalCountSmem = static_cast<size_t>(kGalWarps) * kGalHS * 4;

@@ -260,6 +260,7 @@ int g_psell_ctas = 0;
 // + arrival + wait sits on the critical path of every application.
 int32_t g_fused_rows = 0;
 int32_t g_fork_rows = 0;  // IG_OPT_FORK_ROWS
+int g_gal_short = 1;      // IG_OPT_GAL_SHORT: prefetching SpGEMM for B rows <= 32 entries
 // Levels below the finest with at most this many DOFs live in the L2-persisting
 // arena (ig_hier::alloc); 0 = off.  Arena size g_l2_bytes.
 // Measured (profiles/option_sweep.py 18/19): C4 V-cycle 903 -> 881 us, C3
@@ -1801,6 +1802,10 @@ int ig_set_option(int32_t option, int64_t value) {
     g_red_ctas = static_cast<int>(value);
     return IG_OK;
   }
+  if (option == IG_OPT_GAL_SHORT) {
+    g_gal_short = value != 0;
+    return IG_OK;
+  }
   if (option == IG_OPT_FORK_ROWS) {
     if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: fork rows out of range");
     g_fork_rows = static_cast<int32_t>(value);
@@ -2544,7 +2549,22 @@ GalMat gal_spgemm(const GalMat& a, const GalMat& b, cudaStream_t st) {
   int64_t* off = dmalloc<int64_t>(static_cast<size_t>(c.nr) + 1);
   c.ptr = dmalloc<int32_t>(static_cast<size_t>(c.nr) + 1);
   const unsigned g = static_cast<unsigned>((c.nr + kGalWarps - 1) / kGalWarps);
-  if (g) k_gal_count<<<g, 32 * kGalWarps, kGalCountSmem, st>>>(a.view(), b.view(), cnt);
+  // B rows of at most 32 entries (R^T): the prefetching kernel.
+  int32_t bmax = 0;
+  {
+    std::vector<int32_t> bp(static_cast<size_t>(b.nr) + 1);
+    CK(cudaMemcpyAsync(bp.data(), b.ptr, sizeof(int32_t) * (b.nr + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int32_t i = 0; i < b.nr; ++i) bmax = std::max(bmax, bp[i + 1] - bp[i]);
+  }
+  const bool shortb = bmax <= 32 && g_gal_short;
+  if (shortb) {
+    CK(cudaFuncSetAttribute(k_gal_short<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGalFillSmem)));
+    CK(cudaFuncSetAttribute(k_gal_short<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGalFillSmem)));
+    if (g) k_gal_short<false><<<g, 32 * kGalWarps, kGalCountSmem, st>>>(a.view(), b.view(), cnt, nullptr, nullptr, nullptr);
+  } else if (g) {
+    k_gal_count<<<g, 32 * kGalWarps, kGalCountSmem, st>>>(a.view(), b.view(), cnt);
+  }
   CK(cudaGetLastError());
   // Rows that do not fit the per-warp table: fail loudly.
   {
@@ -2560,7 +2580,10 @@ GalMat gal_spgemm(const GalMat& a, const GalMat& b, cudaStream_t st) {
   c.nnz = gal_offsets(c.nr, cnt, off, c.ptr, st);
   c.col = dmalloc<int32_t>(static_cast<size_t>(c.nnz));
   c.val = dmalloc<double>(static_cast<size_t>(c.nnz));
-  if (g) k_gal_fill<<<g, 32 * kGalWarps, kGalFillSmem, st>>>(a.view(), b.view(), off, c.col, c.val);
+  if (g && shortb)
+    k_gal_short<true><<<g, 32 * kGalWarps, kGalFillSmem, st>>>(a.view(), b.view(), nullptr, off, c.col, c.val);
+  else if (g)
+    k_gal_fill<<<g, 32 * kGalWarps, kGalFillSmem, st>>>(a.view(), b.view(), off, c.col, c.val);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
   cudaFree(cnt);

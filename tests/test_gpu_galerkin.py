@@ -55,3 +55,16 @@ def test_galerkin_rejects_mismatched_restriction(c1_case):
     R[1], R[2] = R[2], R[1]
     with pytest.raises(ValueError):
         galerkin_hierarchy(c1_case.level_A(L - 1), R)
+
+
+@pytest.mark.parametrize("short", [0, 1])
+def test_galerkin_kernel_paths_bitwise(d3_case, short):
+    """Both SpGEMM paths (the prefetching short-B-row kernel and the general
+    one, IG_OPT_GAL_SHORT) give the host's coarse operators bit for bit."""
+    from paper_1903_10977_b200 import _ffi
+    lib = _ffi.gpu()
+    lib.ig_set_option(_ffi.IG_OPT_GAL_SHORT, short)
+    try:
+        _check(d3_case)
+    finally:
+        lib.ig_set_option(_ffi.IG_OPT_GAL_SHORT, 1)
