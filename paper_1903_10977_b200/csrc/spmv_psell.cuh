@@ -117,6 +117,26 @@ __device__ __forceinline__ void fast2_dispatch(const double* __restrict__ x, int
   }
 }
 
+// The rows this lane will own in a slice (psell_slice's mapping), from the
+// static metadata: lets a kernel issue its per-row loads (residual source,
+// the x being corrected) ahead of the slice's product chain.
+__device__ __forceinline__ void psell_rows(const PSell& A, const uint4 mu, int& row, int& row2) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t pk = mu.w;
+  const int count = static_cast<int>((pk >> 11) & 0x3f);
+  row = -1;
+  row2 = -1;
+  if (count == 0 || lane >= count) return;
+  if ((pk & (1u << 17)) && ((pk >> 19) & 0x3f) == 1) {
+    row = static_cast<int>(mu.x) + 2 * lane;
+    row2 = row + 1;
+  } else if (pk & (1u << 17)) {
+    row = static_cast<int>(mu.x) + lane;
+  } else {
+    row = __ldg(A.rlist + mu.x + lane);
+  }
+}
+
 // One warp, one slice.  Returns the row this lane owns (-1: none) and its
 // sum; FAST2 slices give each lane a second row (row2 / acc2, else -1).
 template <bool STREAM>
@@ -239,14 +259,19 @@ __global__ void __launch_bounds__(kCta, IG_PSPMV_MINB) k_pspmv(PSell A, const do
                                                const double* rsrc, const PcgState* st) {
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(A.meta + slice));  // static: before the wait
+  int pr, pr2;
+  psell_rows(A, mu, pr, pr2);
   pdl_entry();
   if (pcg_done(st)) return;
+  // The residual source is loaded before the product chain, not after it.
+  const double r1 = (MODE == 1 && pr >= 0) ? rsrc[pr] : 0.0;
+  const double r2 = (MODE == 1 && pr2 >= 0) ? rsrc[pr2] : 0.0;
   double acc, acc2;
   int row2;
   const int row = psell_slice<STREAM>(A, mu, x, acc, row2, acc2);
   if (row < 0) return;
-  y[row] = (MODE == 0) ? acc : rsrc[row] - acc;
-  if (row2 >= 0) y[row2] = (MODE == 0) ? acc2 : rsrc[row2] - acc2;
+  y[row] = (MODE == 0) ? acc : r1 - acc;
+  if (row2 >= 0) y[row2] = (MODE == 0) ? acc2 : r2 - acc2;
 }
 
 // p . Ap over the canonical 256-row chunks (kernels.cuh: last_cta_total), then
@@ -275,17 +300,22 @@ __global__ void __launch_bounds__(kCta, IG_PPROLONG_MINB) k_pprolong(PSell P, co
                                                   const PcgState* st) {
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(P.meta + slice));  // static: before the wait
+  int pr, pr2;
+  psell_rows(P, mu, pr, pr2);
   pdl_entry();
   if (pcg_done(st)) return;
+  // The x being corrected is loaded before the product chain, not after it.
+  const double x1 = pr >= 0 ? x[pr] : 0.0;
+  const double x2 = pr2 >= 0 ? x[pr2] : 0.0;
   double c, c2;
   int row2;
   const int row = psell_slice<STREAM>(P, mu, xc, c, row2, c2);
   if (row < 0) return;
   cor[row] = c;
-  x[row] = x[row] + c;
+  x[row] = x1 + c;
   if (row2 >= 0) {
     cor[row2] = c2;
-    x[row2] = x[row2] + c2;
+    x[row2] = x2 + c2;
   }
 }
 
