@@ -454,6 +454,8 @@ __device__ __forceinline__ void spmv_grp_item(const Sell& A, int t, const double
   // round trip instead of U (the small levels are latency-bound).
   constexpr int U = 16;
   double acc = 0.0;
+  double rs = 0.0;
+  bool have_rs = false;
   for (int k0 = 0; k0 < wlen; k0 += G * U) {
     double v[U];
     int32_t c[U];
@@ -467,7 +469,13 @@ __device__ __forceinline__ void spmv_grp_item(const Sell& A, int t, const double
         c[u] = od ? row + __ldg(dc + k) : __ldg(A.col + base + static_cast<int64_t>(k) * kSell);
       }
     }
-    if (pdl && k0 == 0) pdl_entry();  // values / columns are static: loaded before the predecessor wait
+    if (pdl && k0 == 0) {
+      pdl_entry();  // values / columns are static: loaded before the predecessor wait
+      if (MODE == 1 && valid_row && g == 0) {
+        rs = rsrc[row];  // ahead of the product chain
+        have_rs = true;
+      }
+    }
     double prod[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) prod[u] = (k0 + u * G + g < len) ? v[u] * __ldg(x + c[u]) : 0.0;
@@ -483,7 +491,8 @@ __device__ __forceinline__ void spmv_grp_item(const Sell& A, int t, const double
     }
   }
   if (pdl && wlen == 0) pdl_entry();
-  if (valid_row && g == 0) y[row] = (MODE == 0) ? acc : rsrc[row] - acc;
+  if (MODE == 1 && valid_row && g == 0 && !have_rs) rs = rsrc[row];
+  if (valid_row && g == 0) y[row] = (MODE == 0) ? acc : rs - acc;
 }
 template <int MODE, int G>
 __global__ void IG_GRP_BOUNDS k_spmv_grp(Sell A, const double* __restrict__ x, double* y,
@@ -507,9 +516,10 @@ __global__ void __launch_bounds__(kCta, SpmvVar<VAR>::MINB) k_prolong(Sell P, co
   pdl_entry();
   if (pcg_done(st)) return;
   if (row >= P.n_rows) return;
+  const double xo = x[row];  // ahead of the product chain
   const double c = sell_row<STREAM, VAR>(P, row, xc);
   cor[row] = c;
-  x[row] = x[row] + c;
+  x[row] = xo + c;
 }
 
 // ------------------------------------------------- exact division ---------
@@ -954,6 +964,7 @@ __global__ void IG_AS_BOUNDS k_as_complex(AsGather S, const double* __restrict__
   for (int u = 0; u < U; ++u) ls[u] = (q0 + u < q1 && code[u] < 0) ? S.sval[-code[u] - 1] : 1.0;
   pdl_entry();
   const double rd = r[d];
+  const double xo = ACC ? x[d] : 0.0;  // ahead of the list sum
   double v[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) v[u] = (q0 + u < q1) ? (code[u] < 0 ? (rd / ls[u]) / ls[u] : ybuf[code[u]]) : 0.0;
@@ -984,7 +995,7 @@ __global__ void IG_AS_BOUNDS k_as_complex(AsGather S, const double* __restrict__
       if (qb + u < q1) acc = acc + w[u];
   }
   const double out = S.gamma * acc;
-  x[d] = ACC ? x[d] + out : out;
+  x[d] = ACC ? xo + out : out;
 }
 
 // ---------------------------------------------- fused additive smoother ----
