@@ -252,6 +252,7 @@ int g_psell_pairs = 1;  // FAST slices with two rows per lane (x reuse across a 
 // decide), applied as unused dynamic shared memory: fewer resident warps keep
 // more of each warp's x lines in L1 (the gathers are L1-hit-rate bound).
 int g_psell_ctas = 0;
+int g_psell_ctab = 1;  // IG_OPT_PSELL_CTAB: FAST2 value sequences from a constant-bank table
 // Levels with at most this many DOFs run the additive smoother as one fused
 // kernel (kernels.cuh k_as_fused) instead of the fork/join split.  Off by
 // default: measured slower on every workload (C2 V-cycle 228 -> 272 us, C4
@@ -286,6 +287,8 @@ struct HostPSell {
   int32_t smul = 1, sshift = 0;
   int64_t layout_bytes = 0;  // matrix words read from HBM per product (shared sequences once)
   int64_t n_fast = 0, n_general = 0, fast_rows = 0;
+  std::vector<double> tab;   // constant-bank value table (spmv_psell.cuh PValTab)
+  int64_t tab_rows = 0;      // rows whose FAST2 values come from the table
 };
 
 // Host-side data-parallel loop over [0, n) in contiguous ranges (layout
@@ -580,6 +583,39 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
   }
   if (!pending.empty()) emit_general(pending);
   if (s.V.size() > 0xF0000000ull || s.O.size() > 0xF0000000ull) return false;
+  // Constant-bank value table: the FAST2 value sequences covering the most
+  // rows, as long as they fit (kPValTab doubles); their slices read values
+  // from the kernel-parameter table instead of V (pk bit 31, vbase = offset).
+  if (g_psell_ctab) {
+    std::unordered_map<uint32_t, std::pair<int64_t, int32_t>> use;  // vbase -> (rows, length)
+    for (const PSliceMeta& m : s.meta)
+      if ((m.pk & (1u << 17)) && ((m.pk >> 19) & 0x3f) == 1) {
+        auto& u = use[m.vbase];
+        u.first += 2 * static_cast<int64_t>((m.pk >> 11) & 0x3f);
+        u.second = static_cast<int32_t>(m.pk & kPMaxLen);
+      }
+    std::vector<std::pair<int64_t, uint32_t>> order;
+    for (const auto& [vb, u] : use) order.push_back({u.first, vb});
+    std::sort(order.begin(), order.end(), [](const auto& x, const auto& y) {
+      return x.first != y.first ? x.first > y.first : x.second < y.second;
+    });
+    std::unordered_map<uint32_t, uint32_t> toff;
+    for (const auto& [rows, vb] : order) {
+      const int32_t L = use[vb].second;
+      if (static_cast<int64_t>(s.tab.size()) + L > kPValTab) continue;
+      toff[vb] = static_cast<uint32_t>(s.tab.size());
+      s.tab.insert(s.tab.end(), s.V.begin() + vb, s.V.begin() + vb + L);
+      s.tab_rows += rows;
+    }
+    for (PSliceMeta& m : s.meta)
+      if ((m.pk & (1u << 17)) && ((m.pk >> 19) & 0x3f) == 1) {
+        auto it = toff.find(m.vbase);
+        if (it != toff.end()) {
+          m.vbase = it->second;
+          m.pk |= 1u << 31;
+        }
+      }
+  }
   // Pad to whole CTAs (count 0 = empty slice); dictionary rows of GENERAL
   // slices read up to the slice's padded length past their start.
   while (s.meta.size() % (kCta / 32) != 0 || s.meta.empty()) s.meta.push_back(PSliceMeta{0, 0, 0, 0});
@@ -618,6 +654,7 @@ struct DevSell {
   int64_t t_bytes = 0;  // matrix bytes of the compact layout (cols + vals)
   bool has_p = false;   // pattern-SELL layout present (spmv_psell.cuh)
   PSell p{};
+  std::shared_ptr<PValTab> ptab;  // constant-bank value table (zeros when unused)
   int64_t p_bytes = 0;  // HostPSell::layout_bytes
   int64_t n_fast = 0, n_general = 0;
   int64_t layout_matrix_bytes() const { return has_p ? p_bytes : 8 * explicit_vals + 4 * explicit_cols + 4 * int64_t(s.n_rows); }
@@ -855,6 +892,13 @@ struct ig_hier {
         d.p.V = upload(hp.V.data(), hp.V.size());
         d.p.O = upload(hp.O.data(), hp.O.size());
         d.p.dict_w = hp.dict_w;
+        d.ptab = std::make_shared<PValTab>();
+        std::memset(d.ptab.get(), 0, sizeof(PValTab));
+        std::copy(hp.tab.begin(), hp.tab.end(), d.ptab->v);
+        if (std::getenv("IG_TIMING"))
+          std::fprintf(stderr, "[psell] %d x %d: %lld fast / %lld general slices, value table %zu doubles (%lld rows)\n",
+                       nr, nc, static_cast<long long>(hp.n_fast), static_cast<long long>(hp.n_general), hp.tab.size(),
+                       static_cast<long long>(hp.tab_rows));
         d.p_bytes = hp.layout_bytes;
         d.n_fast = hp.n_fast;
         d.n_general = hp.n_general;
@@ -897,12 +941,13 @@ struct ig_hier {
     if (A.has_p) {
       const unsigned gp = static_cast<unsigned>(A.p.n_slices / (kCta / 32));
       const size_t sm = psell_smem();
+      const PValTab& tb = *A.ptab;
       if (mode == 0) {
-        if (A.stream) launch(k_pspmv<0, true>, gp, kCta, sm, stream, A.p, x, y, rsrc, s);
-        else launch(k_pspmv<0, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s);
+        if (A.stream) launch(k_pspmv<0, true>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
+        else launch(k_pspmv<0, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
       } else {
-        if (A.stream) launch(k_pspmv<1, true>, gp, kCta, sm, stream, A.p, x, y, rsrc, s);
-        else launch(k_pspmv<1, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s);
+        if (A.stream) launch(k_pspmv<1, true>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
+        else launch(k_pspmv<1, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
       }
       CK(cudaGetLastError());
       if (red) {  // p . Ap over the canonical chunks, alpha / Breakdown
@@ -964,8 +1009,8 @@ struct ig_hier {
     if (l.P.has_p) {
       const unsigned gp = static_cast<unsigned>(l.P.p.n_slices / (kCta / 32));
       const size_t sm = psell_smem();
-      if (l.P.stream) launch(k_pprolong<true>, gp, kCta, sm, stream, l.P.p, xc, l.cor, x, s);
-      else launch(k_pprolong<false>, gp, kCta, sm, stream, l.P.p, xc, l.cor, x, s);
+      if (l.P.stream) launch(k_pprolong<true>, gp, kCta, sm, stream, l.P.p, xc, l.cor, x, s, *l.P.ptab);
+      else launch(k_pprolong<false>, gp, kCta, sm, stream, l.P.p, xc, l.cor, x, s, *l.P.ptab);
       CK(cudaGetLastError());
       return;
     }
@@ -1802,6 +1847,10 @@ int ig_set_option(int32_t option, int64_t value) {
     g_red_ctas = static_cast<int>(value);
     return IG_OK;
   }
+  if (option == IG_OPT_PSELL_CTAB) {
+    g_psell_ctab = value != 0;
+    return IG_OK;
+  }
   if (option == IG_OPT_GAL_SHORT) {
     g_gal_short = value != 0;
     return IG_OK;
@@ -1830,7 +1879,7 @@ int ig_set_option(int32_t option, int64_t value) {
     if (value < 0 || value > 8) return fail(IG_INVALID_ARGUMENT, "ig_set_option: pattern-SELL CTAs per SM in 0..8");
     g_psell_ctas = static_cast<int>(value);
     const int sm = static_cast<int>(psell_smem());
-    void (*ks[])(PSell, const double*, double*, const double*, const PcgState*) = {
+    void (*ks[])(PSell, const double*, double*, const double*, const PcgState*, const PValTab) = {
         k_pspmv<0, true>, k_pspmv<0, false>, k_pspmv<1, true>, k_pspmv<1, false>};
     for (auto k : ks) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_pprolong<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);

@@ -42,6 +42,7 @@
 namespace igk {
 
 // pk: lmax (11 bits) | count << 11 (6) | fast << 17 | ulen << 18 | wv << 19 (6) | wo << 25 (6)
+//     | FAST2 values in the constant-bank table << 31 (vbase = table offset)
 struct PSliceMeta {
   uint32_t a;      // FAST: first row; GENERAL: index of the slice's entries in rlist/ginfo
   uint32_t vbase;  // FAST: value sequence; GENERAL: value table
@@ -102,6 +103,57 @@ __device__ __forceinline__ void fast2_segment(const double* __restrict__ x, int 
     acc1 = acc1 + v[j] * X[P + j + 1];
   }
 }
+// Constant-bank value table (a __grid_constant__ kernel parameter): the most
+// frequent FAST2 value sequences of the matrix (the interior stencils).  A
+// warp-uniform indexed read of a kernel parameter is a constant-cache load
+// (LDC / uniform datapath), not an L1TEX request -- and the L1 data pipe is
+// what bounds this kernel (the per-run value loads were ~1/4 of its
+// wavefronts).  FAST2 slices whose sequence is in the table carry pk bit 31
+// and vbase = table offset.
+constexpr int kPValTab = 1024;  // doubles (8 KB of kernel parameters; 32 KB measured: same graph time, but a direct launch then costs ~20 us)
+struct PValTab {
+  double v[kPValTab];
+};
+template <int P, int M>
+__device__ __forceinline__ void fast2_segment_tab(const double* __restrict__ x, int a, const PValTab& tab, int vo,
+                                                  double& acc0, double& acc1) {
+  constexpr int C = M + 1 + P;
+  const double* xb = x + (a - P);
+  const double2* xb2 = reinterpret_cast<const double2*>(xb);
+  double X[C + 1], v[M];
+#pragma unroll
+  for (int q = 0; 2 * q < C; ++q) {
+    if (2 * q + 1 < C) {
+      const double2 t = __ldg(xb2 + q);
+      X[2 * q] = t.x;
+      X[2 * q + 1] = t.y;
+    } else {
+      X[2 * q] = __ldg(xb + 2 * q);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < M; ++j) v[j] = tab.v[vo + j];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    acc0 = acc0 + v[j] * X[P + j];
+    acc1 = acc1 + v[j] * X[P + j + 1];
+  }
+}
+template <int P>
+__device__ __forceinline__ void fast2_dispatch_tab(const double* __restrict__ x, int a, int m, const PValTab& tab,
+                                                   int vo, double& acc0, double& acc1) {
+  switch (m) {  // warp-uniform
+    case 1: fast2_segment_tab<P, 1>(x, a, tab, vo, acc0, acc1); break;
+    case 2: fast2_segment_tab<P, 2>(x, a, tab, vo, acc0, acc1); break;
+    case 3: fast2_segment_tab<P, 3>(x, a, tab, vo, acc0, acc1); break;
+    case 4: fast2_segment_tab<P, 4>(x, a, tab, vo, acc0, acc1); break;
+    case 5: fast2_segment_tab<P, 5>(x, a, tab, vo, acc0, acc1); break;
+    case 6: fast2_segment_tab<P, 6>(x, a, tab, vo, acc0, acc1); break;
+    case 7: fast2_segment_tab<P, 7>(x, a, tab, vo, acc0, acc1); break;
+    default: fast2_segment_tab<P, 8>(x, a, tab, vo, acc0, acc1); break;
+  }
+}
+
 template <int P>
 __device__ __forceinline__ void fast2_dispatch(const double* __restrict__ x, int a, int m,
                                                const double* __restrict__ vp, double& acc0, double& acc1) {
@@ -141,7 +193,7 @@ __device__ __forceinline__ void psell_rows(const PSell& A, const uint4 mu, int& 
 // sum; FAST2 slices give each lane a second row (row2 / acc2, else -1).
 template <bool STREAM>
 __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const double* __restrict__ x, double& acc,
-                                           int& row2, double& acc2) {
+                                           int& row2, double& acc2, const PValTab* tab = nullptr) {
   acc = 0.0;
   acc2 = 0.0;
   row2 = -1;
@@ -155,6 +207,21 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
     const int ra = static_cast<int>(mu.x) + 2 * cl;
     const double* vp = A.V + mu.y;
     const int p0 = static_cast<int>(mu.x) & 1;
+    if (tab != nullptr && (pk >> 31)) {  // values from the constant-bank table (warp-uniform branch)
+      int vo = static_cast<int>(mu.y);
+      for (const int2* sg = A.seg + mu.z;; ++sg) {
+        const int2 e = __ldg(sg);
+        if (e.y == 0) break;
+        if (((p0 + e.x) & 1) == 0)
+          fast2_dispatch_tab<0>(x, ra + e.x, e.y, *tab, vo, acc, acc2);
+        else
+          fast2_dispatch_tab<1>(x, ra + e.x, e.y, *tab, vo, acc, acc2);
+        vo += e.y;
+      }
+      if (lane >= count) return -1;
+      row2 = ra + 1;
+      return ra;
+    }
     for (const int2* sg = A.seg + mu.z;; ++sg) {
       const int2 e = __ldg(sg);
       if (e.y == 0) break;
@@ -256,7 +323,8 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
 #endif
 template <int MODE, bool STREAM>
 __global__ void __launch_bounds__(kCta, IG_PSPMV_MINB) k_pspmv(PSell A, const double* __restrict__ x, double* y,
-                                               const double* rsrc, const PcgState* st) {
+                                               const double* rsrc, const PcgState* st,
+                                               const __grid_constant__ PValTab tab) {
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(A.meta + slice));  // static: before the wait
   int pr, pr2;
@@ -268,7 +336,7 @@ __global__ void __launch_bounds__(kCta, IG_PSPMV_MINB) k_pspmv(PSell A, const do
   const double r2 = (MODE == 1 && pr2 >= 0) ? rsrc[pr2] : 0.0;
   double acc, acc2;
   int row2;
-  const int row = psell_slice<STREAM>(A, mu, x, acc, row2, acc2);
+  const int row = psell_slice<STREAM>(A, mu, x, acc, row2, acc2, &tab);
   if (row < 0) return;
   y[row] = (MODE == 0) ? acc : r1 - acc;
   if (row2 >= 0) y[row2] = (MODE == 0) ? acc2 : r2 - acc2;
@@ -297,7 +365,7 @@ __global__ void __launch_bounds__(kCta) k_pap(int n, const double* __restrict__ 
 // Prolongation fused with the correction (k_prolong on the pattern layout).
 template <bool STREAM>
 __global__ void __launch_bounds__(kCta, IG_PPROLONG_MINB) k_pprolong(PSell P, const double* __restrict__ xc, double* cor, double* x,
-                                                  const PcgState* st) {
+                                                  const PcgState* st, const __grid_constant__ PValTab tab) {
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(P.meta + slice));  // static: before the wait
   int pr, pr2;
@@ -309,7 +377,7 @@ __global__ void __launch_bounds__(kCta, IG_PPROLONG_MINB) k_pprolong(PSell P, co
   const double x2 = pr2 >= 0 ? x[pr2] : 0.0;
   double c, c2;
   int row2;
-  const int row = psell_slice<STREAM>(P, mu, xc, c, row2, c2);
+  const int row = psell_slice<STREAM>(P, mu, xc, c, row2, c2, &tab);
   if (row < 0) return;
   cor[row] = c;
   x[row] = x1 + c;

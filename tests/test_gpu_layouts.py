@@ -165,3 +165,34 @@ def test_fused_smoother_bitwise(request, case_name):
         assert np.array_equal(np.array(rep.residuals), ro) and np.array_equal(x, xo)
     finally:
         h.close()
+
+
+@pytest.mark.parametrize("ctab", [0, 1])
+def test_constant_value_table_bitwise(ctab):
+    """FAST2 value sequences read from the constant-bank kernel-parameter table
+    (IG_OPT_PSELL_CTAB) or from HBM give the same bits -- on a THB hierarchy,
+    whose prolongation operators also carry FAST2 slices (pattern layout
+    forced on every level)."""
+    from paper_1903_10977_b200 import MgHierarchy, _ffi, build_case, configs, pcg
+    lib = _ffi.gpu()
+    case = build_case(configs.c5(base=64, levels=4))
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_CTAB, ctab)
+    lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 0)
+    try:
+        h = MgHierarchy(case)
+    finally:
+        lib.ig_set_option(_ffi.IG_OPT_PSELL_CTAB, 1)
+        lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
+    lv = case.levels_c()
+    try:
+        for l in range(1, h.levels()):
+            A, R = h.level(l)
+            x = rng_vec(170 + l, A.cols())
+            assert np.array_equal(h.spmv(l, x, 0), orc.spmv(lv, l, x, 0))
+            xc = rng_vec(190 + l, R.rows())
+            assert np.array_equal(h.spmv(l, xc, 3), orc.spmv(lv, l, xc, 3))
+        x, rep = pcg(h.A, case.b, h, tol=1e-8, maxit=1000)
+        st, xo, ro, it, _ = orc.pcg(lv, case.b, tol=1e-8, maxit=1000, mode=orc.GPU_ORDER)
+        assert st == 0 and rep.iterations == it and np.array_equal(x, xo)
+    finally:
+        h.close()
