@@ -583,15 +583,19 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
   }
   if (!pending.empty()) emit_general(pending);
   if (s.V.size() > 0xF0000000ull || s.O.size() > 0xF0000000ull) return false;
-  // Constant-bank value table: the FAST2 value sequences covering the most
-  // rows, as long as they fit (kPValTab doubles); their slices read values
-  // from the kernel-parameter table instead of V (pk bit 31, vbase = offset).
+  // Constant-bank value table: the FAST / FAST2 value sequences covering the
+  // most rows, as long as they fit (kPValTab doubles); their slices read
+  // values from the kernel-parameter table instead of V (pk bit 31, vbase =
+  // table offset).
   if (g_psell_ctab) {
+    // FAST2 (rows = 2 x count) and FAST (rows = count) slices compete for the
+    // table by the rows they cover; both read V[vbase ..] otherwise.
     std::unordered_map<uint32_t, std::pair<int64_t, int32_t>> use;  // vbase -> (rows, length)
     for (const PSliceMeta& m : s.meta)
-      if ((m.pk & (1u << 17)) && ((m.pk >> 19) & 0x3f) == 1) {
+      if (m.pk & (1u << 17)) {
+        const bool f2 = ((m.pk >> 19) & 0x3f) == 1;
         auto& u = use[m.vbase];
-        u.first += 2 * static_cast<int64_t>((m.pk >> 11) & 0x3f);
+        u.first += (f2 ? 2 : 1) * static_cast<int64_t>((m.pk >> 11) & 0x3f);
         u.second = static_cast<int32_t>(m.pk & kPMaxLen);
       }
     std::vector<std::pair<int64_t, uint32_t>> order;
@@ -608,7 +612,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       s.tab_rows += rows;
     }
     for (PSliceMeta& m : s.meta)
-      if ((m.pk & (1u << 17)) && ((m.pk >> 19) & 0x3f) == 1) {
+      if (m.pk & (1u << 17)) {
         auto it = toff.find(m.vbase);
         if (it != toff.end()) {
           m.vbase = it->second;

@@ -235,6 +235,28 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
     row2 = ra + 1;
     return ra;
   }
+  if ((pk & (1u << 17)) && tab != nullptr && (pk >> 31)) {  // FAST, values from the constant-bank table
+    const int row = static_cast<int>(mu.x) + cl;
+    const double* xr = x + ((row * A.smul) >> A.sshift);
+    const int vo = static_cast<int>(mu.y);
+    const int4* op4 = reinterpret_cast<const int4*>(A.O + mu.z);
+    int k = 0;
+    for (; k + 8 <= L; k += 8) {
+      const int4 b0 = __ldg(op4 + (k >> 2)), b1 = __ldg(op4 + (k >> 2) + 1);
+      const double x0 = __ldg(xr + b0.x), x1 = __ldg(xr + b0.y), x2 = __ldg(xr + b0.z), x3 = __ldg(xr + b0.w);
+      const double x4 = __ldg(xr + b1.x), x5 = __ldg(xr + b1.y), x6 = __ldg(xr + b1.z), x7 = __ldg(xr + b1.w);
+      acc = acc + tab->v[vo + k] * x0;
+      acc = acc + tab->v[vo + k + 1] * x1;
+      acc = acc + tab->v[vo + k + 2] * x2;
+      acc = acc + tab->v[vo + k + 3] * x3;
+      acc = acc + tab->v[vo + k + 4] * x4;
+      acc = acc + tab->v[vo + k + 5] * x5;
+      acc = acc + tab->v[vo + k + 6] * x6;
+      acc = acc + tab->v[vo + k + 7] * x7;
+    }
+    for (; k < L; ++k) acc = acc + tab->v[vo + k] * __ldg(xr + __ldg(A.O + mu.z + k));
+    return lane < count ? row : -1;
+  }
   if (pk & (1u << 17)) {                // FAST (warp-uniform branch)
     const int row = static_cast<int>(mu.x) + cl;
     const double* xr = x + ((row * A.smul) >> A.sshift);
