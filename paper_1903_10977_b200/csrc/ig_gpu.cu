@@ -261,6 +261,7 @@ int g_psell_ctab = 1;  // IG_OPT_PSELL_CTAB: FAST2 value sequences from a consta
 // + arrival + wait sits on the critical path of every application.
 int32_t g_fused_rows = 0;
 int32_t g_fork_rows = 0;  // IG_OPT_FORK_ROWS
+int32_t g_cluster_rows = 0;  // IG_OPT_CLUSTER_AS_ROWS: smoother levels up to this size run k_as_cluster
 int g_gal_short = 1;      // IG_OPT_GAL_SHORT: prefetching SpGEMM for B rows <= 32 entries
 // Levels below the finest with at most this many DOFs live in the L2-persisting
 // arena (ig_hier::alloc); 0 = off.  Arena size g_l2_bytes.
@@ -782,6 +783,7 @@ struct ig_hier {
   unsigned int* fused_ctr = nullptr;  // k_as_fused arrival counters (2)
   unsigned fused_cap = 0;             // co-resident CTAs of k_as_fused (occupancy x SMs)
   int32_t fused_rows = 0;             // levels with n <= this use k_as_fused
+  int32_t cluster_rows = 0;           // levels with n <= this use k_as_cluster
   double* residuals = nullptr;
   int32_t res_cap = 0;
   double *r = nullptr, *z = nullptr, *p = nullptr, *ap = nullptr;
@@ -1033,6 +1035,26 @@ struct ig_hier {
   void smoother(const Level& l, const double* r, double* x, bool acc, PcgState* s, const double* rdot, int dir = -1) {
     if (l.ms) {
       ms_smoother(l, r, x, acc, s, rdot, dir < 0 ? (acc ? 1 : 0) : dir);
+      return;
+    }
+    if (l.n <= cluster_rows && !rdot) {  // small level: one cluster kernel (k_as_cluster)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(kAsClusterCtas);
+      cfg.blockDim = dim3(kAsClusterThreads);
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = kAsClusterCtas;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[1].val.programmaticStreamSerializationAllowed = g_use_pdl ? 1 : 0;
+      cfg.attrs = attr;
+      cfg.numAttrs = 2;
+      if (acc)
+        CK(cudaLaunchKernelEx(&cfg, k_as_cluster<true>, l.G, l.S, r, l.ybuf, x));
+      else
+        CK(cudaLaunchKernelEx(&cfg, k_as_cluster<false>, l.G, l.S, r, l.ybuf, x));
       return;
     }
     if (l.n <= fused_rows) {  // one kernel: blocks, singletons, then lists (k_as_fused)
@@ -1851,6 +1873,11 @@ int ig_set_option(int32_t option, int64_t value) {
     g_red_ctas = static_cast<int>(value);
     return IG_OK;
   }
+  if (option == IG_OPT_CLUSTER_AS_ROWS) {
+    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: cluster rows out of range");
+    g_cluster_rows = static_cast<int32_t>(value);
+    return IG_OK;
+  }
   if (option == IG_OPT_PSELL_CTAB) {
     g_psell_ctab = value != 0;
     return IG_OK;
@@ -2092,6 +2119,25 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_as_fused<true>, kCta, 0));
       h->fused_cap = static_cast<unsigned>(std::max(1, std::min(occ0, occ1)) * h->num_sms);
       h->fused_rows = g_fused_rows;
+      h->cluster_rows = 0;
+      if (g_cluster_rows > 0) {
+        CK(cudaFuncSetAttribute(k_as_cluster<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CK(cudaFuncSetAttribute(k_as_cluster<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(kAsClusterCtas);
+        cfg.blockDim = dim3(kAsClusterThreads);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kAsClusterCtas;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, k_as_cluster<false>, &cfg) == cudaSuccess && ncl >= 1)
+          h->cluster_rows = g_cluster_rows;
+        cudaGetLastError();
+      }
     }
     h->st = h->alloc<PcgState>(1);
     CK(cudaMemset(h->st, 0, sizeof(PcgState)));
@@ -2122,7 +2168,7 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       // smoother: [blocks] + simple + [complex | finish_red on the finest], twice;
       // plus SpMV-residual x2, restriction, prolongation
       int per_app = (L.n_multi > 0 ? 1 : 0) + 1 + (L.S.n_complex > 0 ? 1 : 0);
-      if (L.n <= h->fused_rows) per_app = 1;  // k_as_fused
+      if (L.n <= h->fused_rows || L.n <= h->cluster_rows) per_app = 1;  // k_as_fused / k_as_cluster
       if (L.ms) {
         int ne = 0;
         for (const auto& mc : L.colors) ne += mc.n_items > 0 ? 1 : 0;

@@ -1088,6 +1088,32 @@ __global__ void __launch_bounds__(kCta) k_as_fused(AsGroups G, AsGather S, const
   }
 }
 
+// Whole additive smoother of a SMALL level in one kernel launched as one
+// thread-block cluster (kAsClusterCtas CTAs): block solves and singleton DOFs,
+// a cluster barrier (release/acquire: the ybuf writes of every CTA become
+// visible), then the list sums.  Replaces three dependent launches and the
+// graph fork/join where the work is a few microseconds (IG_OPT_CLUSTER_AS_ROWS).
+// Same per-item code as the split kernels: bit-identical.
+constexpr int kAsClusterCtas = 16;
+constexpr int kAsClusterThreads = 512;
+template <bool ACC>
+__global__ void __launch_bounds__(kAsClusterThreads) k_as_cluster(AsGroups G, AsGather S, const double* __restrict__ r,
+                                                                 double* ybuf, double* x) {
+  pdl_entry();
+  const int nt = static_cast<int>(gridDim.x * blockDim.x);
+  const int gt = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
+  const int lane = threadIdx.x & 31;
+  const int nitems = G.n_groups + G.n_wblocks;
+  for (int w = gt >> 5; w < nitems; w += nt >> 5) as_blocks_item(G, w, lane, r, ybuf);
+  for (int d = gt; d < S.n; d += nt) as_simple_item<ACC>(S, d, r, x);
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  for (int c = gt; c < S.n_complex; c += nt) {
+    const int d = S.cdof[c];
+    const double out = S.gamma * as_list_sum_y(S, c, r[d], YbufL2{ybuf});
+    x[d] = ACC ? x[d] + out : out;
+  }
+}
+
 // Finest level inside PCG: complex DOFs finish here, simple DOFs read back
 // k_as_simple's result, and every DOF contributes r_d * z_d to r . z in the
 // canonical chunk order.

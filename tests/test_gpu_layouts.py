@@ -138,19 +138,23 @@ def test_breakdown_through_pattern_sell():
         h.close()
 
 
+@pytest.mark.parametrize("variant", ["fused", "cluster"])
 @pytest.mark.parametrize("case_name", ["c1_case", "d3_case", "star_case", "c3_small_case"])
-def test_fused_smoother_bitwise(request, case_name):
-    """The single-kernel additive smoother (k_as_fused, IG_OPT_FUSED_AS_ROWS;
-    off by default) on every level gives the same bits as the fork/join split:
-    smoother applications, V-cycles and the whole PCG solve vs the oracle."""
+def test_fused_smoother_bitwise(request, case_name, variant):
+    """The single-kernel additive smoothers (k_as_fused on a co-resident grid,
+    IG_OPT_FUSED_AS_ROWS; k_as_cluster as one 16-CTA cluster,
+    IG_OPT_CLUSTER_AS_ROWS) on every level give the same bits as the fork/join
+    split: smoother applications, V-cycles and the whole PCG solve vs the oracle."""
     from paper_1903_10977_b200 import MgHierarchy, _ffi, pcg
     lib = _ffi.gpu()
     case = request.getfixturevalue(case_name)
-    lib.ig_set_option(_ffi.IG_OPT_FUSED_AS_ROWS, 1 << 30)
+    opt = _ffi.IG_OPT_FUSED_AS_ROWS if variant == "fused" else _ffi.IG_OPT_CLUSTER_AS_ROWS
+    default = 0 if variant == "fused" else int(getattr(_ffi, "CLUSTER_AS_ROWS_DEFAULT", 0))
+    lib.ig_set_option(opt, 1 << 30)
     try:
         h = MgHierarchy(case)
     finally:
-        lib.ig_set_option(_ffi.IG_OPT_FUSED_AS_ROWS, 0)
+        lib.ig_set_option(opt, default)
     lv = case.levels_c()
     try:
         for l in range(1, h.levels()):
