@@ -201,7 +201,10 @@ def main():
     if args.no_graph:
         lib.ig_set_option(_ffi.IG_OPT_USE_GRAPH, 0)
 
-    case, desc, t_setup = build_workload(args.workload, args.threads, args.smoother)
+    # Host setup threads: all cores for one rank; an equal share per rank when
+    # several ranks (one per GPU) build their replicas at once.
+    threads = args.threads or (max(1, (os.cpu_count() or 1) // world) if world > 1 else 0)
+    case, desc, t_setup = build_workload(args.workload, threads, args.smoother)
     t0 = time.perf_counter()
     h = MgHierarchy(case)
     t_upload = time.perf_counter() - t0
