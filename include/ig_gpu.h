@@ -308,6 +308,7 @@ const char *ig_last_error(void);
 #define IG_OPT_PSELL_CTAS 15  /* pattern-SELL SpMV occupancy cap, CTAs per SM (0 = registers decide) */
 #define IG_OPT_L2_ROWS 18       /* levels below the finest with <= this many DOFs in an L2-persisting arena (default 300000; 0 = off) */
 #define IG_OPT_CLUSTER_AS_ROWS 25 /* smoother levels with <= this many DOFs run as one 16-CTA cluster kernel */
+#define IG_OPT_PSELL_LINES2 27    /* 1 (default): pattern-SELL slices covering two x-lines (shared column runs) */
 #define IG_OPT_PSELL_CTAB 23     /* 1 (default): FAST2 value sequences of the pattern SELL from a constant-bank table */
 #define IG_OPT_GAL_SHORT 21      /* 1 (default): device Galerkin uses the prefetching SpGEMM when B rows have <= 32 entries */
 #define IG_OPT_FORK_ROWS 20      /* smoother levels below this many DOFs run the block solves on the main stream (no fork/join) */

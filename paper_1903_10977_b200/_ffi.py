@@ -97,6 +97,7 @@ IG_OPT_L2_MB = 19
 IG_OPT_FORK_ROWS = 20
 IG_OPT_GAL_SHORT = 21
 IG_OPT_PSELL_CTAB = 23
+IG_OPT_PSELL_LINES2 = 27
 IG_OPT_CLUSTER_AS_ROWS = 25
 
 _host = None

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -252,7 +253,8 @@ int g_psell_pairs = 1;  // FAST slices with two rows per lane (x reuse across a 
 // decide), applied as unused dynamic shared memory: fewer resident warps keep
 // more of each warp's x lines in L1 (the gathers are L1-hit-rate bound).
 int g_psell_ctas = 0;
-int g_psell_ctab = 1;  // IG_OPT_PSELL_CTAB: FAST2 value sequences from a constant-bank table
+int g_psell_ctab = 1;
+int g_psell_lines2 = 1;  // IG_OPT_PSELL_LINES2: FAST4 slices (two x-lines per slice)  // IG_OPT_PSELL_CTAB: FAST2 value sequences from a constant-bank table
 // Levels with at most this many DOFs run the additive smoother as one fused
 // kernel (kernels.cuh k_as_fused) instead of the fork/join split.  Off by
 // default: measured slower on every workload (C2 V-cycle 228 -> 272 us, C4
@@ -288,6 +290,8 @@ struct HostPSell {
   int32_t smul = 1, sshift = 0;
   int64_t layout_bytes = 0;  // matrix words read from HBM per product (shared sequences once)
   int64_t n_fast = 0, n_general = 0, fast_rows = 0;
+  std::vector<int4> useg;    // FAST4 union segment lists (header {D, n}, then {o, m, vA, vB})
+  int64_t n_fast4 = 0;
   std::vector<double> tab;   // constant-bank value table (spmv_psell.cuh PValTab)
   int64_t tab_rows = 0;      // rows whose FAST2 values come from the table
 };
@@ -541,8 +545,125 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
   };
   // Slices in row order: FAST pieces of the long runs; leftover rows are
   // collected 32 at a time into GENERAL slices.
+  // FAST2 / FAST pieces of a run [a, b) (representative row rep: the run's
+  // pattern).  FAST2 (unscaled base only: rows r and r+1 then see the same
+  // column run shifted by one): pieces of up to 64 rows, an even count; the
+  // odd remainder goes to FAST slices.
+  const bool f2ok = g_psell_pairs && s.smul == 1 && s.sshift == 0;
+  auto emit_piece = [&](int32_t a, int32_t b, int32_t rep) {
+    if (b <= a) return;
+    lmax_all = std::max(lmax_all, len(rep));
+    const uint32_t vb = v_start(rep);
+    int32_t i = a;
+    if (f2ok && b - a >= 2) {
+      const uint32_t sg = seg_start(rep);
+      for (; b - i >= 2;) {
+        const int cnt = std::min(64, (b - i) & ~1);
+        s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, sg, pack(len(rep), cnt / 2, true, true, 1, 0)});
+        s.layout_bytes += 16;
+        ++s.n_fast;
+        s.fast_rows += cnt;
+        i += cnt;
+      }
+    }
+    if (i < b) {
+      const uint32_t ob = o_start(rep);
+      for (; i < b; i += 32) {
+        const int cnt = std::min(32, b - i);
+        s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, ob, pack(len(rep), cnt, true, true, 0, 0)});
+        s.layout_bytes += 16;
+        ++s.n_fast;
+        s.fast_rows += cnt;
+      }
+    }
+  };
+  // FAST4: two x-line runs A = [a0, a1) and B = A + D with the same pattern,
+  // where D is the run's first segment stride (the next line).  Their column
+  // runs coincide except at the ends (3D p = 2: 30 distinct lines instead of
+  // 50), so one slice computes 2 rows of each line per lane from one union
+  // segment list (`useg`: header {D, n}, then {offset, m, value index for A
+  // or -1, for B or -1}, offsets ascending -- each row still sums its own
+  // runs in ascending order).
+  const size_t nruns = run_start.size() > 0 ? run_start.size() - 1 : 0;
+  std::vector<int32_t> pairB(nruns, -1), pa0(nruns, 0), pa1(nruns, 0), pD(nruns, 0);
+  std::vector<uint8_t> is_b(nruns, 0);
+  std::vector<int32_t> pairA(nruns, -1);  // B run -> its A run
+  int64_t why[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (f2ok && g_psell_lines2) {
+    for (size_t r = 0; r < nruns; ++r) {
+      const int32_t r0 = run_start[r], r1 = run_start[r + 1];
+      if (r1 - r0 < kPMinRun || is_b[r] || len(r0) < 2) { ++why[0]; continue; }
+      // First segment stride: segments = maximal runs of consecutive columns.
+      int32_t k = ptr[r0], o0 = col[k] - r0, o1 = 0;
+      bool found = false;  // (offsets are negative before the diagonal)
+      for (int32_t q = k + 1; q < ptr[r0 + 1]; ++q)
+        if (col[q] != col[q - 1] + 1) {
+          o1 = col[q] - r0;
+          found = true;
+          break;
+        }
+      if (!found) { ++why[1]; continue; }
+      const int32_t DD = o1 - o0;
+      if (DD <= 0) { ++why[1]; continue; }
+      // Partner run: the run containing r0 + DD, same pattern.
+      const int32_t tb = r0 + DD;
+      if (tb >= nr) { ++why[2]; continue; }
+      const size_t rb = static_cast<size_t>(std::upper_bound(run_start.begin(), run_start.end(), tb) - run_start.begin()) - 1;
+      if (rb >= nruns || rb == r || is_b[rb] || pairB[rb] >= 0) { ++why[3]; continue; }
+      const int32_t b0 = run_start[rb], b1 = run_start[rb + 1];
+      if (b1 - b0 < kPMinRun) { ++why[4]; continue; }
+      if (hv[b0] != hv[r0] || ho[b0] != ho[r0] || !veq(b0, r0) || !oeq(b0, r0)) { ++why[5]; continue; }
+      const int32_t a0 = std::max(r0, b0 - DD), a1 = std::min(r1, b1 - DD);
+      if (a1 - a0 < 16) { ++why[6]; continue; }
+      ++why[7];
+      pairB[r] = static_cast<int32_t>(rb);
+      pa0[r] = a0;
+      pa1[r] = a0 + ((a1 - a0) & ~1);
+      pD[r] = DD;
+      is_b[rb] = 1;
+      pairA[rb] = static_cast<int32_t>(r);
+    }
+  }
+  if (std::getenv("IG_TIMING"))
+    std::fprintf(stderr, "[psell pairs] f2ok=%d lines2=%d runs=%zu: skipped %lld, no 2nd run %lld, past end %lld, partner taken %lld, partner short %lld, pattern differs %lld, overlap < 16 %lld, paired %lld\n",
+                 f2ok ? 1 : 0, g_psell_lines2, nruns, (long long)why[0], (long long)why[1], (long long)why[2], (long long)why[3],
+                 (long long)why[4], (long long)why[5], (long long)why[6], (long long)why[7]);
+  std::map<std::pair<uint32_t, int32_t>, uint32_t> useg_of;  // (segment list, D) -> union list
+  auto union_start = [&](int32_t rep, int32_t D) -> uint32_t {
+    const uint32_t sg = seg_start(rep);
+    auto it = useg_of.find({sg, D});
+    if (it != useg_of.end()) return it->second;
+    std::vector<int4> ent;
+    int32_t cum = 0;
+    std::vector<int4> a, b;
+    for (uint32_t q = sg; s.seg[q].y != 0; ++q) {
+      a.push_back(make_int4(s.seg[q].x, s.seg[q].y, cum, -1));
+      b.push_back(make_int4(s.seg[q].x + D, s.seg[q].y, -1, cum));
+      cum += s.seg[q].y;
+    }
+    size_t ia = 0, ib = 0;
+    while (ia < a.size() || ib < b.size()) {
+      if (ib == b.size() || (ia < a.size() && a[ia].x < b[ib].x)) {
+        ent.push_back(a[ia++]);
+      } else if (ia == a.size() || b[ib].x < a[ia].x) {
+        ent.push_back(b[ib++]);
+      } else if (a[ia].y == b[ib].y) {  // shared column run
+        ent.push_back(make_int4(a[ia].x, a[ia].y, a[ia].z, b[ib].w));
+        ++ia;
+        ++ib;
+      } else {
+        ent.push_back(a[ia++]);
+      }
+    }
+    const uint32_t st = static_cast<uint32_t>(s.useg.size());
+    s.useg.push_back(make_int4(D, static_cast<int>(ent.size()), 0, 0));
+    s.useg.insert(s.useg.end(), ent.begin(), ent.end());
+    s.layout_bytes += 16 * static_cast<int64_t>(ent.size() + 1);
+    useg_of[{sg, D}] = st;
+    return st;
+  };
   std::vector<int32_t> pending;
-  for (size_t r = 0; r + 1 < run_start.size(); ++r) {
+  for (size_t r = 0; r < nruns; ++r) {
     const int32_t r0 = run_start[r], r1 = run_start[r + 1];
     if (r1 - r0 < kPMinRun) {
       for (int32_t i = r0; i < r1; ++i) {
@@ -554,31 +675,35 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       }
       continue;
     }
-    lmax_all = std::max(lmax_all, len(r0));
-    const uint32_t vb = v_start(r0);
-    int32_t i = r0;
-    // FAST2 (unscaled base only: rows r and r+1 then see the same column run
-    // shifted by one): pieces of up to 64 rows, an even count.
-    if (g_psell_pairs && s.smul == 1 && s.sshift == 0 && r1 - r0 >= 2) {
-      const uint32_t sg = seg_start(r0);
-      for (; r1 - i >= 2; ) {
-        const int cnt = std::min(64, (r1 - i) & ~1);
-        s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, sg, pack(len(r0), cnt / 2, true, true, 1, 0)});
+    // Rows of this run already computed as the B line of an earlier pair.
+    int32_t c0 = r1, c1 = r1;
+    if (is_b[r]) {
+      const int32_t q = pairA[r];
+      c0 = pa0[q] + pD[q];
+      c1 = pa1[q] + pD[q];
+    }
+    if (pairB[r] >= 0) {
+      const int32_t a0 = pa0[r], a1 = pa1[r];
+      // (a run used as A is never a B: is_b[r] == 0 here)
+      emit_piece(r0, a0, r0);
+      const uint32_t vb = v_start(r0);
+      const uint32_t ug = union_start(r0, pD[r]);
+      lmax_all = std::max(lmax_all, len(r0));
+      for (int32_t i = a0; i < a1;) {
+        const int cnt = std::min(64, a1 - i);
+        s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, ug, pack(len(r0), cnt / 2, true, true, 2, 0)});
         s.layout_bytes += 16;
         ++s.n_fast;
-        s.fast_rows += cnt;
+        s.fast_rows += 2 * cnt;
+        ++s.n_fast4;
         i += cnt;
       }
-    }
-    if (i < r1) {
-      const uint32_t ob = o_start(r0);
-      for (; i < r1; i += 32) {
-        const int cnt = std::min(32, r1 - i);
-        s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, ob, pack(len(r0), cnt, true, true, 0, 0)});
-        s.layout_bytes += 16;
-        ++s.n_fast;
-        s.fast_rows += cnt;
-      }
+      emit_piece(a1, r1, r0);
+    } else if (is_b[r]) {
+      emit_piece(r0, c0, r0);
+      emit_piece(c1, r1, r0);
+    } else {
+      emit_piece(r0, r1, r0);
     }
     if (s.V.size() > 0xF0000000ull || s.O.size() > 0xF0000000ull) return false;
   }
@@ -594,9 +719,9 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
     std::unordered_map<uint32_t, std::pair<int64_t, int32_t>> use;  // vbase -> (rows, length)
     for (const PSliceMeta& m : s.meta)
       if (m.pk & (1u << 17)) {
-        const bool f2 = ((m.pk >> 19) & 0x3f) == 1;
+        const int wv = static_cast<int>((m.pk >> 19) & 0x3f);  // 0 FAST, 1 FAST2, 2 FAST4
         auto& u = use[m.vbase];
-        u.first += (f2 ? 2 : 1) * static_cast<int64_t>((m.pk >> 11) & 0x3f);
+        u.first += (wv == 2 ? 4 : wv == 1 ? 2 : 1) * static_cast<int64_t>((m.pk >> 11) & 0x3f);
         u.second = static_cast<int32_t>(m.pk & kPMaxLen);
       }
     std::vector<std::pair<int64_t, uint32_t>> order;
@@ -895,6 +1020,8 @@ struct ig_hier {
         d.p.sshift = hp.sshift;
         if (hp.seg.empty()) hp.seg.push_back(make_int2(0, 0));
         d.p.seg = upload(hp.seg.data(), hp.seg.size());
+        if (hp.useg.empty()) hp.useg.push_back(make_int4(0, 0, 0, 0));
+        d.p.useg = upload(hp.useg.data(), hp.useg.size());
         d.p.V = upload(hp.V.data(), hp.V.size());
         d.p.O = upload(hp.O.data(), hp.O.size());
         d.p.dict_w = hp.dict_w;
@@ -902,9 +1029,9 @@ struct ig_hier {
         std::memset(d.ptab.get(), 0, sizeof(PValTab));
         std::copy(hp.tab.begin(), hp.tab.end(), d.ptab->v);
         if (std::getenv("IG_TIMING"))
-          std::fprintf(stderr, "[psell] %d x %d: %lld fast / %lld general slices, value table %zu doubles (%lld rows)\n",
-                       nr, nc, static_cast<long long>(hp.n_fast), static_cast<long long>(hp.n_general), hp.tab.size(),
-                       static_cast<long long>(hp.tab_rows));
+          std::fprintf(stderr, "[psell] %d x %d: %lld fast (%lld two-line) / %lld general slices, value table %zu doubles (%lld rows)\n",
+                       nr, nc, static_cast<long long>(hp.n_fast), static_cast<long long>(hp.n_fast4),
+                       static_cast<long long>(hp.n_general), hp.tab.size(), static_cast<long long>(hp.tab_rows));
         d.p_bytes = hp.layout_bytes;
         d.n_fast = hp.n_fast;
         d.n_general = hp.n_general;
@@ -1876,6 +2003,10 @@ int ig_set_option(int32_t option, int64_t value) {
   if (option == IG_OPT_CLUSTER_AS_ROWS) {
     if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: cluster rows out of range");
     g_cluster_rows = static_cast<int32_t>(value);
+    return IG_OK;
+  }
+  if (option == IG_OPT_PSELL_LINES2) {
+    g_psell_lines2 = value != 0;
     return IG_OK;
   }
   if (option == IG_OPT_PSELL_CTAB) {

@@ -65,6 +65,7 @@ struct PSell {
   int32_t dict_w;
   int32_t smul, sshift;  // base(row) = (row * smul) >> sshift
   const int2* seg;       // FAST2 segment lists (first offset, length); length 0 ends a list
+  const int4* useg;      // FAST4 union lists: header {D, n}, then {offset, length, value index A | -1, B | -1}
 };
 
 template <bool STREAM>
@@ -172,14 +173,22 @@ __device__ __forceinline__ void fast2_dispatch(const double* __restrict__ x, int
 // The rows this lane will own in a slice (psell_slice's mapping), from the
 // static metadata: lets a kernel issue its per-row loads (residual source,
 // the x being corrected) ahead of the slice's product chain.
-__device__ __forceinline__ void psell_rows(const PSell& A, const uint4 mu, int& row, int& row2) {
+__device__ __forceinline__ void psell_rows(const PSell& A, const uint4 mu, int* rows) {
   const int lane = threadIdx.x & 31;
   const uint32_t pk = mu.w;
   const int count = static_cast<int>((pk >> 11) & 0x3f);
-  row = -1;
-  row2 = -1;
+  int& row = rows[0];
+  int& row2 = rows[1];
+  row = row2 = rows[2] = rows[3] = -1;
   if (count == 0 || lane >= count) return;
-  if ((pk & (1u << 17)) && ((pk >> 19) & 0x3f) == 1) {
+  const int wv = static_cast<int>((pk >> 19) & 0x3f);
+  if ((pk & (1u << 17)) && wv == 2) {  // FAST4: B rows at + D
+    const int D = __ldg(A.useg + mu.z).x;
+    row = static_cast<int>(mu.x) + 2 * lane;
+    row2 = row + 1;
+    rows[2] = row + D;
+    rows[3] = row + D + 1;
+  } else if ((pk & (1u << 17)) && wv == 1) {
     row = static_cast<int>(mu.x) + 2 * lane;
     row2 = row + 1;
   } else if (pk & (1u << 17)) {
@@ -189,20 +198,112 @@ __device__ __forceinline__ void psell_rows(const PSell& A, const uint4 mu, int& 
   }
 }
 
+// FAST4: one union column run (offset o from the lane's A row, length M) for
+// the lane's rows ra, ra+1 (line A) and ra+D, ra+D+1 (line B): the x values
+// are loaded once; A's rows add their products if vA >= 0, B's if vB >= 0.
+template <int P, int M, class VS>
+__device__ __forceinline__ void fast4_segment(const double* __restrict__ x, int a, const VS& vs, int vA, int vB,
+                                              double& acc0, double& acc1, double& acc2, double& acc3) {
+  constexpr int C = M + 1 + P;
+  const double* xb = x + (a - P);
+  const double2* xb2 = reinterpret_cast<const double2*>(xb);
+  double X[C + 1];
+#pragma unroll
+  for (int q = 0; 2 * q < C; ++q) {
+    if (2 * q + 1 < C) {
+      const double2 t = __ldg(xb2 + q);
+      X[2 * q] = t.x;
+      X[2 * q + 1] = t.y;
+    } else {
+      X[2 * q] = __ldg(xb + 2 * q);
+    }
+  }
+  if (vA >= 0) {  // warp-uniform
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const double v = vs(vA + j);
+      acc0 = acc0 + v * X[P + j];
+      acc1 = acc1 + v * X[P + j + 1];
+    }
+  }
+  if (vB >= 0) {
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const double v = vs(vB + j);
+      acc2 = acc2 + v * X[P + j];
+      acc3 = acc3 + v * X[P + j + 1];
+    }
+  }
+}
+struct VGlob {
+  const double* p;
+  __device__ __forceinline__ double operator()(int j) const { return __ldg(p + j); }
+};
+struct VTabl {
+  const PValTab* t;
+  int o;  // the sequence's offset in the table
+  __device__ __forceinline__ double operator()(int j) const { return t->v[o + j]; }
+};
+template <int P, class VS>
+__device__ __forceinline__ void fast4_dispatch(const double* __restrict__ x, int a, int m, const VS& vs, int vA, int vB,
+                                               double& acc0, double& acc1, double& acc2, double& acc3) {
+  switch (m) {  // warp-uniform
+    case 1: fast4_segment<P, 1>(x, a, vs, vA, vB, acc0, acc1, acc2, acc3); break;
+    case 2: fast4_segment<P, 2>(x, a, vs, vA, vB, acc0, acc1, acc2, acc3); break;
+    case 3: fast4_segment<P, 3>(x, a, vs, vA, vB, acc0, acc1, acc2, acc3); break;
+    case 4: fast4_segment<P, 4>(x, a, vs, vA, vB, acc0, acc1, acc2, acc3); break;
+    case 5: fast4_segment<P, 5>(x, a, vs, vA, vB, acc0, acc1, acc2, acc3); break;
+    case 6: fast4_segment<P, 6>(x, a, vs, vA, vB, acc0, acc1, acc2, acc3); break;
+    case 7: fast4_segment<P, 7>(x, a, vs, vA, vB, acc0, acc1, acc2, acc3); break;
+    default: fast4_segment<P, 8>(x, a, vs, vA, vB, acc0, acc1, acc2, acc3); break;
+  }
+}
+template <class VS>
+__device__ __forceinline__ void fast4_slice(const double* __restrict__ x, const int4* __restrict__ ug, int n, int ra,
+                                           int p0, const VS& vs, double* acc) {
+  for (int u = 0; u < n; ++u) {
+    const int4 e = __ldg(ug + u);
+    if (((p0 + e.x) & 1) == 0)
+      fast4_dispatch<0>(x, ra + e.x, e.y, vs, e.z, e.w, acc[0], acc[1], acc[2], acc[3]);
+    else
+      fast4_dispatch<1>(x, ra + e.x, e.y, vs, e.z, e.w, acc[0], acc[1], acc[2], acc[3]);
+  }
+}
+
 // One warp, one slice.  Returns the row this lane owns (-1: none) and its
 // sum; FAST2 slices give each lane a second row (row2 / acc2, else -1).
 template <bool STREAM>
 __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const double* __restrict__ x, double& acc,
-                                           int& row2, double& acc2, const PValTab* tab = nullptr) {
+                                           int& row2, double& acc2, const PValTab* tab, int* rowx, double* accx) {
   acc = 0.0;
   acc2 = 0.0;
   row2 = -1;
+  rowx[0] = rowx[1] = -1;
   const int lane = threadIdx.x & 31;
   const uint32_t pk = mu.w;
   const int count = static_cast<int>((pk >> 11) & 0x3f);
   if (count == 0) return -1;  // padding slice (warp-uniform)
   const int L = static_cast<int>(pk & kPMaxLen);
   const int cl = min(lane, count - 1);  // surplus lanes recompute the last row, store nothing
+  if ((pk & (1u << 17)) && ((pk >> 19) & 0x3f) == 2) {  // FAST4: rows of two x-lines (warp-uniform)
+    const int ra = static_cast<int>(mu.x) + 2 * cl;
+    const int p0 = static_cast<int>(mu.x) & 1;
+    const int4 hd = __ldg(A.useg + mu.z);
+    double a4[4] = {0.0, 0.0, 0.0, 0.0};
+    if (tab != nullptr && (pk >> 31))
+      fast4_slice(x, A.useg + mu.z + 1, hd.y, ra, p0, VTabl{tab, static_cast<int>(mu.y)}, a4);
+    else
+      fast4_slice(x, A.useg + mu.z + 1, hd.y, ra, p0, VGlob{A.V + mu.y}, a4);
+    acc = a4[0];
+    acc2 = a4[1];
+    if (lane >= count) return -1;
+    row2 = ra + 1;
+    rowx[0] = ra + hd.x;
+    rowx[1] = ra + hd.x + 1;
+    accx[0] = a4[2];
+    accx[1] = a4[3];
+    return ra;
+  }
   if ((pk & (1u << 17)) && ((pk >> 19) & 0x3f) == 1) {  // FAST2: `count` row pairs (warp-uniform)
     const int ra = static_cast<int>(mu.x) + 2 * cl;
     const double* vp = A.V + mu.y;
@@ -349,19 +450,24 @@ __global__ void __launch_bounds__(kCta, IG_PSPMV_MINB) k_pspmv(PSell A, const do
                                                const __grid_constant__ PValTab tab) {
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(A.meta + slice));  // static: before the wait
-  int pr, pr2;
-  psell_rows(A, mu, pr, pr2);
+  int pr[4];
+  psell_rows(A, mu, pr);
   pdl_entry();
   if (pcg_done(st)) return;
   // The residual source is loaded before the product chain, not after it.
-  const double r1 = (MODE == 1 && pr >= 0) ? rsrc[pr] : 0.0;
-  const double r2 = (MODE == 1 && pr2 >= 0) ? rsrc[pr2] : 0.0;
-  double acc, acc2;
-  int row2;
-  const int row = psell_slice<STREAM>(A, mu, x, acc, row2, acc2, &tab);
+  double rs[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) rs[k] = (MODE == 1 && pr[k] >= 0) ? rsrc[pr[k]] : 0.0;
+  double acc, acc2, accx[2];
+  int row2, rowx[2];
+  const int row = psell_slice<STREAM>(A, mu, x, acc, row2, acc2, &tab, rowx, accx);
   if (row < 0) return;
-  y[row] = (MODE == 0) ? acc : r1 - acc;
-  if (row2 >= 0) y[row2] = (MODE == 0) ? acc2 : r2 - acc2;
+  y[row] = (MODE == 0) ? acc : rs[0] - acc;
+  if (row2 >= 0) y[row2] = (MODE == 0) ? acc2 : rs[1] - acc2;
+  if (rowx[0] >= 0) {
+    y[rowx[0]] = (MODE == 0) ? accx[0] : rs[2] - accx[0];
+    y[rowx[1]] = (MODE == 0) ? accx[1] : rs[3] - accx[1];
+  }
 }
 
 // p . Ap over the canonical 256-row chunks (kernels.cuh: last_cta_total), then
@@ -390,22 +496,29 @@ __global__ void __launch_bounds__(kCta, IG_PPROLONG_MINB) k_pprolong(PSell P, co
                                                   const PcgState* st, const __grid_constant__ PValTab tab) {
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(P.meta + slice));  // static: before the wait
-  int pr, pr2;
-  psell_rows(P, mu, pr, pr2);
+  int pr[4];
+  psell_rows(P, mu, pr);
   pdl_entry();
   if (pcg_done(st)) return;
   // The x being corrected is loaded before the product chain, not after it.
-  const double x1 = pr >= 0 ? x[pr] : 0.0;
-  const double x2 = pr2 >= 0 ? x[pr2] : 0.0;
-  double c, c2;
-  int row2;
-  const int row = psell_slice<STREAM>(P, mu, xc, c, row2, c2, &tab);
+  double xo[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) xo[k] = pr[k] >= 0 ? x[pr[k]] : 0.0;
+  double c, c2, cx[2];
+  int row2, rowx[2];
+  const int row = psell_slice<STREAM>(P, mu, xc, c, row2, c2, &tab, rowx, cx);
   if (row < 0) return;
   cor[row] = c;
-  x[row] = x1 + c;
+  x[row] = xo[0] + c;
   if (row2 >= 0) {
     cor[row2] = c2;
-    x[row2] = x2 + c2;
+    x[row2] = xo[1] + c2;
+  }
+  if (rowx[0] >= 0) {
+    cor[rowx[0]] = cx[0];
+    x[rowx[0]] = xo[2] + cx[0];
+    cor[rowx[1]] = cx[1];
+    x[rowx[1]] = xo[3] + cx[1];
   }
 }
 

@@ -200,3 +200,40 @@ def test_constant_value_table_bitwise(ctab):
         assert st == 0 and rep.iterations == it and np.array_equal(x, xo)
     finally:
         h.close()
+
+
+@pytest.fixture(scope="module")
+def d3_48_case():
+    """3D C4-like case at 48^3 (x-line runs of ~44 rows: long enough to pair)."""
+    from paper_1903_10977_b200 import build_case, configs
+    return build_case(configs.c4(res=48, levels=4))
+
+
+@pytest.mark.parametrize("lines2", [0, 1])
+def test_two_line_slices_bitwise(d3_48_case, lines2):
+    """FAST4 slices (two x-lines per slice sharing their column runs,
+    IG_OPT_PSELL_LINES2; pattern layout forced on every level) give the
+    oracle's bits for the level products and the PCG solve."""
+    from paper_1903_10977_b200 import MgHierarchy, _ffi, pcg
+    lib = _ffi.gpu()
+    d3_case = d3_48_case
+    lv = d3_case.levels_c()
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_LINES2, lines2)
+    lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 0)
+    try:
+        h = MgHierarchy(d3_case)
+    finally:
+        lib.ig_set_option(_ffi.IG_OPT_PSELL_LINES2, 1)
+        lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
+    try:
+        for l in range(1, h.levels()):
+            A, _ = h.level(l)
+            x = rng_vec(370 + l, A.cols())
+            y0 = rng_vec(380 + l, A.rows())
+            assert np.array_equal(h.spmv(l, x, 0), orc.spmv(lv, l, x, 0))
+            assert np.array_equal(h.spmv(l, x, 1, y0), orc.spmv(lv, l, x, 1, y0))
+        x, rep = pcg(h.A, d3_case.b, h, tol=1e-8, maxit=1000)
+        st, xo, ro, it, _ = orc.pcg(lv, d3_case.b, tol=1e-8, maxit=1000, mode=orc.GPU_ORDER)
+        assert st == 0 and rep.iterations == it and np.array_equal(x, xo)
+    finally:
+        h.close()
