@@ -589,7 +589,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
   std::vector<uint8_t> is_b(nruns, 0);
   std::vector<int32_t> pairA(nruns, -1);  // B run -> its A run
   int64_t why[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (f2ok && g_psell_lines2) {
+  if (f2ok && g_psell_lines2 && nr == nc) {  // square operators only (k_pprolong has no two-line path)
     for (size_t r = 0; r < nruns; ++r) {
       const int32_t r0 = run_start[r], r1 = run_start[r + 1];
       if (r1 - r0 < kPMinRun || is_b[r] || len(r0) < 2) { ++why[0]; continue; }

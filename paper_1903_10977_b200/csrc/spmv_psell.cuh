@@ -173,6 +173,7 @@ __device__ __forceinline__ void fast2_dispatch(const double* __restrict__ x, int
 // The rows this lane will own in a slice (psell_slice's mapping), from the
 // static metadata: lets a kernel issue its per-row loads (residual source,
 // the x being corrected) ahead of the slice's product chain.
+template <bool F4 = true>
 __device__ __forceinline__ void psell_rows(const PSell& A, const uint4 mu, int* rows) {
   const int lane = threadIdx.x & 31;
   const uint32_t pk = mu.w;
@@ -182,7 +183,7 @@ __device__ __forceinline__ void psell_rows(const PSell& A, const uint4 mu, int* 
   row = row2 = rows[2] = rows[3] = -1;
   if (count == 0 || lane >= count) return;
   const int wv = static_cast<int>((pk >> 19) & 0x3f);
-  if ((pk & (1u << 17)) && wv == 2) {  // FAST4: B rows at + D
+  if (F4 && (pk & (1u << 17)) && wv == 2) {  // FAST4: B rows at + D
     const int D = __ldg(A.useg + mu.z).x;
     row = static_cast<int>(mu.x) + 2 * lane;
     row2 = row + 1;
@@ -272,7 +273,7 @@ __device__ __forceinline__ void fast4_slice(const double* __restrict__ x, const 
 
 // One warp, one slice.  Returns the row this lane owns (-1: none) and its
 // sum; FAST2 slices give each lane a second row (row2 / acc2, else -1).
-template <bool STREAM>
+template <bool STREAM, bool F4 = true>
 __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const double* __restrict__ x, double& acc,
                                            int& row2, double& acc2, const PValTab* tab, int* rowx, double* accx) {
   acc = 0.0;
@@ -285,7 +286,7 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
   if (count == 0) return -1;  // padding slice (warp-uniform)
   const int L = static_cast<int>(pk & kPMaxLen);
   const int cl = min(lane, count - 1);  // surplus lanes recompute the last row, store nothing
-  if ((pk & (1u << 17)) && ((pk >> 19) & 0x3f) == 2) {  // FAST4: rows of two x-lines (warp-uniform)
+  if (F4 && (pk & (1u << 17)) && ((pk >> 19) & 0x3f) == 2) {  // FAST4: rows of two x-lines (warp-uniform)
     const int ra = static_cast<int>(mu.x) + 2 * cl;
     const int p0 = static_cast<int>(mu.x) & 1;
     const int4 hd = __ldg(A.useg + mu.z);
@@ -496,29 +497,23 @@ __global__ void __launch_bounds__(kCta, IG_PPROLONG_MINB) k_pprolong(PSell P, co
                                                   const PcgState* st, const __grid_constant__ PValTab tab) {
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(P.meta + slice));  // static: before the wait
+  // (Two-line slices exist only in square matrices: never in P.)
   int pr[4];
-  psell_rows(P, mu, pr);
+  psell_rows<false>(P, mu, pr);
   pdl_entry();
   if (pcg_done(st)) return;
   // The x being corrected is loaded before the product chain, not after it.
-  double xo[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) xo[k] = pr[k] >= 0 ? x[pr[k]] : 0.0;
+  const double x1 = pr[0] >= 0 ? x[pr[0]] : 0.0;
+  const double x2 = pr[1] >= 0 ? x[pr[1]] : 0.0;
   double c, c2, cx[2];
   int row2, rowx[2];
-  const int row = psell_slice<STREAM>(P, mu, xc, c, row2, c2, &tab, rowx, cx);
+  const int row = psell_slice<STREAM, false>(P, mu, xc, c, row2, c2, &tab, rowx, cx);
   if (row < 0) return;
   cor[row] = c;
-  x[row] = xo[0] + c;
+  x[row] = x1 + c;
   if (row2 >= 0) {
     cor[row2] = c2;
-    x[row2] = xo[1] + c2;
-  }
-  if (rowx[0] >= 0) {
-    cor[rowx[0]] = cx[0];
-    x[rowx[0]] = xo[2] + cx[0];
-    cor[rowx[1]] = cx[1];
-    x[rowx[1]] = xo[3] + cx[1];
+    x[row2] = x2 + c2;
   }
 }
 
