@@ -603,6 +603,13 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
           break;
         }
       if (!found) { ++why[1]; continue; }
+      // Only rows of many column runs (3D stencils: 25 for p = 2) pay: in 2D
+      // (5 runs, 6 after the merge) the slices measured slower (C3 +1.3 %).
+      {
+        int32_t runs = 1;
+        for (int32_t q = k + 1; q < ptr[r0 + 1]; ++q) runs += col[q] != col[q - 1] + 1 ? 1 : 0;
+        if (runs < 9) { ++why[1]; continue; }
+      }
       const int32_t DD = o1 - o0;
       if (DD <= 0) { ++why[1]; continue; }
       // Partner run: the run containing r0 + DD, same pattern.
@@ -785,6 +792,7 @@ struct DevSell {
   bool has_p = false;   // pattern-SELL layout present (spmv_psell.cuh)
   PSell p{};
   std::shared_ptr<PValTab> ptab;  // constant-bank value table (zeros when unused)
+  bool has_f4 = false;            // the pattern layout holds two-line slices
   int64_t p_bytes = 0;  // HostPSell::layout_bytes
   int64_t n_fast = 0, n_general = 0;
   int64_t layout_matrix_bytes() const { return has_p ? p_bytes : 8 * explicit_vals + 4 * explicit_cols + 4 * int64_t(s.n_rows); }
@@ -1025,6 +1033,7 @@ struct ig_hier {
         d.p.V = upload(hp.V.data(), hp.V.size());
         d.p.O = upload(hp.O.data(), hp.O.size());
         d.p.dict_w = hp.dict_w;
+        d.has_f4 = hp.n_fast4 > 0;
         d.ptab = std::make_shared<PValTab>();
         std::memset(d.ptab.get(), 0, sizeof(PValTab));
         std::copy(hp.tab.begin(), hp.tab.end(), d.ptab->v);
@@ -1075,7 +1084,10 @@ struct ig_hier {
       const unsigned gp = static_cast<unsigned>(A.p.n_slices / (kCta / 32));
       const size_t sm = psell_smem();
       const PValTab& tb = *A.ptab;
-      if (mode == 0) {
+      if (!A.has_f4 && !A.stream) {  // no two-line slices: the leaner instantiation
+        if (mode == 0) launch(k_pspmv<0, false, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
+        else launch(k_pspmv<1, false, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
+      } else if (mode == 0) {
         if (A.stream) launch(k_pspmv<0, true>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
         else launch(k_pspmv<0, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
       } else {

@@ -445,27 +445,27 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
 #ifndef IG_PPROLONG_MINB
 #define IG_PPROLONG_MINB 4
 #endif
-template <int MODE, bool STREAM>
+template <int MODE, bool STREAM, bool F4 = true>
 __global__ void __launch_bounds__(kCta, IG_PSPMV_MINB) k_pspmv(PSell A, const double* __restrict__ x, double* y,
                                                const double* rsrc, const PcgState* st,
                                                const __grid_constant__ PValTab tab) {
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(A.meta + slice));  // static: before the wait
   int pr[4];
-  psell_rows(A, mu, pr);
+  psell_rows<F4>(A, mu, pr);
   pdl_entry();
   if (pcg_done(st)) return;
   // The residual source is loaded before the product chain, not after it.
   double rs[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) rs[k] = (MODE == 1 && pr[k] >= 0) ? rsrc[pr[k]] : 0.0;
+  for (int k = 0; k < (F4 ? 4 : 2); ++k) rs[k] = (MODE == 1 && pr[k] >= 0) ? rsrc[pr[k]] : 0.0;
   double acc, acc2, accx[2];
   int row2, rowx[2];
-  const int row = psell_slice<STREAM>(A, mu, x, acc, row2, acc2, &tab, rowx, accx);
+  const int row = psell_slice<STREAM, F4>(A, mu, x, acc, row2, acc2, &tab, rowx, accx);
   if (row < 0) return;
   y[row] = (MODE == 0) ? acc : rs[0] - acc;
   if (row2 >= 0) y[row2] = (MODE == 0) ? acc2 : rs[1] - acc2;
-  if (rowx[0] >= 0) {
+  if (F4 && rowx[0] >= 0) {
     y[rowx[0]] = (MODE == 0) ? accx[0] : rs[2] - accx[0];
     y[rowx[1]] = (MODE == 0) ? accx[1] : rs[3] - accx[1];
   }
