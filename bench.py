@@ -371,6 +371,7 @@ def main():
                          "layout_bytes_per_launch": int(info.bytes_spmv_finest_layout),
                          "layout_gbs": info.bytes_spmv_finest_layout / (spmv_ms * 1e-3) / 1e9,
                          "layout_frac": info.bytes_spmv_finest_layout / (spmv_ms * 1e-3) / 1e9 / hbm,
+                         "frac_vs_nominal_8tbs": achieved / 8000.0,  # also vs the ~8 TB/s nominal
                          "note": ("achieved counts CSR-minimal bytes (12 B/nnz, SURVEY.md App. C); the "
                                   "pattern SELL reads only layout_bytes_per_launch from HBM (matrix words "
                                   "shared by runs of identical rows are read once), so frac > 1 is expected; "
