@@ -303,7 +303,7 @@ const char *ig_last_error(void);
 #define IG_OPT_PDL 9          /* 1 (default): programmatic dependent launch for every kernel; 0: plain stream order */
 #define IG_OPT_TAIL_CLUSTER 10 /* persistent small-level kernel: 1 one 16-CTA cluster, 0 cooperative grid */
 #define IG_OPT_MS_LAZY 11     /* multiplicative sweep: 1 lazily updated residual, 0 (default) classic per-colour updates */
-#define IG_OPT_AS_SPLIT 12    /* additive smoother: 1 (default) small blocks fused with singletons, 0 all blocks on the side stream */
+#define IG_OPT_AS_SPLIT 12    /* additive smoother: 1 small blocks fused with singletons, 0 (default) all blocks on the side stream */
 #define IG_OPT_RED_CTAS 13    /* CTAs per SM of the canonical-reduction kernels (default 8) */
 #define IG_OPT_PSELL_CTAS 15  /* pattern-SELL SpMV occupancy cap, CTAs per SM (0 = registers decide) */
 #define IG_OPT_L2_ROWS 18       /* levels below the finest with <= this many DOFs in an L2-persisting arena (default 300000; 0 = off) */

@@ -113,7 +113,11 @@ int g_tail_cluster = 1;
 // (uncoalesced): C4 V-cycle 9.3 -> 77 ms, C5 1.6 -> 7.1 ms.  Kept, off.
 int g_ms_lazy = 0;
 int g_red_ctas = 8;  // CTAs per SM of the canonical-reduction kernels (profiles/option_sweep.py 13)
-int g_split = 1;  // additive smoother: small groups (smax <= 4) with the singleton DOFs, big ones on the side stream  // 1: the small levels run in one 16-CTA cluster (cluster barriers); 0: cooperative grid
+// Additive smoother: 1 = small groups (smax <= 4) fused with the singleton
+// DOFs on the main stream; 0 (default) = every block solve on the side
+// stream and the lean (28-register) singleton kernel on the main stream
+// (C4 PCG 115.8 -> 114.6 ms, C3 15.87 -> 15.21 ms, C2 +0.5 %).
+int g_split = 0;
 // Compact-SELL layouts (spmv_tma.cuh) measured SLOWER than the row-dictionary
 // SELL on C4 (finest SpMV 442 us direct / 410 us TMA-staged vs 303 us;
 // profiles/spmv_layouts.py), so they are off by default.
@@ -1232,7 +1236,12 @@ struct ig_hier {
     }
     const unsigned g = grid_of(l.n);
     const int32_t gctas = static_cast<int32_t>((static_cast<int64_t>(n_small) * 32 + kCta - 1) / kCta);
-    if (acc)
+    if (gctas == 0) {  // no small groups here (IG_OPT_AS_SPLIT 0): the lean singleton kernel
+      if (acc)
+        launch(k_as_simple<true>, g, kCta, 0, stream, l.S, r, x, s);
+      else
+        launch(k_as_simple<false>, g, kCta, 0, stream, l.S, r, x, s);
+    } else if (acc)
       launch(k_as_small_simple<true>, g + gctas, kCta, 0, stream, l.G, big.n_groups, gctas, l.S, r, l.ybuf, x, s);
     else
       launch(k_as_small_simple<false>, g + gctas, kCta, 0, stream, l.G, big.n_groups, gctas, l.S, r, l.ybuf, x, s);

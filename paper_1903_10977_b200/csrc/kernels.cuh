@@ -900,11 +900,18 @@ __device__ __forceinline__ void as_simple_item(const AsGather& S, int d, const d
 template <bool ACC>
 __global__ void __launch_bounds__(kCta) k_as_simple(AsGather S, const double* __restrict__ r, double* x,
                                                     const PcgState* st) {
-  pdl_entry();
-  if (pcg_done(st)) return;
   const int d = blockIdx.x * kCta + threadIdx.x;
   if (d >= S.n) return;
-  as_simple_item<ACC>(S, d, r, x);
+  const int h = S.head[d];  // static: before the predecessor wait
+  const double l = S.sdiag[d];
+  if (h < 0) return;
+  pdl_entry();
+  const double rd = r[d];
+  const double xo = ACC ? x[d] : 0.0;
+  double acc = 0.0;
+  acc = acc + (rd / l) / l;
+  const double out = S.gamma * acc;
+  x[d] = ACC ? xo + out : out;
 }
 // Small groups (smax <= 4: faces of the box, most multi-DOF blocks) fused
 // with the singleton DOFs: CTAs [0, n_gctas) run groups g_begin.. of G with
