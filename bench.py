@@ -10,8 +10,12 @@ metric through the C-ABI call with host buffers (ig_pcg: H2D of b, solve, D2H
 of x and the residual history inside the timed region).
 
 --impl reference times the CPU oracle (oracle/liboracle.so, the C restatement
-of the reference's single-threaded solve -- the reference itself cannot be
-built here) on a bounded sample of the same workload.
+of the reference's solve -- the reference itself cannot be built here,
+SURVEY.md §0.2) on all host threads: every timed step is one COMPLETE solve
+of the same workload (same hierarchy, tol, zero guess), no extrapolation.
+The oracle's OpenMP loops are bit-identical to its sequential order
+(oracle/oracle.c header), so the threaded run computes exactly the
+single-threaded restatement.
 """
 from __future__ import annotations
 
@@ -134,32 +138,39 @@ def host_cpu():
     return {"nproc": os.cpu_count(), "model": model}
 
 
-def pinned_core0(fn):
-    """Run fn() pinned to host core 0 (taskset -c 0), then
-    restore the affinity."""
+def host_threads() -> int:
     try:
-        old = os.sched_getaffinity(0)
-        os.sched_setaffinity(0, {sorted(old)[0]})
+        return len(os.sched_getaffinity(0))
     except (AttributeError, OSError):
-        old = None
-    try:
-        return fn()
-    finally:
-        if old is not None:
-            os.sched_setaffinity(0, old)
+        return os.cpu_count() or 1
 
 
-def cpu_sample(case, iters_full: int, sample_iters: int):
-    """Oracle (single-threaded C restatement) on the first `sample_iters` PCG
-    iterations, extrapolated to the full solve: the prologue costs one
-    preconditioner application, every iteration one SpMV + one V-cycle."""
+def oracle_solve(case, maxit: int = 1000, threads: int = 0):
+    """One oracle PCG solve (sequential-order reductions, the natural reading
+    of the reference) on `threads` host threads (0 = all)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_ffi as orc
-    st, x, res, it, sec = pinned_core0(
-        lambda: orc.pcg(case.levels_c(), case.b, tol=1e-8, maxit=sample_iters, mode=orc.SEQ))
-    per_unit = sec / (it + 1)
-    t_full = per_unit * (iters_full + 1)
-    return case.n / t_full, sec, it
+    orc.set_threads(threads or host_threads())
+    st, x, res, it, sec = orc.pcg(case.levels_c(), case.b, tol=1e-8, maxit=maxit, mode=orc.SEQ)
+    return st, it, sec, orc.get_threads()
+
+
+def common_config(desc, case, world):
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": desc, "n_dofs": int(case.n), "nnz_finest": int(case.A.nnz),
+            "levels": int(case.n_levels), "level_dofs": [int(v) for v in case.level_dofs()],
+            "tol": 1e-8, "maxit": 1000, "initial_guess": "zero", "parallelism": f"replicas x{world}",
+            "l2": "no flush: working set (matrix hierarchy ~3.6 GB for C4) >> 126 MB L2"}
+
+
+def profile_evidence(workload: str):
+    """Per-launch DRAM bytes and the binding unit of the dominant kernel, from
+    the committed ncu --set full summary (profiles/spmv_traffic.json)."""
+    tp = os.path.join(ROOT, "profiles", "spmv_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            return json.load(f).get(workload, {})
+    return {}
 
 
 def main():
@@ -172,7 +183,6 @@ def main():
     ap.add_argument("--threads", type=int, default=0, help="host setup threads (0 = all)")
     ap.add_argument("--smoother", default="as", choices=["as", "ms"],
                     help="as: additive Schwarz (the BASELINE configs); ms: multiplicative colored Schwarz")
-    ap.add_argument("--cpu-sample-iters", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-device-setup", action="store_true", help="skip the ig_hier_build setup measurement")
     ap.add_argument("--no-graph", action="store_true",
@@ -270,7 +280,6 @@ def main():
     torch.cuda.synchronize()
     spmv_ms = e0.elapsed_time(e1) / nspmv
     hbm, peak_src = peaks()
-    achieved = info.bytes_spmv_finest / (spmv_ms * 1e-3) / 1e9
     kernel_name = ("k_pspmv (finest A p, pattern SELL; spmv_psell.cuh)" if n > 40000
                    else "k_spmv_grp (finest A p, row-dictionary SELL)")
 
@@ -337,19 +346,20 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, sec, sit = cpu_sample(case, iters, args.cpu_sample_iters)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": (f"oracle/liboracle.so (C restatement of solvers.cpp/multigrid.cpp/smoothers.cpp, "
-                          f"single-threaded like the reference, -O3 -ffp-contract=off, pinned to host core 0): "
-                          f"first {sit} PCG iterations of the same {args.workload.upper()} hierarchy took "
-                          f"{sec:.2f} s, extrapolated to the {iters}-iteration solve"),
-               "host": host_cpu()}
+        cst, cit, csec, cth = oracle_solve(case)
+        assert cst == 0, f"oracle solve did not converge (status {cst})"
+        cpu = {"value": n / csec, "unit": UNIT, "cores": cth, "kind": "port",
+               "sample": (f"one complete {args.workload.upper()} solve ({cit} PCG iterations to 1e-8, zero "
+                          f"guess, {csec:.2f} s) of oracle/liboracle.so -- the C restatement of "
+                          f"solvers.cpp/multigrid.cpp/smoothers.cpp, -O3 -ffp-contract=off, sequential-order "
+                          f"dots -- on {cth} host threads (OpenMP loops bit-identical to one thread)"),
+               "iterations": cit, "seconds": csec, "complete_solves": 1, "host": host_cpu()}
 
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "spmv_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            traffic = json.load(f).get(args.workload, {}).get("bytes_per_launch")
+    ev = profile_evidence(args.workload)
+    traffic = ev.get("bytes_per_launch")
+    layout_bytes = int(info.bytes_spmv_finest_layout)
+    layout_gbs = layout_bytes / (spmv_ms * 1e-3) / 1e9
+    csr_gbs = info.bytes_spmv_finest / (spmv_ms * 1e-3) / 1e9
 
     if rank == 0:
         line = {
@@ -357,25 +367,25 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded immersed geometry, host-assembled operator (penalty Dirichlet), f=1",
-            "config": {"workload": desc, "n_dofs": n, "nnz_finest": int(case.A.nnz), "levels": L,
-                       "level_dofs": [int(info.n[i]) for i in range(L)], "tol": 1e-8,
-                       "iterations": iters, "parallelism": f"replicas x{world}",
-                       "l2": "no flush: working set (matrix hierarchy ~3.6 GB) >> 126 MB L2"},
+            "config": common_config(desc, case, world),
             "iterations": iters,
             "vcycles_per_s": 1e3 / vc_ms, "vcycle_ms": vc_ms, "vcycle_gbs": vc_gbs,
             "vcycle_frac_of_hbm": vc_gbs / hbm,
-            "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": achieved,
-                         "peak": hbm, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": traffic, "algorithmic_bytes_per_launch": int(info.bytes_spmv_finest),
+            "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": layout_gbs,
+                         "peak": hbm, "peak_source": peak_src, "unit": "GB/s", "frac": layout_gbs / hbm,
+                         "traffic": traffic, "algorithmic_bytes_per_launch": layout_bytes,
                          "launch_ms": spmv_ms,
-                         "layout_bytes_per_launch": int(info.bytes_spmv_finest_layout),
-                         "layout_gbs": info.bytes_spmv_finest_layout / (spmv_ms * 1e-3) / 1e9,
-                         "layout_frac": info.bytes_spmv_finest_layout / (spmv_ms * 1e-3) / 1e9 / hbm,
-                         "frac_vs_nominal_8tbs": achieved / 8000.0,  # also vs the ~8 TB/s nominal
-                         "note": ("achieved counts CSR-minimal bytes (12 B/nnz, SURVEY.md App. C); the "
-                                  "pattern SELL reads only layout_bytes_per_launch from HBM (matrix words "
-                                  "shared by runs of identical rows are read once), so frac > 1 is expected; "
-                                  "traffic is ncu dram read+write bytes per launch (profiles/)")},
+                         "algorithmic_bytes_def": ("bytes the pattern-SELL layout must read once per launch "
+                                                   "(slice metadata, deduplicated value/offset sequences, "
+                                                   "GENERAL tables) + x, y once: DESIGN.md §5"),
+                         "traffic_frac": (traffic / (spmv_ms * 1e-3) / 1e9 / hbm) if traffic else None,
+                         "binding_unit": ev.get("binding_unit"),
+                         "csr_equivalent": {"bytes_per_launch": int(info.bytes_spmv_finest), "gbs": csr_gbs,
+                                            "frac": csr_gbs / hbm,
+                                            "note": ("CSR-minimal bytes (12 B/nnz + vectors, SURVEY.md App. C) "
+                                                     "that a CSR kernel would have to move for the same "
+                                                     "product: an effective bandwidth, not a roofline "
+                                                     "fraction")}},
             "vcycle_layout_gbs": info.bytes_vcycle_layout / (vc_ms * 1e-3) / 1e9,
             "cpu_baseline": cpu,
             "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
@@ -391,43 +401,37 @@ def main():
 
 
 def run_reference(args, world, rank):
+    """The reference arm: the oracle port (the reference cannot be built here,
+    DESIGN.md §2) on all host threads.  Warm-up steps are bounded samples (the
+    first 3 PCG iterations: page-in and caches, there is nothing to compile);
+    every TIMED step is one complete solve."""
     if rank != 0:
         return
     case, desc, t_setup = build_workload(args.workload, args.threads, args.smoother)
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import oracle_ffi as orc
-    # Each step times a bounded sample (the first iterations of the same
-    # solve); the per-iteration cost is extrapolated to the full solve's
-    # iteration count, which the oracle reaches on the same hierarchy.
-    iters_full = int(os.environ.get("IG_REF_ITERS", "0")) or None
-    samples = []
-    sample_iters = max(1, args.cpu_sample_iters // 2)
-    for k in range(args.warmup + args.steps):
-        st, x, res, it, sec = orc.pcg(case.levels_c(), case.b, tol=1e-8, maxit=sample_iters, mode=orc.SEQ)
-        if k >= args.warmup:
-            samples.append(sec / (it + 1))
-    per_unit = statistics.median(samples)
-    if iters_full is None:
-        # Oracle (sequential-order) iteration counts of the full solves,
-        # pinned by tests/test_thb.py, tests/test_gpu_configs.py and the C4 golden.
-        iters_full = {"c1": 25, "c2": 27, "c2-1": 18, "c2-2": 27, "c2-3": 55, "c2-4": 106,
-                      "c3": 38, "c4": 115, "c5": 37}[args.workload]
-        if args.smoother == "ms":
-            st, _, _, iters_full, _ = orc.pcg(case.levels_c(), case.b, tol=1e-8, maxit=1000, mode=orc.SEQ)
-    t_full = per_unit * (iters_full + 1)
-    v = case.n / t_full
+    for _ in range(args.warmup):
+        oracle_solve(case, maxit=3)
+    secs, its = [], []
+    for _ in range(args.steps):
+        st, it, sec, th = oracle_solve(case)
+        assert st == 0, f"oracle solve did not converge (status {st})"
+        secs.append(sec)
+        its.append(it)
+    t = sum(secs) / len(secs)
+    v = case.n / t
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded immersed geometry, host-assembled operator (penalty Dirichlet), f=1",
-            "config": {"workload": desc, "n_dofs": case.n, "levels": case.n_levels, "tol": 1e-8,
-                       "iterations": iters_full},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-                             "sample": (f"oracle/liboracle.so single-threaded (the reference's solve is "
-                                        f"single-threaded, SURVEY.md §0.1): {sample_iters} PCG iterations per "
-                                        f"step, median per-iteration time extrapolated to {iters_full} "
-                                        f"iterations")},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": common_config(desc, case, world),
+            "iterations": its[0], "complete_solves_timed": len(secs),
+            "solve_seconds": {"min": min(secs), "median": statistics.median(secs), "max": max(secs)},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": th, "kind": "port",
+                             "sample": (f"{len(secs)} complete solves ({its[0]} PCG iterations each) of "
+                                        f"oracle/liboracle.so, the C restatement of the reference's solve "
+                                        f"(sequential-order dots), on {th} host threads; warm-up steps = "
+                                        f"the first 3 iterations")},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup_seconds": {"host_setup": t_setup}}
     print(json.dumps(line), flush=True)
 
 

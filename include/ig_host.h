@@ -81,6 +81,13 @@ int igh_assembly_payload(const igh_case *c, ig_assembly *out);
 int igh_prefilter_blocks(const igh_case *c, int32_t level, int32_t *n_blocks,
                          const int32_t **blk_ptr, const int32_t **blk_dofs);
 int igh_get_info(const igh_case *c, igh_info *out);
+/* Finest level, per DOF: physical volume of the DOF's support divided by the
+ * volume of its untrimmed support cells (1 = support entirely inside the
+ * domain; sliver DOFs near a cut boundary -> 0).  out: n doubles.  Built
+ * uniform (B-spline / Lagrange) cases only; THB and .igh-read cases return
+ * IG_UNSUPPORTED.  Used by the parity tests to exclude sliver DOFs (whose
+ * coefficients reach 1e19 on C4) from per-DOF error checks. */
+int igh_support_fraction(const igh_case *c, double *out);
 /* Kept anchors of level l as untrimmed tensor indices (ax, ay, az) -> n x 3. */
 int igh_anchors(const igh_case *c, int32_t level, int32_t *out_xyz);
 int igh_write(const igh_case *c, const char *path);

@@ -2,14 +2,34 @@
  * oracle.c — CPU restatement of the reference's solve phase.  TEST
  * INFRASTRUCTURE ONLY (see oracle.h): the checker for the GPU path and the
  * timed CPU baseline; never linked into the product.
+ *
+ * Threading: the row-, block- and chunk-parallel loops below (OpenMP) change
+ * no arithmetic.  Every output value is produced by exactly one thread with
+ * the same operands in the same order as the sequential loop it replaces
+ * (per-row SpMV sums, per-DOF sums over ascending blocks / ascending rows of
+ * R, per-chunk dot trees); only ORC_SEQ dots stay sequential.  So the result
+ * is bit-identical for every thread count (tests/test_oracle.py checks 1 vs
+ * many threads), and the many-thread run is the CPU baseline "with all the
+ * host threads it can use".
  */
 #define _POSIX_C_SOURCE 199309L
 #include "oracle.h"
 
+#include <limits.h>
 #include <math.h>
+#include <omp.h>
 #include <stdlib.h>
 #include <string.h>
 #include <time.h>
+
+void orc_set_threads(int n) { omp_set_num_threads(n > 0 ? n : omp_get_num_procs()); }
+int orc_get_threads(void) { return omp_get_max_threads(); }
+
+/* [lo, hi) slice t of T of the index range [0, n). */
+static void slice_of(int64_t n, int t, int T, int64_t *lo, int64_t *hi) {
+  *lo = n * t / T;
+  *hi = n * (t + 1) / T;
+}
 
 /* ---------------------------------------------------------- reductions -- */
 
@@ -50,6 +70,7 @@ double orc_dot(int mode, int64_t n, const double *a, const double *b) {
   }
   const int64_t nc = (n + 255) / 256;
   double *P = (double *)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1));
+#pragma omp parallel for schedule(static) if (nc > 64)
   for (int64_t c = 0; c < nc; ++c) {
     double v[256];
     for (int t = 0; t < 256; ++t) {
@@ -66,6 +87,7 @@ double orc_dot(int mode, int64_t n, const double *a, const double *b) {
 /* ------------------------------------------------------------- sparse --- */
 
 void orc_spmv(const ig_csr *A, const double *x, double *y, int resid) {
+#pragma omp parallel for schedule(static, 256) if (A->n_rows > 4096)
   for (int32_t i = 0; i < A->n_rows; ++i) {
     double acc = 0.0;
     for (int32_t k = A->row_ptr[i]; k < A->row_ptr[i + 1]; ++k) acc = acc + A->val[k] * x[A->col_idx[k]];
@@ -74,14 +96,39 @@ void orc_spmv(const ig_csr *A, const double *x, double *y, int resid) {
 }
 
 void orc_spmv_t(const ig_csr *A, const double *x, double *y) {
-  for (int32_t j = 0; j < A->n_cols; ++j) y[j] = 0.0;
-  for (int32_t c = 0; c < A->n_rows; ++c) {
-    const double xc = x[c];
+  /* y[f] = sum over rows c ascending (then k ascending) of A(c,f) x[c].  Each
+   * thread owns a contiguous range of f and walks the rows whose column
+   * span meets it, so every y[f] is summed in the sequential order. */
+  const int32_t nr = A->n_rows, ncol = A->n_cols;
+  int32_t *cmin = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nr > 0 ? nr : 1));
+  int32_t *cmax = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nr > 0 ? nr : 1));
+#pragma omp parallel for schedule(static) if (nr > 4096)
+  for (int32_t c = 0; c < nr; ++c) {
+    int32_t lo = INT_MAX, hi = -1;
     for (int32_t k = A->row_ptr[c]; k < A->row_ptr[c + 1]; ++k) {
       const int32_t f = A->col_idx[k];
-      y[f] = y[f] + A->val[k] * xc;
+      lo = f < lo ? f : lo;
+      hi = f > hi ? f : hi;
+    }
+    cmin[c] = lo;
+    cmax[c] = hi;
+  }
+#pragma omp parallel if (nr > 4096)
+  {
+    int64_t f0, f1;
+    slice_of(ncol, omp_get_thread_num(), omp_get_num_threads(), &f0, &f1);
+    for (int64_t j = f0; j < f1; ++j) y[j] = 0.0;
+    for (int32_t c = 0; c < nr; ++c) {
+      if (cmax[c] < f0 || cmin[c] >= f1) continue;
+      const double xc = x[c];
+      for (int32_t k = A->row_ptr[c]; k < A->row_ptr[c + 1]; ++k) {
+        const int32_t f = A->col_idx[k];
+        if (f >= f0 && f < f1) y[f] = y[f] + A->val[k] * xc;
+      }
     }
   }
+  free(cmin);
+  free(cmax);
 }
 
 /* --------------------------------------------------------- block solves -- */
@@ -107,20 +154,50 @@ static void tri_solve(int s, int ld, const double *L, double *y) {
 static void llt_solve(int s, const double *L, double *y) { tri_solve(s, s, L, y); }
 
 void orc_as_apply(const ig_level *lv, int32_t n, const double *r, double *x) {
+  /* x[d] = gamma * (0 + sum over blocks b ascending of (L_b^-T L_b^-1 P_b^T r)_d).
+   * Phase 1 solves every block into Y (block-parallel); phase 2 gives each
+   * thread a DOF range and adds the block results in ascending block order,
+   * exactly the sequential accumulation. */
   const ig_blocks *B = &lv->blocks;
-  for (int32_t i = 0; i < n; ++i) x[i] = 0.0;
-  double y[1024];
-  for (int32_t b = 0; b < B->n_blocks; ++b) {
+  const int32_t nb = B->n_blocks;
+  const int64_t tot = nb > 0 ? B->blk_ptr[nb] : 0;
+  double *Y = (double *)malloc(sizeof(double) * (size_t)(tot > 0 ? tot : 1));
+  int32_t *bmin = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nb > 0 ? nb : 1));
+  int32_t *bmax = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nb > 0 ? nb : 1));
+#pragma omp parallel for schedule(dynamic, 512) if (nb > 2048)
+  for (int32_t b = 0; b < nb; ++b) {
     const int32_t o = B->blk_ptr[b];
     const int s = B->blk_ptr[b + 1] - o;
-    for (int i = 0; i < s; ++i) y[i] = r[B->blk_dofs[o + i]];
-    llt_solve(s, B->fac + B->fac_ptr[b], y);
+    int32_t lo = INT_MAX, hi = -1;
     for (int i = 0; i < s; ++i) {
       const int32_t d = B->blk_dofs[o + i];
-      x[d] = x[d] + y[i];
+      Y[o + i] = r[d];
+      lo = d < lo ? d : lo;
+      hi = d > hi ? d : hi;
     }
+    llt_solve(s, B->fac + B->fac_ptr[b], Y + o);
+    bmin[b] = lo;
+    bmax[b] = hi;
   }
-  for (int32_t i = 0; i < n; ++i) x[i] = lv->gamma * x[i];
+#pragma omp parallel if (nb > 2048)
+  {
+    int64_t d0, d1;
+    slice_of(n, omp_get_thread_num(), omp_get_num_threads(), &d0, &d1);
+    for (int64_t i = d0; i < d1; ++i) x[i] = 0.0;
+    for (int32_t b = 0; b < nb; ++b) {
+      if (bmax[b] < d0 || bmin[b] >= d1) continue;
+      const int32_t o = B->blk_ptr[b];
+      const int s = B->blk_ptr[b + 1] - o;
+      for (int i = 0; i < s; ++i) {
+        const int32_t d = B->blk_dofs[o + i];
+        if (d >= d0 && d < d1) x[d] = x[d] + Y[o + i];
+      }
+    }
+    for (int64_t i = d0; i < d1; ++i) x[i] = lv->gamma * x[i];
+  }
+  free(Y);
+  free(bmin);
+  free(bmax);
 }
 
 /* Colored multiplicative sweep (smoothers.cpp:186-208).  The residual `cur`
@@ -133,7 +210,8 @@ void orc_ms_apply(const ig_level *lv, int32_t n, const double *r, double *x, int
   const int C = B->n_colors;
   double *cur = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
   double *delta = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
-  double y[1024];
+  const int par = n > 4096;
+#pragma omp parallel for schedule(static) if (par)
   for (int32_t i = 0; i < n; ++i) {
     x[i] = 0.0;
     cur[i] = r[i];
@@ -141,9 +219,14 @@ void orc_ms_apply(const ig_level *lv, int32_t n, const double *r, double *x, int
   for (int step = 0; step < C; ++step) {
     const int col = dir == 0 ? C - 1 - step : step;
     int any = 0;
+#pragma omp parallel for schedule(static) if (par)
     for (int32_t i = 0; i < n; ++i) delta[i] = 0.0;
+    /* Same-colour blocks touch disjoint DOFs: block-parallel, each delta[d]
+     * written by one block as 0 + y. */
+#pragma omp parallel for schedule(dynamic, 512) reduction(| : any) if (par)
     for (int32_t b = 0; b < B->n_blocks; ++b) {
       if (B->color_of[b] != col) continue;
+      double y[1024];
       const int32_t o = B->blk_ptr[b];
       const int s = B->blk_ptr[b + 1] - o;
       for (int i = 0; i < s; ++i) y[i] = cur[B->blk_dofs[o + i]];
@@ -155,9 +238,11 @@ void orc_ms_apply(const ig_level *lv, int32_t n, const double *r, double *x, int
       any = 1;
     }
     if (!any) continue;
+#pragma omp parallel for schedule(static) if (par)
     for (int32_t i = 0; i < n; ++i) x[i] = x[i] + delta[i];
     if (step + 1 < C) orc_spmv(&lv->A, delta, cur, 1); /* cur -= A * delta */
   }
+#pragma omp parallel for schedule(static) if (par)
   for (int32_t i = 0; i < n; ++i) x[i] = lv->gamma * x[i];
   free(cur);
   free(delta);
@@ -205,9 +290,11 @@ int orc_vcycle_at(const ig_level *levels, int32_t n_levels, const ig_coarse *co,
   orc_spmv(&lv->R, res, rc, 0);                       /* R res                    */
   orc_vcycle_at(levels, n_levels, co, l - 1, rc, xc); /* coarse_x                 */
   orc_spmv_t(&lv->R, xc, tmp);                        /* correction = R^T coarse_x */
+#pragma omp parallel for schedule(static) if (n > 4096)
   for (int32_t i = 0; i < n; ++i) x[i] = x[i] + tmp[i];
   orc_spmv(&lv->A, tmp, res, 1);                      /* res -= A correction      */
   orc_smoother_apply(lv, n, res, tmp, 1);             /* S(res, Reverse)          */
+#pragma omp parallel for schedule(static) if (n > 4096)
   for (int32_t i = 0; i < n; ++i) x[i] = x[i] + tmp[i];
   free(res);
   free(tmp);
@@ -261,8 +348,11 @@ int orc_pcg(const ig_level *levels, int32_t n_levels, const ig_coarse *co, int m
       break;
     }
     const double alpha = rz / pap;
-    for (int32_t i = 0; i < n; ++i) x[i] = x[i] + alpha * p[i];
-    for (int32_t i = 0; i < n; ++i) r[i] = r[i] - alpha * ap[i];
+#pragma omp parallel for schedule(static) if (n > 4096)
+    for (int32_t i = 0; i < n; ++i) {
+      x[i] = x[i] + alpha * p[i];
+      r[i] = r[i] - alpha * ap[i];
+    }
     *iterations = k + 1;
     const double rel = sqrt(orc_dot(mode, n, r, r)) / bnorm;
     residuals[k + 1] = rel;
@@ -273,6 +363,7 @@ int orc_pcg(const ig_level *levels, int32_t n_levels, const ig_coarse *co, int m
     orc_vcycle_at(levels, n_levels, co, n_levels - 1, r, z);
     const double rz_next = orc_dot(mode, n, r, z);
     const double beta = rz_next / rz;
+#pragma omp parallel for schedule(static) if (n > 4096)
     for (int32_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
     rz = rz_next;
   }
@@ -329,6 +420,7 @@ int orc_richardson(const ig_level *levels, int32_t n_levels, const ig_coarse *co
       break;
     }
     orc_vcycle_at(levels, n_levels, co, n_levels - 1, r, dx);
+#pragma omp parallel for schedule(static) if (n > 4096)
     for (int32_t i = 0; i < n; ++i) x[i] = x[i] + dx[i];
     orc_spmv(A, dx, r, 1); /* r -= A dx */
   }

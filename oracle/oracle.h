@@ -7,7 +7,9 @@
  * (paper_1903_10977_b200/) links, loads or calls it.
  *
  * It consumes exactly the payload that crosses the drop-in boundary
- * (include/ig_gpu.h: ig_level[], ig_coarse) and restates, single-threaded:
+ * (include/ig_gpu.h: ig_level[], ig_coarse) and restates (OpenMP-parallel
+ * over rows / blocks / chunks with every value summed in the sequential
+ * order, so bit-identical for any thread count; see oracle.c):
  *   pcg              proj/src/solvers.cpp:17-71
  *   richardson       proj/src/solvers.cpp:73-120
  *   vcycle_at        proj/src/multigrid.cpp:90-108
@@ -42,6 +44,10 @@ extern "C" {
 #endif
 
 enum { ORC_SEQ = 0, ORC_GPU_ORDER = 1 };
+
+/* Thread count for the parallel loops (n <= 0: all processors). */
+void orc_set_threads(int n);
+int orc_get_threads(void);
 
 /* Canonical dot product (mode as above). */
 double orc_dot(int mode, int64_t n, const double *a, const double *b);

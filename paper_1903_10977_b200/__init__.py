@@ -459,6 +459,14 @@ class Case:
         piv = np.ctypeslib.as_array(co.piv, (max(n, 1),))[:n]
         return L, piv, co.rank
 
+    def support_fraction(self) -> np.ndarray:
+        """Finest level, per DOF: physical support volume / untrimmed support
+        cell volume (igh_support_fraction; uniform spaces only)."""
+        out = np.zeros(self.n)
+        _check(_ffi.host(), _ffi.host().igh_support_fraction(self._h, out.ctypes.data_as(C.POINTER(C.c_double))),
+               "support_fraction")
+        return out
+
     def anchors(self, l: int) -> np.ndarray:
         out = np.zeros((self.info.n[l], 3), np.int32)
         _check(_ffi.host(), _ffi.host().igh_anchors(self._h, l, out.ctypes.data_as(_ip)), "anchors")

@@ -124,6 +124,7 @@ def host() -> C.CDLL:
         lib.igh_assembly_payload.argtypes = [C.c_void_p, P(ig_assembly)]
         lib.igh_prefilter_blocks.argtypes = [C.c_void_p, i32, P(i32), P(P(i32)), P(P(i32))]
         lib.igh_get_info.argtypes = [C.c_void_p, P(igh_info)]
+        lib.igh_support_fraction.argtypes = [C.c_void_p, P(f64)]
         lib.igh_anchors.argtypes = [C.c_void_p, i32, P(i32)]
         lib.igh_write.argtypes = [C.c_void_p, C.c_char_p]
         lib.igh_read.argtypes = [C.c_char_p, P(C.c_void_p)]

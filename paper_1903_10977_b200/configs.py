@@ -87,11 +87,12 @@ def c4_geometry(seed: int = 1, r: float = 0.3) -> str:
     return f"complement(sphere({0.5 + dx!r}, {0.5 + dy!r}, {0.5 + dz!r}, {r!r}))"
 
 
-def c4(res: int = 128, levels: int = 6, threads: int = 0) -> CaseConfig:
+def c4(res: int = 128, levels: int = 6, threads: int = 0, seed: int = 1) -> CaseConfig:
     """3D cube minus sphere, 128^3, p=2, 6 levels (configs[3], the north star).
     Dirichlet on the sphere only (cube faces natural).  Cut-cell quadrature
-    depth 2 (octree) in 3D; see DESIGN.md."""
-    return CaseConfig(geometry=c4_geometry(1), dim=3, resolution=(res, res, res), degree=2, levels=levels,
+    depth 2 (octree) in 3D; see DESIGN.md.  `seed` draws the sphere offset
+    (the mesh/cut-independence family, tests/test_gpu_mesh_independence.py)."""
+    return CaseConfig(geometry=c4_geometry(seed), dim=3, resolution=(res, res, res), degree=2, levels=levels,
                       quad_depth=2, dirichlet_box_sides=False, smoother=SmootherConfig("additive-schwarz"),
                       threads=threads)
 
@@ -107,6 +108,11 @@ def c5(threads: int = 0, base: int = 128, levels: int = 6) -> CaseConfig:
     return CaseConfig(geometry=f"disc({c!r}, {c!r}, 0.4)", dim=2, resolution=(base, base, 1), family="thb",
                       degree=2, levels=levels, smoother=SmootherConfig("additive-schwarz"), threads=threads,
                       refine_passes=2, refine_circle=(c, c, 0.4), refine_dist=0.05)
+
+
+def c4_levels(res: int) -> int:
+    """Levels so the coarsest grid is 4 cells per axis (D7): 16 -> 3 ... 128 -> 6."""
+    return max(1, res.bit_length() - 2)
 
 
 CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}

@@ -591,6 +591,18 @@ Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& 
     }
   }
   out.eta = eta;
+  out.el_vol.assign(static_cast<size_t>(ne), 1.0);
+  for (size_t k = 0; k < special_list.size(); ++k) {
+    const int e = special_list[k];
+    if (s.el_tag[e] != kCut) continue;
+    if (dim == 2) {
+      double lo[3], hi[3];
+      g.cell_box(s.el_ix[e], s.el_iy[e], 0, lo, hi);
+      out.el_vol[e] = sdata[k].volume / ((hi[0] - lo[0]) * (hi[1] - lo[1]));
+    } else {
+      out.el_vol[e] = sdata[k].volume;
+    }
+  }
   const auto ta1 = tnow();
 
   // Element tables for the device row gather (same data, flattened).

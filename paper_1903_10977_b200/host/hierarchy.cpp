@@ -484,6 +484,8 @@ struct igh_case {
   std::vector<double> tabK, tabF;
   std::vector<int32_t> el_table;
   int32_t n_tables = 0;
+  // Finest level: physical support volume / untrimmed support cell volume per DOF.
+  std::vector<double> supp_frac;
   std::vector<double> gamma;
   std::vector<int32_t> kind;
   std::vector<double> coarseL;
@@ -743,6 +745,24 @@ int igh_build(const igh_config* cfg, igh_case** out) {
     c->rank = pstrf_lower(n0, c->coarseL.data(), c->piv.data(), 1e-14 * max_diag);
     const double t2 = now();
     c->b = std::move(as.b);
+    if (!thb && !as.el_vol.empty()) {
+      const Space& s = *c->spaces.back();
+      const int dim = s.grid.dim;
+      c->supp_frac.assign(static_cast<size_t>(s.n()), 0.0);
+      for (int a = 0; a < s.n(); ++a) {
+        int32_t ax[3];
+        anchor_xyz(s, a, ax);
+        double cells = 1.0;
+        for (int d = 0; d < dim; ++d) {
+          int lo, hi;
+          anchor_cells(s.family, ax[d], s.p, s.grid.res[d], lo, hi);
+          cells *= hi - lo + 1;
+        }
+        double v = 0.0;
+        for (int64_t k = s.supp_ptr[a]; k < s.supp_ptr[a + 1]; ++k) v += as.el_vol[s.supp_el[k]];
+        c->supp_frac[a] = v / cells;
+      }
+    }
     c->xyz.resize(L);
     for (int l = 0; l < L; ++l) {
       if (thb) {  // (ax, ay, hierarchy level)
@@ -772,6 +792,15 @@ int igh_build(const igh_config* cfg, igh_case** out) {
   } catch (const std::exception& e) {
     return fail(e.what());
   }
+}
+
+int igh_support_fraction(const igh_case* c, double* out) {
+  if (!c || !out) return fail("igh_support_fraction: null argument");
+  if (c->supp_frac.empty())
+    return fail("igh_support_fraction: only built uniform (B-spline / Lagrange) cases carry support fractions",
+                IG_UNSUPPORTED);
+  std::copy(c->supp_frac.begin(), c->supp_frac.end(), out);
+  return IG_OK;
 }
 
 int igh_prefilter_blocks(const igh_case* c, int32_t level, int32_t* n_blocks, const int32_t** blk_ptr,

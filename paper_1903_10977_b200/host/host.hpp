@@ -217,6 +217,8 @@ struct Assembled {
   std::vector<double> tabK, tabF;
   std::vector<int32_t> el_table;
   int32_t n_tables = 0;
+  // Physical volume fraction of every active element's cell (1 for Inside).
+  std::vector<double> el_vol;
 };
 
 Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& q,

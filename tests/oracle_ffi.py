@@ -37,8 +37,19 @@ def lib():
         L.orc_pcg.argtypes = [lvp, C.c_int32, cop, C.c_int, _dp, C.c_double, C.c_int32, _dp, _dp,
                               C.POINTER(C.c_int32), _dp]
         L.orc_richardson.argtypes = L.orc_pcg.argtypes
+        L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_get_threads.restype = C.c_int
         _lib = L
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """Oracle thread count (n <= 0: all processors); results do not depend on it."""
+    lib().orc_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return lib().orc_get_threads()
 
 
 def _p(a: np.ndarray):

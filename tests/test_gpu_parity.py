@@ -5,13 +5,16 @@ The device kernels fix every summation order to the one oracle.c documents,
 so against the oracle in GPU-order mode the results must be BIT-IDENTICAL
 (np.array_equal); against the sequential-reduction oracle they must meet the
 north-star tolerances: iterations +-1, residual history within 1e-9 relative
-over the first 10 iterations, final x within 1e-8 relative L2.
+over the first 10 iterations, final x within 1e-8 relative L2 AND in the
+energy norm AND per DOF on the non-sliver DOFs (tests/parity.py says why the
+relative L2 alone is vacuous on immersed 3D cases).
 """
 import numpy as np
 import pytest
 
 import oracle_ffi as orc
 from conftest import rng_vec
+from parity import assert_history_close, assert_solution_close
 
 pytestmark = pytest.mark.gpu
 
@@ -105,11 +108,8 @@ def test_pcg_tolerance_vs_sequential_oracle(request, name):
     x, rep = pcg(h.A, b, h, tol=1e-8, maxit=1000)
     st, xo, ro, it, _ = orc.pcg(lv, b, tol=1e-8, maxit=1000, mode=orc.SEQ)
     assert st == 0
-    assert abs(rep.iterations - it) <= 1
-    k = min(11, len(ro), len(rep.residuals))
-    rg = np.array(rep.residuals[:k])
-    assert np.all(np.abs(rg - ro[:k]) <= RES_TOL * np.abs(ro[:k]))
-    assert np.linalg.norm(x - xo) <= X_TOL * np.linalg.norm(xo)
+    assert_history_close(rep.residuals, ro, rep.iterations, it, RES_TOL)
+    assert_solution_close(h.case, x, xo, X_TOL)
     # The report must not flatter the residual (proj/tests/test_solvers.cpp:82).
     A = h.A.to_scipy()
     assert np.linalg.norm(b - A @ x) / np.linalg.norm(b) <= 2e-8
@@ -231,9 +231,16 @@ def test_c4_full_size_matches_golden():
     assert [float(v).hex() for v in x[go["x_sample_idx"]]] == go["x_sample"]
     sq = g["seq"]
     rs = np.array([float.fromhex(v) for v in sq["residuals"]])
-    assert abs(rep.iterations - sq["iterations"]) <= 1
-    k = min(11, len(rs))
-    assert np.all(np.abs(np.array(rep.residuals[:k]) - rs[:k]) <= RES_TOL * rs[:k])
+    assert_history_close(rep.residuals, rs, rep.iterations, sq["iterations"], RES_TOL)
+    # x against a complete sequential-order oracle solve (all host threads;
+    # bit-identical to one thread), in relative L2, energy norm and per DOF on
+    # the non-sliver DOFs.
+    orc.set_threads(0)
+    st, xs, rso, its, _ = orc.pcg(case.levels_c(), case.b, tol=1e-8, maxit=1000, mode=orc.SEQ)
+    assert st == 0 and its == sq["iterations"]
+    assert [float(v).hex() for v in rso] == sq["residuals"]
+    err = assert_solution_close(case, x, xs, X_TOL)
+    print("C4 x vs SEQ oracle:", err)
     # true residual through the device SpMV (mode 1: b - A x)
     r = h.spmv(h.levels() - 1, x, 1, case.b)
     assert np.linalg.norm(r) / np.linalg.norm(case.b) <= 2e-8
