@@ -149,6 +149,8 @@ typedef struct {
   int64_t explicit_cols_A[16];
   int64_t bytes_spmv_finest_layout;
   int64_t bytes_vcycle_layout;
+  int32_t coarse_n;           /* coarsest level size and accepted pivots      */
+  int32_t coarse_rank;        /* (MgHierarchy::coarse_rank, multigrid.hpp:60) */
 } ig_info;
 
 /* Upload a hierarchy (copied; the host arrays may be freed afterwards).
@@ -183,7 +185,10 @@ int ig_level_spmv(ig_hier *h, int32_t level, const double *x, double *y,
 int ig_pcg(ig_hier *h, const double *b, double tol, int32_t maxit, double *x,
            double *residuals, int32_t *iterations, double *seconds);
 
-/* --- device-resident variants (async on ig_hier_stream) ----------------- */
+/* --- device-resident variants (async on ig_hier_stream) -----------------
+ * Device vectors must be 16-byte aligned (the kernels read x with 16-byte
+ * vector loads; cudaMalloc / torch allocations are); an unaligned pointer,
+ * e.g. a torch slice t[1:], returns IG_INVALID_ARGUMENT. */
 int ig_vcycle_device(ig_hier *h, const double *d_r, double *d_x);
 /* ig_level_spmv on device buffers (modes as ig_level_spmv); used to time the
  * dominant kernel in isolation. */
@@ -210,13 +215,6 @@ int ig_richardson(ig_hier *h, const double *b, double tol, int32_t maxit, double
 int ig_debug_vcycle_timeline(ig_hier *h, const double *d_r, double *d_x,
                              int32_t max_steps, float *ms, int32_t *levels,
                              char *labels, int32_t label_len, int32_t *count);
-
-/* Debug: run the persistent small-level kernel (levels 1..top, see
- * IG_OPT_TAIL_ROWS) once on d_r -> d_x with a %globaltimer stamp after every
- * phase (ns, written to stamps[0..*count)); IG_UNSUPPORTED if the hierarchy
- * has no such kernel. */
-int ig_debug_tail_profile(ig_hier *h, const double *d_r, double *d_x, uint64_t *stamps,
-                          int32_t cap, int32_t *count);
 
 /* --- the step before the path: global assembly -- */
 /* A = 0.5 (K + K^T) and b from the element tables on the device, bit-identical
@@ -291,30 +289,34 @@ int ig_hier_build(const ig_csr *A_fine, const ig_csr *R, const ig_blocks *prefil
 /* Thread-local message for the last non-OK status. */
 const char *ig_last_error(void);
 
-/* Build options (set before ig_hier_create; process-wide). 0 = default. */
+/* Options.  ig_set_option sets the process-wide DEFAULTS; ig_hier_create
+ * snapshots them into the new handle (later ig_set_option calls do not
+ * affect existing handles, so handles with different options coexist and
+ * run concurrently).  ig_hier_set_option changes the runtime options of one
+ * handle: IG_OPT_USE_GRAPH, IG_OPT_PDL, IG_OPT_RED_CTAS (layout options only
+ * act at creation and are rejected there with IG_INVALID_ARGUMENT). */
 #define IG_OPT_USE_GRAPH 1 /* 1 (default): CUDA-graph PCG loop; 0: host loop */
 #define IG_OPT_ROW_DICT 2  /* 1 (default): row-dictionary SELL; 0: plain SELL */
-#define IG_OPT_SPMV_VARIANT 3 /* SpMV batch/prefetch variant 0..3 (kernels.cuh SpmvVar) */
 #define IG_OPT_SMALL_ROWS 4   /* matrices with <= this many rows use the 8-lanes-per-row SpMV */
-#define IG_OPT_TMA_ROWS 5     /* matrices with >= this many rows use the compact SELL (0: never) */
-#define IG_OPT_TSELL_KERNEL 6 /* compact-SELL kernel: 0 direct thread-per-row, 1 TMA-staged */
 #define IG_OPT_PSELL 7        /* 1 (default): pattern SELL for matrices above IG_OPT_SMALL_ROWS rows */
-#define IG_OPT_TAIL_ROWS 8    /* levels (below the finest) up to this many rows run in one persistent kernel; 0 = off */
 #define IG_OPT_PDL 9          /* 1 (default): programmatic dependent launch for every kernel; 0: plain stream order */
-#define IG_OPT_TAIL_CLUSTER 10 /* persistent small-level kernel: 1 one 16-CTA cluster, 0 cooperative grid */
-#define IG_OPT_MS_LAZY 11     /* multiplicative sweep: 1 lazily updated residual, 0 (default) classic per-colour updates */
-#define IG_OPT_AS_SPLIT 12    /* additive smoother: 1 small blocks fused with singletons, 0 (default) all blocks on the side stream */
 #define IG_OPT_RED_CTAS 13    /* CTAs per SM of the canonical-reduction kernels (default 8) */
 #define IG_OPT_PSELL_CTAS 15  /* pattern-SELL SpMV occupancy cap, CTAs per SM (0 = registers decide) */
 #define IG_OPT_L2_ROWS 18       /* levels below the finest with <= this many DOFs in an L2-persisting arena (default 300000; 0 = off) */
-#define IG_OPT_CLUSTER_AS_ROWS 25 /* smoother levels with <= this many DOFs run as one 16-CTA cluster kernel */
 #define IG_OPT_PSELL_LINES2 27    /* 1 (default): pattern-SELL slices covering two x-lines (shared column runs) */
 #define IG_OPT_PSELL_CTAB 23     /* 1 (default): FAST2 value sequences of the pattern SELL from a constant-bank table */
 #define IG_OPT_GAL_SHORT 21      /* 1 (default): device Galerkin uses the prefetching SpGEMM when B rows have <= 32 entries */
-#define IG_OPT_FORK_ROWS 20      /* smoother levels below this many DOFs run the block solves on the main stream (no fork/join) */
 #define IG_OPT_L2_MB 19          /* size of that arena in MiB (default 64) */
-#define IG_OPT_FUSED_AS_ROWS 16 /* levels with <= this many DOFs run the additive smoother as one fused kernel (default 0: off, measured slower) */
 int ig_set_option(int32_t option, int64_t value);
+int ig_hier_set_option(ig_hier *h, int32_t option, int64_t value);
+
+/* pcg(A, b, precond) / richardson (solvers.hpp:51-59) multiply by the A they
+ * are given; the device solve multiplies by the finest A of the hierarchy.
+ * IG_OK when `a` is that operator -- the same arrays passed to ig_hier_create
+ * (or ig_hier_build), or a copy with identical sizes, row pointers, columns and
+ * value bits (content hash) -- else IG_INVALID_ARGUMENT.  The drop-in
+ * surfaces (immergrid_gpu::pcg, Python pcg) call it before solving. */
+int ig_hier_matches(ig_hier *h, const ig_csr *a);
 
 #ifdef __cplusplus
 }

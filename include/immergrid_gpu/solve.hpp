@@ -102,7 +102,7 @@ class MgHierarchy {
     ig_info info{};
     check(ig_hier_info(h, &info), "MgHierarchy::build_on_device");
     for (int l = 0; l < n_levels; ++l) m.n_.push_back(info.n[l]);
-    m.rank_ = -1;  // not reported by the device build; see ig_pstrf for the factor itself
+    m.rank_ = info.coarse_rank;  // the device pstrf's accepted pivots
     return m;
   }
 
@@ -125,17 +125,55 @@ class MgHierarchy {
   std::vector<int> n_;
 };
 
+enum class SweepDir { Forward, Reverse };  // smoothers.hpp:14
+
+// Smoother of one level (smoothers.hpp:67-85) as held by the device
+// hierarchy: apply(r, dir) and apply_symmetric(r).  A view: the hierarchy must
+// outlive it (as the reference's Smoother references its level's A).
+class Smoother {
+ public:
+  Smoother(const MgHierarchy& h, int level) : h_(&h), level_(level) {
+    if (level < 1 || level >= h.levels())
+      throw std::invalid_argument("Smoother: levels 1..levels()-1 carry a smoother (level 0 is the coarse solve)");
+  }
+  Vec apply(const Vec& r, SweepDir dir = SweepDir::Forward) const {
+    size_check(r);
+    Vec x(r.size());
+    check(ig_smoother_apply_dir(h_->handle(), level_, r.data(), x.data(), dir == SweepDir::Forward ? 0 : 1),
+          "Smoother::apply");
+    return x;
+  }
+  // Symmetric double iteration (M^-1 + M^-T - M^-T A M^-1) r (smoothers.cpp:211-214).
+  Vec apply_symmetric(const Vec& r) const {
+    size_check(r);
+    Vec x(r.size());
+    check(ig_smoother_apply_symmetric(h_->handle(), level_, r.data(), x.data()), "Smoother::apply_symmetric");
+    return x;
+  }
+  int level() const { return level_; }
+
+ private:
+  void size_check(const Vec& r) const {
+    if (static_cast<int>(r.size()) != h_->n(level_)) throw std::invalid_argument("Smoother: size mismatch");
+  }
+  const MgHierarchy* h_;
+  int level_;
+};
+
 // One-based wrapper (multigrid.hpp:73-75).
 inline Vec vcycle(const MgHierarchy& h, int ell, const Vec& r) { return h.vcycle_at(ell - 1, r); }
 
 // pcg(A, b, precond, tol, maxit) (solvers.hpp:51-53) with precond = the device
 // hierarchy built on A (the reference passes the same fine matrix to build and
-// pcg, runner.cpp:219,233); the whole iteration runs on the device.
+// pcg, runner.cpp:219,233); the whole iteration runs on the device and
+// multiplies by the hierarchy's finest A, so `a` must be that operator (the
+// same arrays or an identical copy: ig_hier_matches), else invalid_argument.
 inline std::pair<Vec, ConvergenceReport> pcg(const ig_csr& a, const Vec& b, const MgHierarchy& precond,
                                              double tol = 1e-10, int maxit = 1000) {
   const int n = precond.n(precond.levels() - 1);
   if (a.n_rows != a.n_cols || a.n_rows != static_cast<int>(b.size()) || n != a.n_rows)
     throw std::invalid_argument("pcg: dimension mismatch");
+  check(ig_hier_matches(precond.handle(), &a), "pcg");
   Vec x(b.size()), res(static_cast<size_t>(maxit) + 1);
   int32_t it = 0;
   double sec = 0.0;
@@ -158,6 +196,7 @@ inline std::pair<Vec, ConvergenceReport> richardson(const ig_csr& a, const Vec& 
   const int n = precond.n(precond.levels() - 1);
   if (a.n_rows != a.n_cols || a.n_rows != static_cast<int>(b.size()) || n != a.n_rows)
     throw std::invalid_argument("richardson: dimension mismatch");
+  check(ig_hier_matches(precond.handle(), &a), "richardson");
   Vec x(b.size()), res(static_cast<size_t>(maxit) + 1);
   int32_t it = 0;
   double sec = 0.0;

@@ -567,10 +567,10 @@ class MgHierarchy:
         self._lv = lv
         self._n = [lv[i].A.n_rows for i in range(nl)]
         self.A = SpMat.from_c(lv[nl - 1].A, case)
-        self._rank = co.contents.rank
         info = _ffi.ig_info()
         lib.ig_hier_info(self._h, C.byref(info))
         self.info = info
+        self._rank = info.coarse_rank  # the device pstrf's rank
         self.setup_seconds = (sec[0], sec[1], sec[2])
         return self
 
@@ -661,6 +661,39 @@ def vcycle(h: MgHierarchy, ell: int, r) -> np.ndarray:
     return h.vcycle_at(ell - 1, r)
 
 
+def _check_operator(a, precond: MgHierarchy, what: str):
+    """The reference multiplies by the `a` it is given (solvers.cpp:45); the
+    device solve multiplies by the hierarchy's finest A.  Accept `a` only when
+    it IS that operator: None, the same object, or a CSR (SpMat / scipy) with
+    identical sizes, row pointers, columns and value bits (ig_hier_matches)."""
+    fineA = precond.A
+    if a is None or a is fineA:
+        return
+    shape = getattr(a, "shape", None)
+    if shape is None or tuple(shape) != fineA.shape:
+        raise ValueError(f"{what}: dimension mismatch")
+    if isinstance(a, SpMat):
+        rp, ci, vv = a.row_ptr, a.col_idx, a.val
+    else:
+        try:
+            csr = a.tocsr()
+        except AttributeError:
+            raise TypeError(f"{what}: `a` must be the CSR operator the hierarchy was built on") from None
+        rp, ci, vv = csr.indptr, csr.indices, csr.data
+    rp = np.ascontiguousarray(rp, np.int32)
+    ci = np.ascontiguousarray(ci, np.int32)
+    vv = np.ascontiguousarray(vv, np.float64)
+    m = _ffi.ig_csr()
+    m.n_rows, m.n_cols = shape
+    m.nnz = int(rp[-1])
+    m.row_ptr = rp.ctypes.data_as(C.POINTER(C.c_int32))
+    m.col_idx = ci.ctypes.data_as(C.POINTER(C.c_int32))
+    m.val = vv.ctypes.data_as(_dp)
+    lib = _ffi.gpu()
+    if lib.ig_hier_matches(precond.handle, C.byref(m)) != _ffi.IG_OK:
+        raise ValueError(f"{what}: {lib.ig_last_error().decode()}")
+
+
 def pcg(a, b, precond: MgHierarchy, tol: float = 1e-10, maxit: int = 1000):
     """Preconditioned CG with zero initial guess (solvers.cpp:17-71), run
     entirely on the device.  ``precond`` must be the GPU MgHierarchy built on
@@ -670,10 +703,7 @@ def pcg(a, b, precond: MgHierarchy, tol: float = 1e-10, maxit: int = 1000):
     if not isinstance(precond, MgHierarchy):
         raise TypeError("pcg: the preconditioner must be a device MgHierarchy (no CPU fallback)")
     fineA = precond.A
-    if a is not None and a is not fineA:
-        shape = getattr(a, "shape", None)
-        if shape is None or tuple(shape) != fineA.shape:
-            raise ValueError("pcg: dimension mismatch")
+    _check_operator(a, precond, "pcg")
     n = fineA.rows()
     if fineA.rows() != fineA.cols() or np.shape(b) != (n,):
         raise ValueError("pcg: dimension mismatch")
@@ -706,8 +736,7 @@ def richardson(a, b, precond: MgHierarchy, tol: float = 1e-10, maxit: int = 1000
         raise TypeError("richardson: the preconditioner must be a device MgHierarchy (no CPU fallback)")
     fineA = precond.A
     n = fineA.rows()
-    if a is not None and a is not fineA and tuple(getattr(a, "shape", ())) != fineA.shape:
-        raise ValueError("richardson: dimension mismatch")
+    _check_operator(a, precond, "richardson")
     if np.shape(b) != (n,):
         raise ValueError("richardson: dimension mismatch")
     bb = _as_f64(b, n)

@@ -51,7 +51,8 @@ class ig_info(C.Structure):
                 ("bytes_spmv_finest", i64), ("device_bytes", i64),
                 ("kernels_vcycle", i32), ("kernels_pcg_iter", i32),
                 ("explicit_vals_A", i64 * 16), ("explicit_cols_A", i64 * 16),
-                ("bytes_spmv_finest_layout", i64), ("bytes_vcycle_layout", i64)]
+                ("bytes_spmv_finest_layout", i64), ("bytes_vcycle_layout", i64),
+                ("coarse_n", i32), ("coarse_rank", i32)]
 
 
 class igh_config(C.Structure):
@@ -79,26 +80,16 @@ IG_OP_VCYCLE = 1
 IG_OP_SMOOTHER_SYMMETRIC = 2
 IG_OPT_USE_GRAPH = 1
 IG_OPT_ROW_DICT = 2
-IG_OPT_SPMV_VARIANT = 3
 IG_OPT_SMALL_ROWS = 4
-IG_OPT_TMA_ROWS = 5
-IG_OPT_TSELL_KERNEL = 6
 IG_OPT_PSELL = 7
-IG_OPT_TAIL_ROWS = 8
 IG_OPT_PDL = 9
-IG_OPT_TAIL_CLUSTER = 10
-IG_OPT_MS_LAZY = 11
-IG_OPT_AS_SPLIT = 12
 IG_OPT_RED_CTAS = 13
 IG_OPT_PSELL_CTAS = 15
-IG_OPT_FUSED_AS_ROWS = 16
 IG_OPT_L2_ROWS = 18
 IG_OPT_L2_MB = 19
-IG_OPT_FORK_ROWS = 20
 IG_OPT_GAL_SHORT = 21
 IG_OPT_PSELL_CTAB = 23
 IG_OPT_PSELL_LINES2 = 27
-IG_OPT_CLUSTER_AS_ROWS = 25
 
 _host = None
 _gpu = None
@@ -145,7 +136,7 @@ GPU_SYMBOLS = (
     "ig_pcg_result", "ig_last_error", "ig_set_option", "ig_richardson",
     "ig_smoother_apply_dir", "ig_smoother_apply_symmetric", "ig_galerkin_hierarchy", "ig_csr_free",
     "ig_factorize_blocks", "ig_blocks_free", "ig_pstrf", "ig_hier_build",
-    "ig_operator_columns", "ig_assemble",
+    "ig_operator_columns", "ig_assemble", "ig_hier_set_option", "ig_hier_matches",
 )
 
 
@@ -186,5 +177,7 @@ def gpu() -> C.CDLL:
         lib.ig_pcg_result.argtypes = [vp, dp, P(i32)]
         lib.ig_last_error.restype = C.c_char_p
         lib.ig_set_option.argtypes = [i32, i64]
+        lib.ig_hier_set_option.argtypes = [vp, i32, i64]
+        lib.ig_hier_matches.argtypes = [vp, P(ig_csr)]
         _gpu = lib
     return _gpu

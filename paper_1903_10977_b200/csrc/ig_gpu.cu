@@ -33,15 +33,12 @@
 #include "galerkin.cuh"
 #include "blockfac.cuh"
 #include "assemble.cuh"
-#include "spmv_tma.cuh"
-#include "vtail.cuh"
 
 using namespace igk;
 
 namespace {
 
 thread_local std::string g_err;
-int g_use_graph = 1;
 
 struct Error : std::runtime_error {
   int code;
@@ -58,7 +55,42 @@ struct Error : std::runtime_error {
 
 inline unsigned grid_of(int64_t n) { return static_cast<unsigned>((n + kCta - 1) / kCta); }
 
-int g_use_pdl = 1;  // programmatic dependent launch for every kernel (kernels.cuh: pdl_entry)
+// Options (include/ig_gpu.h IG_OPT_*).  ig_set_option writes the process-wide
+// DEFAULTS; every handle snapshots them at ig_hier_create (ig_hier::opt) and
+// ig_hier_set_option changes the runtime ones of one handle, so handles built
+// with different options coexist and run concurrently.  Code below reads
+// opt(): the options of the handle whose API call is running on this thread
+// (OptScope), else the defaults (handle-free entry points).
+struct Opts {
+  int use_graph = 1;     // CUDA-graph PCG / V-cycle (0: host-launched kernels)
+  int use_pdl = 1;       // programmatic dependent launch for every kernel (kernels.cuh: pdl_entry)
+  int use_dict = 1;      // row dictionary in the SELL layout
+  int small_rows = 12000;  // matrices up to this many rows use k_spmv_grp (profiles/option_sweep.py)
+  int red_ctas = 8;      // CTAs per SM of the canonical-reduction kernels (profiles/option_sweep.py 13)
+  int use_psell = 1;     // pattern SELL above small_rows
+  int psell_pairs = 1;   // FAST slices with two rows per lane (x reuse across a column run)
+  // Occupancy cap of the pattern-SELL kernels (CTAs per SM, 0 = registers
+  // decide), applied as unused dynamic shared memory.
+  int psell_ctas = 0;
+  int psell_ctab = 1;    // FAST2 value sequences from a constant-bank table
+  int psell_lines2 = 1;  // FAST4 slices (two x-lines per slice)
+  int gal_short = 1;     // prefetching SpGEMM for B rows <= 32 entries
+  // Levels below the finest with at most this many DOFs live in the
+  // L2-persisting arena (ig_hier::alloc); 0 = off.  Arena size l2_bytes.
+  // Measured (profiles/option_sweep.py 18/19): C4 V-cycle 903 -> 881 us, C3
+  // 424 -> 395 us; an arena above the device's persisting maximum (83 MB on
+  // B200) thrashes and gains nothing.
+  int32_t l2_rows = 300000;
+  size_t l2_bytes = size_t(64) << 20;
+};
+Opts g_defaults;
+thread_local const Opts* t_opts = nullptr;
+inline const Opts& opt() { return t_opts ? *t_opts : g_defaults; }
+struct OptScope {
+  const Opts* prev;
+  explicit OptScope(const Opts* o) : prev(t_opts) { t_opts = o; }
+  ~OptScope() { t_opts = prev; }
+};
 
 // Every kernel launch of the library: cudaLaunchKernelEx with programmatic
 // stream serialization, so consecutive kernels on a stream (and in the
@@ -73,7 +105,7 @@ void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStre
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = g_use_pdl ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = opt().use_pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
@@ -94,35 +126,6 @@ struct HostSell {
   int64_t explicit_cols = 0;  // nnz whose column is read from HBM
 };
 
-int g_use_dict = 1;
-int g_spmv_variant = 3;  // profiles/spmv_variants.py: best full-PCG time on C4
-int g_small_rows = 12000;  // matrices up to this many rows use k_spmv_grp (profiles/option_sweep.py)
-// Levels up to this many rows (below the finest) run in k_vtail; 0 = off.
-// Off by default: measured SLOWER than the graph-launched kernels with
-// programmatic dependent launch, both as a cooperative grid (C5 V-cycle 285
-// -> 538 us: 1.2 us grid barriers plus the slowest warp's latency chain per
-// phase) and as one 16-CTA cluster (0.6 us cluster barriers, but every phase
-// still waits for its slowest row: C5 243 -> 300 us, C4 1029 -> 1097 us with
-// only L1 + coarse inside; profiles/tail_profile.py, option_sweep.py 8).
-// In the graph consecutive small kernels overlap their launch and drain.
-int g_tail_rows = 0;
-int g_tail_cluster = 1;
-// Multiplicative sweep: 1 lazily updated residual (k_msl_*), 0 classic
-// per-colour updates (default).  The lazy form halves the kernel count but
-// each DOF walks its own row's colour groups with indirect Delta gathers
-// (uncoalesced): C4 V-cycle 9.3 -> 77 ms, C5 1.6 -> 7.1 ms.  Kept, off.
-int g_ms_lazy = 0;
-int g_red_ctas = 8;  // CTAs per SM of the canonical-reduction kernels (profiles/option_sweep.py 13)
-// Additive smoother: 1 = small groups (smax <= 4) fused with the singleton
-// DOFs on the main stream; 0 (default) = every block solve on the side
-// stream and the lean (28-register) singleton kernel on the main stream
-// (C4 PCG 115.8 -> 114.6 ms, C3 15.87 -> 15.21 ms, C2 +0.5 %).
-int g_split = 0;
-// Compact-SELL layouts (spmv_tma.cuh) measured SLOWER than the row-dictionary
-// SELL on C4 (finest SpMV 442 us direct / 410 us TMA-staged vs 303 us;
-// profiles/spmv_layouts.py), so they are off by default.
-int g_tma_rows = 0;        // matrices with at least this many rows use the compact layout (0 = never)
-int g_tsell_kernel = 0;    // compact layout kernel: 0 thread-per-row direct, 1 TMA-staged
 constexpr int kDictEntries = 8;
 
 uint64_t fnv(const void* p, size_t bytes, uint64_t h = 1469598103934665603ULL) {
@@ -188,7 +191,7 @@ HostSell to_sell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col,
   // Row dictionary: value sequences, then column-offset patterns among them.
   std::vector<int32_t> vd(static_cast<size_t>(std::max(nr, 1)), 0), od(static_cast<size_t>(std::max(nr, 1)), 0);
   std::vector<int32_t> vreps, oreps;
-  if (g_use_dict && nr >= 256) {
+  if (opt().use_dict && nr >= 256) {
     const int64_t min_count = std::max<int64_t>(64, nr / 200);
     std::vector<uint8_t> all(static_cast<size_t>(nr), 1);
     auto vkey = [&](int32_t i) {
@@ -251,34 +254,10 @@ HostSell to_sell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col,
 
 // ------------------------------------------------ pattern SELL (host) ------
 // Host image of spmv_psell.cuh's PSell.  See that header for the layout.
-int g_use_psell = 1;
-int g_psell_pairs = 1;  // FAST slices with two rows per lane (x reuse across a column run)
-// Occupancy cap of the pattern-SELL kernels (CTAs per SM, 0 = registers
-// decide), applied as unused dynamic shared memory: fewer resident warps keep
-// more of each warp's x lines in L1 (the gathers are L1-hit-rate bound).
-int g_psell_ctas = 0;
-int g_psell_ctab = 1;
-int g_psell_lines2 = 1;  // IG_OPT_PSELL_LINES2: FAST4 slices (two x-lines per slice)  // IG_OPT_PSELL_CTAB: FAST2 value sequences from a constant-bank table
-// Levels with at most this many DOFs run the additive smoother as one fused
-// kernel (kernels.cuh k_as_fused) instead of the fork/join split.  Off by
-// default: measured slower on every workload (C2 V-cycle 228 -> 272 us, C4
-// 907 -> 936 us with levels <= 300k rows fused): the split kernels already
-// overlap under PDL and the graph fork, and the fused kernel's phase-1 fence
-// + arrival + wait sits on the critical path of every application.
-int32_t g_fused_rows = 0;
-int32_t g_fork_rows = 0;  // IG_OPT_FORK_ROWS
-int32_t g_cluster_rows = 0;  // IG_OPT_CLUSTER_AS_ROWS: smoother levels up to this size run k_as_cluster
-int g_gal_short = 1;      // IG_OPT_GAL_SHORT: prefetching SpGEMM for B rows <= 32 entries
-// Levels below the finest with at most this many DOFs live in the L2-persisting
-// arena (ig_hier::alloc); 0 = off.  Arena size g_l2_bytes.
-// Measured (profiles/option_sweep.py 18/19): C4 V-cycle 903 -> 881 us, C3
-// 424 -> 395 us; an arena above the device's persisting maximum (83 MB on
-// B200) thrashes and gains nothing.
-int32_t g_l2_rows = 300000;
-size_t g_l2_bytes = size_t(64) << 20;
 size_t psell_smem() {
-  if (g_psell_ctas <= 0) return 0;
-  return static_cast<size_t>(std::max(0, 233472 / g_psell_ctas - 1024 - 1024)) & ~size_t(1023);
+  const int c = opt().psell_ctas;
+  if (c <= 0) return 0;
+  return static_cast<size_t>(std::max(0, 233472 / c - 1024 - 1024)) & ~size_t(1023);
 }
 constexpr int kPDictEntries = 32;
 constexpr int kPMinRun = 8;  // shorter runs of identical rows go to GENERAL slices
@@ -321,6 +300,47 @@ void parallel_rows(int32_t n, F fn) {
 inline uint64_t mix64(uint64_t h, uint64_t w) {
   h ^= w + 0x9E3779B97F4A7C15ULL + (h << 6) + (h >> 2);
   return h * 0xff51afd7ed558ccdULL;
+}
+
+// Content hash of a CSR operator (sizes, row pointers, columns, value bits):
+// fixed 65536-row chunks hashed in parallel, combined in chunk order, so the
+// value does not depend on the thread count.
+uint64_t csr_hash(const ig_csr& a) {
+  constexpr int32_t kRows = 4096;
+  const int32_t nr = a.n_rows;
+  const int32_t nch = (nr + kRows - 1) / kRows;
+  std::vector<uint64_t> part(static_cast<size_t>(std::max(nch, 1)), 0);
+  auto work = [&](int32_t c0, int32_t c1) {
+    for (int32_t c = c0; c < c1; ++c) {
+      uint64_t h = 0x243F6A8885A308D3ULL + static_cast<uint64_t>(c);
+      const int32_t r0 = c * kRows, r1 = std::min(nr, r0 + kRows);
+      for (int32_t i = r0; i < r1; ++i) {
+        h = mix64(h, static_cast<uint64_t>(a.row_ptr[i + 1] - a.row_ptr[i]));
+        for (int32_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+          uint64_t vb;
+          std::memcpy(&vb, &a.val[k], 8);
+          h = mix64(h, (static_cast<uint64_t>(static_cast<uint32_t>(a.col_idx[k])) << 32) ^ vb);
+        }
+      }
+      part[c] = h;
+    }
+  };
+  const int32_t hw = static_cast<int32_t>(std::max(1u, std::min(32u, std::thread::hardware_concurrency())));
+  if (nch < 16 || hw == 1) {
+    work(0, nch);
+  } else {
+    std::vector<std::thread> th;
+    const int32_t step = (nch + hw - 1) / hw;
+    for (int32_t t = 0; t < hw; ++t) {
+      const int32_t c0 = t * step, c1 = std::min(nch, c0 + step);
+      if (c0 < c1) th.emplace_back(work, c0, c1);
+    }
+    for (auto& x : th) x.join();
+  }
+  uint64_t h = mix64(static_cast<uint64_t>(a.n_rows), static_cast<uint64_t>(a.n_cols));
+  h = mix64(h, static_cast<uint64_t>(a.nnz));
+  for (uint64_t p : part) h = mix64(h, p);
+  return h;
 }
 
 // Returns false when the matrix does not fit the format (row longer than
@@ -553,7 +573,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
   // pattern).  FAST2 (unscaled base only: rows r and r+1 then see the same
   // column run shifted by one): pieces of up to 64 rows, an even count; the
   // odd remainder goes to FAST slices.
-  const bool f2ok = g_psell_pairs && s.smul == 1 && s.sshift == 0;
+  const bool f2ok = opt().psell_pairs && s.smul == 1 && s.sshift == 0;
   auto emit_piece = [&](int32_t a, int32_t b, int32_t rep) {
     if (b <= a) return;
     lmax_all = std::max(lmax_all, len(rep));
@@ -593,7 +613,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
   std::vector<uint8_t> is_b(nruns, 0);
   std::vector<int32_t> pairA(nruns, -1);  // B run -> its A run
   int64_t why[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (f2ok && g_psell_lines2 && nr == nc) {  // square operators only (k_pprolong has no two-line path)
+  if (f2ok && opt().psell_lines2 && nr == nc) {  // square operators only (k_pprolong has no two-line path)
     for (size_t r = 0; r < nruns; ++r) {
       const int32_t r0 = run_start[r], r1 = run_start[r + 1];
       if (r1 - r0 < kPMinRun || is_b[r] || len(r0) < 2) { ++why[0]; continue; }
@@ -637,7 +657,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
   }
   if (std::getenv("IG_TIMING"))
     std::fprintf(stderr, "[psell pairs] f2ok=%d lines2=%d runs=%zu: skipped %lld, no 2nd run %lld, past end %lld, partner taken %lld, partner short %lld, pattern differs %lld, overlap < 16 %lld, paired %lld\n",
-                 f2ok ? 1 : 0, g_psell_lines2, nruns, (long long)why[0], (long long)why[1], (long long)why[2], (long long)why[3],
+                 f2ok ? 1 : 0, opt().psell_lines2, nruns, (long long)why[0], (long long)why[1], (long long)why[2], (long long)why[3],
                  (long long)why[4], (long long)why[5], (long long)why[6], (long long)why[7]);
   std::map<std::pair<uint32_t, int32_t>, uint32_t> useg_of;  // (segment list, D) -> union list
   auto union_start = [&](int32_t rep, int32_t D) -> uint32_t {
@@ -724,7 +744,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
   // most rows, as long as they fit (kPValTab doubles); their slices read
   // values from the kernel-parameter table instead of V (pk bit 31, vbase =
   // table offset).
-  if (g_psell_ctab) {
+  if (opt().psell_ctab) {
     // FAST2 (rows = 2 x count) and FAST (rows = count) slices compete for the
     // table by the rows they cover; both read V[vbase ..] otherwise.
     std::unordered_map<uint32_t, std::pair<int64_t, int32_t>> use;  // vbase -> (rows, length)
@@ -790,9 +810,6 @@ struct DevSell {
   bool stream = false;
   int64_t nnz = 0, slots = 0;
   int64_t explicit_vals = 0, explicit_cols = 0;
-  bool has_t = false;  // TMA-staged compact layout present (large matrices)
-  TSell t{};
-  int64_t t_bytes = 0;  // matrix bytes of the compact layout (cols + vals)
   bool has_p = false;   // pattern-SELL layout present (spmv_psell.cuh)
   PSell p{};
   std::shared_ptr<PValTab> ptab;  // constant-bank value table (zeros when unused)
@@ -801,58 +818,6 @@ struct DevSell {
   int64_t n_fast = 0, n_general = 0;
   int64_t layout_matrix_bytes() const { return has_p ? p_bytes : 8 * explicit_vals + 4 * explicit_cols + 4 * int64_t(s.n_rows); }
 };
-
-// Compact TMA layout from the SELL image (spmv_tma.cuh: TSell).
-struct HostTSell {
-  std::vector<TSliceMeta> meta;
-  std::vector<int32_t> cols;
-  std::vector<double> vals;
-};
-
-HostTSell to_tsell(const HostSell& s) {
-  HostTSell t;
-  const int32_t nslice = (s.nr + kSell - 1) / kSell;
-  t.meta.resize(static_cast<size_t>(std::max(nslice, 1)));
-  for (int32_t sl = 0; sl < nslice; ++sl) {
-    TSliceMeta m{};
-    const int64_t w = (s.slice_ptr[sl + 1] - s.slice_ptr[sl]) / kSell;
-    m.nch = static_cast<int32_t>((w + kKC - 1) / kKC);
-    std::vector<int> cl, vl;  // lanes needing explicit cols / vals
-    for (int lane = 0; lane < kSell; ++lane) {
-      const int32_t row = sl * kSell + lane;
-      if (row >= s.nr) continue;
-      const int info = s.rowinfo[row];
-      if ((info & 0xffff) == 0) continue;
-      if (((info >> 24) & 0xff) == 0) {
-        m.cmask |= 1u << lane;
-        cl.push_back(lane);
-      }
-      if (((info >> 16) & 0xff) == 0) {
-        m.vmask |= 1u << lane;
-        vl.push_back(lane);
-      }
-    }
-    m.col_off = static_cast<int64_t>(t.cols.size());
-    m.val_off = static_cast<int64_t>(t.vals.size());
-    const int64_t kpad = static_cast<int64_t>(m.nch) * kKC;
-    t.cols.resize(t.cols.size() + static_cast<size_t>(kpad * cl.size()), 0);
-    t.vals.resize(t.vals.size() + static_cast<size_t>(kpad * vl.size()), 0.0);
-    for (int64_t k = 0; k < kpad; ++k) {
-      for (size_t j = 0; j < cl.size(); ++j) {
-        const int32_t row = sl * kSell + cl[j];
-        if (k < (s.rowinfo[row] & 0xffff))
-          t.cols[m.col_off + k * static_cast<int64_t>(cl.size()) + j] = s.col[s.slice_ptr[sl] + k * kSell + cl[j]];
-      }
-      for (size_t j = 0; j < vl.size(); ++j) {
-        const int32_t row = sl * kSell + vl[j];
-        if (k < (s.rowinfo[row] & 0xffff))
-          t.vals[m.val_off + k * static_cast<int64_t>(vl.size()) + j] = s.val[s.slice_ptr[sl] + k * kSell + vl[j]];
-      }
-    }
-    t.meta[sl] = m;
-  }
-  return t;
-}
 
 struct Level {
   int32_t n = 0;
@@ -879,13 +844,6 @@ struct Level {
   };
   std::vector<MsColor> colors;  // [colour]; empty colours have n_items == 0
   double *ms_cur = nullptr, *ms_delta = nullptr, *ms_x = nullptr;
-  // Lazily updated sweep (kernels.cuh LazyLoad / k_msl_*).
-  bool msl = false;
-  MslRows msl_rows{};
-  int32_t* msl_dptr = nullptr;
-  int2* msl_dlist = nullptr;
-  double* msl_delta = nullptr;
-  int64_t msl_entries = 0;
 };
 
 // Algorithmic byte counts (CSR-minimal traffic).
@@ -896,6 +854,11 @@ int64_t bytes_spmv(int64_t nr, int64_t nin, int64_t nnz, bool resid) {
 }  // namespace
 
 struct ig_hier {
+  Opts opts;              // snapshot of the defaults at ig_hier_create (ig_hier_set_option)
+  // The finest operator the handle was built on (ig_hier_matches): the
+  // caller's arrays and sizes, and a content hash for copies of it.
+  ig_csr fine_src{};
+  uint64_t fine_hash = 0;
   std::vector<Level> lv;  // [0] coarsest
   int32_t L = 0;
   int32_t n0 = 0, rank = 0;
@@ -904,23 +867,12 @@ struct ig_hier {
   int coarse_threads = 32;
   size_t coarse_smem = 0;
   int coarse_use_smem = 0;
-  // Persistent small-level V-cycle (vtail.cuh): levels 1..tail_top.
-  int tail_top = 0;
-  TailLevel* tail_lv = nullptr;  // device array [0 .. tail_top]
-  unsigned tail_grid = 0;
-  bool tail_cluster = false;
-  size_t tail_smem = 0;
-  bool tail_sm = false;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // block solves, forked from / joined into `stream`
   int num_sms = 148;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   PcgState* st = nullptr;
   double* partials = nullptr;
-  unsigned int* fused_ctr = nullptr;  // k_as_fused arrival counters (2)
-  unsigned fused_cap = 0;             // co-resident CTAs of k_as_fused (occupancy x SMs)
-  int32_t fused_rows = 0;             // levels with n <= this use k_as_fused
-  int32_t cluster_rows = 0;           // levels with n <= this use k_as_cluster
   double* residuals = nullptr;
   int32_t res_cap = 0;
   double *r = nullptr, *z = nullptr, *p = nullptr, *ap = nullptr;
@@ -983,29 +935,6 @@ struct ig_hier {
     d.slots = h.slice_ptr.back();
     d.explicit_vals = h.explicit_vals;
     d.explicit_cols = h.explicit_cols;
-    if (g_tma_rows > 0 && h.nr >= g_tma_rows) {
-      const HostTSell t = to_tsell(h);
-      d.has_t = true;
-      d.t.n_rows = h.nr;
-      d.t.n_slices = (h.nr + kSell - 1) / kSell;
-      d.t.n_chunks = static_cast<int32_t>((static_cast<int64_t>(h.nr) + kCta - 1) / kCta);
-      d.t.meta = upload(t.meta.data(), t.meta.size());
-      d.t.rowinfo = d.s.rowinfo;
-      d.t.cols = upload(t.cols.data(), t.cols.size());
-      d.t.vals = upload(t.vals.data(), t.vals.size());
-      d.t.dict_w = d.s.dict_w;
-      d.t.dval = d.s.dval;
-      d.t.doff = d.s.doff;
-      d.t_bytes = static_cast<int64_t>(t.cols.size()) * 4 + static_cast<int64_t>(t.vals.size()) * 8;
-      static bool attr_done = false;
-      if (!attr_done) {
-        CK(cudaFuncSetAttribute(k_spmv_tma<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem));
-        CK(cudaFuncSetAttribute(k_spmv_tma<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem));
-        CK(cudaFuncSetAttribute(k_spmv_tma<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem));
-        CK(cudaFuncSetAttribute(k_spmv_tma<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem));
-        attr_done = true;
-      }
-    }
     // Stream (evict-first) matrices far larger than L2; keep small ones cached.
     d.stream = d.slots * 12 > (int64_t(48) << 20);
     return d;
@@ -1014,7 +943,7 @@ struct ig_hier {
   // it fits), the row-dictionary SELL otherwise (and for the small levels,
   // which run k_spmv_grp on it).
   DevSell make_matrix(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, const double* val, int64_t nnz) {
-    if (g_use_psell && nr > g_small_rows) {
+    if (opt().use_psell && nr > opt().small_rows) {
       HostPSell hp;
       if (to_psell(nr, nc, ptr, col, val, hp)) {
         DevSell d;
@@ -1057,10 +986,17 @@ struct ig_hier {
     }
     return upload_sell(to_sell(nr, nc, ptr, col, val), nnz);
   }
-  ~ig_hier() {
+  // Cached graphs bake in the launch attributes (PDL) and grids: dropped when
+  // a runtime option of the handle changes.
+  void drop_graphs() {
     if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
     if (rich_exec) cudaGraphExecDestroy(rich_exec);
     for (auto& g : vc_graphs) cudaGraphExecDestroy(g.exec);
+    pcg_exec = rich_exec = nullptr;
+    vc_graphs.clear();
+  }
+  ~ig_hier() {
+    drop_graphs();
     for (void* p : allocs) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -1073,12 +1009,7 @@ struct ig_hier {
   // ------------------------------------------------------------ launches --
   template <int M, bool S, bool R>
   void spmv_var(unsigned g, const DevSell& A, const double* x, double* y, const double* rsrc, PcgState* s) {
-    switch (g_spmv_variant) {
-      case 1: launch(k_spmv<M, S, R, 1>, g, kCta, 0, stream, A.s, x, y, rsrc, s, partials); break;
-      case 2: launch(k_spmv<M, S, R, 2>, g, kCta, 0, stream, A.s, x, y, rsrc, s, partials); break;
-      case 3: launch(k_spmv<M, S, R, 3>, g, kCta, 0, stream, A.s, x, y, rsrc, s, partials); break;
-      default: launch(k_spmv<M, S, R, 0>, g, kCta, 0, stream, A.s, x, y, rsrc, s, partials); break;
-    }
+    launch(k_spmv<M, S, R>, g, kCta, 0, stream, A.s, x, y, rsrc, s, partials);
   }
   void spmv(const DevSell& A, int mode, const double* x, double* y, const double* rsrc,
             PcgState* s = nullptr, bool red = false) {
@@ -1105,28 +1036,7 @@ struct ig_hier {
       }
       return;
     }
-    if (A.has_t && g_tsell_kernel == 0) {  // large matrix: compact SELL, thread per row
-      if (red)
-        launch(k_spmv_cmp<0, true>, g, kCta, 0, stream, A.t, x, y, rsrc, s, partials);
-      else if (mode == 0)
-        launch(k_spmv_cmp<0, false>, g, kCta, 0, stream, A.t, x, y, rsrc, s, partials);
-      else
-        launch(k_spmv_cmp<1, false>, g, kCta, 0, stream, A.t, x, y, rsrc, s, partials);
-      CK(cudaGetLastError());
-      return;
-    }
-    if (A.has_t) {  // large matrix: TMA-staged compact SELL, persistent grid
-      const unsigned gt = static_cast<unsigned>(std::min<int64_t>(A.t.n_chunks, static_cast<int64_t>(num_sms) * 2));
-      if (red)
-        launch(k_spmv_tma<0, true>, gt, kCta, kTSmem, stream, A.t, x, y, rsrc, s, partials);
-      else if (mode == 0)
-        launch(k_spmv_tma<0, false>, gt, kCta, kTSmem, stream, A.t, x, y, rsrc, s, partials);
-      else
-        launch(k_spmv_tma<1, false>, gt, kCta, kTSmem, stream, A.t, x, y, rsrc, s, partials);
-      CK(cudaGetLastError());
-      return;
-    }
-    if (!red && A.s.n_rows <= g_small_rows) {  // latency-bound level: 8 lanes per row
+    if (!red && A.s.n_rows <= opt().small_rows) {  // latency-bound level: 8 lanes per row
       const unsigned gg = grid_of(static_cast<int64_t>(A.s.n_rows) * 8);
       if (mode == 0)
         launch(k_spmv_grp<0, 8>, gg, kCta, 0, stream, A.s, x, y, rsrc);
@@ -1146,12 +1056,7 @@ struct ig_hier {
   }
   template <bool S>
   void prolong_var(unsigned g, const Level& l, const double* xc, double* x, PcgState* s) {
-    switch (g_spmv_variant) {
-      case 1: launch(k_prolong<S, 1>, g, kCta, 0, stream, l.P.s, xc, l.cor, x, s); break;
-      case 2: launch(k_prolong<S, 2>, g, kCta, 0, stream, l.P.s, xc, l.cor, x, s); break;
-      case 3: launch(k_prolong<S, 3>, g, kCta, 0, stream, l.P.s, xc, l.cor, x, s); break;
-      default: launch(k_prolong<S, 0>, g, kCta, 0, stream, l.P.s, xc, l.cor, x, s); break;
-    }
+    launch(k_prolong<S>, g, kCta, 0, stream, l.P.s, xc, l.cor, x, s);
   }
   void prolong(const Level& l, const double* xc, double* x, PcgState* s) {
     const unsigned g = grid_of(l.P.s.n_rows);
@@ -1180,52 +1085,10 @@ struct ig_hier {
       ms_smoother(l, r, x, acc, s, rdot, dir < 0 ? (acc ? 1 : 0) : dir);
       return;
     }
-    if (l.n <= cluster_rows && !rdot) {  // small level: one cluster kernel (k_as_cluster)
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(kAsClusterCtas);
-      cfg.blockDim = dim3(kAsClusterThreads);
-      cfg.stream = stream;
-      cudaLaunchAttribute attr[2];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = kAsClusterCtas;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[1].val.programmaticStreamSerializationAllowed = g_use_pdl ? 1 : 0;
-      cfg.attrs = attr;
-      cfg.numAttrs = 2;
-      if (acc)
-        CK(cudaLaunchKernelEx(&cfg, k_as_cluster<true>, l.G, l.S, r, l.ybuf, x));
-      else
-        CK(cudaLaunchKernelEx(&cfg, k_as_cluster<false>, l.G, l.S, r, l.ybuf, x));
-      return;
-    }
-    if (l.n <= fused_rows) {  // one kernel: blocks, singletons, then lists (k_as_fused)
-      const int64_t need = std::max<int64_t>((static_cast<int64_t>(l.G.n_groups + l.G.n_wblocks) + 7) / 8,
-                                             (static_cast<int64_t>(l.n) + kCta - 1) / kCta);
-      const unsigned gf = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(need, fused_cap)));
-      if (acc)
-        launch(k_as_fused<true>, gf, kCta, 0, stream, l.G, l.S, r, l.ybuf, x, fused_ctr, s);
-      else
-        launch(k_as_fused<false>, gf, kCta, 0, stream, l.G, l.S, r, l.ybuf, x, fused_ctr, s);
-      CK(cudaGetLastError());
-      if (rdot) launch(k_pcg_rz, red_grid(l.n), kCta, 0, stream, l.n, rdot, x, s, partials);
-      return;
-    }
-    // Big groups (smax > 4) and warp blocks on the side stream; the small
-    // groups fused with the singleton DOFs on the main stream.
-    AsGroups big = l.G;
-    big.n_groups = g_split ? l.g_small : l.G.n_groups;
-    const int32_t n_small = l.G.n_groups - big.n_groups;
-    const bool multi = big.n_groups + big.n_wblocks > 0;
-    // Levels below g_fork_rows DOFs keep the block solves on the main stream
-    // (a serial PDL chain) instead of forking them onto the side stream.
-    const bool fork = multi && l.n >= g_fork_rows;
-    if (multi && !fork) {
-      const unsigned gb = static_cast<unsigned>((static_cast<int64_t>(big.n_groups + big.n_wblocks) * 32 + 127) / 128);
-      launch(k_as_blocks, gb, 128, 0, stream, big, r, l.ybuf, s);
-      CK(cudaGetLastError());
-    }
+    // Every block solve on the side stream (forked from / joined into the
+    // main stream); the singleton DOFs on the main stream meanwhile.
+    const AsGroups& big = l.G;
+    const bool fork = big.n_groups + big.n_wblocks > 0;
     if (fork) {
       CK(cudaEventRecord(ev_fork, stream));
       CK(cudaStreamWaitEvent(side, ev_fork, 0));
@@ -1235,16 +1098,10 @@ struct ig_hier {
       CK(cudaEventRecord(ev_join, side));
     }
     const unsigned g = grid_of(l.n);
-    const int32_t gctas = static_cast<int32_t>((static_cast<int64_t>(n_small) * 32 + kCta - 1) / kCta);
-    if (gctas == 0) {  // no small groups here (IG_OPT_AS_SPLIT 0): the lean singleton kernel
-      if (acc)
-        launch(k_as_simple<true>, g, kCta, 0, stream, l.S, r, x, s);
-      else
-        launch(k_as_simple<false>, g, kCta, 0, stream, l.S, r, x, s);
-    } else if (acc)
-      launch(k_as_small_simple<true>, g + gctas, kCta, 0, stream, l.G, big.n_groups, gctas, l.S, r, l.ybuf, x, s);
+    if (acc)
+      launch(k_as_simple<true>, g, kCta, 0, stream, l.S, r, x, s);
     else
-      launch(k_as_small_simple<false>, g + gctas, kCta, 0, stream, l.G, big.n_groups, gctas, l.S, r, l.ybuf, x, s);
+      launch(k_as_simple<false>, g, kCta, 0, stream, l.S, r, x, s);
     CK(cudaGetLastError());
     if (fork) CK(cudaStreamWaitEvent(stream, ev_join, 0));
     if (rdot) {
@@ -1270,35 +1127,12 @@ struct ig_hier {
   }
   // Grid of the canonical-reduction kernels (kernels.cuh chunk_reduce): at
   // most 4 CTAs per SM, each looping over 256-element chunks.
-  int red_ctas = g_red_ctas;
-  unsigned red_grid(int64_t n) const { return static_cast<unsigned>(std::min<int64_t>(grid_of(n), red_ctas * num_sms)); }
+  unsigned red_grid(int64_t n) const {
+    return static_cast<unsigned>(std::min<int64_t>(grid_of(n), static_cast<int64_t>(opt().red_ctas) * num_sms));
+  }
   void ms_smoother(const Level& l, const double* r, double* out, bool acc, PcgState* s, const double* rdot, int dir) {
     const int32_t n = l.n;
     const int C = static_cast<int>(l.colors.size());
-    if (l.msl) {
-      for (int step = 0; step < C; ++step) {
-        const int c = dir == 0 ? C - 1 - step : step;
-        const Level::MsColor& mc = l.colors[c];
-        if (mc.n_items == 0) continue;
-        LazyLoad ld;
-        ld.r = r;
-        ld.R = l.msl_rows;
-        ld.delta = l.msl_delta;
-        ld.color = c;
-        ld.dir = dir;
-        const unsigned gb = static_cast<unsigned>((static_cast<int64_t>(mc.n_items) * 32 + 127) / 128);
-        launch(k_msl_blocks, gb, 128, 0, stream, mc.G, ld, l.msl_delta, s);
-      }
-      const unsigned g = grid_of(n);
-      if (rdot) {
-        if (acc) launch(k_msl_finish<true, true>, red_grid(n), kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
-        else launch(k_msl_finish<false, true>, red_grid(n), kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
-      } else {
-        if (acc) launch(k_msl_finish<true, false>, g, kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
-        else launch(k_msl_finish<false, false>, g, kCta, 0, stream, n, l.gamma, dir, l.msl_dptr, l.msl_dlist, l.msl_delta, out, rdot, s, partials);
-      }
-      return;
-    }
     launch(k_ms_init, grid_of(n), kCta, 0, stream, n, r, l.ms_cur, l.ms_x, s);
     for (int step = 0; step < C; ++step) {
       const int c = dir == 0 ? C - 1 - step : step;
@@ -1334,51 +1168,7 @@ struct ig_hier {
   }
   // MgHierarchy::vcycle_at (multigrid.cpp:90-108).  rdot != null: PCG mode on
   // the finest level (the last kernel also reduces r . z).
-  void tail(int top, const double* r, double* x, unsigned long long* prof = nullptr, int debug_mode = 0) {
-    TailParams P;
-    P.prof = prof;
-    P.debug_mode = debug_mode;
-    P.lv = tail_lv;
-    P.top = top;
-    P.r_top = r;
-    P.x_top = x;
-    P.n0 = n0;
-    P.rank = rank;
-    P.Lp = Lp;
-    P.piv = piv;
-    void* args[] = {&P};
-    if (tail_cluster) {  // one thread-block cluster, cluster barriers
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(kTailCluster);
-      cfg.blockDim = dim3(kTailThreads);
-      cfg.dynamicSmemBytes = tail_smem;
-      cfg.stream = stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = kTailCluster;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      if (tail_sm)
-        CK(cudaLaunchKernelEx(&cfg, k_vtail<true, true>, P));
-      else
-        CK(cudaLaunchKernelEx(&cfg, k_vtail<false, true>, P));
-      return;
-    }
-    if (tail_sm)
-      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_vtail<true, false>), dim3(tail_grid), dim3(kTailThreads),
-                                     args, tail_smem, stream));
-    else
-      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_vtail<false, false>), dim3(tail_grid),
-                                     dim3(kTailThreads), args, tail_smem, stream));
-  }
   void vcycle(int l, const double* r, double* x, PcgState* s, const double* rdot) {
-    if (l > 0 && l <= tail_top && !rdot) {  // small levels: one persistent kernel
-      tail(l, r, x);
-      mark("tail", l);
-      return;
-    }
     if (l == 0) {
       coarse(r, x, s);
       if (rdot) {  // 1-level hierarchy inside PCG: r . z as a separate pass
@@ -1523,7 +1313,7 @@ struct ig_hier {
     hs.residuals = residuals;
     CK(cudaMemcpyAsync(st, &hs, sizeof(PcgState), cudaMemcpyHostToDevice, stream));
     const int32_t n = lv[L - 1].n;
-    if (g_use_graph) {
+    if (opt().use_graph) {
       if (!rich_exec) build_rich_graph();
       CK(cudaGraphLaunch(rich_exec, stream));
       return;
@@ -1571,7 +1361,7 @@ struct ig_hier {
       pcg_init(0, 0);
       return;
     }
-    if (g_use_graph) {
+    if (opt().use_graph) {
       if (!pcg_exec) build_pcg_graph();
       CK(cudaGraphLaunch(pcg_exec, stream));
     } else {
@@ -1610,6 +1400,11 @@ struct ig_hier {
 };
 
 namespace {
+
+// Device vectors handed to the *_device entry points are read with 16-byte
+// vector loads (pattern-SELL x pairs) and written by the same kernels that
+// write the library's own (cudaMalloc-aligned) buffers.
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 int fail(int code, const std::string& m) {
   g_err = m;
@@ -1900,106 +1695,6 @@ void build_ms(ig_hier& h, Level& L, const ig_level& src, const ig_csr& A) {
   L.ms_x = h.alloc<double>(n);
 }
 
-// Lazily updated multiplicative sweep (kernels.cuh LazyLoad): per colour the
-// block solves with their Delta positions in one pool; per row its entries
-// grouped by the colours of their columns (ascending colour, ascending
-// column); per DOF its (colour, pool position) list.
-void build_msl(ig_hier& h, Level& L, const ig_level& src, const ig_csr& A) {
-  const ig_blocks& B = src.blocks;
-  const int32_t n = L.n, nb = B.n_blocks;
-  if (nb <= 0 || !B.blk_ptr || !B.blk_dofs || !B.fac_ptr || !B.fac)
-    throw Error(IG_INVALID_ARGUMENT, "smoother: empty block layout");
-  if (B.n_colors <= 0 || !B.color_of) throw Error(IG_INVALID_ARGUMENT, "multiplicative smoother: no block colours");
-  const int C = B.n_colors;
-  L.ms = true;
-  L.msl = true;
-  L.gamma = src.gamma;
-  L.n_blocks = nb;
-  auto bsize = [&](int32_t b) { return B.blk_ptr[b + 1] - B.blk_ptr[b]; };
-  std::vector<std::vector<int32_t>> cb(static_cast<size_t>(C));
-  for (int32_t b = 0; b < nb; ++b) {
-    const int32_t s = bsize(b);
-    if (s <= 0) throw Error(IG_INVALID_ARGUMENT, "smoother: empty block");
-    if (s > 128) throw Error(IG_INVALID_ARGUMENT, "smoother: block larger than 128 DOFs");
-    if (B.color_of[b] < 0 || B.color_of[b] >= C) throw Error(IG_INVALID_ARGUMENT, "smoother: colour out of range");
-    for (int32_t i = B.blk_ptr[b]; i < B.blk_ptr[b + 1]; ++i)
-      if (B.blk_dofs[i] < 0 || B.blk_dofs[i] >= n) throw Error(IG_INVALID_ARGUMENT, "smoother: DOF out of range");
-    L.sum_s += s;
-    L.sum_s2 += static_cast<int64_t>(s) * s;
-    L.packed_F += static_cast<int64_t>(s) * (s + 1) / 2;
-    if (s > 1) ++L.n_multi;
-    cb[B.color_of[b]].push_back(b);
-  }
-  // Pool positions: colour by colour, blocks ascending, members in order.
-  std::vector<int32_t> ypos(static_cast<size_t>(nb), 0);
-  std::vector<std::vector<std::pair<int32_t, int32_t>>> dl(static_cast<size_t>(n));  // DOF -> (colour, pos)
-  int64_t pool = 0;
-  std::vector<int32_t> mark(static_cast<size_t>(n), -1);
-  L.colors.resize(static_cast<size_t>(C));
-  for (int c = 0; c < C; ++c) {
-    Level::MsColor& mc = L.colors[c];
-    if (cb[c].empty()) continue;
-    std::vector<int32_t> grouped, warped;
-    for (int32_t b : cb[c]) {
-      const int32_t s = bsize(b);
-      (s >= 9 && s <= 32 ? warped : grouped).push_back(b);
-      ypos[b] = static_cast<int32_t>(pool);
-      for (int32_t i = 0; i < s; ++i) {
-        const int32_t d = B.blk_dofs[B.blk_ptr[b] + i];
-        if (mark[d] == c) throw Error(IG_INVALID_ARGUMENT, "smoother: same-colour blocks share a DOF");
-        mark[d] = c;
-        dl[d].push_back({c, static_cast<int32_t>(pool + i)});
-      }
-      pool += s;
-      mc.n_dofs += s;
-    }
-    if (pool > INT32_MAX) throw Error(IG_INVALID_ARGUMENT, "smoother: too many block entries");
-    mc.G = build_groups(h, B, grouped, warped, ypos);
-    mc.n_items = mc.G.n_groups + mc.G.n_wblocks;
-  }
-  // Per DOF: (colour, pos) ascending colour (filled in colour order already).
-  std::vector<int32_t> dptr(static_cast<size_t>(n) + 1, 0);
-  std::vector<int2> dlist;
-  for (int32_t d = 0; d < n; ++d) {
-    for (const auto& [c, q] : dl[d]) dlist.push_back(make_int2(c, q));
-    dptr[d + 1] = static_cast<int32_t>(dlist.size());
-  }
-  // Per row: entries grouped by colour (ascending), columns ascending.
-  std::vector<int32_t> gptr(static_cast<size_t>(n) + 1, 0), epos;
-  std::vector<int4> ghead;
-  std::vector<double> eval;
-  std::vector<std::vector<std::pair<int32_t, double>>> bucket(static_cast<size_t>(C));
-  std::vector<int32_t> used;
-  for (int32_t d = 0; d < n; ++d) {
-    used.clear();
-    for (int32_t k = A.row_ptr[d]; k < A.row_ptr[d + 1]; ++k) {
-      const int32_t col = A.col_idx[k];
-      for (const auto& [c, q] : dl[col]) {
-        if (bucket[c].empty()) used.push_back(c);
-        bucket[c].push_back({q, A.val[k]});
-      }
-    }
-    std::sort(used.begin(), used.end());
-    for (int32_t c : used) {
-      ghead.push_back(make_int4(c, static_cast<int>(epos.size()), static_cast<int>(bucket[c].size()), 0));
-      for (const auto& [q, v] : bucket[c]) {
-        epos.push_back(q);
-        eval.push_back(v);
-      }
-      bucket[c].clear();
-    }
-    gptr[d + 1] = static_cast<int32_t>(ghead.size());
-    if (epos.size() > static_cast<size_t>(INT32_MAX)) throw Error(IG_UNSUPPORTED, "lazy sweep: too many entries");
-  }
-  L.msl_rows.gptr = h.upload(gptr.data(), gptr.size());
-  L.msl_rows.ghead = h.upload(ghead.data(), ghead.size());
-  L.msl_rows.epos = h.upload(epos.data(), epos.size());
-  L.msl_rows.eval = h.upload(eval.data(), eval.size());
-  L.msl_dptr = h.upload(dptr.data(), dptr.size());
-  L.msl_dlist = h.upload(dlist.data(), dlist.size());
-  L.msl_delta = h.alloc<double>(static_cast<size_t>(std::max<int64_t>(pool, 1)));
-  L.msl_entries = static_cast<int64_t>(epos.size());
-}
 
 }  // namespace
 
@@ -2009,58 +1704,43 @@ const char* ig_last_error(void) { return g_err.c_str(); }
 
 int ig_set_option(int32_t option, int64_t value) {
   if (option == IG_OPT_USE_GRAPH) {
-    g_use_graph = value != 0;
+    g_defaults.use_graph = value != 0;
     return IG_OK;
   }
   if (option == IG_OPT_ROW_DICT) {
-    g_use_dict = value != 0;
+    g_defaults.use_dict = value != 0;
     return IG_OK;
   }
   if (option == IG_OPT_RED_CTAS) {
     if (value < 1 || value > 64) return fail(IG_INVALID_ARGUMENT, "ig_set_option: reduction CTAs per SM in 1..64");
-    g_red_ctas = static_cast<int>(value);
-    return IG_OK;
-  }
-  if (option == IG_OPT_CLUSTER_AS_ROWS) {
-    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: cluster rows out of range");
-    g_cluster_rows = static_cast<int32_t>(value);
+    g_defaults.red_ctas = static_cast<int>(value);
     return IG_OK;
   }
   if (option == IG_OPT_PSELL_LINES2) {
-    g_psell_lines2 = value != 0;
+    g_defaults.psell_lines2 = value != 0;
     return IG_OK;
   }
   if (option == IG_OPT_PSELL_CTAB) {
-    g_psell_ctab = value != 0;
+    g_defaults.psell_ctab = value != 0;
     return IG_OK;
   }
   if (option == IG_OPT_GAL_SHORT) {
-    g_gal_short = value != 0;
-    return IG_OK;
-  }
-  if (option == IG_OPT_FORK_ROWS) {
-    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: fork rows out of range");
-    g_fork_rows = static_cast<int32_t>(value);
+    g_defaults.gal_short = value != 0;
     return IG_OK;
   }
   if (option == IG_OPT_L2_MB) {
     if (value < 1 || value > 4096) return fail(IG_INVALID_ARGUMENT, "ig_set_option: L2 arena MB in 1..4096");
-    g_l2_bytes = static_cast<size_t>(value) << 20;
+    g_defaults.l2_bytes = static_cast<size_t>(value) << 20;
     return IG_OK;
   }
   if (option == IG_OPT_L2_ROWS) {
     if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: L2 rows out of range");
-    g_l2_rows = static_cast<int32_t>(value);
-    return IG_OK;
-  }
-  if (option == IG_OPT_FUSED_AS_ROWS) {
-    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: fused smoother rows out of range");
-    g_fused_rows = static_cast<int32_t>(value);
+    g_defaults.l2_rows = static_cast<int32_t>(value);
     return IG_OK;
   }
   if (option == IG_OPT_PSELL_CTAS) {
     if (value < 0 || value > 8) return fail(IG_INVALID_ARGUMENT, "ig_set_option: pattern-SELL CTAs per SM in 0..8");
-    g_psell_ctas = static_cast<int>(value);
+    g_defaults.psell_ctas = static_cast<int>(value);
     const int sm = static_cast<int>(psell_smem());
     void (*ks[])(PSell, const double*, double*, const double*, const PcgState*, const PValTab) = {
         k_pspmv<0, true>, k_pspmv<0, false>, k_pspmv<1, true>, k_pspmv<1, false>};
@@ -2069,51 +1749,53 @@ int ig_set_option(int32_t option, int64_t value) {
     cudaFuncSetAttribute(k_pprolong<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     return IG_OK;
   }
-  if (option == IG_OPT_AS_SPLIT) {
-    g_split = value != 0;
-    return IG_OK;
-  }
-  if (option == IG_OPT_MS_LAZY) {
-    g_ms_lazy = value != 0;
-    return IG_OK;
-  }
-  if (option == IG_OPT_TAIL_CLUSTER) {
-    g_tail_cluster = value != 0;
-    return IG_OK;
-  }
   if (option == IG_OPT_PDL) {
-    g_use_pdl = value != 0;
-    return IG_OK;
-  }
-  if (option == IG_OPT_TAIL_ROWS) {
-    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: bad row threshold");
-    g_tail_rows = static_cast<int>(value);
+    g_defaults.use_pdl = value != 0;
     return IG_OK;
   }
   if (option == IG_OPT_PSELL) {
-    g_use_psell = value != 0;
-    return IG_OK;
-  }
-  if (option == IG_OPT_TSELL_KERNEL) {
-    g_tsell_kernel = value != 0;
-    return IG_OK;
-  }
-  if (option == IG_OPT_TMA_ROWS) {
-    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: bad row threshold");
-    g_tma_rows = static_cast<int>(value);
+    g_defaults.use_psell = value != 0;
     return IG_OK;
   }
   if (option == IG_OPT_SMALL_ROWS) {
     if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: bad row threshold");
-    g_small_rows = static_cast<int>(value);
-    return IG_OK;
-  }
-  if (option == IG_OPT_SPMV_VARIANT) {
-    if (value < 0 || value > 3) return fail(IG_INVALID_ARGUMENT, "ig_set_option: SpMV variant in 0..3");
-    g_spmv_variant = static_cast<int>(value);
+    g_defaults.small_rows = static_cast<int>(value);
     return IG_OK;
   }
   return fail(IG_INVALID_ARGUMENT, "ig_set_option: unknown option");
+}
+
+int ig_hier_matches(ig_hier* h, const ig_csr* a) {
+  if (!h || !a) return fail(IG_INVALID_ARGUMENT, "ig_hier_matches: null argument");
+  const ig_csr& f = h->fine_src;
+  if (a->n_rows != f.n_rows || a->n_cols != f.n_cols || a->nnz != f.nnz)
+    return fail(IG_INVALID_ARGUMENT, "the operator's dimensions / nnz differ from the hierarchy's finest A");
+  if (a->row_ptr == f.row_ptr && a->col_idx == f.col_idx && a->val == f.val) return IG_OK;
+  if (!a->row_ptr || !a->col_idx || !a->val) return fail(IG_INVALID_ARGUMENT, "ig_hier_matches: null arrays");
+  if (csr_hash(*a) != h->fine_hash)
+    return fail(IG_INVALID_ARGUMENT, "the operator differs from the finest A the hierarchy was built on "
+                                     "(the device solve multiplies by that A)");
+  return IG_OK;
+}
+
+int ig_hier_set_option(ig_hier* h, int32_t option, int64_t value) {
+  if (!h) return fail(IG_INVALID_ARGUMENT, "ig_hier_set_option: null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  Opts& o = h->opts;
+  if (option == IG_OPT_USE_GRAPH) {
+    o.use_graph = value != 0;
+  } else if (option == IG_OPT_PDL) {
+    o.use_pdl = value != 0;
+  } else if (option == IG_OPT_RED_CTAS) {
+    if (value < 1 || value > 64) return fail(IG_INVALID_ARGUMENT, "ig_hier_set_option: reduction CTAs per SM in 1..64");
+    o.red_ctas = static_cast<int>(value);
+  } else {
+    return fail(IG_INVALID_ARGUMENT,
+                "ig_hier_set_option: only IG_OPT_USE_GRAPH, IG_OPT_PDL and IG_OPT_RED_CTAS change after "
+                "ig_hier_create (layout options: ig_set_option before creating the handle)");
+  }
+  h->drop_graphs();
+  return IG_OK;
 }
 
 int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* coarse, ig_hier** out) {
@@ -2123,6 +1805,8 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     return fail(IG_INVALID_ARGUMENT, "ig_hier_create: need 1..16 levels and a coarse factor");
   return guarded([&] {
     auto h = std::make_unique<ig_hier>();
+    h->opts = g_defaults;
+    OptScope os_(&h->opts);
     h->L = n_levels;
     h->lv.resize(n_levels);
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
@@ -2134,17 +1818,21 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     CK(cudaEventCreate(&h->ev1));
     ig_info& I = h->info;
     I.n_levels = n_levels;
-    if (g_l2_rows > 0 && n_levels > 1) {
+    I.coarse_n = coarse->n;
+    I.coarse_rank = coarse->rank;
+    h->fine_src = levels[n_levels - 1].A;
+    h->fine_hash = csr_hash(levels[n_levels - 1].A);
+    if (opt().l2_rows > 0 && n_levels > 1) {
       void* p = nullptr;
-      CK(cudaMalloc(&p, g_l2_bytes));
+      CK(cudaMalloc(&p, opt().l2_bytes));
       h->allocs.push_back(p);
       h->arena = static_cast<char*>(p);
-      h->arena_cap = g_l2_bytes;
+      h->arena_cap = opt().l2_bytes;
     }
     for (int l = 0; l < n_levels; ++l) {
       const ig_level& s = levels[l];
       Level& L = h->lv[l];
-      h->arena_on = l < n_levels - 1 && s.A.n_rows <= g_l2_rows;
+      h->arena_on = l < n_levels - 1 && s.A.n_rows <= opt().l2_rows;
       check_csr(s.A, "A");
       if (s.A.n_rows != s.A.n_cols) throw Error(IG_INVALID_ARGUMENT, "A must be square");
       L.n = s.A.n_rows;
@@ -2175,9 +1863,7 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       const auto t3 = tnow();
       L.res = h->alloc<double>(L.n);
       L.cor = h->alloc<double>(L.n);
-      if (s.smoother_kind == IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ && g_ms_lazy)
-        build_msl(*h, L, s, s.A);
-      else if (s.smoother_kind == IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ)
+      if (s.smoother_kind == IG_SMOOTHER_MULTIPLICATIVE_SCHWARZ)
         build_ms(*h, L, s, s.A);
       else
         build_smoother(*h, L, s);
@@ -2263,34 +1949,6 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     h->hb = h->alloc<double>(nf);
     h->hx = h->alloc<double>(nf);
     h->partials = h->alloc<double>(grid_of(nf) + 1);
-    h->fused_ctr = h->alloc<unsigned int>(2);
-    CK(cudaMemset(h->fused_ctr, 0, 2 * sizeof(unsigned int)));
-    {
-      int occ0 = 0, occ1 = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, k_as_fused<false>, kCta, 0));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_as_fused<true>, kCta, 0));
-      h->fused_cap = static_cast<unsigned>(std::max(1, std::min(occ0, occ1)) * h->num_sms);
-      h->fused_rows = g_fused_rows;
-      h->cluster_rows = 0;
-      if (g_cluster_rows > 0) {
-        CK(cudaFuncSetAttribute(k_as_cluster<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        CK(cudaFuncSetAttribute(k_as_cluster<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(kAsClusterCtas);
-        cfg.blockDim = dim3(kAsClusterThreads);
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = kAsClusterCtas;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, k_as_cluster<false>, &cfg) == cudaSuccess && ncl >= 1)
-          h->cluster_rows = g_cluster_rows;
-        cudaGetLastError();
-      }
-    }
     h->st = h->alloc<PcgState>(1);
     CK(cudaMemset(h->st, 0, sizeof(PcgState)));
     h->ensure_residuals(1000);
@@ -2309,7 +1967,6 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       if (L.ms) {  // colored sweep: block solves + the colours' residual updates + init/finish
         as = 8 * L.packed_F + 16 * L.sum_s + 40 * n;
         for (const auto& mc : L.colors) as += 12 * mc.S.nnz + 16 * mc.n_dofs;
-        if (L.msl) as = 8 * L.packed_F + 16 * L.sum_s + 16 * L.msl_entries / 2 + 24 * n;  // ~half the entries per sweep
       }
       vc += 2 * bytes_spmv(n, n, L.A.nnz, true);
       vc += 2 * as + 8 * n;                                              // second application accumulates
@@ -2320,11 +1977,10 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       // smoother: [blocks] + simple + [complex | finish_red on the finest], twice;
       // plus SpMV-residual x2, restriction, prolongation
       int per_app = (L.n_multi > 0 ? 1 : 0) + 1 + (L.S.n_complex > 0 ? 1 : 0);
-      if (L.n <= h->fused_rows || L.n <= h->cluster_rows) per_app = 1;  // k_as_fused / k_as_cluster
       if (L.ms) {
         int ne = 0;
         for (const auto& mc : L.colors) ne += mc.n_items > 0 ? 1 : 0;
-        per_app = L.msl ? ne + 1 : 2 + 2 * ne - 1;  // lazy: blocks per colour + finish
+        per_app = 2 + 2 * ne - 1;
       }
       kv += 2 * per_app + 4 + (l == n_levels - 1 && !L.ms ? 1 : 0);  // finest: + r . z pass
       I.explicit_vals_A[l] = L.A.explicit_vals;
@@ -2341,76 +1997,6 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     I.bytes_pcg_iter = vc + I.bytes_spmv_finest + 80 * static_cast<int64_t>(nf);
     I.kernels_vcycle = kv;
     I.kernels_pcg_iter = kv + 3 + (F.A.has_p ? 1 : 0);  // + k_pap after a pattern-SELL A p
-    // Small levels below the finest: one cooperative persistent kernel.
-    if (g_tail_rows > 0 && h->rank <= kTailThreads) {
-      int top = 0;
-      for (int l = 1; l <= n_levels - 2 && h->lv[l].n <= g_tail_rows && h->lv[l].n <= g_small_rows; ++l) top = l;
-      int coop = 0;
-      CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, 0));
-      if (top > 0 && coop) {
-        std::vector<TailLevel> tl(static_cast<size_t>(top) + 1);
-        for (int l = 0; l <= top; ++l) {
-          const Level& Lv = h->lv[l];
-          TailLevel& t = tl[l];
-          t = TailLevel{};
-          t.n = Lv.n;
-          t.r_in = Lv.r_in;
-          t.x = Lv.x;
-          if (l == 0) continue;
-          t.A = Lv.A.s;
-          t.R = Lv.R.s;
-          t.P = Lv.P.s;
-          t.G = Lv.G;
-          t.S = Lv.S;
-          t.n_items = Lv.G.n_groups + Lv.G.n_wblocks;
-          t.res = Lv.res;
-          t.cor = Lv.cor;
-          t.ybuf = Lv.ybuf;
-        }
-        h->tail_lv = h->upload(tl.data(), tl.size());
-        h->tail_sm = h->coarse_use_smem != 0;
-        h->tail_smem = h->coarse_smem;
-        int max_optin = 0;
-        CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
-        const int cap = max_optin - 2048;  // headroom for the kernels' static shared memory
-        CK(cudaFuncSetAttribute(k_vtail<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
-        CK(cudaFuncSetAttribute(k_vtail<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
-        CK(cudaFuncSetAttribute(k_vtail<true, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        CK(cudaFuncSetAttribute(k_vtail<false, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        if (g_tail_cluster) {
-          cudaLaunchConfig_t cfg = {};
-          cfg.gridDim = dim3(kTailCluster);
-          cfg.blockDim = dim3(kTailThreads);
-          cfg.dynamicSmemBytes = h->tail_smem;
-          cudaLaunchAttribute attr[1];
-          attr[0].id = cudaLaunchAttributeClusterDimension;
-          attr[0].val.clusterDim.x = kTailCluster;
-          attr[0].val.clusterDim.y = 1;
-          attr[0].val.clusterDim.z = 1;
-          cfg.attrs = attr;
-          cfg.numAttrs = 1;
-          int nclusters = 0;
-          const cudaError_t e = h->tail_sm ? cudaOccupancyMaxActiveClusters(&nclusters, k_vtail<true, true>, &cfg)
-                                           : cudaOccupancyMaxActiveClusters(&nclusters, k_vtail<false, true>, &cfg);
-          if (e == cudaSuccess && nclusters >= 1) {
-            h->tail_cluster = true;
-            h->tail_grid = kTailCluster;
-            h->tail_top = top;
-          }
-          cudaGetLastError();
-        } else {
-          int occ = 0;
-          if (h->tail_sm)
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vtail<true, false>, kTailThreads, h->tail_smem));
-          else
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vtail<false, false>, kTailThreads, h->tail_smem));
-          if (occ >= 1) {
-            h->tail_grid = static_cast<unsigned>(h->num_sms * std::min(occ, 2));
-            h->tail_top = top;
-          }
-        }
-      }
-    }
     CK(cudaDeviceSynchronize());
     *out = h.release();
     return IG_OK;
@@ -2431,6 +2017,7 @@ int ig_vcycle_at(ig_hier* h, int32_t level, const double* r, double* x) {
   if (!h || !r || !x) return fail(IG_INVALID_ARGUMENT, "vcycle_at: null argument");
   if (level < 0 || level >= h->L) return fail(IG_INVALID_ARGUMENT, "vcycle_at: level out of range");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   return guarded([&] {
     Level& L = h->lv[level];
     CK(cudaMemcpyAsync(L.r_in, r, sizeof(double) * L.n, cudaMemcpyHostToDevice, h->stream));
@@ -2455,6 +2042,7 @@ int ig_smoother_apply(ig_hier* h, int32_t level, const double* r, double* x) {
   if (!h || !r || !x) return fail(IG_INVALID_ARGUMENT, "smoother_apply: null argument");
   if (level < 1 || level >= h->L) return fail(IG_INVALID_ARGUMENT, "smoother_apply: level has no smoother");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   return guarded([&] {
     Level& L = h->lv[level];
     CK(cudaMemcpyAsync(L.r_in, r, sizeof(double) * L.n, cudaMemcpyHostToDevice, h->stream));
@@ -2470,6 +2058,7 @@ int ig_smoother_apply_dir(ig_hier* h, int32_t level, const double* r, double* x,
   if (level < 1 || level >= h->L) return fail(IG_INVALID_ARGUMENT, "smoother_apply: level has no smoother");
   if (dir != 0 && dir != 1) return fail(IG_INVALID_ARGUMENT, "smoother_apply: dir must be 0 (Forward) or 1 (Reverse)");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   return guarded([&] {
     Level& L = h->lv[level];
     CK(cudaMemcpyAsync(L.r_in, r, sizeof(double) * L.n, cudaMemcpyHostToDevice, h->stream));
@@ -2484,6 +2073,7 @@ int ig_smoother_apply_symmetric(ig_hier* h, int32_t level, const double* r, doub
   if (!h || !r || !x) return fail(IG_INVALID_ARGUMENT, "smoother_apply_symmetric: null argument");
   if (level < 1 || level >= h->L) return fail(IG_INVALID_ARGUMENT, "smoother_apply_symmetric: level has no smoother");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   return guarded([&] {
     Level& L = h->lv[level];
     CK(cudaMemcpyAsync(L.r_in, r, sizeof(double) * L.n, cudaMemcpyHostToDevice, h->stream));
@@ -2502,6 +2092,7 @@ int ig_level_spmv(ig_hier* h, int32_t level, const double* x, double* y, int32_t
   if (mode < 0 || mode > 3) return fail(IG_INVALID_ARGUMENT, "level_spmv: bad mode");
   if (mode >= 2 && level == 0) return fail(IG_INVALID_ARGUMENT, "level_spmv: coarsest level has no R");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   return guarded([&] {
     Level& L = h->lv[level];
     const DevSell* M = nullptr;
@@ -2525,9 +2116,12 @@ int ig_level_spmv(ig_hier* h, int32_t level, const double* x, double* y, int32_t
 
 int ig_level_spmv_device(ig_hier* h, int32_t level, const double* d_x, double* d_y, int32_t mode) {
   if (!h || !d_x || !d_y) return fail(IG_INVALID_ARGUMENT, "level_spmv_device: null argument");
+  if (!aligned16(d_x) || !aligned16(d_y))
+    return fail(IG_INVALID_ARGUMENT, "level_spmv_device: device vectors must be 16-byte aligned");
   if (level < 0 || level >= h->L || mode < 0 || mode > 3 || (mode >= 2 && level == 0))
     return fail(IG_INVALID_ARGUMENT, "level_spmv_device: bad level or mode");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   return guarded([&] {
     Level& L = h->lv[level];
     if (mode <= 1 && level == 0 && h->L > 1)
@@ -2541,7 +2135,9 @@ int ig_level_spmv_device(ig_hier* h, int32_t level, const double* d_x, double* d
 int ig_debug_vcycle_timeline(ig_hier* h, const double* d_r, double* d_x, int32_t max_steps, float* ms,
                              int32_t* levels, char* labels, int32_t label_len, int32_t* count) {
   if (!h || !d_r || !d_x || !ms || !count) return fail(IG_INVALID_ARGUMENT, "timeline: null argument");
+  if (!aligned16(d_r) || !aligned16(d_x)) return fail(IG_INVALID_ARGUMENT, "timeline: device vectors must be 16-byte aligned");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   return guarded([&] {
     std::vector<ig_hier::Mark> tl;
     cudaEvent_t start;
@@ -2577,44 +2173,14 @@ int ig_debug_vcycle_timeline(ig_hier* h, const double* d_r, double* d_x, int32_t
   });
 }
 
-int ig_debug_tail_profile(ig_hier* h, const double* d_r, double* d_x, uint64_t* stamps, int32_t cap,
-                          int32_t* count) {
-  if (!h || !d_r || !d_x || !stamps || !count || cap == 0) return fail(IG_INVALID_ARGUMENT, "tail_profile: bad argument");
-  const bool spmv_only = cap < 0;  // undocumented profiling mode: only the descent SpMVs
-  if (spmv_only) cap = -cap;
-  std::lock_guard<std::mutex> lk(h->mu);
-  if (h->tail_top <= 0) return fail(IG_UNSUPPORTED, "tail_profile: no persistent small-level kernel");
-  return guarded([&] {
-    const int top = h->tail_top;
-    const size_t ns = 256 + 64 * static_cast<size_t>(h->tail_grid);
-    unsigned long long* dp = nullptr;
-    CK(cudaMalloc(&dp, ns * sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(dp, 0, ns * sizeof(unsigned long long), h->stream));
-    h->tail(top, d_r, d_x, dp, spmv_only ? 1 : 0);
-    std::vector<unsigned long long> hs(ns);
-    CK(cudaMemcpyAsync(hs.data(), dp, ns * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    cudaFree(dp);
-    int32_t k = 0;
-    while (k < 256 && k < cap && hs[k] != 0) {
-      stamps[k] = hs[k];
-      ++k;
-    }
-    *count = k;
-    // Then, if room: the grid size and per-CTA arrival times of each barrier.
-    if (cap >= static_cast<int32_t>(ns) + 1) {
-      stamps[256] = h->tail_grid;
-      for (size_t q = 256; q < ns; ++q) stamps[q + 1] = hs[q];
-    }
-    return IG_OK;
-  });
-}
-
 int ig_vcycle_device(ig_hier* h, const double* d_r, double* d_x) {
   if (!h || !d_r || !d_x) return fail(IG_INVALID_ARGUMENT, "vcycle_device: null argument");
+  if (!aligned16(d_r) || !aligned16(d_x))
+    return fail(IG_INVALID_ARGUMENT, "vcycle_device: device vectors must be 16-byte aligned");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   return guarded([&] {
-    if (!g_use_graph) {
+    if (!opt().use_graph) {
       h->vcycle(h->L - 1, d_r, d_x, nullptr, nullptr);
       return IG_OK;
     }
@@ -2637,7 +2203,10 @@ int ig_vcycle_device(ig_hier* h, const double* d_r, double* d_x) {
 
 int ig_pcg_device(ig_hier* h, const double* d_b, double tol, int32_t maxit, double* d_x) {
   if (!h || !d_b || !d_x) return fail(IG_INVALID_ARGUMENT, "pcg_device: null argument");
+  if (!aligned16(d_b) || !aligned16(d_x))
+    return fail(IG_INVALID_ARGUMENT, "pcg_device: device vectors must be 16-byte aligned");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   return guarded([&] {
     h->pcg_launch(d_b, d_x, tol, maxit);
     return IG_OK;
@@ -2647,6 +2216,7 @@ int ig_pcg_device(ig_hier* h, const double* d_b, double tol, int32_t maxit, doub
 int ig_pcg_result(ig_hier* h, double* residuals, int32_t* iterations) {
   if (!h) return fail(IG_INVALID_ARGUMENT, "pcg_result: null handle");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   return guarded([&] {
     const int s = h->pcg_collect(residuals, iterations);
     if (s == IG_NOT_CONVERGED) g_err = "pcg: no convergence within the iteration budget";
@@ -2660,6 +2230,7 @@ int ig_pcg(ig_hier* h, const double* b, double tol, int32_t maxit, double* x, do
   if (!h || !b || !x || !residuals || !iterations) return fail(IG_INVALID_ARGUMENT, "pcg: null argument");
   if (maxit < 0) return fail(IG_INVALID_ARGUMENT, "pcg: maxit must be >= 0");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   return guarded([&] {
     const int32_t n = h->lv[h->L - 1].n;
     CK(cudaMemcpyAsync(h->hb, b, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
@@ -2682,6 +2253,7 @@ int ig_richardson(ig_hier* h, const double* b, double tol, int32_t maxit, double
   if (!h || !b || !x || !residuals || !iterations) return fail(IG_INVALID_ARGUMENT, "richardson: null argument");
   if (maxit < 0) return fail(IG_INVALID_ARGUMENT, "richardson: maxit must be >= 0");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   return guarded([&] {
     const int32_t n = h->lv[h->L - 1].n;
     CK(cudaMemcpyAsync(h->hb, b, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
@@ -2808,7 +2380,7 @@ GalMat gal_spgemm(const GalMat& a, const GalMat& b, cudaStream_t st) {
     CK(cudaStreamSynchronize(st));
     for (int32_t i = 0; i < b.nr; ++i) bmax = std::max(bmax, bp[i + 1] - bp[i]);
   }
-  const bool shortb = bmax <= 32 && g_gal_short;
+  const bool shortb = bmax <= 32 && opt().gal_short;
   if (shortb) {
     CK(cudaFuncSetAttribute(k_gal_short<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGalFillSmem)));
     CK(cudaFuncSetAttribute(k_gal_short<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGalFillSmem)));
@@ -3296,6 +2868,7 @@ int ig_operator_columns(ig_hier* h, int32_t kind, int32_t j0, int32_t count, dou
   if (!h || !out) return fail(IG_INVALID_ARGUMENT, "operator_columns: null argument");
   if (kind < IG_OP_A || kind > IG_OP_SMOOTHER_SYMMETRIC) return fail(IG_INVALID_ARGUMENT, "operator_columns: bad kind");
   std::lock_guard<std::mutex> lk(h->mu);
+  OptScope os_(&h->opts);
   const int32_t top = h->L - 1;
   const int32_t n = h->lv[top].n;
   if (j0 < 0 || count < 0 || j0 + static_cast<int64_t>(count) > n)

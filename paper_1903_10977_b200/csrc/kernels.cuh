@@ -271,33 +271,13 @@ __device__ __forceinline__ int32_t ld_col(const int32_t* p) {
   return __ldg(p);
 }
 
-// SpMV code variants (IG_OPT_SPMV_VARIANT; chosen from measurement,
-// profiles/spmv_variants.py): batch width U, loop KIND (0: unpredicated full
-// batches + scalar tail, 1: software-pipelined predicated batches,
-// 2: predicated batches) and the __launch_bounds__ min-blocks hint MINB
-// (register cap -> occupancy).  The thread-per-row chain is latency-bound
-// once the row dictionary removes most HBM traffic, so occupancy wins.
-template <int VAR>
-struct SpmvVar;
-template <>
-struct SpmvVar<0> {
-  static constexpr int U = 8, KIND = 0, MINB = 1;
-};
-template <>
-struct SpmvVar<1> {
-  static constexpr int U = 4, KIND = 0, MINB = 8;
-};
-template <>
-struct SpmvVar<2> {
-  static constexpr int U = 8, KIND = 0, MINB = 6;
-};
-template <>
-struct SpmvVar<3> {
-  static constexpr int U = 8, KIND = 2, MINB = 1;
-};
-
-// Row dot product, ascending k, unrolled loads (the sum itself stays serial).
-template <bool STREAM, int VAR = 0>
+// Row dot product, ascending k: batches of 8 predicated loads (values,
+// columns, then x) ahead of the serial sum.  Entries past the row end are
+// never added (acc + 0*x could turn -0 into +0 and break bit-parity with the
+// oracle).  Chosen from measurement among four batch/pipelining variants
+// (round 1, profiles/spmv_variants.py): the thread-per-row chain is
+// latency-bound once the row dictionary removes most HBM traffic.
+template <bool STREAM>
 __device__ __forceinline__ double sell_row(const Sell& A, int row, const double* __restrict__ x) {
   const int64_t base = A.slice_ptr[row >> 5] + (row & 31);
   const int info = A.rowinfo[row];
@@ -308,92 +288,43 @@ __device__ __forceinline__ double sell_row(const Sell& A, int row, const double*
   const int32_t* cp = A.col + base;
   const double* dv = A.dval + (vd > 0 ? (vd - 1) * A.dict_w : 0);
   const int32_t* dc = A.doff + (od > 0 ? (od - 1) * A.dict_w : 0);
-  // Entries past the row end are never added (acc + 0*x could turn -0 into
-  // +0 and break bit-parity with the oracle).
-  constexpr int U = SpmvVar<VAR>::U;
-  constexpr int KIND = SpmvVar<VAR>::KIND;
+  constexpr int U = 8;
   double acc = 0.0;
   auto val_at = [&](int k) { return vd ? __ldg(dv + k) : ld_val<STREAM>(vp + k * kSell); };
   auto col_at = [&](int k) { return od ? row + __ldg(dc + k) : ld_col<STREAM>(cp + k * kSell); };
-  if (KIND == 0) {
-    int k = 0;
-    for (; k + U <= len; k += U) {
-      double v[U];
-      int32_t c[U];
+  for (int k = 0; k < len; k += U) {
+    double v[U];
+    int32_t c[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < U; ++u) {
+      v[u] = 0.0;
+      c[u] = row;
+      if (k + u < len) {
         v[u] = val_at(k + u);
         c[u] = col_at(k + u);
       }
-      double xv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = __ldg(x + c[u]);
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc = acc + v[u] * xv[u];
     }
-    for (; k < len; ++k) acc = acc + val_at(k) * __ldg(x + col_at(k));
-    return acc;
-  }
-  double v[U];
-  int32_t c[U];
-  auto load = [&](int k0, double* vv, int32_t* cc) {
+    double xv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = k0 + u;
-      vv[u] = 0.0;
-      cc[u] = row;
-      if (k < len) {
-        vv[u] = val_at(k);
-        cc[u] = col_at(k);
-      }
-    }
-  };
-  if (KIND == 1) {
-    if (len > 0) load(0, v, c);
-    for (int k = 0; k < len; k += U) {
-      double vn[U];
-      int32_t cn[U];
-      const bool more = k + U < len;
-      if (more) load(k + U, vn, cn);
-      double xv[U];
+    for (int u = 0; u < U; ++u) xv[u] = (k + u < len) ? __ldg(x + c[u]) : 0.0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = (k + u < len) ? __ldg(x + c[u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (k + u < len) acc = acc + v[u] * xv[u];
-      if (more) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          v[u] = vn[u];
-          c[u] = cn[u];
-        }
-      }
-    }
-  } else {
-    for (int k = 0; k < len; k += U) {
-      load(k, v, c);
-      double xv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = (k + u < len) ? __ldg(x + c[u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (k + u < len) acc = acc + v[u] * xv[u];
-    }
+    for (int u = 0; u < U; ++u)
+      if (k + u < len) acc = acc + v[u] * xv[u];
   }
   return acc;
 }
 
 // MODE 0: y = A x.  MODE 1: y = r - A x with r read from y (in place allowed).
 // RED: also reduce x_i * y_i (p . Ap) into the PCG state.
-template <int MODE, bool STREAM, bool RED, int VAR>
-__global__ void __launch_bounds__(kCta, SpmvVar<VAR>::MINB) k_spmv(Sell A, const double* __restrict__ x, double* y,
+template <int MODE, bool STREAM, bool RED>
+__global__ void __launch_bounds__(kCta, 1) k_spmv(Sell A, const double* __restrict__ x, double* y,
                                                const double* rsrc, PcgState* st, double* partials) {
   pdl_entry();
   if (pcg_done(st)) return;
   const int row = blockIdx.x * kCta + threadIdx.x;
   double prod = 0.0;
   if (row < A.n_rows) {
-    const double acc = sell_row<STREAM, VAR>(A, row, x);
+    const double acc = sell_row<STREAM>(A, row, x);
     double out;
     if (MODE == 0)
       out = acc;
@@ -503,8 +434,8 @@ __global__ void IG_GRP_BOUNDS k_spmv_grp(Sell A, const double* __restrict__ x, d
 // Prolongation fused with the correction: cor = P xc (P = R^T stored as CSR
 // over fine rows, ascending coarse index == Eigen's column-major R^T product
 // order) and x += cor.
-template <bool STREAM, int VAR>
-__global__ void __launch_bounds__(kCta, SpmvVar<VAR>::MINB) k_prolong(Sell P, const double* __restrict__ xc, double* cor,
+template <bool STREAM>
+__global__ void __launch_bounds__(kCta, 1) k_prolong(Sell P, const double* __restrict__ xc, double* cor,
                                                   double* x, const PcgState* st) {
   const int row = blockIdx.x * kCta + threadIdx.x;
   if (row < P.n_rows) {  // static layout words into L1 while the predecessor finishes
@@ -517,7 +448,7 @@ __global__ void __launch_bounds__(kCta, SpmvVar<VAR>::MINB) k_prolong(Sell P, co
   if (pcg_done(st)) return;
   if (row >= P.n_rows) return;
   const double xo = x[row];  // ahead of the product chain
-  const double c = sell_row<STREAM, VAR>(P, row, xc);
+  const double c = sell_row<STREAM>(P, row, xc);
   cor[row] = c;
   x[row] = xo + c;
 }
@@ -904,8 +835,11 @@ __global__ void __launch_bounds__(kCta) k_as_simple(AsGather S, const double* __
   if (d >= S.n) return;
   const int h = S.head[d];  // static: before the predecessor wait
   const double l = S.sdiag[d];
-  if (h < 0) return;
+  // Every thread waits, also those of multi-block DOFs: a grid in which no
+  // thread waited could complete before its predecessor and break the
+  // transitive PDL ordering the later kernels rely on.
   pdl_entry();
+  if (h < 0) return;
   const double rd = r[d];
   const double xo = ACC ? x[d] : 0.0;
   double acc = 0.0;
@@ -913,38 +847,6 @@ __global__ void __launch_bounds__(kCta) k_as_simple(AsGather S, const double* __
   const double out = S.gamma * acc;
   x[d] = ACC ? xo + out : out;
 }
-// Small groups (smax <= 4: faces of the box, most multi-DOF blocks) fused
-// with the singleton DOFs: CTAs [0, n_gctas) run groups g_begin.. of G with
-// the lean 4-wide solve (4 warps per CTA), the rest the singleton DOFs.
-// Registers stay low (no 8-wide or warp-block code), so it runs at full
-// occupancy next to the big groups and warp blocks on the side stream.
-template <bool ACC>
-__global__ void IG_AS_BOUNDS k_as_small_simple(AsGroups G, int32_t g_begin, int32_t n_gctas, AsGather S,
-                                                          const double* __restrict__ r, double* ybuf, double* x,
-                                                          const PcgState* st) {
-  if (static_cast<int32_t>(blockIdx.x) < n_gctas) {
-    const int g = g_begin + static_cast<int>((blockIdx.x * kCta + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (g >= G.n_groups) return;
-    const int s = G.size[g * 32 + lane];
-    if (s == 0) return;
-    block_solve<4, false, RLoad, PdlWait>(G, g, lane, s, G.smax[g], r, ybuf, nullptr, PdlWait{});
-    return;
-  }
-  const int d = (blockIdx.x - n_gctas) * kCta + threadIdx.x;
-  if (d >= S.n) return;
-  const int h = S.head[d];  // static: both loads in flight before the predecessor wait
-  const double l = S.sdiag[d];
-  if (h < 0) return;
-  pdl_entry();
-  const double rd = r[d];
-  const double xo = ACC ? x[d] : 0.0;
-  double acc = 0.0;
-  acc = acc + (rd / l) / l;
-  const double out = S.gamma * acc;
-  x[d] = ACC ? xo + out : out;
-}
-
 template <bool ACC>
 __device__ __forceinline__ void as_complex_item(const AsGather& S, int c, const double* __restrict__ r,
                                                 const double* __restrict__ ybuf, double* x) {
@@ -1005,146 +907,6 @@ __global__ void IG_AS_BOUNDS k_as_complex(AsGather S, const double* __restrict__
   x[d] = ACC ? xo + out : out;
 }
 
-// ---------------------------------------------- fused additive smoother ----
-// The whole AS application of one level in ONE kernel (levels up to
-// IG_OPT_FUSED_AS_ROWS rows), replacing fork -> {k_as_blocks ||
-// k_as_small_simple} -> join -> k_as_complex.  On the small levels those
-// three dependent launches plus the graph's fork/join cost ~22 us per
-// application for a few microseconds of work.
-//   phase 1  block items (groups of small blocks, warp blocks) -> ybuf
-//            (warps of the bounded grid stride over the items);
-//            then the CTA arrives on ctr[0]
-//   phase 2  singleton DOFs (no ybuf dependency) while others finish phase 1
-//   phase 3  wait for all CTAs' phase-1 arrivals, then the DOFs with
-//            contribution lists (ybuf read through L2: written by other SMs
-//            in this launch)
-// The grid never exceeds the co-resident capacity (host: occupancy x SMs),
-// so the wait cannot starve; with PDL the dependents launch only after every
-// CTA of this grid has started.  The last CTA to leave resets both counters.
-// Per-DOF arithmetic and order are those of the split kernels (bit-identical).
-struct YbufL2 {
-  const double* p;
-  __device__ __forceinline__ double operator()(int i) const { return __ldcg(p + i); }
-};
-template <class YB>
-__device__ __forceinline__ double as_list_sum_y(const AsGather& S, int c, double rd, YB yb) {
-  const int q0 = S.cptr[c], q1 = S.cptr[c + 1];
-  double acc = 0.0;
-  constexpr int U = 8;
-  for (int qb = q0; qb < q1; qb += U) {
-    int code[U];
-    double v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) code[u] = (qb + u < q1) ? S.centry[qb + u] : 0;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (qb + u < q1) {
-        if (code[u] < 0) {
-          const double ls = S.sval[-code[u] - 1];
-          v[u] = (rd / ls) / ls;
-        } else {
-          v[u] = yb(code[u]);
-        }
-      } else {
-        v[u] = 0.0;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (qb + u < q1) acc = acc + v[u];
-  }
-  return acc;
-}
-template <bool ACC>
-__global__ void __launch_bounds__(kCta) k_as_fused(AsGroups G, AsGather S, const double* __restrict__ r,
-                                                  double* ybuf, double* x, unsigned int* ctr, const PcgState* st) {
-  pdl_entry();
-  if (pcg_done(st)) return;
-  const int lane = threadIdx.x & 31;
-  const int nwarps = static_cast<int>(gridDim.x) * (kCta / 32);
-  const int nitems = G.n_groups + G.n_wblocks;
-  for (int w = static_cast<int>(blockIdx.x) * (kCta / 32) + (threadIdx.x >> 5); w < nitems; w += nwarps)
-    as_blocks_item(G, w, lane, r, ybuf);
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(&ctr[0], 1u);
-  const int nthreads = static_cast<int>(gridDim.x) * kCta;
-  for (int d = static_cast<int>(blockIdx.x) * kCta + threadIdx.x; d < S.n; d += nthreads)
-    as_simple_item<ACC>(S, d, r, x);
-  if (threadIdx.x == 0) {
-    unsigned int seen;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
-    } while (seen < gridDim.x);
-  }
-  __syncthreads();
-  const YbufL2 yb{ybuf};
-  for (int c = static_cast<int>(blockIdx.x) * kCta + threadIdx.x; c < S.n_complex; c += nthreads) {
-    const int d = S.cdof[c];
-    const double out = S.gamma * as_list_sum_y(S, c, r[d], yb);
-    x[d] = ACC ? x[d] + out : out;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int prev = atomicAdd(&ctr[1], 1u);
-    if (prev == gridDim.x - 1) {  // everyone has passed the wait: reset for the next launch
-      ctr[0] = 0u;
-      ctr[1] = 0u;
-      __threadfence();
-    }
-  }
-}
-
-// Whole additive smoother of a SMALL level in one kernel launched as one
-// thread-block cluster (kAsClusterCtas CTAs): block solves and singleton DOFs,
-// a cluster barrier (release/acquire: the ybuf writes of every CTA become
-// visible), then the list sums.  Replaces three dependent launches and the
-// graph fork/join where the work is a few microseconds (IG_OPT_CLUSTER_AS_ROWS).
-// Same per-item code as the split kernels: bit-identical.
-constexpr int kAsClusterCtas = 16;
-constexpr int kAsClusterThreads = 512;
-template <bool ACC>
-__global__ void __launch_bounds__(kAsClusterThreads) k_as_cluster(AsGroups G, AsGather S, const double* __restrict__ r,
-                                                                 double* ybuf, double* x) {
-  pdl_entry();
-  const int nt = static_cast<int>(gridDim.x * blockDim.x);
-  const int gt = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
-  const int lane = threadIdx.x & 31;
-  const int nitems = G.n_groups + G.n_wblocks;
-  for (int w = gt >> 5; w < nitems; w += nt >> 5) as_blocks_item(G, w, lane, r, ybuf);
-  for (int d = gt; d < S.n; d += nt) as_simple_item<ACC>(S, d, r, x);
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-  for (int c = gt; c < S.n_complex; c += nt) {
-    const int d = S.cdof[c];
-    const double out = S.gamma * as_list_sum_y(S, c, r[d], YbufL2{ybuf});
-    x[d] = ACC ? x[d] + out : out;
-  }
-}
-
-// Finest level inside PCG: complex DOFs finish here, simple DOFs read back
-// k_as_simple's result, and every DOF contributes r_d * z_d to r . z in the
-// canonical chunk order.
-template <bool ACC>
-__global__ void __launch_bounds__(kCta) k_as_finish_red(AsGather S, const double* __restrict__ r,
-                                                        const double* __restrict__ ybuf, double* x,
-                                                        const double* rdot, PcgState* st, double* partials) {
-  pdl_entry();
-  if (pcg_done(st)) return;
-  double rz;
-  const bool last = chunk_reduce(S.n, [&](int d) {
-    double xn;
-    if (S.head[d] >= 0) {
-      xn = x[d];
-    } else {
-      const double out = S.gamma * as_list_sum(S, d, r[d], ybuf);
-      xn = ACC ? x[d] + out : out;
-      x[d] = xn;
-    }
-    return rdot[d] * xn;
-  }, partials, &st->counter[2], &rz);
-  if (last && threadIdx.x == 0) rz_update(st, rz);
-}
-
 // r . z as its own pass, for a 1-level hierarchy whose preconditioner is the
 // coarse solve alone (no smoother kernel to fuse the reduction into).
 __global__ void __launch_bounds__(kCta) k_pcg_rz(int32_t n, const double* __restrict__ r,
@@ -1200,7 +962,7 @@ __global__ void __launch_bounds__(kCta) k_ms_update(Sell S, const int32_t* __res
   pdl_entry();
   if (pcg_done(st)) return;
   if (j >= S.n_rows) return;
-  const double acc = sell_row<false, 3>(S, j, delta);
+  const double acc = sell_row<false>(S, j, delta);
   const int i = rowmap[j];
   cur[i] = cur[i] - acc;
 }
@@ -1212,100 +974,6 @@ __global__ void __launch_bounds__(kCta) k_ms_finish(int32_t n, double gamma, con
   if (pcg_done(st)) return;
   auto elem = [&](int i) {
     const double v = gamma * xms[i];
-    const double o = ACC ? out[i] + v : v;
-    out[i] = o;
-    return RED ? rdot[i] * o : 0.0;
-  };
-  if (RED) {
-    double rz;
-    if (chunk_reduce(n, elem, partials, &st->counter[2], &rz))
-      if (threadIdx.x == 0) rz_update(st, rz);
-  } else {
-    for (int i = blockIdx.x * kCta + threadIdx.x; i < n; i += gridDim.x * kCta) elem(i);
-  }
-}
-
-// Lazily updated multiplicative sweep (IG_OPT_MS_LAZY; measured slower, off
-// by default -- see ig_gpu.cu g_ms_lazy).  The classic sweep above
-// updates the frozen residual of EVERY row after every colour; here a block
-// of colour c' forms the residual of its own DOFs when it needs it:
-//   cur_d = ((r_d - t_{c1,d}) - t_{c2,d}) - ...,  t_{c,d} = sum_{k in D_c} A_dk Delta_c(k)
-// over the colours c processed before c', in processing order, each sum in
-// ascending k -- the same operations, in the same order, as the reference's
-// incremental `cur -= A * delta` on row d (colours without neighbours of d
-// add +0 there and are skipped).  x is assembled at the end from the
-// colours' Delta of each DOF, in processing order, as x += delta does.
-// One kernel per colour plus one finish, instead of two per colour.
-struct MslRows {
-  const int32_t* gptr;  // n+1: row d's colour groups [gptr[d], gptr[d+1])
-  const int4* ghead;    // (colour, first entry, count, 0), colours ascending
-  const int32_t* epos;  // entry: position of Delta_c(k) in the delta pool
-  const double* eval;   // entry: A_dk
-};
-struct LazyLoad {
-  const double* r;
-  MslRows R;
-  const double* delta;
-  int color;  // the colour being solved
-  int dir;    // 0 Forward (processed before: higher colours), 1 Reverse (lower)
-  __device__ __forceinline__ double gsum(int4 h) const {
-    constexpr int U = 8;
-    double t = 0.0;
-    for (int e0 = h.y; e0 < h.y + h.z; e0 += U) {
-      double v[U], dv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool in = e0 + u < h.y + h.z;
-        v[u] = in ? __ldg(R.eval + e0 + u) : 0.0;
-        dv[u] = in ? __ldg(delta + __ldg(R.epos + e0 + u)) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (e0 + u < h.y + h.z) t = t + v[u] * dv[u];
-    }
-    return t;
-  }
-  __device__ __forceinline__ double operator()(int d) const {
-    double cur = __ldg(r + d);
-    const int g0 = __ldg(R.gptr + d), g1 = __ldg(R.gptr + d + 1);
-    if (dir == 0) {
-      for (int g = g1 - 1; g >= g0; --g) {
-        const int4 h = __ldg(R.ghead + g);
-        if (h.x <= color) break;
-        cur = cur - gsum(h);
-      }
-    } else {
-      for (int g = g0; g < g1; ++g) {
-        const int4 h = __ldg(R.ghead + g);
-        if (h.x >= color) break;
-        cur = cur - gsum(h);
-      }
-    }
-    return cur;
-  }
-};
-__global__ void __launch_bounds__(128) k_msl_blocks(AsGroups G, LazyLoad ld, double* delta, const PcgState* st) {
-  pdl_entry();
-  if (pcg_done(st)) return;
-  as_blocks_item<false, LazyLoad>(G, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, ld, delta,
-                                  nullptr);
-}
-// x_d = sum of Delta_c(d) over d's colours in processing order (from 0), then
-// out = gamma * x (ACC: out += gamma * x); RED: r . z (finest level in PCG).
-template <bool ACC, bool RED>
-__global__ void __launch_bounds__(kCta) k_msl_finish(int32_t n, double gamma, int dir, const int32_t* __restrict__ dptr,
-                                                     const int2* __restrict__ dlist, const double* __restrict__ delta,
-                                                     double* out, const double* rdot, PcgState* st, double* partials) {
-  pdl_entry();
-  if (pcg_done(st)) return;
-  auto elem = [&](int i) {
-    const int q0 = dptr[i], q1 = dptr[i + 1];
-    double x = 0.0;
-    if (dir == 0)
-      for (int q = q1 - 1; q >= q0; --q) x = x + delta[dlist[q].y];
-    else
-      for (int q = q0; q < q1; ++q) x = x + delta[dlist[q].y];
-    const double v = gamma * x;
     const double o = ACC ? out[i] + v : v;
     out[i] = o;
     return RED ? rdot[i] * o : 0.0;

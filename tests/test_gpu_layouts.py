@@ -90,35 +90,6 @@ def test_pattern_sell_nonfinite_and_signed_zero(star_case):
         h.close()
 
 
-@pytest.mark.parametrize("cluster", [1, 0])
-@pytest.mark.parametrize("case_name", ["c1_case", "d3_case", "star_case", "c3_small_case"])
-def test_small_level_tail_kernel_bitwise(request, case_name, cluster):
-    """The persistent small-level V-cycle kernel (vtail.cuh; one thread-block
-    cluster or a cooperative grid) gives the same bits as the kernel-per-step
-    V-cycle: V-cycles from every level and the whole PCG solve."""
-    from paper_1903_10977_b200 import MgHierarchy, _ffi, pcg
-    lib = _ffi.gpu()
-    case = request.getfixturevalue(case_name)
-    lib.ig_set_option(_ffi.IG_OPT_TAIL_ROWS, 12000)
-    lib.ig_set_option(_ffi.IG_OPT_TAIL_CLUSTER, cluster)
-    try:
-        h = MgHierarchy(case)
-    finally:
-        lib.ig_set_option(_ffi.IG_OPT_TAIL_ROWS, 0)
-        lib.ig_set_option(_ffi.IG_OPT_TAIL_CLUSTER, 1)
-    lv = case.levels_c()
-    try:
-        for l in range(h.levels()):
-            r = rng_vec(17 + l, h._n[l])
-            assert np.array_equal(h.vcycle_at(l, r), orc.vcycle_at(lv, l, r))
-        x, rep = pcg(h.A, case.b, h, tol=1e-8, maxit=1000)
-        st, xo, ro, it, _ = orc.pcg(lv, case.b, tol=1e-8, maxit=1000, mode=orc.GPU_ORDER)
-        assert st == 0 and rep.iterations == it
-        assert np.array_equal(np.array(rep.residuals), ro) and np.array_equal(x, xo)
-    finally:
-        h.close()
-
-
 def test_breakdown_through_pattern_sell():
     """proj/tests/test_solvers.cpp:153-173 with the finest A in the pattern
     layout: p.Ap <= 0 is detected by k_pap (the separate canonical reduction)
@@ -134,39 +105,6 @@ def test_breakdown_through_pattern_sell():
         with pytest.raises(Breakdown) as e:
             pcg(h.A, np.array([0.0, 1.0]), h)
         assert len(e.value.report.residuals) >= 1
-    finally:
-        h.close()
-
-
-@pytest.mark.parametrize("variant", ["fused", "cluster"])
-@pytest.mark.parametrize("case_name", ["c1_case", "d3_case", "star_case", "c3_small_case"])
-def test_fused_smoother_bitwise(request, case_name, variant):
-    """The single-kernel additive smoothers (k_as_fused on a co-resident grid,
-    IG_OPT_FUSED_AS_ROWS; k_as_cluster as one 16-CTA cluster,
-    IG_OPT_CLUSTER_AS_ROWS) on every level give the same bits as the fork/join
-    split: smoother applications, V-cycles and the whole PCG solve vs the oracle."""
-    from paper_1903_10977_b200 import MgHierarchy, _ffi, pcg
-    lib = _ffi.gpu()
-    case = request.getfixturevalue(case_name)
-    opt = _ffi.IG_OPT_FUSED_AS_ROWS if variant == "fused" else _ffi.IG_OPT_CLUSTER_AS_ROWS
-    default = 0 if variant == "fused" else int(getattr(_ffi, "CLUSTER_AS_ROWS_DEFAULT", 0))
-    lib.ig_set_option(opt, 1 << 30)
-    try:
-        h = MgHierarchy(case)
-    finally:
-        lib.ig_set_option(opt, default)
-    lv = case.levels_c()
-    try:
-        for l in range(1, h.levels()):
-            r = rng_vec(27 + l, h._n[l])
-            assert np.array_equal(h.smoother_apply(l, r), orc.smoother_apply(lv, l, r))
-        for l in range(h.levels()):
-            r = rng_vec(37 + l, h._n[l])
-            assert np.array_equal(h.vcycle_at(l, r), orc.vcycle_at(lv, l, r))
-        x, rep = pcg(h.A, case.b, h, tol=1e-8, maxit=1000)
-        st, xo, ro, it, _ = orc.pcg(lv, case.b, tol=1e-8, maxit=1000, mode=orc.GPU_ORDER)
-        assert st == 0 and rep.iterations == it
-        assert np.array_equal(np.array(rep.residuals), ro) and np.array_equal(x, xo)
     finally:
         h.close()
 

@@ -29,19 +29,12 @@ def _cases():
     }
 
 
-@pytest.fixture(scope="module", params=[(c, lazy) for c in ["c1", "star-lagrange", "thb-refined", "3d"] for lazy in (1, 0)],
-                ids=lambda p: f"{p[0]}-{'lazy' if p[1] else 'classic'}")
+@pytest.fixture(scope="module", params=["c1", "star-lagrange", "thb-refined", "3d"])
 def ms_hier(request):
-    """Both device sweeps: the classic per-colour residual update (default)
-    and the lazily updated residual (IG_OPT_MS_LAZY = 1)."""
-    from paper_1903_10977_b200 import MgHierarchy, _ffi, build_case
-    name, lazy = request.param
-    case = build_case(_cases()[name])
-    _ffi.gpu().ig_set_option(_ffi.IG_OPT_MS_LAZY, lazy)
-    try:
-        h = MgHierarchy(case)
-    finally:
-        _ffi.gpu().ig_set_option(_ffi.IG_OPT_MS_LAZY, 0)
+    """The device sweep (per-colour block solves + residual updates)."""
+    from paper_1903_10977_b200 import MgHierarchy, build_case
+    case = build_case(_cases()[request.param])
+    h = MgHierarchy(case)
     yield h
     h.close()
 
