@@ -190,6 +190,8 @@ int ig_pcg(ig_hier *h, const double *b, double tol, int32_t maxit, double *x,
  * vector loads; cudaMalloc / torch allocations are); an unaligned pointer,
  * e.g. a torch slice t[1:], returns IG_INVALID_ARGUMENT. */
 int ig_vcycle_device(ig_hier *h, const double *d_r, double *d_x);
+/* vcycle_at(level, r) (multigrid.hpp:49) on device buffers of that level's size. */
+int ig_vcycle_at_device(ig_hier *h, int32_t level, const double *d_r, double *d_x);
 /* ig_level_spmv on device buffers (modes as ig_level_spmv); used to time the
  * dominant kernel in isolation. */
 int ig_level_spmv_device(ig_hier *h, int32_t level, const double *d_x,

@@ -136,7 +136,7 @@ GPU_SYMBOLS = (
     "ig_pcg_result", "ig_last_error", "ig_set_option", "ig_richardson",
     "ig_smoother_apply_dir", "ig_smoother_apply_symmetric", "ig_galerkin_hierarchy", "ig_csr_free",
     "ig_factorize_blocks", "ig_blocks_free", "ig_pstrf", "ig_hier_build",
-    "ig_operator_columns", "ig_assemble", "ig_hier_set_option", "ig_hier_matches",
+    "ig_operator_columns", "ig_assemble", "ig_hier_set_option", "ig_hier_matches", "ig_vcycle_at_device",
 )
 
 
@@ -171,6 +171,7 @@ def gpu() -> C.CDLL:
         lib.ig_pcg.argtypes = [vp, dp, f64, i32, dp, dp, P(i32), dp]
         lib.ig_richardson.argtypes = [vp, dp, f64, i32, dp, dp, P(i32), dp]
         lib.ig_vcycle_device.argtypes = [vp, vp, vp]
+        lib.ig_vcycle_at_device.argtypes = [vp, i32, vp, vp]
         lib.ig_level_spmv_device.argtypes = [vp, i32, vp, vp, i32]
         lib.ig_debug_vcycle_timeline.argtypes = [vp, vp, vp, i32, P(C.c_float), P(i32), C.c_char_p, i32, P(i32)]
         lib.ig_pcg_device.argtypes = [vp, vp, f64, i32, vp]

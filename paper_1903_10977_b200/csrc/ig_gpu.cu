@@ -819,6 +819,11 @@ struct DevSell {
   int64_t layout_matrix_bytes() const { return has_p ? p_bytes : 8 * explicit_vals + 4 * explicit_cols + 4 * int64_t(s.n_rows); }
 };
 
+// Additive smoother levels with at least this many DOFs run the small-block
+// groups (k_as_blocks4) on a second side stream (profiles/level_costs.py:
+// C4 finest level 453 -> 440 us per V-cycle).
+constexpr int32_t kSplitRows = 100000;
+
 struct Level {
   int32_t n = 0;
   DevSell A, R, P;
@@ -868,9 +873,10 @@ struct ig_hier {
   size_t coarse_smem = 0;
   int coarse_use_smem = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t side = nullptr;  // block solves, forked from / joined into `stream`
+  cudaStream_t side = nullptr;   // block solves, forked from / joined into `stream`
+  cudaStream_t side2 = nullptr;  // small-block groups (k_as_blocks4), concurrently
   int num_sms = 148;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
   PcgState* st = nullptr;
   double* partials = nullptr;
   double* residuals = nullptr;
@@ -880,6 +886,7 @@ struct ig_hier {
   cudaGraphExec_t pcg_exec = nullptr;
   cudaGraphExec_t rich_exec = nullptr;
   struct VcGraph {
+    int level;
     const double* r;
     double* x;
     cudaGraphExec_t exec;
@@ -1002,7 +1009,9 @@ struct ig_hier {
     if (ev1) cudaEventDestroy(ev1);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_join2) cudaEventDestroy(ev_join2);
     if (side) cudaStreamDestroy(side);
+    if (side2) cudaStreamDestroy(side2);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -1085,17 +1094,32 @@ struct ig_hier {
       ms_smoother(l, r, x, acc, s, rdot, dir < 0 ? (acc ? 1 : 0) : dir);
       return;
     }
-    // Every block solve on the side stream (forked from / joined into the
-    // main stream); the singleton DOFs on the main stream meanwhile.
-    const AsGroups& big = l.G;
-    const bool fork = big.n_groups + big.n_wblocks > 0;
-    if (fork) {
-      CK(cudaEventRecord(ev_fork, stream));
+    // Block solves on two side streams forked from / joined into the main
+    // stream: the groups of small blocks (smax <= 4, k_as_blocks4, few
+    // registers) and the rest (larger groups and warp blocks, k_as_blocks);
+    // the singleton DOFs run on the main stream meanwhile.
+    // Only large levels split: on small ones the second graph branch costs
+    // more than it overlaps (C5 / C2 levels below 40k DOFs +2-5 us each).
+    const bool split = l.n >= kSplitRows;
+    AsGroups big = l.G;
+    big.n_groups = split ? l.g_small : l.G.n_groups;  // groups are sorted by size: [0, g_small) have smax > 4
+    const int32_t n_small = l.G.n_groups - big.n_groups;
+    const bool fork1 = big.n_groups + big.n_wblocks > 0;
+    const bool fork2 = n_small > 0;
+    if (fork1 || fork2) CK(cudaEventRecord(ev_fork, stream));
+    if (fork1) {
       CK(cudaStreamWaitEvent(side, ev_fork, 0));
       const unsigned gb = static_cast<unsigned>((static_cast<int64_t>(big.n_groups + big.n_wblocks) * 32 + 127) / 128);
       launch(k_as_blocks, gb, 128, 0, side, big, r, l.ybuf, s);
       CK(cudaGetLastError());
       CK(cudaEventRecord(ev_join, side));
+    }
+    if (fork2) {
+      CK(cudaStreamWaitEvent(side2, ev_fork, 0));
+      const unsigned gs = static_cast<unsigned>((static_cast<int64_t>(n_small) * 32 + 127) / 128);
+      launch(k_as_blocks4, gs, 128, 0, side2, l.G, l.g_small, r, l.ybuf, s);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(ev_join2, side2));
     }
     const unsigned g = grid_of(l.n);
     if (acc)
@@ -1103,7 +1127,8 @@ struct ig_hier {
     else
       launch(k_as_simple<false>, g, kCta, 0, stream, l.S, r, x, s);
     CK(cudaGetLastError());
-    if (fork) CK(cudaStreamWaitEvent(stream, ev_join, 0));
+    if (fork1) CK(cudaStreamWaitEvent(stream, ev_join, 0));
+    if (fork2) CK(cudaStreamWaitEvent(stream, ev_join2, 0));
     if (rdot) {
       // Complex DOFs, then r . z as a plain streaming reduction (the fused
       // k_as_finish_red keeps the list walks inside the reduction chunks and
@@ -1151,7 +1176,26 @@ struct ig_hier {
       else launch(k_ms_finish<false, false>, grid_of(n), kCta, 0, stream, n, l.gamma, l.ms_x, out, rdot, s, partials);
     }
   }
+  template <int R>
+  void coarse_warp(bool sm, const double* r, double* x, PcgState* s) {
+    if (sm)
+      launch(k_coarse_warp<R, true>, 1, 32, coarse_smem, stream, n0, rank, Lp, piv, r, x, s);
+    else
+      launch(k_coarse_warp<R, false>, 1, 32, 0, stream, n0, rank, Lp, piv, r, x, s);
+  }
   void coarse_launch(bool sm, const double* r, double* x, PcgState* s) {
+    if (rank <= 256) {  // single-warp solve, R = ceil(rank / 32) rows per lane
+      switch ((std::max(rank, 1) + 31) / 32) {
+        case 1: coarse_warp<1>(sm, r, x, s); return;
+        case 2: coarse_warp<2>(sm, r, x, s); return;
+        case 3: coarse_warp<3>(sm, r, x, s); return;
+        case 4: coarse_warp<4>(sm, r, x, s); return;
+        case 5: coarse_warp<5>(sm, r, x, s); return;
+        case 6: coarse_warp<6>(sm, r, x, s); return;
+        case 7: coarse_warp<7>(sm, r, x, s); return;
+        default: coarse_warp<8>(sm, r, x, s); return;
+      }
+    }
     const bool big = coarse_threads > 256;
     if (sm && !big)
       launch(k_coarse<true, false>, 1, coarse_threads, coarse_smem, stream, n0, rank, Lp, piv, r, x, s);
@@ -1811,9 +1855,11 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     h->lv.resize(n_levels);
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->side2, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, 0));
     CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_join2, cudaEventDisableTiming));
     CK(cudaEventCreate(&h->ev0));
     CK(cudaEventCreate(&h->ev1));
     ig_info& I = h->info;
@@ -1922,6 +1968,7 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
       CK(cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &av));
       CK(cudaStreamSetAttribute(h->side, cudaStreamAttributeAccessPolicyWindow, &av));
+      CK(cudaStreamSetAttribute(h->side2, cudaStreamAttributeAccessPolicyWindow, &av));
     }
     h->coarse_threads = static_cast<int>(std::max<int64_t>(32, (rk + 31) / 32 * 32));  // one row per thread
     // [packed L11][forward results: rank][backward results: rank]
@@ -1936,6 +1983,10 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
       // created later can shrink them below another handle's need.
       CK(cudaFuncSetAttribute(k_coarse<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_cap));
       CK(cudaFuncSetAttribute(k_coarse<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_cap));
+      void (*kw[])(int32_t, int32_t, const double*, const int32_t*, const double*, double*, const PcgState*) = {
+          k_coarse_warp<1, true>, k_coarse_warp<2, true>, k_coarse_warp<3, true>, k_coarse_warp<4, true>,
+          k_coarse_warp<5, true>, k_coarse_warp<6, true>, k_coarse_warp<7, true>, k_coarse_warp<8, true>};
+      for (auto k : kw) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_cap));
     } else {
       h->coarse_use_smem = 0;
       h->coarse_smem = sizeof(double) * static_cast<size_t>(2 * rk + 2);
@@ -1976,7 +2027,8 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
              layout_spmv(L.P, n, nc, false) + 16 * n;
       // smoother: [blocks] + simple + [complex | finish_red on the finest], twice;
       // plus SpMV-residual x2, restriction, prolongation
-      int per_app = (L.n_multi > 0 ? 1 : 0) + 1 + (L.S.n_complex > 0 ? 1 : 0);
+      const int32_t gb = L.n >= kSplitRows ? L.g_small : L.G.n_groups;
+      int per_app = (gb + L.G.n_wblocks > 0 ? 1 : 0) + (L.G.n_groups > gb ? 1 : 0) + 1 + (L.S.n_complex > 0 ? 1 : 0);
       if (L.ms) {
         int ne = 0;
         for (const auto& mc : L.colors) ne += mc.n_items > 0 ? 1 : 0;
@@ -2173,32 +2225,38 @@ int ig_debug_vcycle_timeline(ig_hier* h, const double* d_r, double* d_x, int32_t
   });
 }
 
-int ig_vcycle_device(ig_hier* h, const double* d_r, double* d_x) {
+int ig_vcycle_at_device(ig_hier* h, int32_t level, const double* d_r, double* d_x) {
   if (!h || !d_r || !d_x) return fail(IG_INVALID_ARGUMENT, "vcycle_device: null argument");
+  if (level < 0 || level >= h->L) return fail(IG_INVALID_ARGUMENT, "vcycle_at_device: level out of range");
   if (!aligned16(d_r) || !aligned16(d_x))
     return fail(IG_INVALID_ARGUMENT, "vcycle_device: device vectors must be 16-byte aligned");
   std::lock_guard<std::mutex> lk(h->mu);
   OptScope os_(&h->opts);
   return guarded([&] {
     if (!opt().use_graph) {
-      h->vcycle(h->L - 1, d_r, d_x, nullptr, nullptr);
+      h->vcycle(level, d_r, d_x, nullptr, nullptr);
       return IG_OK;
     }
     cudaGraphExec_t ex = nullptr;
     for (auto& g : h->vc_graphs)
-      if (g.r == d_r && g.x == d_x) ex = g.exec;
+      if (g.level == level && g.r == d_r && g.x == d_x) ex = g.exec;
     if (!ex) {
       cudaGraph_t g;
       CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-      h->vcycle(h->L - 1, d_r, d_x, nullptr, nullptr);
+      h->vcycle(level, d_r, d_x, nullptr, nullptr);
       CK(cudaStreamEndCapture(h->stream, &g));
       CK(cudaGraphInstantiate(&ex, g, 0));
       CK(cudaGraphDestroy(g));
-      h->vc_graphs.push_back({d_r, d_x, ex});
+      h->vc_graphs.push_back({level, d_r, d_x, ex});
     }
     CK(cudaGraphLaunch(ex, h->stream));
     return IG_OK;
   });
+}
+
+int ig_vcycle_device(ig_hier* h, const double* d_r, double* d_x) {
+  if (!h) return fail(IG_INVALID_ARGUMENT, "vcycle_device: null argument");
+  return ig_vcycle_at_device(h, h->L - 1, d_r, d_x);
 }
 
 int ig_pcg_device(ig_hier* h, const double* d_b, double tol, int32_t maxit, double* d_x) {

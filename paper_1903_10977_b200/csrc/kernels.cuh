@@ -152,28 +152,44 @@ __device__ __forceinline__ bool grid_finish(unsigned int nparts, const double* p
 // and returns its product.  Launch with red_grid (ig_gpu.cu).
 template <class F>
 __device__ __forceinline__ bool chunk_reduce(int n, F f, double* partials, unsigned int* counter, double* total) {
-  __shared__ double sm8c[8];
-  const unsigned int nchunks = static_cast<unsigned int>((n + kCta - 1) / kCta);
-  // Up to 4 chunks' element work first (their loads in flight together),
-  // then their per-chunk trees in chunk order.
+  // Two buffers of B x 8 warp sums: consecutive rounds alternate, so one
+  // barrier per round (not one per chunk) separates writers from readers.
   constexpr int B = 4;
+  __shared__ double smc[2][B][8];
+  const unsigned int nchunks = static_cast<unsigned int>((n + kCta - 1) / kCta);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int buf = 0;
+  // B chunks per round: their element work first (loads in flight together),
+  // then the B warp butterflies interleaved (independent shuffle chains), one
+  // barrier, and thread u < B finishes chunk u's tree -- the same per-chunk
+  // tree (cta_reduce) as one CTA per chunk.
   for (unsigned int c0 = blockIdx.x; c0 < nchunks; c0 += B * gridDim.x) {
-    double prod[B];
+    double v[B];
 #pragma unroll
     for (int u = 0; u < B; ++u) {
       const unsigned int c = c0 + u * gridDim.x;
       const int i = static_cast<int>(c) * kCta + threadIdx.x;
-      prod[u] = (c < nchunks && i < n) ? f(i) : 0.0;
+      v[u] = (c < nchunks && i < n) ? f(i) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const unsigned int c = c0 + u * gridDim.x;
-      if (c < nchunks) {  // CTA-uniform
-        const double part = cta_reduce(prod[u], sm8c);
-        if (threadIdx.x == 0) partials[c] = part;
-        __syncthreads();  // sm8c reuse
+    for (int o = 16; o >= 1; o >>= 1) {
+#pragma unroll
+      for (int u = 0; u < B; ++u) v[u] = v[u] + __shfl_xor_sync(0xffffffffu, v[u], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < B; ++u) smc[buf][u][w] = v[u];
+    }
+    __syncthreads();
+    if (threadIdx.x < B) {
+      const unsigned int c = c0 + threadIdx.x * gridDim.x;
+      if (c < nchunks) {
+        const double* q = smc[buf][threadIdx.x];
+        partials[c] = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+        __threadfence();  // each writer publishes its own partial before the arrival
       }
     }
+    buf ^= 1;
   }
   return grid_finish(nchunks, partials, counter, total);
 }
@@ -691,6 +707,21 @@ __device__ __forceinline__ void as_blocks_item(const AsGroups& G, int w, int lan
     warp_block_solve<MS, LD, WT>(G, w - G.n_groups, lane, r, ybuf, xms, wt);
   }
 }
+// Groups of small blocks only (smax <= 4: ~90 % of the multi-DOF blocks on
+// the C4 levels), groups g_begin.. of G: without the 8-wide and warp-block
+// code the kernel needs a third of k_as_blocks' registers, so all of its
+// warps are resident at once.  It runs on its own side stream, concurrently
+// with k_as_blocks (groups < g_begin and the warp blocks) and the singleton
+// DOFs.
+__global__ void __launch_bounds__(128) k_as_blocks4(AsGroups G, int32_t g_begin, const double* __restrict__ r,
+                                                    double* ybuf, const PcgState* st) {
+  const int g = g_begin + static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= G.n_groups) return;
+  const int s = G.size[g * 32 + lane];
+  if (s == 0) return;
+  block_solve<4, false, RLoad, PdlWait>(G, g, lane, s, G.smax[g], r, ybuf, nullptr, PdlWait{});
+}
 __global__ void IG_ASB_BOUNDS k_as_blocks(AsGroups G, const double* __restrict__ r,
                                                    double* ybuf, const PcgState* st) {
   // pcg_done is a compile-time no-op for V-cycle kernels (see above); the
@@ -1140,6 +1171,83 @@ __device__ __forceinline__ void coarse_solve_cta(int32_t n, int32_t rank, const 
   }
   if (own) x[piv[i] - 1] = y;
   for (int k = rank + threadIdx.x; k < n; k += blockDim.x) x[piv[k] - 1] = 0.0;
+}
+
+// Single-warp solve for ranks up to 32 R (R rows per lane: row i = lane +
+// 32 t).  Every step keeps the pivot chain inside one warp -- the owner lane
+// divides, one shuffle hands y_j to all lanes, each lane applies it to its R
+// rows -- so there is no cross-warp publication or spinning on the chain
+// (the multi-warp pipeline below pays ~2.3x the in-warp step for its
+// handoffs: rank 216, 51 us vs ~20 us).  Same operation order per row as the
+// oracle: forward column-oriented (ascending j), backward dot accumulated in
+// descending k, one (exact) division per pivot.
+template <int R, bool SM>
+__global__ void __launch_bounds__(32, 1) k_coarse_warp(int32_t n, int32_t rank, const double* __restrict__ Lp,
+                                                     const int32_t* __restrict__ piv,
+                                                     const double* __restrict__ r, double* x,
+                                                     const PcgState* st) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ unsigned long long mbar;
+  const int64_t np = static_cast<int64_t>(rank) * (rank + 1) / 2;
+  const int64_t np_al = (np + 1) & ~int64_t(1);
+  if (SM && np > 0) bulk_copy_to_smem(smem, Lp, static_cast<size_t>(np_al) * sizeof(double), &mbar);
+  const double* L = SM ? smem : Lp;
+  const int lane = threadIdx.x;
+  auto off = [&](int j) { return j * rank - (j * (j - 1)) / 2 - j; };  // packed column-major lower
+  double y[R], acc[R], dg[R], rdg[R];
+  int oi[R], pv[R];
+  bool ok = true;
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    const int i = lane + 32 * t;
+    const bool own = i < rank;
+    oi[t] = own ? off(i) : 0;
+    pv[t] = own ? piv[i] - 1 : 0;
+    dg[t] = own ? L[oi[t] + i] : 1.0;
+    rdg[t] = safe_rcp(dg[t]);
+    ok = ok && (!own || (isfinite(rdg[t]) && rdg[t] != 0.0));
+    acc[t] = 0.0;
+  }
+  const bool fast = __all_sync(0xffffffffu, ok);
+  pdl_entry();  // L11, pivots and diagonals are static: staged before the predecessor wait
+#pragma unroll
+  for (int t = 0; t < R; ++t) y[t] = (lane + 32 * t < rank) ? r[pv[t]] : 0.0;
+  // ---- forward: y_j = y_j / L_jj ; y_i -= L_ij y_j (i > j), j ascending ----
+#pragma unroll
+  for (int tb = 0; tb < R; ++tb) {
+    const int jend = min(32, rank - 32 * tb);
+    for (int jj = 0; jj < jend; ++jj) {
+      const int j = 32 * tb + jj;
+      const int oj = off(j);
+      const double q = fast ? exact_div(y[tb], dg[tb], rdg[tb]) : y[tb] / dg[tb];
+      const double yj = __shfl_sync(0xffffffffu, q, jj);
+      if (lane == jj) y[tb] = yj;
+#pragma unroll
+      for (int t = tb; t < R; ++t) {
+        const int i = lane + 32 * t;
+        if ((t > tb || lane > jj) && i < rank) y[t] = y[t] - L[oj + i] * yj;
+      }
+    }
+  }
+  // ---- backward: y_i = (y_i - sum_{k desc > i} L_ki y_k) / L_ii -----------
+#pragma unroll
+  for (int tb = R - 1; tb >= 0; --tb) {
+    const int kend = min(32, rank - 32 * tb);
+    for (int kk = kend - 1; kk >= 0; --kk) {
+      const int k = 32 * tb + kk;
+      const double u = y[tb] - acc[tb];
+      const double q = fast ? exact_div(u, dg[tb], rdg[tb]) : u / dg[tb];
+      const double yk = __shfl_sync(0xffffffffu, q, kk);
+      if (lane == kk) y[tb] = yk;
+#pragma unroll
+      for (int t = 0; t <= tb; ++t)
+        if (t < tb || lane < kk) acc[t] = acc[t] + L[oi[t] + k] * yk;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < R; ++t)
+    if (lane + 32 * t < rank) x[pv[t]] = y[t];
+  for (int k = rank + lane; k < n; k += 32) x[piv[k] - 1] = 0.0;
 }
 
 // BIG: ranks above 256 (up to 1024 threads).
