@@ -2,6 +2,7 @@
 
   python profiles/profile_c4.py spmv     # 3 finest-level SpMVs (A p)
   python profiles/profile_c4.py vcycle   # one V-cycle, direct launches (no graph)
+  python profiles/profile_c4.py vcycle2  # two V-cycles (profile the second, warm L2)
   python profiles/profile_c4.py pcg      # one solve capped at 2 iterations
 
 Never a timing source: numbers printed under ncu are not bench values.
@@ -31,11 +32,12 @@ def main():
     if mode == "spmv":
         for _ in range(3):
             assert lib.ig_level_spmv_device(h.handle, L - 1, vp(db.data_ptr()), vp(dx.data_ptr()), 0) == 0
-    elif mode == "vcycle":
-        lib.ig_set_option(_ffi.IG_OPT_USE_GRAPH, 0)
-        assert lib.ig_vcycle_device(h.handle, vp(db.data_ptr()), vp(dx.data_ptr())) == 0
+    elif mode in ("vcycle", "vcycle2"):
+        lib.ig_hier_set_option(h.handle, _ffi.IG_OPT_USE_GRAPH, 0)
+        for _ in range(2 if mode == "vcycle2" else 1):
+            assert lib.ig_vcycle_device(h.handle, vp(db.data_ptr()), vp(dx.data_ptr())) == 0
     elif mode == "pcg":
-        lib.ig_set_option(_ffi.IG_OPT_USE_GRAPH, 0)
+        lib.ig_hier_set_option(h.handle, _ffi.IG_OPT_USE_GRAPH, 0)
         assert lib.ig_pcg_device(h.handle, vp(db.data_ptr()), 1e-8, 2, vp(dx.data_ptr())) == 0
         lib.ig_pcg_result(h.handle, None, None)
     torch.cuda.synchronize()
