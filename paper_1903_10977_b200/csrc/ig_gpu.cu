@@ -82,6 +82,11 @@ struct Opts {
   // B200) thrashes and gains nothing.
   int32_t l2_rows = 300000;
   size_t l2_bytes = size_t(64) << 20;
+  // Additive smoother on small levels (profiles/level_costs.py): four lanes
+  // per complex DOF up to complex4_rows DOFs; main stream only (no fork /
+  // join) up to one_stream_rows DOFs.
+  int32_t complex4_rows = 100000;
+  int32_t one_stream_rows = 40000;
 };
 Opts g_defaults;
 thread_local const Opts* t_opts = nullptr;
@@ -1098,6 +1103,26 @@ struct ig_hier {
     // stream: the groups of small blocks (smax <= 4, k_as_blocks4, few
     // registers) and the rest (larger groups and warp blocks, k_as_blocks);
     // the singleton DOFs run on the main stream meanwhile.
+    if (l.n <= opt().one_stream_rows) {  // small level: blocks + singletons, then the lists, all PDL-chained
+      const int32_t items = l.G.n_groups + l.G.n_wblocks;
+      const int32_t nb = (items * 32 + 127) / 128;
+      const unsigned gtot = static_cast<unsigned>(nb + (l.n + 127) / 128);
+      if (acc)
+        launch(k_as_blocks_simple<true>, gtot, 128, 0, stream, l.G, nb, l.S, r, l.ybuf, x, s);
+      else
+        launch(k_as_blocks_simple<false>, gtot, 128, 0, stream, l.G, nb, l.S, r, l.ybuf, x, s);
+      CK(cudaGetLastError());
+      if (l.S.n_complex > 0) {
+        const unsigned gc = grid_of(static_cast<int64_t>(l.S.n_complex) * 4);
+        if (acc)
+          launch(k_as_complex4<true>, gc, kCta, 0, stream, l.S, r, l.ybuf, x, s);
+        else
+          launch(k_as_complex4<false>, gc, kCta, 0, stream, l.S, r, l.ybuf, x, s);
+      }
+      if (rdot) launch(k_pcg_rz, red_grid(l.n), kCta, 0, stream, l.n, rdot, x, s, partials);
+      CK(cudaGetLastError());
+      return;
+    }
     // Only large levels split: on small ones the second graph branch costs
     // more than it overlaps (C5 / C2 levels below 40k DOFs +2-5 us each).
     const bool split = l.n >= kSplitRows;
@@ -1141,6 +1166,12 @@ struct ig_hier {
           launch(k_as_complex<false>, gc, kCta, 0, stream, l.S, r, l.ybuf, x, s);
       }
       launch(k_pcg_rz, red_grid(l.n), kCta, 0, stream, l.n, rdot, x, s, partials);
+    } else if (l.S.n_complex > 0 && l.n <= opt().complex4_rows) {  // latency-bound: four lanes per DOF
+      const unsigned gc = grid_of(static_cast<int64_t>(l.S.n_complex) * 4);
+      if (acc)
+        launch(k_as_complex4<true>, gc, kCta, 0, stream, l.S, r, l.ybuf, x, s);
+      else
+        launch(k_as_complex4<false>, gc, kCta, 0, stream, l.S, r, l.ybuf, x, s);
     } else if (l.S.n_complex > 0) {
       const unsigned gc = grid_of(l.S.n_complex);
       if (acc)
@@ -1782,6 +1813,12 @@ int ig_set_option(int32_t option, int64_t value) {
     g_defaults.l2_rows = static_cast<int32_t>(value);
     return IG_OK;
   }
+  if (option == IG_OPT_COMPLEX4_ROWS || option == IG_OPT_ONE_STREAM_ROWS) {
+    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: rows out of range");
+    (option == IG_OPT_COMPLEX4_ROWS ? g_defaults.complex4_rows : g_defaults.one_stream_rows) =
+        static_cast<int32_t>(value);
+    return IG_OK;
+  }
   if (option == IG_OPT_PSELL_CTAS) {
     if (value < 0 || value > 8) return fail(IG_INVALID_ARGUMENT, "ig_set_option: pattern-SELL CTAs per SM in 0..8");
     g_defaults.psell_ctas = static_cast<int>(value);
@@ -1830,12 +1867,16 @@ int ig_hier_set_option(ig_hier* h, int32_t option, int64_t value) {
     o.use_graph = value != 0;
   } else if (option == IG_OPT_PDL) {
     o.use_pdl = value != 0;
+  } else if (option == IG_OPT_COMPLEX4_ROWS || option == IG_OPT_ONE_STREAM_ROWS) {
+    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_hier_set_option: rows out of range");
+    (option == IG_OPT_COMPLEX4_ROWS ? o.complex4_rows : o.one_stream_rows) = static_cast<int32_t>(value);
   } else if (option == IG_OPT_RED_CTAS) {
     if (value < 1 || value > 64) return fail(IG_INVALID_ARGUMENT, "ig_hier_set_option: reduction CTAs per SM in 1..64");
     o.red_ctas = static_cast<int>(value);
   } else {
     return fail(IG_INVALID_ARGUMENT,
-                "ig_hier_set_option: only IG_OPT_USE_GRAPH, IG_OPT_PDL and IG_OPT_RED_CTAS change after "
+                "ig_hier_set_option: only IG_OPT_USE_GRAPH, IG_OPT_PDL, IG_OPT_RED_CTAS, IG_OPT_COMPLEX4_ROWS and "
+                "IG_OPT_ONE_STREAM_ROWS change after "
                 "ig_hier_create (layout options: ig_set_option before creating the handle)");
   }
   h->drop_graphs();

@@ -878,6 +878,35 @@ __global__ void __launch_bounds__(kCta) k_as_simple(AsGather S, const double* __
   const double out = S.gamma * acc;
   x[d] = ACC ? xo + out : out;
 }
+// Small levels: the block solves (groups and warp blocks, CTAs [0, nb)) and
+// the singleton DOFs (CTAs nb..) in ONE kernel on the main stream, so the
+// smoother is two PDL-chained kernels (this, then k_as_complex4) instead of a
+// graph fork / join around three (each join is a full dependency edge).
+template <bool ACC>
+__global__ void IG_ASB_BOUNDS k_as_blocks_simple(AsGroups G, int32_t nb, AsGather S, const double* __restrict__ r,
+                                                 double* ybuf, double* x, const PcgState* st) {
+  if (static_cast<int32_t>(blockIdx.x) < nb) {
+    as_blocks_item<false, RLoad, PdlWait>(G, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, r,
+                                          ybuf, nullptr, PdlWait{});
+    return;
+  }
+  const int d = (blockIdx.x - nb) * blockDim.x + threadIdx.x;
+  if (d >= S.n) {
+    pdl_entry();
+    return;
+  }
+  const int h = S.head[d];
+  const double l = S.sdiag[d];
+  pdl_entry();
+  if (h < 0) return;
+  const double rd = r[d];
+  const double xo = ACC ? x[d] : 0.0;
+  double acc = 0.0;
+  acc = acc + (rd / l) / l;
+  const double out = S.gamma * acc;
+  x[d] = ACC ? xo + out : out;
+}
+
 template <bool ACC>
 __device__ __forceinline__ void as_complex_item(const AsGather& S, int c, const double* __restrict__ r,
                                                 const double* __restrict__ ybuf, double* x) {
@@ -933,6 +962,68 @@ __global__ void IG_AS_BOUNDS k_as_complex(AsGather S, const double* __restrict__
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (qb + u < q1) acc = acc + w[u];
+  }
+  const double out = S.gamma * acc;
+  x[d] = ACC ? xo + out : out;
+}
+
+// Complex DOFs on the latency-bound small levels: four lanes per DOF.  Every
+// lane prefetches 8 list codes (and singleton factors) before the predecessor
+// wait, so a list of up to 32 entries costs ONE dependent round trip (its
+// ybuf gathers) instead of two per batch of 8; the group's lane 0 then adds
+// the 32 values in list order (shuffles), the same operand sequence as
+// k_as_complex.  Longer lists continue serially in lane 0.
+template <bool ACC>
+__global__ void IG_AS_BOUNDS k_as_complex4(AsGather S, const double* __restrict__ r,
+                                           const double* __restrict__ ybuf, double* x, const PcgState* st) {
+  const int t = blockIdx.x * kCta + threadIdx.x;
+  const int c = t >> 2, g = t & 3;
+  const int lane = threadIdx.x & 31, gbase = lane & ~3;
+  const bool valid = c < S.n_complex;
+  int d = 0, q0 = 0, q1 = 0;
+  if (valid) {
+    d = S.cdof[c];
+    q0 = S.cptr[c];
+    q1 = S.cptr[c + 1];
+  }
+  constexpr int U = 8;
+  const int qb = q0 + U * g;
+  int code[U];
+  double ls[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) code[u] = (qb + u < q1) ? S.centry[qb + u] : 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) ls[u] = (qb + u < q1 && code[u] < 0) ? S.sval[-code[u] - 1] : 1.0;
+  // Warp-uniform bound of the shuffle loop: the longest list in the warp.
+  int len = q1 - q0;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
+  pdl_entry();
+  const double rd = valid ? r[d] : 0.0;
+  const double xo = (ACC && valid && g == 0) ? x[d] : 0.0;
+  double v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) v[u] = (qb + u < q1) ? (code[u] < 0 ? (rd / ls[u]) / ls[u] : ybuf[code[u]]) : 0.0;
+  double acc = 0.0;
+  const int rounds = min(4, (len + U - 1) / U);
+  for (int j = 0; j < rounds; ++j) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double w = __shfl_sync(0xffffffffu, v[u], gbase + j);
+      if (g == 0 && q0 + U * j + u < q1) acc = acc + w;
+    }
+  }
+  if (!valid || g != 0) return;
+  for (int q = q0 + 4 * U; q < q1; ++q) {  // lists longer than 32 entries
+    const int cd = S.centry[q];
+    double w;
+    if (cd < 0) {
+      const double l2 = S.sval[-cd - 1];
+      w = (rd / l2) / l2;
+    } else {
+      w = ybuf[cd];
+    }
+    acc = acc + w;
   }
   const double out = S.gamma * acc;
   x[d] = ACC ? xo + out : out;

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("workload", nargs="?", default="c4")
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--opt", action="append", default=[], help="NAME=VALUE (ig_set_option before the hierarchy)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -30,6 +31,9 @@ def main():
     from paper_1903_10977_b200 import MgHierarchy, _ffi
     lib = _ffi.gpu()
     case, desc, _ = bench.build_workload(args.workload, 0)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        assert lib.ig_set_option(getattr(_ffi, "IG_OPT_" + k), int(v)) == 0, kv
     h = MgHierarchy(case)
     stream = torch.cuda.ExternalStream(lib.ig_hier_stream(h.handle))
     vp = C.c_void_p

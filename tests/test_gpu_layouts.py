@@ -175,3 +175,33 @@ def test_two_line_slices_bitwise(d3_48_case, lines2):
         assert st == 0 and rep.iterations == it and np.array_equal(x, xo)
     finally:
         h.close()
+
+
+@pytest.mark.parametrize("complex4,one_stream", [(0, 0), (1 << 30, 0), (1 << 30, 1 << 30)])
+@pytest.mark.parametrize("case_name", ["c1_case", "d3_case", "star_case"])
+def test_small_level_smoother_variants_bitwise(request, case_name, complex4, one_stream):
+    """The additive smoother's small-level launch variants -- complex DOFs
+    one lane or four lanes each (k_as_complex / k_as_complex4), with or
+    without the fork / join (k_as_blocks_simple) -- forced on every level:
+    smoother, V-cycles and the whole solve bit-identical to the oracle."""
+    from paper_1903_10977_b200 import MgHierarchy, _ffi, pcg
+    lib = _ffi.gpu()
+    case = request.getfixturevalue(case_name)
+    h = MgHierarchy(case)
+    lv = case.levels_c()
+    try:
+        assert lib.ig_hier_set_option(h.handle, _ffi.IG_OPT_COMPLEX4_ROWS, complex4) == 0
+        assert lib.ig_hier_set_option(h.handle, _ffi.IG_OPT_ONE_STREAM_ROWS, one_stream) == 0
+        for l in range(1, h.levels()):
+            r = rng_vec(57 + l, h._n[l])
+            assert np.array_equal(h.smoother_apply(l, r), orc.smoother_apply(lv, l, r))
+            assert np.array_equal(h.smoother_apply(l, r, 1), orc.smoother_apply(lv, l, r, 1))
+        for l in range(h.levels()):
+            r = rng_vec(67 + l, h._n[l])
+            assert np.array_equal(h.vcycle_at(l, r), orc.vcycle_at(lv, l, r))
+        x, rep = pcg(h.A, case.b, h, tol=1e-8, maxit=1000)
+        st, xo, ro, it, _ = orc.pcg(lv, case.b, tol=1e-8, maxit=1000, mode=orc.GPU_ORDER)
+        assert st == 0 and rep.iterations == it
+        assert np.array_equal(np.array(rep.residuals), ro) and np.array_equal(x, xo)
+    finally:
+        h.close()
