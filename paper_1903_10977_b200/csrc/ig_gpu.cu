@@ -87,6 +87,12 @@ struct Opts {
   // join) up to one_stream_rows DOFs.
   int32_t complex4_rows = 100000;
   int32_t one_stream_rows = 40000;
+  // Tolerance mode of the coarse solve: x = P M P^T r with the
+  // explicit M = L11^-T L11^-1 (columns from the substitution solves of unit
+  // vectors) as one parallel GEMV with FMA -- NOT bit-identical to the
+  // substitution order; validated against the sequential-order oracle at the
+  // north-star tolerances (tests/test_gpu_fast_mode.py).  Off by default.
+  int fast_coarse = 0;
 };
 Opts g_defaults;
 thread_local const Opts* t_opts = nullptr;
@@ -873,6 +879,8 @@ struct ig_hier {
   int32_t L = 0;
   int32_t n0 = 0, rank = 0;
   double* Lp = nullptr;  // packed lower L11
+  double* Minv = nullptr;  // tolerance mode: rank x rank row-major M = L11^-T L11^-1
+  bool fast_coarse = false;
   int32_t* piv = nullptr;
   int coarse_threads = 32;
   size_t coarse_smem = 0;
@@ -1238,6 +1246,11 @@ struct ig_hier {
       launch(k_coarse<false, true>, 1, coarse_threads, coarse_smem, stream, n0, rank, Lp, piv, r, x, s);
   }
   void coarse(const double* r, double* x, PcgState* s) {
+    if (fast_coarse) {  // tolerance mode: one warp per row of M
+      launch(k_coarse_gemv, static_cast<unsigned>((n0 + 7) / 8), 256, 0, stream, n0, rank, Minv, piv, r, x, s);
+      CK(cudaGetLastError());
+      return;
+    }
     coarse_launch(coarse_use_smem != 0, r, x, s);
     CK(cudaGetLastError());
   }
@@ -1813,6 +1826,10 @@ int ig_set_option(int32_t option, int64_t value) {
     g_defaults.l2_rows = static_cast<int32_t>(value);
     return IG_OK;
   }
+  if (option == IG_OPT_FAST_COARSE) {
+    g_defaults.fast_coarse = value != 0;
+    return IG_OK;
+  }
   if (option == IG_OPT_COMPLEX4_ROWS || option == IG_OPT_ONE_STREAM_ROWS) {
     if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: rows out of range");
     (option == IG_OPT_COMPLEX4_ROWS ? g_defaults.complex4_rows : g_defaults.one_stream_rows) =
@@ -1989,6 +2006,28 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     h->arena_on = h->arena != nullptr;
     h->Lp = h->upload(packed.data(), packed.size());
     h->piv = h->upload(coarse->piv, static_cast<size_t>(n0));
+    if (opt().fast_coarse && rk > 0) {
+      // Column j of M: the oracle-order substitutions (oracle.c tri_solve) of e_j.
+      std::vector<double> M(static_cast<size_t>(rk * rk)), y(static_cast<size_t>(rk));
+      auto L = [&](int64_t i, int64_t j) { return coarse->L[j * n0 + i]; };
+      for (int64_t j = 0; j < rk; ++j) {
+        std::fill(y.begin(), y.end(), 0.0);
+        y[j] = 1.0;
+        for (int64_t c = 0; c < rk; ++c) {
+          const double yc = y[c] / L(c, c);
+          y[c] = yc;
+          for (int64_t i = c + 1; i < rk; ++i) y[i] = y[i] - L(i, c) * yc;
+        }
+        for (int64_t i = rk - 1; i >= 0; --i) {
+          double acc = 0.0;
+          for (int64_t k = rk - 1; k > i; --k) acc = acc + L(k, i) * y[k];
+          y[i] = (y[i] - acc) / L(i, i);
+        }
+        for (int64_t i = 0; i < rk; ++i) M[i * rk + j] = y[i];
+      }
+      h->Minv = h->upload(M.data(), M.size());
+      h->fast_coarse = true;
+    }
     h->arena_on = false;
     if (h->arena && h->arena_used > 0) {
       size_t lim = 0;

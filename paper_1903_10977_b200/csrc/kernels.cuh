@@ -1341,6 +1341,28 @@ __global__ void __launch_bounds__(32, 1) k_coarse_warp(int32_t n, int32_t rank, 
   for (int k = rank + lane; k < n; k += 32) x[piv[k] - 1] = 0.0;
 }
 
+// Tolerance-mode coarse solve (ig_gpu.cu Opts::fast_coarse): x[piv_i] =
+// sum_j M_ij r[piv_j] for i < rank (FMA, lane-split, xor-tree), 0 beyond the
+// rank.  One warp per row; rows of M are contiguous, so loads coalesce.
+__global__ void __launch_bounds__(256) k_coarse_gemv(int32_t n, int32_t rank, const double* __restrict__ M,
+                                                     const int32_t* __restrict__ piv, const double* __restrict__ r,
+                                                     double* x, const PcgState* st) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  pdl_entry();
+  if (row >= n) return;
+  if (row >= rank) {
+    if (lane == 0) x[piv[row] - 1] = 0.0;
+    return;
+  }
+  const double* m = M + static_cast<int64_t>(row) * rank;
+  double acc = 0.0;
+  for (int j = lane; j < rank; j += 32) acc = __fma_rn(__ldg(m + j), r[piv[j] - 1], acc);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) x[piv[row] - 1] = acc;
+}
+
 // BIG: ranks above 256 (up to 1024 threads).
 template <bool SM, bool BIG = false>
 __global__ void __launch_bounds__(BIG ? 1024 : 256, 1) k_coarse(int32_t n, int32_t rank, const double* __restrict__ Lp,

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--json", default=None)
     ap.add_argument("--opt", action="append", default=[], help="NAME=VALUE (ig_set_option before the hierarchy)")
+    ap.add_argument("--smoother", default="as", choices=["as", "ms"])
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -30,7 +31,7 @@ def main():
     import bench
     from paper_1903_10977_b200 import MgHierarchy, _ffi
     lib = _ffi.gpu()
-    case, desc, _ = bench.build_workload(args.workload, 0)
+    case, desc, _ = bench.build_workload(args.workload, 0, args.smoother)
     for kv in args.opt:
         k, v = kv.split("=")
         assert lib.ig_set_option(getattr(_ffi, "IG_OPT_" + k), int(v)) == 0, kv
