@@ -90,6 +90,8 @@ IG_OPT_L2_MB = 19
 IG_OPT_COMPLEX4_ROWS = 28
 IG_OPT_ONE_STREAM_ROWS = 29
 IG_OPT_FAST_COARSE = 30
+IG_OPT_FAST_BLOCKS = 33
+IG_OPT_PSELL_PAIRS_ROWS = 32
 IG_OPT_GAL_SHORT = 21
 IG_OPT_PSELL_CTAB = 23
 IG_OPT_PSELL_LINES2 = 27

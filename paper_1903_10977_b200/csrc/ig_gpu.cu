@@ -69,6 +69,7 @@ struct Opts {
   int red_ctas = 8;      // CTAs per SM of the canonical-reduction kernels (profiles/option_sweep.py 13)
   int use_psell = 1;     // pattern SELL above small_rows
   int psell_pairs = 1;   // FAST slices with two rows per lane (x reuse across a column run)
+  int32_t psell_pairs_rows = 0;  // ... for matrices with at least this many rows
   // Occupancy cap of the pattern-SELL kernels (CTAs per SM, 0 = registers
   // decide), applied as unused dynamic shared memory.
   int psell_ctas = 0;
@@ -93,6 +94,11 @@ struct Opts {
   // substitution order; validated against the sequential-order oracle at the
   // north-star tolerances (tests/test_gpu_fast_mode.py).  Off by default.
   int fast_coarse = 0;
+  // Tolerance mode of the additive smoother's block solves: the factor slots
+  // hold the lower triangle of the explicit inverse M_b = (L_b L_b^T)^-1
+  // (columns from the oracle-order substitutions of unit vectors) and the
+  // kernels apply y = M_b r_b (FMA, ascending j) instead of the substitutions.
+  int fast_blocks = 0;
 };
 Opts g_defaults;
 thread_local const Opts* t_opts = nullptr;
@@ -584,7 +590,9 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
   // pattern).  FAST2 (unscaled base only: rows r and r+1 then see the same
   // column run shifted by one): pieces of up to 64 rows, an even count; the
   // odd remainder goes to FAST slices.
-  const bool f2ok = opt().psell_pairs && s.smul == 1 && s.sshift == 0;
+  // Pair / two-line slices (64 / 128 rows per warp) trade parallelism for x
+  // reuse: only matrices with at least psell_pairs_rows rows use them.
+  const bool f2ok = opt().psell_pairs && nr >= opt().psell_pairs_rows && s.smul == 1 && s.sshift == 0;
   auto emit_piece = [&](int32_t a, int32_t b, int32_t rep) {
     if (b <= a) return;
     lmax_all = std::max(lmax_all, len(rep));
@@ -1571,7 +1579,40 @@ void build_smoother(ig_hier& h, Level& L, const ig_level& src) {
   }
   if (yl > INT32_MAX) throw Error(IG_INVALID_ARGUMENT, "smoother: too many block entries");
   L.n_multi = static_cast<int32_t>(grouped.size() + warped.size());
-  L.G = build_groups(h, B, grouped, warped, ypos);
+  std::vector<double> minv;  // tolerance mode: explicit inverses in the factor layout
+  ig_blocks BI = B;
+  if (opt().fast_blocks) {
+    minv.assign(B.fac, B.fac + B.fac_ptr[nb]);
+    parallel_rows(nb, [&](int32_t b0, int32_t b1) {
+      std::vector<double> y;
+      for (int32_t b = b0; b < b1; ++b) {
+        const int s = bsize(b);
+        if (s == 1) continue;
+        const double* f = B.fac + B.fac_ptr[b];
+        double* m = minv.data() + B.fac_ptr[b];
+        auto L = [&](int i, int j) { return f[static_cast<size_t>(j) * s + i]; };
+        y.assign(static_cast<size_t>(s), 0.0);
+        for (int j = 0; j < s; ++j) {  // column j of M: the oracle's LLT solve of e_j
+          std::fill(y.begin(), y.end(), 0.0);
+          y[j] = 1.0;
+          for (int c = 0; c < s; ++c) {
+            const double yc = y[c] / L(c, c);
+            y[c] = yc;
+            for (int i = c + 1; i < s; ++i) y[i] = y[i] - L(i, c) * yc;
+          }
+          for (int i = s - 1; i >= 0; --i) {
+            double acc = 0.0;
+            for (int k = s - 1; k > i; --k) acc = acc + L(k, i) * y[k];
+            y[i] = (y[i] - acc) / L(i, i);
+          }
+          for (int i = j; i < s; ++i) m[static_cast<size_t>(j) * s + i] = y[i];  // lower triangle of M
+        }
+      }
+    });
+    BI.fac = minv.data();
+  }
+  L.G = build_groups(h, BI, grouped, warped, ypos);
+  L.G.inv = opt().fast_blocks ? 1 : 0;
   {
     std::vector<int32_t> gs(grouped.size());
     for (size_t k = 0; k < grouped.size(); ++k) gs[k] = bsize(grouped[k]);
@@ -1826,8 +1867,17 @@ int ig_set_option(int32_t option, int64_t value) {
     g_defaults.l2_rows = static_cast<int32_t>(value);
     return IG_OK;
   }
+  if (option == IG_OPT_PSELL_PAIRS_ROWS) {
+    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: rows out of range");
+    g_defaults.psell_pairs_rows = static_cast<int32_t>(value);
+    return IG_OK;
+  }
   if (option == IG_OPT_FAST_COARSE) {
     g_defaults.fast_coarse = value != 0;
+    return IG_OK;
+  }
+  if (option == IG_OPT_FAST_BLOCKS) {
+    g_defaults.fast_blocks = value != 0;
     return IG_OK;
   }
   if (option == IG_OPT_COMPLEX4_ROWS || option == IG_OPT_ONE_STREAM_ROWS) {

@@ -522,6 +522,9 @@ struct AsGroups {
   const int64_t* w_fac_off;  // full s x s column-major factor
   const int32_t* w_dofs;
   const double* w_fac;
+  // Tolerance mode (ig_gpu.cu Opts::fast_blocks): the factor slots hold the
+  // lower triangle of the explicit inverse, applied as y = M r (FMA).
+  int32_t inv;
 };
 
 __device__ __forceinline__ int packed_idx(int i, int j, int smax) {
@@ -574,6 +577,24 @@ __device__ __forceinline__ void block_solve(const AsGroups& G, int g, int lane, 
   wt();
 #pragma unroll
   for (int i = 0; i < SM; ++i) y[i] = (i < s) ? r(dof[i]) : 0.0;
+  if (!MS && G.inv) {  // tolerance mode: y = M r with M symmetric, lower triangle stored
+    double z[SM];
+#pragma unroll
+    for (int i = 0; i < SM; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < SM; ++j) {
+        const double mij = i >= j ? Lp[packed_idx(i, j, SM)] : Lp[packed_idx(j, i, SM)];
+        if (j < s) acc = __fma_rn(mij, y[j], acc);
+      }
+      z[i] = acc;
+    }
+    const int pos = G.ypos[g * 32 + lane];
+#pragma unroll
+    for (int i = 0; i < SM; ++i)
+      if (i < s) block_out<MS>(ybuf, xms, pos + i, z[i]);
+    return;
+  }
   double rd[SM];  // reciprocal pivots, computed off the substitution chain
 #pragma unroll
   for (int j = 0; j < SM; ++j) rd[j] = safe_rcp(Lp[packed_idx(j, j, SM)]);
@@ -613,6 +634,16 @@ __device__ __noinline__ void block_solve_any(const AsGroups& G, int g, int lane,
   const int32_t* dp = G.dofs + G.dof_off[g] + lane;
   const double* fp = G.fac + G.fac_off[g] + lane;
   for (int i = 0; i < s; ++i) y[i] = r(dp[i * 32]);
+  if (!MS && G.inv) {  // tolerance mode: y = M r
+    const int pos = G.ypos[g * 32 + lane];
+    for (int i = 0; i < s; ++i) {
+      double acc = 0.0;
+      for (int j = 0; j < s; ++j)
+        acc = __fma_rn(fp[(i >= j ? packed_idx(i, j, smax) : packed_idx(j, i, smax)) * 32], y[j], acc);
+      block_out<MS>(ybuf, xms, pos + i, acc);
+    }
+    return;
+  }
   for (int j = 0; j < s; ++j) {
     const double yj = y[j] / fp[packed_idx(j, j, smax) * 32];
     y[j] = yj;
@@ -644,6 +675,16 @@ __device__ __forceinline__ void warp_block_solve(const AsGroups& G, int b, int l
   const double dg = lane < s ? __ldg(f + lane * s + lane) : 1.0;  // own pivot L(lane, lane)
   wt();
   double y = lane < s ? r(mydof) : 0.0;
+  if (!MS && G.inv) {  // tolerance mode: lane i computes (M r)_i, r_j by shuffle, ascending j
+    double z = 0.0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double yj = __shfl_sync(0xffffffffu, y, j);
+      if (j < s) z = __fma_rn(m[j], yj, z);
+    }
+    if (lane < s) block_out<MS>(ybuf, xms, G.w_ypos[b] + lane, z);
+    return;
+  }
   const double rdg = safe_rcp(dg);
   double acc = 0.0;
   if (__all_sync(0xffffffffu, isfinite(rdg) && rdg != 0.0)) {

@@ -1,6 +1,7 @@
 """Tolerance mode (SURVEY.md §7.3 "fast mode"): the coarse solve as an
-explicit-inverse GEMV (IG_OPT_FAST_COARSE) instead of the oracle-order
-substitutions.  Not bit-identical by construction, so it is held to the
+explicit-inverse GEMV (IG_OPT_FAST_COARSE) and the additive-Schwarz block
+solves as explicit-inverse matvecs (IG_OPT_FAST_BLOCKS) instead of the
+oracle-order substitutions.  Not bit-identical by construction, so it is held to the
 north-star tolerances against the sequential-order oracle -- iterations +-1,
 residual history 1e-9 over the first 10 iterations, x within 1e-8 in relative
 L2, energy norm and non-sliver per-DOF error (tests/parity.py) -- on every
@@ -15,19 +16,25 @@ from parity import assert_history_close, assert_solution_close
 pytestmark = pytest.mark.gpu
 
 
-def _fast_hierarchy(case):
+MODES = {"coarse": ("IG_OPT_FAST_COARSE",), "blocks": ("IG_OPT_FAST_BLOCKS",),
+         "both": ("IG_OPT_FAST_COARSE", "IG_OPT_FAST_BLOCKS")}
+
+
+def _fast_hierarchy(case, mode="both"):
     from paper_1903_10977_b200 import MgHierarchy, _ffi
     lib = _ffi.gpu()
-    assert lib.ig_set_option(_ffi.IG_OPT_FAST_COARSE, 1) == 0
+    for o in MODES[mode]:
+        assert lib.ig_set_option(getattr(_ffi, o), 1) == 0
     try:
         return MgHierarchy(case)
     finally:
-        lib.ig_set_option(_ffi.IG_OPT_FAST_COARSE, 0)
+        for o in MODES[mode]:
+            lib.ig_set_option(getattr(_ffi, o), 0)
 
 
-def _check(case):
+def _check(case, mode="both"):
     from paper_1903_10977_b200 import pcg
-    h = _fast_hierarchy(case)
+    h = _fast_hierarchy(case, mode)
     try:
         x, rep = pcg(h.A, case.b, h, tol=1e-8, maxit=1000)
         assert rep.converged
@@ -40,18 +47,23 @@ def _check(case):
         r = np.random.default_rng(3).uniform(-1, 1, case.level_dofs()[0])
         xc, xo = h.coarse_solve(r), orc.coarse_solve(lv, r)
         assert np.linalg.norm(xc - xo) <= 1e-8 * np.linalg.norm(xo)
+        for l in range(1, h.levels()):  # the smoother alone, against the oracle's substitutions
+            rl = np.random.default_rng(l).uniform(-1, 1, case.level_dofs()[l])
+            zs, zo = h.smoother_apply(l, rl), orc.smoother_apply(lv, l, rl)
+            assert np.linalg.norm(zs - zo) <= 1e-8 * np.linalg.norm(zo)
         return rep.iterations, err
     finally:
         h.close()
 
 
+@pytest.mark.parametrize("mode", list(MODES))
 @pytest.mark.parametrize("name", ["c1_case", "d3_case", "star_case"])
-def test_fast_coarse_small(request, name):
-    print(name, _check(request.getfixturevalue(name)))
+def test_fast_small(request, name, mode):
+    print(name, mode, _check(request.getfixturevalue(name), mode))
 
 
 @pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
-def test_fast_coarse_full_size(cfg):
+def test_fast_full_size(cfg):
     from paper_1903_10977_b200 import build_case, configs
     make = {"c2": lambda: configs.c2(p=2, seed=configs.c2_seed()), "c3": configs.c3, "c4": configs.c4,
             "c5": configs.c5}[cfg]
