@@ -123,6 +123,33 @@ typedef struct {
   const int32_t *kept;                          /* untrimmed -> DOF or -1 */
 } ig_assembly;
 
+/* Cut-element quadrature of the 3D uniform B-spline case on the device (the
+ * element integration of the reference's assemble(), proj/src/assembly.cpp
+ * :55-160, for elements classified Cut; this repository's 3D extension of
+ * recurse_cut, proj/src/quadrature.cpp:255-300: octree bisection to `depth`,
+ * Kuhn 6-tetrahedra per cut leaf clipped against psi >= 0 with bisection edge
+ * roots, collapsed Gauss rules, interface penalty).  igh_cut3_payload fills it
+ * from a host-built case; ig_cut_quadrature3 returns the same element
+ * matrices as the host, bit for bit. */
+typedef struct {
+  int32_t p;                /* degree: q = p + 1 local functions per axis, nl = q^3 */
+  int32_t n_cut;            /* cut elements */
+  const double *lo;         /* n_cut x 3: lower corner of each cut element (physical) */
+  const int32_t *cls;       /* n_cut x 3: extraction class per axis */
+  int32_t n_cls[3];
+  const double *ext[3];     /* per axis: n_cls[d] x q x q, column-major E(i, k) */
+  double h[3];              /* cell size */
+  double beta, f;           /* penalty (already resolved), body force */
+  int32_t depth, classify_depth;
+  double edge_tol;
+  int32_t prog_len;         /* level-set program: postfix, op codes 0 const(v), 1 linear(c0 c1 c2 d dim), */
+  const double *prog;       /* 2 ball(c0 c1 c2 r dim), 3 box(lo0 lo1 lo2 hi0 hi1 hi2 dim), 4 min, 5 max, 6 neg */
+  const double *gauss_tet;  /* 2 nodes, then 2 weights on [0,1] (tetrahedra, 2 x 2 x 2 points) */
+  const double *gauss_tri;  /* 3 nodes, then 3 weights on [0,1] (interface triangles, 3 x 3 points) */
+  const double *gauss_box;  /* q nodes, then q weights on [-1,1] (inside sub-boxes, tensor moments) */
+  const int32_t *table;     /* n_cut: the element's table index in igh_assembly_payload (K, F) */
+} ig_cut3;
+
 typedef struct ig_hier ig_hier;
 
 /* Device-side sizes and algorithmic byte counts. */
@@ -287,6 +314,13 @@ int ig_pstrf(int32_t n, double *a, int32_t *piv, double tol, int32_t *rank);
 int ig_hier_build(const ig_csr *A_fine, const ig_csr *R, const ig_blocks *prefilter, const double *gamma,
                   int32_t smoother_kind, double filter_ratio, int32_t n_levels, ig_hier **out,
                   double *seconds);
+
+/* Element matrices of the cut elements on the device: K (n_cut x nl x nl,
+ * row-major, symmetric), F (n_cut x nl), vol (n_cut: integrated volume
+ * fraction, may be NULL); bit-identical to the host's element tables.
+ * seconds (may be NULL): device time.  IG_UNSUPPORTED for level sets without
+ * a device program or p > 3. */
+int ig_cut_quadrature3(const ig_cut3 *in, double *K, double *F, double *vol, double *seconds);
 
 /* Thread-local message for the last non-OK status. */
 const char *ig_last_error(void);

@@ -88,6 +88,12 @@ int igh_get_info(const igh_case *c, igh_info *out);
  * IG_UNSUPPORTED.  Used by the parity tests to exclude sliver DOFs (whose
  * coefficients reach 1e19 on C4) from per-DOF error checks. */
 int igh_support_fraction(const igh_case *c, double *out);
+/* Cut-element quadrature payload of a built 3D uniform B-spline case
+ * (ig_cut3, ig_gpu.h): the finest level's cut elements, their extraction
+ * classes, the level-set program and the quadrature rules.  Owned by the case.
+ * IG_UNSUPPORTED for 2D, THB, file-read cases or level sets without a device
+ * program. */
+int igh_cut3_payload(igh_case *c, ig_cut3 *out);
 /* Kept anchors of level l as untrimmed tensor indices (ax, ay, az) -> n x 3. */
 int igh_anchors(const igh_case *c, int32_t level, int32_t *out_xyz);
 int igh_write(const igh_case *c, const char *path);

@@ -293,16 +293,52 @@ def factorize_blocks(A: "SpMat", blk_ptr, blk_dofs, filter_ratio: float = 1e-16)
     return optr, odofs, ofp, ofac, int(filt.value), (sec[0], sec[1])
 
 
-def assemble_on_device(case):
+def cut_quadrature_on_device(case):
+    """Element matrices of the finest level's cut elements computed on the
+    device (ig_cut_quadrature3: octree + clipped Kuhn tetrahedra + interface
+    triangles, the host's element3 operation for operation).  Returns
+    (table, K, F, vol, seconds): `table[k]` is the element-table index the
+    host stored the same element under (igh_assembly_payload), K is
+    n_cut x nl x nl, F n_cut x nl.  3D uniform B-spline cases, p <= 2."""
+    pay = _ffi.ig_cut3()
+    _check(_ffi.host(), _ffi.host().igh_cut3_payload(case._h, C.byref(pay)), "igh_cut3_payload")
+    n, q = pay.n_cut, pay.p + 1
+    nl = q ** 3
+    K = np.zeros((n, nl, nl))
+    F = np.zeros((n, nl))
+    vol = np.zeros(n)
+    sec = C.c_double()
+    lib = _ffi.gpu()
+    _check(lib, lib.ig_cut_quadrature3(C.byref(pay), K.ctypes.data_as(_dp), F.ctypes.data_as(_dp),
+                                       vol.ctypes.data_as(_dp), C.byref(sec)), "ig_cut_quadrature3")
+    table = np.ctypeslib.as_array(pay.table, (n,)).copy() if n else np.zeros(0, np.int32)
+    return table, K, F, vol, sec.value
+
+
+def assemble_on_device(case, device_cut: bool = False):
     """The finest level's global assembly on the GPU:
-    the host case's element tables (cut-cell quadrature stays on the host)
-    go through ig_assemble, which sums the element contributions in the
-    reference's setFromTriplets order and symmetrises (assembly.cpp:164-180).
-    Returns (A as SpMat, b, (wall_seconds, device_seconds)), bit-identical to
-    the host assembly (case.A, case.b)."""
+    the element tables go through ig_assemble, which sums the element
+    contributions in the reference's setFromTriplets order and symmetrises
+    (assembly.cpp:164-180).  device_cut: the cut elements' tables are
+    integrated on the device too (cut_quadrature_on_device; 3D B-splines),
+    else the host case's tables are used.  Returns (A as SpMat, b,
+    (wall_seconds, device_seconds)), bit-identical to the host assembly
+    (case.A, case.b)."""
     lib = _ffi.gpu()
     pay = _ffi.ig_assembly()
     _check(_ffi.host(), _ffi.host().igh_assembly_payload(case._h, C.byref(pay)), "igh_assembly_payload")
+    keep = None
+    if device_cut:
+        table, Kc, Fc, _, _ = cut_quadrature_on_device(case)
+        q = pay.p + 1
+        nl = q ** pay.dim
+        Kall = np.ctypeslib.as_array(pay.K, (pay.n_tables * nl * nl,)).reshape(pay.n_tables, nl * nl).copy()
+        Fall = np.ctypeslib.as_array(pay.F, (pay.n_tables * nl,)).reshape(pay.n_tables, nl).copy()
+        Kall[table] = Kc.reshape(len(table), nl * nl)
+        Fall[table] = Fc
+        keep = (Kall, Fall)
+        pay.K = Kall.ctypes.data_as(_dp)
+        pay.F = Fall.ctypes.data_as(_dp)
     out = _ffi.ig_csr()
     b = np.empty(pay.n)
     sec = (C.c_double * 2)()
@@ -313,6 +349,7 @@ def assemble_on_device(case):
         A = SpMat(m.shape[0], m.shape[1], m.row_ptr.copy(), m.col_idx.copy(), m.val.copy())
     finally:
         lib.ig_csr_free(C.byref(out))
+    del keep
     return A, b, (sec[0], sec[1])
 
 

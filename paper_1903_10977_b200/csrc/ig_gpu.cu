@@ -33,6 +33,7 @@
 #include "galerkin.cuh"
 #include "blockfac.cuh"
 #include "assemble.cuh"
+#include "cutquad.cuh"
 
 using namespace igk;
 
@@ -3216,6 +3217,82 @@ int ig_assemble(const ig_assembly* a, ig_csr* A_out, double* b_out, double* seco
   if (seconds) seconds[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (rc != IG_OK) ig_csr_free(A_out);
   return rc;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------ cut-element quadrature --
+extern "C" {
+
+int ig_cut_quadrature3(const ig_cut3* in, double* K, double* F, double* vol, double* seconds) {
+  if (!in || !K || !F) return fail(IG_INVALID_ARGUMENT, "cut_quadrature3: null argument");
+  if (in->p < 1 || in->p > 2)
+    return fail(IG_UNSUPPORTED, "cut_quadrature3: degrees 1 and 2 on the device (shared-memory basis tables)");
+  if (in->depth < 0 || in->depth > 3 || in->classify_depth < 0 || in->classify_depth > 6)
+    return fail(IG_INVALID_ARGUMENT, "cut_quadrature3: depth in 0..3, classify depth in 0..6");
+  if (in->prog_len <= 0 || !in->prog) return fail(IG_UNSUPPORTED, "cut_quadrature3: no level-set program");
+  if (in->n_cut == 0) return IG_OK;
+  return guarded([&] {
+    const int q = in->p + 1, nl = q * q * q;
+    const int64_t n = in->n_cut;
+    std::vector<void*> mem;
+    auto up = [&](const void* src, size_t bytes) {
+      void* d = nullptr;
+      CK(cudaMalloc(&d, std::max<size_t>(bytes, 8)));
+      mem.push_back(d);
+      if (bytes && src) CK(cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice));
+      return d;
+    };
+    struct Free {
+      std::vector<void*>& m;
+      ~Free() {
+        for (void* p : m) cudaFree(p);
+      }
+    } free_{mem};
+    ig_cut3 D = *in;
+    D.lo = static_cast<const double*>(up(in->lo, sizeof(double) * 3 * n));
+    D.cls = static_cast<const int32_t*>(up(in->cls, sizeof(int32_t) * 3 * n));
+    for (int d = 0; d < 3; ++d)
+      D.ext[d] = static_cast<const double*>(up(in->ext[d], sizeof(double) * in->n_cls[d] * q * q));
+    D.prog = static_cast<const double*>(up(in->prog, sizeof(double) * in->prog_len));
+    D.gauss_tet = static_cast<const double*>(up(in->gauss_tet, sizeof(double) * 4));
+    D.gauss_tri = static_cast<const double*>(up(in->gauss_tri, sizeof(double) * 6));
+    D.gauss_box = static_cast<const double*>(up(in->gauss_box, sizeof(double) * 2 * q));
+    D.table = nullptr;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0));
+    int64_t* dcount = static_cast<int64_t*>(up(nullptr, sizeof(int64_t) * (n + 1)));
+    k_cq_prims<false><<<static_cast<unsigned>(n), kCqThreads>>>(D, nullptr, dcount, nullptr);
+    CK(cudaGetLastError());
+    std::vector<int64_t> cnt(static_cast<size_t>(n)), offs(static_cast<size_t>(n) + 1, 0);
+    CK(cudaMemcpy(cnt.data(), dcount, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+    for (int64_t e = 0; e < n; ++e) offs[e + 1] = offs[e] + cnt[e];
+    int64_t* doff = static_cast<int64_t*>(up(offs.data(), sizeof(int64_t) * (n + 1)));
+    double* prim = static_cast<double*>(up(nullptr, sizeof(double) * kCqPrim * std::max<int64_t>(offs[n], 1)));
+    k_cq_prims<true><<<static_cast<unsigned>(n), kCqThreads>>>(D, doff, nullptr, prim);
+    CK(cudaGetLastError());
+    double* dK = static_cast<double*>(up(nullptr, sizeof(double) * n * nl * nl));
+    double* dF = static_cast<double*>(up(nullptr, sizeof(double) * n * nl));
+    double* dv = static_cast<double*>(up(nullptr, sizeof(double) * n));
+    if (nl == 27)
+      k_cq_integrate<27><<<static_cast<unsigned>(n), kCqThreads>>>(D, doff, prim, dK, dF, dv);
+    else
+      k_cq_integrate<8><<<static_cast<unsigned>(n), kCqThreads>>>(D, doff, prim, dK, dF, dv);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CK(cudaMemcpy(K, dK, sizeof(double) * n * nl * nl, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(F, dF, sizeof(double) * n * nl, cudaMemcpyDeviceToHost));
+    if (vol) CK(cudaMemcpy(vol, dv, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    if (seconds) *seconds = ms * 1e-3;
+    return IG_OK;
+  });
 }
 
 }  // extern "C"

@@ -486,6 +486,9 @@ struct igh_case {
   int32_t n_tables = 0;
   // Finest level: physical support volume / untrimmed support cell volume per DOF.
   std::vector<double> supp_frac;
+  // Cut-element quadrature payload (igh_cut3_payload), built on demand.
+  std::vector<double> cut_lo, cut_ext[3], cut_prog, g_tet, g_tri, g_box;
+  std::vector<int32_t> cut_cls, cut_table;
   std::vector<double> gamma;
   std::vector<int32_t> kind;
   std::vector<double> coarseL;
@@ -788,6 +791,75 @@ int igh_build(const igh_config* cfg, igh_case** out) {
       std::fprintf(stderr, "igh_build: assemble %.3f s, mg setup %.3f s (galerkin %.3f, block factorization %.3f)\n",
                    t1 - t0, t2 - t1, t_gal, t_fac);
     *out = c.release();
+    return IG_OK;
+  } catch (const std::exception& e) {
+    return fail(e.what());
+  }
+}
+
+int igh_cut3_payload(igh_case* c, ig_cut3* out) {
+  if (!c || !out) return fail("igh_cut3_payload: null argument");
+  if (c->spaces.empty() || c->el_table.empty() || c->cfg.dim != 3 || c->cfg.family != 1)
+    return fail("igh_cut3_payload: built 3D uniform B-spline cases only", IG_UNSUPPORTED);
+  try {
+    const Space& s = *c->spaces.back();
+    const int q = s.p + 1;
+    if (c->cut_prog.empty() && !s.ls.program(c->cut_prog))
+      return fail("igh_cut3_payload: the level set has no device program (star / affine)", IG_UNSUPPORTED);
+    const int ncls = static_cast<int>(s.ext[0].size() * s.ext[1].size() * s.ext[2].size());
+    if (c->cut_table.empty()) {
+      const int ne = static_cast<int>(s.el_ix.size());
+      for (int e = 0; e < ne; ++e) {
+        if (c->el_table[e] < ncls) continue;  // Inside class tables; the rest are the cut elements
+        double lo[3], hi[3];
+        s.grid.cell_box(s.el_ix[e], s.el_iy[e], s.el_iz[e], lo, hi);
+        c->cut_lo.insert(c->cut_lo.end(), lo, lo + 3);
+        c->cut_cls.push_back(s.ext_cls[0][s.el_ix[e]]);
+        c->cut_cls.push_back(s.ext_cls[1][s.el_iy[e]]);
+        c->cut_cls.push_back(s.ext_cls[2][s.el_iz[e]]);
+        c->cut_table.push_back(c->el_table[e]);
+      }
+      for (int d = 0; d < 3; ++d) {
+        c->cut_ext[d].clear();
+        for (const Mat& m : s.ext[d]) c->cut_ext[d].insert(c->cut_ext[d].end(), m.a.begin(), m.a.end());
+      }
+      auto rule01 = [](int n, std::vector<double>& out01) {  // assembly.cpp gauss01
+        std::vector<double> nd, wt;
+        gauss_legendre(n, nd, wt);
+        out01.clear();
+        for (int i = 0; i < n; ++i) out01.push_back(0.5 * (nd[i] + 1.0));
+        for (int i = 0; i < n; ++i) out01.push_back(0.5 * wt[i]);
+      };
+      rule01(2, c->g_tet);
+      rule01(3, c->g_tri);
+      std::vector<double> nd, wt;
+      gauss_legendre(q, nd, wt);
+      c->g_box = nd;
+      c->g_box.insert(c->g_box.end(), wt.begin(), wt.end());
+    }
+    *out = ig_cut3{};
+    out->p = s.p;
+    out->n_cut = static_cast<int32_t>(c->cut_table.size());
+    out->lo = c->cut_lo.data();
+    out->cls = c->cut_cls.data();
+    for (int d = 0; d < 3; ++d) {
+      out->n_cls[d] = static_cast<int32_t>(s.ext[d].size());
+      out->ext[d] = c->cut_ext[d].data();
+      out->h[d] = s.grid.h(d);
+    }
+    double hmin = s.grid.h(0);
+    for (int d = 1; d < 3; ++d) hmin = std::min(hmin, s.grid.h(d));
+    out->beta = c->cfg.beta > 0.0 ? c->cfg.beta : 2.0 / hmin;  // default_penalty (assembly.cpp:7-10)
+    out->f = c->cfg.body_force;
+    out->depth = c->cfg.quad_depth;
+    out->classify_depth = c->cfg.classify_depth;
+    out->edge_tol = c->cfg.edge_tol;
+    out->prog_len = static_cast<int32_t>(c->cut_prog.size());
+    out->prog = c->cut_prog.data();
+    out->gauss_tet = c->g_tet.data();
+    out->gauss_tri = c->g_tri.data();
+    out->gauss_box = c->g_box.data();
+    out->table = c->cut_table.data();
     return IG_OK;
   } catch (const std::exception& e) {
     return fail(e.what());

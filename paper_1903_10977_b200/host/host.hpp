@@ -90,6 +90,9 @@ class LevelSet {
   // if the node can bound psi over an axis box (used only to skip sampling
   // when every lattice sample provably has one sign).
   bool bounds(const double* lo, const double* hi, int dim, double& vmin, double& vmax) const;
+  // Postfix program for the device evaluator (ig_cut3); false if a node has
+  // no bit-exact device form.
+  bool program(std::vector<double>& out) const;
   const std::shared_ptr<const LsNode>& node() const { return node_; }
 
  private:

@@ -17,6 +17,10 @@ struct LsNode {
   virtual bool bounds(const double*, const double*, int, double&, double&) const {
     return false;
   }
+  // Postfix program for the device evaluator (ig_gpu.h ig_cut3: op codes
+  // 0 const, 1 linear, 2 ball, 3 box, 4 min, 5 max, 6 neg); false for nodes
+  // without a bit-exact device form (star: atan2 / sin; affine).
+  virtual bool emit(std::vector<double>&) const { return false; }
 };
 
 namespace {
@@ -24,6 +28,10 @@ namespace {
 struct ConstNode final : LsNode {
   double v;
   explicit ConstNode(double v_) : v(v_) {}
+  bool emit(std::vector<double>& o) const override {
+    o.insert(o.end(), {0.0, v});
+    return true;
+  }
   double eval(const double*) const override { return v; }
   bool bounds(const double*, const double*, int, double& a, double& b) const override {
     a = b = v;
@@ -35,6 +43,10 @@ struct ConstNode final : LsNode {
 struct LinearNode final : LsNode {
   double c[3], d;
   int dim;
+  bool emit(std::vector<double>& o) const override {
+    o.insert(o.end(), {1.0, c[0], c[1], c[2], d, static_cast<double>(dim)});
+    return true;
+  }
   double eval(const double* p) const override {
     return dim == 2 ? c[0] * p[0] + c[1] * p[1] + d : c[0] * p[0] + c[1] * p[1] + c[2] * p[2] + d;
   }
@@ -53,6 +65,10 @@ struct LinearNode final : LsNode {
 struct BallNode final : LsNode {
   double c[3], r;
   int dim;
+  bool emit(std::vector<double>& o) const override {
+    o.insert(o.end(), {2.0, c[0], c[1], c[2], r, static_cast<double>(dim)});
+    return true;
+  }
   double eval(const double* p) const override {
     const double dx = p[0] - c[0], dy = p[1] - c[1];
     if (dim == 2) return r - std::sqrt(dx * dx + dy * dy);
@@ -89,6 +105,10 @@ struct StarNode final : LsNode {
 struct BoxNode final : LsNode {
   double lo[3], hi[3];
   int dim;
+  bool emit(std::vector<double>& o) const override {
+    o.insert(o.end(), {3.0, lo[0], lo[1], lo[2], hi[0], hi[1], hi[2], static_cast<double>(dim)});
+    return true;
+  }
   double eval(const double* p) const override {
     double v = std::min(std::min(p[0] - lo[0], hi[0] - p[0]), std::min(p[1] - lo[1], hi[1] - p[1]));
     if (dim == 3) v = std::min(v, std::min(p[2] - lo[2], hi[2] - p[2]));
@@ -118,6 +138,12 @@ enum class Comb { Min, Max, Neg };
 struct CombineNode final : LsNode {
   Comb op;
   std::shared_ptr<const LsNode> a, b;
+  bool emit(std::vector<double>& o) const override {
+    if (!a->emit(o)) return false;
+    if (op != Comb::Neg && !b->emit(o)) return false;
+    o.push_back(op == Comb::Min ? 4.0 : (op == Comb::Max ? 5.0 : 6.0));
+    return true;
+  }
   double eval(const double* p) const override {
     switch (op) {
       case Comb::Min: return std::min(a->eval(p), b->eval(p));
@@ -319,6 +345,10 @@ struct Parser {
 
 LevelSet::LevelSet() : node_(std::make_shared<ConstNode>(1.0)) {}
 double LevelSet::operator()(const double* p) const { return node_->eval(p); }
+bool LevelSet::program(std::vector<double>& out) const {
+  out.clear();
+  return node_->emit(out);
+}
 bool LevelSet::bounds(const double* lo, const double* hi, int dim, double& a, double& b) const {
   return node_->bounds(lo, hi, dim, a, b);
 }
