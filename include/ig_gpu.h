@@ -150,6 +150,32 @@ typedef struct {
   const int32_t *table;     /* n_cut: the element's table index in igh_assembly_payload (K, F) */
 } ig_cut3;
 
+/* The reference's 2D cut-cell quadrature on the device (proj/src/
+ * quadrature.cpp:128-372 recurse_cut / leaf_polygons / refine_chords /
+ * fan_triangulate / interface_segments / side_rule, and the element loop of
+ * assemble(), proj/src/assembly.cpp:55-162) for every individually integrated
+ * element of a uniform 2D case: cut elements and elements on the embedding-box
+ * boundary.  igh_cut2_payload fills it; ig_cut_quadrature2 returns the host's
+ * element matrices bit for bit. */
+typedef struct {
+  int32_t p;               /* degree: q = p + 1, nl = q^2 */
+  int32_t n_elem;
+  const double *lo, *hi;   /* n_elem x 2: the element cell (physical) */
+  const int32_t *cls;      /* n_elem x 2: extraction class per axis */
+  const int32_t *cut;      /* n_elem: 1 = cut element (recurse_cut + interface), 0 = tensor rule */
+  const int32_t *sides;    /* n_elem: bit k = box side k of the element carries the Dirichlet penalty */
+  int32_t n_cls[2];
+  const double *ext[2];    /* per axis: n_cls[d] x q x q, column-major */
+  double beta, f;
+  int32_t depth, classify_depth, gauss_order;
+  double edge_tol;
+  int32_t prog_len;
+  const double *prog;      /* level-set program (ig_cut3) */
+  const double *gauss_q;   /* gauss_order nodes, then weights, on [-1,1] */
+  const double *gauss_q1;  /* gauss_order + 1 nodes, then weights (collapsed triangle rule, q > 3) */
+  const int32_t *table;    /* n_elem: table index in igh_assembly_payload */
+} ig_cut2;
+
 typedef struct ig_hier ig_hier;
 
 /* Device-side sizes and algorithmic byte counts. */
@@ -321,6 +347,9 @@ int ig_hier_build(const ig_csr *A_fine, const ig_csr *R, const ig_blocks *prefil
  * seconds (may be NULL): device time.  IG_UNSUPPORTED for level sets without
  * a device program or p > 3. */
 int ig_cut_quadrature3(const ig_cut3 *in, double *K, double *F, double *vol, double *seconds);
+/* 2D: K (n_elem x nl x nl), F (n_elem x nl), vol (volume-rule weight sums, may
+ * be NULL), bit-identical to the host.  p <= 4. */
+int ig_cut_quadrature2(const ig_cut2 *in, double *K, double *F, double *vol, double *seconds);
 
 /* Thread-local message for the last non-OK status. */
 const char *ig_last_error(void);

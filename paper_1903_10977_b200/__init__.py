@@ -294,23 +294,30 @@ def factorize_blocks(A: "SpMat", blk_ptr, blk_dofs, filter_ratio: float = 1e-16)
 
 
 def cut_quadrature_on_device(case):
-    """Element matrices of the finest level's cut elements computed on the
-    device (ig_cut_quadrature3: octree + clipped Kuhn tetrahedra + interface
-    triangles, the host's element3 operation for operation).  Returns
-    (table, K, F, vol, seconds): `table[k]` is the element-table index the
-    host stored the same element under (igh_assembly_payload), K is
-    n_cut x nl x nl, F n_cut x nl.  3D uniform B-spline cases, p <= 2."""
-    pay = _ffi.ig_cut3()
-    _check(_ffi.host(), _ffi.host().igh_cut3_payload(case._h, C.byref(pay)), "igh_cut3_payload")
-    n, q = pay.n_cut, pay.p + 1
-    nl = q ** 3
+    """Element matrices of the finest level's individually integrated
+    elements computed on the device: 3D cut elements (ig_cut_quadrature3:
+    octree + clipped Kuhn tetrahedra + interface triangles) or, in 2D, cut
+    and box-side elements (ig_cut_quadrature2: the reference's recurse_cut /
+    leaf polygons / chord refinement / fan triangulation / interface and side
+    rules) -- the host's element integration operation for operation.
+    Returns (table, K, F, vol, seconds): `table[k]` is the element-table index
+    the host stored the same element under (igh_assembly_payload), K is
+    n x nl x nl, F n x nl.  Uniform B-spline / Lagrange cases."""
+    lib = _ffi.gpu()
+    if _ffi.host().igh_cut3_payload(case._h, C.byref(_ffi.ig_cut3())) != _ffi.IG_OK:  # 2D (or unsupported)
+        pay = _ffi.ig_cut2()
+        _check(_ffi.host(), _ffi.host().igh_cut2_payload(case._h, C.byref(pay)), "igh_cut2_payload")
+        n, nl, fn = pay.n_elem, (pay.p + 1) ** 2, lib.ig_cut_quadrature2
+    else:
+        pay = _ffi.ig_cut3()
+        _check(_ffi.host(), _ffi.host().igh_cut3_payload(case._h, C.byref(pay)), "igh_cut3_payload")
+        n, nl, fn = pay.n_cut, (pay.p + 1) ** 3, lib.ig_cut_quadrature3
     K = np.zeros((n, nl, nl))
     F = np.zeros((n, nl))
     vol = np.zeros(n)
     sec = C.c_double()
-    lib = _ffi.gpu()
-    _check(lib, lib.ig_cut_quadrature3(C.byref(pay), K.ctypes.data_as(_dp), F.ctypes.data_as(_dp),
-                                       vol.ctypes.data_as(_dp), C.byref(sec)), "ig_cut_quadrature3")
+    _check(lib, fn(C.byref(pay), K.ctypes.data_as(_dp), F.ctypes.data_as(_dp), vol.ctypes.data_as(_dp),
+                   C.byref(sec)), "cut quadrature")
     table = np.ctypeslib.as_array(pay.table, (n,)).copy() if n else np.zeros(0, np.int32)
     return table, K, F, vol, sec.value
 

@@ -62,6 +62,13 @@ class ig_cut3(C.Structure):
                 ("gauss_tet", P(f64)), ("gauss_tri", P(f64)), ("gauss_box", P(f64)), ("table", P(i32))]
 
 
+class ig_cut2(C.Structure):
+    _fields_ = [("p", i32), ("n_elem", i32), ("lo", P(f64)), ("hi", P(f64)), ("cls", P(i32)), ("cut", P(i32)),
+                ("sides", P(i32)), ("n_cls", i32 * 2), ("ext", P(f64) * 2), ("beta", f64), ("f", f64),
+                ("depth", i32), ("classify_depth", i32), ("gauss_order", i32), ("edge_tol", f64),
+                ("prog_len", i32), ("prog", P(f64)), ("gauss_q", P(f64)), ("gauss_q1", P(f64)), ("table", P(i32))]
+
+
 class igh_config(C.Structure):
     _fields_ = [("dim", i32), ("geometry", C.c_char_p), ("origin", f64 * 3),
                 ("extent", f64 * 3), ("resolution", i32 * 3), ("family", i32),
@@ -129,6 +136,7 @@ def host() -> C.CDLL:
         lib.igh_get_info.argtypes = [C.c_void_p, P(igh_info)]
         lib.igh_support_fraction.argtypes = [C.c_void_p, P(f64)]
         lib.igh_cut3_payload.argtypes = [C.c_void_p, P(ig_cut3)]
+        lib.igh_cut2_payload.argtypes = [C.c_void_p, P(ig_cut2)]
         lib.igh_anchors.argtypes = [C.c_void_p, i32, P(i32)]
         lib.igh_write.argtypes = [C.c_void_p, C.c_char_p]
         lib.igh_read.argtypes = [C.c_char_p, P(C.c_void_p)]
@@ -149,7 +157,7 @@ GPU_SYMBOLS = (
     "ig_pcg_result", "ig_last_error", "ig_set_option", "ig_richardson",
     "ig_smoother_apply_dir", "ig_smoother_apply_symmetric", "ig_galerkin_hierarchy", "ig_csr_free",
     "ig_factorize_blocks", "ig_blocks_free", "ig_pstrf", "ig_hier_build",
-    "ig_operator_columns", "ig_assemble", "ig_hier_set_option", "ig_hier_matches", "ig_vcycle_at_device", "ig_cut_quadrature3",
+    "ig_operator_columns", "ig_assemble", "ig_hier_set_option", "ig_hier_matches", "ig_vcycle_at_device", "ig_cut_quadrature3", "ig_cut_quadrature2",
 )
 
 
@@ -194,5 +202,6 @@ def gpu() -> C.CDLL:
         lib.ig_hier_set_option.argtypes = [vp, i32, i64]
         lib.ig_hier_matches.argtypes = [vp, P(ig_csr)]
         lib.ig_cut_quadrature3.argtypes = [P(ig_cut3), dp, dp, dp, dp]
+        lib.ig_cut_quadrature2.argtypes = [P(ig_cut2), dp, dp, dp, dp]
         _gpu = lib
     return _gpu

@@ -34,6 +34,7 @@
 #include "blockfac.cuh"
 #include "assemble.cuh"
 #include "cutquad.cuh"
+#include "cutquad2.cuh"
 
 using namespace igk;
 
@@ -3280,6 +3281,85 @@ int ig_cut_quadrature3(const ig_cut3* in, double* K, double* F, double* vol, dou
       k_cq_integrate<27><<<static_cast<unsigned>(n), kCqThreads>>>(D, doff, prim, dK, dF, dv);
     else
       k_cq_integrate<8><<<static_cast<unsigned>(n), kCqThreads>>>(D, doff, prim, dK, dF, dv);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CK(cudaMemcpy(K, dK, sizeof(double) * n * nl * nl, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(F, dF, sizeof(double) * n * nl, cudaMemcpyDeviceToHost));
+    if (vol) CK(cudaMemcpy(vol, dv, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    if (seconds) *seconds = ms * 1e-3;
+    return IG_OK;
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int ig_cut_quadrature2(const ig_cut2* in, double* K, double* F, double* vol, double* seconds) {
+  if (!in || !K || !F) return fail(IG_INVALID_ARGUMENT, "cut_quadrature2: null argument");
+  if (in->p < 1 || in->p > 4) return fail(IG_UNSUPPORTED, "cut_quadrature2: degrees 1..4");
+  if (in->depth < 0 || in->depth > 6 || in->classify_depth < 0 || in->classify_depth > 8 || in->gauss_order < 1 ||
+      in->gauss_order > 16)
+    return fail(IG_INVALID_ARGUMENT, "cut_quadrature2: depth in 0..6, classify depth in 0..8, Gauss order 1..16");
+  if (in->prog_len <= 0 || !in->prog) return fail(IG_UNSUPPORTED, "cut_quadrature2: no level-set program");
+  if (in->n_elem == 0) return IG_OK;
+  return guarded([&] {
+    const int q = in->p + 1, nl = q * q, go = in->gauss_order;
+    const int64_t n = in->n_elem;
+    std::vector<void*> mem;
+    auto up = [&](const void* src, size_t bytes) {
+      void* d = nullptr;
+      CK(cudaMalloc(&d, std::max<size_t>(bytes, 8)));
+      mem.push_back(d);
+      if (bytes && src) CK(cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice));
+      return d;
+    };
+    struct Free {
+      std::vector<void*>& m;
+      ~Free() {
+        for (void* p : m) cudaFree(p);
+      }
+    } free_{mem};
+    ig_cut2 D = *in;
+    D.lo = static_cast<const double*>(up(in->lo, sizeof(double) * 2 * n));
+    D.hi = static_cast<const double*>(up(in->hi, sizeof(double) * 2 * n));
+    D.cls = static_cast<const int32_t*>(up(in->cls, sizeof(int32_t) * 2 * n));
+    D.cut = static_cast<const int32_t*>(up(in->cut, sizeof(int32_t) * n));
+    D.sides = static_cast<const int32_t*>(up(in->sides, sizeof(int32_t) * n));
+    for (int d = 0; d < 2; ++d)
+      D.ext[d] = static_cast<const double*>(up(in->ext[d], sizeof(double) * in->n_cls[d] * q * q));
+    D.prog = static_cast<const double*>(up(in->prog, sizeof(double) * in->prog_len));
+    D.gauss_q = static_cast<const double*>(up(in->gauss_q, sizeof(double) * 2 * go));
+    D.gauss_q1 = static_cast<const double*>(up(in->gauss_q1, sizeof(double) * 2 * (go + 1)));
+    D.table = nullptr;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0));
+    int64_t* dn = static_cast<int64_t*>(up(nullptr, sizeof(int64_t) * 3 * n));
+    k_cq2_points<false><<<static_cast<unsigned>(n), kCq2Threads>>>(D, nullptr, dn, nullptr);
+    CK(cudaGetLastError());
+    std::vector<int64_t> cnt(static_cast<size_t>(3 * n)), offs(static_cast<size_t>(n) + 1, 0);
+    CK(cudaMemcpy(cnt.data(), dn, sizeof(int64_t) * 3 * n, cudaMemcpyDeviceToHost));
+    for (int64_t e = 0; e < n; ++e) offs[e + 1] = offs[e] + cnt[3 * e] + cnt[3 * e + 1] + cnt[3 * e + 2];
+    int64_t* doff = static_cast<int64_t*>(up(offs.data(), sizeof(int64_t) * (n + 1)));
+    double* pts = static_cast<double*>(up(nullptr, sizeof(double) * 4 * std::max<int64_t>(offs[n], 1)));
+    k_cq2_points<true><<<static_cast<unsigned>(n), kCq2Threads>>>(D, doff, nullptr, pts);
+    CK(cudaGetLastError());
+    double* dK = static_cast<double*>(up(nullptr, sizeof(double) * n * nl * nl));
+    double* dF = static_cast<double*>(up(nullptr, sizeof(double) * n * nl));
+    double* dv = static_cast<double*>(up(nullptr, sizeof(double) * n));
+    switch (q) {
+      case 2: k_cq2_integrate<4><<<static_cast<unsigned>(n), kCq2Threads>>>(D, doff, dn, pts, dK, dF, dv); break;
+      case 3: k_cq2_integrate<9><<<static_cast<unsigned>(n), kCq2Threads>>>(D, doff, dn, pts, dK, dF, dv); break;
+      case 4: k_cq2_integrate<16><<<static_cast<unsigned>(n), kCq2Threads>>>(D, doff, dn, pts, dK, dF, dv); break;
+      default: k_cq2_integrate<25><<<static_cast<unsigned>(n), kCq2Threads>>>(D, doff, dn, pts, dK, dF, dv); break;
+    }
     CK(cudaGetLastError());
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));

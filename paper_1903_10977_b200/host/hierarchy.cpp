@@ -489,6 +489,8 @@ struct igh_case {
   // Cut-element quadrature payload (igh_cut3_payload), built on demand.
   std::vector<double> cut_lo, cut_ext[3], cut_prog, g_tet, g_tri, g_box;
   std::vector<int32_t> cut_cls, cut_table;
+  std::vector<double> c2_lo, c2_hi, c2_ext[2], c2_gq, c2_gq1;
+  std::vector<int32_t> c2_cls, c2_cut, c2_sides, c2_table;
   std::vector<double> gamma;
   std::vector<int32_t> kind;
   std::vector<double> coarseL;
@@ -860,6 +862,79 @@ int igh_cut3_payload(igh_case* c, ig_cut3* out) {
     out->gauss_tri = c->g_tri.data();
     out->gauss_box = c->g_box.data();
     out->table = c->cut_table.data();
+    return IG_OK;
+  } catch (const std::exception& e) {
+    return fail(e.what());
+  }
+}
+
+int igh_cut2_payload(igh_case* c, ig_cut2* out) {
+  if (!c || !out) return fail("igh_cut2_payload: null argument");
+  if (c->spaces.empty() || c->el_table.empty() || c->cfg.dim != 2)
+    return fail("igh_cut2_payload: built 2D uniform cases only", IG_UNSUPPORTED);
+  try {
+    const Space& s = *c->spaces.back();
+    if (c->cut_prog.empty() && !s.ls.program(c->cut_prog))
+      return fail("igh_cut2_payload: the level set has no device program (star / affine)", IG_UNSUPPORTED);
+    const int ncls = static_cast<int>(s.ext[0].size() * s.ext[1].size());
+    const int go = c->cfg.gauss_order > 0 ? c->cfg.gauss_order : c->cfg.degree + 1;
+    if (c->c2_table.empty()) {
+      const int ne = static_cast<int>(s.el_ix.size());
+      for (int e = 0; e < ne; ++e) {
+        if (c->el_table[e] < ncls) continue;
+        double lo[3], hi[3];
+        s.grid.cell_box(s.el_ix[e], s.el_iy[e], 0, lo, hi);
+        c->c2_lo.insert(c->c2_lo.end(), lo, lo + 2);
+        c->c2_hi.insert(c->c2_hi.end(), hi, hi + 2);
+        c->c2_cls.push_back(s.ext_cls[0][s.el_ix[e]]);
+        c->c2_cls.push_back(s.ext_cls[1][s.el_iy[e]]);
+        c->c2_cut.push_back(s.el_tag[e] == kCut ? 1 : 0);
+        int mask = 0;  // box_sides (assembly.cpp:24-33): 0 bottom, 1 right, 2 top, 3 left
+        if (c->cfg.dirichlet_box_sides) {
+          if (s.el_iy[e] == 0) mask |= 1;
+          if (s.el_ix[e] == s.grid.res[0] - 1) mask |= 2;
+          if (s.el_iy[e] == s.grid.res[1] - 1) mask |= 4;
+          if (s.el_ix[e] == 0) mask |= 8;
+        }
+        c->c2_sides.push_back(mask);
+        c->c2_table.push_back(c->el_table[e]);
+      }
+      for (int d = 0; d < 2; ++d) {
+        c->c2_ext[d].clear();
+        for (const Mat& m : s.ext[d]) c->c2_ext[d].insert(c->c2_ext[d].end(), m.a.begin(), m.a.end());
+      }
+      std::vector<double> nd, wt;
+      gauss_legendre(go, nd, wt);
+      c->c2_gq = nd;
+      c->c2_gq.insert(c->c2_gq.end(), wt.begin(), wt.end());
+      gauss_legendre(go + 1, nd, wt);
+      c->c2_gq1 = nd;
+      c->c2_gq1.insert(c->c2_gq1.end(), wt.begin(), wt.end());
+    }
+    *out = ig_cut2{};
+    out->p = s.p;
+    out->n_elem = static_cast<int32_t>(c->c2_table.size());
+    out->lo = c->c2_lo.data();
+    out->hi = c->c2_hi.data();
+    out->cls = c->c2_cls.data();
+    out->cut = c->c2_cut.data();
+    out->sides = c->c2_sides.data();
+    for (int d = 0; d < 2; ++d) {
+      out->n_cls[d] = static_cast<int32_t>(s.ext[d].size());
+      out->ext[d] = c->c2_ext[d].data();
+    }
+    const double hmin = std::min(s.grid.h(0), s.grid.h(1));
+    out->beta = c->cfg.beta > 0.0 ? c->cfg.beta : 2.0 / hmin;
+    out->f = c->cfg.body_force;
+    out->depth = c->cfg.quad_depth;
+    out->classify_depth = c->cfg.classify_depth;
+    out->gauss_order = go;
+    out->edge_tol = c->cfg.edge_tol;
+    out->prog_len = static_cast<int32_t>(c->cut_prog.size());
+    out->prog = c->cut_prog.data();
+    out->gauss_q = c->c2_gq.data();
+    out->gauss_q1 = c->c2_gq1.data();
+    out->table = c->c2_table.data();
     return IG_OK;
   } catch (const std::exception& e) {
     return fail(e.what());
