@@ -176,6 +176,32 @@ typedef struct {
   const int32_t *table;    /* n_elem: table index in igh_assembly_payload */
 } ig_cut2;
 
+/* THB (truncated hierarchical B-spline) element integration and global
+ * assembly on the device (the host's assemble_g, host/thb.cpp: the reference's
+ * assemble() over a hierarchical mesh, proj/src/assembly.cpp:36-183).  Every
+ * element is integrated individually (its truncated functions: `erow_ptr`
+ * rows of `E`, Bernstein coefficients x fastest) with the 2D quadrature of
+ * ig_cut2; rows are gathered per DOF over its support in ascending element
+ * order (setFromTriplets), exact zeros dropped, then A = 0.5 (A + A^T). */
+typedef struct {
+  int32_t p, n, n_elem;
+  const double *lo, *hi;      /* n_elem x 2: element cells at their levels */
+  const int32_t *cut;         /* n_elem */
+  const int32_t *sides;       /* n_elem: box-side bit mask (at the element's level) */
+  const int32_t *erow_ptr;    /* n_elem + 1: the element's functions */
+  const int32_t *anchors;     /* erow_ptr[n_elem]: their global DOFs, in row order */
+  const double *E;            /* erow_ptr[n_elem] x (p+1)^2 */
+  const int64_t *supp_ptr;    /* n + 1 */
+  const int32_t *supp_el;     /* elements of each DOF's support, ascending */
+  const int32_t *supp_li;     /* the DOF's row in that element */
+  double beta, f;
+  int32_t depth, classify_depth, gauss_order;
+  double edge_tol;
+  int32_t prog_len;
+  const double *prog;
+  const double *gauss_q, *gauss_q1;
+} ig_thb_asm;
+
 typedef struct ig_hier ig_hier;
 
 /* Device-side sizes and algorithmic byte counts. */
@@ -350,6 +376,10 @@ int ig_cut_quadrature3(const ig_cut3 *in, double *K, double *F, double *vol, dou
 /* 2D: K (n_elem x nl x nl), F (n_elem x nl), vol (volume-rule weight sums, may
  * be NULL), bit-identical to the host.  p <= 4. */
 int ig_cut_quadrature2(const ig_cut2 *in, double *K, double *F, double *vol, double *seconds);
+/* THB: A_out (host CSR, free with ig_csr_free) and b_out (n doubles),
+ * bit-identical to the host assembly.  seconds (may be NULL): [0] wall,
+ * [1] device time.  Elements with more than 64 functions: IG_UNSUPPORTED. */
+int ig_assemble_thb(const ig_thb_asm *in, ig_csr *A_out, double *b_out, double *seconds);
 
 /* Thread-local message for the last non-OK status. */
 const char *ig_last_error(void);

@@ -97,6 +97,9 @@ int igh_cut3_payload(igh_case *c, ig_cut3 *out);
 /* 2D uniform (B-spline / Lagrange) case: every individually integrated
  * element (cut, or with embedding-box sides) for ig_cut_quadrature2. */
 int igh_cut2_payload(igh_case *c, ig_cut2 *out);
+/* THB case (family 2): the finest level's elements, truncated extraction
+ * rows, supports and quadrature data for ig_assemble_thb. */
+int igh_thb_payload(igh_case *c, ig_thb_asm *out);
 /* Kept anchors of level l as untrimmed tensor indices (ax, ay, az) -> n x 3. */
 int igh_anchors(const igh_case *c, int32_t level, int32_t *out_xyz);
 int igh_write(const igh_case *c, const char *path);

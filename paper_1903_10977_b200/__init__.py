@@ -326,12 +326,25 @@ def assemble_on_device(case, device_cut: bool = False):
     """The finest level's global assembly on the GPU:
     the element tables go through ig_assemble, which sums the element
     contributions in the reference's setFromTriplets order and symmetrises
-    (assembly.cpp:164-180).  device_cut: the cut elements' tables are
-    integrated on the device too (cut_quadrature_on_device; 3D B-splines),
-    else the host case's tables are used.  Returns (A as SpMat, b,
+    (assembly.cpp:164-180).  device_cut: the individually integrated
+    elements' tables are computed on the device too (cut_quadrature_on_device),
+    else the host case's tables are used.  THB cases: every element is
+    integrated and gathered on the device (ig_assemble_thb).  Returns (A as SpMat, b,
     (wall_seconds, device_seconds)), bit-identical to the host assembly
     (case.A, case.b)."""
     lib = _ffi.gpu()
+    thb = _ffi.ig_thb_asm()
+    if _ffi.host().igh_thb_payload(case._h, C.byref(thb)) == _ffi.IG_OK:  # THB: element integration + gather
+        out = _ffi.ig_csr()
+        b = np.empty(thb.n)
+        sec = (C.c_double * 2)()
+        _check(lib, lib.ig_assemble_thb(C.byref(thb), C.byref(out), b.ctypes.data_as(_dp), sec), "ig_assemble_thb")
+        try:
+            m = SpMat.from_c(out)
+            A = SpMat(m.shape[0], m.shape[1], m.row_ptr.copy(), m.col_idx.copy(), m.val.copy())
+        finally:
+            lib.ig_csr_free(C.byref(out))
+        return A, b, (sec[0], sec[1])
     pay = _ffi.ig_assembly()
     _check(_ffi.host(), _ffi.host().igh_assembly_payload(case._h, C.byref(pay)), "igh_assembly_payload")
     keep = None

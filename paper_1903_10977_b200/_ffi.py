@@ -69,6 +69,14 @@ class ig_cut2(C.Structure):
                 ("prog_len", i32), ("prog", P(f64)), ("gauss_q", P(f64)), ("gauss_q1", P(f64)), ("table", P(i32))]
 
 
+class ig_thb_asm(C.Structure):
+    _fields_ = [("p", i32), ("n", i32), ("n_elem", i32), ("lo", P(f64)), ("hi", P(f64)), ("cut", P(i32)),
+                ("sides", P(i32)), ("erow_ptr", P(i32)), ("anchors", P(i32)), ("E", P(f64)),
+                ("supp_ptr", P(i64)), ("supp_el", P(i32)), ("supp_li", P(i32)), ("beta", f64), ("f", f64),
+                ("depth", i32), ("classify_depth", i32), ("gauss_order", i32), ("edge_tol", f64),
+                ("prog_len", i32), ("prog", P(f64)), ("gauss_q", P(f64)), ("gauss_q1", P(f64))]
+
+
 class igh_config(C.Structure):
     _fields_ = [("dim", i32), ("geometry", C.c_char_p), ("origin", f64 * 3),
                 ("extent", f64 * 3), ("resolution", i32 * 3), ("family", i32),
@@ -137,6 +145,7 @@ def host() -> C.CDLL:
         lib.igh_support_fraction.argtypes = [C.c_void_p, P(f64)]
         lib.igh_cut3_payload.argtypes = [C.c_void_p, P(ig_cut3)]
         lib.igh_cut2_payload.argtypes = [C.c_void_p, P(ig_cut2)]
+        lib.igh_thb_payload.argtypes = [C.c_void_p, P(ig_thb_asm)]
         lib.igh_anchors.argtypes = [C.c_void_p, i32, P(i32)]
         lib.igh_write.argtypes = [C.c_void_p, C.c_char_p]
         lib.igh_read.argtypes = [C.c_char_p, P(C.c_void_p)]
@@ -157,7 +166,7 @@ GPU_SYMBOLS = (
     "ig_pcg_result", "ig_last_error", "ig_set_option", "ig_richardson",
     "ig_smoother_apply_dir", "ig_smoother_apply_symmetric", "ig_galerkin_hierarchy", "ig_csr_free",
     "ig_factorize_blocks", "ig_blocks_free", "ig_pstrf", "ig_hier_build",
-    "ig_operator_columns", "ig_assemble", "ig_hier_set_option", "ig_hier_matches", "ig_vcycle_at_device", "ig_cut_quadrature3", "ig_cut_quadrature2",
+    "ig_operator_columns", "ig_assemble", "ig_hier_set_option", "ig_hier_matches", "ig_vcycle_at_device", "ig_cut_quadrature3", "ig_cut_quadrature2", "ig_assemble_thb",
 )
 
 
@@ -203,5 +212,6 @@ def gpu() -> C.CDLL:
         lib.ig_hier_matches.argtypes = [vp, P(ig_csr)]
         lib.ig_cut_quadrature3.argtypes = [P(ig_cut3), dp, dp, dp, dp]
         lib.ig_cut_quadrature2.argtypes = [P(ig_cut2), dp, dp, dp, dp]
+        lib.ig_assemble_thb.argtypes = [P(ig_thb_asm), P(ig_csr), dp, dp]
         _gpu = lib
     return _gpu

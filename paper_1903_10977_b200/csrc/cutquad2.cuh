@@ -453,6 +453,26 @@ __global__ void __launch_bounds__(kCq2Threads) k_cq2_points(ig_cut2 I, const int
 
 // Element matrices: volume points add w (gx_i gx_j + gy_i gy_j) and w f val_i;
 // interface and side points add (w beta) val_i val_j (assembly.cpp:66-131).
+// spline::bernstein (host/spline_linalg.cpp)
+__device__ __forceinline__ void cq2_bernstein(int p, double x, double* val, double* der) {
+  double lower[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  val[0] = 1.0;
+  for (int j = 1; j <= p; ++j) {
+    if (j == p)
+      for (int k = 0; k < p; ++k) lower[k] = val[k];
+    double saved = 0.0;
+    for (int r = 0; r < j; ++r) {
+      const double temp = val[r];
+      val[r] = saved + (1.0 - x) * temp;
+      saved = x * temp;
+    }
+    val[j] = saved;
+  }
+  der[0] = -p * lower[0];
+  for (int r = 1; r < p; ++r) der[r] = p * (lower[r - 1] - lower[r]);
+  der[p] = p * lower[p - 1];
+}
+
 template <int NL>
 __global__ void __launch_bounds__(kCq2Threads) k_cq2_integrate(ig_cut2 I, const int64_t* __restrict__ off,
                                                               const int64_t* __restrict__ npt,
@@ -562,6 +582,161 @@ __global__ void __launch_bounds__(kCq2Threads) k_cq2_integrate(ig_cut2 I, const 
     if (ei[s] >= 0) K[ei[s] * NL + ej[s]] = acc[s];
   if (threadIdx.x < NL) Fout[static_cast<int64_t>(e) * NL + threadIdx.x] = facc;
   if (threadIdx.x == 0 && vout) vout[e] = vol;
+}
+
+// ------------------------------------------------------------ THB -------
+// Element integration of a THB element (host/thb.cpp assemble_g): the
+// element's truncated functions are `nl` rows of Bernstein coefficients
+// (eval_el), every element is integrated with the ig_cut2 point rules; K is
+// the full nl x nl element matrix (shared-memory accumulators, one owner per
+// entry), F nl values.  Elements with more than kThbMaxRows rows set *bad.
+constexpr int kThbMaxRows = 32;
+constexpr int kThbBatch = 16;
+__global__ void __launch_bounds__(kCq2Threads) k_thb_integrate(ig_cut2 I, const int32_t* __restrict__ erow_ptr,
+                                                              const double* __restrict__ Eall,
+                                                              const int64_t* __restrict__ off,
+                                                              const int64_t* __restrict__ npt,
+                                                              const double* __restrict__ pts,
+                                                              const int64_t* __restrict__ koff, double* Kout,
+                                                              double* Fout, int* bad) {
+  const int e = blockIdx.x;
+  if (e >= I.n_elem) return;
+  const int p = I.p, q = p + 1, nb = q * q;
+  const int nl = erow_ptr[e + 1] - erow_ptr[e];
+  if (nl > kThbMaxRows) {
+    if (threadIdx.x == 0) atomicAdd(bad, 1);
+    return;
+  }
+  const double lo0 = I.lo[2 * e], lo1 = I.lo[2 * e + 1];
+  const double sx = I.hi[2 * e] - lo0, sy = I.hi[2 * e + 1] - lo1;
+  __shared__ double Es[kThbMaxRows * kCq2MaxQ * kCq2MaxQ];
+  __shared__ double Ks[kThbMaxRows * kThbMaxRows];
+  __shared__ double bb[kThbBatch][3][kCq2MaxQ * kCq2MaxQ];
+  __shared__ double bas[kThbBatch][3][kThbMaxRows];
+  const double* E = Eall + static_cast<int64_t>(erow_ptr[e]) * nb;
+  for (int t = threadIdx.x; t < nl * nb; t += blockDim.x) Es[t] = E[t];
+  for (int t = threadIdx.x; t < nl * nl; t += blockDim.x) Ks[t] = 0.0;
+  double facc = 0.0;
+  const int64_t nvol = npt[3 * e], ntot = npt[3 * e] + npt[3 * e + 1] + npt[3 * e + 2];
+  const double* P = pts + 4 * off[e];
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < ntot; b0 += kThbBatch) {
+    const int nbt = static_cast<int>(ntot - b0 < kThbBatch ? ntot - b0 : kThbBatch);
+    for (int t = threadIdx.x; t < nbt; t += blockDim.x) {
+      const double* pt = P + 4 * (b0 + t);
+      const double u = (pt[0] - lo0) / sx, v = (pt[1] - lo1) / sy;
+      double bu[kCq2MaxQ], du[kCq2MaxQ], bv[kCq2MaxQ], dv[kCq2MaxQ];
+      cq2_bernstein(p, u, bu, du);
+      cq2_bernstein(p, v, bv, dv);
+      for (int jy = 0; jy < q; ++jy)
+        for (int jx = 0; jx < q; ++jx) {
+          const int k = jy * q + jx;
+          bb[t][0][k] = bu[jx] * bv[jy];
+          bb[t][1][k] = du[jx] * bv[jy];
+          bb[t][2][k] = bu[jx] * dv[jy];
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nbt * nl; t += blockDim.x) {
+      const int pi = t / nl, r = t % nl;
+      double a = 0.0, b = 0.0, c = 0.0;
+      for (int k = 0; k < nb; ++k) {
+        a += Es[r * nb + k] * bb[pi][0][k];
+        b += Es[r * nb + k] * bb[pi][1][k];
+        c += Es[r * nb + k] * bb[pi][2][k];
+      }
+      bas[pi][0][r] = a;
+      bas[pi][1][r] = b / sx;
+      bas[pi][2][r] = c / sy;
+    }
+    __syncthreads();
+    for (int k = 0; k < nbt; ++k) {
+      const int64_t g = b0 + k;
+      const double w = P[4 * g + 2];
+      if (g < nvol) {
+        for (int t = threadIdx.x; t < nl * nl; t += blockDim.x) {
+          const int i = t / nl, j = t % nl;
+          Ks[t] += w * (bas[k][1][i] * bas[k][1][j] + bas[k][2][i] * bas[k][2][j]);
+        }
+        if (threadIdx.x < nl && I.f != 0.0) facc += w * I.f * bas[k][0][threadIdx.x];
+      } else {
+        const double wb = w * I.beta;
+        for (int t = threadIdx.x; t < nl * nl; t += blockDim.x) {
+          const int i = t / nl, j = t % nl;
+          Ks[t] += wb * (bas[k][0][i] * bas[k][0][j]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < nl * nl; t += blockDim.x) Kout[koff[e] + t] = Ks[t];
+  if (threadIdx.x < nl) Fout[erow_ptr[e] + threadIdx.x] = facc;
+}
+
+// Row gather of the THB assembly (assemble_g): DOF a walks its support in
+// ascending element order, adds its element row's nonzero entries to a list in
+// first-appearance order (exact zeros dropped), b_a sums its F entries; the
+// list is then sorted by column.  FILL = false: counts; FILL = true: CSR.
+constexpr int kThbMaxCols = 160;
+template <bool FILL>
+__global__ void __launch_bounds__(128) k_thb_rows(int32_t n, const int64_t* __restrict__ supp_ptr,
+                                                 const int32_t* __restrict__ supp_el,
+                                                 const int32_t* __restrict__ supp_li,
+                                                 const int32_t* __restrict__ erow_ptr,
+                                                 const int32_t* __restrict__ anchors,
+                                                 const int64_t* __restrict__ koff, const double* __restrict__ K,
+                                                 const double* __restrict__ F, int32_t* cnt, const int64_t* rowoff,
+                                                 int32_t* col, double* val, double* b, int* bad) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  int32_t cs[kThbMaxCols];
+  double vs[kThbMaxCols];
+  int m = 0;
+  double bsum = 0.0;
+  for (int64_t s = supp_ptr[a]; s < supp_ptr[a + 1]; ++s) {
+    const int e = supp_el[s], li = supp_li[s];
+    const int r0 = erow_ptr[e], nl = erow_ptr[e + 1] - r0;
+    bsum += F[r0 + li];
+    const double* Ke = K + koff[e] + static_cast<int64_t>(li) * nl;
+    for (int lj = 0; lj < nl; ++lj) {
+      const double v = Ke[lj];
+      if (v == 0.0) continue;
+      const int32_t c = anchors[r0 + lj];
+      int k = 0;
+      while (k < m && cs[k] != c) ++k;
+      if (k < m) {
+        vs[k] = vs[k] + v;
+      } else if (m < kThbMaxCols) {
+        cs[m] = c;
+        vs[m] = v;
+        ++m;
+      } else {
+        atomicAdd(bad, 1);
+      }
+    }
+  }
+  if (!FILL) {
+    cnt[a] = m;
+    return;
+  }
+  for (int i = 1; i < m; ++i) {  // insertion sort by column (columns are distinct)
+    const int32_t c = cs[i];
+    const double v = vs[i];
+    int j = i - 1;
+    while (j >= 0 && cs[j] > c) {
+      cs[j + 1] = cs[j];
+      vs[j + 1] = vs[j];
+      --j;
+    }
+    cs[j + 1] = c;
+    vs[j + 1] = v;
+  }
+  const int64_t o = rowoff[a];
+  for (int k = 0; k < m; ++k) {
+    col[o + k] = cs[k];
+    val[o + k] = vs[k];
+  }
+  b[a] = bsum;
 }
 
 }  // namespace igk

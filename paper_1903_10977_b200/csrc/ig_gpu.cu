@@ -3376,3 +3376,141 @@ int ig_cut_quadrature2(const ig_cut2* in, double* K, double* F, double* vol, dou
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int ig_assemble_thb(const ig_thb_asm* in, ig_csr* A_out, double* b_out, double* seconds) {
+  if (!in || !A_out || !b_out) return fail(IG_INVALID_ARGUMENT, "assemble_thb: null argument");
+  *A_out = ig_csr{};
+  if (in->p < 1 || in->p > 4) return fail(IG_UNSUPPORTED, "assemble_thb: degrees 1..4");
+  if (in->prog_len <= 0 || !in->prog) return fail(IG_UNSUPPORTED, "assemble_thb: no level-set program");
+  if (in->n <= 0 || in->n_elem <= 0) return fail(IG_INVALID_ARGUMENT, "assemble_thb: empty space");
+  const auto tw0 = std::chrono::steady_clock::now();
+  return guarded([&] {
+    const int q = in->p + 1, nb = q * q, go = in->gauss_order;
+    const int64_t ne = in->n_elem, n = in->n;
+    std::vector<void*> mem;
+    auto up = [&](const void* src, size_t bytes) {
+      void* d = nullptr;
+      CK(cudaMalloc(&d, std::max<size_t>(bytes, 8)));
+      mem.push_back(d);
+      if (bytes && src) CK(cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice));
+      return d;
+    };
+    struct Free {
+      std::vector<void*>& m;
+      ~Free() {
+        for (void* p : m) cudaFree(p);
+      }
+    } free_{mem};
+    const int64_t nrows = in->erow_ptr[ne];
+    std::vector<int64_t> koff(static_cast<size_t>(ne) + 1, 0);
+    for (int64_t e = 0; e < ne; ++e) {
+      const int64_t nl = in->erow_ptr[e + 1] - in->erow_ptr[e];
+      koff[e + 1] = koff[e] + nl * nl;
+    }
+    ig_cut2 V{};
+    V.p = in->p;
+    V.n_elem = in->n_elem;
+    V.lo = static_cast<const double*>(up(in->lo, sizeof(double) * 2 * ne));
+    V.hi = static_cast<const double*>(up(in->hi, sizeof(double) * 2 * ne));
+    V.cut = static_cast<const int32_t*>(up(in->cut, sizeof(int32_t) * ne));
+    V.sides = static_cast<const int32_t*>(up(in->sides, sizeof(int32_t) * ne));
+    V.beta = in->beta;
+    V.f = in->f;
+    V.depth = in->depth;
+    V.classify_depth = in->classify_depth;
+    V.gauss_order = go;
+    V.edge_tol = in->edge_tol;
+    V.prog_len = in->prog_len;
+    V.prog = static_cast<const double*>(up(in->prog, sizeof(double) * in->prog_len));
+    V.gauss_q = static_cast<const double*>(up(in->gauss_q, sizeof(double) * 2 * go));
+    V.gauss_q1 = static_cast<const double*>(up(in->gauss_q1, sizeof(double) * 2 * (go + 1)));
+    auto* erow = static_cast<int32_t*>(up(in->erow_ptr, sizeof(int32_t) * (ne + 1)));
+    auto* anch = static_cast<int32_t*>(up(in->anchors, sizeof(int32_t) * nrows));
+    auto* dE = static_cast<double*>(up(in->E, sizeof(double) * nrows * nb));
+    auto* sptr = static_cast<int64_t*>(up(in->supp_ptr, sizeof(int64_t) * (n + 1)));
+    auto* sel = static_cast<int32_t*>(up(in->supp_el, sizeof(int32_t) * in->supp_ptr[n]));
+    auto* sli = static_cast<int32_t*>(up(in->supp_li, sizeof(int32_t) * in->supp_ptr[n]));
+    auto* dkoff = static_cast<int64_t*>(up(koff.data(), sizeof(int64_t) * (ne + 1)));
+    auto* bad = static_cast<int*>(up(nullptr, sizeof(int)));
+    CK(cudaMemset(bad, 0, sizeof(int)));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0));
+    int64_t* dn = static_cast<int64_t*>(up(nullptr, sizeof(int64_t) * 3 * ne));
+    k_cq2_points<false><<<static_cast<unsigned>(ne), kCq2Threads>>>(V, nullptr, dn, nullptr);
+    CK(cudaGetLastError());
+    std::vector<int64_t> cnt(static_cast<size_t>(3 * ne)), offs(static_cast<size_t>(ne) + 1, 0);
+    CK(cudaMemcpy(cnt.data(), dn, sizeof(int64_t) * 3 * ne, cudaMemcpyDeviceToHost));
+    for (int64_t e = 0; e < ne; ++e) offs[e + 1] = offs[e] + cnt[3 * e] + cnt[3 * e + 1] + cnt[3 * e + 2];
+    auto* doff = static_cast<int64_t*>(up(offs.data(), sizeof(int64_t) * (ne + 1)));
+    auto* pts = static_cast<double*>(up(nullptr, sizeof(double) * 4 * std::max<int64_t>(offs[ne], 1)));
+    k_cq2_points<true><<<static_cast<unsigned>(ne), kCq2Threads>>>(V, doff, nullptr, pts);
+    CK(cudaGetLastError());
+    auto* dK = static_cast<double*>(up(nullptr, sizeof(double) * std::max<int64_t>(koff[ne], 1)));
+    auto* dF = static_cast<double*>(up(nullptr, sizeof(double) * std::max<int64_t>(nrows, 1)));
+    k_thb_integrate<<<static_cast<unsigned>(ne), kCq2Threads>>>(V, erow, dE, doff, dn, pts, dkoff, dK, dF, bad);
+    CK(cudaGetLastError());
+    auto* rc = static_cast<int32_t*>(up(nullptr, sizeof(int32_t) * n));
+    const unsigned gr = static_cast<unsigned>((n + 127) / 128);
+    k_thb_rows<false><<<gr, 128>>>(static_cast<int32_t>(n), sptr, sel, sli, erow, anch, dkoff, dK, dF, rc, nullptr,
+                                   nullptr, nullptr, nullptr, bad);
+    CK(cudaGetLastError());
+    std::vector<int32_t> hc(static_cast<size_t>(n));
+    CK(cudaMemcpy(hc.data(), rc, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> ro(static_cast<size_t>(n) + 1, 0);
+    std::vector<int32_t> rp(static_cast<size_t>(n) + 1, 0);
+    for (int64_t a = 0; a < n; ++a) ro[a + 1] = ro[a] + hc[a];
+    const int64_t nnz = ro[n];
+    if (nnz > INT32_MAX) throw Error(IG_UNSUPPORTED, "assemble_thb: more than 2^31 nonzeros");
+    for (int64_t a = 0; a <= n; ++a) rp[a] = static_cast<int32_t>(ro[a]);
+    auto* dro = static_cast<int64_t*>(up(ro.data(), sizeof(int64_t) * (n + 1)));
+    auto* drp = static_cast<int32_t*>(up(rp.data(), sizeof(int32_t) * (n + 1)));
+    auto* col = static_cast<int32_t*>(up(nullptr, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+    auto* val = static_cast<double*>(up(nullptr, sizeof(double) * std::max<int64_t>(nnz, 1)));
+    auto* sym = static_cast<double*>(up(nullptr, sizeof(double) * std::max<int64_t>(nnz, 1)));
+    auto* db = static_cast<double*>(up(nullptr, sizeof(double) * n));
+    k_thb_rows<true><<<gr, 128>>>(static_cast<int32_t>(n), sptr, sel, sli, erow, anch, dkoff, dK, dF, nullptr, dro,
+                                  col, val, db, bad);
+    CK(cudaGetLastError());
+    k_asm_sym<<<gr, 128>>>(static_cast<int32_t>(n), drp, col, val, sym, bad);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    int hbad = 0;
+    CK(cudaMemcpy(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost));
+    if (hbad) throw Error(IG_UNSUPPORTED, "assemble_thb: an element has more than 32 functions, a row more than "
+                                          "160 columns, or the pattern is unsymmetric");
+    auto* hp = static_cast<int32_t*>(std::malloc(4 * (static_cast<size_t>(n) + 1)));
+    auto* hcol = static_cast<int32_t*>(std::malloc(4 * std::max<size_t>(static_cast<size_t>(nnz), 1)));
+    auto* hv = static_cast<double*>(std::malloc(8 * std::max<size_t>(static_cast<size_t>(nnz), 1)));
+    if (!hp || !hcol || !hv) {
+      std::free(hp);
+      std::free(hcol);
+      std::free(hv);
+      throw Error(IG_CUDA_ERROR, "assemble_thb: host allocation failed");
+    }
+    std::copy(rp.begin(), rp.end(), hp);
+    CK(cudaMemcpy(hcol, col, 4 * static_cast<size_t>(nnz), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hv, sym, 8 * static_cast<size_t>(nnz), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b_out, db, 8 * static_cast<size_t>(n), cudaMemcpyDeviceToHost));
+    A_out->n_rows = A_out->n_cols = static_cast<int32_t>(n);
+    A_out->nnz = nnz;
+    A_out->row_ptr = hp;
+    A_out->col_idx = hcol;
+    A_out->val = hv;
+    if (seconds) {
+      seconds[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - tw0).count();
+      seconds[1] = ms * 1e-3;
+    }
+    return IG_OK;
+  });
+}
+
+}  // extern "C"

@@ -491,6 +491,9 @@ struct igh_case {
   std::vector<int32_t> cut_cls, cut_table;
   std::vector<double> c2_lo, c2_hi, c2_ext[2], c2_gq, c2_gq1;
   std::vector<int32_t> c2_cls, c2_cut, c2_sides, c2_table;
+  std::vector<double> t_lo, t_hi, t_E;
+  std::vector<int32_t> t_cut, t_sides, t_rptr, t_anchors, t_sel, t_sli;
+  std::vector<int64_t> t_sptr;
   std::vector<double> gamma;
   std::vector<int32_t> kind;
   std::vector<double> coarseL;
@@ -935,6 +938,89 @@ int igh_cut2_payload(igh_case* c, ig_cut2* out) {
     out->gauss_q = c->c2_gq.data();
     out->gauss_q1 = c->c2_gq1.data();
     out->table = c->c2_table.data();
+    return IG_OK;
+  } catch (const std::exception& e) {
+    return fail(e.what());
+  }
+}
+
+int igh_thb_payload(igh_case* c, ig_thb_asm* out) {
+  if (!c || !out) return fail("igh_thb_payload: null argument");
+  if (c->gspaces.empty()) return fail("igh_thb_payload: built THB cases only", IG_UNSUPPORTED);
+  try {
+    const GSpace& s = *c->gspaces.back();
+    if (c->cut_prog.empty() && !s.ls.program(c->cut_prog))
+      return fail("igh_thb_payload: the level set has no device program (star / affine)", IG_UNSUPPORTED);
+    const HMesh& mesh = s.mesh;
+    const int go = c->cfg.gauss_order > 0 ? c->cfg.gauss_order : c->cfg.degree + 1;
+    if (c->t_rptr.empty()) {
+      const int ne = static_cast<int>(s.el.size());
+      c->t_rptr.assign(1, 0);
+      for (int e = 0; e < ne; ++e) {
+        const GSpace::El& el = s.el[e];
+        double lo[2], hi[2];
+        mesh.cell_box(el.l, el.ix, el.iy, lo, hi);
+        c->t_lo.insert(c->t_lo.end(), lo, lo + 2);
+        c->t_hi.insert(c->t_hi.end(), hi, hi + 2);
+        c->t_cut.push_back(el.tag == kCut ? 1 : 0);
+        int mask = 0;
+        if (c->cfg.dirichlet_box_sides) {
+          const int cx = mesh.cells_x(el.l), cy = mesh.cells_y(el.l);
+          if (el.iy == 0) mask |= 1;
+          if (el.ix == cx - 1) mask |= 2;
+          if (el.iy == cy - 1) mask |= 4;
+          if (el.ix == 0) mask |= 8;
+        }
+        c->t_sides.push_back(mask);
+        c->t_anchors.insert(c->t_anchors.end(), el.anchors.begin(), el.anchors.end());
+        c->t_E.insert(c->t_E.end(), el.E.begin(), el.E.end());
+        c->t_rptr.push_back(static_cast<int32_t>(c->t_anchors.size()));
+      }
+      const int n = s.n();
+      c->t_sptr.assign(1, 0);
+      for (int a = 0; a < n; ++a) {
+        for (int e : s.supp[a]) {
+          const GSpace::El& el = s.el[e];
+          const int li = static_cast<int>(std::find(el.anchors.begin(), el.anchors.end(), a) - el.anchors.begin());
+          c->t_sel.push_back(e);
+          c->t_sli.push_back(li);
+        }
+        c->t_sptr.push_back(static_cast<int64_t>(c->t_sel.size()));
+      }
+      std::vector<double> nd, wt;
+      gauss_legendre(go, nd, wt);
+      c->c2_gq = nd;
+      c->c2_gq.insert(c->c2_gq.end(), wt.begin(), wt.end());
+      gauss_legendre(go + 1, nd, wt);
+      c->c2_gq1 = nd;
+      c->c2_gq1.insert(c->c2_gq1.end(), wt.begin(), wt.end());
+    }
+    *out = ig_thb_asm{};
+    out->p = s.p;
+    out->n = s.n();
+    out->n_elem = static_cast<int32_t>(s.el.size());
+    out->lo = c->t_lo.data();
+    out->hi = c->t_hi.data();
+    out->cut = c->t_cut.data();
+    out->sides = c->t_sides.data();
+    out->erow_ptr = c->t_rptr.data();
+    out->anchors = c->t_anchors.data();
+    out->E = c->t_E.data();
+    out->supp_ptr = c->t_sptr.data();
+    out->supp_el = c->t_sel.data();
+    out->supp_li = c->t_sli.data();
+    const int M = mesh.max_level();
+    const double hmin = std::min(mesh.g.extent[0] / mesh.cells_x(M), mesh.g.extent[1] / mesh.cells_y(M));
+    out->beta = c->cfg.beta > 0.0 ? c->cfg.beta : 2.0 / hmin;
+    out->f = c->cfg.body_force;
+    out->depth = c->cfg.quad_depth;
+    out->classify_depth = c->cfg.classify_depth;
+    out->gauss_order = go;
+    out->edge_tol = c->cfg.edge_tol;
+    out->prog_len = static_cast<int32_t>(c->cut_prog.size());
+    out->prog = c->cut_prog.data();
+    out->gauss_q = c->c2_gq.data();
+    out->gauss_q1 = c->c2_gq1.data();
     return IG_OK;
   } catch (const std::exception& e) {
     return fail(e.what());

@@ -43,7 +43,15 @@ def test_assembly_c4_full_size():
           f"{case.info.seconds_assemble:.2f} s (incl. cut-cell quadrature)")
 
 
-def test_assembly_thb_not_supported():
+@pytest.mark.parametrize("full", [False, True])
+def test_assembly_thb_bitwise(full):
+    """THB (C5's space): every element integrated on the device (truncated
+    extraction rows, the 2D quadrature rules) and gathered per DOF over its
+    support in element order -- A and b bit-identical to the host's
+    assemble_g (host/thb.cpp)."""
     from paper_1903_10977_b200 import assemble_on_device, build_case, configs
-    with pytest.raises(ValueError):
-        assemble_on_device(build_case(configs.c5(base=32, levels=3)))
+    case = build_case(configs.c5() if full else configs.c5(base=32, levels=3))
+    A, b, (wall, dev) = assemble_on_device(case)
+    assert np.array_equal(A.row_ptr, case.A.row_ptr) and np.array_equal(A.col_idx, case.A.col_idx)
+    assert np.array_equal(A.val, case.A.val) and np.array_equal(b, case.b)
+    print(f"THB n={case.n}: {dev * 1e3:.1f} ms device, {wall:.2f} s wall")
