@@ -104,6 +104,25 @@ __device__ __forceinline__ double cta_reduce(double v, double* sm8) {
   return t;
 }
 
+// Lane t of the last CTA: P[t] + P[t+256] + ... in ascending order (the
+// canonical partials sum).  All 16 loads of a batch are issued before its
+// adds -- predicated, so even a short tail is one L2 round trip per 16
+// partials (profiles/reduce_micro.cu: -2 us per reduction kernel at C4 size
+// against 8-load batches with a serial remainder).  The predicated-off
+// slots add +0, a no-op: the running sum starts at +0 and is never -0.
+__device__ __forceinline__ double partials_lane_sum(const double* partials, unsigned int nparts) {
+  constexpr int T = 16;
+  double a = 0.0;
+  for (unsigned int k = threadIdx.x; k < nparts; k += T * kCta) {
+    double q[T];
+#pragma unroll
+    for (int u = 0; u < T; ++u) q[u] = (k + u * kCta < nparts) ? __ldcg(partials + k + u * kCta) : 0.0;
+#pragma unroll
+    for (int u = 0; u < T; ++u) a = a + q[u];
+  }
+  return a;
+}
+
 // Arrive once per CTA (after this CTA wrote its chunk partials); the last CTA
 // to arrive reduces all nparts partials (lane t sums P[t], P[t+256], ...
 // ascending, then cta_reduce) and returns true with *total set (valid in every
@@ -122,19 +141,7 @@ __device__ __forceinline__ bool grid_finish(unsigned int nparts, const double* p
   __syncthreads();
   if (!is_last) return false;
   __threadfence();
-  // Loads are issued 8 at a time ahead of the (serial) adds so the tail is
-  // one L2 round trip per 8 partials, not per partial.
-  double a = 0.0;
-  unsigned int k = threadIdx.x;
-  for (; k + 7 * kCta < nparts; k += 8 * kCta) {
-    double q[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) q[u] = __ldcg(partials + k + u * kCta);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) a = a + q[u];
-  }
-  for (; k < nparts; k += kCta) a = a + __ldcg(partials + k);
-  const double t = cta_reduce(a, sm8f);
+  const double t = cta_reduce(partials_lane_sum(partials, nparts), sm8f);
   if (threadIdx.x == 0) {
     tot = t;
     *counter = 0u;
@@ -213,20 +220,7 @@ __device__ __forceinline__ bool last_cta_total(double v, double* partials,
   __syncthreads();
   if (!is_last) return false;
   __threadfence();
-  // Lane t: P[t] + P[t+256] + ... in ascending order.  Loads are issued 8 at a
-  // time ahead of the (serial) adds so the tail is one L2 round trip per 8
-  // partials, not per partial.
-  double a = 0.0;
-  const unsigned int nb = gridDim.x;
-  unsigned int k = threadIdx.x;
-  for (; k + 7 * kCta < nb; k += 8 * kCta) {
-    double q[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) q[u] = __ldcg(partials + k + u * kCta);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) a = a + q[u];
-  }
-  for (; k < nb; k += kCta) a = a + __ldcg(partials + k);
+  const double a = partials_lane_sum(partials, gridDim.x);
   __syncthreads();  // sm8 reuse
   const double t = cta_reduce(a, sm8);
   if (threadIdx.x == 0) {
