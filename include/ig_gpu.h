@@ -371,7 +371,7 @@ int ig_hier_build(const ig_csr *A_fine, const ig_csr *R, const ig_blocks *prefil
  * row-major, symmetric), F (n_cut x nl), vol (n_cut: integrated volume
  * fraction, may be NULL); bit-identical to the host's element tables.
  * seconds (may be NULL): device time.  IG_UNSUPPORTED for level sets without
- * a device program or p > 3. */
+ * a device program or p > 2 (shared-memory basis tables). */
 int ig_cut_quadrature3(const ig_cut3 *in, double *K, double *F, double *vol, double *seconds);
 /* 2D: K (n_elem x nl x nl), F (n_elem x nl), vol (volume-rule weight sums, may
  * be NULL), bit-identical to the host.  p <= 4. */

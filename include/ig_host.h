@@ -68,6 +68,19 @@ typedef struct {
 
 void igh_config_default(igh_config *cfg);
 int igh_build(const igh_config *cfg, igh_case **out);
+/* The geometric half of igh_build only -- the host part of the device setup
+ * pipeline: trimmed spaces of every level, the
+ * restrictions R, the pre-filter Schwarz layouts (+ colours), the damping,
+ * the Inside-class element tables and the element -> table map.  The cut /
+ * box-side elements are NOT integrated (their tables stay zero: the device
+ * computes them, ig_cut_quadrature2/3), nothing is assembled (A of every
+ * level is an n x n pattern without entries, the rhs zeros), no Galerkin
+ * product, block factorisation or pivoted Cholesky is formed (ig_assemble +
+ * ig_hier_build do that on the device).  The payload functions
+ * (igh_cut2/3_payload, igh_thb_payload, igh_assembly_payload,
+ * igh_prefilter_blocks) and igh_levels (R, gamma, colours) work on such a
+ * case; igh_write and igh_support_fraction do not. */
+int igh_build_geometry(const igh_config *cfg, igh_case **out);
 /* Pointers stay owned by the case (valid until igh_destroy). */
 int igh_levels(const igh_case *c, const ig_level **levels, int32_t *n_levels,
                const ig_coarse **coarse);

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes as C
 import dataclasses
+import time
 from typing import Optional, Sequence
 
 import numpy as np
@@ -35,7 +36,7 @@ from . import _ffi
 __all__ = [
     "ConvergenceReport", "Breakdown", "NotConverged", "ResolutionError",
     "SmootherConfig", "CaseConfig", "SpMat", "Case", "build_case",
-    "MgHierarchy", "vcycle", "pcg", "seed_offsets",
+    "MgHierarchy", "vcycle", "pcg", "seed_offsets", "setup_on_device", "DeviceSetup",
 ]
 
 _dp = C.POINTER(C.c_double)
@@ -373,6 +374,57 @@ def assemble_on_device(case, device_cut: bool = False):
     return A, b, (sec[0], sec[1])
 
 
+@dataclasses.dataclass
+class DeviceSetup:
+    """setup_on_device's result: the geometry-only host case, the device-
+    assembled finest system (A, b) and the device-built hierarchy."""
+    case: "Case"
+    A: "SpMat"
+    b: np.ndarray
+    hierarchy: "MgHierarchy"
+    seconds: dict
+
+    def close(self):
+        self.hierarchy.close()
+        self.case.close()
+
+
+def setup_on_device(cfg_or_case) -> DeviceSetup:
+    """The whole setup with every numeric stage on the GPU (SURVEY.md 8(f)
+    rows 2-3; runner.cpp:523-532 build_case + multigrid.cpp:12-75 build):
+      host    igh_build_geometry: trimmed spaces, restrictions, pre-filter
+              Schwarz layouts, Inside-class element tables (no integration of
+              cut / box-side elements, no assembly, no Galerkin, no factors);
+      device  cut-element quadrature (ig_cut_quadrature2/3) or, for THB, every
+              element's integration (ig_assemble_thb), then the row-gather
+              assembly + symmetrisation (ig_assemble);
+      device  Galerkin chain, block eigen-filter + LLT, coarsest pivoted
+              Cholesky, layouts (ig_hier_build).
+    A, b and the hierarchy are bit-identical to the host pipeline's
+    (build_case + MgHierarchy; tests/test_gpu_device_setup.py).  Level sets
+    without a device program (star / affine) are IG_UNSUPPORTED.  seconds:
+    host_geometry, assembly (wall; device part in assembly_device),
+    hierarchy (wall; device kernels in hierarchy_device), total."""
+    t0 = time.perf_counter()
+    own = not isinstance(cfg_or_case, Case)
+    case = build_case(cfg_or_case, geometry_only=True) if own else cfg_or_case
+    try:
+        if not case.geometry_only:
+            raise ValueError("setup_on_device: pass a CaseConfig or a geometry-only case")
+        t1 = time.perf_counter()
+        A, b, asec = assemble_on_device(case, device_cut=True)
+        t2 = time.perf_counter()
+        h = MgHierarchy.build_on_device(case, A)
+        t3 = time.perf_counter()
+    except BaseException:
+        if own:
+            case.close()
+        raise
+    sec = {"host_geometry": t1 - t0, "assembly": t2 - t1, "assembly_device": asec[1],
+           "hierarchy": t3 - t2, "hierarchy_device": h.setup_seconds[1], "total": t3 - t0}
+    return DeviceSetup(case, A, b, h, sec)
+
+
 class TooLarge(RuntimeError):
     """spectral.hpp:16 TooLarge."""
 
@@ -442,28 +494,36 @@ def dense_spectrum(h: "MgHierarchy", name: str = "vcycle", want_vectors: bool = 
 
 class Case:
     """Host-built case: fine system (A, b) and the multigrid hierarchy payload
-    that crosses the C-ABI (owned by libig_host.so until close())."""
+    that crosses the C-ABI (owned by libig_host.so until close()).
+    geometry_only (build_case(cfg, geometry_only=True), igh_build_geometry):
+    spaces, restrictions, pre-filter block layouts and element tables only --
+    A and b are None until the device pipeline (setup_on_device) forms them."""
 
-    def __init__(self, handle: C.c_void_p, cfg: Optional[CaseConfig] = None):
+    def __init__(self, handle: C.c_void_p, cfg: Optional[CaseConfig] = None, geometry_only: bool = False):
         self._h = handle
         self.config = cfg
+        self.geometry_only = geometry_only
         lib = _ffi.host()
         self._lv = C.POINTER(_ffi.ig_level)()
         nl = C.c_int32()
         self._co = C.POINTER(_ffi.ig_coarse)()
         lib.igh_levels(self._h, C.byref(self._lv), C.byref(nl), C.byref(self._co))
         self.n_levels = nl.value
-        n = C.c_int32()
-        bp = lib.igh_rhs(self._h, C.byref(n))
-        self.b = np.ctypeslib.as_array(bp, (n.value,)).copy()
         info = _ffi.igh_info()
         lib.igh_get_info(self._h, C.byref(info))
         self.info = info
+        if geometry_only:
+            self.b = None
+            self.A = None
+            return
+        n = C.c_int32()
+        bp = lib.igh_rhs(self._h, C.byref(n))
+        self.b = np.ctypeslib.as_array(bp, (n.value,)).copy()
         self.A = SpMat.from_c(self._lv[self.n_levels - 1].A, self)
 
     @property
     def n(self) -> int:
-        return self.b.shape[0]
+        return self.info.n[self.n_levels - 1]
 
     def level_dofs(self):
         return [self.info.n[i] for i in range(self.n_levels)]
@@ -550,12 +610,15 @@ class Case:
             pass
 
 
-def build_case(cfg: CaseConfig) -> Case:
-    """build_case + MgHierarchy::build host half (runner.cpp:523-532, multigrid.cpp:12-75)."""
+def build_case(cfg: CaseConfig, geometry_only: bool = False) -> Case:
+    """build_case + MgHierarchy::build host half (runner.cpp:523-532, multigrid.cpp:12-75).
+    geometry_only: the geometric half only (igh_build_geometry) -- the host
+    part of the device setup pipeline (setup_on_device)."""
     c = cfg.to_c()
     h = C.c_void_p()
-    _check(_ffi.host(), _ffi.host().igh_build(C.byref(c), C.byref(h)), "igh_build")
-    return Case(h, cfg)
+    fn = _ffi.host().igh_build_geometry if geometry_only else _ffi.host().igh_build
+    _check(_ffi.host(), fn(C.byref(c), C.byref(h)), "igh_build_geometry" if geometry_only else "igh_build")
+    return Case(h, cfg, geometry_only)
 
 
 # -------------------------------------------------------------- device -----
@@ -573,6 +636,8 @@ class MgHierarchy:
     def __init__(self, case):
         """`case`: a host-built Case, or any payload exposing levels_c() ->
         (ig_level*, n_levels, ig_coarse*) (the C-ABI boundary structs)."""
+        if getattr(case, "geometry_only", False):
+            raise ValueError("MgHierarchy: a geometry-only case has no operators (use setup_on_device)")
         lib = _ffi.gpu()
         lv, nl, co = case.levels_c()
         self._h = C.c_void_p()
@@ -587,16 +652,24 @@ class MgHierarchy:
         self.info = info
 
     @staticmethod
-    def build_on_device(case) -> "MgHierarchy":
+    def build_on_device(case, A: Optional["SpMat"] = None) -> "MgHierarchy":
         """MgHierarchy::build's algebraic half on the GPU (ig_hier_build): the
         Galerkin chain, the Schwarz block factorisations and the coarsest
         pivoted Cholesky are computed on the device from the finest operator,
         the restrictions and the pre-filter block layouts of the host-built
         `case` (its own coarse operators and factors are NOT used).  The
-        handle is bit-identical to MgHierarchy(case).  self.setup_seconds =
-        (wall, device kernels, ig_hier_create)."""
+        handle is bit-identical to MgHierarchy(case).  A: the finest operator
+        (default: the case's; required for a geometry-only case -- the device
+        assembly's, setup_on_device).  self.setup_seconds = (wall, device
+        kernels, ig_hier_create)."""
         lib = _ffi.gpu()
         lv, nl, co = case.levels_c()
+        if A is None:
+            if getattr(case, "geometry_only", False):
+                raise ValueError("build_on_device: a geometry-only case needs the finest operator A")
+            A = SpMat.from_c(lv[nl - 1].A, case)
+        if A.shape != (case.n, case.n):
+            raise ValueError(f"build_on_device: A is {A.shape}, the finest level has {case.n} DOFs")
         sm = case.config.smoother if case.config is not None else SmootherConfig()
         R = (_ffi.ig_csr * nl)()
         pre = (_ffi.ig_blocks * nl)()
@@ -617,13 +690,19 @@ class MgHierarchy:
         self = MgHierarchy.__new__(MgHierarchy)
         self._h = C.c_void_p()
         sec = (C.c_double * 3)()
-        _check(lib, lib.ig_hier_build(C.byref(lv[nl - 1].A), R, pre, gam, lv[nl - 1].smoother_kind if nl > 1 else 2,
+        rp = np.ascontiguousarray(A.row_ptr, np.int32)
+        ci = np.ascontiguousarray(A.col_idx, np.int32)
+        vv = np.ascontiguousarray(A.val, np.float64)
+        keep += [rp, ci, vv]
+        a = _ffi.ig_csr(A.shape[0], A.shape[1], A.nnz, rp.ctypes.data_as(C.POINTER(C.c_int32)),
+                        ci.ctypes.data_as(C.POINTER(C.c_int32)), vv.ctypes.data_as(C.POINTER(C.c_double)))
+        _check(lib, lib.ig_hier_build(C.byref(a), R, pre, gam, lv[nl - 1].smoother_kind if nl > 1 else 2,
                                       float(sm.filter_ratio), nl, C.byref(self._h), sec), "ig_hier_build")
         del keep
         self.case = case
         self._lv = lv
         self._n = [lv[i].A.n_rows for i in range(nl)]
-        self.A = SpMat.from_c(lv[nl - 1].A, case)
+        self.A = A
         info = _ffi.ig_info()
         lib.ig_hier_info(self._h, C.byref(info))
         self.info = info

@@ -136,6 +136,7 @@ def host() -> C.CDLL:
         lib.igh_config_default.argtypes = [P(igh_config)]
         lib.igh_config_default.restype = None
         lib.igh_build.argtypes = [P(igh_config), P(C.c_void_p)]
+        lib.igh_build_geometry.argtypes = [P(igh_config), P(C.c_void_p)]
         lib.igh_levels.argtypes = [C.c_void_p, P(P(ig_level)), P(i32), P(P(ig_coarse))]
         lib.igh_rhs.argtypes = [C.c_void_p, P(i32)]
         lib.igh_rhs.restype = P(f64)

@@ -32,7 +32,7 @@ constexpr int kCqBatch = 32;        // points per integration batch
 __device__ __forceinline__ double cq_min(double a, double b) { return (b < a) ? b : a; }  // std::min
 __device__ __forceinline__ double cq_max(double a, double b) { return (a < b) ? b : a; }  // std::max
 
-__device__ double ls_eval(const double* __restrict__ P, int len, const double* p) {
+__device__ double ls_eval(const double* P, int len, const double* p) {
   double st[16];
   int sp = 0;
   for (int k = 0; k < len;) {
@@ -76,7 +76,7 @@ __device__ double ls_eval(const double* __restrict__ P, int len, const double* p
 }
 
 // LsNode::bounds over an axis box (every node of a device program has one).
-__device__ void ls_bounds(const double* __restrict__ P, int len, const double* lo, const double* hi, int dim,
+__device__ void ls_bounds(const double* P, int len, const double* lo, const double* hi, int dim,
                           double& a, double& b) {
   double sa[16], sb[16];
   int sp = 0;
@@ -152,6 +152,61 @@ __device__ void ls_bounds(const double* __restrict__ P, int len, const double* l
   b = sb[0];
 }
 
+// The program specialised to an axis box: a min (max) node whose child B
+// lies, over the whole box, strictly above (below) its other child A by more
+// than a rounding margin is replaced by A -- min(a, b) returns a bit for bit
+// wherever b > a, so every value (and every ls_bounds interval of a sub-box)
+// the specialised program produces inside the box equals the full program's.
+// A union of 64 discs (C3) keeps the one or two discs near an element.
+// Returns the specialised length (<= len) written to out.
+__device__ int ls_specialize(const double* P, int len, const double* lo, const double* hi, int dim,
+                             double* out) {
+  double sa[16], sb[16];
+  int ss[16];
+  int sp = 0, o = 0;
+  double scale = 0.0;
+  for (int d = 0; d < dim; ++d) scale = cq_max(scale, fabs(lo[d]) + fabs(hi[d]));
+  const double m = 1e-9 * (1.0 + scale);
+  for (int k = 0; k < len;) {
+    const int op = static_cast<int>(P[k]);
+    if (op <= 3) {  // primitive: copy, and its interval over the box
+      const int sz = op == 0 ? 2 : (op == 3 ? 8 : 6);
+      ls_bounds(P + k, sz, lo, hi, dim, sa[sp], sb[sp]);
+      ss[sp++] = o;
+      for (int t = 0; t < sz; ++t) out[o++] = P[k + t];
+      k += sz;
+      continue;
+    }
+    if (op == 6) {  // negation
+      const double a = -sb[sp - 1], b = -sa[sp - 1];
+      sa[sp - 1] = a;
+      sb[sp - 1] = b;
+      out[o++] = 6.0;
+      k += 1;
+      continue;
+    }
+    --sp;  // min / max of A = [sp - 1] and B = [sp] (B's code follows A's)
+    const bool mn = op == 4;
+    const bool dropB = mn ? (sa[sp] > sb[sp - 1] + m) : (sb[sp] < sa[sp - 1] - m);
+    const bool dropA = mn ? (sa[sp - 1] > sb[sp] + m) : (sb[sp - 1] < sa[sp] - m);
+    if (dropB) {
+      o = ss[sp];
+    } else if (dropA) {
+      const int n = o - ss[sp];
+      for (int t = 0; t < n; ++t) out[ss[sp - 1] + t] = out[ss[sp] + t];
+      o = ss[sp - 1] + n;
+      sa[sp - 1] = sa[sp];
+      sb[sp - 1] = sb[sp];
+    } else {
+      sa[sp - 1] = mn ? cq_min(sa[sp - 1], sa[sp]) : cq_max(sa[sp - 1], sa[sp]);
+      sb[sp - 1] = mn ? cq_min(sb[sp - 1], sb[sp]) : cq_max(sb[sp - 1], sb[sp]);
+      out[o++] = static_cast<double>(op);
+    }
+    k += 1;
+  }
+  return o;
+}
+
 // classify_cell (host/levelset.cpp): 0 Inside, 1 Outside, 2 Cut.
 __device__ int cq_classify(const double* P, int len, const double* lo, const double* hi, int depth) {
   double vmin, vmax;
@@ -223,7 +278,9 @@ struct CqSink {
 
 struct CqCtx {
   const ig_cut3* in;
-  const double* elo;  // element lower corner (physical)
+  const double* elo;   // element lower corner (physical)
+  const double* prog;  // level-set program (the element's specialisation)
+  int prog_len;
 };
 
 __device__ __forceinline__ void cq_ref(const CqCtx& c, const double* x, double* u) {
@@ -243,7 +300,7 @@ __device__ void cq_clip_tet(const CqCtx& c, const double x[4][3], const double f
   const ig_cut3& I = *c.in;
   auto cross = [&](int a, int b, double* u) {
     double r[3];
-    if (W) cq_isect(I.prog, I.prog_len, x[a], x[b], I.edge_tol, r);
+    if (W) cq_isect(c.prog, c.prog_len, x[a], x[b], I.edge_tol, r);
     else r[0] = r[1] = r[2] = 0.0;
     cq_ref(c, r, u);
   };
@@ -322,7 +379,7 @@ __device__ void cq_cut_leaf(const CqCtx& c, const double* lo, const double* hi, 
     x[k][0] = (k & 1) ? hi[0] : lo[0];
     x[k][1] = (k & 2) ? hi[1] : lo[1];
     x[k][2] = (k & 4) ? hi[2] : lo[2];
-    f[k] = ls_eval(I.prog, I.prog_len, x[k]);
+    f[k] = ls_eval(c.prog, c.prog_len, x[k]);
   }
   for (int t = 0; t < 6; ++t) {
     double tx[4][3], tf[4];
@@ -359,7 +416,7 @@ __device__ void cq_leaf(const CqCtx& c, int leaf, int D, CqSink<W>& sk) {
           hi[k] = mid[k];
       }
     }
-    const int cls = cq_classify(I.prog, I.prog_len, lo, hi, I.classify_depth);
+    const int cls = cq_classify(c.prog, c.prog_len, lo, hi, I.classify_depth);
     if (cls == 1) return;
     if (cls == 0) {
       const int rest = leaf & ((1 << (3 * (D - d))) - 1);
@@ -380,12 +437,34 @@ __device__ void cq_leaf(const CqCtx& c, int leaf, int D, CqSink<W>& sk) {
 
 // Counts (W = false: count[e]) or writes (W = true: from prim + off[e])
 // the primitives of every cut element; one CTA per element.
+// Per-element specialised programs (ls_specialize), one thread per element:
+// element e's program at out + e * len (len = the full program's length, an
+// upper bound), its length in olen[e].  3D: the cell [lo, lo + h]; 2D: the
+// box [lo, hi]; both grown by half the cell size on every side (every point
+// the element's leaves, chords and bisections evaluate lies inside).
+__global__ void k_ls_specialize(const double* __restrict__ P, int len, int n, int dim, const double* __restrict__ elo,
+                                const double* __restrict__ ehi, const double* h3, double* out, int* olen) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  for (int k = 0; k < dim; ++k) {
+    const double a = elo[static_cast<int64_t>(dim) * e + k];
+    const double b = ehi ? ehi[static_cast<int64_t>(dim) * e + k] : a + h3[k];
+    const double g = 0.5 * (b - a);
+    lo[k] = a - g;
+    hi[k] = b + g;
+  }
+  olen[e] = ls_specialize(P, len, lo, hi, dim, out + static_cast<int64_t>(e) * len);
+}
+
 template <bool W>
 __global__ void __launch_bounds__(kCqThreads) k_cq_prims(ig_cut3 I, const int64_t* __restrict__ off,
-                                                        int64_t* count, double* prim) {
+                                                        int64_t* count, double* prim, const double* eprog,
+                                                        const int* elen) {
   const int e = blockIdx.x;
   if (e >= I.n_cut) return;
-  CqCtx c{&I, I.lo + 3 * static_cast<int64_t>(e)};
+  const int sl = elen[e];
+  CqCtx c{&I, I.lo + 3 * static_cast<int64_t>(e), eprog + static_cast<int64_t>(e) * I.prog_len, sl};
   const int D = I.depth;
   const int nleaf = 1 << (3 * D);
   const int l0 = static_cast<int>(static_cast<int64_t>(nleaf) * threadIdx.x / blockDim.x);

@@ -384,11 +384,16 @@ __device__ void cq2_side(const ig_cut2& I, const Box2d& cell, int side, Cq2Sink<
 // Points of element e: [volume points | interface points | side points].
 // npt[3 e + k]: counts (W = false); off: per-element point offsets (W = true).
 template <bool W>
-__global__ void __launch_bounds__(kCq2Threads) k_cq2_points(ig_cut2 I, const int64_t* __restrict__ off,
-                                                           int64_t* npt, double* pts) {
+__global__ void __launch_bounds__(kCq2Threads) k_cq2_points(ig_cut2 I0, const int64_t* __restrict__ off,
+                                                           int64_t* npt, double* pts, const double* eprog,
+                                                           const int* elen) {
   const int e = blockIdx.x;
-  if (e >= I.n_elem) return;
-  const Box2d root{{I.lo[2 * e], I.lo[2 * e + 1]}, {I.hi[2 * e], I.hi[2 * e + 1]}};
+  if (e >= I0.n_elem) return;
+  const Box2d root{{I0.lo[2 * e], I0.lo[2 * e + 1]}, {I0.hi[2 * e], I0.hi[2 * e + 1]}};
+  // The element's specialised level-set program (cutquad.cuh k_ls_specialize).
+  ig_cut2 I = I0;
+  I.prog = eprog + static_cast<int64_t>(e) * I0.prog_len;
+  I.prog_len = elen[e];
   const bool cut = I.cut[e] != 0;
   const int D = I.depth;
   const int nleaf = 1 << (2 * D);

@@ -3264,15 +3264,22 @@ int ig_cut_quadrature3(const ig_cut3* in, double* K, double* F, double* vol, dou
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0));
+    // Every element's level-set program specialised to its cell (cutquad.cuh).
+    double* eprog = static_cast<double*>(up(nullptr, sizeof(double) * n * in->prog_len));
+    int* elen = static_cast<int*>(up(nullptr, sizeof(int) * n));
+    double* dh = static_cast<double*>(up(in->h, sizeof(double) * 3));
+    k_ls_specialize<<<static_cast<unsigned>((n + 127) / 128), 128>>>(D.prog, in->prog_len, static_cast<int>(n), 3, D.lo,
+                                                                      nullptr, dh, eprog, elen);
+    CK(cudaGetLastError());
     int64_t* dcount = static_cast<int64_t*>(up(nullptr, sizeof(int64_t) * (n + 1)));
-    k_cq_prims<false><<<static_cast<unsigned>(n), kCqThreads>>>(D, nullptr, dcount, nullptr);
+    k_cq_prims<false><<<static_cast<unsigned>(n), kCqThreads>>>(D, nullptr, dcount, nullptr, eprog, elen);
     CK(cudaGetLastError());
     std::vector<int64_t> cnt(static_cast<size_t>(n)), offs(static_cast<size_t>(n) + 1, 0);
     CK(cudaMemcpy(cnt.data(), dcount, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
     for (int64_t e = 0; e < n; ++e) offs[e + 1] = offs[e] + cnt[e];
     int64_t* doff = static_cast<int64_t*>(up(offs.data(), sizeof(int64_t) * (n + 1)));
     double* prim = static_cast<double*>(up(nullptr, sizeof(double) * kCqPrim * std::max<int64_t>(offs[n], 1)));
-    k_cq_prims<true><<<static_cast<unsigned>(n), kCqThreads>>>(D, doff, nullptr, prim);
+    k_cq_prims<true><<<static_cast<unsigned>(n), kCqThreads>>>(D, doff, nullptr, prim, eprog, elen);
     CK(cudaGetLastError());
     double* dK = static_cast<double*>(up(nullptr, sizeof(double) * n * nl * nl));
     double* dF = static_cast<double*>(up(nullptr, sizeof(double) * n * nl));
@@ -3341,15 +3348,20 @@ int ig_cut_quadrature2(const ig_cut2* in, double* K, double* F, double* vol, dou
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0));
+    double* eprog = static_cast<double*>(up(nullptr, sizeof(double) * n * in->prog_len));
+    int* elen = static_cast<int*>(up(nullptr, sizeof(int) * n));
+    k_ls_specialize<<<static_cast<unsigned>((n + 127) / 128), 128>>>(D.prog, in->prog_len, static_cast<int>(n), 2, D.lo,
+                                                                      D.hi, nullptr, eprog, elen);
+    CK(cudaGetLastError());
     int64_t* dn = static_cast<int64_t*>(up(nullptr, sizeof(int64_t) * 3 * n));
-    k_cq2_points<false><<<static_cast<unsigned>(n), kCq2Threads>>>(D, nullptr, dn, nullptr);
+    k_cq2_points<false><<<static_cast<unsigned>(n), kCq2Threads>>>(D, nullptr, dn, nullptr, eprog, elen);
     CK(cudaGetLastError());
     std::vector<int64_t> cnt(static_cast<size_t>(3 * n)), offs(static_cast<size_t>(n) + 1, 0);
     CK(cudaMemcpy(cnt.data(), dn, sizeof(int64_t) * 3 * n, cudaMemcpyDeviceToHost));
     for (int64_t e = 0; e < n; ++e) offs[e + 1] = offs[e] + cnt[3 * e] + cnt[3 * e + 1] + cnt[3 * e + 2];
     int64_t* doff = static_cast<int64_t*>(up(offs.data(), sizeof(int64_t) * (n + 1)));
     double* pts = static_cast<double*>(up(nullptr, sizeof(double) * 4 * std::max<int64_t>(offs[n], 1)));
-    k_cq2_points<true><<<static_cast<unsigned>(n), kCq2Threads>>>(D, doff, nullptr, pts);
+    k_cq2_points<true><<<static_cast<unsigned>(n), kCq2Threads>>>(D, doff, nullptr, pts, eprog, elen);
     CK(cudaGetLastError());
     double* dK = static_cast<double*>(up(nullptr, sizeof(double) * n * nl * nl));
     double* dF = static_cast<double*>(up(nullptr, sizeof(double) * n * nl));
@@ -3439,15 +3451,20 @@ int ig_assemble_thb(const ig_thb_asm* in, ig_csr* A_out, double* b_out, double* 
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0));
+    double* eprog = static_cast<double*>(up(nullptr, sizeof(double) * ne * in->prog_len));
+    int* elen = static_cast<int*>(up(nullptr, sizeof(int) * ne));
+    k_ls_specialize<<<static_cast<unsigned>((ne + 127) / 128), 128>>>(V.prog, in->prog_len, static_cast<int>(ne), 2, V.lo,
+                                                                       V.hi, nullptr, eprog, elen);
+    CK(cudaGetLastError());
     int64_t* dn = static_cast<int64_t*>(up(nullptr, sizeof(int64_t) * 3 * ne));
-    k_cq2_points<false><<<static_cast<unsigned>(ne), kCq2Threads>>>(V, nullptr, dn, nullptr);
+    k_cq2_points<false><<<static_cast<unsigned>(ne), kCq2Threads>>>(V, nullptr, dn, nullptr, eprog, elen);
     CK(cudaGetLastError());
     std::vector<int64_t> cnt(static_cast<size_t>(3 * ne)), offs(static_cast<size_t>(ne) + 1, 0);
     CK(cudaMemcpy(cnt.data(), dn, sizeof(int64_t) * 3 * ne, cudaMemcpyDeviceToHost));
     for (int64_t e = 0; e < ne; ++e) offs[e + 1] = offs[e] + cnt[3 * e] + cnt[3 * e + 1] + cnt[3 * e + 2];
     auto* doff = static_cast<int64_t*>(up(offs.data(), sizeof(int64_t) * (ne + 1)));
     auto* pts = static_cast<double*>(up(nullptr, sizeof(double) * 4 * std::max<int64_t>(offs[ne], 1)));
-    k_cq2_points<true><<<static_cast<unsigned>(ne), kCq2Threads>>>(V, doff, nullptr, pts);
+    k_cq2_points<true><<<static_cast<unsigned>(ne), kCq2Threads>>>(V, doff, nullptr, pts, eprog, elen);
     CK(cudaGetLastError());
     auto* dK = static_cast<double*>(up(nullptr, sizeof(double) * std::max<int64_t>(koff[ne], 1)));
     auto* dF = static_cast<double*>(up(nullptr, sizeof(double) * std::max<int64_t>(nrows, 1)));

@@ -172,15 +172,25 @@ __device__ __forceinline__ void fast2_dispatch(const double* __restrict__ x, int
 
 // The rows this lane will own in a slice (psell_slice's mapping), from the
 // static metadata: lets a kernel issue its per-row loads (residual source,
-// the x being corrected) ahead of the slice's product chain.
+// the x being corrected) ahead of the slice's product chain.  GENERAL slices:
+// gen = {row, ginfo} of the lane's (clamped) entry, loaded here together --
+// both depend on the slice metadata only, so psell_slice's chain is meta ->
+// {row, info} -> offsets -> x instead of meta -> row -> info -> offsets -> x
+// (profiles: the prolongation's ginfo wait was 8 % of its stall samples).
 template <bool F4 = true>
-__device__ __forceinline__ void psell_rows(const PSell& A, const uint4 mu, int* rows) {
+__device__ __forceinline__ void psell_rows(const PSell& A, const uint4 mu, int* rows, uint2& gen) {
   const int lane = threadIdx.x & 31;
   const uint32_t pk = mu.w;
   const int count = static_cast<int>((pk >> 11) & 0x3f);
   int& row = rows[0];
   int& row2 = rows[1];
   row = row2 = rows[2] = rows[3] = -1;
+  gen = make_uint2(0u, 0u);
+  if (count > 0 && !(pk & (1u << 17))) {
+    const int idx = static_cast<int>(mu.x) + min(lane, count - 1);
+    gen.x = static_cast<uint32_t>(__ldg(A.rlist + idx));
+    gen.y = __ldg(A.ginfo + idx);
+  }
   if (count == 0 || lane >= count) return;
   const int wv = static_cast<int>((pk >> 19) & 0x3f);
   if (F4 && (pk & (1u << 17)) && wv == 2) {  // FAST4: B rows at + D
@@ -195,7 +205,7 @@ __device__ __forceinline__ void psell_rows(const PSell& A, const uint4 mu, int* 
   } else if (pk & (1u << 17)) {
     row = static_cast<int>(mu.x) + lane;
   } else {
-    row = __ldg(A.rlist + mu.x + lane);
+    row = static_cast<int>(gen.x);
   }
 }
 
@@ -273,9 +283,11 @@ __device__ __forceinline__ void fast4_slice(const double* __restrict__ x, const 
 
 // One warp, one slice.  Returns the row this lane owns (-1: none) and its
 // sum; FAST2 slices give each lane a second row (row2 / acc2, else -1).
+// gen: psell_rows' {row, ginfo} (GENERAL slices).
 template <bool STREAM, bool F4 = true>
-__device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const double* __restrict__ x, double& acc,
-                                           int& row2, double& acc2, const PValTab* tab, int* rowx, double* accx) {
+__device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const uint2 gen, const double* __restrict__ x,
+                                           double& acc, int& row2, double& acc2, const PValTab* tab, int* rowx,
+                                           double* accx) {
   acc = 0.0;
   acc2 = 0.0;
   row2 = -1;
@@ -385,9 +397,8 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
     for (; k < L; ++k) acc = acc + __ldg(vp + k) * __ldg(xr + __ldg(op + k));
     return lane < count ? row : -1;
   }
-  const int idx = static_cast<int>(mu.x) + cl;
-  const int row = __ldg(A.rlist + idx);
-  const uint32_t info = __ldg(A.ginfo + idx);
+  const int row = static_cast<int>(gen.x);
+  const uint32_t info = gen.y;
   const int len = static_cast<int>(info & kPMaxLen);
   const int vsel = static_cast<int>((info >> 11) & 0x3f);
   const int vi = static_cast<int>((info >> 17) & 0x1f);
@@ -452,7 +463,8 @@ __global__ void __launch_bounds__(kCta, IG_PSPMV_MINB) k_pspmv(PSell A, const do
   const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(A.meta + slice));  // static: before the wait
   int pr[4];
-  psell_rows<F4>(A, mu, pr);
+  uint2 gen;
+  psell_rows<F4>(A, mu, pr, gen);
   pdl_entry();
   if (pcg_done(st)) return;
   // The residual source is loaded before the product chain, not after it.
@@ -461,7 +473,7 @@ __global__ void __launch_bounds__(kCta, IG_PSPMV_MINB) k_pspmv(PSell A, const do
   for (int k = 0; k < (F4 ? 4 : 2); ++k) rs[k] = (MODE == 1 && pr[k] >= 0) ? rsrc[pr[k]] : 0.0;
   double acc, acc2, accx[2];
   int row2, rowx[2];
-  const int row = psell_slice<STREAM, F4>(A, mu, x, acc, row2, acc2, &tab, rowx, accx);
+  const int row = psell_slice<STREAM, F4>(A, mu, gen, x, acc, row2, acc2, &tab, rowx, accx);
   if (row < 0) return;
   y[row] = (MODE == 0) ? acc : rs[0] - acc;
   if (row2 >= 0) y[row2] = (MODE == 0) ? acc2 : rs[1] - acc2;
@@ -499,7 +511,8 @@ __global__ void __launch_bounds__(kCta, IG_PPROLONG_MINB) k_pprolong(PSell P, co
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(P.meta + slice));  // static: before the wait
   // (Two-line slices exist only in square matrices: never in P.)
   int pr[4];
-  psell_rows<false>(P, mu, pr);
+  uint2 gen;
+  psell_rows<false>(P, mu, pr, gen);
   pdl_entry();
   if (pcg_done(st)) return;
   // The x being corrected is loaded before the product chain, not after it.
@@ -507,7 +520,7 @@ __global__ void __launch_bounds__(kCta, IG_PPROLONG_MINB) k_pprolong(PSell P, co
   const double x2 = pr[1] >= 0 ? x[pr[1]] : 0.0;
   double c, c2, cx[2];
   int row2, rowx[2];
-  const int row = psell_slice<STREAM, false>(P, mu, xc, c, row2, c2, &tab, rowx, cx);
+  const int row = psell_slice<STREAM, false>(P, mu, gen, xc, c, row2, c2, &tab, rowx, cx);
   if (row < 0) return;
   cor[row] = c;
   x[row] = x1 + c;

@@ -489,7 +489,7 @@ ElemData element3(const Space& s, int cx, int cy, int cz, const double* lo, cons
 }
 }  // namespace
 
-Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& qc, int threads) {
+Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& qc, int threads, bool numeric) {
   const Grid& g = s.grid;
   const int dim = g.dim, p = s.p, nl = s.nloc();
   const double beta = prob.beta > 0.0 ? prob.beta : default_penalty(g);
@@ -572,7 +572,7 @@ Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& 
   // Special elements.
   double eta = 1.0;
 #pragma omp parallel for schedule(dynamic, 4) num_threads(threads) reduction(min : eta)
-  for (int64_t k = 0; k < static_cast<int64_t>(special_list.size()); ++k) {
+  for (int64_t k = 0; k < (numeric ? static_cast<int64_t>(special_list.size()) : 0); ++k) {
     const int e = special_list[k];
     const bool cut = s.el_tag[e] == kCut;
     if (dim == 2) {
@@ -629,6 +629,13 @@ Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& 
         out.el_table[e] = (cz * ncy + cy) * ncx + cx;
       }
     }
+  }
+
+  if (!numeric) {  // geometric half: no row gather, no symmetrisation
+    out.A.nr = out.A.nc = s.n();
+    out.A.ptr.assign(static_cast<size_t>(s.n()) + 1, 0);
+    out.b.assign(static_cast<size_t>(s.n()), 0.0);
+    return out;
   }
 
   auto elem = [&](int e) -> const ElemData& {

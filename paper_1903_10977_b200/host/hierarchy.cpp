@@ -504,6 +504,7 @@ struct igh_case {
   ig_coarse co{};
   igh_info info{};
   std::vector<std::vector<int32_t>> xyz;  // per level anchors (ax,ay,az)
+  bool geometric = false;  // igh_build_geometry: no operators, factors or rhs
   void wire();
 };
 
@@ -553,7 +554,7 @@ void igh_case::wire() {
     bb.n_colors = B[l].n_colors;
     bb.color_of = B[l].color.empty() ? nullptr : B[l].color.data();
   }
-  co.n = A.empty() ? 0 : A[0].nr;
+  co.n = (A.empty() || geometric) ? 0 : A[0].nr;
   co.rank = rank;
   co.L = coarseL.data();
   co.piv = piv.data();
@@ -594,7 +595,14 @@ void igh_config_default(igh_config* c) {
   c->threads = 0;
 }
 
-int igh_build(const igh_config* cfg, igh_case** out) {
+}  // extern "C"
+
+namespace {
+// igh_build (numeric) and igh_build_geometry (numeric = false: spaces,
+// restrictions, pre-filter block layouts, colours, damping and the element
+// tables of the Inside classes; no cut-element integration, no assembly, no
+// Galerkin products, no factorisations -- the device pipeline computes those).
+int build_impl(const igh_config* cfg, igh_case** out, bool numeric) {
   if (!cfg || !out) return fail("igh_build: null argument");
   *out = nullptr;
   try {
@@ -639,7 +647,18 @@ int igh_build(const igh_config* cfg, igh_case** out) {
     std::vector<std::unique_ptr<Space>> down;
     std::vector<std::unique_ptr<GSpace>> gdown;
     double t_gal = 0.0, t_fac = 0.0;
+    auto empty_op = [](int32_t n) {  // geometric half: an n x n operator without entries
+      Csr m;
+      m.nr = m.nc = n;
+      m.ptr.assign(static_cast<size_t>(n) + 1, 0);
+      return m;
+    };
     auto galerkin = [&](Csr r) {  // A_c = R (A R^T) (multigrid.cpp:39-41)
+      if (!numeric) {
+        Adown.push_back(empty_op(r.nr));
+        Rdown.push_back(std::move(r));
+        return;
+      }
       const double tg = now();
       struct Acc { double& t; double t0; ~Acc() { t += now() - t0; } } acc_{t_gal, tg};
       const Csr rt = transpose(r);
@@ -653,7 +672,12 @@ int igh_build(const igh_config* cfg, igh_case** out) {
       for (int k = 0; k < cfg->refine_passes; ++k)
         mesh.refine_near_circle(cfg->refine_circle[0], cfg->refine_circle[1], cfg->refine_circle[2], cfg->refine_dist);
       gdown.push_back(build_thb(mesh, ls, cfg->degree, cfg->classify_depth, threads));
-      as = assemble_g(*gdown[0], prob, qc, threads);
+      if (numeric) {
+        as = assemble_g(*gdown[0], prob, qc, threads);
+      } else {
+        as.A = empty_op(gdown[0]->n());
+        as.b.assign(static_cast<size_t>(gdown[0]->n()), 0.0);
+      }
       t1 = now();
       Adown.push_back(std::move(as.A));
       for (int l = 1; l < L; ++l) {
@@ -665,7 +689,7 @@ int igh_build(const igh_config* cfg, igh_case** out) {
       }
     } else {
       down.push_back(build_space(g, ls, fam, cfg->degree, cfg->classify_depth, threads));
-      as = assemble(*down[0], prob, qc, threads);
+      as = assemble(*down[0], prob, qc, threads, numeric);
       c->tabK = std::move(as.tabK);
       c->tabF = std::move(as.tabF);
       c->el_table = std::move(as.el_table);
@@ -730,7 +754,7 @@ int igh_build(const igh_config* cfg, igh_case** out) {
       c->pre_ptr[l] = b.ptr;
       c->pre_dofs[l] = b.dofs;
       const double tf = now();
-      factorize_blocks(c->A[l], b, cfg->filter_ratio, threads);
+      if (numeric) factorize_blocks(c->A[l], b, cfg->filter_ratio, threads);
       t_fac += now() - tf;
       double gm = cfg->gamma;
       if (gm <= 0.0) {
@@ -742,7 +766,7 @@ int igh_build(const igh_config* cfg, igh_case** out) {
     }
     // Coarsest pivoted Cholesky (multigrid.cpp:57-73).
     const Csr& a1 = c->A[0];
-    const int n0 = a1.nr;
+    const int n0 = numeric ? a1.nr : 0;
     c->coarseL.assign(static_cast<size_t>(n0) * n0, 0.0);
     for (int i = 0; i < n0; ++i)
       for (int32_t k = a1.ptr[i]; k < a1.ptr[i + 1]; ++k)
@@ -753,7 +777,7 @@ int igh_build(const igh_config* cfg, igh_case** out) {
     c->rank = pstrf_lower(n0, c->coarseL.data(), c->piv.data(), 1e-14 * max_diag);
     const double t2 = now();
     c->b = std::move(as.b);
-    if (!thb && !as.el_vol.empty()) {
+    if (numeric && !thb && !as.el_vol.empty()) {
       const Space& s = *c->spaces.back();
       const int dim = s.grid.dim;
       c->supp_frac.assign(static_cast<size_t>(s.n()), 0.0);
@@ -787,6 +811,7 @@ int igh_build(const igh_config* cfg, igh_case** out) {
       c->xyz[l].resize(static_cast<size_t>(s.n()) * 3);
       for (int a = 0; a < s.n(); ++a) anchor_xyz(s, a, &c->xyz[l][static_cast<size_t>(a) * 3]);
     }
+    c->geometric = !numeric;
     c->wire();
     c->info.cut_elements = as.cut_elements;
     c->info.eta = as.eta;
@@ -801,6 +826,12 @@ int igh_build(const igh_config* cfg, igh_case** out) {
     return fail(e.what());
   }
 }
+}  // namespace
+
+extern "C" {
+
+int igh_build(const igh_config* cfg, igh_case** out) { return build_impl(cfg, out, true); }
+int igh_build_geometry(const igh_config* cfg, igh_case** out) { return build_impl(cfg, out, false); }
 
 int igh_cut3_payload(igh_case* c, ig_cut3* out) {
   if (!c || !out) return fail("igh_cut3_payload: null argument");
@@ -1203,6 +1234,8 @@ const char kMagic[8] = {'I', 'G', 'H', '1', 0, 0, 0, 2};  // last byte: version
 extern "C" {
 
 int igh_write(const igh_case* c, const char* path) {
+  if (!c || !path) return fail("igh_write: null argument");
+  if (c->geometric) return fail("igh_write: a geometry-only case (igh_build_geometry) has no hierarchy to write");
   try {
     std::ofstream f(path, std::ios::binary);
     if (!f) return fail(std::string("igh_write: cannot open ") + path);

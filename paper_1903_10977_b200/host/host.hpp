@@ -224,8 +224,12 @@ struct Assembled {
   std::vector<double> el_vol;
 };
 
+// numeric = false: the geometric half only (igh_build_geometry) -- element
+// classes, Inside-class tables and the element -> table map; the individually
+// integrated elements' tables stay zero (the device fills them), A is an
+// empty n x n pattern and b zeros (no row gather, no symmetrisation).
 Assembled assemble(const Space& s, const ProblemConfig& prob, const QuadConfig& q,
-                   int threads);
+                   int threads, bool numeric = true);
 
 // ------------------------------------------------------- 2D quadrature ----
 struct QuadRule2 {
