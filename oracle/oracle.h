@@ -19,12 +19,17 @@
  *   LLT::solve       Eigen (forward column-oriented with L, backward row-dot with L^T)
  *   SpMV             Eigen RowMajor sparse*dense: per-row ascending sum
  *
- * Parity pinning: the reference cannot be built here (Eigen/LAPACKE absent,
- * SURVEY.md §8c) and records no exact iteration counts or residual digits.
- * The restatement is pinned by the reference's own known-answer tests
- * (tests/test_oracle_pins.py: proj/tests/test_solvers.cpp, test_multigrid.cpp,
- * test_smoothers.cpp identities).  Exact digits are therefore "parity
- * unpinned" against the reference binary; see DESIGN.md §Oracle.
+ * Parity pinning: the reference cannot be built as shipped (Eigen/LAPACKE
+ * absent), but its own hot-path sources (solvers.cpp,
+ * multigrid.cpp, smoothers.cpp) compile unmodified against the Eigen / LAPACKE
+ * stand-in of oracle/ref_shim into oracle/_ref/libimmergrid_ref.so (`make ref`,
+ * ref_glue.cpp).  tests/test_reference_pin.py holds this restatement to that
+ * library BIT FOR BIT in ORC_SEQ mode (pcg, richardson, vcycle_at, both
+ * sweeps, coarse_solve, on C1-C5 at full size through the committed records
+ * of tests/golden/reference_solves.json), and tests/test_oracle.py to the
+ * reference's known-answer tests.  Not observable in any build here: Eigen's
+ * internal kernel orders (SIMD dot, blocked triangular solves, blocked
+ * dpstrf); tests/test_noise_floor.py bounds their effect.
  *
  * Reductions (dot, norm): ORC_SEQ sums in ascending index order (the natural
  * reading of Eigen's redux); ORC_GPU_ORDER sums in the documented chunked tree
