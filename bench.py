@@ -183,6 +183,11 @@ def main():
     ap.add_argument("--threads", type=int, default=0, help="host setup threads (0 = all)")
     ap.add_argument("--smoother", default="as", choices=["as", "ms"],
                     help="as: additive Schwarz (the BASELINE configs); ms: multiplicative colored Schwarz")
+    ap.add_argument("--ref-kind", default="port", choices=["port", "reference"],
+                    help="--impl reference: 'port' = the threaded oracle restatement (default: the faster, "
+                         "harder CPU arm; complete solves in seconds); 'reference' = the reference's own "
+                         "single-threaded solvers.cpp/multigrid.cpp/smoothers.cpp from oracle/_ref "
+                         "(C4: ~3 min per complete solve, use --steps 1 --warmup 0)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-device-setup", action="store_true", help="skip the ig_hier_build setup measurement")
     ap.add_argument("--no-fast-mode", action="store_true", help="skip the tolerance-mode (fast coarse) measurement")
@@ -442,12 +447,31 @@ def run_reference(args, world, rank):
     if rank != 0:
         return
     case, desc, t_setup = build_workload(args.workload, args.threads, args.smoother)
+    kind, what = "port", ("oracle/liboracle.so, the C restatement of the reference's solve "
+                          "(sequential-order dots)")
+    solve = oracle_solve
+    if args.ref_kind == "reference":
+        # The reference's own sources (oracle/_ref, built where /root/reference
+        # exists), single-threaded like the reference.
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import reference_ffi as ref
+        if not ref.available():
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libimmergrid_ref.so not built"}))
+            return
+        rh = ref.RefHierarchy(case.levels_c())
+        kind, what = "reference", ("oracle/_ref/libimmergrid_ref.so: the reference's own solvers.cpp / multigrid.cpp "
+                                   "/ smoothers.cpp compiled against the Eigen stand-in (single-threaded)")
+
+        def solve(case, maxit=1000):
+            t0 = time.perf_counter()
+            st, _, _, it = rh.pcg(case.b, tol=1e-8, maxit=maxit)
+            return (0 if maxit < 1000 else st), it, time.perf_counter() - t0, 1
     for _ in range(args.warmup):
-        oracle_solve(case, maxit=3)
+        solve(case, maxit=3)
     secs, its = [], []
     for _ in range(args.steps):
-        st, it, sec, th = oracle_solve(case)
-        assert st == 0, f"oracle solve did not converge (status {st})"
+        st, it, sec, th = solve(case)
+        assert st == 0, f"CPU solve did not converge (status {st})"
         secs.append(sec)
         its.append(it)
     t = sum(secs) / len(secs)
@@ -459,10 +483,9 @@ def run_reference(args, world, rank):
             "config": common_config(desc, case, world),
             "iterations": its[0], "complete_solves_timed": len(secs),
             "solve_seconds": {"min": min(secs), "median": statistics.median(secs), "max": max(secs)},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": th, "kind": "port",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": th, "kind": kind,
                              "sample": (f"{len(secs)} complete solves ({its[0]} PCG iterations each) of "
-                                        f"oracle/liboracle.so, the C restatement of the reference's solve "
-                                        f"(sequential-order dots), on {th} host threads; warm-up steps = "
+                                        f"{what}, on {th} host threads; warm-up steps = "
                                         f"the first 3 iterations")},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "setup_seconds": {"host_setup": t_setup}}
