@@ -290,6 +290,9 @@ int ig_pcg_result(ig_hier *h, double *residuals, int32_t *iterations);
 int ig_richardson(ig_hier *h, const double *b, double tol, int32_t maxit, double *x,
                   double *residuals, int32_t *iterations, double *seconds);
 
+/* Host-only (no device work): slice statistics of the pattern-SELL layout the
+ * library would build for `a` (out: >= 32 entries; see csrc/ig_gpu.cu). */
+int ig_debug_psell_stats(const ig_csr *a, int64_t *out, int32_t n_out);
 /* Debug: run one V-cycle with direct launches and an event after every step
  * (smoother, residual, restriction, prolongation, coarse solve); writes the
  * elapsed ms per step, its level and a label (label_len bytes each). */
@@ -399,6 +402,7 @@ const char *ig_last_error(void);
 #define IG_OPT_PSELL_CTAS 15  /* pattern-SELL SpMV occupancy cap, CTAs per SM (0 = registers decide) */
 #define IG_OPT_L2_ROWS 18       /* levels below the finest with <= this many DOFs in an L2-persisting arena (default 300000; 0 = off) */
 #define IG_OPT_PSELL_LINES2 27    /* 1 (default): pattern-SELL slices covering two x-lines (shared column runs) */
+#define IG_OPT_PSELL_MULTI 34     /* 1 (default): pattern-SELL slices packing row pairs of up to four short runs (FAST2M) */
 #define IG_OPT_PSELL_CTAB 23     /* 1 (default): FAST2 value sequences of the pattern SELL from a constant-bank table */
 #define IG_OPT_GAL_SHORT 21      /* 1 (default): device Galerkin uses the prefetching SpGEMM when B rows have <= 32 entries */
 #define IG_OPT_L2_MB 19          /* size of that arena in MiB (default 64) */

@@ -117,6 +117,7 @@ IG_OPT_PSELL_PAIRS_ROWS = 32
 IG_OPT_GAL_SHORT = 21
 IG_OPT_PSELL_CTAB = 23
 IG_OPT_PSELL_LINES2 = 27
+IG_OPT_PSELL_MULTI = 34
 
 _host = None
 _gpu = None

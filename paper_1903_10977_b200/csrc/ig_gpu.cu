@@ -77,6 +77,7 @@ struct Opts {
   int psell_ctas = 0;
   int psell_ctab = 1;    // FAST2 value sequences from a constant-bank table
   int psell_lines2 = 1;  // FAST4 slices (two x-lines per slice)
+  int psell_multi = 1;   // FAST2M slices (row pairs of up to four short runs per slice)
   int gal_short = 1;     // prefetching SpGEMM for B rows <= 32 entries
   // Levels below the finest with at most this many DOFs live in the
   // L2-persisting arena (ig_hier::alloc); 0 = off.  Arena size l2_bytes.
@@ -294,6 +295,7 @@ struct HostPSell {
   int64_t n_fast = 0, n_general = 0, fast_rows = 0;
   std::vector<int4> useg;    // FAST4 union segment lists (header {D, n}, then {o, m, vA, vB})
   int64_t n_fast4 = 0;
+  int64_t n_fast2m = 0;      // FAST2M slices (their tables live in useg too)
   std::vector<double> tab;   // constant-bank value table (spmv_psell.cuh PValTab)
   int64_t tab_rows = 0;      // rows whose FAST2 values come from the table
 };
@@ -595,12 +597,104 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
   // Pair / two-line slices (64 / 128 rows per warp) trade parallelism for x
   // reuse: only matrices with at least psell_pairs_rows rows use them.
   const bool f2ok = opt().psell_pairs && nr >= opt().psell_pairs_rows && s.smul == 1 && s.sshift == 0;
+  // FAST2M: pieces that would leave most of a FAST2 slice's lanes idle (the
+  // x-line pieces either side of an immersed boundary: 16-60 rows, each with
+  // its own column offsets) are pooled per (value sequence, column-run
+  // lengths) and packed, up to four pieces and 32 row pairs per slice.  Table
+  // in useg: {first rows of the four pieces}, {lane starts s1 | s2 << 8 |
+  // s3 << 16, odd-tail mask, segment list (run lengths), runs}, then one int4
+  // of piece offsets per column run.  An odd tail is the last lane of a piece
+  // owning one row only.
+  const bool fmok = f2ok && opt().psell_multi && nr == nc;
+  struct Loose { int32_t a, b, rep; };
+  struct Pool { uint32_t vb, sg; int32_t len, nseg; std::vector<Loose> q; int lanes = 0; };
+  std::map<std::pair<uint32_t, uint64_t>, Pool> pools;  // (value sequence, hash of the run lengths)
+  auto flush_pool = [&](Pool& pl) {
+    if (pl.q.empty()) return;
+    int4 R = make_int4(0, 0, 0, 0), hd = make_int4(0, 0, static_cast<int>(pl.sg), pl.nseg);
+    int st[4] = {0, 64, 64, 64}, lanes = 0;
+    int32_t* Rp = &R.x;
+    std::vector<int4> offs(static_cast<size_t>(pl.nseg), make_int4(0, 0, 0, 0));
+    for (size_t k = 0; k < pl.q.size(); ++k) {
+      const Loose& L = pl.q[k];
+      Rp[k] = L.a;
+      st[k] = lanes;
+      lanes += (L.b - L.a + 1) / 2;
+      if ((L.b - L.a) & 1) hd.y |= 1 << k;
+      int u = 0;  // first column of every run of the representative row
+      for (int32_t q = ptr[L.rep]; q < ptr[L.rep + 1]; ++u) {
+        (&offs[static_cast<size_t>(u)].x)[k] = col[q] - L.rep;
+        int32_t m = 1;
+        while (q + m < ptr[L.rep + 1] && m < 8 && col[q + m] == col[q] + m) ++m;
+        q += m;
+      }
+      s.fast_rows += L.b - L.a;
+    }
+    for (size_t k = pl.q.size(); k < 4; ++k) {  // unused pieces repeat the first (never selected)
+      Rp[k] = Rp[0];
+      for (auto& o : offs) (&o.x)[k] = o.x;
+    }
+    hd.x = st[1] | st[2] << 8 | st[3] << 16;
+    const uint32_t z = static_cast<uint32_t>(s.useg.size());
+    s.useg.push_back(R);
+    s.useg.push_back(hd);
+    s.useg.insert(s.useg.end(), offs.begin(), offs.end());
+    s.meta.push_back(PSliceMeta{static_cast<uint32_t>(R.x), pl.vb, z, pack(pl.len, lanes, true, true, 3, 0)});
+    s.layout_bytes += 16 + 16 * static_cast<int64_t>(offs.size() + 2);
+    ++s.n_fast;
+    ++s.n_fast2m;
+    pl.q.clear();
+    pl.lanes = 0;
+  };
+  auto pool_piece = [&](int32_t a, int32_t b, int32_t rep, uint32_t vb) {
+    uint64_t hs = 0x1234567;
+    int32_t nseg = 0;
+    for (int32_t q = ptr[rep]; q < ptr[rep + 1]; ++nseg) {
+      int32_t m = 1;
+      while (q + m < ptr[rep + 1] && m < 8 && col[q + m] == col[q] + m) ++m;
+      hs = mix64(hs, static_cast<uint64_t>(m));
+      q += m;
+    }
+    Pool& pl = pools[{vb, hs}];
+    if (pl.q.empty() && pl.lanes == 0 && pl.nseg == 0) {
+      pl.vb = vb;
+      pl.sg = seg_start(rep);
+      pl.len = len(rep);
+      pl.nseg = nseg;
+    }
+    while (a < b) {
+      const int room = 32 - pl.lanes;
+      const int32_t take = std::min(b - a, 2 * room);  // a split leaves an even count behind
+      pl.q.push_back(Loose{a, a + take, rep});
+      pl.lanes += (take + 1) / 2;
+      a += take;
+      if (pl.lanes == 32 || pl.q.size() == 4) flush_pool(pl);
+    }
+  };
   auto emit_piece = [&](int32_t a, int32_t b, int32_t rep) {
     if (b <= a) return;
     lmax_all = std::max(lmax_all, len(rep));
     const uint32_t vb = v_start(rep);
     int32_t i = a;
-    if (f2ok && b - a >= 2) {
+    if (fmok) {
+      // Whole 64-row slices stay FAST2; the remainder (< 56 rows, or odd) is pooled.
+      for (; b - i >= 64; i += 64) {
+        const uint32_t sg = seg_start(rep);
+        s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, sg, pack(len(rep), 32, true, true, 1, 0)});
+        s.layout_bytes += 16;
+        ++s.n_fast;
+        s.fast_rows += 64;
+      }
+      const int32_t rem = b - i;
+      // (the phantom second row of an odd tail reads x one past the piece's
+      // last column run: keep it inside x)
+      const bool tail_ok = !(rem & 1) || col[ptr[b - 1 + 1] - 1] + 1 < nc;
+      if (rem > 0 && len(rep) > 0 && tail_ok && !(rem >= 56 && !(rem & 1))) {
+        pool_piece(i, b, rep, vb);
+        return;
+      }
+    }
+    if (f2ok && b - i >= 2) {
       const uint32_t sg = seg_start(rep);
       for (; b - i >= 2;) {
         const int cnt = std::min(64, (b - i) & ~1);
@@ -759,6 +853,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
     }
     if (s.V.size() > 0xF0000000ull || s.O.size() > 0xF0000000ull) return false;
   }
+  for (auto& kv : pools) flush_pool(kv.second);
   if (!pending.empty()) emit_general(pending);
   if (s.V.size() > 0xF0000000ull || s.O.size() > 0xF0000000ull) return false;
   // Constant-bank value table: the FAST / FAST2 value sequences covering the
@@ -773,7 +868,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       if (m.pk & (1u << 17)) {
         const int wv = static_cast<int>((m.pk >> 19) & 0x3f);  // 0 FAST, 1 FAST2, 2 FAST4
         auto& u = use[m.vbase];
-        u.first += (wv == 2 ? 4 : wv == 1 ? 2 : 1) * static_cast<int64_t>((m.pk >> 11) & 0x3f);
+        u.first += (wv == 2 ? 4 : wv == 1 || wv == 3 ? 2 : 1) * static_cast<int64_t>((m.pk >> 11) & 0x3f);
         u.second = static_cast<int32_t>(m.pk & kPMaxLen);
       }
     std::vector<std::pair<int64_t, uint32_t>> order;
@@ -996,7 +1091,7 @@ struct ig_hier {
         d.p.V = upload(hp.V.data(), hp.V.size());
         d.p.O = upload(hp.O.data(), hp.O.size());
         d.p.dict_w = hp.dict_w;
-        d.has_f4 = hp.n_fast4 > 0;
+        d.has_f4 = hp.n_fast4 > 0 || hp.n_fast2m > 0;
         d.ptab = std::make_shared<PValTab>();
         std::memset(d.ptab.get(), 0, sizeof(PValTab));
         std::copy(hp.tab.begin(), hp.tab.end(), d.ptab->v);
@@ -1048,18 +1143,18 @@ struct ig_hier {
     const unsigned g = grid_of(A.s.n_rows);
     if (g == 0) return;
     if (A.has_p) {
-      const unsigned gp = static_cast<unsigned>(A.p.n_slices / (kCta / 32));
+      const unsigned gp = static_cast<unsigned>(A.p.n_slices / (kPCta / 32));
       const size_t sm = psell_smem();
       const PValTab& tb = *A.ptab;
       if (!A.has_f4 && !A.stream) {  // no two-line slices: the leaner instantiation
-        if (mode == 0) launch(k_pspmv<0, false, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
-        else launch(k_pspmv<1, false, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
+        if (mode == 0) launch(k_pspmv<0, false, false>, gp, kPCta, sm, stream, A.p, x, y, rsrc, s, tb);
+        else launch(k_pspmv<1, false, false>, gp, kPCta, sm, stream, A.p, x, y, rsrc, s, tb);
       } else if (mode == 0) {
-        if (A.stream) launch(k_pspmv<0, true>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
-        else launch(k_pspmv<0, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
+        if (A.stream) launch(k_pspmv<0, true>, gp, kPCta, sm, stream, A.p, x, y, rsrc, s, tb);
+        else launch(k_pspmv<0, false>, gp, kPCta, sm, stream, A.p, x, y, rsrc, s, tb);
       } else {
-        if (A.stream) launch(k_pspmv<1, true>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
-        else launch(k_pspmv<1, false>, gp, kCta, sm, stream, A.p, x, y, rsrc, s, tb);
+        if (A.stream) launch(k_pspmv<1, true>, gp, kPCta, sm, stream, A.p, x, y, rsrc, s, tb);
+        else launch(k_pspmv<1, false>, gp, kPCta, sm, stream, A.p, x, y, rsrc, s, tb);
       }
       CK(cudaGetLastError());
       if (red) {  // p . Ap over the canonical chunks, alpha / Breakdown
@@ -1855,6 +1950,10 @@ int ig_set_option(int32_t option, int64_t value) {
     g_defaults.psell_ctab = value != 0;
     return IG_OK;
   }
+  if (option == IG_OPT_PSELL_MULTI) {
+    g_defaults.psell_multi = value != 0;
+    return IG_OK;
+  }
   if (option == IG_OPT_GAL_SHORT) {
     g_defaults.gal_short = value != 0;
     return IG_OK;
@@ -2312,6 +2411,34 @@ int ig_level_spmv_device(ig_hier* h, int32_t level, const double* d_x, double* d
       throw Error(IG_UNSUPPORTED, "level_spmv_device: coarsest A is not resident (dense factor only)");
     const DevSell& M = mode <= 1 ? L.A : (mode == 2 ? L.R : L.P);
     h->spmv(M, mode == 1 ? 1 : 0, d_x, d_y, d_y);
+    return IG_OK;
+  });
+}
+
+// Host-only: builds the pattern-SELL layout of a CSR operator (no device
+// work) and reports its slice statistics (profiles/psell_stats.py), classes
+// c = GENERAL, FAST, FAST2, FAST4, FAST2M: out[c] slices, out[5 + c] lanes
+// used, out[10 + 4 c + b] slices by lanes used (1-8, 9-16, 17-24, 25-32),
+// out[30] layout bytes, out[31] rows reading values from the constant-bank table.
+int ig_debug_psell_stats(const ig_csr* a, int64_t* out, int32_t n_out) {
+  if (!a || !out || n_out < 32) return fail(IG_INVALID_ARGUMENT, "debug_psell_stats: bad argument");
+  return guarded([&] {
+    OptScope os_(&g_defaults);
+    HostPSell hp;
+    for (int i = 0; i < n_out; ++i) out[i] = 0;
+    if (!to_psell(a->n_rows, a->n_cols, a->row_ptr, a->col_idx, a->val, hp)) return IG_UNSUPPORTED;
+    for (const PSliceMeta& m : hp.meta) {
+      const int count = static_cast<int>((m.pk >> 11) & 0x3f);
+      if (count == 0) continue;
+      const bool fast = m.pk & (1u << 17);
+      const int wv = static_cast<int>((m.pk >> 19) & 0x3f);
+      const int cls = !fast ? 0 : wv == 0 ? 1 : wv == 1 ? 2 : wv == 2 ? 3 : 4;
+      ++out[cls];
+      out[5 + cls] += count;
+      ++out[10 + 4 * cls + (count - 1) / 8];
+    }
+    out[30] = hp.layout_bytes;
+    out[31] = hp.tab_rows;
     return IG_OK;
   });
 }

@@ -170,6 +170,84 @@ __device__ __forceinline__ void fast2_dispatch(const double* __restrict__ x, int
   }
 }
 
+// FAST2M (row pairs of up to four pieces per slice; table layout in
+// ig_gpu.cu: to_psell).  The lane's first row; pid = its piece; odd = its
+// second row does not exist (odd tail of the piece).
+__device__ __forceinline__ int fast2m_lane(const int4* __restrict__ tb, int cl, int count, int& odd, int* pid_out = nullptr) {
+  const int4 hd = __ldg(tb + 1);
+  const int s1 = hd.x & 0xff, s2 = (hd.x >> 8) & 0xff, s3 = (hd.x >> 16) & 0xff;
+  const int pid = (cl >= s1 ? 1 : 0) + (cl >= s2 ? 1 : 0) + (cl >= s3 ? 1 : 0);
+  const int st = pid == 0 ? 0 : pid == 1 ? s1 : pid == 2 ? s2 : s3;
+  const int en = min(count, pid == 0 ? s1 : pid == 1 ? s2 : pid == 2 ? s3 : 64);
+  const int r0 = __ldg(reinterpret_cast<const int*>(tb) + pid);
+  odd = ((hd.y >> pid) & 1) && cl == en - 1;
+  if (pid_out) *pid_out = pid;
+  return r0 + 2 * (cl - st);
+}
+// One column run (M consecutive columns from a = lane's first row + the
+// piece's offset) for the lane's rows ra and ra + 1.  The parity of a differs
+// from lane to lane here, so the aligned 16-byte loads start at a - (a & 1) and
+// the M + 1 operands are selected per lane; each row still adds its M products
+// in ascending order.  Never reads past x[a + M].
+template <int M, class VS>
+__device__ __forceinline__ void fast2m_segment(const double* __restrict__ x, int a, const VS& vs, int vo, double& acc0,
+                                               double& acc1) {
+  const int p = a & 1;
+  const double* xb = x + (a - p);
+  const double2* xb2 = reinterpret_cast<const double2*>(xb);
+  constexpr int C0 = M + 1;  // operands when p = 0 (W[0..M]); p = 1 uses W[1..M+1]
+  double W[C0 + 2];
+#pragma unroll
+  for (int q = 0; 2 * q <= C0; ++q) {
+    if (2 * q + 1 < C0) {
+      const double2 t = __ldg(xb2 + q);
+      W[2 * q] = t.x;
+      W[2 * q + 1] = t.y;
+    } else if (2 * q + 1 == C0) {  // W[M] always, W[M + 1] only when p = 1
+      if (p) {
+        const double2 t = __ldg(xb2 + q);
+        W[2 * q] = t.x;
+        W[2 * q + 1] = t.y;
+      } else {
+        W[2 * q] = __ldg(xb + 2 * q);
+        W[2 * q + 1] = 0.0;
+      }
+    } else {  // 2 q == C0: W[M + 1], only when p = 1
+      W[2 * q] = p ? __ldg(xb + 2 * q) : 0.0;
+    }
+  }
+  double S[C0];
+#pragma unroll
+  for (int j = 0; j < C0; ++j) S[j] = p ? W[j + 1] : W[j];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const double v = vs(vo + j);
+    acc0 = acc0 + v * S[j];
+    acc1 = acc1 + v * S[j + 1];
+  }
+}
+template <class VS>
+__device__ __forceinline__ void fast2m_slice(const double* __restrict__ x, const int4* __restrict__ tb, const int2* __restrict__ sg,
+                                            int n, int ra, int pid, const VS& vs, double& acc0, double& acc1) {
+  const int* ob = reinterpret_cast<const int*>(tb + 2) + pid;
+  int vo = 0;
+  for (int u = 0; u < n; ++u) {
+    const int m = __ldg(sg + u).y;  // warp-uniform
+    const int a = ra + __ldg(ob + 4 * u);
+    switch (m) {
+      case 1: fast2m_segment<1>(x, a, vs, vo, acc0, acc1); break;
+      case 2: fast2m_segment<2>(x, a, vs, vo, acc0, acc1); break;
+      case 3: fast2m_segment<3>(x, a, vs, vo, acc0, acc1); break;
+      case 4: fast2m_segment<4>(x, a, vs, vo, acc0, acc1); break;
+      case 5: fast2m_segment<5>(x, a, vs, vo, acc0, acc1); break;
+      case 6: fast2m_segment<6>(x, a, vs, vo, acc0, acc1); break;
+      case 7: fast2m_segment<7>(x, a, vs, vo, acc0, acc1); break;
+      default: fast2m_segment<8>(x, a, vs, vo, acc0, acc1); break;
+    }
+    vo += m;
+  }
+}
+
 // The rows this lane will own in a slice (psell_slice's mapping), from the
 // static metadata: lets a kernel issue its per-row loads (residual source,
 // the x being corrected) ahead of the slice's product chain.  GENERAL slices:
@@ -193,7 +271,11 @@ __device__ __forceinline__ void psell_rows(const PSell& A, const uint4 mu, int* 
   }
   if (count == 0 || lane >= count) return;
   const int wv = static_cast<int>((pk >> 19) & 0x3f);
-  if (F4 && (pk & (1u << 17)) && wv == 2) {  // FAST4: B rows at + D
+  if (F4 && (pk & (1u << 17)) && wv == 3) {  // FAST2M: row pairs of up to four pieces
+    int odd;
+    row = fast2m_lane(A.useg + mu.z, lane, count, odd);
+    row2 = odd ? -1 : row + 1;
+  } else if (F4 && (pk & (1u << 17)) && wv == 2) {  // FAST4: B rows at + D
     const int D = __ldg(A.useg + mu.z).x;
     row = static_cast<int>(mu.x) + 2 * lane;
     row2 = row + 1;
@@ -298,6 +380,19 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
   if (count == 0) return -1;  // padding slice (warp-uniform)
   const int L = static_cast<int>(pk & kPMaxLen);
   const int cl = min(lane, count - 1);  // surplus lanes recompute the last row, store nothing
+  if (F4 && (pk & (1u << 17)) && ((pk >> 19) & 0x3f) == 3) {  // FAST2M: row pairs of several pieces (warp-uniform)
+    const int4* tb = A.useg + mu.z;
+    int odd, pid;
+    const int ra = fast2m_lane(tb, cl, count, odd, &pid);
+    const int4 hd = __ldg(tb + 1);
+    if (tab != nullptr && (pk >> 31))
+      fast2m_slice(x, tb, A.seg + hd.z, hd.w, ra, pid, VTabl{tab, static_cast<int>(mu.y)}, acc, acc2);
+    else
+      fast2m_slice(x, tb, A.seg + hd.z, hd.w, ra, pid, VGlob{A.V + mu.y}, acc, acc2);
+    if (lane >= count) return -1;
+    row2 = odd ? -1 : ra + 1;
+    return ra;
+  }
   if (F4 && (pk & (1u << 17)) && ((pk >> 19) & 0x3f) == 2) {  // FAST4: rows of two x-lines (warp-uniform)
     const int ra = static_cast<int>(mu.x) + 2 * cl;
     const int p0 = static_cast<int>(mu.x) & 1;
@@ -456,12 +551,25 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
 #ifndef IG_PPROLONG_MINB
 #define IG_PPROLONG_MINB 4
 #endif
+#ifndef IG_PSPMV_CTA
+#define IG_PSPMV_CTA 64  // threads per k_pspmv CTA: slices differ in cost (a FAST4 warp does 4x the products of a FAST one), small CTAs keep a slow warp from holding seven finished ones resident (C4 finest A p 134.4 -> 122.4 us vs 256; slices are padded to multiples of 8 per matrix)
+#endif
+constexpr int kPCta = IG_PSPMV_CTA;
 template <int MODE, bool STREAM, bool F4 = true>
-__global__ void __launch_bounds__(kCta, IG_PSPMV_MINB) k_pspmv(PSell A, const double* __restrict__ x, double* y,
+__global__ void __launch_bounds__(kPCta, IG_PSPMV_MINB * (256 / kPCta)) k_pspmv(PSell A, const double* __restrict__ x, double* y,
                                                const double* rsrc, const PcgState* st,
                                                const __grid_constant__ PValTab tab) {
-  const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
+  const int slice = blockIdx.x * (kPCta / 32) + (threadIdx.x >> 5);
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(A.meta + slice));  // static: before the wait
+#ifdef IG_DBG_SKIP  // timing experiments only (profiles/build_variants.sh): drop one slice class
+  {
+    const bool fast = mu.w & (1u << 17);
+    const int wv = static_cast<int>((mu.w >> 19) & 0x3f);
+    if ((IG_DBG_SKIP == 1 && !fast) || (IG_DBG_SKIP == 2 && fast && wv != 2) || (IG_DBG_SKIP == 3 && fast && wv == 2) ||
+        (IG_DBG_SKIP == 4 && fast))
+      return;
+  }
+#endif
   int pr[4];
   uint2 gen;
   psell_rows<F4>(A, mu, pr, gen);

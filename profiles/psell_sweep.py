@@ -24,6 +24,10 @@ def main():
           "c5": configs.c5}
     vp = C.c_void_p
     tag = os.environ.get("IG_GPU_LIB", "libig_gpu.so")
+    for kv in filter(None, os.environ.get("IG_OPTS", "").split(",")):  # e.g. IG_OPTS=34=0,27=1
+        k, v = kv.split("=")
+        assert lib.ig_set_option(int(k), int(v)) == 0
+        tag += f" opt{k}={v}"
     for wl in wls:
         case = build_case(mk[wl]())
         db = torch.from_numpy(case.b).cuda()
