@@ -118,6 +118,7 @@ IG_OPT_GAL_SHORT = 21
 IG_OPT_PSELL_CTAB = 23
 IG_OPT_PSELL_LINES2 = 27
 IG_OPT_PSELL_MULTI = 34
+IG_OPT_PSELL_AB = 35
 
 _host = None
 _gpu = None

@@ -78,6 +78,7 @@ struct Opts {
   int psell_ctab = 1;    // FAST2 value sequences from a constant-bank table
   int psell_lines2 = 1;  // FAST4 slices (two x-lines per slice)
   int psell_multi = 1;   // FAST2M slices (row pairs of up to four short runs per slice)
+  int psell_ab = 1;      // FASTAB slices (row pairs with one column list, two value sequences: prolongations)
   int gal_short = 1;     // prefetching SpGEMM for B rows <= 32 entries
   // Levels below the finest with at most this many DOFs live in the
   // L2-persisting arena (ig_hier::alloc); 0 = off.  Arena size l2_bytes.
@@ -296,6 +297,7 @@ struct HostPSell {
   std::vector<int4> useg;    // FAST4 union segment lists (header {D, n}, then {o, m, vA, vB})
   int64_t n_fast4 = 0;
   int64_t n_fast2m = 0;      // FAST2M slices (their tables live in useg too)
+  int64_t n_fastab = 0;      // FASTAB slices
   std::vector<double> tab;   // constant-bank value table (spmv_psell.cuh PValTab)
   int64_t tab_rows = 0;      // rows whose FAST2 values come from the table
 };
@@ -385,7 +387,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
     }
   });
   const int cand[3][2] = {{1, 0}, {2, 0}, {1, 1}};
-  size_t best_runs = SIZE_MAX;
+  size_t best_runs = SIZE_MAX, best_oruns = SIZE_MAX;
   std::vector<uint64_t> hcur(static_cast<size_t>(nr));
   for (const auto& c : cand) {
     if (c[0] == 2 && nc < nr) continue;  // scaling up only for wide (restriction-shaped) matrices
@@ -398,10 +400,16 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
         hcur[i] = h;
       }
     });
-    size_t runs = 0;  // consecutive-row changes of (values, offsets)
-    for (int32_t i = 1; i < nr; ++i) runs += (hv[i] != hv[i - 1] || hcur[i] != hcur[i - 1]) ? 1 : 0;
-    if (runs < best_runs) {
+    size_t runs = 0, oruns = 0;  // consecutive-row changes of the offsets alone (what the scale decides: a
+                                 // prolongation's rows alternate two value sequences under every scale), then
+                                 // of (values, offsets)
+    for (int32_t i = 1; i < nr; ++i) {
+      runs += (hv[i] != hv[i - 1] || hcur[i] != hcur[i - 1]) ? 1 : 0;
+      oruns += hcur[i] != hcur[i - 1] ? 1 : 0;
+    }
+    if (oruns < best_oruns || (oruns == best_oruns && runs < best_runs)) {
       best_runs = runs;
+      best_oruns = oruns;
       s.smul = c[0];
       s.sshift = c[1];
       ho.swap(hcur);
@@ -808,11 +816,73 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
     useg_of[{sg, D}] = st;
     return st;
   };
+  // FASTAB (half-scaled base only, i.e. prolongation-shaped matrices): items
+  // = consecutive rows (r, r + 1) with the SAME column list; runs of items
+  // whose first rows share one value sequence, whose second rows share
+  // another, and whose columns advance by one per item (offsets against
+  // base(r) = r >> 1 constant).  One lane per item: every x is gathered once
+  // for both rows.  Values interleaved {A_k, B_k}.
+  std::vector<uint8_t> claimed(static_cast<size_t>(nr), 0);
+  if (opt().psell_ab && s.smul == 1 && s.sshift == 1) {
+    auto ceq = [&](int32_t a, int32_t b) {
+      return len(a) == len(b) && len(a) > 0 &&
+             std::memcmp(col + ptr[a], col + ptr[b], sizeof(int32_t) * static_cast<size_t>(len(a))) == 0;
+    };
+    std::vector<int32_t> items;  // first rows
+    for (int32_t i = 0; i + 1 < nr;) {
+      if (!in_fast[i] && !in_fast[i + 1] && ceq(i, i + 1)) {
+        items.push_back(i);
+        i += 2;
+      } else {
+        ++i;
+      }
+    }
+    std::map<std::pair<uint64_t, uint64_t>, std::vector<std::pair<uint32_t, int32_t>>> abseq;  // -> (start, first row)
+    auto ab_start = [&](int32_t i) -> uint32_t {
+      auto& b = abseq[{hv[i], hv[i + 1]}];
+      for (const auto& [st, r] : b)
+        if (veq(i, r) && veq(i + 1, r + 1)) return st;
+      s.V.resize((s.V.size() + 1) & ~size_t(1), 0.0);
+      const uint32_t st = static_cast<uint32_t>(s.V.size());
+      for (int32_t k = 0; k < len(i); ++k) {
+        s.V.push_back(val[ptr[i] + k]);
+        s.V.push_back(val[ptr[i + 1] + k]);
+      }
+      s.layout_bytes += 16 * static_cast<int64_t>(len(i));
+      b.push_back({st, i});
+      return st;
+    };
+    for (size_t a = 0; a < items.size();) {
+      size_t b = a + 1;
+      const int32_t f = items[a];
+      while (b < items.size() && items[b] == items[b - 1] + 2 && hv[items[b]] == hv[f] && hv[items[b] + 1] == hv[f + 1] &&
+             ho[items[b]] == ho[f] && veq(items[b], f) && veq(items[b] + 1, f + 1) && oeq(items[b], f))
+        ++b;
+      if (b - a >= static_cast<size_t>(kPMinRun)) {
+        lmax_all = std::max(lmax_all, 2 * len(f));
+        const uint32_t vb = ab_start(f), ob = o_start(f);
+        for (size_t q = a; q < b; q += 32) {
+          const int cnt = static_cast<int>(std::min<size_t>(32, b - q));
+          s.meta.push_back(PSliceMeta{static_cast<uint32_t>(items[q]), vb, ob, pack(len(f), cnt, true, true, 4, 0)});
+          s.layout_bytes += 16;
+          ++s.n_fast;
+          ++s.n_fastab;
+          s.fast_rows += 2 * cnt;
+        }
+        for (size_t q = a; q < b; ++q) claimed[items[q]] = claimed[items[q] + 1] = 1;
+      }
+      a = b;
+    }
+  }
+  if (std::getenv("IG_TIMING"))
+    std::fprintf(stderr, "[psell base] %d x %d: smul %d sshift %d, %lld FASTAB slices\n", nr, nc, s.smul, s.sshift,
+                 static_cast<long long>(s.n_fastab));
   std::vector<int32_t> pending;
   for (size_t r = 0; r < nruns; ++r) {
     const int32_t r0 = run_start[r], r1 = run_start[r + 1];
     if (r1 - r0 < kPMinRun) {
       for (int32_t i = r0; i < r1; ++i) {
+        if (claimed[i]) continue;
         pending.push_back(i);
         if (pending.size() == 32) {
           emit_general(pending);
@@ -868,8 +938,8 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       if (m.pk & (1u << 17)) {
         const int wv = static_cast<int>((m.pk >> 19) & 0x3f);  // 0 FAST, 1 FAST2, 2 FAST4
         auto& u = use[m.vbase];
-        u.first += (wv == 2 ? 4 : wv == 1 || wv == 3 ? 2 : 1) * static_cast<int64_t>((m.pk >> 11) & 0x3f);
-        u.second = static_cast<int32_t>(m.pk & kPMaxLen);
+        u.first += (wv == 2 ? 4 : wv == 1 || wv == 3 || wv == 4 ? 2 : 1) * static_cast<int64_t>((m.pk >> 11) & 0x3f);
+        u.second = static_cast<int32_t>(m.pk & kPMaxLen) * (wv == 4 ? 2 : 1);  // FASTAB: interleaved pair sequence
       }
     std::vector<std::pair<int64_t, uint32_t>> order;
     for (const auto& [vb, u] : use) order.push_back({u.first, vb});
@@ -1954,6 +2024,10 @@ int ig_set_option(int32_t option, int64_t value) {
     g_defaults.psell_multi = value != 0;
     return IG_OK;
   }
+  if (option == IG_OPT_PSELL_AB) {
+    g_defaults.psell_ab = value != 0;
+    return IG_OK;
+  }
   if (option == IG_OPT_GAL_SHORT) {
     g_defaults.gal_short = value != 0;
     return IG_OK;
@@ -2432,7 +2506,7 @@ int ig_debug_psell_stats(const ig_csr* a, int64_t* out, int32_t n_out) {
       if (count == 0) continue;
       const bool fast = m.pk & (1u << 17);
       const int wv = static_cast<int>((m.pk >> 19) & 0x3f);
-      const int cls = !fast ? 0 : wv == 0 ? 1 : wv == 1 ? 2 : wv == 2 ? 3 : 4;
+      const int cls = !fast ? 0 : wv == 0 ? 1 : wv == 1 || wv == 4 ? 2 : wv == 2 ? 3 : 4;  // (FASTAB counted with FAST2)
       ++out[cls];
       out[5 + cls] += count;
       ++out[10 + 4 * cls + (count - 1) / 8];

@@ -281,7 +281,7 @@ __device__ __forceinline__ void psell_rows(const PSell& A, const uint4 mu, int* 
     row2 = row + 1;
     rows[2] = row + D;
     rows[3] = row + D + 1;
-  } else if ((pk & (1u << 17)) && wv == 1) {
+  } else if ((pk & (1u << 17)) && (wv == 1 || wv == 4)) {  // FAST2 / FASTAB: row pairs
     row = static_cast<int>(mu.x) + 2 * lane;
     row2 = row + 1;
   } else if (pk & (1u << 17)) {
@@ -439,6 +439,51 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
       else
         fast2_dispatch<1>(x, ra + e.x, e.y, vp, acc, acc2);
       vp += e.y;
+    }
+    if (lane >= count) return -1;
+    row2 = ra + 1;
+    return ra;
+  }
+  if ((pk & (1u << 17)) && ((pk >> 19) & 0x3f) == 4) {  // FASTAB: row pairs sharing their columns (warp-uniform)
+    // Rows ra and ra + 1 have the same column list (a prolongation's two
+    // fine rows under one coarse stencil) and their own value sequences,
+    // stored interleaved {A_k, B_k}; each x is gathered once for both.
+    const int ra = static_cast<int>(mu.x) + 2 * cl;
+    const double* xr = x + ((ra * A.smul) >> A.sshift);
+    const int4* op4 = reinterpret_cast<const int4*>(A.O + mu.z);
+    const bool tb = tab != nullptr && (pk >> 31);
+    const double2* vp2 = reinterpret_cast<const double2*>(A.V + mu.y);
+    const int vo = static_cast<int>(mu.y);
+    int k = 0;
+    for (; k + 4 <= L; k += 4) {
+      const int4 b = __ldg(op4 + (k >> 2));
+      const double x0 = __ldg(xr + b.x), x1 = __ldg(xr + b.y), x2 = __ldg(xr + b.z), x3 = __ldg(xr + b.w);
+      double2 v0, v1, v2, v3;
+      if (tb) {
+        v0 = make_double2(tab->v[vo + 2 * k], tab->v[vo + 2 * k + 1]);
+        v1 = make_double2(tab->v[vo + 2 * k + 2], tab->v[vo + 2 * k + 3]);
+        v2 = make_double2(tab->v[vo + 2 * k + 4], tab->v[vo + 2 * k + 5]);
+        v3 = make_double2(tab->v[vo + 2 * k + 6], tab->v[vo + 2 * k + 7]);
+      } else {
+        v0 = __ldg(vp2 + k);
+        v1 = __ldg(vp2 + k + 1);
+        v2 = __ldg(vp2 + k + 2);
+        v3 = __ldg(vp2 + k + 3);
+      }
+      acc = acc + v0.x * x0;
+      acc2 = acc2 + v0.y * x0;
+      acc = acc + v1.x * x1;
+      acc2 = acc2 + v1.y * x1;
+      acc = acc + v2.x * x2;
+      acc2 = acc2 + v2.y * x2;
+      acc = acc + v3.x * x3;
+      acc2 = acc2 + v3.y * x3;
+    }
+    for (; k < L; ++k) {
+      const double xk = __ldg(xr + __ldg(A.O + mu.z + k));
+      const double2 v = tb ? make_double2(tab->v[vo + 2 * k], tab->v[vo + 2 * k + 1]) : __ldg(vp2 + k);
+      acc = acc + v.x * xk;
+      acc2 = acc2 + v.y * xk;
     }
     if (lane >= count) return -1;
     row2 = ra + 1;

@@ -109,6 +109,41 @@ def test_breakdown_through_pattern_sell():
         h.close()
 
 
+@pytest.mark.parametrize("ab,ctab", [(0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("case_name", ["d3_48_case", "c3_small_case", "c1_case"])
+def test_pair_item_prolongation_bitwise(request, case_name, ab, ctab):
+    """FASTAB slices (IG_OPT_PSELL_AB: a prolongation's row pairs sharing one
+    column list, two interleaved value sequences, values from HBM or the
+    constant-bank table) against the GENERAL-slice layout: restriction,
+    prolongation (+ correction), V-cycles and the solve give the oracle's
+    bits (pattern layout forced on every level)."""
+    from paper_1903_10977_b200 import MgHierarchy, _ffi, pcg
+    lib = _ffi.gpu()
+    case = request.getfixturevalue(case_name)
+    lv = case.levels_c()
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_AB, ab)
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_CTAB, ctab)
+    lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 0)
+    try:
+        h = MgHierarchy(case)
+    finally:
+        lib.ig_set_option(_ffi.IG_OPT_PSELL_AB, 1)
+        lib.ig_set_option(_ffi.IG_OPT_PSELL_CTAB, 1)
+        lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
+    try:
+        for l in range(1, h.levels()):
+            A, R = h.level(l)
+            x = rng_vec(470 + l, A.cols())
+            assert np.array_equal(h.spmv(l, x, 2), orc.spmv(lv, l, x, 2))
+            xc = rng_vec(490 + l, R.rows())
+            assert np.array_equal(h.spmv(l, xc, 3), orc.spmv(lv, l, xc, 3))
+        x, rep = pcg(h.A, case.b, h, tol=1e-8, maxit=1000)
+        st, xo, ro, it, _ = orc.pcg(lv, case.b, tol=1e-8, maxit=1000, mode=orc.GPU_ORDER)
+        assert st == 0 and rep.iterations == it and np.array_equal(x, xo)
+    finally:
+        h.close()
+
+
 @pytest.mark.parametrize("ctab", [0, 1])
 def test_constant_value_table_bitwise(ctab):
     """FAST2 value sequences read from the constant-bank kernel-parameter table
