@@ -119,6 +119,7 @@ IG_OPT_PSELL_CTAB = 23
 IG_OPT_PSELL_LINES2 = 27
 IG_OPT_PSELL_MULTI = 34
 IG_OPT_PSELL_AB = 35
+IG_OPT_PSELL_ROWS4 = 36
 
 _host = None
 _gpu = None

@@ -78,6 +78,7 @@ struct Opts {
   int psell_ctab = 1;    // FAST2 value sequences from a constant-bank table
   int psell_lines2 = 1;  // FAST4 slices (two x-lines per slice)
   int psell_multi = 1;   // FAST2M slices (row pairs of up to four short runs per slice)
+  int psell_rows4 = 1;   // FAST8 slices (four rows of each of two x-lines per lane)
   int psell_ab = 1;      // FASTAB slices (row pairs with one column list, two value sequences: prolongations)
   int gal_short = 1;     // prefetching SpGEMM for B rows <= 32 entries
   // Levels below the finest with at most this many DOFs live in the
@@ -298,6 +299,7 @@ struct HostPSell {
   int64_t n_fast4 = 0;
   int64_t n_fast2m = 0;      // FAST2M slices (their tables live in useg too)
   int64_t n_fastab = 0;      // FASTAB slices
+  int64_t n_fast8 = 0;       // FAST8 slices
   std::vector<double> tab;   // constant-bank value table (spmv_psell.cuh PValTab)
   int64_t tab_rows = 0;      // rows whose FAST2 values come from the table
 };
@@ -772,7 +774,8 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       ++why[7];
       pairB[r] = static_cast<int32_t>(rb);
       pa0[r] = a0;
-      pa1[r] = a0 + ((a1 - a0) & ~1);
+      // (FAST8 slices take whole groups of four rows per line; FAST4 pairs)
+      pa1[r] = a0 + ((a1 - a0) & (opt().psell_rows4 && a1 - a0 >= 32 ? ~3 : ~1));
       pD[r] = DD;
       is_b[rb] = 1;
       pairA[rb] = static_cast<int32_t>(r);
@@ -810,7 +813,9 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       }
     }
     const uint32_t st = static_cast<uint32_t>(s.useg.size());
-    s.useg.push_back(make_int4(D, static_cast<int>(ent.size()), 0, 0));
+    int all5 = ent.empty() ? 0 : 1;  // every union run 5 long: the pipelined slice loop applies
+    for (const int4& e : ent) all5 = all5 && e.y == 5;
+    s.useg.push_back(make_int4(D, static_cast<int>(ent.size()), all5, 0));
     s.useg.insert(s.useg.end(), ent.begin(), ent.end());
     s.layout_bytes += 16 * static_cast<int64_t>(ent.size() + 1);
     useg_of[{sg, D}] = st;
@@ -905,13 +910,16 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       const uint32_t vb = v_start(r0);
       const uint32_t ug = union_start(r0, pD[r]);
       lmax_all = std::max(lmax_all, len(r0));
+      const bool rows4 = opt().psell_rows4 && a1 - a0 >= 32 && (a1 - a0) % 4 == 0;
       for (int32_t i = a0; i < a1;) {
-        const int cnt = std::min(64, a1 - i);
-        s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, ug, pack(len(r0), cnt / 2, true, true, 2, 0)});
+        const int cnt = std::min(rows4 ? 128 : 64, a1 - i);
+        s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, ug,
+                                    pack(len(r0), rows4 ? cnt / 4 : cnt / 2, true, true, rows4 ? 5 : 2, 0)});
         s.layout_bytes += 16;
         ++s.n_fast;
         s.fast_rows += 2 * cnt;
         ++s.n_fast4;
+        if (rows4) ++s.n_fast8;
         i += cnt;
       }
       emit_piece(a1, r1, r0);
@@ -938,7 +946,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       if (m.pk & (1u << 17)) {
         const int wv = static_cast<int>((m.pk >> 19) & 0x3f);  // 0 FAST, 1 FAST2, 2 FAST4
         auto& u = use[m.vbase];
-        u.first += (wv == 2 ? 4 : wv == 1 || wv == 3 || wv == 4 ? 2 : 1) * static_cast<int64_t>((m.pk >> 11) & 0x3f);
+        u.first += (wv == 5 ? 8 : wv == 2 ? 4 : wv == 1 || wv == 3 || wv == 4 ? 2 : 1) * static_cast<int64_t>((m.pk >> 11) & 0x3f);
         u.second = static_cast<int32_t>(m.pk & kPMaxLen) * (wv == 4 ? 2 : 1);  // FASTAB: interleaved pair sequence
       }
     std::vector<std::pair<int64_t, uint32_t>> order;
@@ -2024,6 +2032,10 @@ int ig_set_option(int32_t option, int64_t value) {
     g_defaults.psell_multi = value != 0;
     return IG_OK;
   }
+  if (option == IG_OPT_PSELL_ROWS4) {
+    g_defaults.psell_rows4 = value != 0;
+    return IG_OK;
+  }
   if (option == IG_OPT_PSELL_AB) {
     g_defaults.psell_ab = value != 0;
     return IG_OK;
@@ -2506,7 +2518,7 @@ int ig_debug_psell_stats(const ig_csr* a, int64_t* out, int32_t n_out) {
       if (count == 0) continue;
       const bool fast = m.pk & (1u << 17);
       const int wv = static_cast<int>((m.pk >> 19) & 0x3f);
-      const int cls = !fast ? 0 : wv == 0 ? 1 : wv == 1 || wv == 4 ? 2 : wv == 2 ? 3 : 4;  // (FASTAB counted with FAST2)
+      const int cls = !fast ? 0 : wv == 0 ? 1 : wv == 1 || wv == 4 ? 2 : wv == 2 || wv == 5 ? 3 : 4;  // (FASTAB counted with FAST2)
       ++out[cls];
       out[5 + cls] += count;
       ++out[10 + 4 * cls + (count - 1) / 8];

@@ -363,6 +363,136 @@ __device__ __forceinline__ void fast4_slice(const double* __restrict__ x, const 
   }
 }
 
+// FAST4 slices whose union runs all have length 5 (the 3D p = 2 interior
+// stencil), software-pipelined: the x window of run u + 1 is in flight while
+// run u is summed -- one slice is ~30 dependent L2 round trips otherwise, and
+// its warp spends most of its life waiting (FAST4 alone: 36 % of the FP64
+// pipe).  Same loads, same products, same order.
+#ifndef IG_F4_PIPE
+#define IG_F4_PIPE 0
+#endif
+__device__ __forceinline__ void f4_window(const double* __restrict__ x, int a, int P, double* W) {
+  const double* xb = x + (a - P);
+  const double2* xb2 = reinterpret_cast<const double2*>(xb);
+  const double2 t0 = __ldg(xb2), t1 = __ldg(xb2 + 1), t2 = __ldg(xb2 + 2);
+  W[0] = t0.x;
+  W[1] = t0.y;
+  W[2] = t1.x;
+  W[3] = t1.y;
+  W[4] = t2.x;
+  W[5] = t2.y;
+  W[6] = P ? __ldg(xb + 6) : 0.0;  // x[a + 5]: never reads past it
+}
+template <int P, class VS>
+__device__ __forceinline__ void f4_sum5(const double* W, const VS& vs, int vA, int vB, double* acc) {
+  if (vA >= 0) {  // warp-uniform
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const double v = vs(vA + j);
+      acc[0] = acc[0] + v * W[P + j];
+      acc[1] = acc[1] + v * W[P + j + 1];
+    }
+  }
+  if (vB >= 0) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const double v = vs(vB + j);
+      acc[2] = acc[2] + v * W[P + j];
+      acc[3] = acc[3] + v * W[P + j + 1];
+    }
+  }
+}
+template <class VS>
+__device__ __forceinline__ void fast4_slice5(const double* __restrict__ x, const int4* __restrict__ ug, int n, int ra,
+                                            int p0, const VS& vs, double* acc) {
+  double Wa[7], Wb[7];
+  int4 ea = __ldg(ug), eb = ea;
+  int Pa = (p0 + ea.x) & 1, Pb = 0;
+  f4_window(x, ra + ea.x, Pa, Wa);
+  for (int u = 0; u < n; u += 2) {
+    if (u + 1 < n) {
+      eb = __ldg(ug + u + 1);
+      Pb = (p0 + eb.x) & 1;
+      f4_window(x, ra + eb.x, Pb, Wb);
+    }
+    if (Pa == 0) f4_sum5<0>(Wa, vs, ea.z, ea.w, acc);
+    else f4_sum5<1>(Wa, vs, ea.z, ea.w, acc);
+    if (u + 1 >= n) break;
+    if (u + 2 < n) {
+      ea = __ldg(ug + u + 2);
+      Pa = (p0 + ea.x) & 1;
+      f4_window(x, ra + ea.x, Pa, Wa);
+    }
+    if (Pb == 0) f4_sum5<0>(Wb, vs, eb.z, eb.w, acc);
+    else f4_sum5<1>(Wb, vs, eb.z, eb.w, acc);
+  }
+}
+
+// FAST8: as FAST4 with FOUR rows of each of the two x-lines per lane (rows
+// ra .. ra + 3 and ra + D .. ra + D + 3): one window of M + 3 values feeds 4 M
+// products per line -- 1.6 B of x per product through the L1 data pipe (the
+// unit that bounds this kernel) instead of FAST4's 2.8 B, and one warp per
+// 124-row line pair instead of two.
+template <int P, int M, class VS>
+__device__ __forceinline__ void fast8_segment(const double* __restrict__ x, int a, const VS& vs, int vA, int vB,
+                                              double* acc) {
+  constexpr int C = M + 3 + P;  // values needed from base = a - P
+  const double* xb = x + (a - P);
+  const double2* xb2 = reinterpret_cast<const double2*>(xb);
+  double X[C + 1];
+#pragma unroll
+  for (int q = 0; 2 * q < C; ++q) {
+    if (2 * q + 1 < C) {
+      const double2 t = __ldg(xb2 + q);
+      X[2 * q] = t.x;
+      X[2 * q + 1] = t.y;
+    } else {
+      X[2 * q] = __ldg(xb + 2 * q);  // last value only: never read past x[a + M + 2]
+    }
+  }
+  if (vA >= 0) {  // warp-uniform
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const double v = vs(vA + j);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = acc[r] + v * X[P + j + r];
+    }
+  }
+  if (vB >= 0) {
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const double v = vs(vB + j);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[4 + r] = acc[4 + r] + v * X[P + j + r];
+    }
+  }
+}
+template <int P, class VS>
+__device__ __forceinline__ void fast8_dispatch(const double* __restrict__ x, int a, int m, const VS& vs, int vA, int vB,
+                                               double* acc) {
+  switch (m) {  // warp-uniform
+    case 1: fast8_segment<P, 1>(x, a, vs, vA, vB, acc); break;
+    case 2: fast8_segment<P, 2>(x, a, vs, vA, vB, acc); break;
+    case 3: fast8_segment<P, 3>(x, a, vs, vA, vB, acc); break;
+    case 4: fast8_segment<P, 4>(x, a, vs, vA, vB, acc); break;
+    case 5: fast8_segment<P, 5>(x, a, vs, vA, vB, acc); break;
+    case 6: fast8_segment<P, 6>(x, a, vs, vA, vB, acc); break;
+    case 7: fast8_segment<P, 7>(x, a, vs, vA, vB, acc); break;
+    default: fast8_segment<P, 8>(x, a, vs, vA, vB, acc); break;
+  }
+}
+template <class VS>
+__device__ __forceinline__ void fast8_slice(const double* __restrict__ x, const int4* __restrict__ ug, int n, int ra,
+                                           int p0, const VS& vs, double* acc) {
+  for (int u = 0; u < n; ++u) {
+    const int4 e = __ldg(ug + u);
+    if (((p0 + e.x) & 1) == 0)
+      fast8_dispatch<0>(x, ra + e.x, e.y, vs, e.z, e.w, acc);
+    else
+      fast8_dispatch<1>(x, ra + e.x, e.y, vs, e.z, e.w, acc);
+  }
+}
+
 // One warp, one slice.  Returns the row this lane owns (-1: none) and its
 // sum; FAST2 slices give each lane a second row (row2 / acc2, else -1).
 // gen: psell_rows' {row, ginfo} (GENERAL slices).
@@ -398,7 +528,9 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
     const int p0 = static_cast<int>(mu.x) & 1;
     const int4 hd = __ldg(A.useg + mu.z);
     double a4[4] = {0.0, 0.0, 0.0, 0.0};
-    if (tab != nullptr && (pk >> 31))
+    if (IG_F4_PIPE && hd.z && tab != nullptr && (pk >> 31))  // every run 5 long, values in the table
+      fast4_slice5(x, A.useg + mu.z + 1, hd.y, ra, p0, VTabl{tab, static_cast<int>(mu.y)}, a4);
+    else if (tab != nullptr && (pk >> 31))
       fast4_slice(x, A.useg + mu.z + 1, hd.y, ra, p0, VTabl{tab, static_cast<int>(mu.y)}, a4);
     else
       fast4_slice(x, A.useg + mu.z + 1, hd.y, ra, p0, VGlob{A.V + mu.y}, a4);
@@ -610,11 +742,42 @@ __global__ void __launch_bounds__(kPCta, IG_PSPMV_MINB * (256 / kPCta)) k_pspmv(
   {
     const bool fast = mu.w & (1u << 17);
     const int wv = static_cast<int>((mu.w >> 19) & 0x3f);
-    if ((IG_DBG_SKIP == 1 && !fast) || (IG_DBG_SKIP == 2 && fast && wv != 2) || (IG_DBG_SKIP == 3 && fast && wv == 2) ||
-        (IG_DBG_SKIP == 4 && fast))
+    if ((IG_DBG_SKIP == 1 && !fast) || (IG_DBG_SKIP == 2 && fast && wv != 2) || (IG_DBG_SKIP == 3 && fast && (wv == 2 || wv == 5)) ||
+        (IG_DBG_SKIP == 4 && fast) || (IG_DBG_SKIP == 5 && fast && wv == 3) || (IG_DBG_SKIP == 6 && !(fast && wv == 3)) ||
+        (IG_DBG_SKIP == 7 && !(fast && (wv == 2 || wv == 5))))
       return;
   }
 #endif
+  if (F4 && (mu.w & (1u << 17)) && ((mu.w >> 19) & 0x3f) == 5) {  // FAST8 (warp-uniform): own epilogue, 8 rows per lane
+    const int lane = threadIdx.x & 31;
+    const int count = static_cast<int>((mu.w >> 11) & 0x3f);
+    const int4 hd = __ldg(A.useg + mu.z);
+    pdl_entry();
+    if (pcg_done(st)) return;
+    const int ra = static_cast<int>(mu.x) + 4 * min(lane, count - 1);
+    double a8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (mu.w >> 31)
+      fast8_slice(x, A.useg + mu.z + 1, hd.y, ra, static_cast<int>(mu.x) & 1, VTabl{&tab, static_cast<int>(mu.y)}, a8);
+    else
+      fast8_slice(x, A.useg + mu.z + 1, hd.y, ra, static_cast<int>(mu.x) & 1, VGlob{A.V + mu.y}, a8);
+    if (lane >= count) return;
+    if (MODE == 1) {  // (the eight residual sources together, after the chain: no registers held across it)
+      double rs8[8];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        rs8[r] = rsrc[ra + r];
+        rs8[4 + r] = rsrc[ra + hd.x + r];
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) a8[r] = rs8[r] - a8[r];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      y[ra + r] = a8[r];
+      y[ra + hd.x + r] = a8[4 + r];
+    }
+    return;
+  }
   int pr[4];
   uint2 gen;
   psell_rows<F4>(A, mu, pr, gen);
