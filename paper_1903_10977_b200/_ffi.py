@@ -120,6 +120,7 @@ IG_OPT_PSELL_LINES2 = 27
 IG_OPT_PSELL_MULTI = 34
 IG_OPT_PSELL_AB = 35
 IG_OPT_PSELL_ROWS4 = 36
+IG_OPT_PSELL_EDGE_ROWS = 37
 
 _host = None
 _gpu = None

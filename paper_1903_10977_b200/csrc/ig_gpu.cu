@@ -24,6 +24,7 @@
 #include <string>
 #include <thread>
 #include <unordered_map>
+#include <unordered_set>
 #include <utility>
 #include <vector>
 
@@ -79,6 +80,7 @@ struct Opts {
   int psell_lines2 = 1;  // FAST4 slices (two x-lines per slice)
   int psell_multi = 1;   // FAST2M slices (row pairs of up to four short runs per slice)
   int psell_rows4 = 1;   // FAST8 slices (four rows of each of two x-lines per lane)
+  int32_t psell_edge_rows = 100000;  // FASTE slices (edge-compacted x) for square matrices with at least this many rows (0 = off)
   int psell_ab = 1;      // FASTAB slices (row pairs with one column list, two value sequences: prolongations)
   int gal_short = 1;     // prefetching SpGEMM for B rows <= 32 entries
   // Levels below the finest with at most this many DOFs live in the
@@ -300,6 +302,8 @@ struct HostPSell {
   int64_t n_fast2m = 0;      // FAST2M slices (their tables live in useg too)
   int64_t n_fastab = 0;      // FASTAB slices
   int64_t n_fast8 = 0;       // FAST8 slices
+  int64_t n_faste = 0;       // FASTE slices
+  std::vector<int32_t> G;    // FASTE: xe[i] = x[G[i]] (the edge-compacted copy of x, gathered before the product)
   std::vector<double> tab;   // constant-bank value table (spmv_psell.cuh PValTab)
   int64_t tab_rows = 0;      // rows whose FAST2 values come from the table
 };
@@ -879,9 +883,161 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       a = b;
     }
   }
+  // FASTE: leftover rows whose gathers are STRIDED -- the first / last rows of
+  // every x-line (a B-spline line's end functions: six value classes in 3D,
+  // ~5 % of the rows but ~25 % of the kernel's L1 wavefronts as GENERAL
+  // slices, whose 32 lanes touch 10-16 cache lines per gather).  The columns
+  // they read form equal-length blocks (the last / first columns of
+  // consecutive lines); xe = those blocks transposed (xe[c T + t] = column c
+  // of block t), gathered from x by a small kernel before the product.  In
+  // xe, rows of one class on consecutive lines read consecutive elements
+  // with ONE offset sequence -- also next to an immersed boundary, where the
+  // line starts are irregular in x but every line still has its ends -- so
+  // they run as FAST-style slices (warp-uniform values and offsets, coalesced
+  // gathers).  rlist / ginfo hold each lane's row and its anchor block.
+  if (opt().psell_edge_rows > 0 && nr >= opt().psell_edge_rows && nr == nc && s.smul == 1 && s.sshift == 0) {
+    constexpr size_t kEdgeMin = 256;  // rows per value class
+    constexpr int32_t kEdgeRun = 16;  // consecutive anchors per run
+    std::unordered_map<uint64_t, std::vector<int32_t>> cls;
+    std::unordered_set<uint64_t> run_values;  // value sequences of the long runs: their stray rows are no edge rows
+    for (int32_t i = 0; i < nr; ++i)
+      if (in_fast[i] && brk[i]) run_values.insert(hv[i]);
+    for (int32_t i = 0; i < nr; ++i)
+      if (!in_fast[i] && !claimed[i] && len(i) > 0 && !run_values.count(hv[i])) cls[hv[i]].push_back(i);
+    std::vector<int32_t> fam;
+    for (auto& kv : cls) {
+      if (kv.second.size() < kEdgeMin) continue;
+      for (int32_t r : kv.second)
+        if (veq(r, kv.second[0])) fam.push_back(r);
+    }
+    std::sort(fam.begin(), fam.end());
+    if (static_cast<int64_t>(fam.size()) * 50 >= nr) {  // at least 2 % of the rows
+      std::vector<uint8_t> used(static_cast<size_t>(nc), 0);
+      for (int32_t r : fam)
+        for (int32_t k = ptr[r]; k < ptr[r + 1]; ++k) used[col[k]] = 1;
+      std::vector<int32_t> bstart, blen;
+      std::map<int32_t, int64_t> hist;
+      int64_t total = 0;
+      for (int32_t j = 0; j < nc;) {
+        if (!used[j]) {
+          ++j;
+          continue;
+        }
+        const int32_t j0 = j;
+        while (j < nc && used[j]) ++j;
+        bstart.push_back(j0);
+        blen.push_back(j - j0);
+        hist[j - j0] += j - j0;
+        total += j - j0;
+      }
+      int32_t Wb = 0;
+      int64_t cov = 0;
+      for (const auto& [w, c] : hist)
+        if (c > cov) {
+          cov = c;
+          Wb = w;
+        }
+      if (std::getenv("IG_TIMING"))
+        std::fprintf(stderr, "[psell edge] family %zu rows, %zu column blocks, modal length %d covering %lld of %lld columns\n",
+                     fam.size(), bstart.size(), Wb, static_cast<long long>(cov), static_cast<long long>(total));
+      if (Wb >= 2 && Wb <= 64 && cov * 2 >= total) {
+        std::vector<int32_t> tof(static_cast<size_t>(nc), -1);
+        std::vector<uint8_t> cof(static_cast<size_t>(nc), 0);
+        int32_t T = 0;
+        for (size_t b = 0; b < bstart.size(); ++b)
+          if (blen[b] == Wb) {
+            for (int32_t c = 0; c < Wb; ++c) {
+              tof[bstart[b] + c] = T;
+              cof[bstart[b] + c] = static_cast<uint8_t>(c);
+            }
+            ++T;
+          }
+        struct ER {
+          uint64_t key;
+          int32_t ta, row;
+        };
+        std::vector<ER> er;
+        auto xoff = [&](int32_t r, int32_t k, int32_t ta) {  // offset of entry k of row r in xe, against its anchor
+          const int32_t c = col[ptr[r] + k];
+          return static_cast<int32_t>(cof[c]) * T + (tof[c] - ta);
+        };
+        for (int32_t r : fam) {
+          bool ok = true;
+          for (int32_t k = ptr[r]; k < ptr[r + 1] && ok; ++k) ok = tof[col[k]] >= 0;
+          if (!ok) continue;
+          const int32_t ta = tof[col[ptr[r]]];
+          uint64_t h = mix64(hv[r], 0xE5);
+          for (int32_t k = 0; k < len(r); ++k) h = mix64(h, static_cast<uint64_t>(static_cast<uint32_t>(xoff(r, k, ta))));
+          er.push_back(ER{h, ta, r});
+        }
+        std::sort(er.begin(), er.end(), [](const ER& a, const ER& b) {
+          return a.key != b.key ? a.key < b.key : a.ta != b.ta ? a.ta < b.ta : a.row < b.row;
+        });
+        std::unordered_map<uint64_t, std::vector<std::pair<uint32_t, int32_t>>> eseq;  // key -> (O start, row)
+        auto same = [&](const ER& a, const ER& b) {  // values and xe offsets equal
+          if (a.key != b.key || !veq(a.row, b.row)) return false;
+          for (int32_t k = 0; k < len(a.row); ++k)
+            if (xoff(a.row, k, a.ta) != xoff(b.row, k, b.ta)) return false;
+          return true;
+        };
+        for (size_t a = 0; a < er.size();) {
+          size_t b = a + 1;
+          while (b < er.size() && er[b].ta == er[b - 1].ta + 1 && same(er[a], er[b])) ++b;
+          if (b - a >= static_cast<size_t>(kEdgeRun)) {
+            const int32_t rep = er[a].row;
+            lmax_all = std::max(lmax_all, len(rep));
+            const uint32_t vb = v_start(rep);
+            uint32_t ob = 0;
+            {
+              auto& bk = eseq[er[a].key];
+              bool found = false;
+              for (const auto& [st, r0] : bk) {
+                ER t{er[a].key, tof[col[ptr[r0]]], r0};
+                if (same(er[a], t)) {
+                  ob = st;
+                  found = true;
+                  break;
+                }
+              }
+              if (!found) {
+                s.O.resize((s.O.size() + 3) & ~size_t(3), 0);
+                ob = static_cast<uint32_t>(s.O.size());
+                for (int32_t k = 0; k < len(rep); ++k) s.O.push_back(xoff(rep, k, er[a].ta));
+                s.layout_bytes += 4 * static_cast<int64_t>(len(rep));
+                bk.push_back({ob, rep});
+              }
+            }
+            for (size_t q = a; q < b; q += 32) {
+              const int cnt = static_cast<int>(std::min<size_t>(32, b - q));
+              const uint32_t at = static_cast<uint32_t>(s.rlist.size());
+              for (int u = 0; u < cnt; ++u) {
+                s.rlist.push_back(er[q + u].row);
+                s.ginfo.push_back(static_cast<uint32_t>(er[q + u].ta));
+                claimed[er[q + u].row] = 1;
+              }
+              s.meta.push_back(PSliceMeta{at, vb, ob, pack(len(rep), cnt, false, false, 0, 0) | 1u << 31});
+              s.layout_bytes += 16 + 8 * static_cast<int64_t>(cnt);
+              ++s.n_faste;
+              s.fast_rows += cnt;
+            }
+          }
+          a = b;
+        }
+        if (s.n_faste > 0) {
+          s.G.assign(static_cast<size_t>(Wb) * T, 0);
+          for (size_t b2 = 0, t = 0; b2 < bstart.size(); ++b2)
+            if (blen[b2] == Wb) {
+              for (int32_t c = 0; c < Wb; ++c) s.G[static_cast<size_t>(c) * T + t] = bstart[b2] + c;
+              ++t;
+            }
+          s.layout_bytes += 20 * static_cast<int64_t>(s.G.size());  // gather list + xe written and read
+        }
+      }
+    }
+  }
   if (std::getenv("IG_TIMING"))
-    std::fprintf(stderr, "[psell base] %d x %d: smul %d sshift %d, %lld FASTAB slices\n", nr, nc, s.smul, s.sshift,
-                 static_cast<long long>(s.n_fastab));
+    std::fprintf(stderr, "[psell base] %d x %d: smul %d sshift %d, %lld FASTAB slices, %lld FASTE slices (xe %zu)\n", nr, nc,
+                 s.smul, s.sshift, static_cast<long long>(s.n_fastab), static_cast<long long>(s.n_faste), s.G.size());
   std::vector<int32_t> pending;
   for (size_t r = 0; r < nruns; ++r) {
     const int32_t r0 = run_start[r], r1 = run_start[r + 1];
@@ -943,7 +1099,11 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
     // table by the rows they cover; both read V[vbase ..] otherwise.
     std::unordered_map<uint32_t, std::pair<int64_t, int32_t>> use;  // vbase -> (rows, length)
     for (const PSliceMeta& m : s.meta)
-      if (m.pk & (1u << 17)) {
+      if (!(m.pk & (1u << 17)) && (m.pk >> 31)) {  // FASTE: one row per lane
+        auto& u = use[m.vbase];
+        u.first += static_cast<int64_t>((m.pk >> 11) & 0x3f);
+        u.second = static_cast<int32_t>(m.pk & kPMaxLen);
+      } else if (m.pk & (1u << 17)) {
         const int wv = static_cast<int>((m.pk >> 19) & 0x3f);  // 0 FAST, 1 FAST2, 2 FAST4
         auto& u = use[m.vbase];
         u.first += (wv == 5 ? 8 : wv == 2 ? 4 : wv == 1 || wv == 3 || wv == 4 ? 2 : 1) * static_cast<int64_t>((m.pk >> 11) & 0x3f);
@@ -963,7 +1123,13 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       s.tab_rows += rows;
     }
     for (PSliceMeta& m : s.meta)
-      if (m.pk & (1u << 17)) {
+      if (!(m.pk & (1u << 17)) && (m.pk >> 31)) {  // FASTE: table flag in bit 18
+        auto it = toff.find(m.vbase);
+        if (it != toff.end()) {
+          m.vbase = it->second;
+          m.pk |= 1u << 18;
+        }
+      } else if (m.pk & (1u << 17)) {
         auto it = toff.find(m.vbase);
         if (it != toff.end()) {
           m.vbase = it->second;
@@ -1008,6 +1174,9 @@ struct DevSell {
   PSell p{};
   std::shared_ptr<PValTab> ptab;  // constant-bank value table (zeros when unused)
   bool has_f4 = false;            // the pattern layout holds two-line slices
+  int32_t n_xe = 0;               // FASTE: size of the edge-compacted copy xe of the input vector
+  const int32_t* xgather = nullptr;
+  double* xe = nullptr;
   int64_t p_bytes = 0;  // HostPSell::layout_bytes
   int64_t n_fast = 0, n_general = 0;
   int64_t layout_matrix_bytes() const { return has_p ? p_bytes : 8 * explicit_vals + 4 * explicit_cols + 4 * int64_t(s.n_rows); }
@@ -1166,6 +1335,12 @@ struct ig_hier {
         d.p.seg = upload(hp.seg.data(), hp.seg.size());
         if (hp.useg.empty()) hp.useg.push_back(make_int4(0, 0, 0, 0));
         d.p.useg = upload(hp.useg.data(), hp.useg.size());
+        d.n_xe = static_cast<int32_t>(hp.G.size());
+        if (d.n_xe > 0) {
+          d.xgather = upload(hp.G.data(), hp.G.size());
+          d.xe = alloc<double>(hp.G.size());
+          d.p.xe = d.xe;
+        }
         d.p.V = upload(hp.V.data(), hp.V.size());
         d.p.O = upload(hp.O.data(), hp.O.size());
         d.p.dict_w = hp.dict_w;
@@ -1224,6 +1399,10 @@ struct ig_hier {
       const unsigned gp = static_cast<unsigned>(A.p.n_slices / (kPCta / 32));
       const size_t sm = psell_smem();
       const PValTab& tb = *A.ptab;
+      if (A.n_xe > 0) {  // FASTE slices read the edge-compacted copy of x
+        launch(k_xgather, static_cast<unsigned>((A.n_xe + kCta - 1) / kCta), kCta, 0, stream, A.n_xe, A.xgather, x, A.xe);
+        CK(cudaGetLastError());
+      }
       if (!A.has_f4 && !A.stream) {  // no two-line slices: the leaner instantiation
         if (mode == 0) launch(k_pspmv<0, false, false>, gp, kPCta, sm, stream, A.p, x, y, rsrc, s, tb);
         else launch(k_pspmv<1, false, false>, gp, kPCta, sm, stream, A.p, x, y, rsrc, s, tb);
@@ -2036,6 +2215,11 @@ int ig_set_option(int32_t option, int64_t value) {
     g_defaults.psell_rows4 = value != 0;
     return IG_OK;
   }
+  if (option == IG_OPT_PSELL_EDGE_ROWS) {
+    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: bad row count");
+    g_defaults.psell_edge_rows = static_cast<int32_t>(value);
+    return IG_OK;
+  }
   if (option == IG_OPT_PSELL_AB) {
     g_defaults.psell_ab = value != 0;
     return IG_OK;
@@ -2518,7 +2702,7 @@ int ig_debug_psell_stats(const ig_csr* a, int64_t* out, int32_t n_out) {
       if (count == 0) continue;
       const bool fast = m.pk & (1u << 17);
       const int wv = static_cast<int>((m.pk >> 19) & 0x3f);
-      const int cls = !fast ? 0 : wv == 0 ? 1 : wv == 1 || wv == 4 ? 2 : wv == 2 || wv == 5 ? 3 : 4;  // (FASTAB counted with FAST2)
+      const int cls = !fast ? ((m.pk >> 31) ? 1 : 0) : wv == 0 ? 1 : wv == 1 || wv == 4 ? 2 : wv == 2 || wv == 5 ? 3 : 4;  // (FASTE with FAST)  // (FASTAB counted with FAST2)
       ++out[cls];
       out[5 + cls] += count;
       ++out[10 + 4 * cls + (count - 1) / 8];

@@ -50,6 +50,10 @@ struct PSliceMeta {
   uint32_t pk;
 };
 
+#ifndef IG_GEN_UNROLL
+#define IG_GEN_UNROLL 1
+#endif
+constexpr int kGenUnroll = IG_GEN_UNROLL;  // GENERAL slices: 8-entry blocks in flight per loop trip
 constexpr int kPLenBits = 11;
 constexpr int kPMaxLen = (1 << kPLenBits) - 1;
 
@@ -66,6 +70,7 @@ struct PSell {
   int32_t smul, sshift;  // base(row) = (row * smul) >> sshift
   const int2* seg;       // FAST2 segment lists (first offset, length); length 0 ends a list
   const int4* useg;      // FAST4 union lists: header {D, n}, then {offset, length, value index A | -1, B | -1}
+  const double* xe;      // FASTE: edge-compacted copy of x (k_xgather), else null
 };
 
 template <bool STREAM>
@@ -669,6 +674,40 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
     for (; k < L; ++k) acc = acc + __ldg(vp + k) * __ldg(xr + __ldg(op + k));
     return lane < count ? row : -1;
   }
+  if (pk >> 31) {  // FASTE (warp-uniform): lane's row gen.x, anchor gen.y in xe; one value / offset sequence
+    const int row = static_cast<int>(gen.x);
+    const double* xr = A.xe + gen.y;
+    const bool tb = tab != nullptr && (pk & (1u << 18));
+    const int vo = static_cast<int>(mu.y);
+    const double2* vp2 = reinterpret_cast<const double2*>(A.V + mu.y);
+    const int4* op4 = reinterpret_cast<const int4*>(A.O + mu.z);
+    int k = 0;
+    for (; k + 8 <= L; k += 8) {
+      const int4 b0 = __ldg(op4 + (k >> 2)), b1 = __ldg(op4 + (k >> 2) + 1);
+      const double x0 = __ldg(xr + b0.x), x1 = __ldg(xr + b0.y), x2 = __ldg(xr + b0.z), x3 = __ldg(xr + b0.w);
+      const double x4 = __ldg(xr + b1.x), x5 = __ldg(xr + b1.y), x6 = __ldg(xr + b1.z), x7 = __ldg(xr + b1.w);
+      double v[8];
+      if (tb) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = tab->v[vo + k + u];
+      } else {
+        const double2 a0 = __ldg(vp2 + (k >> 1)), a1 = __ldg(vp2 + (k >> 1) + 1);
+        const double2 a2 = __ldg(vp2 + (k >> 1) + 2), a3 = __ldg(vp2 + (k >> 1) + 3);
+        v[0] = a0.x, v[1] = a0.y, v[2] = a1.x, v[3] = a1.y, v[4] = a2.x, v[5] = a2.y, v[6] = a3.x, v[7] = a3.y;
+      }
+      acc = acc + v[0] * x0;
+      acc = acc + v[1] * x1;
+      acc = acc + v[2] * x2;
+      acc = acc + v[3] * x3;
+      acc = acc + v[4] * x4;
+      acc = acc + v[5] * x5;
+      acc = acc + v[6] * x6;
+      acc = acc + v[7] * x7;
+    }
+    for (; k < L; ++k)
+      acc = acc + (tb ? tab->v[vo + k] : __ldg(A.V + mu.y + k)) * __ldg(xr + __ldg(A.O + mu.z + k));
+    return lane < count ? row : -1;
+  }
   const int row = static_cast<int>(gen.x);
   const uint32_t info = gen.y;
   const int len = static_cast<int>(info & kPMaxLen);
@@ -684,6 +723,7 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
   const int L8 = (L + 7) & ~7;
   const int lfull = (pk & (1u << 18)) ? (L & ~7) : 0;  // blocks every row fills
   int k = 0;
+#pragma unroll kGenUnroll
   for (; k < lfull; k += 8) {
     const double2 a0 = __ldg(vp2 + (k >> 1) * vs), a1 = __ldg(vp2 + ((k >> 1) + 1) * vs);
     const double2 a2 = __ldg(vp2 + ((k >> 1) + 2) * vs), a3 = __ldg(vp2 + ((k >> 1) + 3) * vs);
@@ -797,6 +837,16 @@ __global__ void __launch_bounds__(kPCta, IG_PSPMV_MINB * (256 / kPCta)) k_pspmv(
     y[rowx[0]] = (MODE == 0) ? accx[0] : rs[2] - accx[0];
     y[rowx[1]] = (MODE == 0) ? accx[1] : rs[3] - accx[1];
   }
+}
+
+// FASTE: the edge-compacted copy of the input vector, xe[i] = x[G[i]]
+// (ig_gpu.cu: to_psell), gathered ahead of the product that reads it.
+__global__ void __launch_bounds__(kCta) k_xgather(int n, const int32_t* __restrict__ G, const double* __restrict__ x,
+                                                 double* __restrict__ xe) {
+  const int i = blockIdx.x * kCta + threadIdx.x;
+  const int g = i < n ? __ldg(G + i) : 0;  // static: before the wait
+  pdl_entry();
+  if (i < n) xe[i] = x[g];
 }
 
 // p . Ap over the canonical 256-row chunks (kernels.cuh: last_cta_total), then

@@ -182,14 +182,17 @@ def d3_48_case():
     return build_case(configs.c4(res=48, levels=4))
 
 
-@pytest.mark.parametrize("lines2,multi,rows4", [(0, 0, 1), (1, 0, 0), (0, 1, 1), (1, 1, 0), (1, 1, 1)])
-def test_two_line_slices_bitwise(d3_48_case, lines2, multi, rows4):
+@pytest.mark.parametrize("lines2,multi,rows4,edge", [(0, 0, 1, 0), (1, 0, 0, 1), (0, 1, 1, 1), (1, 1, 0, 0), (1, 1, 1, 1),
+                                                     (1, 1, 1, 0)])
+def test_two_line_slices_bitwise(d3_48_case, lines2, multi, rows4, edge):
     """FAST4 slices (two x-lines per slice sharing their column runs,
     IG_OPT_PSELL_LINES2) and FAST2M slices (row pairs of up to four short runs
     per slice, per-lane column offsets and load parity, IG_OPT_PSELL_MULTI),
     pattern layout forced on every level: the oracle's bits for the level
     products and the PCG solve under every combination; rows4: the two-line
-    slices with four rows of each line per lane (FAST8, IG_OPT_PSELL_ROWS4)."""
+    slices with four rows of each line per lane (FAST8, IG_OPT_PSELL_ROWS4);
+    edge: the x-line end rows as FASTE slices over the edge-compacted copy of
+    x (IG_OPT_PSELL_EDGE_ROWS, k_xgather before every product)."""
     from paper_1903_10977_b200 import MgHierarchy, _ffi, pcg
     lib = _ffi.gpu()
     d3_case = d3_48_case
@@ -197,6 +200,7 @@ def test_two_line_slices_bitwise(d3_48_case, lines2, multi, rows4):
     lib.ig_set_option(_ffi.IG_OPT_PSELL_LINES2, lines2)
     lib.ig_set_option(_ffi.IG_OPT_PSELL_MULTI, multi)
     lib.ig_set_option(_ffi.IG_OPT_PSELL_ROWS4, rows4)
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_EDGE_ROWS, 1 if edge else 0)
     lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 0)
     try:
         h = MgHierarchy(d3_case)
@@ -204,6 +208,7 @@ def test_two_line_slices_bitwise(d3_48_case, lines2, multi, rows4):
         lib.ig_set_option(_ffi.IG_OPT_PSELL_LINES2, 1)
         lib.ig_set_option(_ffi.IG_OPT_PSELL_MULTI, 1)
         lib.ig_set_option(_ffi.IG_OPT_PSELL_ROWS4, 1)
+        lib.ig_set_option(_ffi.IG_OPT_PSELL_EDGE_ROWS, 100000)
         lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
     try:
         for l in range(1, h.levels()):
