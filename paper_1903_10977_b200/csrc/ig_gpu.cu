@@ -80,6 +80,9 @@ struct Opts {
   int psell_lines2 = 1;  // FAST4 slices (two x-lines per slice)
   int psell_multi = 1;   // FAST2M slices (row pairs of up to four short runs per slice)
   int psell_rows4 = 1;   // FAST8 slices (four rows of each of two x-lines per lane)
+  int32_t psell_rows4_rows = 1000000;  // ... for matrices with at least this many rows: below, a product is
+                                       // less than one wave of warps and bound by the slice's dependent chain
+                                       // (C4 level 4, 267k rows: 138.7 -> 122.5 us per V-cycle with FAST4 there)
   int32_t psell_edge_rows = 100000;  // FASTE slices (edge-compacted x) for square matrices with at least this many rows (0 = off)
   int psell_ab = 1;      // FASTAB slices (row pairs with one column list, two value sequences: prolongations)
   int gal_short = 1;     // prefetching SpGEMM for B rows <= 32 entries
@@ -779,7 +782,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       pairB[r] = static_cast<int32_t>(rb);
       pa0[r] = a0;
       // (FAST8 slices take whole groups of four rows per line; FAST4 pairs)
-      pa1[r] = a0 + ((a1 - a0) & (opt().psell_rows4 && a1 - a0 >= 32 ? ~3 : ~1));
+      pa1[r] = a0 + ((a1 - a0) & (opt().psell_rows4 && nr >= opt().psell_rows4_rows && a1 - a0 >= 32 ? ~3 : ~1));
       pD[r] = DD;
       is_b[rb] = 1;
       pairA[rb] = static_cast<int32_t>(r);
@@ -817,9 +820,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       }
     }
     const uint32_t st = static_cast<uint32_t>(s.useg.size());
-    int all5 = ent.empty() ? 0 : 1;  // every union run 5 long: the pipelined slice loop applies
-    for (const int4& e : ent) all5 = all5 && e.y == 5;
-    s.useg.push_back(make_int4(D, static_cast<int>(ent.size()), all5, 0));
+    s.useg.push_back(make_int4(D, static_cast<int>(ent.size()), 0, 0));
     s.useg.insert(s.useg.end(), ent.begin(), ent.end());
     s.layout_bytes += 16 * static_cast<int64_t>(ent.size() + 1);
     useg_of[{sg, D}] = st;
@@ -1066,7 +1067,7 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
       const uint32_t vb = v_start(r0);
       const uint32_t ug = union_start(r0, pD[r]);
       lmax_all = std::max(lmax_all, len(r0));
-      const bool rows4 = opt().psell_rows4 && a1 - a0 >= 32 && (a1 - a0) % 4 == 0;
+      const bool rows4 = opt().psell_rows4 && nr >= opt().psell_rows4_rows && a1 - a0 >= 32 && (a1 - a0) % 4 == 0;
       for (int32_t i = a0; i < a1;) {
         const int cnt = std::min(rows4 ? 128 : 64, a1 - i);
         s.meta.push_back(PSliceMeta{static_cast<uint32_t>(i), vb, ug,
@@ -2213,6 +2214,11 @@ int ig_set_option(int32_t option, int64_t value) {
   }
   if (option == IG_OPT_PSELL_ROWS4) {
     g_defaults.psell_rows4 = value != 0;
+    return IG_OK;
+  }
+  if (option == IG_OPT_PSELL_ROWS4_ROWS) {
+    if (value < 0 || value > INT32_MAX) return fail(IG_INVALID_ARGUMENT, "ig_set_option: bad row count");
+    g_defaults.psell_rows4_rows = static_cast<int32_t>(value);
     return IG_OK;
   }
   if (option == IG_OPT_PSELL_EDGE_ROWS) {

@@ -50,10 +50,6 @@ struct PSliceMeta {
   uint32_t pk;
 };
 
-#ifndef IG_GEN_UNROLL
-#define IG_GEN_UNROLL 1
-#endif
-constexpr int kGenUnroll = IG_GEN_UNROLL;  // GENERAL slices: 8-entry blocks in flight per loop trip
 constexpr int kPLenBits = 11;
 constexpr int kPMaxLen = (1 << kPLenBits) - 1;
 
@@ -368,71 +364,6 @@ __device__ __forceinline__ void fast4_slice(const double* __restrict__ x, const 
   }
 }
 
-// FAST4 slices whose union runs all have length 5 (the 3D p = 2 interior
-// stencil), software-pipelined: the x window of run u + 1 is in flight while
-// run u is summed -- one slice is ~30 dependent L2 round trips otherwise, and
-// its warp spends most of its life waiting (FAST4 alone: 36 % of the FP64
-// pipe).  Same loads, same products, same order.
-#ifndef IG_F4_PIPE
-#define IG_F4_PIPE 0
-#endif
-__device__ __forceinline__ void f4_window(const double* __restrict__ x, int a, int P, double* W) {
-  const double* xb = x + (a - P);
-  const double2* xb2 = reinterpret_cast<const double2*>(xb);
-  const double2 t0 = __ldg(xb2), t1 = __ldg(xb2 + 1), t2 = __ldg(xb2 + 2);
-  W[0] = t0.x;
-  W[1] = t0.y;
-  W[2] = t1.x;
-  W[3] = t1.y;
-  W[4] = t2.x;
-  W[5] = t2.y;
-  W[6] = P ? __ldg(xb + 6) : 0.0;  // x[a + 5]: never reads past it
-}
-template <int P, class VS>
-__device__ __forceinline__ void f4_sum5(const double* W, const VS& vs, int vA, int vB, double* acc) {
-  if (vA >= 0) {  // warp-uniform
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      const double v = vs(vA + j);
-      acc[0] = acc[0] + v * W[P + j];
-      acc[1] = acc[1] + v * W[P + j + 1];
-    }
-  }
-  if (vB >= 0) {
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      const double v = vs(vB + j);
-      acc[2] = acc[2] + v * W[P + j];
-      acc[3] = acc[3] + v * W[P + j + 1];
-    }
-  }
-}
-template <class VS>
-__device__ __forceinline__ void fast4_slice5(const double* __restrict__ x, const int4* __restrict__ ug, int n, int ra,
-                                            int p0, const VS& vs, double* acc) {
-  double Wa[7], Wb[7];
-  int4 ea = __ldg(ug), eb = ea;
-  int Pa = (p0 + ea.x) & 1, Pb = 0;
-  f4_window(x, ra + ea.x, Pa, Wa);
-  for (int u = 0; u < n; u += 2) {
-    if (u + 1 < n) {
-      eb = __ldg(ug + u + 1);
-      Pb = (p0 + eb.x) & 1;
-      f4_window(x, ra + eb.x, Pb, Wb);
-    }
-    if (Pa == 0) f4_sum5<0>(Wa, vs, ea.z, ea.w, acc);
-    else f4_sum5<1>(Wa, vs, ea.z, ea.w, acc);
-    if (u + 1 >= n) break;
-    if (u + 2 < n) {
-      ea = __ldg(ug + u + 2);
-      Pa = (p0 + ea.x) & 1;
-      f4_window(x, ra + ea.x, Pa, Wa);
-    }
-    if (Pb == 0) f4_sum5<0>(Wb, vs, eb.z, eb.w, acc);
-    else f4_sum5<1>(Wb, vs, eb.z, eb.w, acc);
-  }
-}
-
 // FAST8: as FAST4 with FOUR rows of each of the two x-lines per lane (rows
 // ra .. ra + 3 and ra + D .. ra + D + 3): one window of M + 3 values feeds 4 M
 // products per line -- 1.6 B of x per product through the L1 data pipe (the
@@ -533,9 +464,7 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
     const int p0 = static_cast<int>(mu.x) & 1;
     const int4 hd = __ldg(A.useg + mu.z);
     double a4[4] = {0.0, 0.0, 0.0, 0.0};
-    if (IG_F4_PIPE && hd.z && tab != nullptr && (pk >> 31))  // every run 5 long, values in the table
-      fast4_slice5(x, A.useg + mu.z + 1, hd.y, ra, p0, VTabl{tab, static_cast<int>(mu.y)}, a4);
-    else if (tab != nullptr && (pk >> 31))
+    if (tab != nullptr && (pk >> 31))
       fast4_slice(x, A.useg + mu.z + 1, hd.y, ra, p0, VTabl{tab, static_cast<int>(mu.y)}, a4);
     else
       fast4_slice(x, A.useg + mu.z + 1, hd.y, ra, p0, VGlob{A.V + mu.y}, a4);
@@ -723,7 +652,6 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
   const int L8 = (L + 7) & ~7;
   const int lfull = (pk & (1u << 18)) ? (L & ~7) : 0;  // blocks every row fills
   int k = 0;
-#pragma unroll kGenUnroll
   for (; k < lfull; k += 8) {
     const double2 a0 = __ldg(vp2 + (k >> 1) * vs), a1 = __ldg(vp2 + ((k >> 1) + 1) * vs);
     const double2 a2 = __ldg(vp2 + ((k >> 1) + 2) * vs), a3 = __ldg(vp2 + ((k >> 1) + 3) * vs);

@@ -200,6 +200,7 @@ def test_two_line_slices_bitwise(d3_48_case, lines2, multi, rows4, edge):
     lib.ig_set_option(_ffi.IG_OPT_PSELL_LINES2, lines2)
     lib.ig_set_option(_ffi.IG_OPT_PSELL_MULTI, multi)
     lib.ig_set_option(_ffi.IG_OPT_PSELL_ROWS4, rows4)
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_ROWS4_ROWS, 0)
     lib.ig_set_option(_ffi.IG_OPT_PSELL_EDGE_ROWS, 1 if edge else 0)
     lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 0)
     try:
@@ -208,6 +209,7 @@ def test_two_line_slices_bitwise(d3_48_case, lines2, multi, rows4, edge):
         lib.ig_set_option(_ffi.IG_OPT_PSELL_LINES2, 1)
         lib.ig_set_option(_ffi.IG_OPT_PSELL_MULTI, 1)
         lib.ig_set_option(_ffi.IG_OPT_PSELL_ROWS4, 1)
+        lib.ig_set_option(_ffi.IG_OPT_PSELL_ROWS4_ROWS, 1000000)
         lib.ig_set_option(_ffi.IG_OPT_PSELL_EDGE_ROWS, 100000)
         lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
     try:
