@@ -2542,6 +2542,7 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
         per_app = 2 + 2 * ne - 1;
       }
       kv += 2 * per_app + 4 + (l == n_levels - 1 && !L.ms ? 1 : 0);  // finest: + r . z pass
+      kv += L.A.n_xe > 0 ? 2 : 0;  // k_xgather ahead of the two residual products (FASTE slices)
       I.explicit_vals_A[l] = L.A.explicit_vals;
       I.explicit_cols_A[l] = L.A.explicit_cols;
     }
@@ -2555,7 +2556,7 @@ int ig_hier_create(const ig_level* levels, int32_t n_levels, const ig_coarse* co
     I.explicit_cols_A[n_levels - 1] = F.A.explicit_cols;
     I.bytes_pcg_iter = vc + I.bytes_spmv_finest + 80 * static_cast<int64_t>(nf);
     I.kernels_vcycle = kv;
-    I.kernels_pcg_iter = kv + 3 + (F.A.has_p ? 1 : 0);  // + k_pap after a pattern-SELL A p
+    I.kernels_pcg_iter = kv + 3 + (F.A.has_p ? 1 : 0) + (F.A.n_xe > 0 ? 1 : 0);  // + k_pap after a pattern-SELL A p, + k_xgather
     CK(cudaDeviceSynchronize());
     *out = h.release();
     return IG_OK;

@@ -12,8 +12,8 @@ python bench.py --workload c5 --smoother ms --no-device-setup > $O/b_c5_ms.json 
 python bench.py --impl reference > $O/b_ref_c4.json 2> $O/b_ref_c4.err
 python profiles/level_costs.py c4 --json $O/level_costs_c4.json > $O/level_costs_c4.log 2>&1
 python profiles/spmv_modes.py c4 > $O/spmv_modes_c4.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c4.csv \
-  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-device-setup > $O/ncu_launch.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $O/launches_c4.csv \
+  python bench.py --steps 1 --warmup 1 --no-graph --no-cpu-baseline --no-device-setup --no-fast-mode > $O/ncu_launch.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_pspmv -s 1 -c 1 -f -o $O/pspmv_full \
   python profiles/profile_c4.py spmv > $O/ncu_pspmv.log 2>&1
 ncu -i $O/pspmv_full.ncu-rep --page raw --csv > $O/pspmv_raw.csv 2>&1
