@@ -1446,10 +1446,10 @@ struct ig_hier {
   void prolong(const Level& l, const double* xc, double* x, PcgState* s) {
     const unsigned g = grid_of(l.P.s.n_rows);
     if (l.P.has_p) {
-      const unsigned gp = static_cast<unsigned>(l.P.p.n_slices / (kCta / 32));
+      const unsigned gp = static_cast<unsigned>(l.P.p.n_slices / (kPCta / 32));
       const size_t sm = psell_smem();
-      if (l.P.stream) launch(k_pprolong<true>, gp, kCta, sm, stream, l.P.p, xc, l.cor, x, s, *l.P.ptab);
-      else launch(k_pprolong<false>, gp, kCta, sm, stream, l.P.p, xc, l.cor, x, s, *l.P.ptab);
+      if (l.P.stream) launch(k_pprolong<true>, gp, kPCta, sm, stream, l.P.p, xc, l.cor, x, s, *l.P.ptab);
+      else launch(k_pprolong<false>, gp, kPCta, sm, stream, l.P.p, xc, l.cor, x, s, *l.P.ptab);
       CK(cudaGetLastError());
       return;
     }

@@ -232,9 +232,17 @@ __device__ __forceinline__ void fast2m_slice(const double* __restrict__ x, const
                                             int n, int ra, int pid, const VS& vs, double& acc0, double& acc1) {
   const int* ob = reinterpret_cast<const int*>(tb + 2) + pid;
   int vo = 0;
+  // (The next run's length and offset are loaded a run ahead: the offset
+  // table is per slice -- an L2 round trip that would otherwise sit in front
+  // of every run's window loads.)
+  int mn = n > 0 ? __ldg(sg).y : 0, on = n > 0 ? __ldg(ob) : 0;
   for (int u = 0; u < n; ++u) {
-    const int m = __ldg(sg + u).y;  // warp-uniform
-    const int a = ra + __ldg(ob + 4 * u);
+    const int m = mn;  // warp-uniform
+    const int a = ra + on;
+    if (u + 1 < n) {
+      mn = __ldg(sg + u + 1).y;
+      on = __ldg(ob + 4 * (u + 1));
+    }
     switch (m) {
       case 1: fast2m_segment<1>(x, a, vs, vo, acc0, acc1); break;
       case 2: fast2m_segment<2>(x, a, vs, vo, acc0, acc1); break;
@@ -355,8 +363,10 @@ __device__ __forceinline__ void fast4_dispatch(const double* __restrict__ x, int
 template <class VS>
 __device__ __forceinline__ void fast4_slice(const double* __restrict__ x, const int4* __restrict__ ug, int n, int ra,
                                            int p0, const VS& vs, double* acc) {
+  int4 en = __ldg(ug);
   for (int u = 0; u < n; ++u) {
-    const int4 e = __ldg(ug + u);
+    const int4 e = en;
+    if (u + 1 < n) en = __ldg(ug + u + 1);  // a run ahead
     if (((p0 + e.x) & 1) == 0)
       fast4_dispatch<0>(x, ra + e.x, e.y, vs, e.z, e.w, acc[0], acc[1], acc[2], acc[3]);
     else
@@ -420,8 +430,10 @@ __device__ __forceinline__ void fast8_dispatch(const double* __restrict__ x, int
 template <class VS>
 __device__ __forceinline__ void fast8_slice(const double* __restrict__ x, const int4* __restrict__ ug, int n, int ra,
                                            int p0, const VS& vs, double* acc) {
+  int4 en = __ldg(ug);
   for (int u = 0; u < n; ++u) {
-    const int4 e = __ldg(ug + u);
+    const int4 e = en;
+    if (u + 1 < n) en = __ldg(ug + u + 1);  // a run ahead
     if (((p0 + e.x) & 1) == 0)
       fast8_dispatch<0>(x, ra + e.x, e.y, vs, e.z, e.w, acc);
     else
@@ -799,9 +811,9 @@ __global__ void __launch_bounds__(kCta) k_pap(int n, const double* __restrict__ 
 
 // Prolongation fused with the correction (k_prolong on the pattern layout).
 template <bool STREAM>
-__global__ void __launch_bounds__(kCta, IG_PPROLONG_MINB) k_pprolong(PSell P, const double* __restrict__ xc, double* cor, double* x,
+__global__ void __launch_bounds__(kPCta, IG_PPROLONG_MINB * (256 / kPCta)) k_pprolong(PSell P, const double* __restrict__ xc, double* cor, double* x,
                                                   const PcgState* st, const __grid_constant__ PValTab tab) {
-  const int slice = blockIdx.x * (kCta / 32) + (threadIdx.x >> 5);
+  const int slice = blockIdx.x * (kPCta / 32) + (threadIdx.x >> 5);
   const uint4 mu = __ldg(reinterpret_cast<const uint4*>(P.meta + slice));  // static: before the wait
   // (Two-line slices exist only in square matrices: never in P.)
   int pr[4];

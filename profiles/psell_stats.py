@@ -18,6 +18,9 @@ def load(wl, res, which="A"):
     cfg = configs.c4(res=res, levels=configs.c4_levels(res)) if wl == "c4" else configs.CONFIGS[wl]()
     case = build_case(cfg)
     A = case.A.to_scipy().tocsr()
+    if which.startswith("L"):  # level operator A_l, e.g. L4
+        A = case.level_A(int(which[1:])).to_scipy().tocsr()
+        A.sort_indices()
     if which in ("P", "R"):
         from paper_1903_10977_b200 import SpMat
         R = SpMat.from_c(case._lv[case.n_levels - 1].R, case).to_scipy().tocsr()
@@ -39,7 +42,7 @@ def main():
     lib = _ffi.gpu()
     a = _ffi.ig_csr()
     a.n_rows = len(ptr) - 1
-    a.n_cols = int(col.max()) + 1 if which != "A" else a.n_rows
+    a.n_cols = int(col.max()) + 1 if which in ("P", "R") else a.n_rows
     a.nnz = len(col)
     a.row_ptr = ptr.ctypes.data_as(C.POINTER(C.c_int32))
     a.col_idx = col.ctypes.data_as(C.POINTER(C.c_int32))

@@ -1,6 +1,6 @@
 """Finest-level pattern-SELL products timed alone (CUDA events on the library
 stream): A x, r - A x (distinct and in-place), restriction, prolongation.
-  python profiles/spmv_modes.py [workload]"""
+  python profiles/spmv_modes.py [workload] [level]"""
 import ctypes as C
 import os
 import sys
@@ -19,7 +19,7 @@ def main():
           "c5": configs.c5}
     case = build_case(mk[wl]())
     h = MgHierarchy(case)
-    L = h.info.n_levels
+    L = int(sys.argv[2]) + 1 if len(sys.argv) > 2 else h.info.n_levels  # optional level (default: finest)
     n, nc = h.info.n[L - 1], h.info.n[L - 2]
     vp = C.c_void_p
     g = torch.Generator(device="cuda").manual_seed(1)
@@ -41,7 +41,7 @@ def main():
         return e0.elapsed_time(e1) / reps * 1e3
 
     sp = lib.ig_level_spmv_device
-    print(f"{wl} finest level n={n}")
+    print(f"{wl} level {L - 1} n={n}")
     print(f"  A x            {timeit(lambda: sp(h.handle, L - 1, vp(x.data_ptr()), vp(y.data_ptr()), 0)):7.1f} us")
     print(f"  r - A x        {timeit(lambda: sp(h.handle, L - 1, vp(x.data_ptr()), vp(y.data_ptr()), 1)):7.1f} us")
     print(f"  restriction    {timeit(lambda: sp(h.handle, L - 1, vp(x.data_ptr()), vp(yc.data_ptr()), 2)):7.1f} us")
