@@ -413,6 +413,55 @@ __device__ __forceinline__ void fast8_segment(const double* __restrict__ x, int 
     }
   }
 }
+// FAST8, column runs of 5 (the 3D p = 2 stencil): lanes are 32 bytes apart,
+// so the window is read with 32-byte loads (sm_100 LDG.256: a warp request is
+// 1 KB of consecutive bytes) from the 32-byte boundary below -- 2 requests
+// when the run starts on it, else 2 + the 1-3 remaining values -- instead of
+// 4-5 16-byte requests that each touch all of the warp's 8-9 cache lines.
+// Q = the run's first element modulo 4 (warp-uniform).  Never reads past
+// x[a + 7], the last operand.
+#ifndef IG_F8_LD256
+#define IG_F8_LD256 1
+#endif
+__device__ __forceinline__ void ldg256(const double* p, double* v) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+template <int Q, class VS>
+__device__ __forceinline__ void fast8_segment5(const double* __restrict__ x, int a, const VS& vs, int vA, int vB,
+                                               double* acc) {
+  const double* xb = x + (a - Q);
+  double X[12];
+  ldg256(xb, X);
+  ldg256(xb + 4, X + 4);
+  if (Q == 1) {
+    X[8] = __ldg(xb + 8);
+  } else if (Q == 2) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(xb + 8));
+    X[8] = t.x;
+    X[9] = t.y;
+  } else if (Q == 3) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(xb + 8));
+    X[8] = t.x;
+    X[9] = t.y;
+    X[10] = __ldg(xb + 10);
+  }
+  if (vA >= 0) {  // warp-uniform
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const double v = vs(vA + j);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = acc[r] + v * X[Q + j + r];
+    }
+  }
+  if (vB >= 0) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const double v = vs(vB + j);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[4 + r] = acc[4 + r] + v * X[Q + j + r];
+    }
+  }
+}
 template <int P, class VS>
 __device__ __forceinline__ void fast8_dispatch(const double* __restrict__ x, int a, int m, const VS& vs, int vA, int vB,
                                                double* acc) {
@@ -429,15 +478,26 @@ __device__ __forceinline__ void fast8_dispatch(const double* __restrict__ x, int
 }
 template <class VS>
 __device__ __forceinline__ void fast8_slice(const double* __restrict__ x, const int4* __restrict__ ug, int n, int ra,
-                                           int p0, const VS& vs, double* acc) {
+                                           int a0, const VS& vs, double* acc) {
+  const int p0 = a0 & 1;
   int4 en = __ldg(ug);
+  const int q0 = static_cast<int>((reinterpret_cast<uintptr_t>(x) >> 3) & 3) + a0;  // warp-uniform
   for (int u = 0; u < n; ++u) {
     const int4 e = en;
     if (u + 1 < n) en = __ldg(ug + u + 1);  // a run ahead
-    if (((p0 + e.x) & 1) == 0)
+    if (IG_F8_LD256 && e.y == 5) {
+      // (from the address of the slice's first row, so any 8-byte aligned x works; lanes differ by 32 bytes)
+      switch ((q0 + e.x) & 3) {
+        case 0: fast8_segment5<0>(x, ra + e.x, vs, e.z, e.w, acc); break;
+        case 1: fast8_segment5<1>(x, ra + e.x, vs, e.z, e.w, acc); break;
+        case 2: fast8_segment5<2>(x, ra + e.x, vs, e.z, e.w, acc); break;
+        default: fast8_segment5<3>(x, ra + e.x, vs, e.z, e.w, acc); break;
+      }
+    } else if (((p0 + e.x) & 1) == 0) {
       fast8_dispatch<0>(x, ra + e.x, e.y, vs, e.z, e.w, acc);
-    else
+    } else {
       fast8_dispatch<1>(x, ra + e.x, e.y, vs, e.z, e.w, acc);
+    }
   }
 }
 
@@ -737,9 +797,9 @@ __global__ void __launch_bounds__(kPCta, IG_PSPMV_MINB * (256 / kPCta)) k_pspmv(
     const int ra = static_cast<int>(mu.x) + 4 * min(lane, count - 1);
     double a8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (mu.w >> 31)
-      fast8_slice(x, A.useg + mu.z + 1, hd.y, ra, static_cast<int>(mu.x) & 1, VTabl{&tab, static_cast<int>(mu.y)}, a8);
+      fast8_slice(x, A.useg + mu.z + 1, hd.y, ra, static_cast<int>(mu.x), VTabl{&tab, static_cast<int>(mu.y)}, a8);
     else
-      fast8_slice(x, A.useg + mu.z + 1, hd.y, ra, static_cast<int>(mu.x) & 1, VGlob{A.V + mu.y}, a8);
+      fast8_slice(x, A.useg + mu.z + 1, hd.y, ra, static_cast<int>(mu.x), VGlob{A.V + mu.y}, a8);
     if (lane >= count) return;
     if (MODE == 1) {  // (the eight residual sources together, after the chain: no registers held across it)
       double rs8[8];
