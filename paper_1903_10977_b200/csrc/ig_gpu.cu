@@ -72,7 +72,10 @@ struct Opts {
   int red_ctas = 8;      // CTAs per SM of the canonical-reduction kernels (profiles/option_sweep.py 13)
   int use_psell = 1;     // pattern SELL above small_rows
   int psell_pairs = 1;   // FAST slices with two rows per lane (x reuse across a column run)
-  int32_t psell_pairs_rows = 0;  // ... for matrices with at least this many rows
+  int32_t psell_pairs_rows = 100000;  // ... for matrices with at least this many rows (below, one row per lane:
+                                      // a 38k-row level is a fraction of a wave of warps and the pair slices'
+                                      // longer dependent chains cost more than their x reuse saves -- C4 level 3
+                                      // 58.0 -> 47.0 us per V-cycle; level 4, 267k rows, 120 -> 149 us without pairs)
   // Occupancy cap of the pattern-SELL kernels (CTAs per SM, 0 = registers
   // decide), applied as unused dynamic shared memory.
   int psell_ctas = 0;

@@ -23,9 +23,11 @@ def layout(request):
     small, psell = LAYOUTS[request.param]
     lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, small)
     lib.ig_set_option(_ffi.IG_OPT_PSELL, psell)
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_PAIRS_ROWS, 0)  # pair / two-line / multi-piece slices on the small cases too
     yield request.param
     lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
     lib.ig_set_option(_ffi.IG_OPT_PSELL, 1)
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_PAIRS_ROWS, 100000)
 
 
 @pytest.fixture(scope="module")
@@ -69,10 +71,12 @@ def test_pattern_sell_nonfinite_and_signed_zero(star_case):
     from paper_1903_10977_b200 import MgHierarchy, _ffi
     lib = _ffi.gpu()
     lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 0)
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_PAIRS_ROWS, 0)
     try:
         h = MgHierarchy(star_case)
     finally:
         lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
+        lib.ig_set_option(_ffi.IG_OPT_PSELL_PAIRS_ROWS, 100000)
     lv = star_case.levels_c()
     try:
         l = h.levels() - 1
@@ -97,10 +101,12 @@ def test_breakdown_through_pattern_sell():
     from paper_1903_10977_b200 import Breakdown, MgHierarchy, _ffi, pcg
     lib = _ffi.gpu()
     lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 0)
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_PAIRS_ROWS, 0)
     try:
         h = MgHierarchy(orc.Synthetic(np.diag([1.0, -1.0])))
     finally:
         lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
+        lib.ig_set_option(_ffi.IG_OPT_PSELL_PAIRS_ROWS, 100000)
     try:
         with pytest.raises(Breakdown) as e:
             pcg(h.A, np.array([0.0, 1.0]), h)
@@ -124,12 +130,14 @@ def test_pair_item_prolongation_bitwise(request, case_name, ab, ctab):
     lib.ig_set_option(_ffi.IG_OPT_PSELL_AB, ab)
     lib.ig_set_option(_ffi.IG_OPT_PSELL_CTAB, ctab)
     lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 0)
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_PAIRS_ROWS, 0)
     try:
         h = MgHierarchy(case)
     finally:
         lib.ig_set_option(_ffi.IG_OPT_PSELL_AB, 1)
         lib.ig_set_option(_ffi.IG_OPT_PSELL_CTAB, 1)
         lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
+        lib.ig_set_option(_ffi.IG_OPT_PSELL_PAIRS_ROWS, 100000)
     try:
         for l in range(1, h.levels()):
             A, R = h.level(l)
@@ -155,11 +163,13 @@ def test_constant_value_table_bitwise(ctab):
     case = build_case(configs.c5(base=64, levels=4))
     lib.ig_set_option(_ffi.IG_OPT_PSELL_CTAB, ctab)
     lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 0)
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_PAIRS_ROWS, 0)
     try:
         h = MgHierarchy(case)
     finally:
         lib.ig_set_option(_ffi.IG_OPT_PSELL_CTAB, 1)
         lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
+        lib.ig_set_option(_ffi.IG_OPT_PSELL_PAIRS_ROWS, 100000)
     lv = case.levels_c()
     try:
         for l in range(1, h.levels()):
@@ -203,6 +213,7 @@ def test_two_line_slices_bitwise(d3_48_case, lines2, multi, rows4, edge):
     lib.ig_set_option(_ffi.IG_OPT_PSELL_ROWS4_ROWS, 0)
     lib.ig_set_option(_ffi.IG_OPT_PSELL_EDGE_ROWS, 1 if edge else 0)
     lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 0)
+    lib.ig_set_option(_ffi.IG_OPT_PSELL_PAIRS_ROWS, 0)
     try:
         h = MgHierarchy(d3_case)
     finally:
@@ -212,6 +223,7 @@ def test_two_line_slices_bitwise(d3_48_case, lines2, multi, rows4, edge):
         lib.ig_set_option(_ffi.IG_OPT_PSELL_ROWS4_ROWS, 1000000)
         lib.ig_set_option(_ffi.IG_OPT_PSELL_EDGE_ROWS, 100000)
         lib.ig_set_option(_ffi.IG_OPT_SMALL_ROWS, 12000)
+        lib.ig_set_option(_ffi.IG_OPT_PSELL_PAIRS_ROWS, 100000)
     try:
         for l in range(1, h.levels()):
             A, _ = h.level(l)
