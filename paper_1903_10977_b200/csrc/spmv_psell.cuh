@@ -724,10 +724,22 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
   const int L8 = (L + 7) & ~7;
   const int lfull = (pk & (1u << 18)) ? (L & ~7) : 0;  // blocks every row fills
   int k = 0;
+  // (Each block's offsets are loaded a block ahead: offsets -> gathers is two
+  // dependent round trips per block otherwise, and on the levels that are a
+  // fraction of a wave of warps the slice's chain is the product's time.)
+  int4 nb0 = make_int4(0, 0, 0, 0), nb1 = nb0;
+  if (L8 > 0) {
+    nb0 = ld_off4<STREAM>(op4);
+    nb1 = ld_off4<STREAM>(op4 + wo);
+  }
   for (; k < lfull; k += 8) {
     const double2 a0 = __ldg(vp2 + (k >> 1) * vs), a1 = __ldg(vp2 + ((k >> 1) + 1) * vs);
     const double2 a2 = __ldg(vp2 + ((k >> 1) + 2) * vs), a3 = __ldg(vp2 + ((k >> 1) + 3) * vs);
-    const int4 b0 = ld_off4<STREAM>(op4 + (k >> 2) * wo), b1 = ld_off4<STREAM>(op4 + ((k >> 2) + 1) * wo);
+    const int4 b0 = nb0, b1 = nb1;
+    if (k + 8 < L8) {
+      nb0 = ld_off4<STREAM>(op4 + ((k + 8) >> 2) * wo);
+      nb1 = ld_off4<STREAM>(op4 + (((k + 8) >> 2) + 1) * wo);
+    }
     const double x0 = __ldg(xr + b0.x), x1 = __ldg(xr + b0.y), x2 = __ldg(xr + b0.z), x3 = __ldg(xr + b0.w);
     const double x4 = __ldg(xr + b1.x), x5 = __ldg(xr + b1.y), x6 = __ldg(xr + b1.z), x7 = __ldg(xr + b1.w);
     acc = acc + a0.x * x0;
@@ -742,7 +754,11 @@ __device__ __forceinline__ int psell_slice(const PSell& A, const uint4 mu, const
   for (; k < L8; k += 8) {
     const double2 a0 = __ldg(vp2 + (k >> 1) * vs), a1 = __ldg(vp2 + ((k >> 1) + 1) * vs);
     const double2 a2 = __ldg(vp2 + ((k >> 1) + 2) * vs), a3 = __ldg(vp2 + ((k >> 1) + 3) * vs);
-    const int4 b0 = ld_off4<STREAM>(op4 + (k >> 2) * wo), b1 = ld_off4<STREAM>(op4 + ((k >> 2) + 1) * wo);
+    const int4 b0 = nb0, b1 = nb1;
+    if (k + 8 < L8) {
+      nb0 = ld_off4<STREAM>(op4 + ((k + 8) >> 2) * wo);
+      nb1 = ld_off4<STREAM>(op4 + (((k + 8) >> 2) + 1) * wo);
+    }
     const double xv[8] = {__ldg(xr + b0.x), __ldg(xr + b0.y), __ldg(xr + b0.z), __ldg(xr + b0.w),
                           __ldg(xr + b1.x), __ldg(xr + b1.y), __ldg(xr + b1.z), __ldg(xr + b1.w)};
     const double av[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
