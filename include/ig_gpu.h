@@ -293,6 +293,11 @@ int ig_richardson(ig_hier *h, const double *b, double tol, int32_t maxit, double
 /* Host-only (no device work): slice statistics of the pattern-SELL layout the
  * library would build for `a` (out: >= 32 entries; see csrc/ig_gpu.cu). */
 int ig_debug_psell_stats(const ig_csr *a, int64_t *out, int32_t n_out);
+/* Host-only: y = A x through that layout, interpreted on the CPU with the
+ * kernels' index arithmetic and summation order, every index bounds-checked
+ * (a layout validation for the tests: each row exactly once, no load outside
+ * its array; the result equals the serial CSR row sums bit for bit). */
+int ig_debug_psell_apply(const ig_csr *a, const double *x, double *y);
 /* Debug: run one V-cycle with direct launches and an event after every step
  * (smoother, residual, restriction, prolongation, coarse solve); writes the
  * elapsed ms per step, its level and a label (label_len bytes each). */

@@ -1153,6 +1153,212 @@ bool to_psell(int32_t nr, int32_t nc, const int32_t* ptr, const int32_t* col, co
   return true;
 }
 
+// Host interpreter of the pattern-SELL layout: y = A x slice by slice with
+// the SAME index arithmetic, window extents and summation order as
+// spmv_psell.cuh (k_pspmv / psell_slice), every x / xe / table / pool index
+// bounds-checked.  Test infrastructure (ig_debug_psell_apply): it validates
+// the layout builder on the CPU -- each row computed exactly once, no load
+// outside its array (compute-sanitizer is not available on the GPU pool) --
+// and its results equal the serial CSR row sums bit for bit.
+bool psell_apply_host(const HostPSell& s, int32_t nr, int32_t nc, const double* x, double* y, std::string& err) {
+  std::vector<uint8_t> done(static_cast<size_t>(nr), 0);
+  std::vector<double> xe(s.G.size(), 0.0);
+  for (size_t i = 0; i < s.G.size(); ++i) {
+    if (s.G[i] < 0 || s.G[i] >= nc) return err = "xgather index out of range", false;
+    xe[i] = x[s.G[i]];
+  }
+  auto fail_at = [&](size_t slice, const char* what) {
+    err = std::string("slice ") + std::to_string(slice) + ": " + what;
+    return false;
+  };
+  bool ok = true;
+  const char* why = "";
+  auto X = [&](int64_t i) -> double {
+    if (i < 0 || i >= nc) {
+      ok = false;
+      why = "x index out of range";
+      return 0.0;
+    }
+    return x[i];
+  };
+  auto Vv = [&](int64_t i) -> double {
+    if (i < 0 || i >= static_cast<int64_t>(s.V.size())) {
+      ok = false;
+      why = "V index out of range";
+      return 0.0;
+    }
+    return s.V[static_cast<size_t>(i)];
+  };
+  auto Tv = [&](int64_t i) -> double {
+    if (i < 0 || i >= static_cast<int64_t>(s.tab.size())) {
+      ok = false;
+      why = "value table index out of range";
+      return 0.0;
+    }
+    return s.tab[static_cast<size_t>(i)];
+  };
+  auto Ov = [&](int64_t i) -> int32_t {
+    if (i < 0 || i >= static_cast<int64_t>(s.O.size())) {
+      ok = false;
+      why = "O index out of range";
+      return 0;
+    }
+    return s.O[static_cast<size_t>(i)];
+  };
+  auto put = [&](int64_t row, double v) {
+    if (row < 0 || row >= nr) {
+      ok = false;
+      why = "row out of range";
+      return;
+    }
+    if (done[row]) {
+      ok = false;
+      why = "row computed twice";
+      return;
+    }
+    done[row] = 1;
+    y[row] = v;
+  };
+  auto base = [&](int64_t row) { return (row * s.smul) >> s.sshift; };
+  for (size_t sl = 0; sl < s.meta.size() && ok; ++sl) {
+    const PSliceMeta& m = s.meta[sl];
+    const uint32_t pk = m.pk;
+    const int count = static_cast<int>((pk >> 11) & 0x3f);
+    if (count == 0) continue;
+    const int L = static_cast<int>(pk & kPMaxLen);
+    const bool fast = pk & (1u << 17);
+    const int wv = static_cast<int>((pk >> 19) & 0x3f), wo = static_cast<int>((pk >> 25) & 0x3f);
+    const bool tabv = fast && (pk >> 31);
+    auto val = [&](int64_t j) { return tabv ? Tv(m.vbase + j) : Vv(m.vbase + j); };
+    for (int lane = 0; lane < count && ok; ++lane) {
+      if (fast && (wv == 2 || wv == 5)) {  // FAST4 / FAST8: R rows of each of two lines
+        const int R = wv == 5 ? 4 : 2;
+        if (m.obase + 1 > s.useg.size()) return fail_at(sl, "useg header out of range");
+        const int4 hd = s.useg[m.obase];
+        if (m.obase + 1 + static_cast<size_t>(hd.y) > s.useg.size()) return fail_at(sl, "useg list out of range");
+        const int64_t ra = static_cast<int64_t>(m.a) + R * lane;
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int u = 0; u < hd.y; ++u) {
+          const int4 e = s.useg[m.obase + 1 + u];
+          const int64_t a = ra + e.x;
+          const int M = e.y;
+          if (wv == 5 && M == 5) {  // 32-byte window loads from the 32-byte boundary below (x 32-byte aligned at 0)
+            const int Q = static_cast<int>(a & 3);
+            X(a - Q);
+            X(a + M + 2);
+          } else {
+            X(a - (a & 1));
+            X(a + M + R - 2);
+          }
+          for (int line = 0; line < 2; ++line) {
+            const int vi = line == 0 ? e.z : e.w;
+            if (vi < 0) continue;
+            for (int j = 0; j < M; ++j)
+              for (int r = 0; r < R; ++r) acc[line * R + r] = acc[line * R + r] + val(vi + j) * X(a + j + r);
+          }
+        }
+        for (int r = 0; r < R; ++r) {
+          put(ra + r, acc[r]);
+          put(ra + hd.x + r, acc[R + r]);
+        }
+      } else if (fast && wv == 3) {  // FAST2M
+        if (m.obase + 2 > s.useg.size()) return fail_at(sl, "FAST2M table out of range");
+        const int4 R4 = s.useg[m.obase], hd = s.useg[m.obase + 1];
+        if (m.obase + 2 + static_cast<size_t>(hd.w) > s.useg.size()) return fail_at(sl, "FAST2M offsets out of range");
+        const int s1 = hd.x & 0xff, s2 = (hd.x >> 8) & 0xff, s3 = (hd.x >> 16) & 0xff;
+        const int pid = (lane >= s1) + (lane >= s2) + (lane >= s3);
+        const int st = pid == 0 ? 0 : pid == 1 ? s1 : pid == 2 ? s2 : s3;
+        const int en = std::min(count, pid == 0 ? s1 : pid == 1 ? s2 : pid == 2 ? s3 : 64);
+        const int64_t ra = (&R4.x)[pid] + 2 * (lane - st);
+        const bool odd = ((hd.y >> pid) & 1) && lane == en - 1;
+        double a0 = 0.0, a1 = 0.0;
+        int vo = 0;
+        for (int u = 0; u < hd.w; ++u) {
+          if (static_cast<size_t>(hd.z) + u >= s.seg.size()) return fail_at(sl, "segment list out of range");
+          const int M = s.seg[hd.z + u].y;
+          const int64_t a = ra + (&s.useg[m.obase + 2 + u].x)[pid];
+          X(a - (a & 1));
+          X(a + M);
+          for (int j = 0; j < M; ++j) {
+            const double v = val(vo + j);
+            a0 = a0 + v * X(a + j);
+            a1 = a1 + v * X(a + j + 1);
+          }
+          vo += M;
+        }
+        put(ra, a0);
+        if (!odd) put(ra + 1, a1);
+      } else if (fast && wv == 1) {  // FAST2
+        const int64_t ra = static_cast<int64_t>(m.a) + 2 * lane;
+        double a0 = 0.0, a1 = 0.0;
+        int vo = 0;
+        for (size_t q = m.obase;; ++q) {
+          if (q >= s.seg.size()) return fail_at(sl, "segment list out of range");
+          const int2 e = s.seg[q];
+          if (e.y == 0) break;
+          const int64_t a = ra + e.x;
+          X(a - (a & 1));
+          X(a + e.y);
+          for (int j = 0; j < e.y; ++j) {
+            const double v = val(vo + j);
+            a0 = a0 + v * X(a + j);
+            a1 = a1 + v * X(a + j + 1);
+          }
+          vo += e.y;
+        }
+        put(ra, a0);
+        put(ra + 1, a1);
+      } else if (fast && wv == 4) {  // FASTAB
+        const int64_t ra = static_cast<int64_t>(m.a) + 2 * lane;
+        double a0 = 0.0, a1 = 0.0;
+        for (int k = 0; k < L; ++k) {
+          const double xk = X(base(ra) + Ov(m.obase + k));
+          a0 = a0 + val(2 * k) * xk;
+          a1 = a1 + val(2 * k + 1) * xk;
+        }
+        put(ra, a0);
+        put(ra + 1, a1);
+      } else if (fast) {  // FAST
+        const int64_t row = static_cast<int64_t>(m.a) + lane;
+        double acc = 0.0;
+        for (int k = 0; k < L; ++k) acc = acc + val(k) * X(base(row) + Ov(m.obase + k));
+        put(row, acc);
+      } else if (pk >> 31) {  // FASTE
+        if (m.a + static_cast<size_t>(lane) >= s.rlist.size()) return fail_at(sl, "row list out of range");
+        const int64_t row = s.rlist[m.a + lane], ta = s.ginfo[m.a + lane];
+        const bool tb = pk & (1u << 18);
+        double acc = 0.0;
+        for (int k = 0; k < L; ++k) {
+          const int64_t xi = ta + Ov(m.obase + k);
+          if (xi < 0 || xi >= static_cast<int64_t>(xe.size())) return fail_at(sl, "xe index out of range");
+          acc = acc + (tb ? Tv(m.vbase + k) : Vv(m.vbase + k)) * xe[static_cast<size_t>(xi)];
+        }
+        put(row, acc);
+      } else {  // GENERAL
+        if (m.a + static_cast<size_t>(lane) >= s.rlist.size()) return fail_at(sl, "row list out of range");
+        const int64_t row = s.rlist[m.a + lane];
+        const uint32_t info = s.ginfo[m.a + lane];
+        const int len = static_cast<int>(info & kPMaxLen), vsel = static_cast<int>((info >> 11) & 0x3f);
+        const int vi = static_cast<int>((info >> 17) & 0x1f), oi = static_cast<int>((info >> 22) & 0x1f);
+        const int L8 = (L + 7) & ~7;
+        double acc = 0.0;
+        for (int k = 0; k < L8; ++k) {  // padded entries are gathered too (never added)
+          const int32_t o = Ov(static_cast<int64_t>(m.obase) + static_cast<int64_t>(k / 4) * 4 * wo + 4 * oi + k % 4);
+          const double xv = X(base(row) + o);
+          const double v = vsel ? Vv(static_cast<int64_t>(vsel - 1) * s.dict_w + k)
+                                : Vv(static_cast<int64_t>(m.vbase) + static_cast<int64_t>(k / 2) * 2 * wv + 2 * vi + k % 2);
+          if (k < len) acc = acc + v * xv;
+        }
+        put(row, acc);
+      }
+    }
+    if (!ok) return fail_at(sl, why);
+  }
+  for (int32_t i = 0; i < nr; ++i)
+    if (!done[i]) return err = "row " + std::to_string(i) + " not computed", false;
+  return true;
+}
+
 // Transpose of a CSR (rows of the result visit source rows ascending).
 void csr_transpose(const ig_csr& a, std::vector<int32_t>& tp, std::vector<int32_t>& tc, std::vector<double>& tv) {
   tp.assign(static_cast<size_t>(a.n_cols) + 1, 0);
@@ -2719,6 +2925,21 @@ int ig_debug_psell_stats(const ig_csr* a, int64_t* out, int32_t n_out) {
     }
     out[30] = hp.layout_bytes;
     out[31] = hp.tab_rows;
+    return IG_OK;
+  });
+}
+
+// Host-only: y = A x through the pattern-SELL layout the library would build
+// for `a`, interpreted on the CPU with every index bounds-checked
+// (psell_apply_host).  IG_UNSUPPORTED when the matrix does not fit the format.
+int ig_debug_psell_apply(const ig_csr* a, const double* x, double* y) {
+  if (!a || !x || !y) return fail(IG_INVALID_ARGUMENT, "debug_psell_apply: null argument");
+  return guarded([&] {
+    OptScope os_(&g_defaults);
+    HostPSell hp;
+    if (!to_psell(a->n_rows, a->n_cols, a->row_ptr, a->col_idx, a->val, hp)) return IG_UNSUPPORTED;
+    std::string err;
+    if (!psell_apply_host(hp, a->n_rows, a->n_cols, x, y, err)) throw Error(IG_INVALID_ARGUMENT, "debug_psell_apply: layout validation failed: " + err);
     return IG_OK;
   });
 }
