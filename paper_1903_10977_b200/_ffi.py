@@ -122,6 +122,7 @@ IG_OPT_PSELL_AB = 35
 IG_OPT_PSELL_ROWS4 = 36
 IG_OPT_PSELL_EDGE_ROWS = 37
 IG_OPT_PSELL_ROWS4_ROWS = 38
+IG_OPT_PSELL_ORDER = 39
 
 _host = None
 _gpu = None

@@ -54,6 +54,7 @@ OPTS = {  # name -> (IG_OPT_* name, forced value, default)
     "pairs": ("PSELL_PAIRS_ROWS", 0, 100000),
     "rows4": ("PSELL_ROWS4_ROWS", 0, 1000000),
     "edge": ("PSELL_EDGE_ROWS", 1, 100000),
+    "order": ("PSELL_ORDER", 0, 1),
 }
 
 
@@ -61,7 +62,8 @@ OPTS = {  # name -> (IG_OPT_* name, forced value, default)
 def forced(request):
     from paper_1903_10977_b200 import _ffi
     lib = _ffi.gpu()
-    on = {"all": ("pairs", "rows4", "edge"), "no-edge": ("pairs", "rows4"), "no-rows4": ("pairs", "edge"), "defaults": ()}[request.param]
+    on = {"all": ("pairs", "rows4", "edge"), "no-edge": ("pairs", "rows4", "order"), "no-rows4": ("pairs", "edge"),
+          "defaults": ()}[request.param]
     for k in on:
         lib.ig_set_option(getattr(_ffi, "IG_OPT_" + OPTS[k][0]), OPTS[k][1])
     if request.param == "no-edge":
