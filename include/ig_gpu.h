@@ -411,7 +411,7 @@ const char *ig_last_error(void);
 #define IG_OPT_PSELL_ROWS4 36     /* 1 (default): two-line pattern-SELL slices with four rows of each line per lane (FAST8) */
 #define IG_OPT_PSELL_EDGE_ROWS 37 /* pattern-SELL slices over an edge-compacted copy of x (FASTE: the x-line end rows) for square matrices with at least this many rows (default 100000; 0 = off) */
 #define IG_OPT_PSELL_ROWS4_ROWS 38 /* ... only for matrices with at least this many rows (default 1000000) */
-#define IG_OPT_PSELL_ORDER 39      /* 1 (default): pattern-SELL slices launched by class (GENERAL, two-line, multi-piece, rest); 0: row order */
+#define IG_OPT_PSELL_ORDER 39      /* pattern-SELL slice launch order: 1 (default) by class, GENERAL spread through the two-line slices, then multi-piece, rest; 2: GENERAL first; 0: row order */
 #define IG_OPT_PSELL_AB 35        /* 1 (default): pattern-SELL slices of row pairs sharing one column list (FASTAB, prolongations) */
 #define IG_OPT_PSELL_CTAB 23     /* 1 (default): FAST2 value sequences of the pattern SELL from a constant-bank table */
 #define IG_OPT_GAL_SHORT 21      /* 1 (default): device Galerkin uses the prefetching SpGEMM when B rows have <= 32 entries */
