@@ -57,6 +57,8 @@ def main():
     rd *= scale.get(m["dram__bytes_read.sum"][1], 1.0)
     wr *= scale.get(m["dram__bytes_write.sum"][1], 1.0)
     wf, cyc = g("l1tex__data_pipe_lsu_wavefronts.avg"), g("sm__cycles_active.avg")
+    if wf == 0.0:  # the triage section's raw count is "no data" in some captures: derive it from the throughput fraction
+        wf = g("l1tex__throughput.avg.pct_of_peak_sustained_active") / 100.0 * cyc
     out = [
         ("gpu__time_duration.sum", f"{g('gpu__time_duration.sum'):.2f} {m['gpu__time_duration.sum'][1]}"),
         ("dram__bytes_read.sum", f"{rd:.2f} MB"),
