@@ -415,7 +415,9 @@ def main():
                          "launch_ms": spmv_ms,
                          "algorithmic_bytes_def": ("bytes the pattern-SELL layout must read once per launch "
                                                    "(slice metadata, deduplicated value/offset sequences, "
-                                                   "GENERAL tables) + x, y once: DESIGN.md §5"),
+                                                   "per-slice and GENERAL tables, the edge gather list and "
+                                                   "copy) + x, y once; launch_ms = the product as launched "
+                                                   "(k_xgather + k_pspmv): DESIGN.md §5"),
                          "traffic_frac": (traffic / (spmv_ms * 1e-3) / 1e9 / hbm) if traffic else None,
                          "binding_unit": ev.get("binding_unit"),
                          "csr_equivalent": {"bytes_per_launch": int(info.bytes_spmv_finest), "gbs": csr_gbs,
