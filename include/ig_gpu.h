@@ -415,7 +415,7 @@ const char *ig_last_error(void);
 #define IG_OPT_PSELL_AB 35        /* 1 (default): pattern-SELL slices of row pairs sharing one column list (FASTAB, prolongations) */
 #define IG_OPT_PSELL_CTAB 23     /* 1 (default): FAST2 value sequences of the pattern SELL from a constant-bank table */
 #define IG_OPT_GAL_SHORT 21      /* 1 (default): device Galerkin uses the prefetching SpGEMM when B rows have <= 32 entries */
-#define IG_OPT_L2_MB 19          /* size of that arena in MiB (default 64) */
+#define IG_OPT_L2_MB 19          /* size of that arena in MiB (default 48) */
 #define IG_OPT_COMPLEX4_ROWS 28  /* additive smoother: four lanes per multi-block DOF up to this many DOFs (default 100000) */
 #define IG_OPT_PSELL_PAIRS_ROWS 32 /* pattern-SELL pair / two-line slices only for matrices with at least this many rows (default 100000) */
 #define IG_OPT_FAST_BLOCKS 33     /* tolerance mode: additive-Schwarz block solves as explicit-inverse matvecs (not bit-identical; default 0) */

@@ -97,7 +97,7 @@ struct Opts {
   // 424 -> 395 us; an arena above the device's persisting maximum (83 MB on
   // B200) thrashes and gains nothing.
   int32_t l2_rows = 300000;
-  size_t l2_bytes = size_t(64) << 20;
+  size_t l2_bytes = size_t(48) << 20;  // (64 MiB: the PCG vector kernels lose the L2 they need -- C4 solve 86.0 vs 84.8 ms)
   // Additive smoother on small levels (profiles/level_costs.py): four lanes
   // per complex DOF up to complex4_rows DOFs; main stream only (no fork /
   // join) up to one_stream_rows DOFs.
