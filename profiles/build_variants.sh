@@ -7,11 +7,12 @@
 # results, the class's share of the product's time); -DIG_PSPMV_CTA=, -DIG_PSPMV_MINB=, -DIG_F8_LD256=0.
 set -e
 cd "$(dirname "$0")/../paper_1903_10977_b200"
+mkdir -p ../gpurun_out
 for spec in "$@"; do
   name="${spec%%:*}"; flags="${spec#*:}"
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -fmad=false -Xcompiler -fPIC \
     --expt-relaxed-constexpr -I../include $flags -shared -o "libig_gpu_$name.so" csrc/*.cu -lcudart \
-    2> "/tmp/ptxas_$name.log" &
+    2> "../gpurun_out/ptxas_$name.log" &
 done
 wait
 for spec in "$@"; do
