@@ -266,3 +266,48 @@ def test_small_level_smoother_variants_bitwise(request, case_name, complex4, one
         assert np.array_equal(np.array(rep.residuals), ro) and np.array_equal(x, xo)
     finally:
         h.close()
+
+
+@pytest.mark.parametrize("shift", [0, 2, 4, 6])
+def test_two_line_windows_with_16_byte_aligned_vectors(d3_48_case, shift):
+    """FAST8 reads its windows with 32-byte loads from the 32-byte boundary
+    below each column run, found from the ADDRESS of x: a device vector that is
+    only 16-byte aligned (a view starting `shift` doubles into a buffer) must
+    give the same bits as the oracle (ig_level_spmv_device, A x and r - A x)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1903_10977_b200 import MgHierarchy, _ffi
+    lib = _ffi.gpu()
+    lv = d3_48_case.levels_c()
+    for k, v in ((_ffi.IG_OPT_PSELL_ROWS4_ROWS, 0), (_ffi.IG_OPT_PSELL_PAIRS_ROWS, 0), (_ffi.IG_OPT_SMALL_ROWS, 0)):
+        lib.ig_set_option(k, v)
+    try:
+        h = MgHierarchy(d3_48_case)
+    finally:
+        for k, v in ((_ffi.IG_OPT_PSELL_ROWS4_ROWS, 1000000), (_ffi.IG_OPT_PSELL_PAIRS_ROWS, 100000),
+                     (_ffi.IG_OPT_SMALL_ROWS, 12000)):
+            lib.ig_set_option(k, v)
+    try:
+        l = h.levels() - 1
+        n = h._n[l]
+        x = rng_vec(611, n)
+        y0 = rng_vec(612, n)
+        bx = torch.zeros(n + 8, dtype=torch.float64, device="cuda")
+        by = torch.zeros(n + 8, dtype=torch.float64, device="cuda")
+        vx, vy = bx[shift:shift + n], by[shift:shift + n]
+        assert vx.data_ptr() % 16 == 0
+        vp = C.c_void_p
+        vx.copy_(torch.from_numpy(x))
+        torch.cuda.synchronize()
+        assert lib.ig_level_spmv_device(h.handle, l, vp(vx.data_ptr()), vp(vy.data_ptr()), 0) == _ffi.IG_OK
+        torch.cuda.synchronize()
+        assert np.array_equal(vy.cpu().numpy(), orc.spmv(lv, l, x, 0))
+        vy.copy_(torch.from_numpy(y0))
+        torch.cuda.synchronize()
+        assert lib.ig_level_spmv_device(h.handle, l, vp(vx.data_ptr()), vp(vy.data_ptr()), 1) == _ffi.IG_OK
+        torch.cuda.synchronize()
+        assert np.array_equal(vy.cpu().numpy(), orc.spmv(lv, l, x, 1, y0))
+    finally:
+        h.close()
